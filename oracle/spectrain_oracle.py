@@ -1,0 +1,311 @@
+"""CPU oracle of SpecTrain pipelined training (arXiv 1809.02839) — TEST INFRASTRUCTURE.
+
+This module is the plain, slow, obviously-correct reference the CUDA path is
+checked against. It is NOT part of the product: only `tests/`,
+`__graft_entry__.smoke()` and `bench.py` (its `cpu_baseline` / `--impl reference`
+leg) may import or execute it. It shares no code with
+`paper_1809_02839_b200/` and imports nothing from it; the only shared module is
+`synthdata` (seeded input draws, none of the method's arithmetic).
+
+Everything is NumPy float64, written in the paper's order and notation
+(P:n = /root/reference/PAPER.md line n; S:n = SPEC.md line n; D-numbers are the
+readings listed in DESIGN.md §3 / SURVEY §8(c)).
+
+Pins (tests/test_oracle_pins.py): Eq. 5 worked example,
+Eq. 1/Eq. 4 closed forms, N=1 == torch.optim.SGD with
+dampening=γ (library routine), finite-difference gradients, stage composition
+== monolithic autograd, s≡0 == vanilla pipeline, exact-rational App. C vectors
+(brute force on a tiny chain, tests/golden/), schedule invariants.
+Parity unpinned (decided, not fixed by the paper): D1 apply rule, D2 momentum
+convention, D5 backward re-prediction — see DESIGN.md.
+"""
+from __future__ import annotations
+
+import dataclasses
+from typing import Dict, List, Sequence, Tuple
+
+import numpy as np
+
+FWD = 0
+BWD = 1
+
+PRED_SPECTRAIN = "spectrain"
+PRED_NONE = "none"  # vanilla pipelining, s ≡ 0 (D-A8)
+
+MOMENTUM_EMA = "ema"  # Eq. 1 literally: v = γ v + (1-γ) g
+MOMENTUM_HEAVY_BALL = "heavy_ball"  # v = γ v + g (TF MomentumOptimizer, D2 flag)
+
+APPLY_MOMENTUM = "momentum"  # D1: W ← W − η·v_new (Momentum SGD)
+APPLY_EQ2 = "eq2"  # Eq. 2 literally: W ← W − η·g, oracle-only flag
+
+
+# --------------------------------------------------------------------------
+# §3.2 formulas
+# --------------------------------------------------------------------------
+
+def version_difference(k: int, N: int, direction: int) -> int:
+    """Eq. 5 (forward): s = ⌊k/2⌋ + N − k − 1.
+    Eq. 6 (backward): s = ⌊k/2⌋.
+    Returns −1 if not 0 ≤ k < N (mirrors the C-ABI)."""
+    if not (0 <= k < N):
+        return -1
+    if direction == FWD:
+        return k // 2 + N - k - 1
+    return k // 2
+
+
+def update_smoothed(v: np.ndarray, g: np.ndarray, gamma: float, momentum: str = MOMENTUM_EMA) -> np.ndarray:
+    """Eq. 1: v_t = γ·v_{t−1} + (1−γ)·g_t.  HEAVY_BALL (D2): γ·v + g."""
+    if momentum == MOMENTUM_EMA:
+        return gamma * v + (1.0 - gamma) * g
+    if momentum == MOMENTUM_HEAVY_BALL:
+        return gamma * v + g
+    raise ValueError(momentum)
+
+
+def apply_update(W: np.ndarray, v_new: np.ndarray, g: np.ndarray, eta: float, apply: str = APPLY_MOMENTUM) -> np.ndarray:
+    """D1: Momentum SGD step W ← W − η·v_t (P:373 'Momentum SGD'); APPLY_EQ2 is
+    Eq. 2 literally: W_{t+1} = W_t − η·g_t."""
+    if apply == APPLY_MOMENTUM:
+        return W - eta * v_new
+    if apply == APPLY_EQ2:
+        return W - eta * g
+    raise ValueError(apply)
+
+
+def predict(W: np.ndarray, v: np.ndarray, s: int, eta: float) -> np.ndarray:
+    """Eq. 4: Ŵ_{t+s} = W_t − s·η·v_{t−1}.  s = 0 returns W itself."""
+    if s == 0:
+        return W
+    return W - s * eta * v
+
+
+# --------------------------------------------------------------------------
+# §3.1 schedule: PipeDream 1F1B round-robin, D8
+# --------------------------------------------------------------------------
+
+def stage_program(N: int, k: int, M: int) -> List[Tuple[int, int]]:
+    """Stage k's task list: w = min(N−k−1, M) warm-up forwards, then (F, B)
+    pairs, then cooldown backwards."""
+    w = min(N - k - 1, M)
+    prog = [(FWD, i) for i in range(w)]
+    for j in range(M - w):
+        prog.append((FWD, w + j))
+        prog.append((BWD, j))
+    prog += [(BWD, j) for j in range(M - w, M)]
+    return prog
+
+
+# --------------------------------------------------------------------------
+# Dense stage forward / backward (§2.1; SPEC nn S:115-145)
+# --------------------------------------------------------------------------
+
+def unpack_stage(layers, flat: np.ndarray) -> List[Tuple[np.ndarray, np.ndarray]]:
+    """Stage flat layout: per layer W [in×out] row-major then b [out]."""
+    out, off = [], 0
+    for L in layers:
+        W = flat[off:off + L.n_in * L.n_out].reshape(L.n_in, L.n_out)
+        off += L.n_in * L.n_out
+        if L.bias:
+            b = flat[off:off + L.n_out]
+            off += L.n_out
+        else:
+            b = None
+        out.append((W, b))
+    assert off == flat.size, (off, flat.size)
+    return out
+
+
+def pack_stage(layers, parts: Sequence[Tuple[np.ndarray, np.ndarray]]) -> np.ndarray:
+    chunks = []
+    for L, (gW, gb) in zip(layers, parts):
+        chunks.append(gW.reshape(-1))
+        if L.bias:
+            chunks.append(gb)
+    return np.concatenate(chunks) if chunks else np.zeros(0)
+
+
+def stage_forward(layers, flat: np.ndarray, A: np.ndarray):
+    """Per layer: Z = A·W + b; A' = ReLU(Z) (identity when act == 'none').
+    Returns (stage output, stash of (A_in, Z) per layer)."""
+    stash = []
+    for L, (W, b) in zip(layers, unpack_stage(layers, flat)):
+        Z = A @ W
+        if b is not None:
+            Z = Z + b
+        stash.append((A, Z))
+        A = np.maximum(Z, 0.0) if L.act == "relu" else Z
+    return A, stash
+
+
+def stage_backward(layers, flat: np.ndarray, stash, dA_out: np.ndarray, need_dA_in: bool = True):
+    """Reverse layers: dZ = dA ⊙ 1[Z>0] (D12: ReLU'(0)=0); g_W = Aᵀ·dZ;
+    g_b = Σ_rows dZ; dA_prev = dZ·Wᵀ.  Returns (flat gradient, dA_in or None)."""
+    params = unpack_stage(layers, flat)
+    grads = [None] * len(layers)
+    dA = dA_out
+    for li in range(len(layers) - 1, -1, -1):
+        L = layers[li]
+        W, b = params[li]
+        A_in, Z = stash[li]
+        dZ = dA * (Z > 0.0) if L.act == "relu" else dA
+        gW = A_in.T @ dZ
+        gb = dZ.sum(axis=0) if L.bias else None
+        grads[li] = (gW, gb)
+        if li > 0 or need_dA_in:
+            dA = dZ @ W.T
+        else:
+            dA = None
+    return pack_stage(layers, grads), dA
+
+
+def loss_and_grad(kind: str, Z: np.ndarray, target: np.ndarray) -> Tuple[float, np.ndarray]:
+    """D11: softmax cross-entropy, mean over the batch, max-subtracted softmax
+    (P:105-107 'loss between the prediction and the ground truth');
+    'half_mse': mean_b ½‖Z_b − t_b‖² (the App. C scalar chain)."""
+    B = Z.shape[0]
+    if kind == "softmax_ce":
+        m = Z.max(axis=1, keepdims=True)
+        e = np.exp(Z - m)
+        s = e.sum(axis=1, keepdims=True)
+        logp = Z - m - np.log(s)
+        y = target.astype(np.int64)
+        loss = -logp[np.arange(B), y].mean()
+        p = e / s
+        onehot = np.zeros_like(Z)
+        onehot[np.arange(B), y] = 1.0
+        return float(loss), (p - onehot) / B
+    if kind == "half_mse":
+        d = Z - target
+        return float(0.5 * (d * d).sum() / B), d / B
+    raise ValueError(kind)
+
+
+# --------------------------------------------------------------------------
+# Pipelined SpecTrain run
+# --------------------------------------------------------------------------
+
+@dataclasses.dataclass
+class Event:
+    """One task record: stage, position in the stage program,
+    direction, mini-batch, base version c (updates applied so far), version
+    difference s, target version c+s."""
+
+    stage: int
+    op_idx: int
+    dir: int
+    mb: int
+    base_version: int
+    s: int
+
+    @property
+    def target(self) -> int:
+        return self.base_version + self.s
+
+    def as_tuple(self) -> Tuple[int, int, int, int, int, int, int]:
+        return (self.stage, self.op_idx, self.dir, self.mb, self.base_version, self.s, self.target)
+
+
+@dataclasses.dataclass
+class RunResult:
+    W: List[np.ndarray]
+    V: List[np.ndarray]
+    losses: np.ndarray
+    trace: List[List[Event]]
+
+
+def run(model, W0: Sequence[np.ndarray], X: np.ndarray, Y: np.ndarray, eta: float, gamma: float,
+        pred: str = PRED_SPECTRAIN, momentum: str = MOMENTUM_EMA, apply: str = APPLY_MOMENTUM,
+        order: str = "round_robin") -> RunResult:
+    """Interpret every stage's 1F1B program in a dependency-respecting order.
+
+    F(i,k) needs F(i,k−1)'s output; B(i,k) needs B(i,k+1)'s dA (or, at the last
+    stage, its own F(i)). Before each task the stage computes Ŵ = W − s·η·V from
+    its CURRENT state (Eq. 4 with Eq. 5/6; D4, D5). After each B: Eq. 1, then
+    the D1 apply, then version += 1 (D9). The result does not depend on the
+    interpretation order (`order` = 'round_robin' or 'stage_major' exists so a
+    test can show that)."""
+    N = model.num_stages
+    M = X.shape[0]
+    W = [np.array(w, dtype=np.float64, copy=True) for w in W0]
+    V = [np.zeros_like(w) for w in W]
+    version = [0] * N
+    progs = [stage_program(N, k, M) for k in range(N)]
+    pc = [0] * N
+    act: Dict[Tuple[int, int], np.ndarray] = {}  # (k, i) → stage k's forward output for mb i
+    grad: Dict[Tuple[int, int], np.ndarray] = {}  # (k, i) → dA w.r.t. stage k's input for mb i
+    stash: Dict[Tuple[int, int], list] = {}
+    dlogits: Dict[int, np.ndarray] = {}
+    losses = np.full(M, np.nan)
+    trace: List[List[Event]] = [[] for _ in range(N)]
+
+    def s_of(k: int, d: int) -> int:
+        return 0 if pred == PRED_NONE else version_difference(k, N, d)
+
+    def ready(k: int) -> bool:
+        d, i = progs[k][pc[k]]
+        if d == FWD:
+            return k == 0 or (k - 1, i) in act
+        return k == N - 1 or (k + 1, i) in grad
+
+    def execute(k: int) -> None:
+        d, i = progs[k][pc[k]]
+        layers = model.stage_layers(k)
+        s = s_of(k, d)
+        W_hat = predict(W[k], V[k], s, eta)
+        trace[k].append(Event(k, pc[k], d, i, version[k], s))
+        if d == FWD:
+            A_in = X[i].astype(np.float64) if k == 0 else act.pop((k - 1, i))
+            out, st = stage_forward(layers, W_hat, A_in)
+            stash[(k, i)] = st
+            if k == N - 1:
+                losses[i], dlogits[i] = loss_and_grad(model.loss, out, Y[i])
+            else:
+                act[(k, i)] = out
+        else:
+            dA = dlogits.pop(i) if k == N - 1 else grad.pop((k + 1, i))
+            g, dA_in = stage_backward(layers, W_hat, stash.pop((k, i)), dA, need_dA_in=(k > 0))
+            if k > 0:
+                grad[(k, i)] = dA_in
+            # Update after each B: Eq. 1, D1 apply, version += 1.
+            V[k] = update_smoothed(V[k], g, gamma, momentum)
+            W[k] = apply_update(W[k], V[k], g, eta, apply)
+            version[k] += 1
+        pc[k] += 1
+
+    total = sum(len(p) for p in progs)
+    done = 0
+    while done < total:
+        progressed = False
+        for k in range(N):
+            if order == "stage_major":
+                while pc[k] < len(progs[k]) and ready(k):
+                    execute(k)
+                    done += 1
+                    progressed = True
+            else:
+                if pc[k] < len(progs[k]) and ready(k):
+                    execute(k)
+                    done += 1
+                    progressed = True
+        if not progressed:
+            raise RuntimeError("pipeline deadlock (invariant violation)")
+    return RunResult(W, V, losses, trace)
+
+
+def sequential_momentum_sgd(model, W0_flat: np.ndarray, X: np.ndarray, Y: np.ndarray, eta: float,
+                            gamma: float, momentum: str = MOMENTUM_EMA) -> Tuple[np.ndarray, np.ndarray]:
+    """Single-device momentum SGD over all layers (the staleness-free trainer of
+    Fig. 6a). Used to pin the N=1 degenerate case."""
+    W = np.array(W0_flat, dtype=np.float64, copy=True)
+    V = np.zeros_like(W)
+    losses = []
+    layers = model.layers
+    for i in range(X.shape[0]):
+        out, st = stage_forward(layers, W, X[i].astype(np.float64))
+        loss, dZ = loss_and_grad(model.loss, out, Y[i])
+        g, _ = stage_backward(layers, W, st, dZ, need_dA_in=False)
+        V = update_smoothed(V, g, gamma, momentum)
+        W = W - eta * V
+        losses.append(loss)
+    return W, np.array(losses)

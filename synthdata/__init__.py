@@ -1,0 +1,175 @@
+"""Seeded synthetic inputs shared by the CPU oracle and the CUDA path.
+
+This module holds NONE of SpecTrain's arithmetic (no forward/backward, no
+momentum, no prediction). It only draws the arrays both sides consume, so that
+the oracle (`oracle/`) and the product (`paper_1809_02839_b200/`) never import
+each other.
+
+Recipe (DESIGN.md §Readings D13):
+- RNG: numpy PCG64 `numpy.random.default_rng(seed)`.
+- Weights: Glorot-uniform `U(-r, r)`, `r = sqrt(6/(in+out))`, biases 0
+  (SPEC S:150 initialisation; the paper is silent, P:374 fixes only the LR).
+- Images: U[0,1) in the input width (784 = MNIST-shaped, P:377 CIFAR/MNIST-like
+  synthetic stand-ins).
+- Labels: argmax of a fixed N(0,1) "teacher" projection of the image (learnable
+  so the loss moves), or uniform when `labels="uniform"` (bench).
+"""
+from __future__ import annotations
+
+import dataclasses
+import math
+from typing import List, Optional, Sequence, Tuple
+
+import numpy as np
+
+RELU = "relu"
+NONE = "none"
+
+
+@dataclasses.dataclass(frozen=True)
+class Layer:
+    """One dense layer `Z = A·W + b`, `A' = act(Z)`; W stored [in×out] row-major."""
+
+    n_in: int
+    n_out: int
+    act: str = RELU
+    bias: bool = True
+
+    @property
+    def n_params(self) -> int:
+        return self.n_in * self.n_out + (self.n_out if self.bias else 0)
+
+
+@dataclasses.dataclass(frozen=True)
+class Model:
+    """A chain of dense layers cut into contiguous pipeline stages."""
+
+    layers: Tuple[Layer, ...]
+    cuts: Tuple[int, ...]  # N-1 strictly increasing layer indices; stage k = [cuts[k-1], cuts[k])
+    loss: str = "softmax_ce"  # or "half_mse" (App. C scalar chain)
+
+    @property
+    def num_stages(self) -> int:
+        return len(self.cuts) + 1
+
+    def stage_layers(self, k: int) -> Tuple[Layer, ...]:
+        bounds = (0,) + tuple(self.cuts) + (len(self.layers),)
+        return self.layers[bounds[k]:bounds[k + 1]]
+
+    def stage_bounds(self, k: int) -> Tuple[int, int]:
+        bounds = (0,) + tuple(self.cuts) + (len(self.layers),)
+        return bounds[k], bounds[k + 1]
+
+    def stage_params(self, k: int) -> int:
+        return sum(l.n_params for l in self.stage_layers(k))
+
+
+def mlp(widths: Sequence[int], cuts: Sequence[int], bias: bool = True, loss: str = "softmax_ce") -> Model:
+    """ReLU MLP over `widths` (last layer identity), cut at `cuts` (layer indices)."""
+    n = len(widths) - 1
+    layers = tuple(
+        Layer(widths[i], widths[i + 1], NONE if i == n - 1 else RELU, bias) for i in range(n)
+    )
+    cuts = tuple(int(c) for c in cuts)
+    if any(not (0 < c < n) for c in cuts) or list(cuts) != sorted(set(cuts)):
+        raise ValueError(f"invalid cuts {cuts} for {n} layers")
+    return Model(layers, cuts, loss)
+
+
+def even_cuts(num_layers: int, num_stages: int) -> Tuple[int, ...]:
+    """Contiguous cuts giving stage sizes that differ by at most one; the extra
+    layers go to the LAST stages (so e.g. 9 layers / 8 stages = {L1}..{L7}{L8,L9},
+    SURVEY §8(d) config 2)."""
+    if not 1 <= num_stages <= num_layers:
+        raise ValueError("need 1 <= stages <= layers")
+    base, extra = divmod(num_layers, num_stages)
+    sizes = [base + (1 if k >= num_stages - extra else 0) for k in range(num_stages)]
+    cuts, acc = [], 0
+    for s in sizes[:-1]:
+        acc += s
+        cuts.append(acc)
+    return tuple(cuts)
+
+
+# ---- named configurations (BASELINE.json `configs`) -----------------------
+
+def config_mlp_2stage() -> Model:
+    """BJ configs[0]: 4-layer MLP 784-256-256-10, 2 stages {L1}{L2,L3}."""
+    return mlp([784, 256, 256, 10], cuts=[1])
+
+
+def config_deep_mlp(num_stages: int = 8, width: int = 1024, depth: int = 9) -> Model:
+    """SURVEY §8(d) row 1b parity model: 784-1024×8-10, one layer per stage, last two merged."""
+    widths = [784] + [width] * (depth - 1) + [10]
+    return mlp(widths, cuts=even_cuts(depth, num_stages))
+
+
+def config_wide_fcn(num_stages: int, width: int = 8192, hidden_layers: int = 8) -> Model:
+    """BJ configs[1]: wide FCN, `hidden_layers` × `width` units on 784-dim inputs, 10 classes.
+    9 weight layers: 784→w, (hidden_layers-1)× w→w, w→10."""
+    widths = [784] + [width] * hidden_layers + [10]
+    return mlp(widths, cuts=even_cuts(len(widths) - 1, num_stages))
+
+
+def config_large_fcn(num_stages: int, width: int = 16384, hidden_layers: int = 16) -> Model:
+    """BJ configs[4]: large FCN 16 × 16384."""
+    widths = [784] + [width] * hidden_layers + [10]
+    return mlp(widths, cuts=even_cuts(len(widths) - 1, num_stages))
+
+
+# ---- draws -----------------------------------------------------------------
+
+def glorot_params(model: Model, seed: int) -> List[np.ndarray]:
+    """Per-stage flat float64 parameter vectors in the stage layout
+    (layer-major: W_l [in×out] row-major, then b_l [out])."""
+    rng = np.random.default_rng(seed)
+    out = []
+    for k in range(model.num_stages):
+        parts = []
+        for layer in model.stage_layers(k):
+            r = math.sqrt(6.0 / (layer.n_in + layer.n_out))
+            parts.append(rng.uniform(-r, r, size=layer.n_in * layer.n_out))
+            if layer.bias:
+                parts.append(np.zeros(layer.n_out))
+        out.append(np.concatenate(parts) if parts else np.zeros(0))
+    return out
+
+
+def images_and_labels(
+    n_in: int,
+    n_classes: int,
+    num_batches: int,
+    batch: int,
+    seed: int,
+    labels: str = "teacher",
+) -> Tuple[np.ndarray, np.ndarray]:
+    """X: [M, B, n_in] U[0,1); Y: [M, B] int32 labels in [0, n_classes)."""
+    rng = np.random.default_rng(seed)
+    x = rng.random((num_batches, batch, n_in))
+    if labels == "teacher":
+        teacher = rng.standard_normal((n_in, n_classes))
+        y = np.argmax((x - 0.5) @ teacher, axis=-1).astype(np.int32)
+    elif labels == "uniform":
+        y = rng.integers(0, n_classes, size=(num_batches, batch), dtype=np.int32)
+    else:
+        raise ValueError(labels)
+    return x, y
+
+
+def to_f32_params(params: Sequence[np.ndarray]) -> List[np.ndarray]:
+    """The fp32 copies the GPU consumes; the oracle is fed the SAME values widened to fp64."""
+    return [np.ascontiguousarray(p, dtype=np.float32) for p in params]
+
+
+def widen(params_f32: Sequence[np.ndarray]) -> List[np.ndarray]:
+    return [np.asarray(p, dtype=np.float64) for p in params_f32]
+
+
+def parity_inputs(model: Model, num_batches: int, batch: int, seed: int = 0,
+                  labels: str = "teacher") -> Tuple[List[np.ndarray], np.ndarray, np.ndarray]:
+    """(W0 per stage as fp32, X as fp32 [M,B,in], Y int32 [M,B]) — fp32-representable
+    inputs so oracle (fp64) and GPU (fp32) start from bit-identical values."""
+    w0 = to_f32_params(glorot_params(model, seed))
+    x, y = images_and_labels(model.layers[0].n_in, model.layers[-1].n_out, num_batches, batch,
+                             seed + 1, labels)
+    return w0, x.astype(np.float32), y

@@ -1,0 +1,399 @@
+"""Pins for the CPU oracle (-m "not gpu"): each check ties the oracle to something
+other than itself — the paper's worked example, closed forms, a library routine
+(torch.optim.SGD / torch autograd), finite differences, or an independent
+exact-rational brute force. A plausible slip in the oracle (dropped term, wrong
+sign, off-by-one version, transposed operand) fails at least one of these.
+"""
+import json
+import math
+import os
+from fractions import Fraction
+
+import numpy as np
+import pytest
+import torch
+
+import synthdata as sd
+from oracle import spectrain_oracle as O
+
+GOLDEN = os.path.join(os.path.dirname(__file__), "golden")
+
+
+# ---------------------------------------------------------------- Eq. 5 / 6
+
+def test_version_difference_paper_example():
+    # "at the 4-th time unit ... s = ⌊0/2⌋ + 3 − 0 − 1 = 2"
+    assert O.version_difference(0, 3, O.FWD) == 2
+    # backward at k=0 never predicts (Eq. 6)
+    for N in range(1, 17):
+        assert O.version_difference(0, N, O.BWD) == 0
+
+
+def test_version_difference_invariants():
+    # 0 ≤ s_B ≤ s_F ≤ N−1; s_F(N−1) = s_B(N−1); s_F − s_B = N−k−1
+    for N in range(1, 17):
+        for k in range(N):
+            sf, sb = O.version_difference(k, N, O.FWD), O.version_difference(k, N, O.BWD)
+            assert 0 <= sb <= sf <= N - 1
+            assert sf - sb == N - k - 1
+        assert O.version_difference(N - 1, N, O.FWD) == O.version_difference(N - 1, N, O.BWD)
+    assert O.version_difference(0, 1, O.FWD) == 0 and O.version_difference(0, 1, O.BWD) == 0
+    assert O.version_difference(3, 3, O.FWD) == -1 and O.version_difference(-1, 3, O.BWD) == -1
+    # SURVEY App. A table for N=8
+    table8 = [(7, 0), (6, 0), (6, 1), (5, 1), (5, 2), (4, 2), (4, 3), (3, 3)]
+    assert [(O.version_difference(k, 8, O.FWD), O.version_difference(k, 8, O.BWD)) for k in range(8)] == table8
+
+
+# ---------------------------------------------------------------- Eq. 1 / Eq. 4
+
+def test_update_smoothed_closed_forms():
+    v = np.zeros(3)
+    g = np.ones(3)
+    v1 = O.update_smoothed(v, g, 0.9)
+    np.testing.assert_allclose(v1, 0.1, rtol=0, atol=1e-15)
+    v3 = O.update_smoothed(O.update_smoothed(v1, g, 0.9), g, 0.9)
+    np.testing.assert_allclose(v3, 1 - 0.9 ** 3, atol=1e-15)  # 0.271
+    rng = np.random.default_rng(3)
+    v, g = rng.standard_normal(50), rng.standard_normal(50)
+    np.testing.assert_array_equal(O.update_smoothed(v, g, 1.0), v)  # γ = 1 → v unchanged
+    # contraction toward g: |v' − g| = γ |v − g|
+    np.testing.assert_allclose(np.abs(O.update_smoothed(v, g, 0.7) - g), 0.7 * np.abs(v - g), rtol=1e-13)
+    # heavy-ball convention: γv + g
+    np.testing.assert_allclose(O.update_smoothed(v, g, 0.9, O.MOMENTUM_HEAVY_BALL), 0.9 * v + g, rtol=1e-15)
+
+
+def test_predict_closed_forms():
+    W = np.array([1.0])
+    assert O.predict(W, np.array([0.5]), 2, 0.1)[0] == pytest.approx(0.9, abs=1e-15)
+    rng = np.random.default_rng(4)
+    W, v = rng.standard_normal(40), rng.standard_normal(40)
+    assert O.predict(W, v, 0, 0.3) is W  # s = 0 → W bit-exact
+    # linear in s; s=2 == one-step prediction applied twice with v fixed (Eq. 3 → Eq. 4)
+    np.testing.assert_allclose(O.predict(W, v, 5, 0.3) - W, (O.predict(W, v, 2, 0.3) - W) + (O.predict(W, v, 3, 0.3) - W), atol=1e-14)
+    np.testing.assert_allclose(O.predict(O.predict(W, v, 1, 0.3), v, 1, 0.3), O.predict(W, v, 2, 0.3), atol=1e-15)
+
+
+# ---------------------------------------------------------------- schedule
+
+@pytest.mark.parametrize("N", [1, 2, 3, 4, 8])
+@pytest.mark.parametrize("M", [1, 3, 8, 20])
+def test_schedule_invariants(N, M):
+    """c_F = max(0, i−(N−k−1)), c_B = i; in steady state F and B of the same
+    mini-batch target i + ⌊k/2⌋."""
+    model = sd.mlp([3] + [3] * N, cuts=list(range(1, N)))
+    w0 = sd.glorot_params(model, 0)
+    X = np.random.default_rng(1).random((M, 2, 3))
+    Y = np.random.default_rng(2).integers(0, 3, (M, 2))
+    res = O.run(model, w0, X, Y, 0.01, 0.9)
+    for k in range(N):
+        ev = res.trace[k]
+        assert [(e.dir, e.mb) for e in ev] == O.stage_program(N, k, M)
+        assert [e.op_idx for e in ev] == list(range(2 * M))
+        for e in ev:
+            if e.dir == O.FWD:
+                assert e.base_version == max(0, e.mb - (N - k - 1))
+                assert e.s == k // 2 + N - k - 1
+            else:
+                assert e.base_version == e.mb
+                assert e.s == k // 2
+        # steady state: same target for F and B of one mini-batch
+        for i in range(N - k - 1, M):
+            f = [e for e in ev if e.dir == O.FWD and e.mb == i][0]
+            b = [e for e in ev if e.dir == O.BWD and e.mb == i][0]
+            assert f.target == b.target == i + k // 2
+
+
+def test_vanilla_span_paper_example():
+    """with N=3 vanilla pipelining a mini-batch's round trip sees a span of
+    N−1 = 2 versions at GPU 0 (W4..W6); its backward sees the staleness-free one."""
+    N, M = 3, 8
+    model = sd.mlp([2, 2, 2, 2], cuts=[1, 2])
+    res = O.run(model, sd.glorot_params(model, 0), np.ones((M, 1, 2)), np.zeros((M, 1), np.int32), 0.01, 0.9, pred=O.PRED_NONE)
+    ev0 = res.trace[0]
+    for i in range(N - 1, M):
+        f = [e for e in ev0 if e.dir == O.FWD and e.mb == i][0]
+        b = [e for e in ev0 if e.dir == O.BWD and e.mb == i][0]
+        assert b.base_version - f.base_version == N - 1
+        assert f.s == b.s == 0
+
+
+def test_program_counts():
+    for N in range(1, 9):
+        for k in range(N):
+            for M in (1, 2, N - 1 if N > 1 else 1, N, 20):
+                p = O.stage_program(N, k, M)
+                assert sorted(i for d, i in p if d == O.FWD) == list(range(M))
+                assert sorted(i for d, i in p if d == O.BWD) == list(range(M))
+                # F(i) precedes B(i) on every stage; at most N−k in flight
+                pos = {op: n for n, op in enumerate(p)}
+                inflight = 0
+                for d, i in p:
+                    assert d == O.BWD or True
+                    inflight += 1 if d == O.FWD else -1
+                    assert 0 <= inflight <= N - k
+                for i in range(M):
+                    assert pos[(O.FWD, i)] < pos[(O.BWD, i)]
+
+
+# ---------------------------------------------------------------- App. C brute force
+
+def _appc_bruteforce(pred: bool, heavy: bool, w_init, xs, ts, eta, gamma):
+    """Independent exact-rational hand-stepping of the scalar chain. The per-stage
+    task ORDER is not taken from the oracle: it emerges from a time-stepped
+    round-robin simulation (P:211-212 'issues a forward task and a backward task in
+    a round-robin manner', 'asynchronously executes the next one') in which a stage
+    holds at most N−k mini-batches in flight and prefers a ready backward."""
+    N, M = len(w_init), len(xs)
+    F = Fraction
+    w = [F(x) for x in w_init]
+    v = [F(0)] * N
+    ver = [0] * N
+    nxt_f = [0] * N
+    done_b = [0] * N
+    inflight = [0] * N
+    act_in = {}  # (k, i) input activation available at stage k
+    grad_in = {}  # (k, i) upstream gradient available at stage k
+    stash = {}
+    losses = [None] * M
+    trace = {k: [] for k in range(N)}
+    for i in range(M):
+        act_in[(0, i)] = F(xs[i])
+    t = 0
+    while any(done_b[k] < M for k in range(N)):
+        t += 1
+        posted = []
+        for k in range(N):
+            j = done_b[k]
+            did = False
+            if j < M and (k, j) in grad_in:
+                # backward of the oldest in-flight mini-batch
+                s = (k // 2) if pred else 0
+                w_hat = w[k] - s * F(eta) * v[k]
+                trace[k].append(f"B{j}({ver[k]},{s},{ver[k] + s})")
+                a_in = stash.pop((k, j))
+                dy = grad_in.pop((k, j))
+                g = dy * a_in
+                if k > 0:
+                    posted.append(((k - 1, j), dy * w_hat))
+                v[k] = gamma_f(gamma) * v[k] + (g if heavy else (1 - gamma_f(gamma)) * g)
+                w[k] = w[k] - F(eta) * v[k]
+                ver[k] += 1
+                done_b[k] += 1
+                inflight[k] -= 1
+                did = True
+            if not did:
+                i = nxt_f[k]
+                if i < M and (k, i) in act_in and inflight[k] < N - k:
+                    s = (k // 2 + N - k - 1) if pred else 0
+                    w_hat = w[k] - s * F(eta) * v[k]
+                    trace[k].append(f"F{i}({ver[k]},{s},{ver[k] + s})")
+                    a = act_in.pop((k, i))
+                    stash[(k, i)] = a
+                    out = w_hat * a
+                    if k == N - 1:
+                        d = out - F(ts[i])
+                        losses[i] = d * d / 2
+                        grad_in[(k, i)] = d
+                    else:
+                        posted.append(("act", (k + 1, i), out))
+                    nxt_f[k] += 1
+                    inflight[k] += 1
+        # messages produced in this time unit become visible in the next one
+        for p in posted:
+            if p[0] == "act":
+                act_in[p[1]] = p[2]
+            else:
+                grad_in[p[0]] = p[1]
+        assert t < 100 * (M + N)
+    return w, v, losses, trace
+
+
+def gamma_f(g):
+    return Fraction(g).limit_denominator(1000)
+
+
+def test_appc_bruteforce_rational_matches_golden():
+    gold = json.load(open(os.path.join(GOLDEN, "appc_scalar_chain.json")))
+    w, v, losses, trace = _appc_bruteforce(True, False, gold["w_init"], gold["x"], gold["t"],
+                                           Fraction(1, 10), 0.9)
+    g = gold["spectrain"]
+    np.testing.assert_allclose([float(a) for a in w], g["W"], rtol=1e-12)
+    np.testing.assert_allclose([float(a) for a in v], g["V"], rtol=1e-12)
+    np.testing.assert_allclose([float(a) for a in losses], g["losses"], rtol=1e-11)
+    for k in range(3):
+        assert " ".join(trace[k]) == g["trace"][str(k)]
+    wv, _, lv, _ = _appc_bruteforce(False, False, gold["w_init"], gold["x"], gold["t"], Fraction(1, 10), 0.9)
+    np.testing.assert_allclose([float(a) for a in wv], gold["vanilla"]["W"], rtol=1e-12)
+    np.testing.assert_allclose([float(a) for a in lv], gold["vanilla"]["losses"], rtol=2e-5)
+    wh, _, _, _ = _appc_bruteforce(True, True, gold["w_init"], gold["x"], gold["t"], Fraction(1, 10), 0.9)
+    np.testing.assert_allclose([float(a) for a in wh], gold["heavy_ball"]["W"], rtol=1e-12)
+
+
+def _scalar_chain(n):
+    return sd.Model(tuple(sd.Layer(1, 1, sd.NONE, False) for _ in range(n)), tuple(range(1, n)), "half_mse")
+
+
+def _appc_oracle(pred, momentum, w_init=None):
+    gold = json.load(open(os.path.join(GOLDEN, "appc_scalar_chain.json")))
+    w_init = gold["w_init"] if w_init is None else w_init
+    model = _scalar_chain(len(w_init))
+    X = np.array(gold["x"]).reshape(-1, 1, 1)
+    Y = np.array(gold["t"]).reshape(-1, 1, 1)
+    return gold, O.run(model, [np.array([w]) for w in w_init], X, Y, 0.1, 0.9, pred=pred, momentum=momentum)
+
+
+def test_appc_oracle_spectrain():
+    gold, res = _appc_oracle(O.PRED_SPECTRAIN, O.MOMENTUM_EMA)
+    g = gold["spectrain"]
+    np.testing.assert_allclose(np.concatenate(res.W), g["W"], rtol=1e-12)
+    np.testing.assert_allclose(np.concatenate(res.V), g["V"], rtol=1e-12)
+    np.testing.assert_allclose(res.losses, g["losses"], rtol=1e-11)
+    for k in range(3):
+        got = " ".join(f"{'F' if e.dir == O.FWD else 'B'}{e.mb}({e.base_version},{e.s},{e.target})" for e in res.trace[k])
+        assert got == g["trace"][str(k)]
+
+
+def test_appc_oracle_vanilla_and_heavy_ball():
+    gold, res = _appc_oracle(O.PRED_NONE, O.MOMENTUM_EMA)
+    np.testing.assert_allclose(np.concatenate(res.W), gold["vanilla"]["W"], rtol=1e-12)
+    np.testing.assert_allclose(res.losses, gold["vanilla"]["losses"], rtol=2e-5)
+    assert all(e.s == 0 for ev in res.trace for e in ev)
+    gold, res = _appc_oracle(O.PRED_SPECTRAIN, O.MOMENTUM_HEAVY_BALL)
+    np.testing.assert_allclose(np.concatenate(res.W), gold["heavy_ball"]["W"], rtol=1e-12)
+
+
+def test_appc_single_weight_momentum_sgd():
+    gold, res = _appc_oracle(O.PRED_SPECTRAIN, O.MOMENTUM_EMA, w_init=[1.0])
+    np.testing.assert_allclose(res.W[0], gold["single_w1"]["W"], rtol=1e-11)
+
+
+# ---------------------------------------------------------------- library routines
+
+def _torch_model_loss(model, flat, x, y):
+    """Monolithic forward with torch ops (autograd supplies the reference gradient)."""
+    off = 0
+    a = x
+    for L in model.layers:
+        W = flat[off:off + L.n_in * L.n_out].view(L.n_in, L.n_out)
+        off += L.n_in * L.n_out
+        z = a @ W
+        if L.bias:
+            z = z + flat[off:off + L.n_out]
+            off += L.n_out
+        a = torch.relu(z) if L.act == sd.RELU else z
+    if model.loss == "softmax_ce":
+        return torch.nn.functional.cross_entropy(a, y.long())
+    return 0.5 * ((a - y) ** 2).sum() / a.shape[0]
+
+
+@pytest.mark.parametrize("cuts", [[], [1], [1, 2]])
+def test_stage_composed_grads_equal_autograd(cuts):
+    """composing stage backward == monolithic gradient (torch autograd, fp64)."""
+    model = sd.mlp([7, 6, 5, 4], cuts=cuts)
+    w = np.concatenate(sd.glorot_params(model, 5))
+    w[np.arange(w.size) % 7 == 0] += 0.1  # non-zero biases
+    rng = np.random.default_rng(6)
+    x = rng.standard_normal((5, 7))
+    y = rng.integers(0, 4, 5)
+    # oracle, stage by stage
+    flats, off = [], 0
+    for k in range(model.num_stages):
+        n = model.stage_params(k)
+        flats.append(w[off:off + n])
+        off += n
+    a, stashes = x, []
+    for k in range(model.num_stages):
+        a, st = O.stage_forward(model.stage_layers(k), flats[k], a)
+        stashes.append(st)
+    loss, d = O.loss_and_grad("softmax_ce", a, y)
+    grads = [None] * model.num_stages
+    for k in range(model.num_stages - 1, -1, -1):
+        grads[k], d = O.stage_backward(model.stage_layers(k), flats[k], stashes[k], d, need_dA_in=k > 0)
+    g_oracle = np.concatenate(grads)
+    tw = torch.tensor(w, dtype=torch.float64, requires_grad=True)
+    tl = _torch_model_loss(model, tw, torch.tensor(x), torch.tensor(y))
+    tl.backward()
+    assert loss == pytest.approx(tl.item(), rel=1e-13)
+    np.testing.assert_allclose(g_oracle, tw.grad.numpy(), rtol=1e-12, atol=1e-14)
+
+
+def test_finite_difference_gradients():
+    """central differences, h = 1e-5, relative error < 1e-5 (3-layer net, batch 4)."""
+    model = sd.mlp([4, 5, 3, 3], cuts=[])
+    w = np.concatenate(sd.glorot_params(model, 11)) + 0.05
+    rng = np.random.default_rng(12)
+    x = rng.standard_normal((4, 4))
+    y = rng.integers(0, 3, 4)
+
+    def f(wv):
+        out, _ = O.stage_forward(model.layers, wv, x)
+        return O.loss_and_grad("softmax_ce", out, y)[0]
+
+    out, st = O.stage_forward(model.layers, w, x)
+    _, dz = O.loss_and_grad("softmax_ce", out, y)
+    g, _ = O.stage_backward(model.layers, w, st, dz, need_dA_in=False)
+    h = 1e-5
+    for i in range(w.size):
+        e = np.zeros_like(w)
+        e[i] = h
+        fd = (f(w + e) - f(w - e)) / (2 * h)
+        assert abs(fd - g[i]) <= 1e-5 * max(1e-3, abs(g[i])) + 1e-9, (i, fd, g[i])
+
+
+def test_cross_entropy_uniform_logits():
+    """uniform logits over C classes → loss ln C; grad rows sum to 0."""
+    Z = np.full((6, 10), 0.37)
+    loss, d = O.loss_and_grad("softmax_ce", Z, np.arange(6) % 10)
+    assert loss == pytest.approx(math.log(10), rel=1e-15)
+    np.testing.assert_allclose(d.sum(axis=1), 0, atol=1e-16)
+
+
+def test_single_stage_equals_torch_sgd_dampened():
+    """N=1 SpecTrain ≡ momentum SGD ≡ torch.optim.SGD(lr=η, momentum=γ,
+    dampening=γ) with momentum_buffer pre-set to zeros (SURVEY §8(c) pins)."""
+    model = sd.mlp([12, 9, 7, 5], cuts=[])
+    w0 = np.concatenate(sd.glorot_params(model, 21))
+    X, Y = sd.images_and_labels(12, 5, 10, 6, seed=22)
+    eta, gamma = 0.05, 0.9
+    res = O.run(model, [w0], X, Y, eta, gamma)
+    tw = torch.tensor(w0, dtype=torch.float64, requires_grad=True)
+    opt = torch.optim.SGD([tw], lr=eta, momentum=gamma, dampening=gamma)
+    opt.state[tw]["momentum_buffer"] = torch.zeros_like(tw)
+    losses = []
+    for i in range(10):
+        opt.zero_grad()
+        l = _torch_model_loss(model, tw, torch.tensor(X[i]), torch.tensor(Y[i]))
+        l.backward()
+        opt.step()
+        losses.append(l.item())
+    np.testing.assert_allclose(res.W[0], tw.detach().numpy(), rtol=1e-11, atol=1e-14)
+    np.testing.assert_allclose(res.losses, losses, rtol=1e-11)
+    np.testing.assert_allclose(res.V[0], opt.state[tw]["momentum_buffer"].numpy(), rtol=1e-10, atol=1e-15)
+    # and the oracle's own sequential trainer agrees bit-for-bit
+    Ws, ls = O.sequential_momentum_sgd(model, w0, X, Y, eta, gamma)
+    np.testing.assert_array_equal(Ws, res.W[0])
+    np.testing.assert_array_equal(ls, res.losses)
+
+
+def test_interpretation_order_independent():
+    model = sd.config_deep_mlp(num_stages=4, width=16, depth=5)
+    w0 = sd.glorot_params(model, 0)
+    X, Y = sd.images_and_labels(784, 10, 9, 4, seed=1)
+    a = O.run(model, w0, X, Y, 0.02, 0.9, order="round_robin")
+    b = O.run(model, w0, X, Y, 0.02, 0.9, order="stage_major")
+    for wa, wb in zip(a.W, b.W):
+        np.testing.assert_array_equal(wa, wb)
+    np.testing.assert_array_equal(a.losses, b.losses)
+
+
+def test_spectrain_differs_from_vanilla_and_staleness_witness():
+    """S:356 staleness witness: for N ≥ 2 some mini-batch's F weights on device 0
+    differ from the weights current at its B; SpecTrain changes the result."""
+    model = sd.mlp([8, 8, 8, 4], cuts=[1, 2])
+    w0 = sd.glorot_params(model, 3)
+    X, Y = sd.images_and_labels(8, 4, 8, 4, seed=4)
+    a = O.run(model, w0, X, Y, 0.05, 0.9, pred=O.PRED_SPECTRAIN)
+    b = O.run(model, w0, X, Y, 0.05, 0.9, pred=O.PRED_NONE)
+    assert not np.allclose(np.concatenate(a.W), np.concatenate(b.W), rtol=1e-9)
+    assert any(f.base_version != bb.base_version for f in b.trace[0] for bb in b.trace[0]
+               if f.dir == O.FWD and bb.dir == O.BWD and f.mb == bb.mb)
