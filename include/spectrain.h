@@ -1,0 +1,299 @@
+/*
+ * spectrain.h — C-ABI of libspectrain.so: one SpecTrain pipeline stage per
+ * context (Chen, Yang, Cheng, arXiv 1809.02839).
+ *
+ * Citation key: P:n = PAPER.md line n, S:n = SPEC.md line n (the reference text
+ * the method comes from); DESIGN.md §3 lists every reading (D1..D20) taken where
+ * the paper is silent.
+ *
+ * What a context computes (per pipeline stage k of N):
+ *   - PipeDream 1F1B task order over M mini-batches: min(N-k-1, M) warm-up
+ *     forwards, then (F, B) pairs, then cooldown backwards ("round-robin").
+ *   - Before every task, the predicted weights  Ŵ = W − s·η·v  (Eq. 4)
+ *     with the version difference s of Eq. 5 (forward) or Eq. 6
+ *     (backward); pred = ST_PRED_NONE forces s = 0 (vanilla).
+ *   - Forward per dense layer: Z = A·Ŵ_W + Ŵ_b, A' = ReLU(Z) (identity on the
+ *     network's last layer); softmax cross-entropy (batch mean) on the last stage
+ *     (D11).
+ *   - Backward: dZ = dA ⊙ 1[Z>0]; g_W = Aᵀ·dZ; g_b = Σ_b dZ; dA_prev = dZ·Ŵ_Wᵀ
+ *     (D5: the backward re-predicts with s_B from the current state).
+ *   - After each backward: v ← γ·v + (1−γ)·g (Eq. 1; ST_MOMENTUM_HEAVY_BALL:
+ *     v ← γ·v + g, D2), W ← W − η·v (D1, Momentum SGD P:373), version += 1.
+ *
+ * Memory and ownership. All device memory is allocated by the CALLER (PyTorch in
+ * the shipped binding) with the byte counts st_query_sizes reports, and is
+ * BORROWED by the context until st_destroy. Device pointers must be 256-byte
+ * aligned. Host pointers are read or written only during the call that receives
+ * them. Streams are borrowed as well; every device operation of a context is
+ * ordered on its compute stream (NCCL transfers included), and calls return
+ * before the GPU work finishes unless stated (st_sync blocks).
+ *
+ * Errors. Every function that can fail returns st_status; the message of the last
+ * failure on the calling thread is available from st_last_error(). No C++
+ * exception crosses this boundary. A failed call leaves the context usable only
+ * for st_last_error/st_destroy unless the status is ST_ERR_INPUT/ST_ERR_SHAPE
+ * (argument rejected before any state changed).
+ *
+ * Parameter layout (identical on host and device): stage-local flat fp32
+ * array, layer-major; for each layer W_l [n_in × n_out] row-major, then b_l
+ * [n_out] if the layer has a bias.
+ */
+#ifndef SPECTRAIN_H_
+#define SPECTRAIN_H_
+
+#include <stddef.h>
+#include <stdint.h>
+
+#if defined(__GNUC__)
+#define ST_API __attribute__((visibility("default")))
+#else
+#define ST_API
+#endif
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+typedef enum {
+  ST_OK = 0,
+  ST_ERR_INPUT = 1,     /* invalid argument / configuration */
+  ST_ERR_SHAPE = 2,     /* layer chain or buffer size mismatch */
+  ST_ERR_STATE = 3,     /* op out of program order: fatal invariant */
+  ST_ERR_CUDA = 4,      /* CUDA runtime/driver failure */
+  ST_ERR_NCCL = 5,      /* NCCL failure */
+  ST_ERR_OOM = 6,       /* caller-provided buffer too small */
+  ST_ERR_DIVERGED = 7,  /* non-finite loss; message names the mini-batch */
+  ST_ERR_UNSUPPORTED = 8
+} st_status;
+
+enum { ST_FWD = 0, ST_BWD = 1 };
+enum { ST_ACT_NONE = 0, ST_ACT_RELU = 1 };
+enum { ST_PRED_SPECTRAIN = 0, ST_PRED_NONE = 1 };
+enum { ST_MOMENTUM_EMA = 0, ST_MOMENTUM_HEAVY_BALL = 1 };
+/* GEMM arithmetic. FP32X3 = 3xTF32 split (hi·hi + hi·lo + lo·hi) on tcgen05
+ * tensor cores, fp32 accumulate in TMEM — the parity mode.
+ * TF32 = single-pass tcgen05 kind::tf32 (fast mode, NOT parity-grade).
+ * SIMT = CUDA-core fp32 FMA (bring-up / diagnostic mode). */
+enum { ST_GEMM_FP32X3 = 0, ST_GEMM_TF32 = 1, ST_GEMM_SIMT = 2 };
+enum { ST_LOSS_SOFTMAX_CE = 0 };
+/* Stage-to-stage transport. NCCL: one process per GPU, ncclSend/ncclRecv between
+ * adjacent stages on the compute stream. LOCAL: several stage contexts in ONE
+ * process (same or different GPUs) linked with st_connect_local; messages are
+ * device copies ordered by CUDA events, handed over through host channels. */
+enum { ST_TRANSPORT_NCCL = 0, ST_TRANSPORT_LOCAL = 1 };
+
+typedef struct {
+  int32_t n_in;
+  int32_t n_out;
+  int32_t act;   /* ST_ACT_RELU for hidden layers, ST_ACT_NONE for the network's last layer */
+  int32_t bias;  /* 1: the layer has a bias vector b_l [n_out] */
+} st_layer;
+
+typedef struct {
+  int32_t num_layers;       /* layers of the WHOLE network */
+  const st_layer* layers;   /* [num_layers]; read during st_query_sizes / st_init only */
+  int32_t num_stages;       /* N ≥ 1 */
+  const int32_t* cuts;      /* [N-1] strictly increasing; stage k owns layers [cuts[k-1], cuts[k]) */
+  int32_t stage;            /* k, 0 ≤ k < N */
+  int32_t batch;            /* B ≥ 1 (mini-batch size) */
+  float lr;                 /* η > 0 */
+  float gamma;              /* γ, 0 < γ ≤ 1 */
+  int32_t pred;             /* ST_PRED_* */
+  int32_t momentum;         /* ST_MOMENTUM_* */
+  int32_t gemm;             /* ST_GEMM_* */
+  int32_t loss;             /* ST_LOSS_SOFTMAX_CE */
+  int32_t transport;        /* ST_TRANSPORT_* */
+  int32_t device;           /* CUDA device ordinal of this stage */
+  int64_t max_minibatches;  /* capacity of the on-device loss vector (≥ the M of st_run) */
+  uint8_t nccl_id[128];     /* ST_TRANSPORT_NCCL: ncclUniqueId from st_get_nccl_id on stage 0 */
+} st_config;
+
+/* Byte counts the caller must allocate (0 = not needed: the buffer aliases W). */
+typedef struct {
+  int64_t params;       /* P_k: parameters of this stage (elements) */
+  int64_t w_bytes;      /* W  — current weights */
+  int64_t v_bytes;      /* V  — smoothed gradient, Eq. 1 */
+  int64_t g_bytes;      /* G  — gradient of the last backward */
+  int64_t wf_bytes;     /* WF — Ŵ for the next forward (0 if s_F = 0) */
+  int64_t wb_bytes;     /* WB — Ŵ for the next backward (0 if s_B = 0 or s_B = s_F) */
+  int64_t stash_bytes;  /* activation stash: N−k slots × Σ_l B·n_in_l fp32 */
+  int64_t work_bytes;   /* messages, logits, split-K workspace, counters, losses */
+  int32_t s_fwd;        /* Eq. 5 value used by this stage (0 under ST_PRED_NONE) */
+  int32_t s_bwd;        /* Eq. 6 value */
+} st_sizes;
+
+typedef struct {
+  float* W;
+  float* V;
+  float* G;
+  float* WF;    /* NULL when wf_bytes == 0 */
+  float* WB;    /* NULL when wb_bytes == 0 */
+  void* stash;
+  void* work;
+} st_buffers;
+
+/* One trace record per executed task. base_version = updates
+ * already applied on this stage; s = version difference; target = base + s. */
+typedef struct {
+  int32_t stage;
+  int32_t op_idx;
+  int32_t dir;      /* ST_FWD / ST_BWD */
+  int32_t pad_;
+  int64_t mb;
+  int64_t base_version;
+  int64_t s;
+  int64_t target;
+} st_event;
+
+/* One communication step of a stage program (host-side plan, no device work).
+ * Ops in one record form one ncclGroupStart/End group. kind: 0 send_fwd (to k+1,
+ * activation of mb), 1 recv_fwd (from k−1), 2 send_bwd (to k−1, gradient),
+ * 3 recv_bwd (from k+1). before_op = index of the program op it precedes
+ * (2M = after the last op). */
+typedef struct {
+  int32_t before_op;
+  int32_t n_ops;
+  int32_t kind[2];
+  int64_t mb[2];
+} st_comm_group;
+
+typedef struct {
+  int32_t ops_run;      /* tasks executed by this st_step call (0..3) */
+  int32_t ran_forward;  /* mini-batch index of the forward run, −1 if none */
+  int32_t ran_backward; /* mini-batch index of the backward run, −1 if none */
+  int32_t done;         /* 1 when the stage program is complete */
+  float loss;           /* loss of ran_forward on the last stage (synchronises), else NaN */
+} st_step_info;
+
+typedef struct st_ctx st_ctx;
+
+/* ---- pure / host-only ------------------------------------------------------ */
+
+/* Eq. 5 (dir = ST_FWD): ⌊k/2⌋ + N − k − 1; Eq. 6 (ST_BWD):
+ * ⌊k/2⌋. Returns −1 unless 0 ≤ k < N (and N ≥ 1). */
+ST_API int st_version_difference(int k, int N, int dir);
+
+/* The event list stage k WILL produce for M mini-batches (program of SURVEY §8(c)
+ * step 2 with the Eq. 5/6 values and base versions of §8(a) a1). Host only, no
+ * GPU. out may be NULL to query the count (*n = 2M). ST_ERR_INPUT if cap < 2M. */
+ST_API st_status st_program(int N, int k, int64_t M, int pred, st_event* out, size_t cap, size_t* n);
+
+/* The communication plan of stage k (order of grouped sends/receives the engine
+ * issues). Host only. out may be NULL to query the count. */
+ST_API st_status st_comm_plan(int N, int k, int64_t M, st_comm_group* out, size_t cap, size_t* n);
+
+/* Byte counts for cfg (validates the whole config; no device work). */
+ST_API st_status st_query_sizes(const st_config* cfg, st_sizes* out);
+
+/* 128-byte ncclUniqueId; call on stage 0 and broadcast (torch.distributed). */
+ST_API st_status st_get_nccl_id(uint8_t out[128]);
+
+/* ---- context lifecycle ----------------------------------------------------- */
+
+/* Binds buffers and the compute stream (a cudaStream_t cast to void*; NULL =
+ * legacy default stream), builds the 1F1B program, initialises NCCL for
+ * ST_TRANSPORT_NCCL (collective across the N stage processes: every stage must
+ * call st_init), sets V = 0, WF = WB = W, version = 0. W is NOT initialised:
+ * call st_set_params before the first task. */
+ST_API st_status st_init(const st_config* cfg, const st_buffers* bufs, void* stream, st_ctx** out);
+
+/* LOCAL transport: link ctxs[0..n) as consecutive stages 0..n−1 of one pipeline
+ * in this process. Required before any task of a LOCAL context. */
+ST_API st_status st_connect_local(st_ctx** ctxs, int32_t n);
+
+ST_API void st_destroy(st_ctx* ctx);
+
+/* W ← host[0..n) (n must equal P_k), V ← 0, WF = WB = W, version ← 0, program
+ * restarted. Synchronous. ST_ERR_SHAPE on n mismatch. */
+ST_API st_status st_set_params(st_ctx* ctx, const float* host, size_t n);
+
+/* Copies W and V (either may be NULL) to host and the version counter. Synchronous. */
+ST_API st_status st_get_params(st_ctx* ctx, float* W, float* V, size_t n, int64_t* version);
+
+/* ---- the verbs of one pipeline task ---------------------------------------- */
+
+/* F(mb) with WF. Stage 0 reads x_dev [B × n_in] (device, copied into the
+ * stash); other stages receive the activation from stage k−1. The last stage
+ * reads labels y_dev [B] int32 and writes the loss to its on-device loss vector
+ * at index mb; if loss_host ≠ NULL it synchronises and copies the loss out
+ * (ST_ERR_DIVERGED if non-finite). Non-last stages send their output to k+1.
+ * ST_ERR_STATE if F(mb) is not the next op of the program. */
+ST_API st_status st_stage_forward(st_ctx* ctx, int64_t mb, const float* x_dev, const int32_t* y_dev, float* loss_host);
+
+/* B(mb) with WB: receives dA from k+1 (last stage: its stored CE gradient),
+ * computes dX (sent to k−1 unless k = 0) and G. Does NOT update: the engine
+ * requires st_predict_and_update before the next task. ST_ERR_STATE otherwise. */
+ST_API st_status st_stage_backward(st_ctx* ctx, int64_t mb);
+
+/* The fused K-B kernel on the whole stage arena: Eq. 1, the D1 apply, WF (s_F > 0)
+ * and WB (s_B > 0, s_B ≠ s_F) for the next tasks; version += 1.
+ * ST_ERR_STATE if no backward is pending. */
+ST_API st_status st_predict_and_update(st_ctx* ctx);
+
+/* Runs this stage's next program slot: warm-up F; steady F + B + update;
+ * cooldown B + update. x_dev/y_dev are the inputs of the forward mini-batch
+ * (stage 0 / last stage; others may pass NULL). */
+ST_API st_status st_step(st_ctx* ctx, const float* x_dev, const int32_t* y_dev, st_step_info* out);
+
+/* Whole M-mini-batch program from the current position. xs_dev [M × B × n_in]
+ * (stage 0), ys_dev [M × B] (last stage); losses_host [M] (last stage, may be
+ * NULL) — when non-NULL the call synchronises and checks finiteness. */
+ST_API st_status st_run(st_ctx* ctx, int64_t M, const float* xs_dev, const int32_t* ys_dev, float* losses_host);
+
+/* LOCAL transport: runs st_run on every context of a connected group, one host
+ * thread per stage; returns the first failure. */
+ST_API st_status st_run_group(st_ctx** ctxs, int32_t n, int64_t M, const float* xs_dev, const int32_t* ys_dev,
+                       float* losses_host);
+
+/* Trace of all tasks executed since st_set_params. out may be NULL (count query). */
+ST_API st_status st_get_trace(st_ctx* ctx, st_event* out, size_t cap, size_t* n);
+
+/* Device pointer of the on-device loss vector (last stage; NULL otherwise). */
+ST_API const float* st_losses_device(st_ctx* ctx);
+
+ST_API st_status st_sync(st_ctx* ctx);
+
+/* ---- measurement hooks ----------------------------------------------------- */
+
+/* Profiling: when on, the engine brackets every launch of each kernel class with
+ * CUDA events on the compute stream. Classes: 0 update (K-B), 1 gemm_fwd,
+ * 2 gemm_dx, 3 gemm_dw, 4 loss (CE + bias-grad), 5 comm. */
+ST_API st_status st_set_profiling(st_ctx* ctx, int on);
+/* Per class: total milliseconds and launch count since profiling was switched on
+ * (synchronises). arrays of length 6. */
+ST_API st_status st_get_profile(st_ctx* ctx, double* total_ms, int64_t* launches);
+/* Kernel launches issued by this context since creation (all classes). */
+ST_API int64_t st_kernel_launches(st_ctx* ctx);
+
+/* ---- raw kernels (test and bench hooks on caller arenas) --------------------- */
+
+/* K-B on caller arenas of n fp32: v' = γv + (1−γ)g (HEAVY_BALL: γv + g),
+ * w' = w − η v', WF = w' − s_F η v' (if WF ≠ NULL), WB = w' − s_B η v' (if WB ≠ NULL).
+ * All pointers 16-byte aligned device pointers; n = 0 is a no-op.
+ * ST_ERR_INPUT on misalignment. Stream-ordered. */
+ST_API st_status st_update_predict_raw(float* W, float* V, const float* G, float* WF, float* WB, size_t n, float lr,
+                                float gamma, int sF, int sB, int momentum, void* stream);
+
+/* GEMM kernels of the stage path, on caller buffers (device, row-major fp32).
+ *   op 0 (fwd): Z[B×out] = X[B×in]·W[in×out] + b[out]; relu → ReLU applied.
+ *   op 1 (dX):  D[B×in]  = dZ[B×out]·W[in×out]ᵀ, then ⊙ 1[mask[B×in] > 0] if mask.
+ *   op 2 (dW):  G[in×out] = X[B×in]ᵀ·dZ[B×out]; gb[out] = Σ_b dZ[b,:] if gb ≠ NULL.
+ * Buffer roles: a = X (op 0, 2) or dZ (op 1); b = W (op 0, 1) or dZ (op 2);
+ * bias/mask = b (op 0) or mask (op 1) or gb (op 2); out = Z / D / G.
+ * work: device scratch of st_gemm_workspace_bytes() bytes. */
+ST_API st_status st_gemm_raw(int op, int gemm_mode, int B, int n_in, int n_out, const float* a, const float* b,
+                      const float* aux, float* aux_out, float* out, int relu, void* work, void* stream);
+ST_API int64_t st_gemm_workspace_bytes(int B, int n_in, int n_out);
+
+/* Softmax-CE on caller buffers: logits [B×C], labels [B] → loss_dev[0] (batch
+ * mean) and dlogits [B×C] = (softmax − onehot)/B. */
+ST_API st_status st_softmax_ce_raw(const float* logits, const int32_t* labels, int B, int C, float* loss_dev,
+                            float* dlogits, void* work, void* stream);
+
+ST_API const char* st_last_error(void);
+ST_API const char* st_version(void);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* SPECTRAIN_H_ */

@@ -1,0 +1,681 @@
+// The stage engine behind the C-ABI (include/spectrain.h).
+//
+// One context = one pipeline stage k of N. It owns no device memory:
+// it carves the caller's arenas, runs the stage's 1F1B program (schedule.cpp),
+// and for each task launches, on the borrowed compute stream:
+//   F(i): [recv act] → per layer gemm_fwd with WF (+bias, ReLU) → [CE] → [send act]
+//   B(j): [recv grad] → per layer (reverse) gemm_dx with WB (ReLU mask fused),
+//         gemm_dw (+bias grad) → [send grad]
+//   update: K-B (k_update.cu) — Eq. 1, D1 apply, WF/WB for the next tasks.
+#include <cmath>
+#include <cstring>
+#include <thread>
+
+#include "engine.hpp"
+
+using st::set_error;
+
+namespace st {
+namespace {
+
+int64_t align_up(int64_t x, int64_t a) { return (x + a - 1) / a * a; }
+constexpr int64_t kAlignBytes = 256;
+constexpr int64_t kAlignFloats = kAlignBytes / 4;
+
+struct Layout {
+  std::vector<LayerInfo> layers;
+  int64_t P = 0;
+  int64_t slot_elems = 0;
+  int S = 1;
+  int sF = 0, sB = 0;
+  int in_first = 0, out_last = 0, max_in = 0, max_out = 0;
+  int prev_act = ST_ACT_NONE;  // activation of the layer feeding this stage (k > 0)
+  bool first = true, last = true;
+  // work offsets (bytes)
+  int64_t off_send_fwd = -1, off_recv_bwd = -1, off_send_bwd = -1, off_logits = -1, off_dlogits = -1;
+  int64_t off_bufA = -1, off_bufB = -1, off_losses = -1, off_rowloss = -1, off_ring_fwd = -1, off_ring_bwd = -1;
+  int64_t off_ws = -1;
+  size_t ring_fwd_elems = 0, ring_bwd_elems = 0;
+  st_sizes sizes{};
+};
+
+st_status validate_and_layout(const st_config* c, Layout* L) {
+  if (!c) return set_error(ST_ERR_INPUT, "config is NULL");
+  if (c->num_stages < 1) return set_error(ST_ERR_INPUT, "num_stages must be >= 1 (got %d)", c->num_stages);
+  if (c->stage < 0 || c->stage >= c->num_stages)
+    return set_error(ST_ERR_INPUT, "stage %d outside [0, %d)", c->stage, c->num_stages);
+  if (c->num_layers < c->num_stages || !c->layers)
+    return set_error(ST_ERR_INPUT, "need at least one layer per stage (%d layers, %d stages)", c->num_layers,
+                     c->num_stages);
+  if (c->batch < 1) return set_error(ST_ERR_INPUT, "batch must be >= 1");
+  if (!(c->lr > 0.f) || !std::isfinite(c->lr)) return set_error(ST_ERR_INPUT, "lr must be > 0");
+  if (!(c->gamma > 0.f && c->gamma <= 1.f)) return set_error(ST_ERR_INPUT, "gamma must be in (0, 1]");
+  if (c->pred != ST_PRED_SPECTRAIN && c->pred != ST_PRED_NONE) return set_error(ST_ERR_INPUT, "bad pred");
+  if (c->momentum != ST_MOMENTUM_EMA && c->momentum != ST_MOMENTUM_HEAVY_BALL)
+    return set_error(ST_ERR_INPUT, "bad momentum");
+  if (c->gemm != ST_GEMM_FP32X3 && c->gemm != ST_GEMM_TF32 && c->gemm != ST_GEMM_SIMT)
+    return set_error(ST_ERR_INPUT, "bad gemm mode");
+  if (c->loss != ST_LOSS_SOFTMAX_CE) return set_error(ST_ERR_INPUT, "bad loss");
+  if (c->transport != ST_TRANSPORT_NCCL && c->transport != ST_TRANSPORT_LOCAL)
+    return set_error(ST_ERR_INPUT, "bad transport");
+  if (c->max_minibatches < 1) return set_error(ST_ERR_INPUT, "max_minibatches must be >= 1");
+  const int N = c->num_stages, k = c->stage;
+  if (N > 1 && !c->cuts) return set_error(ST_ERR_INPUT, "cuts is NULL");
+  std::vector<int> bounds{0};
+  for (int i = 0; i < N - 1; ++i) {
+    if (c->cuts[i] <= bounds.back() || c->cuts[i] >= c->num_layers)
+      return set_error(ST_ERR_INPUT, "cuts must be strictly increasing in (0, %d)", c->num_layers);
+    bounds.push_back(c->cuts[i]);
+  }
+  bounds.push_back(c->num_layers);
+  for (int l = 0; l < c->num_layers; ++l) {
+    const st_layer& y = c->layers[l];
+    if (y.n_in < 1 || y.n_out < 1) return set_error(ST_ERR_SHAPE, "layer %d: bad dims", l);
+    if (y.act != ST_ACT_NONE && y.act != ST_ACT_RELU) return set_error(ST_ERR_INPUT, "layer %d: bad act", l);
+    if (l > 0 && c->layers[l - 1].n_out != y.n_in)
+      return set_error(ST_ERR_SHAPE, "layer chain mismatch: layer %d out %d != layer %d in %d", l - 1,
+                       c->layers[l - 1].n_out, l, y.n_in);
+  }
+  const int l0 = bounds[k], l1 = bounds[k + 1];
+  const int64_t B = c->batch;
+  L->first = (k == 0);
+  L->last = (k == N - 1);
+  L->S = N - k;
+  L->prev_act = (k > 0) ? c->layers[l0 - 1].act : ST_ACT_NONE;
+  int64_t off = 0, soff = 0;
+  for (int l = l0; l < l1; ++l) {
+    const st_layer& y = c->layers[l];
+    LayerInfo li{y.n_in, y.n_out, y.act, y.bias ? 1 : 0, off, -1, soff};
+    off += (int64_t)y.n_in * y.n_out;
+    if (y.bias) {
+      li.b_off = off;
+      off += y.n_out;
+    }
+    soff += align_up(B * y.n_in, kAlignFloats);
+    L->max_in = std::max(L->max_in, y.n_in);
+    L->max_out = std::max(L->max_out, y.n_out);
+    L->layers.push_back(li);
+  }
+  L->P = off;
+  L->slot_elems = soff;
+  L->in_first = c->layers[l0].n_in;
+  L->out_last = c->layers[l1 - 1].n_out;
+  L->sF = c->pred == ST_PRED_NONE ? 0 : version_difference(k, N, ST_FWD);
+  L->sB = c->pred == ST_PRED_NONE ? 0 : version_difference(k, N, ST_BWD);
+
+  // work carve-up
+  int64_t w = 0;
+  auto take = [&](int64_t floats) {
+    const int64_t o = w;
+    w += align_up(floats * 4, kAlignBytes);
+    return o;
+  };
+  const int64_t width = std::max(L->max_in, L->max_out);
+  if (!L->last) {
+    L->off_send_fwd = take(B * L->out_last);
+    L->off_recv_bwd = take(B * L->out_last);
+  }
+  if (!L->first) L->off_send_bwd = take(B * L->in_first);
+  if (L->last) {
+    L->off_logits = take(B * L->out_last);
+    L->off_dlogits = take(B * L->out_last);
+    L->off_rowloss = take(B);
+  }
+  L->off_bufA = take(B * width);
+  L->off_bufB = take(B * width);
+  L->off_losses = take(c->max_minibatches);
+  if (c->transport == ST_TRANSPORT_LOCAL) {
+    if (!L->last) {
+      L->ring_fwd_elems = (size_t)(B * L->out_last);
+      L->off_ring_fwd = take((int64_t)L->ring_fwd_elems * (N + 1));
+    }
+    if (!L->first) {
+      L->ring_bwd_elems = (size_t)(B * L->in_first);
+      L->off_ring_bwd = take((int64_t)L->ring_bwd_elems * (N + 1));
+    }
+  }
+  L->off_ws = w;
+  w += align_up(gemm_workspace_bytes((int)B, L->max_in, L->max_out), kAlignBytes);
+
+  st_sizes& z = L->sizes;
+  z.params = L->P;
+  z.w_bytes = z.v_bytes = z.g_bytes = align_up(L->P * 4, kAlignBytes);
+  z.wf_bytes = L->sF > 0 ? z.w_bytes : 0;
+  z.wb_bytes = (L->sB > 0 && L->sB != L->sF) ? z.w_bytes : 0;
+  z.stash_bytes = (int64_t)L->S * L->slot_elems * 4;
+  z.work_bytes = w;
+  z.s_fwd = L->sF;
+  z.s_bwd = L->sB;
+  return ST_OK;
+}
+
+// ---- profiling helpers ----------------------------------------------------------
+struct Timed {
+  st_ctx* c;
+  int cls;
+  cudaEvent_t b = nullptr;
+  Timed(st_ctx* ctx, int k) : c(ctx), cls(k) {
+    if (!c->prof.on) return;
+    cudaEvent_t a = get();
+    b = get();
+    cudaEventRecord(a, c->stream);
+    c->prof.pairs.push_back({cls, a, b});
+  }
+  ~Timed() {
+    if (b) cudaEventRecord(b, c->stream);
+  }
+  cudaEvent_t get() {
+    if (!c->prof.pool.empty()) {
+      cudaEvent_t e = c->prof.pool.back();
+      c->prof.pool.pop_back();
+      return e;
+    }
+    cudaEvent_t e;
+    cudaEventCreate(&e);
+    return e;
+  }
+};
+
+}  // namespace
+
+// ---- engine internals used by capi.cpp -------------------------------------------
+
+st_status query_sizes(const st_config* c, st_sizes* out) {
+  Layout L;
+  ST_TRY(validate_and_layout(c, &L));
+  if (out) *out = L.sizes;
+  return ST_OK;
+}
+
+static void begin_session(st_ctx* c, int64_t M) {
+  c->program = build_program(c->N, c->k, M);
+  c->plan = build_comm_plan(c->N, c->k, M);
+  c->pc = 0;
+  c->plan_sent = 0;
+  c->plan_recv = 0;
+  c->session_M = M;
+  c->pending_update = false;
+}
+
+st_status ctx_init(const st_config* cfg, const st_buffers* bufs, void* stream, st_ctx** out) {
+  if (!out) return set_error(ST_ERR_INPUT, "out is NULL");
+  *out = nullptr;
+  Layout L;
+  ST_TRY(validate_and_layout(cfg, &L));
+  if (!bufs || !bufs->W || !bufs->V || !bufs->G || !bufs->stash || !bufs->work)
+    return set_error(ST_ERR_INPUT, "missing buffer (W, V, G, stash, work are required)");
+  if (L.sizes.wf_bytes && !bufs->WF) return set_error(ST_ERR_INPUT, "WF buffer required (s_F = %d)", L.sF);
+  if (L.sizes.wb_bytes && !bufs->WB) return set_error(ST_ERR_INPUT, "WB buffer required (s_B = %d)", L.sB);
+  auto misaligned = [](const void* p) { return p && ((uintptr_t)p % kAlignBytes) != 0; };
+  if (misaligned(bufs->W) || misaligned(bufs->V) || misaligned(bufs->G) || misaligned(bufs->WF) ||
+      misaligned(bufs->WB) || misaligned(bufs->stash) || misaligned(bufs->work))
+    return set_error(ST_ERR_INPUT, "device buffers must be %lld-byte aligned", (long long)kAlignBytes);
+  ST_CUDA_TRY(cudaSetDevice(cfg->device));
+
+  std::unique_ptr<st_ctx> c(new st_ctx());
+  c->N = cfg->num_stages;
+  c->k = cfg->stage;
+  c->B = cfg->batch;
+  c->lr = cfg->lr;
+  c->gamma = cfg->gamma;
+  c->pred = cfg->pred;
+  c->momentum = cfg->momentum;
+  c->gemm = cfg->gemm;
+  c->loss = cfg->loss;
+  c->transport_kind = cfg->transport;
+  c->device = cfg->device;
+  c->max_mb = cfg->max_minibatches;
+  c->layers = L.layers;
+  c->P = L.P;
+  c->sF = L.sF;
+  c->sB = L.sB;
+  c->max_width_in = L.max_in;
+  c->max_width_out = L.max_out;
+  c->first_stage = L.first;
+  c->last_stage = L.last;
+  c->prev_act = L.prev_act;
+  c->in_first = L.in_first;
+  c->out_last = L.out_last;
+  c->W = bufs->W;
+  c->V = bufs->V;
+  c->G = bufs->G;
+  c->WF_out = L.sF > 0 ? bufs->WF : nullptr;
+  c->WB_out = (L.sB > 0 && L.sB != L.sF) ? bufs->WB : nullptr;
+  c->WF = L.sF > 0 ? bufs->WF : bufs->W;
+  c->WB = L.sB == 0 ? bufs->W : (L.sB == L.sF ? c->WF : bufs->WB);
+  c->stash = static_cast<float*>(bufs->stash);
+  c->slot_elems = L.slot_elems;
+  c->S = L.S;
+  char* w = static_cast<char*>(bufs->work);
+  auto at = [&](int64_t off) { return off < 0 ? nullptr : reinterpret_cast<float*>(w + off); };
+  c->send_fwd = at(L.off_send_fwd);
+  c->recv_bwd = at(L.off_recv_bwd);
+  c->send_bwd = at(L.off_send_bwd);
+  c->logits = at(L.off_logits);
+  c->dlogits = at(L.off_dlogits);
+  c->rowloss = at(L.off_rowloss);
+  c->bufA = at(L.off_bufA);
+  c->bufB = at(L.off_bufB);
+  c->losses_dev = at(L.off_losses);
+  c->ring_fwd = at(L.off_ring_fwd);
+  c->ring_bwd = at(L.off_ring_bwd);
+  c->ring_fwd_elems = L.ring_fwd_elems;
+  c->ring_bwd_elems = L.ring_bwd_elems;
+  c->gemm_ws = w + L.off_ws;
+  c->stream = static_cast<cudaStream_t>(stream);
+
+  if (c->transport_kind == ST_TRANSPORT_NCCL) {
+    st_status e;
+    c->tp = make_nccl_transport(cfg->nccl_id, c->N, c->k, c->device, &e);
+    if (e != ST_OK) return e;
+  }
+  ST_CUDA_TRY(cudaMemsetAsync(c->V, 0, (size_t)c->P * 4, c->stream));
+  ST_CUDA_TRY(cudaMemsetAsync(c->losses_dev, 0xff, (size_t)c->max_mb * 4, c->stream));  // NaN
+  begin_session(c.get(), c->max_mb);
+  *out = c.release();
+  return ST_OK;
+}
+
+st_status ctx_connect_local(st_ctx** ctxs, int n) {
+  if (!ctxs || n < 1) return set_error(ST_ERR_INPUT, "connect_local: need >= 1 context");
+  const int N = ctxs[0]->N;
+  if (n != N) return set_error(ST_ERR_INPUT, "connect_local: %d contexts for a %d-stage pipeline", n, N);
+  for (int k = 0; k < n; ++k) {
+    if (!ctxs[k] || ctxs[k]->k != k || ctxs[k]->N != N || ctxs[k]->transport_kind != ST_TRANSPORT_LOCAL)
+      return set_error(ST_ERR_INPUT, "connect_local: context %d is not stage %d of a LOCAL %d-stage pipeline", k, k,
+                       N);
+    if (ctxs[k]->B != ctxs[0]->B) return set_error(ST_ERR_SHAPE, "connect_local: batch mismatch");
+    if (k > 0 && ctxs[k - 1]->out_last != ctxs[k]->in_first)
+      return set_error(ST_ERR_SHAPE, "connect_local: cut width mismatch between stages %d and %d", k - 1, k);
+  }
+  auto link = make_local_link(N);
+  for (int k = 0; k < n; ++k) {
+    st_ctx* c = ctxs[k];
+    ST_CUDA_TRY(cudaSetDevice(c->device));
+    st_status e;
+    c->tp = make_local_transport(link, k, c->ring_fwd, c->ring_bwd, c->ring_fwd_elems, c->ring_bwd_elems, &e);
+    if (e != ST_OK) return e;
+    c->link = link;
+  }
+  return ST_OK;
+}
+
+void ctx_destroy(st_ctx* c) {
+  if (!c) return;
+  cudaSetDevice(c->device);
+  if (c->stream) cudaStreamSynchronize(c->stream);
+  for (auto& p : c->prof.pairs) {
+    cudaEventDestroy(p.a);
+    cudaEventDestroy(p.b);
+  }
+  for (auto e : c->prof.pool) cudaEventDestroy(e);
+  delete c;
+}
+
+st_status ctx_set_params(st_ctx* c, const float* host, size_t n) {
+  if (!c || !host) return set_error(ST_ERR_INPUT, "NULL argument");
+  if ((int64_t)n != c->P) return set_error(ST_ERR_SHAPE, "set_params: n = %zu but stage has %lld", n, (long long)c->P);
+  ST_CUDA_TRY(cudaSetDevice(c->device));
+  ST_CUDA_TRY(cudaMemcpyAsync(c->W, host, n * 4, cudaMemcpyHostToDevice, c->stream));
+  ST_CUDA_TRY(cudaMemsetAsync(c->V, 0, n * 4, c->stream));
+  if (c->WF_out) ST_CUDA_TRY(cudaMemcpyAsync(c->WF_out, c->W, n * 4, cudaMemcpyDeviceToDevice, c->stream));
+  if (c->WB_out) ST_CUDA_TRY(cudaMemcpyAsync(c->WB_out, c->W, n * 4, cudaMemcpyDeviceToDevice, c->stream));
+  ST_CUDA_TRY(cudaMemsetAsync(c->losses_dev, 0xff, (size_t)c->max_mb * 4, c->stream));
+  ST_CUDA_TRY(cudaStreamSynchronize(c->stream));
+  c->version = 0;
+  c->trace.clear();
+  begin_session(c, c->max_mb);
+  return ST_OK;
+}
+
+st_status ctx_get_params(st_ctx* c, float* W, float* V, size_t n, int64_t* version) {
+  if (!c) return set_error(ST_ERR_INPUT, "NULL context");
+  if ((W || V) && (int64_t)n != c->P)
+    return set_error(ST_ERR_SHAPE, "get_params: n = %zu but stage has %lld", n, (long long)c->P);
+  ST_CUDA_TRY(cudaSetDevice(c->device));
+  ST_CUDA_TRY(cudaStreamSynchronize(c->stream));
+  if (W) ST_CUDA_TRY(cudaMemcpy(W, c->W, n * 4, cudaMemcpyDeviceToHost));
+  if (V) ST_CUDA_TRY(cudaMemcpy(V, c->V, n * 4, cudaMemcpyDeviceToHost));
+  if (version) *version = c->version;
+  return ST_OK;
+}
+
+// ---- communication --------------------------------------------------------------
+
+static CommOp comm_op(st_ctx* c, int kind, int64_t mb) {
+  const size_t nin = (size_t)c->B * c->in_first, nout = (size_t)c->B * c->out_last;
+  switch (kind) {
+    case CK_SEND_FWD: return {kind, mb, c->send_fwd, nout};
+    case CK_RECV_FWD:
+      return {kind, mb, c->stash + (size_t)(mb % c->S) * c->slot_elems + c->layers[0].stash_off, nin};
+    case CK_SEND_BWD: return {kind, mb, c->send_bwd, nin};
+    default: return {kind, mb, c->recv_bwd, nout};
+  }
+}
+
+static st_status issue(st_ctx* c, const CommGroup& g, bool sends, bool recvs) {
+  CommOp ops[2];
+  int n = 0;
+  for (int i = 0; i < g.n_ops; ++i) {
+    const bool is_send = g.kind[i] == CK_SEND_FWD || g.kind[i] == CK_SEND_BWD;
+    if ((is_send && sends) || (!is_send && recvs)) ops[n++] = comm_op(c, g.kind[i], g.mb[i]);
+  }
+  if (n == 0) return ST_OK;
+  if (!c->tp) return set_error(ST_ERR_STATE, "stage %d: transport not connected", c->k);
+  Timed t(c, KC_COMM);
+  return c->tp->group(ops, n, c->stream);
+}
+
+// Before task n: make sure every receive it needs has been issued.
+static st_status comm_before_task(st_ctx* c, size_t n) {
+  const bool eager = c->tp && c->tp->eager_groups();
+  if (eager) {
+    while (c->plan_sent < c->plan.size() && (size_t)c->plan[c->plan_sent].before_op <= n) {
+      ST_TRY(issue(c, c->plan[c->plan_sent], true, true));
+      c->plan_sent++;
+    }
+    c->plan_recv = c->plan_sent;
+  } else {
+    while (c->plan_recv < c->plan.size() && (size_t)c->plan[c->plan_recv].before_op <= n) {
+      ST_TRY(issue(c, c->plan[c->plan_recv], false, true));
+      c->plan_recv++;
+    }
+  }
+  return ST_OK;
+}
+
+// After task n: issue its sends (NCCL: together with the next task's receive).
+static st_status comm_after_task(st_ctx* c, size_t n) {
+  const bool eager = c->tp && c->tp->eager_groups();
+  if (eager) {
+    while (c->plan_sent < c->plan.size() && (size_t)c->plan[c->plan_sent].before_op <= n + 1) {
+      ST_TRY(issue(c, c->plan[c->plan_sent], true, true));
+      c->plan_sent++;
+    }
+    c->plan_recv = c->plan_sent;
+  } else {
+    while (c->plan_sent < c->plan.size() && (size_t)c->plan[c->plan_sent].before_op <= n + 1) {
+      ST_TRY(issue(c, c->plan[c->plan_sent], true, false));
+      c->plan_sent++;
+    }
+  }
+  return ST_OK;
+}
+
+// ---- tasks -----------------------------------------------------------------------
+
+static GemmArgs gargs(st_ctx* c, const LayerInfo& L) {
+  GemmArgs g;
+  g.mode = c->gemm;
+  g.B = c->B;
+  g.n_in = L.n_in;
+  g.n_out = L.n_out;
+  g.work = c->gemm_ws;
+  g.stream = c->stream;
+  return g;
+}
+
+static st_status forward_compute(st_ctx* c, int64_t mb, const float* x_dev, const int32_t* y_dev) {
+  float* slot = c->stash + (size_t)(mb % c->S) * c->slot_elems;
+  const float* Wh = c->WF;  // Eq. 4 with s_F (aliases W when s_F = 0)
+  if (c->first_stage) {
+    if (!x_dev) return set_error(ST_ERR_INPUT, "stage 0 forward needs x_dev");
+    ST_CUDA_TRY(cudaMemcpyAsync(slot + c->layers[0].stash_off, x_dev, (size_t)c->B * c->in_first * 4,
+                                cudaMemcpyDeviceToDevice, c->stream));
+  }
+  const size_t nl = c->layers.size();
+  for (size_t l = 0; l < nl; ++l) {
+    const LayerInfo& L = c->layers[l];
+    float* out = (l + 1 < nl) ? slot + c->layers[l + 1].stash_off : (c->last_stage ? c->logits : c->send_fwd);
+    Timed t(c, KC_GEMM_FWD);
+    ST_TRY(gemm_fwd(gargs(c, L), slot + L.stash_off, Wh + L.w_off, L.bias ? Wh + L.b_off : nullptr, out,
+                    L.act == ST_ACT_RELU));
+    c->launches += gemm_last_launches();
+  }
+  if (c->last_stage) {
+    if (!y_dev) return set_error(ST_ERR_INPUT, "last stage forward needs y_dev");
+    Timed t(c, KC_LOSS);
+    ST_TRY(launch_softmax_ce(c->logits, y_dev, c->B, c->out_last, c->rowloss, c->losses_dev + (mb % c->max_mb),
+                             c->dlogits, c->stream));
+    c->launches += 2;
+  }
+  return ST_OK;
+}
+
+static st_status backward_compute(st_ctx* c, int64_t mb) {
+  float* slot = c->stash + (size_t)(mb % c->S) * c->slot_elems;
+  const float* Wh = c->WB;  // Eq. 4 with s_B (D5: re-predicted from the current state)
+  const float* dZ = c->last_stage ? c->dlogits : c->recv_bwd;
+  const int nl = (int)c->layers.size();
+  float* pp[2] = {c->bufA, c->bufB};
+  int next = 0;
+  for (int l = nl - 1; l >= 0; --l) {
+    const LayerInfo& L = c->layers[l];
+    const float* Ain = slot + L.stash_off;
+    float* D = nullptr;
+    if (!(c->first_stage && l == 0)) {
+      D = (l == 0) ? c->send_bwd : pp[next];
+      if (D == dZ) D = pp[next ^= 1];
+      // ReLU mask of the layer that produced Ain (D12: ReLU'(0) = 0): 1[Z>0] == 1[ReLU(Z)>0]
+      const int producer_act = (l > 0) ? c->layers[l - 1].act : c->prev_act;
+      Timed t(c, KC_GEMM_DX);
+      ST_TRY(gemm_dx(gargs(c, L), dZ, Wh + L.w_off, producer_act == ST_ACT_RELU ? Ain : nullptr, D));
+      c->launches += gemm_last_launches();
+    }
+    {
+      Timed t(c, KC_GEMM_DW);
+      ST_TRY(gemm_dw(gargs(c, L), Ain, dZ, c->G + L.w_off, L.bias ? c->G + L.b_off : nullptr));
+      c->launches += gemm_last_launches();
+    }
+    if (D) {
+      dZ = D;
+      next ^= 1;
+    }
+  }
+  return ST_OK;
+}
+
+static st_status run_task(st_ctx* c, const float* x_dev, const int32_t* y_dev) {
+  if (c->pc >= c->program.size()) return set_error(ST_ERR_STATE, "stage %d: program finished", c->k);
+  if (c->pending_update)
+    return set_error(ST_ERR_STATE, "stage %d: predict_and_update must follow every backward", c->k);
+  const Task t = c->program[c->pc];
+  ST_TRY(comm_before_task(c, c->pc));
+  st_event e{};
+  e.stage = c->k;
+  e.op_idx = (int32_t)c->trace.size();
+  e.dir = t.dir;
+  e.mb = t.mb;
+  e.base_version = c->version;
+  e.s = t.dir == ST_FWD ? c->sF : c->sB;
+  e.target = e.base_version + e.s;
+  c->trace.push_back(e);
+  if (t.dir == ST_FWD)
+    ST_TRY(forward_compute(c, t.mb, x_dev, y_dev));
+  else {
+    ST_TRY(backward_compute(c, t.mb));
+    c->pending_update = true;
+  }
+  ST_TRY(comm_after_task(c, c->pc));
+  c->pc++;
+  return ST_OK;
+}
+
+st_status ctx_update(st_ctx* c) {
+  if (!c->pending_update) return set_error(ST_ERR_STATE, "stage %d: no backward pending", c->k);
+  const UpdateConsts k = make_update_consts(c->lr, c->gamma, c->sF, c->sB, c->momentum);
+  {
+    Timed t(c, KC_UPDATE);
+    ST_TRY(launch_update_predict(c->W, c->V, c->G, c->WF_out, c->WB_out, (size_t)c->P, k, c->stream));
+  }
+  c->launches += 1;
+  c->version += 1;
+  c->pending_update = false;
+  return ST_OK;
+}
+
+static st_status expect(st_ctx* c, int dir, int64_t mb) {
+  if (c->pc >= c->program.size())
+    return set_error(ST_ERR_STATE, "stage %d: program of %lld mini-batches finished", c->k, (long long)c->session_M);
+  const Task& t = c->program[c->pc];
+  if (t.dir != dir || t.mb != mb)
+    return set_error(ST_ERR_STATE, "stage %d: next op is %c(%lld), not %c(%lld)", c->k, t.dir == ST_FWD ? 'F' : 'B',
+                     (long long)t.mb, dir == ST_FWD ? 'F' : 'B', (long long)mb);
+  return ST_OK;
+}
+
+st_status ctx_forward(st_ctx* c, int64_t mb, const float* x_dev, const int32_t* y_dev, float* loss_host) {
+  ST_CUDA_TRY(cudaSetDevice(c->device));
+  ST_TRY(expect(c, ST_FWD, mb));
+  ST_TRY(run_task(c, x_dev, y_dev));
+  if (loss_host && c->last_stage) {
+    ST_CUDA_TRY(cudaMemcpyAsync(loss_host, c->losses_dev + (mb % c->max_mb), 4, cudaMemcpyDeviceToHost, c->stream));
+    ST_CUDA_TRY(cudaStreamSynchronize(c->stream));
+    if (!std::isfinite(*loss_host))
+      return set_error(ST_ERR_DIVERGED, "non-finite loss at mini-batch %lld", (long long)mb);
+  }
+  return ST_OK;
+}
+
+st_status ctx_backward(st_ctx* c, int64_t mb) {
+  ST_CUDA_TRY(cudaSetDevice(c->device));
+  ST_TRY(expect(c, ST_BWD, mb));
+  return run_task(c, nullptr, nullptr);
+}
+
+st_status ctx_predict_and_update(st_ctx* c) {
+  ST_CUDA_TRY(cudaSetDevice(c->device));
+  return ctx_update(c);
+}
+
+static const float* x_of(st_ctx* c, const float* xs, int64_t mb) {
+  return (c->first_stage && xs) ? xs + (size_t)mb * c->B * c->in_first : nullptr;
+}
+static const int32_t* y_of(st_ctx* c, const int32_t* ys, int64_t mb) {
+  return (c->last_stage && ys) ? ys + (size_t)mb * c->B : nullptr;
+}
+
+st_status ctx_step(st_ctx* c, const float* x_dev, const int32_t* y_dev, st_step_info* info) {
+  ST_CUDA_TRY(cudaSetDevice(c->device));
+  st_step_info z{0, -1, -1, 0, NAN};
+  if (c->pending_update) return set_error(ST_ERR_STATE, "stage %d: pending update", c->k);
+  if (c->pc >= c->program.size()) {
+    z.done = 1;
+    if (info) *info = z;
+    return ST_OK;
+  }
+  const Task t = c->program[c->pc];
+  if (t.dir == ST_FWD) {
+    ST_TRY(run_task(c, x_dev, y_dev));
+    z.ops_run++;
+    z.ran_forward = (int32_t)t.mb;
+    if (c->last_stage) {
+      ST_CUDA_TRY(cudaMemcpyAsync(&z.loss, c->losses_dev + (t.mb % c->max_mb), 4, cudaMemcpyDeviceToHost, c->stream));
+      ST_CUDA_TRY(cudaStreamSynchronize(c->stream));
+    }
+  }
+  // a warm-up F is followed by another F; a steady F by its paired B; cooldown is B alone
+  if (c->pc < c->program.size() && c->program[c->pc].dir == ST_BWD) {
+    const Task b = c->program[c->pc];
+    ST_TRY(run_task(c, nullptr, nullptr));
+    ST_TRY(ctx_update(c));
+    z.ops_run += 2;
+    z.ran_backward = (int32_t)b.mb;
+  }
+  z.done = c->pc >= c->program.size();
+  if (info) *info = z;
+  return ST_OK;
+}
+
+st_status ctx_run(st_ctx* c, int64_t M, const float* xs, const int32_t* ys, float* losses_host) {
+  ST_CUDA_TRY(cudaSetDevice(c->device));
+  if (M < 0 || M > c->max_mb)
+    return set_error(ST_ERR_INPUT, "run: M = %lld outside [0, max_minibatches = %lld]", (long long)M,
+                     (long long)c->max_mb);
+  if (c->pc != 0 && c->pc != c->program.size())
+    return set_error(ST_ERR_STATE, "run: stage %d is in the middle of a program (op %zu of %zu)", c->k, c->pc,
+                     c->program.size());
+  if (c->pending_update) return set_error(ST_ERR_STATE, "run: pending update");
+  if (c->first_stage && M > 0 && !xs) return set_error(ST_ERR_INPUT, "run: stage 0 needs xs_dev");
+  if (c->last_stage && M > 0 && !ys) return set_error(ST_ERR_INPUT, "run: last stage needs ys_dev");
+  begin_session(c, M);
+  while (c->pc < c->program.size()) {
+    const Task t = c->program[c->pc];
+    ST_TRY(run_task(c, x_of(c, xs, t.mb), y_of(c, ys, t.mb)));
+    if (t.dir == ST_BWD) ST_TRY(ctx_update(c));
+  }
+  if (losses_host && c->last_stage && M > 0) {
+    ST_CUDA_TRY(cudaMemcpyAsync(losses_host, c->losses_dev, (size_t)M * 4, cudaMemcpyDeviceToHost, c->stream));
+    ST_CUDA_TRY(cudaStreamSynchronize(c->stream));
+    for (int64_t i = 0; i < M; ++i)
+      if (!std::isfinite(losses_host[i]))
+        return set_error(ST_ERR_DIVERGED, "non-finite loss at mini-batch %lld", (long long)i);
+  }
+  return ST_OK;
+}
+
+st_status ctx_run_group(st_ctx** ctxs, int n, int64_t M, const float* xs, const int32_t* ys, float* losses_host) {
+  if (!ctxs || n < 1) return set_error(ST_ERR_INPUT, "run_group: no contexts");
+  std::vector<st_status> res(n, ST_OK);
+  std::vector<std::string> msg(n);
+  std::vector<std::thread> th;
+  for (int k = 0; k < n; ++k) {
+    th.emplace_back([&, k] {
+      st_ctx* c = ctxs[k];
+      cudaSetDevice(c->device);
+      res[k] = ctx_run(c, M, c->first_stage ? xs : nullptr, c->last_stage ? ys : nullptr,
+                       c->last_stage ? losses_host : nullptr);
+      if (res[k] != ST_OK) msg[k] = st_last_error();
+    });
+  }
+  for (auto& t : th) t.join();
+  for (int k = 0; k < n; ++k)
+    if (res[k] != ST_OK) return set_error(res[k], "stage %d: %s", k, msg[k].c_str());
+  return ST_OK;
+}
+
+st_status ctx_get_trace(st_ctx* c, st_event* out, size_t cap, size_t* n) {
+  if (!c || !n) return set_error(ST_ERR_INPUT, "NULL argument");
+  *n = c->trace.size();
+  if (!out) return ST_OK;
+  if (cap < c->trace.size()) return set_error(ST_ERR_INPUT, "trace: cap %zu < %zu events", cap, c->trace.size());
+  memcpy(out, c->trace.data(), c->trace.size() * sizeof(st_event));
+  return ST_OK;
+}
+
+st_status ctx_set_profiling(st_ctx* c, int on) {
+  ST_CUDA_TRY(cudaSetDevice(c->device));
+  ST_CUDA_TRY(cudaStreamSynchronize(c->stream));
+  for (auto& p : c->prof.pairs) {
+    c->prof.pool.push_back(p.a);
+    c->prof.pool.push_back(p.b);
+  }
+  c->prof.pairs.clear();
+  for (int i = 0; i < KC_COUNT; ++i) {
+    c->prof.total_ms[i] = 0;
+    c->prof.launches[i] = 0;
+  }
+  c->prof.on = on != 0;
+  return ST_OK;
+}
+
+st_status ctx_get_profile(st_ctx* c, double* total_ms, int64_t* launches) {
+  ST_CUDA_TRY(cudaSetDevice(c->device));
+  ST_CUDA_TRY(cudaStreamSynchronize(c->stream));
+  for (auto& p : c->prof.pairs) {
+    float ms = 0.f;
+    ST_CUDA_TRY(cudaEventElapsedTime(&ms, p.a, p.b));
+    c->prof.total_ms[p.cls] += ms;
+    c->prof.launches[p.cls] += 1;
+    c->prof.pool.push_back(p.a);
+    c->prof.pool.push_back(p.b);
+  }
+  c->prof.pairs.clear();
+  for (int i = 0; i < KC_COUNT; ++i) {
+    if (total_ms) total_ms[i] = c->prof.total_ms[i];
+    if (launches) launches[i] = c->prof.launches[i];
+  }
+  return ST_OK;
+}
+
+}  // namespace st

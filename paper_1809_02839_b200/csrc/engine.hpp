@@ -1,0 +1,124 @@
+// Stage engine: one SpecTrain pipeline stage bound to caller-owned arenas.
+#pragma once
+
+#include <memory>
+#include <vector>
+
+#include "common.hpp"
+#include "kernels.hpp"
+
+namespace st {
+
+struct Task {
+  int dir;  // ST_FWD / ST_BWD
+  int64_t mb;
+};
+
+enum CommKind { CK_SEND_FWD = 0, CK_RECV_FWD = 1, CK_SEND_BWD = 2, CK_RECV_BWD = 3 };
+using CommGroup = st_comm_group;
+
+int version_difference(int k, int N, int dir);
+std::vector<Task> build_program(int N, int k, int64_t M);
+std::vector<st_event> program_events(int N, int k, int64_t M, int pred);
+std::vector<CommGroup> build_comm_plan(int N, int k, int64_t M);
+
+// One communication op of a group: device buffer + element count.
+struct CommOp {
+  int kind;
+  int64_t mb;
+  float* buf;
+  size_t count;
+};
+
+class Transport {
+ public:
+  virtual ~Transport() = default;
+  // Issue one group on `stream` (NCCL: ncclGroupStart/End; LOCAL: sends then receives).
+  virtual st_status group(const CommOp* ops, int n, cudaStream_t stream) = 0;
+  virtual bool eager_groups() const = 0;  // NCCL: issue whole groups eagerly at task end
+};
+
+std::unique_ptr<Transport> make_nccl_transport(const uint8_t id[128], int N, int k, int device, st_status* err);
+
+struct LocalLink;  // shared channels of a LOCAL pipeline (transport.cpp)
+std::unique_ptr<Transport> make_local_transport(std::shared_ptr<LocalLink> link, int k, float* ring_fwd,
+                                                float* ring_bwd, size_t fwd_elems, size_t bwd_elems,
+                                                st_status* err);
+std::shared_ptr<LocalLink> make_local_link(int N);
+
+struct LayerInfo {
+  int n_in, n_out, act, bias;
+  int64_t w_off;      // offset of W_l in the stage arena (elements)
+  int64_t b_off;      // offset of b_l (−1 if none)
+  int64_t stash_off;  // offset of A_in of this layer inside one stash slot
+};
+
+struct Profiler {
+  bool on = false;
+  struct Pair {
+    int cls;
+    cudaEvent_t a, b;
+  };
+  std::vector<Pair> pairs;
+  std::vector<cudaEvent_t> pool;
+  double total_ms[KC_COUNT] = {};
+  int64_t launches[KC_COUNT] = {};
+};
+
+}  // namespace st
+
+struct st_ctx {
+  // configuration
+  int N = 1, k = 0, B = 1;
+  float lr = 0.f, gamma = 0.f;
+  int pred = ST_PRED_SPECTRAIN, momentum = ST_MOMENTUM_EMA, gemm = ST_GEMM_FP32X3, loss = ST_LOSS_SOFTMAX_CE;
+  int transport_kind = ST_TRANSPORT_NCCL;
+  int device = 0;
+  int64_t max_mb = 0;
+  std::vector<st::LayerInfo> layers;
+  int64_t P = 0;
+  int sF = 0, sB = 0;
+  int max_width_in = 0, max_width_out = 0;
+  bool first_stage = true, last_stage = true;
+
+  // arenas (borrowed)
+  float *W = nullptr, *V = nullptr, *G = nullptr;
+  const float *WF = nullptr, *WB = nullptr;  // weights the next F / B read (may alias W)
+  float *WF_out = nullptr, *WB_out = nullptr;  // K-B outputs (NULL when aliased)
+  int prev_act = ST_ACT_NONE;                  // activation of the layer feeding stage k > 0
+  int in_first = 0, out_last = 0;
+  float* stash = nullptr;
+  int64_t slot_elems = 0;
+  int S = 1;  // stash slots = N − k
+  // work carve-up
+  float* send_fwd = nullptr;  // [B × out_last]  (non-last stage)
+  float* recv_bwd = nullptr;  // [B × out_last]  (non-last stage)
+  float* send_bwd = nullptr;  // [B × in_first]  (k > 0)
+  float* logits = nullptr;    // [B × C]         (last stage)
+  float* dlogits = nullptr;   // [B × C]
+  float* bufA = nullptr;      // [B × max width] backward ping-pong
+  float* bufB = nullptr;
+  float* losses_dev = nullptr;  // [max_mb]
+  float* rowloss = nullptr;     // [B]
+  float* ring_fwd = nullptr;    // LOCAL transport rings
+  float* ring_bwd = nullptr;
+  size_t ring_fwd_elems = 0, ring_bwd_elems = 0;
+  void* gemm_ws = nullptr;
+  cudaStream_t stream = nullptr;
+
+  // program state
+  std::vector<st::Task> program;
+  std::vector<st::CommGroup> plan;
+  size_t pc = 0;
+  size_t plan_sent = 0;  // LOCAL: sends issued (by group index); NCCL: groups issued
+  size_t plan_recv = 0;  // LOCAL: receives issued
+  int64_t session_M = 0;
+  int64_t version = 0;
+  bool pending_update = false;
+  std::vector<st_event> trace;
+  std::unique_ptr<st::Transport> tp;
+  std::shared_ptr<st::LocalLink> link;
+
+  st::Profiler prof;
+  int64_t launches = 0;
+};

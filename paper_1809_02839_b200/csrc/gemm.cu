@@ -1,0 +1,64 @@
+// GEMM dispatch for the stage path: tcgen05 tensor-core kernels (k_gemm_tc.cu)
+// for ST_GEMM_FP32X3 / ST_GEMM_TF32, CUDA-core fp32 (k_gemm_simt.cu) for
+// ST_GEMM_SIMT. Same contract for every mode (kernels.hpp).
+#include "kernels.hpp"
+
+namespace st {
+
+st_status simt_fwd(const GemmArgs& g, const float* X, const float* W, const float* bias, float* Z, int relu);
+st_status simt_dx(const GemmArgs& g, const float* dZ, const float* W, const float* mask, float* D);
+st_status simt_dw(const GemmArgs& g, const float* X, const float* dZ, float* G, float* gb);
+
+st_status tc_fwd(const GemmArgs& g, const float* X, const float* W, const float* bias, float* Z, int relu);
+st_status tc_dx(const GemmArgs& g, const float* dZ, const float* W, const float* mask, float* D);
+st_status tc_dw(const GemmArgs& g, const float* X, const float* dZ, float* G, float* gb);
+int64_t tc_workspace_bytes(int B, int max_in, int max_out);
+int tc_last_launches();
+
+static thread_local int g_last_launches = 0;
+int gemm_last_launches() { return g_last_launches; }
+
+int64_t gemm_workspace_bytes(int B, int max_in, int max_out) { return tc_workspace_bytes(B, max_in, max_out); }
+
+static st_status check(const GemmArgs& g) {
+  if (g.B <= 0 || g.n_in <= 0 || g.n_out <= 0)
+    return set_error(ST_ERR_INPUT, "gemm: bad shape B=%d in=%d out=%d", g.B, g.n_in, g.n_out);
+  if (g.mode != ST_GEMM_SIMT && g.mode != ST_GEMM_FP32X3 && g.mode != ST_GEMM_TF32)
+    return set_error(ST_ERR_INPUT, "gemm: unknown mode %d", g.mode);
+  return ST_OK;
+}
+
+st_status gemm_fwd(const GemmArgs& g, const float* X, const float* W, const float* bias, float* Z, int relu) {
+  ST_TRY(check(g));
+  if (g.mode == ST_GEMM_SIMT) {
+    g_last_launches = 1;
+    return simt_fwd(g, X, W, bias, Z, relu);
+  }
+  st_status s = tc_fwd(g, X, W, bias, Z, relu);
+  g_last_launches = tc_last_launches();
+  return s;
+}
+
+st_status gemm_dx(const GemmArgs& g, const float* dZ, const float* W, const float* mask, float* D) {
+  ST_TRY(check(g));
+  if (g.mode == ST_GEMM_SIMT) {
+    g_last_launches = 1;
+    return simt_dx(g, dZ, W, mask, D);
+  }
+  st_status s = tc_dx(g, dZ, W, mask, D);
+  g_last_launches = tc_last_launches();
+  return s;
+}
+
+st_status gemm_dw(const GemmArgs& g, const float* X, const float* dZ, float* G, float* gb) {
+  ST_TRY(check(g));
+  if (g.mode == ST_GEMM_SIMT) {
+    g_last_launches = gb ? 2 : 1;
+    return simt_dw(g, X, dZ, G, gb);
+  }
+  st_status s = tc_dw(g, X, dZ, G, gb);
+  g_last_launches = tc_last_launches();
+  return s;
+}
+
+}  // namespace st

@@ -1,0 +1,75 @@
+// K-C: softmax cross-entropy forward+backward at the last stage.
+//   loss = mean_b [ logsumexp(Z_b) − Z_b[y_b] ]           (D11 batch mean)
+//   dZ   = (softmax(Z) − onehot(y)) / B
+// One warp per row (max-subtracted softmax), then a single-CTA fixed-order sum of
+// the per-row losses (deterministic).
+#include "kernels.hpp"
+
+namespace st {
+namespace {
+
+__device__ __forceinline__ float warp_max(float v) {
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) v = fmaxf(v, __shfl_xor_sync(0xffffffffu, v, o));
+  return v;
+}
+__device__ __forceinline__ float warp_sum(float v) {
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
+  return v;
+}
+
+__global__ void __launch_bounds__(256) ce_rows_kernel(const float* __restrict__ Z, const int32_t* __restrict__ y,
+                                                      int B, int C, float inv_b, float* __restrict__ rowloss,
+                                                      float* __restrict__ dZ) {
+  const int warp = (blockIdx.x * blockDim.x + threadIdx.x) >> 5;
+  const int lane = threadIdx.x & 31;
+  if (warp >= B) return;
+  const float* z = Z + (size_t)warp * C;
+  float m = -INFINITY;
+  for (int c = lane; c < C; c += 32) m = fmaxf(m, z[c]);
+  m = warp_max(m);
+  float s = 0.f;
+  for (int c = lane; c < C; c += 32) s += expf(z[c] - m);
+  s = warp_sum(s);
+  const int label = y[warp];
+  const float inv_s = 1.0f / s;
+  float* d = dZ + (size_t)warp * C;
+  for (int c = lane; c < C; c += 32) {
+    const float p = expf(z[c] - m) * inv_s;
+    d[c] = (p - (c == label ? 1.0f : 0.0f)) * inv_b;
+  }
+  if (lane == 0) rowloss[warp] = (logf(s) + m) - z[label];
+}
+
+__global__ void __launch_bounds__(1024) mean_kernel(const float* __restrict__ rowloss, int B, float inv_b,
+                                                    float* __restrict__ out) {
+  // fixed-order: thread t sums rows t, t+1024, ...; then a fixed tree
+  __shared__ float part[1024];
+  float acc = 0.f;
+  for (int i = threadIdx.x; i < B; i += 1024) acc += rowloss[i];
+  part[threadIdx.x] = acc;
+  __syncthreads();
+  for (int w = 512; w > 0; w >>= 1) {
+    if ((int)threadIdx.x < w) part[threadIdx.x] += part[threadIdx.x + w];
+    __syncthreads();
+  }
+  if (threadIdx.x == 0) out[0] = part[0] * inv_b;
+}
+
+}  // namespace
+
+st_status launch_softmax_ce(const float* Z, const int32_t* y, int B, int C, float* rowloss, float* loss_out,
+                            float* dZ, cudaStream_t s) {
+  if (B <= 0 || C <= 0) return set_error(ST_ERR_INPUT, "softmax_ce: B=%d C=%d", B, C);
+  const float inv_b = 1.0f / (float)B;
+  const int warps_per_cta = 8;
+  ce_rows_kernel<<<(B + warps_per_cta - 1) / warps_per_cta, 32 * warps_per_cta, 0, s>>>(Z, y, B, C, inv_b,
+                                                                                       rowloss, dZ);
+  ST_CUDA_TRY(cudaGetLastError());
+  mean_kernel<<<1, 1024, 0, s>>>(rowloss, B, inv_b, loss_out);
+  ST_CUDA_TRY(cudaGetLastError());
+  return ST_OK;
+}
+
+}  // namespace st

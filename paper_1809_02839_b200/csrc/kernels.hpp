@@ -1,0 +1,45 @@
+// Launchers of the stage kernels (sm_100a). Every launcher is stream-ordered,
+// checks its launch with cudaGetLastError and returns st_status.
+#pragma once
+
+#include "common.hpp"
+
+namespace st {
+
+// ---- K-B: fused smoothed-gradient update + apply + weight prediction --------
+// (Eq. 1, D1 apply, Eq. 4 P:326-328 for s_F and s_B)
+struct UpdateConsts {
+  float c_gamma;  // γ
+  float c_one;    // (1−γ) for EMA, 1 for heavy-ball
+  float c_eta;    // η
+  float c_f;      // s_F·η
+  float c_b;      // s_B·η
+};
+UpdateConsts make_update_consts(float lr, float gamma, int sF, int sB, int momentum);
+st_status launch_update_predict(float* W, float* V, const float* G, float* WF, float* WB, size_t n,
+                                const UpdateConsts& c, cudaStream_t s);
+
+// ---- GEMMs of a dense stage (row-major fp32 buffers) ---------------------------
+// fwd: Z[B×out] = X[B×in]·W[in×out] + b, optional ReLU
+// dX : D[B×in]  = (dZ[B×out]·Wᵀ) ⊙ 1[mask > 0] (mask may be null)
+// dW : G[in×out] = Xᵀ·dZ ; gb[out] = Σ_b dZ (gb may be null)
+struct GemmArgs {
+  int mode;  // ST_GEMM_*
+  int B, n_in, n_out;
+  void* work;  // split-K workspace (gemm_workspace_bytes)
+  cudaStream_t stream;
+};
+int64_t gemm_workspace_bytes(int B, int max_in, int max_out);
+st_status gemm_fwd(const GemmArgs& g, const float* X, const float* W, const float* bias, float* Z, int relu);
+st_status gemm_dx(const GemmArgs& g, const float* dZ, const float* W, const float* mask, float* D);
+st_status gemm_dw(const GemmArgs& g, const float* X, const float* dZ, float* G, float* gb);
+// number of kernel launches the last gemm_* call issued on this thread
+int gemm_last_launches();
+
+// ---- softmax cross-entropy, batch mean (D11) -----------------------------------
+// loss_out[0] = mean_b −log softmax(Z_b)[y_b];  dZ = (softmax − onehot)/B.
+// rowloss: device scratch [B] floats.
+st_status launch_softmax_ce(const float* Z, const int32_t* y, int B, int C, float* rowloss, float* loss_out,
+                            float* dZ, cudaStream_t s);
+
+}  // namespace st

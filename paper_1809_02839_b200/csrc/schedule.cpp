@@ -1,0 +1,101 @@
+// Host-side 1F1B program and communication plan of one pipeline stage.
+//
+// Program ("issues a forward task and a backward task in a round-robin
+// manner", reading D8): stage k of N runs
+//   w = min(N−k−1, M) warm-up forwards F(0..w−1),
+//   then pairs F(w+j), B(j) for j = 0..M−w−1,
+//   then cooldown backwards B(M−w..M−1).
+// Version differences: Eq. 5 for F, Eq. 6 for B.
+// Base versions: an F(i) runs after B(i−w−1), so c_F = max(0, i−w); a B(j) runs
+// after B(j−1), so c_B = j.
+//
+// Communication plan. Per task: F(i) on k > 0 needs recv_fwd(i)
+// before it; F(i) on k < N−1 is followed by send_fwd(i); B(j) on k < N−1 needs
+// recv_bwd(j); B(j) on k > 0 is followed by send_bwd(j). Between two consecutive
+// tasks the trailing send of the first and the leading receive of the second form
+// ONE NCCL group when they talk to the same peer (Megatron's
+// send_forward_recv_backward / send_backward_recv_forward pairing); otherwise the
+// send is issued first as its own group.
+#include <vector>
+
+#include "engine.hpp"
+
+namespace st {
+
+int version_difference(int k, int N, int dir) {
+  if (N < 1 || k < 0 || k >= N) return -1;
+  return dir == ST_FWD ? (k / 2 + N - k - 1) : (k / 2);
+}
+
+std::vector<Task> build_program(int N, int k, int64_t M) {
+  std::vector<Task> p;
+  if (M <= 0) return p;
+  const int64_t w = std::min<int64_t>(N - k - 1, M);
+  p.reserve((size_t)(2 * M));
+  for (int64_t i = 0; i < w; ++i) p.push_back({ST_FWD, i});
+  for (int64_t j = 0; j < M - w; ++j) {
+    p.push_back({ST_FWD, w + j});
+    p.push_back({ST_BWD, j});
+  }
+  for (int64_t j = M - w; j < M; ++j) p.push_back({ST_BWD, j});
+  return p;
+}
+
+std::vector<st_event> program_events(int N, int k, int64_t M, int pred) {
+  std::vector<Task> p = build_program(N, k, M);
+  std::vector<st_event> ev;
+  ev.reserve(p.size());
+  int64_t version = 0;
+  const int64_t sF = pred == ST_PRED_NONE ? 0 : version_difference(k, N, ST_FWD);
+  const int64_t sB = pred == ST_PRED_NONE ? 0 : version_difference(k, N, ST_BWD);
+  for (size_t n = 0; n < p.size(); ++n) {
+    st_event e{};
+    e.stage = k;
+    e.op_idx = (int32_t)n;
+    e.dir = p[n].dir;
+    e.mb = p[n].mb;
+    e.base_version = version;
+    e.s = p[n].dir == ST_FWD ? sF : sB;
+    e.target = e.base_version + e.s;
+    ev.push_back(e);
+    if (p[n].dir == ST_BWD) ++version;
+  }
+  return ev;
+}
+
+namespace {
+struct Op {
+  int kind;  // CK_*
+  int64_t mb;
+};
+int peer_of(int kind) { return (kind == CK_SEND_FWD || kind == CK_RECV_BWD) ? +1 : -1; }
+}  // namespace
+
+std::vector<CommGroup> build_comm_plan(int N, int k, int64_t M) {
+  std::vector<Task> p = build_program(N, k, M);
+  std::vector<CommGroup> plan;
+  auto pre = [&](const Task& t, Op* o) -> bool {
+    if (t.dir == ST_FWD && k > 0) { *o = {CK_RECV_FWD, t.mb}; return true; }
+    if (t.dir == ST_BWD && k < N - 1) { *o = {CK_RECV_BWD, t.mb}; return true; }
+    return false;
+  };
+  auto post = [&](const Task& t, Op* o) -> bool {
+    if (t.dir == ST_FWD && k < N - 1) { *o = {CK_SEND_FWD, t.mb}; return true; }
+    if (t.dir == ST_BWD && k > 0) { *o = {CK_SEND_BWD, t.mb}; return true; }
+    return false;
+  };
+  for (size_t n = 0; n <= p.size(); ++n) {
+    Op a{}, b{};
+    const bool has_post = n > 0 && post(p[n - 1], &a);
+    const bool has_pre = n < p.size() && pre(p[n], &b);
+    if (has_post && has_pre && peer_of(a.kind) == peer_of(b.kind)) {
+      plan.push_back({(int32_t)n, 2, {a.kind, b.kind}, {a.mb, b.mb}});
+    } else {
+      if (has_post) plan.push_back({(int32_t)n, 1, {a.kind, -1}, {a.mb, -1}});
+      if (has_pre) plan.push_back({(int32_t)n, 1, {b.kind, -1}, {b.mb, -1}});
+    }
+  }
+  return plan;
+}
+
+}  // namespace st
