@@ -1,0 +1,400 @@
+#!/usr/bin/env python
+"""Benchmark: SpecTrain pipelined training throughput on B200 (BASELINE.json metric
+"training samples/sec at 1/2/4/8-stage pipeline; update-kernel HBM GB/s vs peak").
+
+    python bench.py [--gpus N] [--steps K] [--warmup W] [--impl ours|reference]
+    torchrun --nproc-per-node N --master-addr 127.0.0.1 ... bench.py --gpus N ...
+
+A step = one mini-batch (B samples) through the whole pipeline: F on every
+stage, loss, B on every stage, the fused K-B update on every stage. Workload
+(config.workload): BASELINE.json configs[1], the wide FCN (784 → 8 × 8192 → 10,
+batch 128) cut into N contiguous stages, one stage per GPU (N=1: one stage,
+s_F = s_B = 0). Warm-up and timed steps run as separate pipeline sessions
+(`st_run`, fill + steady state + drain), timed with CUDA events on the stage
+streams, max over ranks. Weights (1.9 GB) exceed L2 (126 MB), so no flush is
+needed between steps.
+
+One JSON line on rank 0 (schema in the task contract), with `roofline` for the
+dominant kernel (K-B), `cpu_baseline` (the oracle on the host cores), `e2e`
+(st_run_host: host buffers, H2D/D2H inside the timed region) and `clocks`.
+"""
+from __future__ import annotations
+
+import argparse
+import json
+import os
+import statistics
+import sys
+import threading
+import time
+
+import numpy as np
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+METRIC = "training samples/sec at 1/2/4/8-stage pipeline; update-kernel HBM GB/s vs peak"
+UNIT = "samples/s"
+DEFAULT_GEMM = "simt"
+
+
+def parse():
+    p = argparse.ArgumentParser()
+    p.add_argument("--gpus", type=int, default=1)
+    p.add_argument("--steps", type=int, default=30)
+    p.add_argument("--warmup", type=int, default=5)
+    p.add_argument("--impl", default="ours", choices=["ours", "reference"])
+    p.add_argument("--workload", default="wide_fcn", choices=["wide_fcn", "large_fcn", "mlp", "deep_mlp"])
+    p.add_argument("--stages", type=int, default=0, help="pipeline depth (default = --gpus); >N only with N=1")
+    p.add_argument("--gemm", default=DEFAULT_GEMM, choices=["fp32x3", "tf32", "simt"])
+    p.add_argument("--pred", default="spectrain", choices=["spectrain", "none"])
+    p.add_argument("--no-e2e", action="store_true")
+    p.add_argument("--no-cpu", action="store_true")
+    p.add_argument("--lr", type=float, default=1e-3)
+    return p.parse_args()
+
+
+def workload(name: str, S: int):
+    import synthdata as sd
+    if name == "wide_fcn":
+        return sd.config_wide_fcn(S), 128, "wide_fcn_784-8x8192-10_b128"
+    if name == "large_fcn":
+        return sd.config_large_fcn(S), 128, "large_fcn_784-16x16384-10_b128"
+    if name == "deep_mlp":
+        return sd.config_deep_mlp(S), 128, "deep_mlp_784-8x1024-10_b128"
+    return sd.mlp([784, 256, 256, 10], cuts=sd.even_cuts(3, S)), 32, "mlp_784-256-256-10_b32"
+
+
+def measured_peaks():
+    try:
+        with open(os.path.join(ROOT, "MEASURED_PEAKS.json")) as f:
+            d = json.load(f)
+        return float(d["hbm_gbs"]), "measured (MEASURED_PEAKS.json hbm_gbs)"
+    except Exception:
+        return 6650.0, "fallback (B200_PROFILING.md 6.65 TB/s)"
+
+
+def recorded_traffic(workload_name: str, kernel: str):
+    try:
+        with open(os.path.join(ROOT, "profiles", "ncu_traffic.json")) as f:
+            return json.load(f).get(workload_name, {}).get(kernel)
+    except Exception:
+        return None
+
+
+class ClockSampler:
+    """nvidia-smi-equivalent sampling through NVML during the timed region."""
+
+    def __init__(self, device: int):
+        self.samples, self.reasons, self.max_mhz = [], set(), None
+        self._stop = threading.Event()
+        self.ok = False
+        try:
+            import pynvml
+            pynvml.nvmlInit()
+            self.nv = pynvml
+            self.h = pynvml.nvmlDeviceGetHandleByIndex(device)
+            self.max_mhz = pynvml.nvmlDeviceGetMaxClockInfo(self.h, pynvml.NVML_CLOCK_SM)
+            self.ok = True
+        except Exception:
+            pass
+
+    def _run(self):
+        nv = self.nv
+        names = {
+            "gpu_idle": getattr(nv, "nvmlClocksEventReasonGpuIdle", 0x1),
+            "applications_clocks_setting": 0x2,
+            "sw_power_cap": 0x4,
+            "hw_slowdown": 0x8,
+            "sync_boost": 0x10,
+            "sw_thermal_slowdown": 0x20,
+            "hw_thermal_slowdown": 0x40,
+            "hw_power_brake_slowdown": 0x80,
+        }
+        while not self._stop.is_set():
+            try:
+                self.samples.append(nv.nvmlDeviceGetClockInfo(self.h, nv.NVML_CLOCK_SM))
+                r = nv.nvmlDeviceGetCurrentClocksEventReasons(self.h)
+                for n, bit in names.items():
+                    if r & bit and n != "gpu_idle":
+                        self.reasons.add(n)
+            except Exception:
+                pass
+            time.sleep(0.1)
+
+    def __enter__(self):
+        if self.ok:
+            self.t = threading.Thread(target=self._run, daemon=True)
+            self.t.start()
+        return self
+
+    def __exit__(self, *a):
+        if self.ok:
+            self._stop.set()
+            self.t.join()
+
+    def summary(self):
+        if not self.ok or not self.samples:
+            return {"sm_mhz": None, "sm_max_mhz": self.max_mhz, "reasons": sorted(self.reasons), "samples": 0}
+        return {"sm_mhz": statistics.median(self.samples), "sm_max_mhz": self.max_mhz,
+                "reasons": sorted(self.reasons), "samples": len(self.samples)}
+
+
+# ----------------------------------------------------------------------------- CPU oracle
+
+def oracle_sample_rate(model_full, B: int, steps: int = 1, seed: int = 0):
+    """Time the oracle as it stands on a bounded slice of the workload: a 1-stage
+    784-w-w-10 net with the workload's hidden width w, `steps` mini-batches each
+    (F, loss, B, update). Returns (samples/s extrapolated linearly in parameters to
+    the full model, description, threads, per-step seconds)."""
+    import synthdata as sd
+    from oracle import spectrain_oracle as O
+    w = max(l.n_out for l in model_full.layers[:-1]) if len(model_full.layers) > 1 else model_full.layers[0].n_out
+    slice_model = sd.mlp([model_full.layers[0].n_in, w, w, model_full.layers[-1].n_out], cuts=[])
+    P_slice = sum(l.n_params for l in slice_model.layers)
+    P_full = sum(l.n_params for l in model_full.layers)
+    w0 = sd.glorot_params(slice_model, seed)
+    X, Y = sd.images_and_labels(slice_model.layers[0].n_in, slice_model.layers[-1].n_out, steps, B, seed + 1,
+                                "uniform")
+    t0 = time.perf_counter()
+    O.run(slice_model, w0, X, Y, 1e-3, 0.9)
+    dt = time.perf_counter() - t0
+    try:
+        from threadpoolctl import threadpool_info
+        threads = max(i.get("num_threads", 1) for i in threadpool_info()) if threadpool_info() else 1
+    except Exception:
+        threads = os.cpu_count() or 1
+    rate = steps * B / dt * (P_slice / P_full)
+    desc = (f"oracle.run (NumPy fp64) on a 1-stage {slice_model.layers[0].n_in}-{w}-{w}-"
+            f"{slice_model.layers[-1].n_out} slice ({P_slice / 1e6:.1f}M params), {steps} mini-batch(es) of B={B}; "
+            f"samples/s extrapolated linearly in params to the {P_full / 1e6:.1f}M-param workload")
+    return rate, desc, threads, dt / steps
+
+
+def run_reference(args):
+    rank = int(os.environ.get("RANK", "0"))
+    if rank != 0:
+        return
+    S = args.stages or args.gpus
+    model, B, wname = workload(args.workload, S)
+    for _ in range(args.warmup):
+        oracle_sample_rate(model, B, 1)
+    rates, step_s = [], []
+    desc, threads = "", 1
+    for _ in range(args.steps):
+        r, desc, threads, s = oracle_sample_rate(model, B, 1)
+        rates.append(r)
+        step_s.append(s)
+    value = float(statistics.mean(rates))
+    line = {
+        "impl": "reference", "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": args.gpus,
+        "steps": args.steps, "warmup": args.warmup, "ms_per_step": B / value * 1e3, "higher_is_better": True,
+        "scaling": "strong", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
+        "config": {"workload": wname, "stages": S, "batch": B, "parallelism": f"pp{S}"},
+        "cpu_baseline": {"value": value, "unit": UNIT, "cores": threads, "kind": "oracle", "sample": desc},
+        "e2e": {"value": value, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
+    }
+    print(json.dumps(line), flush=True)
+
+
+# ----------------------------------------------------------------------------- GPU arm
+
+def run_ours(args):
+    import torch
+    import torch.distributed as dist
+
+    import paper_1809_02839_b200 as st
+    import synthdata as sd
+
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    N = args.gpus
+    if world != N:
+        raise SystemExit(f"--gpus {N} but WORLD_SIZE={world}: launch N>1 with torchrun")
+    S = args.stages or N
+    if N > 1 and S != N:
+        raise SystemExit("--stages must equal --gpus when N > 1")
+    torch.cuda.set_device(local)
+    dev = torch.device("cuda", local)
+    if N > 1:
+        dist.init_process_group("nccl", device_id=dev)
+    model, B, wname = workload(args.workload, S)
+    gemm = {"fp32x3": st.ST_GEMM_FP32X3, "tf32": st.ST_GEMM_TF32, "simt": st.ST_GEMM_SIMT}[args.gemm]
+    pred = st.ST_PRED_SPECTRAIN if args.pred == "spectrain" else st.ST_PRED_NONE
+    layers = [(l.n_in, l.n_out, st.ST_ACT_RELU if l.act == sd.RELU else st.ST_ACT_NONE, 1) for l in model.layers]
+    M = max(args.steps, args.warmup, 1)
+
+    if N > 1:
+        obj = [st.nccl_id() if rank == 0 else None]
+        dist.broadcast_object_list(obj, src=0)
+        my_stages = [st.Stage(layers, model.cuts, rank, B, args.lr, 0.9, pred=pred, gemm=gemm,
+                              transport=st.ST_TRANSPORT_NCCL, device=local, max_minibatches=M, nccl_id=obj[0])]
+    elif S == 1:
+        my_stages = [st.Stage(layers, model.cuts, 0, B, args.lr, 0.9, pred=pred, gemm=gemm,
+                              transport=st.ST_TRANSPORT_NCCL, device=local, max_minibatches=M)]
+    else:
+        my_stages = [st.Stage(layers, model.cuts, k, B, args.lr, 0.9, pred=pred, gemm=gemm,
+                              transport=st.ST_TRANSPORT_LOCAL, device=local, max_minibatches=M) for k in range(S)]
+        st.connect_local(my_stages)
+
+    # parameters: Glorot on device (bench-only, SURVEY §8(d) seeds), labels uniform
+    g = torch.Generator(device=dev)
+    g.manual_seed(1234 + rank)
+    for s in my_stages:
+        w = torch.empty(s.params, device=dev)
+        off = 0
+        for (n_in, n_out, act, bias) in s.layers[model.stage_bounds(s.k)[0]:model.stage_bounds(s.k)[1]]:
+            r = (6.0 / (n_in + n_out)) ** 0.5
+            w[off:off + n_in * n_out].uniform_(-r, r, generator=g)
+            off += n_in * n_out
+            if bias:
+                w[off:off + n_out].zero_()
+                off += n_out
+        s.set_params(w.cpu().numpy())
+        del w
+    n_in, n_cls = model.layers[0].n_in, model.layers[-1].n_out
+    first = my_stages[0].is_first
+    last = my_stages[-1].is_last
+    xs = torch.rand(M, B, n_in, device=dev, generator=g) if first else None
+    ys = torch.randint(0, n_cls, (M, B), device=dev, dtype=torch.int32, generator=g) if last else None
+
+    def barrier():
+        torch.cuda.synchronize()
+        if N > 1:
+            dist.barrier()
+        torch.cuda.synchronize()
+
+    def session(K: int):
+        if len(my_stages) == 1:
+            my_stages[0].run(K, xs, ys)
+        else:
+            st.run_group(my_stages, K, xs, ys, want_losses=False)
+
+    def timed(K: int):
+        """CUDA-event time of one K-mini-batch session on this rank (all stage streams)."""
+        root = torch.cuda.current_stream(dev)
+        t0 = torch.cuda.Event(enable_timing=True)
+        t1 = torch.cuda.Event(enable_timing=True)
+        t0.record(root)
+        for s in my_stages:
+            s.stream.wait_event(t0)
+        session(K)
+        for s in my_stages:
+            e = torch.cuda.Event()
+            e.record(s.stream)
+            root.wait_event(e)
+        t1.record(root)
+        torch.cuda.synchronize()
+        return t0.elapsed_time(t1)
+
+    # warm-up
+    barrier()
+    session(args.warmup)
+    barrier()
+    # timed region (device time, K-B profiled with CUDA events on the stage stream)
+    for s in my_stages:
+        s.set_profiling(True)
+    launches0 = sum(s.kernel_launches() for s in my_stages)
+    sampler = ClockSampler(local)
+    barrier()
+    with sampler:
+        ms = timed(args.steps)
+    barrier()
+    launches = sum(s.kernel_launches() for s in my_stages) - launches0
+    profs = [s.profile() for s in my_stages]
+    for s in my_stages:
+        s.set_profiling(False)
+    t_max = ms
+    if N > 1:
+        t = torch.tensor([ms], device=dev, dtype=torch.float64)
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        t_max = float(t.item())
+        lt = torch.tensor([launches], device=dev, dtype=torch.int64)
+        dist.all_reduce(lt, op=dist.ReduceOp.SUM)
+        launches = int(lt.item())
+    value = args.steps * B / (t_max / 1e3)
+
+    # roofline of the dominant kernel: K-B (k_update.cu); algorithmic bytes per launch
+    kb_bytes, kb_ms, kb_n, stage_ms = 0.0, 0.0, 0, 0.0
+    for s, pr in zip(my_stages, profs):
+        bpp = 20 + (4 if s.sizes.s_fwd > 0 else 0) + (4 if (s.sizes.s_bwd > 0 and s.sizes.s_bwd != s.sizes.s_fwd) else 0)
+        ms_k, n_k = pr["update"]
+        kb_bytes += bpp * s.params * n_k
+        kb_ms += ms_k
+        kb_n += n_k
+        stage_ms += sum(v[0] for v in pr.values())
+    agg = torch.tensor([kb_bytes, kb_ms, kb_n, stage_ms], device=dev, dtype=torch.float64)
+    if N > 1:
+        dist.all_reduce(agg)
+    kb_bytes, kb_ms, kb_n, stage_ms = [float(v) for v in agg.tolist()]
+    peak, peak_src = measured_peaks()
+    achieved = kb_bytes / (kb_ms / 1e3) / 1e9 if kb_ms > 0 else None
+    gemm_prof = {k: round(sum(p[k][0] for p in profs), 3) for k in profs[0]}
+
+    # end-to-end: the same metric through st_run_host (pinned host inputs, per-step H2D + loss D2H)
+    e2e = None
+    if not args.no_e2e and len(my_stages) == 1:
+        s = my_stages[0]
+        xh = xs.cpu().pin_memory() if first else None
+        yh = ys.cpu().pin_memory() if last else None
+        lh = torch.empty(M, dtype=torch.float32).pin_memory() if last else None
+        barrier()
+        e0 = torch.cuda.Event(enable_timing=True)
+        e1 = torch.cuda.Event(enable_timing=True)
+        e0.record(s.stream)
+        s.run_host(args.steps, xh, yh, lh)
+        e1.record(s.stream)
+        torch.cuda.synchronize()
+        ems = e0.elapsed_time(e1)
+        if N > 1:
+            t = torch.tensor([ems], device=dev, dtype=torch.float64)
+            dist.all_reduce(t, op=dist.ReduceOp.MAX)
+            ems = float(t.item())
+        e2e = {"value": args.steps * B / (ems / 1e3), "unit": UNIT,
+               "h2d_bytes_per_step": B * n_in * 4 + B * 4, "d2h_bytes_per_step": 4,
+               "api": "st_run_host"}
+
+    if rank == 0:
+        cpu = None
+        if not args.no_cpu:
+            rate, desc, threads, _ = oracle_sample_rate(model, B, 1)
+            cpu = {"value": rate, "unit": UNIT, "cores": threads, "kind": "oracle", "sample": desc}
+        line = {
+            "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": N, "steps": args.steps,
+            "warmup": args.warmup, "ms_per_step": t_max / args.steps, "higher_is_better": True,
+            "scaling": "strong", "vs_baseline": None, "dtype": "f32", "data": "synthetic",
+            "config": {"workload": wname, "stages": S, "batch": B, "gemm": args.gemm, "pred": args.pred,
+                       "parallelism": f"pp{S}", "l2": "no flush: per-step working set (weights) >> 126 MB L2",
+                       "session": "warm-up and timed steps are separate 1F1B sessions (fill + drain included)"},
+            "roofline": {"kernel": "k_update.cu update_predict_kernel (K-B)", "bound": "hbm",
+                         "achieved": achieved, "peak": peak, "unit": "GB/s",
+                         "frac": (achieved / peak) if achieved else None,
+                         "traffic": recorded_traffic(wname, "update_predict_kernel"),
+                         "peak_source": peak_src, "launches": int(kb_n),
+                         "avg_launch_ms": kb_ms / kb_n if kb_n else None,
+                         "share_of_stage_time": kb_ms / stage_ms if stage_ms else None,
+                         "algorithmic_bytes_per_launch": kb_bytes / kb_n if kb_n else None},
+            "kernel_ms_total": gemm_prof,
+            "cpu_baseline": cpu,
+            "e2e": e2e,
+            "gpu_launches": launches,
+            "clocks": sampler.summary(),
+        }
+        print(json.dumps(line), flush=True)
+    for s in my_stages:
+        s.close()
+    if N > 1:
+        dist.destroy_process_group()
+
+
+def main():
+    args = parse()
+    if args.impl == "reference":
+        run_reference(args)
+    else:
+        run_ours(args)
+
+
+if __name__ == "__main__":
+    main()

@@ -240,6 +240,14 @@ ST_API st_status st_step(st_ctx* ctx, const float* x_dev, const int32_t* y_dev, 
  * NULL) — when non-NULL the call synchronises and checks finiteness. */
 ST_API st_status st_run(st_ctx* ctx, int64_t M, const float* xs_dev, const int32_t* ys_dev, float* losses_host);
 
+/* st_run with HOST buffers (the end-to-end entry point): xs_host [M × B × n_in]
+ * (stage 0) and ys_host [M × B] (last stage) are copied to the device per
+ * mini-batch right before its forward (stream-ordered; pinned memory makes the
+ * copies asynchronous), and each mini-batch's loss is copied back to
+ * losses_host[mb] (last stage) as soon as it is computed. Synchronises at the end. */
+ST_API st_status st_run_host(st_ctx* ctx, int64_t M, const float* xs_host, const int32_t* ys_host,
+                             float* losses_host);
+
 /* LOCAL transport: runs st_run on every context of a connected group, one host
  * thread per stage; returns the first failure. */
 ST_API st_status st_run_group(st_ctx** ctxs, int32_t n, int64_t M, const float* xs_dev, const int32_t* ys_dev,

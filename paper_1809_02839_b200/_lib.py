@@ -102,6 +102,7 @@ def _load() -> ctypes.CDLL:
         "st_predict_and_update": (S, [P]),
         "st_step": (S, [P, P, P, ctypes.POINTER(StStepInfo)]),
         "st_run": (S, [P, I64, P, P, P]),
+        "st_run_host": (S, [P, I64, P, P, P]),
         "st_run_group": (S, [ctypes.POINTER(P), ctypes.c_int32, I64, P, P, P]),
         "st_get_trace": (S, [P, ctypes.POINTER(StEvent), U, ctypes.POINTER(U)]),
         "st_losses_device": (P, [P]),
@@ -126,7 +127,7 @@ def _load() -> ctypes.CDLL:
 lib = _load()
 EXPORTED = ("st_version_difference", "st_program", "st_comm_plan", "st_query_sizes", "st_get_nccl_id", "st_init",
             "st_connect_local", "st_destroy", "st_set_params", "st_get_params", "st_stage_forward",
-            "st_stage_backward", "st_predict_and_update", "st_step", "st_run", "st_run_group", "st_get_trace",
+            "st_stage_backward", "st_predict_and_update", "st_step", "st_run", "st_run_host", "st_run_group", "st_get_trace",
             "st_losses_device", "st_sync", "st_set_profiling", "st_get_profile", "st_kernel_launches",
             "st_update_predict_raw", "st_gemm_raw", "st_gemm_workspace_bytes", "st_softmax_ce_raw",
             "st_last_error", "st_version")

@@ -36,7 +36,7 @@ st_status ctx_forward(st_ctx* c, int64_t mb, const float* x_dev, const int32_t* 
 st_status ctx_backward(st_ctx* c, int64_t mb);
 st_status ctx_predict_and_update(st_ctx* c);
 st_status ctx_step(st_ctx* c, const float* x_dev, const int32_t* y_dev, st_step_info* info);
-st_status ctx_run(st_ctx* c, int64_t M, const float* xs, const int32_t* ys, float* losses_host);
+st_status ctx_run(st_ctx* c, int64_t M, const float* xs, const int32_t* ys, float* losses_host, bool host_io);
 st_status ctx_run_group(st_ctx** ctxs, int n, int64_t M, const float* xs, const int32_t* ys, float* losses_host);
 st_status ctx_get_trace(st_ctx* c, st_event* out, size_t cap, size_t* n);
 st_status ctx_set_profiling(st_ctx* c, int on);
@@ -155,7 +155,12 @@ st_status st_step(st_ctx* ctx, const float* x_dev, const int32_t* y_dev, st_step
 
 st_status st_run(st_ctx* ctx, int64_t M, const float* xs_dev, const int32_t* ys_dev, float* losses_host) {
   NEED_CTX(ctx);
-  GUARD({ return ctx_run(ctx, M, xs_dev, ys_dev, losses_host); })
+  GUARD({ return ctx_run(ctx, M, xs_dev, ys_dev, losses_host, false); })
+}
+
+st_status st_run_host(st_ctx* ctx, int64_t M, const float* xs_host, const int32_t* ys_host, float* losses_host) {
+  NEED_CTX(ctx);
+  GUARD({ return ctx_run(ctx, M, xs_host, ys_host, losses_host, true); })
 }
 
 st_status st_run_group(st_ctx** ctxs, int32_t n, int64_t M, const float* xs_dev, const int32_t* ys_dev,

@@ -34,7 +34,7 @@ struct Layout {
   // work offsets (bytes)
   int64_t off_send_fwd = -1, off_recv_bwd = -1, off_send_bwd = -1, off_logits = -1, off_dlogits = -1;
   int64_t off_bufA = -1, off_bufB = -1, off_losses = -1, off_rowloss = -1, off_ring_fwd = -1, off_ring_bwd = -1;
-  int64_t off_ws = -1;
+  int64_t off_ws = -1, off_ystage = -1;
   size_t ring_fwd_elems = 0, ring_bwd_elems = 0;
   st_sizes sizes{};
 };
@@ -120,6 +120,7 @@ st_status validate_and_layout(const st_config* c, Layout* L) {
     L->off_logits = take(B * L->out_last);
     L->off_dlogits = take(B * L->out_last);
     L->off_rowloss = take(B);
+    L->off_ystage = take(B);
   }
   L->off_bufA = take(B * width);
   L->off_bufB = take(B * width);
@@ -254,6 +255,7 @@ st_status ctx_init(const st_config* cfg, const st_buffers* bufs, void* stream, s
   c->logits = at(L.off_logits);
   c->dlogits = at(L.off_dlogits);
   c->rowloss = at(L.off_rowloss);
+  c->y_stage = reinterpret_cast<int32_t*>(at(L.off_ystage));
   c->bufA = at(L.off_bufA);
   c->bufB = at(L.off_bufB);
   c->losses_dev = at(L.off_losses);
@@ -415,13 +417,18 @@ static GemmArgs gargs(st_ctx* c, const LayerInfo& L) {
   return g;
 }
 
-static st_status forward_compute(st_ctx* c, int64_t mb, const float* x_dev, const int32_t* y_dev) {
+static st_status forward_compute(st_ctx* c, int64_t mb, const float* x_dev, const int32_t* y_dev, bool host_io,
+                                 float* loss_host) {
   float* slot = c->stash + (size_t)(mb % c->S) * c->slot_elems;
   const float* Wh = c->WF;  // Eq. 4 with s_F (aliases W when s_F = 0)
   if (c->first_stage) {
-    if (!x_dev) return set_error(ST_ERR_INPUT, "stage 0 forward needs x_dev");
+    if (!x_dev) return set_error(ST_ERR_INPUT, "stage 0 forward needs x");
     ST_CUDA_TRY(cudaMemcpyAsync(slot + c->layers[0].stash_off, x_dev, (size_t)c->B * c->in_first * 4,
-                                cudaMemcpyDeviceToDevice, c->stream));
+                                host_io ? cudaMemcpyHostToDevice : cudaMemcpyDeviceToDevice, c->stream));
+  }
+  if (c->last_stage && host_io && y_dev) {
+    ST_CUDA_TRY(cudaMemcpyAsync(c->y_stage, y_dev, (size_t)c->B * 4, cudaMemcpyHostToDevice, c->stream));
+    y_dev = c->y_stage;
   }
   const size_t nl = c->layers.size();
   for (size_t l = 0; l < nl; ++l) {
@@ -438,6 +445,8 @@ static st_status forward_compute(st_ctx* c, int64_t mb, const float* x_dev, cons
     ST_TRY(launch_softmax_ce(c->logits, y_dev, c->B, c->out_last, c->rowloss, c->losses_dev + (mb % c->max_mb),
                              c->dlogits, c->stream));
     c->launches += 2;
+    if (loss_host)
+      ST_CUDA_TRY(cudaMemcpyAsync(loss_host, c->losses_dev + (mb % c->max_mb), 4, cudaMemcpyDeviceToHost, c->stream));
   }
   return ST_OK;
 }
@@ -475,7 +484,8 @@ static st_status backward_compute(st_ctx* c, int64_t mb) {
   return ST_OK;
 }
 
-static st_status run_task(st_ctx* c, const float* x_dev, const int32_t* y_dev) {
+static st_status run_task(st_ctx* c, const float* x_dev, const int32_t* y_dev, bool host_io = false,
+                          float* loss_host = nullptr) {
   if (c->pc >= c->program.size()) return set_error(ST_ERR_STATE, "stage %d: program finished", c->k);
   if (c->pending_update)
     return set_error(ST_ERR_STATE, "stage %d: predict_and_update must follow every backward", c->k);
@@ -491,7 +501,7 @@ static st_status run_task(st_ctx* c, const float* x_dev, const int32_t* y_dev) {
   e.target = e.base_version + e.s;
   c->trace.push_back(e);
   if (t.dir == ST_FWD)
-    ST_TRY(forward_compute(c, t.mb, x_dev, y_dev));
+    ST_TRY(forward_compute(c, t.mb, x_dev, y_dev, host_io, loss_host));
   else {
     ST_TRY(backward_compute(c, t.mb));
     c->pending_update = true;
@@ -587,7 +597,7 @@ st_status ctx_step(st_ctx* c, const float* x_dev, const int32_t* y_dev, st_step_
   return ST_OK;
 }
 
-st_status ctx_run(st_ctx* c, int64_t M, const float* xs, const int32_t* ys, float* losses_host) {
+st_status ctx_run(st_ctx* c, int64_t M, const float* xs, const int32_t* ys, float* losses_host, bool host_io) {
   ST_CUDA_TRY(cudaSetDevice(c->device));
   if (M < 0 || M > c->max_mb)
     return set_error(ST_ERR_INPUT, "run: M = %lld outside [0, max_minibatches = %lld]", (long long)M,
@@ -601,11 +611,13 @@ st_status ctx_run(st_ctx* c, int64_t M, const float* xs, const int32_t* ys, floa
   begin_session(c, M);
   while (c->pc < c->program.size()) {
     const Task t = c->program[c->pc];
-    ST_TRY(run_task(c, x_of(c, xs, t.mb), y_of(c, ys, t.mb)));
+    float* lh = (host_io && losses_host && c->last_stage && t.dir == ST_FWD) ? losses_host + t.mb : nullptr;
+    ST_TRY(run_task(c, x_of(c, xs, t.mb), y_of(c, ys, t.mb), host_io, lh));
     if (t.dir == ST_BWD) ST_TRY(ctx_update(c));
   }
   if (losses_host && c->last_stage && M > 0) {
-    ST_CUDA_TRY(cudaMemcpyAsync(losses_host, c->losses_dev, (size_t)M * 4, cudaMemcpyDeviceToHost, c->stream));
+    if (!host_io)
+      ST_CUDA_TRY(cudaMemcpyAsync(losses_host, c->losses_dev, (size_t)M * 4, cudaMemcpyDeviceToHost, c->stream));
     ST_CUDA_TRY(cudaStreamSynchronize(c->stream));
     for (int64_t i = 0; i < M; ++i)
       if (!std::isfinite(losses_host[i]))
@@ -624,7 +636,7 @@ st_status ctx_run_group(st_ctx** ctxs, int n, int64_t M, const float* xs, const 
       st_ctx* c = ctxs[k];
       cudaSetDevice(c->device);
       res[k] = ctx_run(c, M, c->first_stage ? xs : nullptr, c->last_stage ? ys : nullptr,
-                       c->last_stage ? losses_host : nullptr);
+                       c->last_stage ? losses_host : nullptr, false);
       if (res[k] != ST_OK) msg[k] = st_last_error();
     });
   }

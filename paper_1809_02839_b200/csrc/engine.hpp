@@ -100,6 +100,7 @@ struct st_ctx {
   float* bufB = nullptr;
   float* losses_dev = nullptr;  // [max_mb]
   float* rowloss = nullptr;     // [B]
+  int32_t* y_stage = nullptr;   // [B] labels staged from host (st_run_host)
   float* ring_fwd = nullptr;    // LOCAL transport rings
   float* ring_bwd = nullptr;
   size_t ring_fwd_elems = 0, ring_bwd_elems = 0;

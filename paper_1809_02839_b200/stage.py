@@ -118,6 +118,12 @@ class Stage:
         check(lib.st_run(self.ctx, M, _ptr(xs), _ptr(ys), out.ctypes.data if out is not None else None))
         return out[:M] if out is not None else None
 
+    def run_host(self, M: int, xs_host, ys_host, losses_host: Optional[np.ndarray] = None) -> None:
+        """End-to-end run from host buffers (numpy arrays or pinned CPU torch tensors)."""
+        def p(a):
+            return None if a is None else (a.data_ptr() if isinstance(a, torch.Tensor) else a.ctypes.data)
+        check(lib.st_run_host(self.ctx, M, p(xs_host), p(ys_host), p(losses_host)))
+
     def trace(self) -> List[Tuple[int, int, int, int, int, int, int]]:
         n = ctypes.c_size_t()
         check(lib.st_get_trace(self.ctx, None, 0, ctypes.byref(n)))
