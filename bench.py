@@ -35,7 +35,7 @@ sys.path.insert(0, ROOT)
 
 METRIC = "training samples/sec at 1/2/4/8-stage pipeline; update-kernel HBM GB/s vs peak"
 UNIT = "samples/s"
-DEFAULT_GEMM = "simt"
+DEFAULT_GEMM = "fp32x3"
 
 
 def parse():

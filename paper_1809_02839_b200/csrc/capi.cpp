@@ -225,6 +225,9 @@ st_status st_gemm_raw(int op, int gemm_mode, int B, int n_in, int n_out, const f
     g.work = work;
     g.stream = static_cast<cudaStream_t>(stream);
     if (!a || !b || !out) return set_error(ST_ERR_INPUT, "gemm_raw: NULL operand");
+    if (!work) return set_error(ST_ERR_INPUT, "gemm_raw: NULL workspace");
+    // split-K tile counters live at the head of the workspace and must start at zero
+    ST_CUDA_TRY(cudaMemsetAsync(work, 0, 64 * 1024, g.stream));
     switch (op) {
       case 0: return gemm_fwd(g, a, b, aux, out, relu);
       case 1: return gemm_dx(g, a, b, aux, out);

@@ -273,6 +273,9 @@ st_status ctx_init(const st_config* cfg, const st_buffers* bufs, void* stream, s
   }
   ST_CUDA_TRY(cudaMemsetAsync(c->V, 0, (size_t)c->P * 4, c->stream));
   ST_CUDA_TRY(cudaMemsetAsync(c->losses_dev, 0xff, (size_t)c->max_mb * 4, c->stream));  // NaN
+  // GEMM workspace: split-K tile counters must start at zero (they self-reset afterwards)
+  ST_CUDA_TRY(cudaMemsetAsync(c->gemm_ws, 0, (size_t)gemm_workspace_bytes(c->B, c->max_width_in, c->max_width_out),
+                              c->stream));
   begin_session(c.get(), c->max_mb);
   *out = c.release();
   return ST_OK;

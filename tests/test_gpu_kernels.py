@@ -8,7 +8,8 @@ from oracle import spectrain_oracle as O
 
 pytestmark = pytest.mark.gpu
 
-GEMM_MODES = ["simt"]
+GEMM_MODES = ["simt", "fp32x3", "tf32"]
+TOL = {"simt": 1e-5, "fp32x3": 1e-5, "tf32": 3e-3}
 
 
 @pytest.fixture(scope="module")
@@ -93,12 +94,13 @@ def test_update_predict_s0_untouched_outputs(st):
     torch.testing.assert_close(W, w0 - 0.1 * V, rtol=1e-6, atol=1e-7)
 
 
-MODES = {"simt": 2, "fp32x3": 0}
+MODES = {"simt": 2, "fp32x3": 0, "tf32": 1}
 
 
 @pytest.mark.parametrize("mode", GEMM_MODES)
 @pytest.mark.parametrize("B,n_in,n_out", [(32, 784, 256), (128, 300, 70), (5, 33, 17), (128, 1024, 1024),
-                                          (96, 160, 200)])
+                                          (96, 160, 200), (128, 4096, 512), (7, 264, 136), (128, 784, 384),
+                                          (16, 128, 4096)])
 def test_stage_gemms_vs_fp64(st, mode, B, n_in, n_out):
     rng = np.random.default_rng(B * 7 + n_in)
     dev = torch.device("cuda", 0)
@@ -109,6 +111,7 @@ def test_stage_gemms_vs_fp64(st, mode, B, n_in, n_out):
     mask = np.maximum(rng.standard_normal((B, n_in)), 0).astype(np.float32)
     t = lambda a: torch.from_numpy(a).to(dev)
     m = MODES[mode]
+    tol = TOL[mode]
     X64, W64, dZ64 = X.astype(np.float64), W.astype(np.float64), dZ.astype(np.float64)
     # fwd + bias + ReLU
     Z = torch.empty(B, n_out, device=dev)
@@ -116,14 +119,14 @@ def test_stage_gemms_vs_fp64(st, mode, B, n_in, n_out):
     ref = np.maximum(X64 @ W64 + b, 0)
     scale = np.abs(X64) @ np.abs(W64) + np.abs(b)
     torch.cuda.synchronize()
-    assert np.all(np.abs(Z.cpu().numpy() - ref) <= 1e-5 * scale + 1e-30)
+    assert np.all(np.abs(Z.cpu().numpy() - ref) <= tol * scale + 1e-30)
     # dX with ReLU mask
     D = torch.empty(B, n_in, device=dev)
     st.gemm_raw(1, m, B, n_in, n_out, t(dZ), t(W), t(mask), None, D)
     ref = (dZ64 @ W64.T) * (mask > 0)
     scale = np.abs(dZ64) @ np.abs(W64.T)
     torch.cuda.synchronize()
-    assert np.all(np.abs(D.cpu().numpy() - ref) <= 1e-5 * scale + 1e-30)
+    assert np.all(np.abs(D.cpu().numpy() - ref) <= tol * scale + 1e-30)
     # dW + bias grad
     G = torch.empty(n_in, n_out, device=dev)
     gb = torch.empty(n_out, device=dev)
@@ -131,7 +134,7 @@ def test_stage_gemms_vs_fp64(st, mode, B, n_in, n_out):
     ref = X64.T @ dZ64
     scale = np.abs(X64.T) @ np.abs(dZ64)
     torch.cuda.synchronize()
-    assert np.all(np.abs(G.cpu().numpy() - ref) <= 1e-5 * scale + 1e-30)
+    assert np.all(np.abs(G.cpu().numpy() - ref) <= tol * scale + 1e-30)
     np.testing.assert_allclose(gb.cpu().numpy(), dZ64.sum(0), rtol=1e-5, atol=1e-5)
 
 

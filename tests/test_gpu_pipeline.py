@@ -14,7 +14,7 @@ from tests.gpu_helpers import assert_parity, build_pipeline, layers_of, oracle_r
 
 pytestmark = pytest.mark.gpu
 
-PARITY_GEMM = "simt"
+PARITY_GEMM = "fp32x3"
 
 
 @pytest.fixture(scope="module")
@@ -50,6 +50,16 @@ def _parity(st, model, batch, M, lr, seed=0, pred=O.PRED_SPECTRAIN, momentum=O.M
 def test_mlp_2stage_config0(st):
     """BJ configs[0]: MLP 784-256-256-10, 2 stages, batch 32, 20 steps."""
     _parity(st, sd.config_mlp_2stage(), 32, 20, 0.05)
+
+
+def test_mlp_2stage_config0_simt_mode(st):
+    """The CUDA-core diagnostic GEMM mode reaches the same parity."""
+    global PARITY_GEMM
+    old, PARITY_GEMM = PARITY_GEMM, "simt"
+    try:
+        _parity(st, sd.config_mlp_2stage(), 32, 20, 0.05)
+    finally:
+        PARITY_GEMM = old
 
 
 def test_deep_mlp_8stage(st):
