@@ -223,6 +223,7 @@ st_status st_gemm_raw(int op, int gemm_mode, int B, int n_in, int n_out, const f
     g.n_in = n_in;
     g.n_out = n_out;
     g.work = work;
+    g.work_bytes = gemm_workspace_bytes(B, n_in, n_out);
     g.stream = static_cast<cudaStream_t>(stream);
     if (!a || !b || !out) return set_error(ST_ERR_INPUT, "gemm_raw: NULL operand");
     if (!work) return set_error(ST_ERR_INPUT, "gemm_raw: NULL workspace");

@@ -416,6 +416,7 @@ static GemmArgs gargs(st_ctx* c, const LayerInfo& L) {
   g.n_in = L.n_in;
   g.n_out = L.n_out;
   g.work = c->gemm_ws;
+  g.work_bytes = gemm_workspace_bytes(c->B, c->max_width_in, c->max_width_out);
   g.stream = c->stream;
   return g;
 }

@@ -14,6 +14,7 @@ st_status tc_dx(const GemmArgs& g, const float* dZ, const float* W, const float*
 st_status tc_dw(const GemmArgs& g, const float* X, const float* dZ, float* G, float* gb);
 int64_t tc_workspace_bytes(int B, int max_in, int max_out);
 int tc_last_launches();
+int simt_last_launches();
 
 static thread_local int g_last_launches = 0;
 int gemm_last_launches() { return g_last_launches; }
@@ -31,8 +32,9 @@ static st_status check(const GemmArgs& g) {
 st_status gemm_fwd(const GemmArgs& g, const float* X, const float* W, const float* bias, float* Z, int relu) {
   ST_TRY(check(g));
   if (g.mode == ST_GEMM_SIMT) {
-    g_last_launches = 1;
-    return simt_fwd(g, X, W, bias, Z, relu);
+    st_status s = simt_fwd(g, X, W, bias, Z, relu);
+    g_last_launches = simt_last_launches();
+    return s;
   }
   st_status s = tc_fwd(g, X, W, bias, Z, relu);
   g_last_launches = tc_last_launches();
@@ -42,8 +44,9 @@ st_status gemm_fwd(const GemmArgs& g, const float* X, const float* W, const floa
 st_status gemm_dx(const GemmArgs& g, const float* dZ, const float* W, const float* mask, float* D) {
   ST_TRY(check(g));
   if (g.mode == ST_GEMM_SIMT) {
-    g_last_launches = 1;
-    return simt_dx(g, dZ, W, mask, D);
+    st_status s = simt_dx(g, dZ, W, mask, D);
+    g_last_launches = simt_last_launches();
+    return s;
   }
   st_status s = tc_dx(g, dZ, W, mask, D);
   g_last_launches = tc_last_launches();
@@ -53,8 +56,9 @@ st_status gemm_dx(const GemmArgs& g, const float* dZ, const float* W, const floa
 st_status gemm_dw(const GemmArgs& g, const float* X, const float* dZ, float* G, float* gb) {
   ST_TRY(check(g));
   if (g.mode == ST_GEMM_SIMT) {
-    g_last_launches = gb ? 2 : 1;
-    return simt_dw(g, X, dZ, G, gb);
+    st_status s = simt_dw(g, X, dZ, G, gb);
+    g_last_launches = simt_last_launches();
+    return s;
   }
   st_status s = tc_dw(g, X, dZ, G, gb);
   g_last_launches = tc_last_launches();

@@ -12,7 +12,7 @@
 namespace st {
 namespace {
 
-enum { EPI_PLAIN = 0, EPI_BIAS = 1, EPI_MASK = 2 };
+enum { EPI_PLAIN = 0, EPI_BIAS = 1, EPI_MASK = 2, EPI_PARTIAL = 3 };
 
 constexpr int TM = 64, TN = 64, TK = 16;
 
@@ -20,14 +20,18 @@ template <int EPI>
 __global__ void __launch_bounds__(256) sgemm_kernel(int M, int N, int K, const float* __restrict__ A, int64_t a_sm,
                                                     int64_t a_sk, const float* __restrict__ Bm, int64_t b_sk,
                                                     int64_t b_sn, float* __restrict__ C, int64_t c_sm, int64_t c_sn,
-                                                    const float* __restrict__ aux, int relu) {
+                                                    const float* __restrict__ aux, int relu, int k_chunk) {
   __shared__ float As[TK][TM + 4];
   __shared__ float Bs[TK][TN + 4];
   const int tid = threadIdx.x;
   const int tx = tid % 16, ty = tid / 16;  // 16×16 threads, 4×4 outputs each
   const int m0 = blockIdx.y * TM, n0 = blockIdx.x * TN;
   float acc[4][4] = {};
-  for (int k0 = 0; k0 < K; k0 += TK) {
+  // split-K: blockIdx.z owns [kb, ke); partials go to C + z·M·N (EPI_PARTIAL)
+  const int kb = blockIdx.z * k_chunk;
+  const int ke = min(K, kb + k_chunk);
+  if (EPI == EPI_PARTIAL) C += (size_t)blockIdx.z * M * N;
+  for (int k0 = kb; k0 < ke; k0 += TK) {
     // A tile TM×TK: 1024 elements, 4 per thread. Map the contiguous dimension to tid.
 #pragma unroll
     for (int r = 0; r < 4; ++r) {
@@ -35,7 +39,7 @@ __global__ void __launch_bounds__(256) sgemm_kernel(int M, int N, int K, const f
       int mm, kk;
       if (a_sk == 1) { kk = e % TK; mm = e / TK; } else { mm = e % TM; kk = e / TM; }
       const int gm = m0 + mm, gk = k0 + kk;
-      As[kk][mm] = (gm < M && gk < K) ? A[gm * a_sm + gk * a_sk] : 0.f;
+      As[kk][mm] = (gm < M && gk < ke) ? A[gm * a_sm + gk * a_sk] : 0.f;
     }
 #pragma unroll
     for (int r = 0; r < 4; ++r) {
@@ -43,7 +47,7 @@ __global__ void __launch_bounds__(256) sgemm_kernel(int M, int N, int K, const f
       int nn, kk;
       if (b_sn == 1) { nn = e % TN; kk = e / TN; } else { kk = e % TK; nn = e / TK; }
       const int gn = n0 + nn, gk = k0 + kk;
-      Bs[kk][nn] = (gn < N && gk < K) ? Bm[gk * b_sk + gn * b_sn] : 0.f;
+      Bs[kk][nn] = (gn < N && gk < ke) ? Bm[gk * b_sk + gn * b_sn] : 0.f;
     }
     __syncthreads();
 #pragma unroll
@@ -75,25 +79,91 @@ __global__ void __launch_bounds__(256) sgemm_kernel(int M, int N, int K, const f
       } else if (EPI == EPI_MASK) {
         if (aux && !(aux[gm * c_sm + gn * c_sn] > 0.f)) v = 0.f;
       }
-      C[gm * c_sm + gn * c_sn] = v;
+      if (EPI == EPI_PARTIAL)
+        C[(size_t)gm * N + gn] = v;
+      else
+        C[gm * c_sm + gn * c_sn] = v;
     }
   }
 }
 
-__global__ void bias_grad_kernel(const float* __restrict__ dZ, int B, int n_out, float* __restrict__ gb) {
-  const int o = blockIdx.x * blockDim.x + threadIdx.x;
-  if (o >= n_out) return;
-  float s = 0.f;
-  for (int b = 0; b < B; ++b) s += dZ[(size_t)b * n_out + o];
-  gb[o] = s;
+// Fixed-order reduction of split-K partials + the real epilogue.
+__global__ void splitk_reduce_kernel(const float* __restrict__ ws, int splits, int M, int N, float* __restrict__ C,
+                                     int64_t c_sm, int64_t c_sn, int epi, const float* __restrict__ aux, int relu) {
+  const int idx = blockIdx.x * blockDim.x + threadIdx.x;
+  if (idx >= M * N) return;
+  const int m = idx / N, n = idx % N;
+  float v = 0.f;
+  for (int z = 0; z < splits; ++z) v += ws[(size_t)z * M * N + idx];
+  if (epi == EPI_BIAS) {
+    if (aux) v += aux[n];
+    if (relu) v = fmaxf(v, 0.f);
+  } else if (epi == EPI_MASK) {
+    if (aux && !(aux[m * c_sm + n * c_sn] > 0.f)) v = 0.f;
+  }
+  C[m * c_sm + n * c_sn] = v;
 }
 
+// g_b[o] = Σ_b dZ[b][o]: 32 columns per CTA × 8 row groups, fixed-order combine.
+__global__ void __launch_bounds__(256) bias_grad_kernel(const float* __restrict__ dZ, int B, int n_out,
+                                                        float* __restrict__ gb) {
+  __shared__ float part[8][33];
+  const int tx = threadIdx.x & 31, ty = threadIdx.x >> 5;
+  const int o = blockIdx.x * 32 + tx;
+  float s = 0.f;
+  if (o < n_out)
+    for (int b = ty; b < B; b += 8) s += dZ[(size_t)b * n_out + o];
+  part[ty][tx] = s;
+  __syncthreads();
+  if (ty == 0 && o < n_out) {
+    float t = part[0][tx];
+#pragma unroll
+    for (int r = 1; r < 8; ++r) t += part[r][tx];
+    gb[o] = t;
+  }
+}
+
+}  // namespace
+
+st_status launch_bias_grad(const float* dZ, int B, int n_out, float* gb, cudaStream_t s) {
+  bias_grad_kernel<<<(n_out + 31) / 32, 256, 0, s>>>(dZ, B, n_out, gb);
+  ST_CUDA_TRY(cudaGetLastError());
+  return ST_OK;
+}
+
+namespace {
+
+thread_local int g_simt_launches = 0;
+
+// Tiles that cannot fill the GPU (e.g. the 10-wide output layer: 2 tiles, K = 8192)
+// are split along K into ≤ #SM/tiles chunks; partials (workspace, after the 64 KB
+// counter block) are reduced in fixed order by a second kernel — deterministic.
 template <int EPI>
 st_status run(int M, int N, int K, const float* A, int64_t a_sm, int64_t a_sk, const float* Bm, int64_t b_sk,
-              int64_t b_sn, float* C, int64_t c_sm, int64_t c_sn, const float* aux, int relu, cudaStream_t s) {
-  dim3 grid((N + TN - 1) / TN, (M + TM - 1) / TM);
-  sgemm_kernel<EPI><<<grid, 256, 0, s>>>(M, N, K, A, a_sm, a_sk, Bm, b_sk, b_sn, C, c_sm, c_sn, aux, relu);
+              int64_t b_sn, float* C, int64_t c_sm, int64_t c_sn, const float* aux, int relu, cudaStream_t s,
+              void* work, int64_t work_bytes) {
+  const int tiles = ((N + TN - 1) / TN) * ((M + TM - 1) / TM);
+  int splits = 1;
+  if (work && tiles < 74 && K >= 8 * TK) splits = std::min(148 / tiles, K / (4 * TK));
+  const int64_t need = (int64_t)splits * M * N * 4;
+  while (splits > 1 && need > work_bytes - 64 * 1024) --splits;
+  dim3 grid((N + TN - 1) / TN, (M + TM - 1) / TM, std::max(1, splits));
+  if (splits <= 1) {
+    sgemm_kernel<EPI><<<grid, 256, 0, s>>>(M, N, K, A, a_sm, a_sk, Bm, b_sk, b_sn, C, c_sm, c_sn, aux, relu, K);
+    ST_CUDA_TRY(cudaGetLastError());
+    g_simt_launches = 1;
+    return ST_OK;
+  }
+  const int chunk = ((K + splits - 1) / splits + TK - 1) / TK * TK;
+  splits = (K + chunk - 1) / chunk;
+  grid.z = splits;
+  float* ws = reinterpret_cast<float*>(static_cast<char*>(work) + 64 * 1024);
+  sgemm_kernel<EPI_PARTIAL><<<grid, 256, 0, s>>>(M, N, K, A, a_sm, a_sk, Bm, b_sk, b_sn, ws, c_sm, c_sn, nullptr, 0,
+                                                 chunk);
   ST_CUDA_TRY(cudaGetLastError());
+  splitk_reduce_kernel<<<(M * N + 255) / 256, 256, 0, s>>>(ws, splits, M, N, C, c_sm, c_sn, EPI, aux, relu);
+  ST_CUDA_TRY(cudaGetLastError());
+  g_simt_launches = 2;
   return ST_OK;
 }
 
@@ -101,28 +171,28 @@ st_status run(int M, int N, int K, const float* A, int64_t a_sm, int64_t a_sk, c
 
 // forward: Z[b][o] = Σ_i X[b][i]·W[i][o] + bias[o]
 st_status simt_fwd(const GemmArgs& g, const float* X, const float* W, const float* bias, float* Z, int relu) {
-  return run<EPI_BIAS>(g.B, g.n_out, g.n_in, X, g.n_in, 1, W, g.n_out, 1, Z, g.n_out, 1, bias, relu, g.stream);
+  return run<EPI_BIAS>(g.B, g.n_out, g.n_in, X, g.n_in, 1, W, g.n_out, 1, Z, g.n_out, 1, bias, relu, g.stream, g.work,
+                       g.work_bytes);
 }
 
 // dX: D[b][i] = Σ_o dZ[b][o]·W[i][o], masked by mask[b][i] > 0
 st_status simt_dx(const GemmArgs& g, const float* dZ, const float* W, const float* mask, float* D) {
-  return run<EPI_MASK>(g.B, g.n_in, g.n_out, dZ, g.n_out, 1, W, 1, g.n_out, D, g.n_in, 1, mask, 0, g.stream);
+  return run<EPI_MASK>(g.B, g.n_in, g.n_out, dZ, g.n_out, 1, W, 1, g.n_out, D, g.n_in, 1, mask, 0, g.stream, g.work,
+                       g.work_bytes);
 }
 
 // dW: G[i][o] = Σ_b X[b][i]·dZ[b][o];  gb[o] = Σ_b dZ[b][o]
 st_status simt_dw(const GemmArgs& g, const float* X, const float* dZ, float* G, float* gb) {
-  ST_TRY(run<EPI_PLAIN>(g.n_in, g.n_out, g.B, X, 1, g.n_in, dZ, g.n_out, 1, G, g.n_out, 1, nullptr, 0, g.stream));
+  ST_TRY(run<EPI_PLAIN>(g.n_in, g.n_out, g.B, X, 1, g.n_in, dZ, g.n_out, 1, G, g.n_out, 1, nullptr, 0, g.stream,
+                        g.work, g.work_bytes));
   if (gb) {
-    bias_grad_kernel<<<(g.n_out + 255) / 256, 256, 0, g.stream>>>(dZ, g.B, g.n_out, gb);
-    ST_CUDA_TRY(cudaGetLastError());
+    const int l = g_simt_launches;
+    ST_TRY(launch_bias_grad(dZ, g.B, g.n_out, gb, g.stream));
+    g_simt_launches = l + 1;
   }
   return ST_OK;
 }
 
-st_status launch_bias_grad(const float* dZ, int B, int n_out, float* gb, cudaStream_t s) {
-  bias_grad_kernel<<<(n_out + 255) / 256, 256, 0, s>>>(dZ, B, n_out, gb);
-  ST_CUDA_TRY(cudaGetLastError());
-  return ST_OK;
-}
+int simt_last_launches() { return g_simt_launches; }
 
 }  // namespace st

@@ -7,13 +7,15 @@
 //   dW  : M = out, N = in, K = B  ;  A(o,b) = dZ[b·out+o] (MN-major), B(i,b) = X[b·in+i]  (MN-major)
 // and the output element (m, n) always lives at out[n·M + m].
 //
-// Pipeline per CTA (one 128 × bn output tile, one K range), 6 warps:
-//   warp 0      TMA producer: raw fp32 tiles (128B-swizzled boxes) → raw ring
-//   warps 2..5  converter: raw tile → K-major SW128 "hi" (and "lo" for FP32X3) tiles
-//               (hi = cvt.rna.tf32(x), lo = x − hi; the 3xTF32 split),
-//               transposing MN-major operands on the way → conv ring
-//   warp 1      MMA issuer: tcgen05.mma.cta_group::1.kind::tf32, fp32 accumulator in
-//               TMEM (128 lanes × bn columns); FP32X3 issues hi·hi + lo·hi + hi·lo
+// Pipeline per CTA (one 128 × bn output tile, one K range), 6 warps, STAGES-deep ring:
+//   warp 0      TMA producer: raw fp32 tiles → stage (K-major operands SWIZZLE_128B,
+//               MN-major operands SWIZZLE_128B_ATOM_32B — the tf32 MN-major UMMA layout)
+//   warps 2..5  converter (FP32X3 only): lo = x − trunc_tf32(x) in the same layout.
+//               The tensor core truncates fp32 inputs to tf32 (tools/probe_tcgen05.cu),
+//               so the raw tile itself is the "hi" operand: no rewrite, no transpose.
+//   warp 1      MMA issuer: tcgen05.mma.cta_group::1.kind::tf32 (A, B from smem),
+//               fp32 accumulator in TMEM (128 lanes × bn columns);
+//               FP32X3 issues hi·hi + lo·hi + hi·lo
 //   warps 2..5  epilogue: tcgen05.ld → fused bias/ReLU (fwd), ReLU mask (dX) → global;
 //               split-K partials are reduced in fixed split order by the last CTA.
 #include <cuda.h>
@@ -32,13 +34,10 @@ namespace {
 constexpr int BM = 128;            // TMEM lanes per tile
 constexpr int BNMAX = 128;         // accumulator columns per tile
 constexpr int BK = 32;             // fp32 elements per 128-byte swizzle row
-constexpr int RS = 3;              // raw (TMA) stages
-constexpr int CS = 2;              // converted stages
 constexpr int kThreads = 192;
-constexpr int TILE_BYTES = BM * BK * 4;  // 16 KB for 128 rows
-constexpr int RAW_STAGE = 2 * TILE_BYTES;
-constexpr int CONV_STAGE = 4 * TILE_BYTES;  // A_hi, A_lo, B_hi, B_lo
-constexpr int SMEM_BYTES = RS * RAW_STAGE + CS * CONV_STAGE + 1024 /*align*/ + 256 /*barriers*/;
+constexpr int TILE_BYTES = BM * BK * 4;   // 16 KB: one 128 × 32 fp32 operand tile
+constexpr int STAGE_BYTES = 4 * TILE_BYTES;  // A raw (= hi), B raw (= hi), A lo, B lo
+constexpr int smem_bytes(int stages) { return stages * STAGE_BYTES + 1024 /*align*/ + 256 /*barriers*/; }
 
 enum { EPI_FWD = 0, EPI_DX = 1, EPI_DW = 2 };
 
@@ -110,90 +109,60 @@ __device__ __forceinline__ void tc_ld16(uint32_t taddr, float* v) {
   for (int i = 0; i < 16; ++i) v[i] = __uint_as_float(r[i]);
 }
 
-// K-major, 128B-swizzled UMMA shared-memory descriptor (rows of 128 B, 8-row atoms of 1024 B).
-__device__ __forceinline__ uint64_t kmajor_desc(uint32_t saddr) {
-  uint64_t d = 0;
-  d |= (uint64_t)((saddr >> 4) & 0x3FFF);
-  d |= (uint64_t)1 << 16;               // LBO (unused for swizzled K-major)
-  d |= (uint64_t)(1024 >> 4) << 32;     // SBO: 8-row group stride
-  d |= (uint64_t)1 << 46;               // descriptor version (sm_100)
-  d |= (uint64_t)2 << 61;               // SWIZZLE_128B
-  return d;
+// UMMA shared-memory descriptors (sm_100 version 1).
+// K-major operand: rows of 128 B (32 fp32 along K), SWIZZLE_128B, 8-row atoms of
+// 1024 B (SBO); a K step of 8 tf32 advances the start address by 32 B.
+__device__ __forceinline__ uint64_t desc_kmajor(uint32_t saddr) {
+  return (uint64_t)((saddr >> 4) & 0x3FFF) | ((uint64_t)1 << 16) | ((uint64_t)(1024 >> 4) << 32) |
+         ((uint64_t)1 << 46) | ((uint64_t)2 << 61);
+}
+// MN-major operand (32-bit elements need SWIZZLE_128B_BASE32B): 32-element MN
+// chunks of 128 B per k row, 32 k rows per chunk (4 KB → LBO), 4-row k groups
+// of 512 B (SBO); a K step of 8 advances the start address by 1024 B.
+__device__ __forceinline__ uint64_t desc_mnmajor(uint32_t saddr) {
+  return (uint64_t)((saddr >> 4) & 0x3FFF) | ((uint64_t)(4096 >> 4) << 16) | ((uint64_t)(512 >> 4) << 32) |
+         ((uint64_t)1 << 46) | ((uint64_t)1 << 61);
+}
+template <bool MN>
+__device__ __forceinline__ uint64_t op_desc(uint32_t base, int kk) {
+  return MN ? desc_mnmajor(base + kk * 1024) : desc_kmajor(base + kk * 32);
 }
 
-__device__ __forceinline__ float tf32_hi(float x) {
-  uint32_t r;
-  asm("cvt.rna.tf32.f32 %0, %1;" : "=r"(r) : "f"(x));
-  return __uint_as_float(r);
-}
+// The tensor core truncates fp32 operands to tf32 (measured: tools/probe_tcgen05.cu),
+// so the raw tile IS the "hi" operand and lo = x − trunc_tf32(x) is exact in fp32.
+__device__ __forceinline__ float lo_part(float x) { return x - __uint_as_float(__float_as_uint(x) & 0xFFFFE000u); }
 
-// 16-byte chunk position inside a K-major SW128 tile: row r, chunk j (0..7)
-__device__ __forceinline__ uint32_t kmaj_off(int r, int j) { return (uint32_t)(r * 128 + ((j ^ (r & 7)) << 4)); }
-
-template <bool kX3>
-__device__ __forceinline__ void split4(float4 v, float4& hi, float4& lo) {
-  hi.x = tf32_hi(v.x);
-  hi.y = tf32_hi(v.y);
-  hi.z = tf32_hi(v.z);
-  hi.w = tf32_hi(v.w);
-  if (kX3) {
-    lo.x = v.x - hi.x;
-    lo.y = v.y - hi.y;
-    lo.z = v.z - hi.z;
-    lo.w = v.w - hi.w;
-  }
-}
-
-// raw K-major tile (TMA SW128 box {32, rows}) → hi/lo K-major tiles: same physical chunk layout.
-template <bool kX3>
-__device__ __forceinline__ void convert_kmajor(const char* raw, char* hi, char* lo, int rows, int tid) {
-  for (int c = tid; c < rows * 8; c += 128) {
-    const float4 v = *reinterpret_cast<const float4*>(raw + c * 16);
-    float4 h, l;
-    split4<kX3>(v, h, l);
-    *reinterpret_cast<float4*>(hi + c * 16) = h;
-    if (kX3) *reinterpret_cast<float4*>(lo + c * 16) = l;
-  }
-}
-
-// raw MN-major tile (rows/32 boxes {32 mn, 32 k}, each 4 KB, SW128) → K-major hi/lo tiles.
-template <bool kX3>
-__device__ __forceinline__ void convert_mnmajor(const char* raw, char* hi, char* lo, int rows, int tid) {
-  for (int r = tid; r < rows; r += 128) {
-    const char* box = raw + (r >> 5) * 4096;
-    const int mm = r & 31;
+// lo = x − hi over `chunks` 16-byte chunks: elementwise, so it is layout-agnostic
+// (raw and lo buffers share the same swizzled arrangement).
+__device__ __forceinline__ void make_lo(const char* raw, char* lo, int chunks, int tid) {
+  int c = tid;
+  for (; c + 3 * 128 < chunks; c += 4 * 128) {
+    float4 v[4];
 #pragma unroll
-    for (int j = 0; j < 8; ++j) {
-      float4 v;
-      float* pv = reinterpret_cast<float*>(&v);
+    for (int u = 0; u < 4; ++u) v[u] = *reinterpret_cast<const float4*>(raw + (c + u * 128) * 16);
 #pragma unroll
-      for (int q = 0; q < 4; ++q) {
-        const int k = 4 * j + q;
-        pv[q] = *reinterpret_cast<const float*>(box + k * 128 + ((((mm >> 2) ^ (k & 7))) << 4) + (mm & 3) * 4);
-      }
-      float4 h, l;
-      split4<kX3>(v, h, l);
-      *reinterpret_cast<float4*>(hi + kmaj_off(r, j)) = h;
-      if (kX3) *reinterpret_cast<float4*>(lo + kmaj_off(r, j)) = l;
+    for (int u = 0; u < 4; ++u) {
+      float4 l = make_float4(lo_part(v[u].x), lo_part(v[u].y), lo_part(v[u].z), lo_part(v[u].w));
+      *reinterpret_cast<float4*>(lo + (c + u * 128) * 16) = l;
     }
   }
+  for (; c < chunks; c += 128) {
+    const float4 v = *reinterpret_cast<const float4*>(raw + c * 16);
+    *reinterpret_cast<float4*>(lo + c * 16) = make_float4(lo_part(v.x), lo_part(v.y), lo_part(v.z), lo_part(v.w));
+  }
 }
 
-template <int EPI, bool A_MN, bool B_MN, bool kX3>
+template <int EPI, bool A_MN, bool B_MN, bool kX3, int STAGES>
 __global__ void __launch_bounds__(kThreads, 1)
     tc_gemm_kernel(const __grid_constant__ CUtensorMap mapA, const __grid_constant__ CUtensorMap mapB, TcParams p) {
   extern __shared__ __align__(1024) uint8_t smem_raw[];
   char* smem = reinterpret_cast<char*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
-  char* raw_base = smem;
-  char* conv_base = smem + RS * RAW_STAGE;
-  uint64_t* bars = reinterpret_cast<uint64_t*>(conv_base + CS * CONV_STAGE);
-  // barrier layout
-  const uint32_t b_raw_full = smem_u32(bars);
-  const uint32_t b_raw_empty = b_raw_full + 8 * RS;
-  const uint32_t b_conv_full = b_raw_empty + 8 * RS;
-  const uint32_t b_conv_empty = b_conv_full + 8 * CS;
-  const uint32_t b_acc_full = b_conv_empty + 8 * CS;
-  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(bars + 2 * RS + 2 * CS + 1);
+  uint64_t* bars = reinterpret_cast<uint64_t*>(smem + STAGES * STAGE_BYTES);
+  const uint32_t b_full = smem_u32(bars);            // TMA landed        (1 arrive + tx)
+  const uint32_t b_conv = b_full + 8 * STAGES;       // lo tiles written  (4 converter warps)
+  const uint32_t b_empty = b_conv + 8 * STAGES;      // MMAs done reading (tcgen05.commit)
+  const uint32_t b_acc_full = b_empty + 8 * STAGES;  // accumulator complete
+  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(bars + 3 * STAGES + 1);
   int* last_flag = reinterpret_cast<int*>(tmem_slot + 1);
 
   const int warp = threadIdx.x >> 5;
@@ -204,15 +173,14 @@ __global__ void __launch_bounds__(kThreads, 1)
   const int kb1 = min(p.kb_total, kb0 + p.kb_per_split);
   const int nkb = kb1 - kb0;
   const int bn = p.bn;
+  const int nbox_b = (bn + 31) / 32;
+  const int b_chunks = B_MN ? nbox_b * 256 : bn * 8;  // 16-byte chunks of the B tile
 
   if (threadIdx.x == 0) {
-    for (int s = 0; s < RS; ++s) {
-      mbar_init(b_raw_full + 8 * s, 1);
-      mbar_init(b_raw_empty + 8 * s, 4);
-    }
-    for (int s = 0; s < CS; ++s) {
-      mbar_init(b_conv_full + 8 * s, 4);
-      mbar_init(b_conv_empty + 8 * s, 1);
+    for (int s = 0; s < STAGES; ++s) {
+      mbar_init(b_full + 8 * s, 1);
+      mbar_init(b_conv + 8 * s, 4);
+      mbar_init(b_empty + 8 * s, 1);
     }
     mbar_init(b_acc_full, 1);
     asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
@@ -234,18 +202,17 @@ __global__ void __launch_bounds__(kThreads, 1)
   if (warp == 0) {
     // ---------------- TMA producer
     if (lane == 0) {
-      const int nbox_b = (bn + 31) / 32;
-      const uint32_t bytes = (uint32_t)(BM * BK * 4 + (B_MN ? nbox_b * 4096 : bn * BK * 4));
+      const uint32_t bytes = (uint32_t)(TILE_BYTES + (B_MN ? nbox_b * 4096 : bn * BK * 4));
       for (int i = 0; i < nkb; ++i) {
-        const int s = i % RS;
-        const uint32_t ph = (i / RS) & 1;
-        mbar_wait(b_raw_empty + 8 * s, ph ^ 1);
-        const uint32_t full = b_raw_full + 8 * s;
+        const int s = i % STAGES;
+        mbar_wait(b_empty + 8 * s, ((i / STAGES) & 1) ^ 1);
+        const uint32_t full = b_full + 8 * s;
         mbar_expect_tx(full, bytes);
         const int k0 = (kb0 + i) * BK;
-        const uint32_t dA = smem_u32(raw_base + s * RAW_STAGE);
+        const uint32_t dA = smem_u32(smem + s * STAGE_BYTES);
         const uint32_t dB = dA + TILE_BYTES;
         if (A_MN) {
+#pragma unroll
           for (int c = 0; c < BM / 32; ++c) tma_load_2d(dA + c * 4096, &mapA, m0 + 32 * c, k0, full);
         } else {
           tma_load_2d(dA, &mapA, k0, m0, full);
@@ -258,53 +225,41 @@ __global__ void __launch_bounds__(kThreads, 1)
       }
     }
   } else if (warp == 1) {
-    // ---------------- MMA issuer
+    // ---------------- MMA issuer (one thread)
     if (lane == 0) {
       for (int i = 0; i < nkb; ++i) {
-        const int s = i % CS;
-        const uint32_t ph = (i / CS) & 1;
-        mbar_wait(b_conv_full + 8 * s, ph);
+        const int s = i % STAGES;
+        const uint32_t ph = (i / STAGES) & 1;
+        mbar_wait((kX3 ? b_conv : b_full) + 8 * s, ph);
         tc_fence_after();
-        const uint32_t base = smem_u32(conv_base + s * CONV_STAGE);
-        const uint32_t a_hi = base, a_lo = base + TILE_BYTES, b_hi = base + 2 * TILE_BYTES,
-                       b_lo = base + 3 * TILE_BYTES;
+        const uint32_t a_hi = smem_u32(smem + s * STAGE_BYTES), b_hi = a_hi + TILE_BYTES;
+        const uint32_t a_lo = a_hi + 2 * TILE_BYTES, b_lo = a_hi + 3 * TILE_BYTES;
 #pragma unroll
         for (int kk = 0; kk < BK / 8; ++kk) {
-          const uint32_t off = kk * 32;  // 8 tf32 = 32 bytes along the swizzled row
           const uint32_t acc = (i > 0 || kk > 0) ? 1u : 0u;
-          tc_mma(tmem, kmajor_desc(a_hi + off), kmajor_desc(b_hi + off), p.idesc, acc);
+          tc_mma(tmem, op_desc<A_MN>(a_hi, kk), op_desc<B_MN>(b_hi, kk), p.idesc, acc);
           if (kX3) {
-            tc_mma(tmem, kmajor_desc(a_lo + off), kmajor_desc(b_hi + off), p.idesc, 1u);
-            tc_mma(tmem, kmajor_desc(a_hi + off), kmajor_desc(b_lo + off), p.idesc, 1u);
+            tc_mma(tmem, op_desc<A_MN>(a_lo, kk), op_desc<B_MN>(b_hi, kk), p.idesc, 1u);
+            tc_mma(tmem, op_desc<A_MN>(a_hi, kk), op_desc<B_MN>(b_lo, kk), p.idesc, 1u);
           }
         }
-        tc_commit(b_conv_empty + 8 * s);
+        tc_commit(b_empty + 8 * s);
       }
       tc_commit(b_acc_full);
     }
   } else {
-    // ---------------- converter (warps 2..5), then epilogue
+    // ---------------- converter (warps 2..5): lo tiles for the 3xTF32 split
     const int ctid = threadIdx.x - 64;  // 0..127
-    for (int i = 0; i < nkb; ++i) {
-      const int rs = i % RS, cs = i % CS;
-      mbar_wait(b_raw_full + 8 * rs, (i / RS) & 1);
-      mbar_wait(b_conv_empty + 8 * cs, ((i / CS) & 1) ^ 1);
-      const char* rA = raw_base + rs * RAW_STAGE;
-      const char* rB = rA + TILE_BYTES;
-      char* cbase = conv_base + cs * CONV_STAGE;
-      if (A_MN)
-        convert_mnmajor<kX3>(rA, cbase, cbase + TILE_BYTES, BM, ctid);
-      else
-        convert_kmajor<kX3>(rA, cbase, cbase + TILE_BYTES, BM, ctid);
-      if (B_MN)
-        convert_mnmajor<kX3>(rB, cbase + 2 * TILE_BYTES, cbase + 3 * TILE_BYTES, bn, ctid);
-      else
-        convert_kmajor<kX3>(rB, cbase + 2 * TILE_BYTES, cbase + 3 * TILE_BYTES, bn, ctid);
-      fence_proxy_async();
-      __syncwarp();
-      if (lane == 0) {
-        mbar_arrive(b_raw_empty + 8 * rs);
-        mbar_arrive(b_conv_full + 8 * cs);
+    if (kX3) {
+      for (int i = 0; i < nkb; ++i) {
+        const int s = i % STAGES;
+        mbar_wait(b_full + 8 * s, (i / STAGES) & 1);
+        char* st = smem + s * STAGE_BYTES;
+        make_lo(st, st + 2 * TILE_BYTES, TILE_BYTES / 16, ctid);
+        make_lo(st + TILE_BYTES, st + 3 * TILE_BYTES, b_chunks, ctid);
+        fence_proxy_async();
+        __syncwarp();
+        if (lane == 0) mbar_arrive(b_conv + 8 * s);
       }
     }
 
@@ -333,6 +288,7 @@ __global__ void __launch_bounds__(kThreads, 1)
       asm volatile("bar.sync 1, 128;" ::: "memory");
       if (*last_flag) {
         __threadfence();
+        const float bias = (EPI == EPI_FWD && p.aux && m < p.M) ? p.aux[m] : 0.f;
         for (int c = 0; c < bn; ++c) {
           const int n = n0 + c;
           float acc = 0.f;
@@ -342,7 +298,7 @@ __global__ void __launch_bounds__(kThreads, 1)
             const size_t o = (size_t)n * p.M + m;
             float v = acc;
             if (EPI == EPI_FWD) {
-              if (p.aux) v += p.aux[m];
+              v += bias;
               if (p.relu) v = fmaxf(v, 0.f);
             } else if (EPI == EPI_DX) {
               if (p.aux && !(p.aux[o] > 0.f)) v = 0.f;
@@ -405,7 +361,9 @@ EncodeFn get_encode() {
 }
 
 // 2D fp32 tensor [outer][inner] with row pitch `pitch` elements; box {32, box_outer}.
-bool make_map(CUtensorMap* m, const float* base, int inner, int outer, int pitch, int box_outer) {
+// K-major operands (inner = K) use SWIZZLE_128B; MN-major ones (inner = M or N) the
+// 32-byte-atom variant the tf32 MN-major UMMA layout requires.
+bool make_map(CUtensorMap* m, const float* base, int inner, int outer, int pitch, int box_outer, bool mn_major) {
   EncodeFn enc = get_encode();
   if (!enc) return false;
   cuuint64_t dims[2] = {(cuuint64_t)inner, (cuuint64_t)outer};
@@ -413,7 +371,9 @@ bool make_map(CUtensorMap* m, const float* base, int inner, int outer, int pitch
   cuuint32_t box[2] = {32, (cuuint32_t)box_outer};
   cuuint32_t es[2] = {1, 1};
   CUresult r = enc(m, CU_TENSOR_MAP_DATA_TYPE_FLOAT32, 2, const_cast<float*>(base), dims, strides, box, es,
-                   CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
+                   CU_TENSOR_MAP_INTERLEAVE_NONE,
+                   mn_major ? CU_TENSOR_MAP_SWIZZLE_128B_ATOM_32B : CU_TENSOR_MAP_SWIZZLE_128B,
+                   CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
                    CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
   return r == CUDA_SUCCESS;
 }
@@ -429,13 +389,13 @@ int num_sms() {
   return sms;
 }
 
-uint32_t make_idesc(int bn) {
+uint32_t make_idesc(int bn, bool a_mn, bool b_mn) {
   uint32_t d = 0;
   d |= 1u << 4;                       // D format F32
   d |= 2u << 7;                       // A format TF32
   d |= 2u << 10;                      // B format TF32
-  d |= 0u << 15;                      // A K-major
-  d |= 0u << 16;                      // B K-major
+  d |= (a_mn ? 1u : 0u) << 15;        // A major (0 = K, 1 = MN)
+  d |= (b_mn ? 1u : 0u) << 16;        // B major
   d |= (uint32_t)(bn >> 3) << 17;     // N >> 3
   d |= (uint32_t)(BM >> 4) << 24;     // M >> 4
   return d;
@@ -474,16 +434,18 @@ st_status launch(const GemmArgs& g, int M, int N, int K, const CUtensorMap& ma, 
   p.relu = relu;
   p.counters = reinterpret_cast<int*>(g.work);
   p.ws = reinterpret_cast<float*>(static_cast<char*>(g.work) + kCounterBytes);
-  p.idesc = make_idesc(p.bn);
+  p.idesc = make_idesc(p.bn, A_MN, B_MN);
   dim3 grid(mt, nt, p.splits);
-  auto kern = (g.mode == ST_GEMM_FP32X3) ? tc_gemm_kernel<EPI, A_MN, B_MN, true> : tc_gemm_kernel<EPI, A_MN, B_MN, false>;
+  constexpr int S = 3;
+  auto kern = (g.mode == ST_GEMM_FP32X3) ? tc_gemm_kernel<EPI, A_MN, B_MN, true, S>
+                                         : tc_gemm_kernel<EPI, A_MN, B_MN, false, S>;
   static bool attr_set[2] = {false, false};
   const int ai = g.mode == ST_GEMM_FP32X3 ? 1 : 0;
   if (!attr_set[ai]) {
-    ST_CUDA_TRY(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, SMEM_BYTES));
+    ST_CUDA_TRY(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, smem_bytes(S)));
     attr_set[ai] = true;
   }
-  kern<<<grid, kThreads, SMEM_BYTES, g.stream>>>(ma, mb, p);
+  kern<<<grid, kThreads, smem_bytes(S), g.stream>>>(ma, mb, p);
   ST_CUDA_TRY(cudaGetLastError());
   g_launches = 1;
   return ST_OK;
@@ -501,15 +463,18 @@ int64_t tc_workspace_bytes(int, int, int) { return (int64_t)kCounterBytes + (int
 st_status simt_fwd(const GemmArgs& g, const float* X, const float* W, const float* bias, float* Z, int relu);
 st_status simt_dx(const GemmArgs& g, const float* dZ, const float* W, const float* mask, float* D);
 st_status simt_dw(const GemmArgs& g, const float* X, const float* dZ, float* G, float* gb);
+int simt_last_launches();
 
 // fwd: M = out, N = B, K = in
 st_status tc_fwd(const GemmArgs& g, const float* X, const float* W, const float* bias, float* Z, int relu) {
   if (!tma_ok(W, g.n_out) || !tma_ok(X, g.n_in) || !get_encode()) {
-    g_launches = 1;
-    return simt_fwd(g, X, W, bias, Z, relu);  // TMA needs 16-byte pitches (e.g. the 10-wide output layer)
+    // TMA needs 16-byte pitches (e.g. the 10-wide output layer): CUDA-core split-K path
+    st_status s = simt_fwd(g, X, W, bias, Z, relu);
+    g_launches = simt_last_launches();
+    return s;
   }
   CUtensorMap ma, mb;
-  if (!make_map(&ma, W, g.n_out, g.n_in, g.n_out, 32) || !make_map(&mb, X, g.n_in, g.B, g.n_in, bn_for(g.B)))
+  if (!make_map(&ma, W, g.n_out, g.n_in, g.n_out, 32, true) || !make_map(&mb, X, g.n_in, g.B, g.n_in, bn_for(g.B), false))
     return set_error(ST_ERR_CUDA, "cuTensorMapEncodeTiled failed (fwd)");
   return launch<EPI_FWD, true, false>(g, g.n_out, g.B, g.n_in, ma, mb, Z, bias, relu);
 }
@@ -517,11 +482,12 @@ st_status tc_fwd(const GemmArgs& g, const float* X, const float* W, const float*
 // dX: M = in, N = B, K = out
 st_status tc_dx(const GemmArgs& g, const float* dZ, const float* W, const float* mask, float* D) {
   if (!tma_ok(W, g.n_out) || !tma_ok(dZ, g.n_out) || !get_encode()) {
-    g_launches = 1;
-    return simt_dx(g, dZ, W, mask, D);
+    st_status s = simt_dx(g, dZ, W, mask, D);
+    g_launches = simt_last_launches();
+    return s;
   }
   CUtensorMap ma, mb;
-  if (!make_map(&ma, W, g.n_out, g.n_in, g.n_out, BM) || !make_map(&mb, dZ, g.n_out, g.B, g.n_out, bn_for(g.B)))
+  if (!make_map(&ma, W, g.n_out, g.n_in, g.n_out, BM, false) || !make_map(&mb, dZ, g.n_out, g.B, g.n_out, bn_for(g.B), false))
     return set_error(ST_ERR_CUDA, "cuTensorMapEncodeTiled failed (dX)");
   return launch<EPI_DX, false, false>(g, g.n_in, g.B, g.n_out, ma, mb, D, mask, 0);
 }
@@ -529,11 +495,12 @@ st_status tc_dx(const GemmArgs& g, const float* dZ, const float* W, const float*
 // dW: M = out, N = in, K = B
 st_status tc_dw(const GemmArgs& g, const float* X, const float* dZ, float* G, float* gb) {
   if (!tma_ok(dZ, g.n_out) || !tma_ok(X, g.n_in) || !get_encode()) {
-    g_launches = gb ? 2 : 1;
-    return simt_dw(g, X, dZ, G, gb);
+    st_status s = simt_dw(g, X, dZ, G, gb);
+    g_launches = simt_last_launches();
+    return s;
   }
   CUtensorMap ma, mb;
-  if (!make_map(&ma, dZ, g.n_out, g.B, g.n_out, 32) || !make_map(&mb, X, g.n_in, g.B, g.n_in, 32))
+  if (!make_map(&ma, dZ, g.n_out, g.B, g.n_out, 32, true) || !make_map(&mb, X, g.n_in, g.B, g.n_in, 32, true))
     return set_error(ST_ERR_CUDA, "cuTensorMapEncodeTiled failed (dW)");
   ST_TRY((launch<EPI_DW, true, true>(g, g.n_out, g.n_in, g.B, ma, mb, G, nullptr, 0)));
   if (gb) {

@@ -26,7 +26,8 @@ st_status launch_update_predict(float* W, float* V, const float* G, float* WF, f
 struct GemmArgs {
   int mode;  // ST_GEMM_*
   int B, n_in, n_out;
-  void* work;  // split-K workspace (gemm_workspace_bytes)
+  void* work;  // split-K workspace (gemm_workspace_bytes), 64 KB zeroed counters first
+  int64_t work_bytes;
   cudaStream_t stream;
 };
 int64_t gemm_workspace_bytes(int B, int max_in, int max_out);

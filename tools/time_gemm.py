@@ -1,0 +1,34 @@
+"""Time the stage GEMMs through st_gemm_raw (CUDA events, warm) — development tool."""
+import sys, os, json
+sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
+import torch
+import paper_1809_02839_b200 as st
+
+def t_op(op, mode, B, n_in, n_out, reps=10):
+    dev = torch.device("cuda", 0)
+    X = torch.randn(B, n_in, device=dev)
+    W = torch.randn(n_in, n_out, device=dev) * 0.01
+    dZ = torch.randn(B, n_out, device=dev)
+    bias = torch.randn(n_out, device=dev)
+    work = torch.zeros(int(st._lib.lib.st_gemm_workspace_bytes(B, n_in, n_out)), dtype=torch.uint8, device=dev)
+    if op == 0: args = (X, W, bias, None, torch.empty(B, n_out, device=dev))
+    elif op == 1: args = (dZ, W, X, None, torch.empty(B, n_in, device=dev))
+    else: args = (X, dZ, None, torch.empty(n_out, device=dev), torch.empty(n_in, n_out, device=dev))
+    f = lambda: st.gemm_raw(op, mode, B, n_in, n_out, *args, relu=(op == 0), work=work)
+    f(); torch.cuda.synchronize()
+    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    e0.record()
+    for _ in range(reps): f()
+    e1.record(); torch.cuda.synchronize()
+    us = e0.elapsed_time(e1) * 1e3 / reps
+    flops = 2.0 * B * n_in * n_out
+    byts = 4.0 * n_in * n_out
+    return us, flops / us / 1e6, byts / us / 1e3
+
+if __name__ == "__main__":
+    shapes = [(128, 8192, 8192), (128, 784, 8192), (128, 8192, 10)]
+    for (B, i, o) in shapes:
+        for mode, mname in ((0, "fp32x3"), (1, "tf32")):
+            for op, oname in ((0, "fwd"), (1, "dX"), (2, "dW")):
+                us, tf, gbs = t_op(op, mode, B, i, o)
+                print(f"{oname:3s} {mname:6s} B={B} in={i} out={o}: {us:8.1f} us  {tf:7.1f} TFLOP/s  weight-bytes {gbs:7.1f} GB/s")
