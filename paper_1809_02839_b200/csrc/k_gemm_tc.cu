@@ -20,6 +20,7 @@
 //               split-K partials are reduced in fixed split order by the last CTA.
 #include <cuda.h>
 
+#include <cstdlib>
 #include <mutex>
 
 #include "kernels.hpp"
@@ -51,6 +52,7 @@ struct TcParams {
   float* ws;         // split-K partials [splits][tiles][BNMAX][BM]
   int* counters;     // [tiles]
   uint32_t idesc;
+  int dev_flags;     // development only (ST_GEMM_DEV_FLAGS): bit0 skip MMAs, bit1 skip converter math
 };
 
 // ------------------------------------------------------------------ PTX helpers
@@ -149,6 +151,104 @@ __device__ __forceinline__ void make_lo(const char* raw, char* lo, int chunks, i
   for (; c < chunks; c += 128) {
     const float4 v = *reinterpret_cast<const float4*>(raw + c * 16);
     *reinterpret_cast<float4*>(lo + c * 16) = make_float4(lo_part(v.x), lo_part(v.y), lo_part(v.z), lo_part(v.w));
+  }
+}
+
+
+// Epilogue (4 warps, 128 threads): TMEM lane = m (the warp's quadrant), columns = n.
+// Fused: fwd bias + ReLU, dX ReLU mask; split-K partials reduced in fixed split order
+// by the last CTA of the tile (deterministic), counters self-reset.
+template <int EPI>
+__device__ __forceinline__ void epilogue(const TcParams& p, uint32_t tmem, int warp, int lane, int m0, int n0,
+                                         int split, int tile, int tiles, int* last_flag, uint32_t b_acc_full) {
+  mbar_wait(b_acc_full, 0);
+  tc_fence_after();
+  const int bn = p.bn;
+  const int ctid = (warp - 2) * 32 + lane;
+  const int quad = warp & 3;
+  const int m = m0 + quad * 32 + lane;
+  const uint32_t trow = tmem + ((uint32_t)(quad * 32) << 16);
+  if (p.splits > 1) {
+    float* wsp = p.ws + ((size_t)split * tiles + tile) * (BNMAX * BM);
+    for (int c = 0; c < bn; c += 16) {
+      float v[16];
+      tc_ld16(trow + c, v);
+#pragma unroll
+      for (int j = 0; j < 16; ++j) wsp[(size_t)(c + j) * BM + quad * 32 + lane] = v[j];
+    }
+    __threadfence();
+    asm volatile("bar.sync 1, 128;" ::: "memory");
+    if (ctid == 0) {
+      const int prev = atomicAdd(p.counters + tile, 1);
+      *last_flag = (prev == p.splits - 1);
+    }
+    asm volatile("bar.sync 1, 128;" ::: "memory");
+    if (*last_flag) {
+      __threadfence();
+      const float bias = (EPI == EPI_FWD && p.aux && m < p.M) ? p.aux[m] : 0.f;
+      // Fixed split order 0..S−1 (deterministic); this CTA's own partial comes from
+      // TMEM, the others from the workspace with 16 independent loads in flight.
+      for (int c = 0; c < bn; c += 16) {
+        float acc[16], mine[16];
+        tc_ld16(trow + c, mine);
+#pragma unroll
+        for (int j = 0; j < 16; ++j) acc[j] = 0.f;
+        for (int s = 0; s < p.splits; ++s) {
+          if (s == split) {
+#pragma unroll
+            for (int j = 0; j < 16; ++j) acc[j] += mine[j];
+          } else {
+            const float* src = p.ws + ((size_t)s * tiles + tile) * (BNMAX * BM) + (size_t)c * BM + quad * 32 + lane;
+            float v[16];
+#pragma unroll
+            for (int j = 0; j < 16; ++j) v[j] = __ldcg(src + (size_t)j * BM);
+#pragma unroll
+            for (int j = 0; j < 16; ++j) acc[j] += v[j];
+          }
+        }
+        if (m < p.M) {
+#pragma unroll
+          for (int j = 0; j < 16; ++j) {
+            const int n = n0 + c + j;
+            if (n < p.N) {
+              const size_t o = (size_t)n * p.M + m;
+              float v = acc[j];
+              if (EPI == EPI_FWD) {
+                v += bias;
+                if (p.relu) v = fmaxf(v, 0.f);
+              } else if (EPI == EPI_DX) {
+                if (p.aux && !(p.aux[o] > 0.f)) v = 0.f;
+              }
+              p.out[o] = v;
+            }
+          }
+        }
+      }
+      if (ctid == 0) p.counters[tile] = 0;  // self-reset for the next launch
+    }
+  } else {
+    const float bias = (EPI == EPI_FWD && p.aux && m < p.M) ? p.aux[m] : 0.f;
+    for (int c = 0; c < bn; c += 16) {
+      float v[16];
+      tc_ld16(trow + c, v);
+      if (m < p.M) {
+#pragma unroll
+        for (int j = 0; j < 16; ++j) {
+          const int n = n0 + c + j;
+          if (n < p.N) {
+            const size_t o = (size_t)n * p.M + m;
+            float x = v[j];
+            if (EPI == EPI_FWD) {
+              x += bias;
+              if (p.relu) x = fmaxf(x, 0.f);
+            } else if (EPI == EPI_DX) {
+              if (p.aux && !(p.aux[o] > 0.f)) x = 0.f;
+            }
+            p.out[o] = x;
+          }
+        }
+      }
+    }
   }
 }
 
@@ -263,75 +363,8 @@ __global__ void __launch_bounds__(kThreads, 1)
       }
     }
 
-    // ---------------- epilogue: TMEM lane = m (this warp's quadrant), columns = n
-    mbar_wait(b_acc_full, 0);
-    tc_fence_after();
-    const int quad = warp & 3;
-    const int m = m0 + quad * 32 + lane;
-    const uint32_t trow = tmem + ((uint32_t)(quad * 32) << 16);
-    const int tiles = gridDim.x * gridDim.y;
-    const int tile = n_tile * gridDim.x + m_tile;
-    if (p.splits > 1) {
-      float* wsp = p.ws + ((size_t)split * tiles + tile) * (BNMAX * BM);
-      for (int c = 0; c < bn; c += 16) {
-        float v[16];
-        tc_ld16(trow + c, v);
-#pragma unroll
-        for (int j = 0; j < 16; ++j) wsp[(size_t)(c + j) * BM + quad * 32 + lane] = v[j];
-      }
-      __threadfence();
-      asm volatile("bar.sync 1, 128;" ::: "memory");
-      if (ctid == 0) {
-        const int prev = atomicAdd(p.counters + tile, 1);
-        *last_flag = (prev == p.splits - 1);
-      }
-      asm volatile("bar.sync 1, 128;" ::: "memory");
-      if (*last_flag) {
-        __threadfence();
-        const float bias = (EPI == EPI_FWD && p.aux && m < p.M) ? p.aux[m] : 0.f;
-        for (int c = 0; c < bn; ++c) {
-          const int n = n0 + c;
-          float acc = 0.f;
-          for (int s = 0; s < p.splits; ++s)
-            acc += __ldcg(p.ws + ((size_t)s * tiles + tile) * (BNMAX * BM) + (size_t)c * BM + quad * 32 + lane);
-          if (m < p.M && n < p.N) {
-            const size_t o = (size_t)n * p.M + m;
-            float v = acc;
-            if (EPI == EPI_FWD) {
-              v += bias;
-              if (p.relu) v = fmaxf(v, 0.f);
-            } else if (EPI == EPI_DX) {
-              if (p.aux && !(p.aux[o] > 0.f)) v = 0.f;
-            }
-            p.out[o] = v;
-          }
-        }
-        if (ctid == 0) p.counters[tile] = 0;  // self-reset for the next launch
-      }
-    } else {
-      const float bias = (EPI == EPI_FWD && p.aux && m < p.M) ? p.aux[m] : 0.f;
-      for (int c = 0; c < bn; c += 16) {
-        float v[16];
-        tc_ld16(trow + c, v);
-        if (m < p.M) {
-#pragma unroll
-          for (int j = 0; j < 16; ++j) {
-            const int n = n0 + c + j;
-            if (n < p.N) {
-              const size_t o = (size_t)n * p.M + m;
-              float x = v[j];
-              if (EPI == EPI_FWD) {
-                x += bias;
-                if (p.relu) x = fmaxf(x, 0.f);
-              } else if (EPI == EPI_DX) {
-                if (p.aux && !(p.aux[o] > 0.f)) x = 0.f;
-              }
-              p.out[o] = x;
-            }
-          }
-        }
-      }
-    }
+    epilogue<EPI>(p, tmem, warp, lane, m0, n0, split, n_tile * gridDim.x + m_tile, gridDim.x * gridDim.y,
+                  last_flag, b_acc_full);
   }
 
   tc_fence_before();
@@ -339,6 +372,413 @@ __global__ void __launch_bounds__(kThreads, 1)
   if (warp == 1) {
     tc_fence_after();
     asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(tmem), "r"(BNMAX));
+  }
+}
+
+
+// ============================================================================
+// FP32X3 forward / dX kernel: weights through TMEM (tcgen05.mma A-from-TMEM).
+//
+// The weight operand (A, 128 rows of W per tile, K-major for dX, MN-major for fwd)
+// streams from HBM through a deep smem ring (RA × 16 KB). Converter warps read
+// each raw tile once, write hi (= raw, the tensor core truncates) and
+// lo = x − trunc_tf32(x) straight into a TMEM ring with tcgen05.st and release the
+// smem slot immediately. The activation operand (B, K-major) arrives as hi + lo
+// tiles by TMA (lo precomputed once per GEMM by split_lo_kernel). The MMA thread
+// issues A_hi·B_hi + A_lo·B_hi + A_hi·B_lo per K step of 8, reading only B from smem.
+// ============================================================================
+constexpr int TS_RA = 6;                 // weight (A) raw ring stages, 16 KB each
+constexpr int TS_RB = 3;                 // activation (B) ring stages, hi + lo ≤ 32 KB
+constexpr int TS_TA = 3;                 // TMEM A slots (64 columns: 32 hi + 32 lo)
+constexpr int TS_THREADS = 224;          // 7 warps
+constexpr int TS_B_STAGE = 2 * BNMAX * BK * 4;
+constexpr int ts_smem_bytes() { return TS_RA * TILE_BYTES + TS_RB * TS_B_STAGE + 1024 + 512; }
+
+__device__ __forceinline__ void tc_mma_ts(uint32_t tmem_d, uint32_t tmem_a, uint64_t bdesc, uint32_t idesc,
+                                          uint32_t accum) {
+  asm volatile(
+      "{\n .reg .pred p;\n setp.ne.b32 p, %4, 0;\n tcgen05.mma.cta_group::1.kind::tf32 [%0], [%1], %2, %3, p;\n}" ::"r"(
+          tmem_d),
+      "r"(tmem_a), "l"(bdesc), "r"(idesc), "r"(accum)
+      : "memory");
+}
+
+__device__ __forceinline__ void tc_st32(uint32_t taddr, const uint32_t* v) {
+  asm volatile(
+      "tcgen05.st.sync.aligned.32x32b.x32.b32 [%0], {%1,%2,%3,%4,%5,%6,%7,%8,%9,%10,%11,%12,%13,%14,%15,%16,%17,%18,"
+      "%19,%20,%21,%22,%23,%24,%25,%26,%27,%28,%29,%30,%31,%32};" ::"r"(taddr),
+      "r"(v[0]), "r"(v[1]), "r"(v[2]), "r"(v[3]), "r"(v[4]), "r"(v[5]), "r"(v[6]), "r"(v[7]), "r"(v[8]), "r"(v[9]),
+      "r"(v[10]), "r"(v[11]), "r"(v[12]), "r"(v[13]), "r"(v[14]), "r"(v[15]), "r"(v[16]), "r"(v[17]), "r"(v[18]),
+      "r"(v[19]), "r"(v[20]), "r"(v[21]), "r"(v[22]), "r"(v[23]), "r"(v[24]), "r"(v[25]), "r"(v[26]), "r"(v[27]),
+      "r"(v[28]), "r"(v[29]), "r"(v[30]), "r"(v[31])
+      : "memory");
+}
+
+template <int EPI, bool A_MN>
+__global__ void __launch_bounds__(TS_THREADS, 1)
+    tc_ts_kernel(const __grid_constant__ CUtensorMap mapA, const __grid_constant__ CUtensorMap mapB,
+                 const __grid_constant__ CUtensorMap mapBlo, TcParams p) {
+  extern __shared__ __align__(1024) uint8_t smem_raw[];
+  char* smem = reinterpret_cast<char*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
+  char* ringA = smem;
+  char* ringB = smem + TS_RA * TILE_BYTES;
+  uint64_t* bars = reinterpret_cast<uint64_t*>(ringB + TS_RB * TS_B_STAGE);
+  const uint32_t a_full = smem_u32(bars);          // TMA landed (A)          [RA]
+  const uint32_t a_free = a_full + 8 * TS_RA;      // converter read it       [RA]
+  const uint32_t b_full = a_free + 8 * TS_RA;      // TMA landed (B hi + lo)  [RB]
+  const uint32_t b_empty = b_full + 8 * TS_RB;     // MMA done with B         [RB]
+  const uint32_t t_full = b_empty + 8 * TS_RB;     // TMEM A slot written     [TA]
+  const uint32_t t_empty = t_full + 8 * TS_TA;     // MMA done with TMEM slot [TA]
+  const uint32_t acc_full = t_empty + 8 * TS_TA;
+  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(bars + 2 * TS_RA + 2 * TS_RB + 2 * TS_TA + 1);
+  int* last_flag = reinterpret_cast<int*>(tmem_slot + 1);
+
+  const int warp = threadIdx.x >> 5;
+  const int lane = threadIdx.x & 31;
+  const int m_tile = blockIdx.x, n_tile = blockIdx.y, split = blockIdx.z;
+  const int m0 = m_tile * BM, n0 = n_tile * BNMAX;
+  const int kb0 = split * p.kb_per_split;
+  const int nkb = min(p.kb_total, kb0 + p.kb_per_split) - kb0;
+  const int bn = p.bn;
+
+  if (threadIdx.x == 0) {
+    for (int s = 0; s < TS_RA; ++s) {
+      mbar_init(a_full + 8 * s, 1);
+      mbar_init(a_free + 8 * s, 4);
+    }
+    for (int s = 0; s < TS_RB; ++s) {
+      mbar_init(b_full + 8 * s, 1);
+      mbar_init(b_empty + 8 * s, 1);
+    }
+    for (int s = 0; s < TS_TA; ++s) {
+      mbar_init(t_full + 8 * s, 4);
+      mbar_init(t_empty + 8 * s, 1);
+    }
+    mbar_init(acc_full, 1);
+    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+  }
+  if (warp == 1) {
+    asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], 512;" ::"r"(smem_u32(tmem_slot)));
+    asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;");
+  }
+  if (warp == 0 && lane == 0) {
+    asm volatile("prefetch.tensormap [%0];" ::"l"(reinterpret_cast<uint64_t>(&mapA)) : "memory");
+    asm volatile("prefetch.tensormap [%0];" ::"l"(reinterpret_cast<uint64_t>(&mapB)) : "memory");
+    asm volatile("prefetch.tensormap [%0];" ::"l"(reinterpret_cast<uint64_t>(&mapBlo)) : "memory");
+  }
+  tc_fence_before();
+  __syncthreads();
+  tc_fence_after();
+  const uint32_t tmem = *tmem_slot;      // accumulator: columns [0, 128)
+  const uint32_t tmemA = tmem + BNMAX;   // A ring: columns [128, 128 + 64·TA)
+
+  if (warp == 0) {
+    // ---------------- TMA producer, weights (A)
+    if (lane == 0) {
+      for (int i = 0; i < nkb; ++i) {
+        const int s = i % TS_RA;
+        mbar_wait(a_free + 8 * s, ((i / TS_RA) & 1) ^ 1);
+        const uint32_t full = a_full + 8 * s;
+        if (p.dev_flags & 8) {
+          mbar_arrive(full);
+          continue;
+        }
+        mbar_expect_tx(full, TILE_BYTES);
+        const int k0 = (kb0 + i) * BK;
+        const uint32_t dA = smem_u32(ringA + s * TILE_BYTES);
+        if (A_MN) {
+#pragma unroll
+          for (int c = 0; c < BM / 32; ++c) tma_load_2d(dA + c * 4096, &mapA, m0 + 32 * c, k0, full);
+        } else {
+          tma_load_2d(dA, &mapA, k0, m0, full);
+        }
+      }
+    }
+  } else if (warp == 6) {
+    // ---------------- TMA producer, activations (B hi + lo)
+    if (lane == 0) {
+      const uint32_t bytes = (uint32_t)(2 * bn * BK * 4);
+      for (int i = 0; i < nkb; ++i) {
+        const int s = i % TS_RB;
+        mbar_wait(b_empty + 8 * s, ((i / TS_RB) & 1) ^ 1);
+        const uint32_t full = b_full + 8 * s;
+        if (p.dev_flags & 4) {
+          mbar_arrive(full);
+          continue;
+        }
+        mbar_expect_tx(full, bytes);
+        const int k0 = (kb0 + i) * BK;
+        const uint32_t dB = smem_u32(ringB + s * TS_B_STAGE);
+        tma_load_2d(dB, &mapB, k0, n0, full);
+        tma_load_2d(dB + BNMAX * BK * 4, &mapBlo, k0, n0, full);
+      }
+    }
+  } else if (warp == 1) {
+    // ---------------- MMA issuer
+    if (lane == 0) {
+      for (int i = 0; i < nkb; ++i) {
+        const int sb = i % TS_RB, ta = i % TS_TA;
+        mbar_wait(t_full + 8 * ta, (i / TS_TA) & 1);
+        mbar_wait(b_full + 8 * sb, (i / TS_RB) & 1);
+        tc_fence_after();
+        const uint32_t b_hi = smem_u32(ringB + sb * TS_B_STAGE), b_lo = b_hi + BNMAX * BK * 4;
+        const uint32_t a_hi = tmemA + ta * 64, a_lo = a_hi + 32;
+#pragma unroll
+        for (int kk = 0; kk < BK / 8; ++kk) {
+          if (p.dev_flags & 1) break;
+          const uint32_t acc = (i > 0 || kk > 0) ? 1u : 0u;
+          tc_mma_ts(tmem, a_hi + kk * 8, desc_kmajor(b_hi + kk * 32), p.idesc, acc);
+          tc_mma_ts(tmem, a_lo + kk * 8, desc_kmajor(b_hi + kk * 32), p.idesc, 1u);
+          tc_mma_ts(tmem, a_hi + kk * 8, desc_kmajor(b_lo + kk * 32), p.idesc, 1u);
+        }
+        tc_commit(b_empty + 8 * sb);
+        tc_commit(t_empty + 8 * ta);
+      }
+      tc_commit(acc_full);
+    }
+  } else {
+    // ---------------- converter (warps 2..5): raw weight tile → TMEM hi / lo
+    const int quad = warp & 3;
+    const int r = quad * 32 + lane;  // tile row = TMEM lane
+    for (int i = 0; i < nkb; ++i) {
+      const int s = i % TS_RA, ta = i % TS_TA;
+      mbar_wait(a_full + 8 * s, (i / TS_RA) & 1);
+      const char* t = ringA + s * TILE_BYTES;
+      uint32_t hi[32], lo[32];
+      if (p.dev_flags & 2) {
+#pragma unroll
+        for (int k = 0; k < 32; ++k) hi[k] = lo[k] = 0;
+      } else if (A_MN) {
+        // element (k, r): box r/32, row k (128 B), 32-byte atoms swizzled by k % 4
+        const char* box = t + (r >> 5) * 4096;
+#pragma unroll
+        for (int k = 0; k < 32; ++k) {
+          const float x = *reinterpret_cast<const float*>(box + k * 128 + ((((r & 31) >> 3) ^ (k & 3)) << 5) +
+                                                          (r & 7) * 4);
+          hi[k] = __float_as_uint(x);
+          lo[k] = __float_as_uint(lo_part(x));
+        }
+      } else {
+        // row r: 8 chunks of 16 B, SWIZZLE_128B
+#pragma unroll
+        for (int j = 0; j < 8; ++j) {
+          const float4 v = *reinterpret_cast<const float4*>(t + r * 128 + ((j ^ (r & 7)) << 4));
+          hi[4 * j + 0] = __float_as_uint(v.x);
+          hi[4 * j + 1] = __float_as_uint(v.y);
+          hi[4 * j + 2] = __float_as_uint(v.z);
+          hi[4 * j + 3] = __float_as_uint(v.w);
+          lo[4 * j + 0] = __float_as_uint(lo_part(v.x));
+          lo[4 * j + 1] = __float_as_uint(lo_part(v.y));
+          lo[4 * j + 2] = __float_as_uint(lo_part(v.z));
+          lo[4 * j + 3] = __float_as_uint(lo_part(v.w));
+        }
+      }
+      __syncwarp();
+      if (lane == 0) mbar_arrive(a_free + 8 * s);  // smem slot can be refilled
+      mbar_wait(t_empty + 8 * ta, ((i / TS_TA) & 1) ^ 1);
+      tc_fence_after();
+      const uint32_t taddr = tmemA + ta * 64 + ((uint32_t)(quad * 32) << 16);
+      tc_st32(taddr, hi);
+      tc_st32(taddr + 32, lo);
+      asm volatile("tcgen05.wait::st.sync.aligned;" ::: "memory");
+      tc_fence_before();
+      __syncwarp();
+      if (lane == 0) mbar_arrive(t_full + 8 * ta);
+    }
+    epilogue<EPI>(p, tmem, warp, lane, m0, n0, split, n_tile * gridDim.x + m_tile, gridDim.x * gridDim.y,
+                  last_flag, acc_full);
+  }
+
+  tc_fence_before();
+  __syncthreads();
+  if (warp == 1) {
+    tc_fence_after();
+    asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, 512;" ::"r"(tmem));
+  }
+}
+
+// lo = x − trunc_tf32(x) of a whole [rows × pitch] activation matrix (the B operand
+// of the FP32X3 forward / dX GEMMs), computed once per GEMM.
+__global__ void split_lo_kernel(const float4* __restrict__ x, float4* __restrict__ lo, size_t n4) {
+  for (size_t i = blockIdx.x * (size_t)blockDim.x + threadIdx.x; i < n4; i += (size_t)gridDim.x * blockDim.x) {
+    const float4 v = x[i];
+    lo[i] = make_float4(lo_part(v.x), lo_part(v.y), lo_part(v.z), lo_part(v.w));
+  }
+}
+
+
+// ============================================================================
+// FP32X3 / TF32 dW kernel (persistent): G = Xᵀ·dZ as Gᵀ tiles (M = out, N = in, K = B).
+//
+// K = batch is short (≤ 128 here), the output (one fp32 per parameter) dominates.
+// Each CTA walks a contiguous range of 128 × 128 output tiles in m-major order.
+// The A operand (dZᵀ rows of the current m-tile, hi + lo, all of K) stays resident
+// in smem and is reloaded only when m changes; B (X columns, hi + lo) streams
+// through a 3-stage ring in K-blocks of 32. Two TMEM accumulators (2 × 128 columns)
+// let the epilogue of tile t overlap the MMAs of tile t + 1. Both lo operands are
+// precomputed by split_lo_kernel (dZ and X are activation-sized).
+// ============================================================================
+constexpr int DW_KMAX = 128;                       // resident-A capacity along K (= batch)
+constexpr int DW_RB = 3;                           // B ring stages (hi + lo, 32 KB)
+constexpr int DW_THREADS = 192;
+constexpr int DW_A_BYTES = 2 * (DW_KMAX / BK) * TILE_BYTES;  // A hi + lo for K ≤ 128: 128 KB
+constexpr int DW_B_STAGE = 2 * TILE_BYTES;
+constexpr int dw_smem_bytes() { return DW_A_BYTES + DW_RB * DW_B_STAGE + 1024 + 512; }
+
+template <bool kX3>
+__global__ void __launch_bounds__(DW_THREADS, 1)
+    tc_dw_kernel(const __grid_constant__ CUtensorMap mapA, const __grid_constant__ CUtensorMap mapAlo,
+                 const __grid_constant__ CUtensorMap mapB, const __grid_constant__ CUtensorMap mapBlo, TcParams p,
+                 int m_tiles, int n_tiles) {
+  extern __shared__ __align__(1024) uint8_t smem_raw[];
+  char* smem = reinterpret_cast<char*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
+  char* Abuf = smem;                      // [hi: kb × 16 KB][lo: kb × 16 KB]
+  char* ringB = smem + DW_A_BYTES;
+  uint64_t* bars = reinterpret_cast<uint64_t*>(ringB + DW_RB * DW_B_STAGE);
+  const uint32_t a_full = smem_u32(bars);         // resident A loaded
+  const uint32_t a_empty = a_full + 8;            // MMAs of the previous m-tile done
+  const uint32_t b_full = a_empty + 8;            // [RB]
+  const uint32_t b_empty = b_full + 8 * DW_RB;    // [RB]
+  const uint32_t c_full = b_empty + 8 * DW_RB;    // [2] accumulator ready
+  const uint32_t c_empty = c_full + 16;           // [2] epilogue drained it
+  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(bars + 4 + 2 * DW_RB);
+
+  const int warp = threadIdx.x >> 5;
+  const int lane = threadIdx.x & 31;
+  const int tiles = m_tiles * n_tiles;
+  const int t_begin = (int)((long long)blockIdx.x * tiles / gridDim.x);
+  const int t_end = (int)((long long)(blockIdx.x + 1) * tiles / gridDim.x);
+  const int nkb = p.kb_total;  // K blocks (K ≤ 128)
+  const int bn = p.bn;
+
+  if (threadIdx.x == 0) {
+    mbar_init(a_full, 1);
+    mbar_init(a_empty, 1);
+    for (int s = 0; s < DW_RB; ++s) {
+      mbar_init(b_full + 8 * s, 1);
+      mbar_init(b_empty + 8 * s, 1);
+    }
+    for (int s = 0; s < 2; ++s) {
+      mbar_init(c_full + 8 * s, 1);
+      mbar_init(c_empty + 8 * s, 4);
+    }
+    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+  }
+  if (warp == 1) {
+    asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], 256;" ::"r"(smem_u32(tmem_slot)));
+    asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;");
+  }
+  tc_fence_before();
+  __syncthreads();
+  tc_fence_after();
+  const uint32_t tmem = *tmem_slot;
+
+  if (warp == 0) {
+    // ---------------- TMA producer: resident A per m-tile, B ring per tile × K-block
+    if (lane == 0) {
+      int cur_m = -1, a_loads = 0, it = 0;
+      for (int t = t_begin; t < t_end; ++t) {
+        const int m_t = t / n_tiles, n_t = t % n_tiles;
+        if (m_t != cur_m) {
+          if (a_loads > 0) mbar_wait(a_empty, (a_loads - 1) & 1);
+          const uint32_t bytes = (uint32_t)((kX3 ? 2 : 1) * nkb * TILE_BYTES);
+          mbar_expect_tx(a_full, bytes);
+          for (int kb = 0; kb < nkb; ++kb) {
+            const uint32_t dA = smem_u32(Abuf + kb * TILE_BYTES);
+#pragma unroll
+            for (int c = 0; c < BM / 32; ++c) {
+              tma_load_2d(dA + c * 4096, &mapA, m_t * BM + 32 * c, kb * BK, a_full);
+              if (kX3) tma_load_2d(dA + (DW_KMAX / BK) * TILE_BYTES + c * 4096, &mapAlo, m_t * BM + 32 * c, kb * BK, a_full);
+            }
+          }
+          cur_m = m_t;
+          ++a_loads;
+        }
+        const int nbox = (bn + 31) / 32;
+        const uint32_t bytes = (uint32_t)((kX3 ? 2 : 1) * nbox * 4096);
+        for (int kb = 0; kb < nkb; ++kb, ++it) {
+          const int s = it % DW_RB;
+          mbar_wait(b_empty + 8 * s, ((it / DW_RB) & 1) ^ 1);
+          const uint32_t full = b_full + 8 * s;
+          mbar_expect_tx(full, bytes);
+          const uint32_t dB = smem_u32(ringB + s * DW_B_STAGE);
+          for (int c = 0; c < nbox; ++c) {
+            tma_load_2d(dB + c * 4096, &mapB, n_t * BNMAX + 32 * c, kb * BK, full);
+            if (kX3) tma_load_2d(dB + TILE_BYTES + c * 4096, &mapBlo, n_t * BNMAX + 32 * c, kb * BK, full);
+          }
+        }
+      }
+    }
+  } else if (warp == 1) {
+    // ---------------- MMA issuer
+    if (lane == 0) {
+      int cur_m = -1, a_loads = 0, it = 0, local = 0;
+      for (int t = t_begin; t < t_end; ++t, ++local) {
+        const int m_t = t / n_tiles;
+        if (m_t != cur_m) {
+          if (a_loads > 0) tc_commit(a_empty);  // all MMAs on the old A issued before this commit
+          mbar_wait(a_full, a_loads & 1);
+          cur_m = m_t;
+          ++a_loads;
+        }
+        const int buf = local & 1;
+        mbar_wait(c_empty + 8 * buf, ((local >> 1) & 1) ^ 1);
+        tc_fence_after();
+        const uint32_t acc_t = tmem + buf * BNMAX;
+        for (int kb = 0; kb < nkb; ++kb, ++it) {
+          const int s = it % DW_RB;
+          mbar_wait(b_full + 8 * s, (it / DW_RB) & 1);
+          tc_fence_after();
+          const uint32_t a_hi = smem_u32(Abuf + kb * TILE_BYTES), a_lo = a_hi + (DW_KMAX / BK) * TILE_BYTES;
+          const uint32_t b_hi = smem_u32(ringB + s * DW_B_STAGE), b_lo = b_hi + TILE_BYTES;
+#pragma unroll
+          for (int kk = 0; kk < BK / 8; ++kk) {
+            const uint32_t acc = (kb > 0 || kk > 0) ? 1u : 0u;
+            tc_mma(acc_t, desc_mnmajor(a_hi + kk * 1024), desc_mnmajor(b_hi + kk * 1024), p.idesc, acc);
+            if (kX3) {
+              tc_mma(acc_t, desc_mnmajor(a_lo + kk * 1024), desc_mnmajor(b_hi + kk * 1024), p.idesc, 1u);
+              tc_mma(acc_t, desc_mnmajor(a_hi + kk * 1024), desc_mnmajor(b_lo + kk * 1024), p.idesc, 1u);
+            }
+          }
+          tc_commit(b_empty + 8 * s);
+        }
+        tc_commit(c_full + 8 * buf);
+      }
+    }
+  } else {
+    // ---------------- epilogue (warps 2..5): accumulator → G[n·M + m]
+    const int quad = warp & 3;
+    int local = 0;
+    for (int t = t_begin; t < t_end; ++t, ++local) {
+      const int m_t = t / n_tiles, n_t = t % n_tiles;
+      const int buf = local & 1;
+      mbar_wait(c_full + 8 * buf, (local >> 1) & 1);
+      tc_fence_after();
+      const int m = m_t * BM + quad * 32 + lane;
+      const uint32_t trow = tmem + buf * BNMAX + ((uint32_t)(quad * 32) << 16);
+      const int n0 = n_t * BNMAX;
+      for (int c = 0; c < bn; c += 16) {
+        float v[16];
+        tc_ld16(trow + c, v);
+        if (m < p.M) {
+#pragma unroll
+          for (int j = 0; j < 16; ++j) {
+            const int n = n0 + c + j;
+            if (n < p.N) __stcs(p.out + (size_t)n * p.M + m, v[j]);
+          }
+        }
+      }
+      tc_fence_before();
+      __syncwarp();
+      if (lane == 0) mbar_arrive(c_empty + 8 * buf);
+    }
+  }
+
+  tc_fence_before();
+  __syncthreads();
+  if (warp == 1) {
+    tc_fence_after();
+    asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, 256;" ::"r"(tmem));
   }
 }
 
@@ -405,6 +845,15 @@ uint32_t make_idesc(int bn, bool a_mn, bool b_mn) {
 // B box of K-major operands has exactly bn rows (OOB rows are zero-filled by TMA).
 int bn_for(int N) { return std::max(16, (std::min(N, BNMAX) + 15) / 16 * 16); }
 
+int dev_flags() {
+  static int f = -1;
+  if (f < 0) {
+    const char* e = getenv("ST_GEMM_DEV_FLAGS");
+    f = e ? atoi(e) : 0;
+  }
+  return f;
+}
+
 bool aligned16(const void* p) { return ((uintptr_t)p & 15u) == 0; }
 
 static thread_local int g_launches = 0;
@@ -424,7 +873,7 @@ st_status launch(const GemmArgs& g, int M, int N, int K, const CUtensorMap& ma, 
   if (tiles < num_sms()) splits = std::min(num_sms() / tiles, p.kb_total);
   if (splits < 1) splits = 1;
   const size_t part_bytes = (size_t)BNMAX * BM * 4;
-  const size_t ws_cap = (size_t)tc_workspace_bytes(0, 0, 0) - kCounterBytes;
+  const size_t ws_cap = (size_t)2 * 148 * BNMAX * BM * 4;
   while (splits > 1 && ((size_t)splits * tiles * part_bytes > ws_cap || tiles > (int)(kCounterBytes / 4))) --splits;
   p.kb_per_split = (p.kb_total + splits - 1) / splits;
   p.splits = (p.kb_total + p.kb_per_split - 1) / p.kb_per_split;
@@ -453,12 +902,73 @@ st_status launch(const GemmArgs& g, int M, int N, int K, const CUtensorMap& ma, 
 
 bool tma_ok(const void* p, int pitch) { return aligned16(p) && (pitch % 4) == 0; }
 
+// split-K plan shared by both kernels
+void plan_splits(TcParams& p, int M, int N, int K) {
+  p.M = M;
+  p.N = N;
+  p.K = K;
+  p.kb_total = (K + BK - 1) / BK;
+  const int mt = (M + BM - 1) / BM, nt = (N + BNMAX - 1) / BNMAX;
+  const int tiles = mt * nt;
+  int splits = 1;
+  if (tiles < num_sms()) splits = std::min(num_sms() / tiles, p.kb_total);
+  if (splits < 1) splits = 1;
+  const size_t part_bytes = (size_t)BNMAX * BM * 4;
+  const size_t ws_cap = (size_t)2 * 148 * BNMAX * BM * 4;
+  while (splits > 1 && ((size_t)splits * tiles * part_bytes > ws_cap || tiles > (int)(kCounterBytes / 4))) --splits;
+  p.kb_per_split = (p.kb_total + splits - 1) / splits;
+  p.splits = (p.kb_total + p.kb_per_split - 1) / p.kb_per_split;
+  p.bn = bn_for(N);
+}
+
+// FP32X3 fwd / dX through the TMEM-A kernel. Bact: the activation operand [N rows × K]
+// (row pitch K); its lo part goes to the workspace tail.
+template <int EPI, bool A_MN>
+st_status launch_ts(const GemmArgs& g, int M, int N, int K, const CUtensorMap& ma, const float* Bact, float* out,
+                    const float* aux, int relu) {
+  TcParams p{};
+  plan_splits(p, M, N, K);
+  p.out = out;
+  p.aux = aux;
+  p.relu = relu;
+  p.counters = reinterpret_cast<int*>(g.work);
+  p.ws = reinterpret_cast<float*>(static_cast<char*>(g.work) + kCounterBytes);
+  p.idesc = make_idesc(p.bn, false, false);
+  p.dev_flags = dev_flags();
+  float* blo = reinterpret_cast<float*>(static_cast<char*>(g.work) + kCounterBytes +
+                                        (size_t)2 * 148 * BNMAX * BM * 4);
+  const size_t n4 = (size_t)N * K / 4;
+  split_lo_kernel<<<std::min<size_t>(4 * 148, (n4 + 255) / 256), 256, 0, g.stream>>>(
+      reinterpret_cast<const float4*>(Bact), reinterpret_cast<float4*>(blo), n4);
+  ST_CUDA_TRY(cudaGetLastError());
+  CUtensorMap mb, mblo;
+  if (!make_map(&mb, Bact, K, N, K, p.bn, false) || !make_map(&mblo, blo, K, N, K, p.bn, false))
+    return set_error(ST_ERR_CUDA, "cuTensorMapEncodeTiled failed (activation operand)");
+  const int mt = (M + BM - 1) / BM, nt = (N + BNMAX - 1) / BNMAX;
+  dim3 grid(mt, nt, p.splits);
+  auto kern = tc_ts_kernel<EPI, A_MN>;
+  static bool attr_set = false;
+  if (!attr_set) {
+    ST_CUDA_TRY(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, ts_smem_bytes()));
+    attr_set = true;
+  }
+  kern<<<grid, TS_THREADS, ts_smem_bytes(), g.stream>>>(ma, mb, mblo, p);
+  ST_CUDA_TRY(cudaGetLastError());
+  g_launches = 2;
+  return ST_OK;
+}
+
 }  // namespace
 
 int tc_last_launches() { return g_launches; }
 // counters (64 KB, zero-initialised by the owner, self-resetting) + split-K partials
 // for up to 2 × #SMs output tiles of 128 × 128 fp32.
-int64_t tc_workspace_bytes(int, int, int) { return (int64_t)kCounterBytes + (int64_t)2 * 148 * BNMAX * BM * 4; }
+// + the lo part of the activation operand (B × max width fp32) for the FP32X3 fwd / dX.
+// lo tails: dW needs both dZ and X (B × (out + in), each padded to 64 floats).
+int64_t tc_workspace_bytes(int B, int max_in, int max_out) {
+  const int64_t lo = ((int64_t)B * max_out + 63) / 64 * 64 + ((int64_t)B * max_in + 63) / 64 * 64;
+  return (int64_t)kCounterBytes + (int64_t)2 * 148 * BNMAX * BM * 4 + std::max<int64_t>(64, lo) * 4 + 256;
+}
 
 st_status simt_fwd(const GemmArgs& g, const float* X, const float* W, const float* bias, float* Z, int relu);
 st_status simt_dx(const GemmArgs& g, const float* dZ, const float* W, const float* mask, float* D);
@@ -474,6 +984,11 @@ st_status tc_fwd(const GemmArgs& g, const float* X, const float* W, const float*
     return s;
   }
   CUtensorMap ma, mb;
+  if (g.mode == ST_GEMM_FP32X3) {
+    if (!make_map(&ma, W, g.n_out, g.n_in, g.n_out, 32, true))
+      return set_error(ST_ERR_CUDA, "cuTensorMapEncodeTiled failed (fwd)");
+    return launch_ts<EPI_FWD, true>(g, g.n_out, g.B, g.n_in, ma, X, Z, bias, relu);
+  }
   if (!make_map(&ma, W, g.n_out, g.n_in, g.n_out, 32, true) || !make_map(&mb, X, g.n_in, g.B, g.n_in, bn_for(g.B), false))
     return set_error(ST_ERR_CUDA, "cuTensorMapEncodeTiled failed (fwd)");
   return launch<EPI_FWD, true, false>(g, g.n_out, g.B, g.n_in, ma, mb, Z, bias, relu);
@@ -487,6 +1002,11 @@ st_status tc_dx(const GemmArgs& g, const float* dZ, const float* W, const float*
     return s;
   }
   CUtensorMap ma, mb;
+  if (g.mode == ST_GEMM_FP32X3) {
+    if (!make_map(&ma, W, g.n_out, g.n_in, g.n_out, BM, false))
+      return set_error(ST_ERR_CUDA, "cuTensorMapEncodeTiled failed (dX)");
+    return launch_ts<EPI_DX, false>(g, g.n_in, g.B, g.n_out, ma, dZ, D, mask, 0);
+  }
   if (!make_map(&ma, W, g.n_out, g.n_in, g.n_out, BM, false) || !make_map(&mb, dZ, g.n_out, g.B, g.n_out, bn_for(g.B), false))
     return set_error(ST_ERR_CUDA, "cuTensorMapEncodeTiled failed (dX)");
   return launch<EPI_DX, false, false>(g, g.n_in, g.B, g.n_out, ma, mb, D, mask, 0);
@@ -498,6 +1018,53 @@ st_status tc_dw(const GemmArgs& g, const float* X, const float* dZ, float* G, fl
     st_status s = simt_dw(g, X, dZ, G, gb);
     g_launches = simt_last_launches();
     return s;
+  }
+  if (g.B <= DW_KMAX) {
+    // persistent kernel: lo of dZ and X precomputed into the workspace tail
+    const bool x3 = g.mode == ST_GEMM_FP32X3;
+    float* lo_base = reinterpret_cast<float*>(static_cast<char*>(g.work) + kCounterBytes +
+                                              (size_t)2 * 148 * BNMAX * BM * 4);
+    float* dzlo = lo_base;
+    float* xlo = lo_base + (((size_t)g.B * g.n_out + 63) / 64 * 64);
+    int launches = 1;
+    if (x3) {
+      const size_t n4a = (size_t)g.B * g.n_out / 4, n4b = (size_t)g.B * g.n_in / 4;
+      split_lo_kernel<<<std::min<size_t>(4 * 148, (n4a + 255) / 256), 256, 0, g.stream>>>(
+          reinterpret_cast<const float4*>(dZ), reinterpret_cast<float4*>(dzlo), n4a);
+      split_lo_kernel<<<std::min<size_t>(4 * 148, (n4b + 255) / 256), 256, 0, g.stream>>>(
+          reinterpret_cast<const float4*>(X), reinterpret_cast<float4*>(xlo), n4b);
+      ST_CUDA_TRY(cudaGetLastError());
+      launches += 2;
+    }
+    CUtensorMap ma, malo, mb, mblo;
+    if (!make_map(&ma, dZ, g.n_out, g.B, g.n_out, 32, true) || !make_map(&malo, dzlo, g.n_out, g.B, g.n_out, 32, true) ||
+        !make_map(&mb, X, g.n_in, g.B, g.n_in, 32, true) || !make_map(&mblo, xlo, g.n_in, g.B, g.n_in, 32, true))
+      return set_error(ST_ERR_CUDA, "cuTensorMapEncodeTiled failed (dW)");
+    TcParams p{};
+    p.M = g.n_out;
+    p.N = g.n_in;
+    p.K = g.B;
+    p.kb_total = (g.B + BK - 1) / BK;
+    p.splits = 1;
+    p.bn = bn_for(g.n_in);
+    p.out = G;
+    p.idesc = make_idesc(p.bn, true, true);
+    const int mt = (g.n_out + BM - 1) / BM, nt = (g.n_in + BNMAX - 1) / BNMAX;
+    const int grid = std::min(mt * nt, num_sms());
+    auto kern = x3 ? tc_dw_kernel<true> : tc_dw_kernel<false>;
+    static bool attr_set[2] = {false, false};
+    if (!attr_set[x3]) {
+      ST_CUDA_TRY(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, dw_smem_bytes()));
+      attr_set[x3] = true;
+    }
+    kern<<<grid, DW_THREADS, dw_smem_bytes(), g.stream>>>(ma, malo, mb, mblo, p, mt, nt);
+    ST_CUDA_TRY(cudaGetLastError());
+    if (gb) {
+      ST_TRY(launch_bias_grad(dZ, g.B, g.n_out, gb, g.stream));
+      ++launches;
+    }
+    g_launches = launches;
+    return ST_OK;
   }
   CUtensorMap ma, mb;
   if (!make_map(&ma, dZ, g.n_out, g.B, g.n_out, 32, true) || !make_map(&mb, X, g.n_in, g.B, g.n_in, 32, true))

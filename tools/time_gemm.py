@@ -17,6 +17,7 @@ def t_op(op, mode, B, n_in, n_out, reps=10):
     f = lambda: st.gemm_raw(op, mode, B, n_in, n_out, *args, relu=(op == 0), work=work)
     f(); torch.cuda.synchronize()
     e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    torch.cuda._sleep(50_000_000)  # let the host enqueue every rep before the GPU starts: pure device time
     e0.record()
     for _ in range(reps): f()
     e1.record(); torch.cuda.synchronize()
