@@ -315,12 +315,16 @@ def run_ours(args):
         launches = int(lt.item())
     value = args.steps * B / (t_max / 1e3)
 
-    # roofline of the dominant kernel: K-B (k_update.cu); algorithmic bytes per launch
+    # roofline of the dominant kernel: the dW GEMM with the fused K-B update
+    # (k_gemm_tc.cu tc_dw_kernel<x3, UPD> + its lo-split and bias-update launches — the
+    # engine's "gemm_dw" class). Algorithmic bytes per launch = the update stream of that
+    # layer: read W, V + write W, V [+ WF] [+ WB] = 16 / 20 / 24 B per parameter
+    # (operand reads of dZ and X, ~B·(in+out)·8 B, are left out: < 1%).
     kb_bytes, kb_ms, kb_n, stage_ms = 0.0, 0.0, 0, 0.0
     for s, pr in zip(my_stages, profs):
-        bpp = 20 + (4 if s.sizes.s_fwd > 0 else 0) + (4 if (s.sizes.s_bwd > 0 and s.sizes.s_bwd != s.sizes.s_fwd) else 0)
-        ms_k, n_k = pr["update"]
-        kb_bytes += bpp * s.params * n_k
+        bpp = 16 + (4 if s.sizes.s_fwd > 0 else 0) + (4 if (s.sizes.s_bwd > 0 and s.sizes.s_bwd != s.sizes.s_fwd) else 0)
+        ms_k, n_k = pr["gemm_dw"]
+        kb_bytes += bpp * s.params * args.steps
         kb_ms += ms_k
         kb_n += n_k
         stage_ms += sum(v[0] for v in pr.values())
@@ -367,14 +371,16 @@ def run_ours(args):
             "config": {"workload": wname, "stages": S, "batch": B, "gemm": args.gemm, "pred": args.pred,
                        "parallelism": f"pp{S}", "l2": "no flush: per-step working set (weights) >> 126 MB L2",
                        "session": "warm-up and timed steps are separate 1F1B sessions (fill + drain included)"},
-            "roofline": {"kernel": "k_update.cu update_predict_kernel (K-B)", "bound": "hbm",
+            "roofline": {"kernel": "k_gemm_tc.cu tc_dw_kernel<FP32X3, fused K-B update> (dW + Eq.1/apply/predict)",
+                         "bound": "hbm",
                          "achieved": achieved, "peak": peak, "unit": "GB/s",
                          "frac": (achieved / peak) if achieved else None,
-                         "traffic": recorded_traffic(wname, "update_predict_kernel"),
+                         "traffic": recorded_traffic(wname, "dw_update_per_step"),
                          "peak_source": peak_src, "launches": int(kb_n),
-                         "avg_launch_ms": kb_ms / kb_n if kb_n else None,
+                         "per": "all dW+update launches of one step (one per layer)",
+                         "ms_per_step": kb_ms / args.steps,
                          "share_of_stage_time": kb_ms / stage_ms if stage_ms else None,
-                         "algorithmic_bytes_per_launch": kb_bytes / kb_n if kb_n else None},
+                         "algorithmic_bytes_per_step": kb_bytes / args.steps},
             "kernel_ms_total": gemm_prof,
             "cpu_baseline": cpu,
             "e2e": e2e,

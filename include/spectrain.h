@@ -293,6 +293,16 @@ ST_API st_status st_gemm_raw(int op, int gemm_mode, int B, int n_in, int n_out, 
                       const float* aux, float* aux_out, float* out, int relu, void* work, void* stream);
 ST_API int64_t st_gemm_workspace_bytes(int B, int n_in, int n_out);
 
+/* dW fused with the K-B update on one layer block (the path st_run takes): with
+ * g = [X[B×in]ᵀ·dZ[B×out] ; Σ_b dZ] never written to HBM, applies Eq. 1, the D1
+ * apply and the Eq. 4 predictions to W / V / WF / WB, each a block of in·out + out
+ * fp32 (weights [in×out] row-major, then the bias). WF / WB may be NULL. G_scratch
+ * (same size) is used only when the fused kernel cannot run (16-byte pitch rule,
+ * SIMT mode). work: st_gemm_workspace_bytes(B, in, out). Stream-ordered. */
+ST_API st_status st_dw_update_raw(int gemm_mode, int B, int n_in, int n_out, const float* X, const float* dZ, float* W,
+                                  float* V, float* WF, float* WB, float lr, float gamma, int sF, int sB, int momentum,
+                                  float* G_scratch, void* work, void* stream);
+
 /* Softmax-CE on caller buffers: logits [B×C], labels [B] → loss_dev[0] (batch
  * mean) and dlogits [B×C] = (softmax − onehot)/B. */
 ST_API st_status st_softmax_ce_raw(const float* logits, const int32_t* labels, int B, int C, float* loss_dev,

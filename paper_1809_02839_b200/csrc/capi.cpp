@@ -47,6 +47,16 @@ st_status launch_bias_grad(const float* dZ, int B, int n_out, float* gb, cudaStr
 
 using namespace st;
 
+static UpdateArgs block_args(float* W, float* V, float* WF, float* WB, size_t off, const UpdateConsts& c) {
+  UpdateArgs u;
+  u.W = W + off;
+  u.V = V + off;
+  u.WF = WF ? WF + off : nullptr;
+  u.WB = WB ? WB + off : nullptr;
+  u.c = c;
+  return u;
+}
+
 #define GUARD(body)                                                           \
   try {                                                                       \
     body                                                                      \
@@ -235,6 +245,26 @@ st_status st_gemm_raw(int op, int gemm_mode, int B, int n_in, int n_out, const f
       case 2: return gemm_dw(g, a, b, out, aux_out);
       default: return set_error(ST_ERR_INPUT, "gemm_raw: op must be 0, 1 or 2");
     }
+  })
+}
+
+st_status st_dw_update_raw(int gemm_mode, int B, int n_in, int n_out, const float* X, const float* dZ, float* W,
+                           float* V, float* WF, float* WB, float lr, float gamma, int sF, int sB, int momentum,
+                           float* G_scratch, void* work, void* stream) {
+  GUARD({
+    if (!X || !dZ || !W || !V || !G_scratch || !work) return set_error(ST_ERR_INPUT, "dw_update_raw: NULL argument");
+    GemmArgs g;
+    g.mode = gemm_mode;
+    g.B = B;
+    g.n_in = n_in;
+    g.n_out = n_out;
+    g.work = work;
+    g.work_bytes = gemm_workspace_bytes(B, n_in, n_out);
+    g.stream = static_cast<cudaStream_t>(stream);
+    ST_CUDA_TRY(cudaMemsetAsync(work, 0, 64 * 1024, g.stream));
+    const UpdateConsts c = make_update_consts(lr, gamma, sF, sB, momentum);
+    const size_t nw = (size_t)n_in * n_out;
+    return gemm_dw_update(g, X, dZ, block_args(W, V, WF, WB, 0, c), block_args(W, V, WF, WB, nw, c), G_scratch);
   })
 }
 

@@ -455,7 +455,22 @@ static st_status forward_compute(st_ctx* c, int64_t mb, const float* x_dev, cons
   return ST_OK;
 }
 
-static st_status backward_compute(st_ctx* c, int64_t mb) {
+static UpdateArgs block_update(st_ctx* c, int64_t off, const UpdateConsts& k) {
+  UpdateArgs u;
+  u.W = c->W + off;
+  u.V = c->V + off;
+  u.WF = c->WF_out ? c->WF_out + off : nullptr;
+  u.WB = c->WB_out ? c->WB_out + off : nullptr;
+  u.c = k;
+  return u;
+}
+
+// fused = true: each layer's dW GEMM applies the K-B update to its own weight and bias
+// blocks in its epilogue (G never reaches HBM); the caller then only bumps the version.
+// Safe per layer: dX_l (which reads WB_l) is issued before dW_l on the same stream and
+// no later task of this backward touches layer l again.
+static st_status backward_compute(st_ctx* c, int64_t mb, bool fused = false) {
+  const UpdateConsts kc = make_update_consts(c->lr, c->gamma, c->sF, c->sB, c->momentum);
   float* slot = c->stash + (size_t)(mb % c->S) * c->slot_elems;
   const float* Wh = c->WB;  // Eq. 4 with s_B (D5: re-predicted from the current state)
   const float* dZ = c->last_stage ? c->dlogits : c->recv_bwd;
@@ -477,7 +492,13 @@ static st_status backward_compute(st_ctx* c, int64_t mb) {
     }
     {
       Timed t(c, KC_GEMM_DW);
-      ST_TRY(gemm_dw(gargs(c, L), Ain, dZ, c->G + L.w_off, L.bias ? c->G + L.b_off : nullptr));
+      if (fused) {
+        UpdateArgs bu{};
+        if (L.bias) bu = block_update(c, L.b_off, kc);
+        ST_TRY(gemm_dw_update(gargs(c, L), Ain, dZ, block_update(c, L.w_off, kc), bu, c->G + L.w_off));
+      } else {
+        ST_TRY(gemm_dw(gargs(c, L), Ain, dZ, c->G + L.w_off, L.bias ? c->G + L.b_off : nullptr));
+      }
       c->launches += gemm_last_launches();
     }
     if (D) {
@@ -489,7 +510,7 @@ static st_status backward_compute(st_ctx* c, int64_t mb) {
 }
 
 static st_status run_task(st_ctx* c, const float* x_dev, const int32_t* y_dev, bool host_io = false,
-                          float* loss_host = nullptr) {
+                          float* loss_host = nullptr, bool fused_update = false) {
   if (c->pc >= c->program.size()) return set_error(ST_ERR_STATE, "stage %d: program finished", c->k);
   if (c->pending_update)
     return set_error(ST_ERR_STATE, "stage %d: predict_and_update must follow every backward", c->k);
@@ -507,8 +528,11 @@ static st_status run_task(st_ctx* c, const float* x_dev, const int32_t* y_dev, b
   if (t.dir == ST_FWD)
     ST_TRY(forward_compute(c, t.mb, x_dev, y_dev, host_io, loss_host));
   else {
-    ST_TRY(backward_compute(c, t.mb));
-    c->pending_update = true;
+    ST_TRY(backward_compute(c, t.mb, fused_update));
+    if (fused_update)
+      c->version += 1;  // the update already ran inside the dW epilogues
+    else
+      c->pending_update = true;
   }
   ST_TRY(comm_after_task(c, c->pc));
   c->pc++;
@@ -591,8 +615,7 @@ st_status ctx_step(st_ctx* c, const float* x_dev, const int32_t* y_dev, st_step_
   // a warm-up F is followed by another F; a steady F by its paired B; cooldown is B alone
   if (c->pc < c->program.size() && c->program[c->pc].dir == ST_BWD) {
     const Task b = c->program[c->pc];
-    ST_TRY(run_task(c, nullptr, nullptr));
-    ST_TRY(ctx_update(c));
+    ST_TRY(run_task(c, nullptr, nullptr, false, nullptr, true));
     z.ops_run += 2;
     z.ran_backward = (int32_t)b.mb;
   }
@@ -616,8 +639,7 @@ st_status ctx_run(st_ctx* c, int64_t M, const float* xs, const int32_t* ys, floa
   while (c->pc < c->program.size()) {
     const Task t = c->program[c->pc];
     float* lh = (host_io && losses_host && c->last_stage && t.dir == ST_FWD) ? losses_host + t.mb : nullptr;
-    ST_TRY(run_task(c, x_of(c, xs, t.mb), y_of(c, ys, t.mb), host_io, lh));
-    if (t.dir == ST_BWD) ST_TRY(ctx_update(c));
+    ST_TRY(run_task(c, x_of(c, xs, t.mb), y_of(c, ys, t.mb), host_io, lh, true));
   }
   if (losses_host && c->last_stage && M > 0) {
     if (!host_io)

@@ -14,6 +14,8 @@ st_status tc_dx(const GemmArgs& g, const float* dZ, const float* W, const float*
 st_status tc_dw(const GemmArgs& g, const float* X, const float* dZ, float* G, float* gb);
 int64_t tc_workspace_bytes(int B, int max_in, int max_out);
 int tc_last_launches();
+bool tc_dw_fusable(const GemmArgs& g, const float* X, const float* dZ);
+st_status tc_dw_update(const GemmArgs& g, const float* X, const float* dZ, const UpdateArgs& w, const UpdateArgs& b);
 int simt_last_launches();
 
 static thread_local int g_last_launches = 0;
@@ -63,6 +65,25 @@ st_status gemm_dw(const GemmArgs& g, const float* X, const float* dZ, float* G, 
   st_status s = tc_dw(g, X, dZ, G, gb);
   g_last_launches = tc_last_launches();
   return s;
+}
+
+st_status gemm_dw_update(const GemmArgs& g, const float* X, const float* dZ, const UpdateArgs& w,
+                         const UpdateArgs& b, float* G_scratch) {
+  ST_TRY(check(g));
+  if (tc_dw_fusable(g, X, dZ)) {
+    st_status s = tc_dw_update(g, X, dZ, w, b);
+    g_last_launches = tc_last_launches();
+    return s;
+  }
+  // fallback (pitch not 16-byte aligned, SIMT mode, B > 128): G through HBM + K-B over the block
+  int launches = 0;
+  ST_TRY(gemm_dw(g, X, dZ, G_scratch, b.W ? G_scratch + (size_t)g.n_in * g.n_out : nullptr));
+  launches += g_last_launches;
+  const size_t n = (size_t)g.n_in * g.n_out + (b.W ? (size_t)g.n_out : 0);
+  // weight and bias blocks are contiguous in the arenas (S:106 layout)
+  ST_TRY(launch_update_predict(w.W, w.V, G_scratch, w.WF, w.WB, n, w.c, g.stream));
+  g_last_launches = launches + 1;
+  return ST_OK;
 }
 
 }  // namespace st

@@ -53,6 +53,7 @@ struct TcParams {
   int* counters;     // [tiles]
   uint32_t idesc;
   int dev_flags;     // development only (ST_GEMM_DEV_FLAGS): bit0 skip MMAs, bit1 skip converter math
+  UpdateArgs upd;    // dW fused with K-B: weight-block targets (index n·M + m, like out)
 };
 
 // ------------------------------------------------------------------ PTX helpers
@@ -99,6 +100,14 @@ __device__ __forceinline__ void tc_mma(uint32_t tmem_d, uint64_t adesc, uint64_t
 __device__ __forceinline__ void tc_commit(uint32_t bar) {
   asm volatile("tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.b64 [%0];" ::"r"(bar) : "memory");
 }
+__device__ __forceinline__ void tc_ld16_nowait(uint32_t taddr, uint32_t* r) {
+  asm volatile(
+      "tcgen05.ld.sync.aligned.32x32b.x16.b32 {%0,%1,%2,%3,%4,%5,%6,%7,%8,%9,%10,%11,%12,%13,%14,%15}, [%16];"
+      : "=r"(r[0]), "=r"(r[1]), "=r"(r[2]), "=r"(r[3]), "=r"(r[4]), "=r"(r[5]), "=r"(r[6]), "=r"(r[7]), "=r"(r[8]),
+        "=r"(r[9]), "=r"(r[10]), "=r"(r[11]), "=r"(r[12]), "=r"(r[13]), "=r"(r[14]), "=r"(r[15])
+      : "r"(taddr));
+}
+__device__ __forceinline__ void tc_wait_ld() { asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory"); }
 __device__ __forceinline__ void tc_ld16(uint32_t taddr, float* v) {
   uint32_t r[16];
   asm volatile(
@@ -607,41 +616,158 @@ __global__ void split_lo_kernel(const float4* __restrict__ x, float4* __restrict
 }
 
 
+
+// K-B update of J elements at o0 + j·stride (j < J) of one parameter block given their
+// gradients g[j]: all loads first (J·2 in flight), then the Eq. 1 / apply / Eq. 4 math.
+template <int J>
+__device__ __forceinline__ void update_cols(const UpdateArgs& u, size_t o0, size_t stride, const float* g) {
+  float w[J], v[J];
+  const float* pw = u.W + o0;
+  const float* pv = u.V + o0;
+#pragma unroll
+  for (int j = 0; j < J; ++j) {
+    w[j] = __ldcs(pw + j * stride);
+    v[j] = __ldcs(pv + j * stride);
+  }
+  float* qw = u.W + o0;
+  float* qv = u.V + o0;
+#pragma unroll
+  for (int j = 0; j < J; ++j) {
+    v[j] = __fmaf_rn(u.c.c_gamma, v[j], __fmul_rn(u.c.c_one, g[j]));
+    w[j] = __fmaf_rn(-u.c.c_eta, v[j], w[j]);
+    __stcs(qw + j * stride, w[j]);
+    __stcs(qv + j * stride, v[j]);
+  }
+  if (u.WF) {
+    float* qf = u.WF + o0;
+#pragma unroll
+    for (int j = 0; j < J; ++j) qf[j * stride] = __fmaf_rn(-u.c.c_f, v[j], w[j]);
+  }
+  if (u.WB) {
+    float* qb = u.WB + o0;
+#pragma unroll
+    for (int j = 0; j < J; ++j) qb[j * stride] = __fmaf_rn(-u.c.c_b, v[j], w[j]);
+  }
+}
+
+
+// 4×4 transpose inside each lane quad: lane r (= lane & 3) holds row r of a 4×4 block
+// (a[x] = M[r][x]); afterwards it holds column r (a[x] = M[x][r]).
+__device__ __forceinline__ void quad_transpose4(float* a, int r) {
+  float x0 = (r & 1) ? a[0] : a[1];
+  float x1 = (r & 1) ? a[2] : a[3];
+  x0 = __shfl_xor_sync(0xffffffffu, x0, 1);
+  x1 = __shfl_xor_sync(0xffffffffu, x1, 1);
+  if (r & 1) {
+    a[0] = x0;
+    a[2] = x1;
+  } else {
+    a[1] = x0;
+    a[3] = x1;
+  }
+  float y0 = (r & 2) ? a[0] : a[2];
+  float y1 = (r & 2) ? a[1] : a[3];
+  y0 = __shfl_xor_sync(0xffffffffu, y0, 2);
+  y1 = __shfl_xor_sync(0xffffffffu, y1, 2);
+  if (r & 2) {
+    a[0] = y0;
+    a[1] = y1;
+  } else {
+    a[2] = y0;
+    a[3] = y1;
+  }
+}
+
+// Fused K-B on a full 32-row × 16-column block held by one warp after tcgen05.ld
+// (lane = row m0w + lane, v[j] = g of column n0c + j). Each lane quad transposes so
+// that lane q·4 + r owns rows m0w + 4q .. +3 of columns n0c + 4i + r (i = 0..3):
+// float4 loads / stores, 4× fewer memory instructions than the lane-per-row form.
+__device__ __forceinline__ void update_block16_vec(const UpdateArgs& u, size_t M, int m0w, int n0c, int lane,
+                                                   float* v) {
+  const int q = lane >> 2, r = lane & 3;
+#pragma unroll
+  for (int i = 0; i < 4; ++i) quad_transpose4(v + 4 * i, r);
+  float4 w4[4], v4[4];
+  size_t o[4];
+#pragma unroll
+  for (int i = 0; i < 4; ++i) {
+    o[i] = (size_t)(n0c + 4 * i + r) * M + m0w + 4 * q;
+    w4[i] = __ldcs(reinterpret_cast<const float4*>(u.W + o[i]));
+    v4[i] = __ldcs(reinterpret_cast<const float4*>(u.V + o[i]));
+  }
+#pragma unroll
+  for (int i = 0; i < 4; ++i) {
+    float* g = v + 4 * i;
+    float* pw = reinterpret_cast<float*>(&w4[i]);
+    float* pv = reinterpret_cast<float*>(&v4[i]);
+#pragma unroll
+    for (int e = 0; e < 4; ++e) {
+      pv[e] = __fmaf_rn(u.c.c_gamma, pv[e], __fmul_rn(u.c.c_one, g[e]));
+      pw[e] = __fmaf_rn(-u.c.c_eta, pv[e], pw[e]);
+    }
+    __stcs(reinterpret_cast<float4*>(u.W + o[i]), w4[i]);
+    __stcs(reinterpret_cast<float4*>(u.V + o[i]), v4[i]);
+    if (u.WF) {
+      float4 f;
+      f.x = __fmaf_rn(-u.c.c_f, pv[0], pw[0]);
+      f.y = __fmaf_rn(-u.c.c_f, pv[1], pw[1]);
+      f.z = __fmaf_rn(-u.c.c_f, pv[2], pw[2]);
+      f.w = __fmaf_rn(-u.c.c_f, pv[3], pw[3]);
+      *reinterpret_cast<float4*>(u.WF + o[i]) = f;
+    }
+    if (u.WB) {
+      float4 f;
+      f.x = __fmaf_rn(-u.c.c_b, pv[0], pw[0]);
+      f.y = __fmaf_rn(-u.c.c_b, pv[1], pw[1]);
+      f.z = __fmaf_rn(-u.c.c_b, pv[2], pw[2]);
+      f.w = __fmaf_rn(-u.c.c_b, pv[3], pw[3]);
+      *reinterpret_cast<float4*>(u.WB + o[i]) = f;
+    }
+  }
+}
+
 // ============================================================================
 // FP32X3 / TF32 dW kernel (persistent): G = Xᵀ·dZ as Gᵀ tiles (M = out, N = in, K = B).
 //
 // K = batch is short (≤ 128 here), the output (one fp32 per parameter) dominates.
 // Each CTA walks a contiguous range of 128 × 128 output tiles in m-major order.
-// The A operand (dZᵀ rows of the current m-tile, hi + lo, all of K) stays resident
-// in smem and is reloaded only when m changes; B (X columns, hi + lo) streams
-// through a 3-stage ring in K-blocks of 32. Two TMEM accumulators (2 × 128 columns)
-// let the epilogue of tile t overlap the MMAs of tile t + 1. Both lo operands are
-// precomputed by split_lo_kernel (dZ and X are activation-sized).
+// The A operand (dZᵀ rows of the current m-tile, all of K) is staged once per m-tile
+// (TMA → smem), split by converter warps into hi / lo and kept RESIDENT IN TMEM
+// (A-from-TMEM MMA); B (X columns, hi + lo precomputed) streams through a 3-stage smem
+// ring. Keeping A out of smem holds the CTA at 160 KB of shared memory, which leaves
+// enough L1 for the epilogue's in-flight loads (tools/probe_tile_stream.cu: the same
+// stream runs at 5.4 TB/s with ≤ 160 KB of smem and 4.0 TB/s with 220 KB).
+// TMEM: accumulators [0, 256) (two buffers), A hi [256, 384), A lo [384, 512).
+// Epilogue: 16 warps in two groups, group g drains accumulator g (tiles local ≡ g mod 2);
+// with kUPD it applies the K-B update in place of storing G (float4 via quad transposes).
 // ============================================================================
-constexpr int DW_KMAX = 128;                       // resident-A capacity along K (= batch)
+constexpr int DW_KMAX = 128;                       // K (= batch) capacity of the resident A
 constexpr int DW_RB = 3;                           // B ring stages (hi + lo, 32 KB)
-constexpr int DW_THREADS = 192;
-constexpr int DW_A_BYTES = 2 * (DW_KMAX / BK) * TILE_BYTES;  // A hi + lo for K ≤ 128: 128 KB
+constexpr int DW_EPI_WARPS = 16;                   // 2 groups × 2 warps per TMEM lane quadrant
+constexpr int DW_CONV_WARPS = 4;
+constexpr int DW_THREADS = 64 + 32 * (DW_EPI_WARPS + DW_CONV_WARPS);
+constexpr int DW_A_BYTES = (DW_KMAX / BK) * TILE_BYTES;  // raw A staging: 64 KB
 constexpr int DW_B_STAGE = 2 * TILE_BYTES;
 constexpr int dw_smem_bytes() { return DW_A_BYTES + DW_RB * DW_B_STAGE + 1024 + 512; }
 
-template <bool kX3>
+template <bool kX3, bool kUPD>
 __global__ void __launch_bounds__(DW_THREADS, 1)
-    tc_dw_kernel(const __grid_constant__ CUtensorMap mapA, const __grid_constant__ CUtensorMap mapAlo,
-                 const __grid_constant__ CUtensorMap mapB, const __grid_constant__ CUtensorMap mapBlo, TcParams p,
-                 int m_tiles, int n_tiles) {
+    tc_dw_kernel(const __grid_constant__ CUtensorMap mapA, const __grid_constant__ CUtensorMap mapB,
+                 const __grid_constant__ CUtensorMap mapBlo, TcParams p, int m_tiles, int n_tiles) {
   extern __shared__ __align__(1024) uint8_t smem_raw[];
   char* smem = reinterpret_cast<char*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
-  char* Abuf = smem;                      // [hi: kb × 16 KB][lo: kb × 16 KB]
+  char* Astage = smem;
   char* ringB = smem + DW_A_BYTES;
   uint64_t* bars = reinterpret_cast<uint64_t*>(ringB + DW_RB * DW_B_STAGE);
-  const uint32_t a_full = smem_u32(bars);         // resident A loaded
-  const uint32_t a_empty = a_full + 8;            // MMAs of the previous m-tile done
-  const uint32_t b_full = a_empty + 8;            // [RB]
-  const uint32_t b_empty = b_full + 8 * DW_RB;    // [RB]
-  const uint32_t c_full = b_empty + 8 * DW_RB;    // [2] accumulator ready
-  const uint32_t c_empty = c_full + 16;           // [2] epilogue drained it
-  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(bars + 4 + 2 * DW_RB);
+  const uint32_t a_full = smem_u32(bars);          // A staging landed (TMA)
+  const uint32_t a_sfree = a_full + 8;             // converter done reading the staging (4 warps)
+  const uint32_t a_tfull = a_sfree + 8;            // A hi / lo written to TMEM (4 warps)
+  const uint32_t a_tempty = a_tfull + 8;           // MMAs on the old A done (commit)
+  const uint32_t b_full = a_tempty + 8;            // [RB]
+  const uint32_t b_empty = b_full + 8 * DW_RB;     // [RB]
+  const uint32_t c_full = b_empty + 8 * DW_RB;     // [2] accumulator ready
+  const uint32_t c_empty = c_full + 16;            // [2] epilogue group drained it (8 warps)
+  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(bars + 4 + 2 * DW_RB + 4);
 
   const int warp = threadIdx.x >> 5;
   const int lane = threadIdx.x & 31;
@@ -650,46 +776,46 @@ __global__ void __launch_bounds__(DW_THREADS, 1)
   const int t_end = (int)((long long)(blockIdx.x + 1) * tiles / gridDim.x);
   const int nkb = p.kb_total;  // K blocks (K ≤ 128)
   const int bn = p.bn;
+  const int conv_w0 = 2 + DW_EPI_WARPS;
 
   if (threadIdx.x == 0) {
     mbar_init(a_full, 1);
-    mbar_init(a_empty, 1);
+    mbar_init(a_sfree, DW_CONV_WARPS);
+    mbar_init(a_tfull, DW_CONV_WARPS);
+    mbar_init(a_tempty, 1);
     for (int s = 0; s < DW_RB; ++s) {
       mbar_init(b_full + 8 * s, 1);
       mbar_init(b_empty + 8 * s, 1);
     }
     for (int s = 0; s < 2; ++s) {
       mbar_init(c_full + 8 * s, 1);
-      mbar_init(c_empty + 8 * s, 4);
+      mbar_init(c_empty + 8 * s, DW_EPI_WARPS / 2);
     }
     asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
   }
   if (warp == 1) {
-    asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], 256;" ::"r"(smem_u32(tmem_slot)));
+    asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], 512;" ::"r"(smem_u32(tmem_slot)));
     asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;");
   }
   tc_fence_before();
   __syncthreads();
   tc_fence_after();
   const uint32_t tmem = *tmem_slot;
+  const uint32_t tA_hi = tmem + 256, tA_lo = tmem + 384;
 
   if (warp == 0) {
-    // ---------------- TMA producer: resident A per m-tile, B ring per tile × K-block
+    // ---------------- TMA producer: A staging per m-tile, B ring per tile × K-block
     if (lane == 0) {
       int cur_m = -1, a_loads = 0, it = 0;
       for (int t = t_begin; t < t_end; ++t) {
         const int m_t = t / n_tiles, n_t = t % n_tiles;
         if (m_t != cur_m) {
-          if (a_loads > 0) mbar_wait(a_empty, (a_loads - 1) & 1);
-          const uint32_t bytes = (uint32_t)((kX3 ? 2 : 1) * nkb * TILE_BYTES);
-          mbar_expect_tx(a_full, bytes);
+          mbar_wait(a_sfree, (a_loads & 1) ^ 1);
+          mbar_expect_tx(a_full, (uint32_t)(nkb * TILE_BYTES));
           for (int kb = 0; kb < nkb; ++kb) {
-            const uint32_t dA = smem_u32(Abuf + kb * TILE_BYTES);
+            const uint32_t dA = smem_u32(Astage + kb * TILE_BYTES);
 #pragma unroll
-            for (int c = 0; c < BM / 32; ++c) {
-              tma_load_2d(dA + c * 4096, &mapA, m_t * BM + 32 * c, kb * BK, a_full);
-              if (kX3) tma_load_2d(dA + (DW_KMAX / BK) * TILE_BYTES + c * 4096, &mapAlo, m_t * BM + 32 * c, kb * BK, a_full);
-            }
+            for (int c = 0; c < BM / 32; ++c) tma_load_2d(dA + c * 4096, &mapA, m_t * BM + 32 * c, kb * BK, a_full);
           }
           cur_m = m_t;
           ++a_loads;
@@ -710,14 +836,14 @@ __global__ void __launch_bounds__(DW_THREADS, 1)
       }
     }
   } else if (warp == 1) {
-    // ---------------- MMA issuer
+    // ---------------- MMA issuer: A (dZᵀ hi / lo) from TMEM, B (X hi / lo) from smem
     if (lane == 0) {
       int cur_m = -1, a_loads = 0, it = 0, local = 0;
       for (int t = t_begin; t < t_end; ++t, ++local) {
         const int m_t = t / n_tiles;
         if (m_t != cur_m) {
-          if (a_loads > 0) tc_commit(a_empty);  // all MMAs on the old A issued before this commit
-          mbar_wait(a_full, a_loads & 1);
+          if (a_loads > 0) tc_commit(a_tempty);  // every MMA on the old A has been issued
+          mbar_wait(a_tfull, a_loads & 1);
           cur_m = m_t;
           ++a_loads;
         }
@@ -729,15 +855,16 @@ __global__ void __launch_bounds__(DW_THREADS, 1)
           const int s = it % DW_RB;
           mbar_wait(b_full + 8 * s, (it / DW_RB) & 1);
           tc_fence_after();
-          const uint32_t a_hi = smem_u32(Abuf + kb * TILE_BYTES), a_lo = a_hi + (DW_KMAX / BK) * TILE_BYTES;
           const uint32_t b_hi = smem_u32(ringB + s * DW_B_STAGE), b_lo = b_hi + TILE_BYTES;
 #pragma unroll
           for (int kk = 0; kk < BK / 8; ++kk) {
+            if (p.dev_flags & 1) break;
             const uint32_t acc = (kb > 0 || kk > 0) ? 1u : 0u;
-            tc_mma(acc_t, desc_mnmajor(a_hi + kk * 1024), desc_mnmajor(b_hi + kk * 1024), p.idesc, acc);
+            const uint32_t ka = kb * BK + kk * 8;
+            tc_mma_ts(acc_t, tA_hi + ka, desc_mnmajor(b_hi + kk * 1024), p.idesc, acc);
             if (kX3) {
-              tc_mma(acc_t, desc_mnmajor(a_lo + kk * 1024), desc_mnmajor(b_hi + kk * 1024), p.idesc, 1u);
-              tc_mma(acc_t, desc_mnmajor(a_hi + kk * 1024), desc_mnmajor(b_lo + kk * 1024), p.idesc, 1u);
+              tc_mma_ts(acc_t, tA_lo + ka, desc_mnmajor(b_hi + kk * 1024), p.idesc, 1u);
+              tc_mma_ts(acc_t, tA_hi + ka, desc_mnmajor(b_lo + kk * 1024), p.idesc, 1u);
             }
           }
           tc_commit(b_empty + 8 * s);
@@ -745,27 +872,81 @@ __global__ void __launch_bounds__(DW_THREADS, 1)
         tc_commit(c_full + 8 * buf);
       }
     }
-  } else {
-    // ---------------- epilogue (warps 2..5): accumulator → G[n·M + m]
+  } else if (warp >= conv_w0) {
+    // ---------------- converter: staged dZᵀ (MN-major boxes) → TMEM hi / lo, once per m-tile
     const int quad = warp & 3;
-    int local = 0;
-    for (int t = t_begin; t < t_end; ++t, ++local) {
+    const int r = quad * 32 + lane;  // tile row (out index) = TMEM lane
+    int cur_m = -1, a_loads = 0;
+    for (int t = t_begin; t < t_end; ++t) {
+      const int m_t = t / n_tiles;
+      if (m_t == cur_m) continue;
+      cur_m = m_t;
+      mbar_wait(a_full, a_loads & 1);
+      mbar_wait(a_tempty, (a_loads & 1) ^ 1);
+      tc_fence_after();
+      for (int kb = 0; kb < nkb; ++kb) {
+        const char* box = Astage + kb * TILE_BYTES + (r >> 5) * 4096;
+        uint32_t hi[32], lo[32];
+#pragma unroll
+        for (int k = 0; k < 32; ++k) {
+          const float x = *reinterpret_cast<const float*>(box + k * 128 + ((((r & 31) >> 3) ^ (k & 3)) << 5) +
+                                                          (r & 7) * 4);
+          hi[k] = __float_as_uint(x);
+          lo[k] = __float_as_uint(lo_part(x));
+        }
+        const uint32_t lane_off = (uint32_t)(quad * 32) << 16;
+        tc_st32(tA_hi + lane_off + kb * BK, hi);
+        if (kX3) tc_st32(tA_lo + lane_off + kb * BK, lo);
+      }
+      asm volatile("tcgen05.wait::st.sync.aligned;" ::: "memory");
+      tc_fence_before();
+      __syncwarp();
+      if (lane == 0) {
+        mbar_arrive(a_sfree);
+        mbar_arrive(a_tfull);
+      }
+      ++a_loads;
+    }
+  } else {
+    // ---------------- epilogue (warps 2..17): accumulator → G[n·M + m], or (kUPD) the
+    // K-B update of W / V / WF / WB at the same index; g never leaves the chip.
+    const int quad = warp & 3;
+    const int group = (warp - 2) >> 3;       // accumulator / tile parity
+    const int half = ((warp - 2) >> 2) & 1;  // which 64 columns of the tile
+    int local = group;
+    for (int t = t_begin + group; t < t_end; t += 2, local += 2) {
       const int m_t = t / n_tiles, n_t = t % n_tiles;
-      const int buf = local & 1;
+      const int buf = group;
       mbar_wait(c_full + 8 * buf, (local >> 1) & 1);
       tc_fence_after();
       const int m = m_t * BM + quad * 32 + lane;
       const uint32_t trow = tmem + buf * BNMAX + ((uint32_t)(quad * 32) << 16);
       const int n0 = n_t * BNMAX;
-      for (int c = 0; c < bn; c += 16) {
+      const int cbeg = half * (BNMAX / 2);
+      const int cend = min(bn, cbeg + BNMAX / 2);
+      const bool full_tile = (n0 + cend <= p.N) && (m_t * BM + BM <= p.M);
+      for (int c = cbeg; c < cend; c += 16) {
+        if (p.dev_flags & 16) break;
+        uint32_t rr[16];
+        tc_ld16_nowait(trow + c, rr);
+        tc_wait_ld();
         float v[16];
-        tc_ld16(trow + c, v);
-        if (m < p.M) {
 #pragma unroll
-          for (int j = 0; j < 16; ++j) {
-            const int n = n0 + c + j;
-            if (n < p.N) __stcs(p.out + (size_t)n * p.M + m, v[j]);
+        for (int j = 0; j < 16; ++j) v[j] = __uint_as_float(rr[j]);
+        const size_t o0 = (size_t)(n0 + c) * p.M + m;  // element (n0 + c + j, m) at o0 + j·M
+        if (kUPD) {
+          const UpdateArgs& u = p.upd;
+          if (full_tile) {
+            update_block16_vec(u, (size_t)p.M, m_t * BM + quad * 32, n0 + c, lane, v);
+          } else if (m < p.M) {
+#pragma unroll
+            for (int j = 0; j < 16; ++j)
+              if (n0 + c + j < p.N) update_cols<1>(u, o0 + (size_t)j * p.M, 0, v + j);
           }
+        } else if (m < p.M) {
+#pragma unroll
+          for (int j = 0; j < 16; ++j)
+            if (n0 + c + j < p.N) __stcs(p.out + o0 + (size_t)j * p.M, v[j]);
         }
       }
       tc_fence_before();
@@ -778,7 +959,7 @@ __global__ void __launch_bounds__(DW_THREADS, 1)
   __syncthreads();
   if (warp == 1) {
     tc_fence_after();
-    asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, 256;" ::"r"(tmem));
+    asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, 512;" ::"r"(tmem));
   }
 }
 
@@ -1012,8 +1193,22 @@ st_status tc_dx(const GemmArgs& g, const float* dZ, const float* W, const float*
   return launch<EPI_DX, false, false>(g, g.n_in, g.B, g.n_out, ma, mb, D, mask, 0);
 }
 
-// dW: M = out, N = in, K = B
+// dW: M = out, N = in, K = B. upd != NULL: fused K-B update of the weight block
+// (and, via gb_upd, of the bias block) instead of writing G / gb.
+st_status tc_dw_impl(const GemmArgs& g, const float* X, const float* dZ, float* G, float* gb, const UpdateArgs* upd,
+                     const UpdateArgs* gb_upd);
 st_status tc_dw(const GemmArgs& g, const float* X, const float* dZ, float* G, float* gb) {
+  return tc_dw_impl(g, X, dZ, G, gb, nullptr, nullptr);
+}
+bool tc_dw_fusable(const GemmArgs& g, const float* X, const float* dZ) {
+  return aligned16(dZ) && g.n_out % 4 == 0 && aligned16(X) && g.n_in % 4 == 0 && get_encode() && g.B <= DW_KMAX &&
+         g.mode != ST_GEMM_SIMT;
+}
+st_status tc_dw_update(const GemmArgs& g, const float* X, const float* dZ, const UpdateArgs& w, const UpdateArgs& b) {
+  return tc_dw_impl(g, X, dZ, nullptr, nullptr, &w, b.W ? &b : nullptr);
+}
+st_status tc_dw_impl(const GemmArgs& g, const float* X, const float* dZ, float* G, float* gb, const UpdateArgs* upd,
+                     const UpdateArgs* gb_upd) {
   if (!tma_ok(dZ, g.n_out) || !tma_ok(X, g.n_in) || !get_encode()) {
     st_status s = simt_dw(g, X, dZ, G, gb);
     g_launches = simt_last_launches();
@@ -1027,18 +1222,17 @@ st_status tc_dw(const GemmArgs& g, const float* X, const float* dZ, float* G, fl
     float* dzlo = lo_base;
     float* xlo = lo_base + (((size_t)g.B * g.n_out + 63) / 64 * 64);
     int launches = 1;
+    (void)dzlo;
     if (x3) {
-      const size_t n4a = (size_t)g.B * g.n_out / 4, n4b = (size_t)g.B * g.n_in / 4;
-      split_lo_kernel<<<std::min<size_t>(4 * 148, (n4a + 255) / 256), 256, 0, g.stream>>>(
-          reinterpret_cast<const float4*>(dZ), reinterpret_cast<float4*>(dzlo), n4a);
+      const size_t n4b = (size_t)g.B * g.n_in / 4;
       split_lo_kernel<<<std::min<size_t>(4 * 148, (n4b + 255) / 256), 256, 0, g.stream>>>(
           reinterpret_cast<const float4*>(X), reinterpret_cast<float4*>(xlo), n4b);
       ST_CUDA_TRY(cudaGetLastError());
-      launches += 2;
+      launches += 1;
     }
-    CUtensorMap ma, malo, mb, mblo;
-    if (!make_map(&ma, dZ, g.n_out, g.B, g.n_out, 32, true) || !make_map(&malo, dzlo, g.n_out, g.B, g.n_out, 32, true) ||
-        !make_map(&mb, X, g.n_in, g.B, g.n_in, 32, true) || !make_map(&mblo, xlo, g.n_in, g.B, g.n_in, 32, true))
+    CUtensorMap ma, mb, mblo;
+    if (!make_map(&ma, dZ, g.n_out, g.B, g.n_out, 32, true) || !make_map(&mb, X, g.n_in, g.B, g.n_in, 32, true) ||
+        !make_map(&mblo, xlo, g.n_in, g.B, g.n_in, 32, true))
       return set_error(ST_ERR_CUDA, "cuTensorMapEncodeTiled failed (dW)");
     TcParams p{};
     p.M = g.n_out;
@@ -1048,18 +1242,25 @@ st_status tc_dw(const GemmArgs& g, const float* X, const float* dZ, float* G, fl
     p.splits = 1;
     p.bn = bn_for(g.n_in);
     p.out = G;
-    p.idesc = make_idesc(p.bn, true, true);
+    p.dev_flags = dev_flags();
+    if (upd) p.upd = *upd;
+    p.idesc = make_idesc(p.bn, false, true);  // A from TMEM, B MN-major
     const int mt = (g.n_out + BM - 1) / BM, nt = (g.n_in + BNMAX - 1) / BNMAX;
     const int grid = std::min(mt * nt, num_sms());
-    auto kern = x3 ? tc_dw_kernel<true> : tc_dw_kernel<false>;
-    static bool attr_set[2] = {false, false};
-    if (!attr_set[x3]) {
+    auto kern = upd ? (x3 ? tc_dw_kernel<true, true> : tc_dw_kernel<false, true>)
+                    : (x3 ? tc_dw_kernel<true, false> : tc_dw_kernel<false, false>);
+    static bool attr_set[4] = {false, false, false, false};
+    const int ai = (x3 ? 1 : 0) + (upd ? 2 : 0);
+    if (!attr_set[ai]) {
       ST_CUDA_TRY(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, dw_smem_bytes()));
-      attr_set[x3] = true;
+      attr_set[ai] = true;
     }
-    kern<<<grid, DW_THREADS, dw_smem_bytes(), g.stream>>>(ma, malo, mb, mblo, p, mt, nt);
+    kern<<<grid, DW_THREADS, dw_smem_bytes(), g.stream>>>(ma, mb, mblo, p, mt, nt);
     ST_CUDA_TRY(cudaGetLastError());
-    if (gb) {
+    if (gb_upd) {
+      ST_TRY(launch_bias_grad_update(dZ, g.B, g.n_out, *gb_upd, g.stream));
+      ++launches;
+    } else if (gb) {
       ST_TRY(launch_bias_grad(dZ, g.B, g.n_out, gb, g.stream));
       ++launches;
     }

@@ -49,10 +49,10 @@ template <bool kWF, bool kWB>
 __global__ void __launch_bounds__(kThreads) update_predict_kernel(float4* __restrict__ W, float4* __restrict__ V,
                                                                   const float4* __restrict__ G,
                                                                   float4* __restrict__ WF, float4* __restrict__ WB,
-                                                                  size_t n4, UpdateConsts c, float* __restrict__ Wt,
-                                                                  float* __restrict__ Vt, const float* __restrict__ Gt,
-                                                                  float* __restrict__ WFt, float* __restrict__ WBt,
-                                                                  int tail) {
+                                                                  size_t n4, UpdateConsts c, float* __restrict__ Ws,
+                                                                  float* __restrict__ Vs, const float* __restrict__ Gs,
+                                                                  float* __restrict__ WFs, float* __restrict__ WBs,
+                                                                  int head, size_t tail0, int tail) {
   const size_t stride = (size_t)gridDim.x * kThreads * kUnroll;
   for (size_t base = (size_t)blockIdx.x * kThreads * kUnroll + threadIdx.x; base < n4; base += stride) {
     float4 w[kUnroll], v[kUnroll], g[kUnroll], wf[kUnroll], wb[kUnroll];
@@ -80,15 +80,15 @@ __global__ void __launch_bounds__(kThreads) update_predict_kernel(float4* __rest
       }
     }
   }
-  // scalar tail (n % 4 elements) — one block handles it
-  if (blockIdx.x == 0 && threadIdx.x < tail) {
-    const int t = threadIdx.x;
-    float w = Wt[t], v = Vt[t], wf = 0.f, wb = 0.f;
-    upd1<kWF, kWB>(w, v, Gt[t], wf, wb, c);
-    Wt[t] = w;
-    Vt[t] = v;
-    if (kWF) WFt[t] = wf;
-    if (kWB) WBt[t] = wb;
+  // scalar head (to reach 16-byte alignment) and tail (n % 4) elements — block 0
+  if (blockIdx.x == 0 && (int)threadIdx.x < head + tail) {
+    const size_t t = (int)threadIdx.x < head ? (size_t)threadIdx.x : tail0 + (threadIdx.x - head);
+    float w = Ws[t], v = Vs[t], wf = 0.f, wb = 0.f;
+    upd1<kWF, kWB>(w, v, Gs[t], wf, wb, c);
+    Ws[t] = w;
+    Vs[t] = v;
+    if (kWF) WFs[t] = wf;
+    if (kWB) WBs[t] = wb;
   }
 }
 
@@ -114,29 +114,67 @@ int grid_for(size_t n4) {
 st_status launch_update_predict(float* W, float* V, const float* G, float* WF, float* WB, size_t n,
                                 const UpdateConsts& c, cudaStream_t s) {
   if (n == 0) return ST_OK;
-  const size_t n4 = n / 4;
-  const int tail = (int)(n % 4);
-  const size_t t0 = n4 * 4;
-  float* WFt = WF ? WF + t0 : nullptr;
-  float* WBt = WB ? WB + t0 : nullptr;
+  // W, V, G, WF, WB share their alignment (same offset into 256-byte aligned arenas, or
+  // 16-byte aligned raw buffers): peel up to 3 scalar elements to reach float4 alignment.
+  int head = (int)(((16 - ((uintptr_t)W & 15)) & 15) / 4);
+  if ((size_t)head > n) head = (int)n;
+  const size_t n4 = (n - head) / 4;
+  const int tail = (int)((n - head) % 4);
+  const size_t tail0 = head + n4 * 4;
   const int grid = grid_for(n4 ? n4 : 1);
-  auto W4 = reinterpret_cast<float4*>(W);
-  auto V4 = reinterpret_cast<float4*>(V);
-  auto G4 = reinterpret_cast<const float4*>(G);
-  auto F4 = reinterpret_cast<float4*>(WF);
-  auto B4 = reinterpret_cast<float4*>(WB);
+  auto W4 = reinterpret_cast<float4*>(W + head);
+  auto V4 = reinterpret_cast<float4*>(V + head);
+  auto G4 = reinterpret_cast<const float4*>(G + head);
+  auto F4 = WF ? reinterpret_cast<float4*>(WF + head) : nullptr;
+  auto B4 = WB ? reinterpret_cast<float4*>(WB + head) : nullptr;
   if (WF && WB)
-    update_predict_kernel<true, true><<<grid, kThreads, 0, s>>>(W4, V4, G4, F4, B4, n4, c, W + t0, V + t0, G + t0,
-                                                                WFt, WBt, tail);
+    update_predict_kernel<true, true><<<grid, kThreads, 0, s>>>(W4, V4, G4, F4, B4, n4, c, W, V, G, WF, WB, head,
+                                                                tail0, tail);
   else if (WF)
-    update_predict_kernel<true, false><<<grid, kThreads, 0, s>>>(W4, V4, G4, F4, B4, n4, c, W + t0, V + t0,
-                                                                 G + t0, WFt, WBt, tail);
+    update_predict_kernel<true, false><<<grid, kThreads, 0, s>>>(W4, V4, G4, F4, B4, n4, c, W, V, G, WF, WB, head,
+                                                                 tail0, tail);
   else if (WB)
-    update_predict_kernel<false, true><<<grid, kThreads, 0, s>>>(W4, V4, G4, F4, B4, n4, c, W + t0, V + t0,
-                                                                 G + t0, WFt, WBt, tail);
+    update_predict_kernel<false, true><<<grid, kThreads, 0, s>>>(W4, V4, G4, F4, B4, n4, c, W, V, G, WF, WB, head,
+                                                                 tail0, tail);
   else
-    update_predict_kernel<false, false><<<grid, kThreads, 0, s>>>(W4, V4, G4, F4, B4, n4, c, W + t0, V + t0,
-                                                                  G + t0, WFt, WBt, tail);
+    update_predict_kernel<false, false><<<grid, kThreads, 0, s>>>(W4, V4, G4, F4, B4, n4, c, W, V, G, WF, WB, head,
+                                                                  tail0, tail);
+  ST_CUDA_TRY(cudaGetLastError());
+  return ST_OK;
+}
+
+namespace {
+// g_b[o] = Σ_b dZ[b][o] (fixed order: 8 row groups, then a fixed combine), then
+// the same K-B arithmetic as update_predict_kernel on the bias entries.
+__global__ void __launch_bounds__(256) bias_grad_update_kernel(const float* __restrict__ dZ, int B, int n_out,
+                                                               UpdateArgs u) {
+  __shared__ float part[8][33];
+  const int tx = threadIdx.x & 31, ty = threadIdx.x >> 5;
+  const int o = blockIdx.x * 32 + tx;
+  float s = 0.f;
+  if (o < n_out)
+    for (int b = ty; b < B; b += 8) s += dZ[(size_t)b * n_out + o];
+  part[ty][tx] = s;
+  __syncthreads();
+  if (ty == 0 && o < n_out) {
+    float g = part[0][tx];
+#pragma unroll
+    for (int r = 1; r < 8; ++r) g += part[r][tx];
+    float w = u.W[o], v = u.V[o], wf = 0.f, wb = 0.f;
+    const float vn = __fmaf_rn(u.c.c_gamma, v, __fmul_rn(u.c.c_one, g));
+    const float wn = __fmaf_rn(-u.c.c_eta, vn, w);
+    if (u.WF) wf = __fmaf_rn(-u.c.c_f, vn, wn);
+    if (u.WB) wb = __fmaf_rn(-u.c.c_b, vn, wn);
+    u.W[o] = wn;
+    u.V[o] = vn;
+    if (u.WF) u.WF[o] = wf;
+    if (u.WB) u.WB[o] = wb;
+  }
+}
+}  // namespace
+
+st_status launch_bias_grad_update(const float* dZ, int B, int n_out, const UpdateArgs& u, cudaStream_t s) {
+  bias_grad_update_kernel<<<(n_out + 31) / 32, 256, 0, s>>>(dZ, B, n_out, u);
   ST_CUDA_TRY(cudaGetLastError());
   return ST_OK;
 }

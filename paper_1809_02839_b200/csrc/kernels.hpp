@@ -19,6 +19,18 @@ UpdateConsts make_update_consts(float lr, float gamma, int sF, int sB, int momen
 st_status launch_update_predict(float* W, float* V, const float* G, float* WF, float* WB, size_t n,
                                 const UpdateConsts& c, cudaStream_t s);
 
+// In-place K-B targets of one parameter block (a layer's weight matrix or bias):
+// pointers at the block's offset in the stage arenas; WF / WB NULL when aliased.
+struct UpdateArgs {
+  float* W;
+  float* V;
+  float* WF;
+  float* WB;
+  UpdateConsts c;
+};
+// g_b = Σ_b dZ[b][o] followed by the K-B update of the bias block (no G write).
+st_status launch_bias_grad_update(const float* dZ, int B, int n_out, const UpdateArgs& u, cudaStream_t s);
+
 // ---- GEMMs of a dense stage (row-major fp32 buffers) ---------------------------
 // fwd: Z[B×out] = X[B×in]·W[in×out] + b, optional ReLU
 // dX : D[B×in]  = (dZ[B×out]·Wᵀ) ⊙ 1[mask > 0] (mask may be null)
@@ -34,6 +46,11 @@ int64_t gemm_workspace_bytes(int B, int max_in, int max_out);
 st_status gemm_fwd(const GemmArgs& g, const float* X, const float* W, const float* bias, float* Z, int relu);
 st_status gemm_dx(const GemmArgs& g, const float* dZ, const float* W, const float* mask, float* D);
 st_status gemm_dw(const GemmArgs& g, const float* X, const float* dZ, float* G, float* gb);
+// dW fused with the K-B update (NEXT-3): g = Xᵀ·dZ never reaches HBM;
+// the epilogue applies Eq. 1 + apply + predictions to the weight block `w` and the
+// bias block `b` (b.W == NULL: no bias). G_scratch is used only by the fallback path.
+st_status gemm_dw_update(const GemmArgs& g, const float* X, const float* dZ, const UpdateArgs& w,
+                         const UpdateArgs& b, float* G_scratch);
 // number of kernel launches the last gemm_* call issued on this thread
 int gemm_last_launches();
 

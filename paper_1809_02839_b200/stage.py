@@ -183,6 +183,22 @@ def gemm_raw(op: int, mode: int, B: int, n_in: int, n_out: int, a: torch.Tensor,
                           1 if relu else 0, _ptr(work), ctypes.c_void_p(st.cuda_stream)))
 
 
+def dw_update_raw(mode: int, X: torch.Tensor, dZ: torch.Tensor, W: torch.Tensor, V: torch.Tensor,
+                  WF: Optional[torch.Tensor], WB: Optional[torch.Tensor], lr: float, gamma: float, sF: int, sB: int,
+                  momentum: int = L.ST_MOMENTUM_EMA, work: Optional[torch.Tensor] = None,
+                  G_scratch: Optional[torch.Tensor] = None, stream: Optional[torch.cuda.Stream] = None) -> None:
+    """Fused dW + K-B update on one layer block (W, V, WF, WB: in·out + out fp32)."""
+    B, n_in = X.shape
+    n_out = dZ.shape[1]
+    st = stream or torch.cuda.current_stream(X.device)
+    if work is None:
+        work = torch.empty(int(lib.st_gemm_workspace_bytes(B, n_in, n_out)), dtype=torch.uint8, device=X.device)
+    if G_scratch is None:
+        G_scratch = torch.empty_like(W)
+    check(lib.st_dw_update_raw(mode, B, n_in, n_out, _ptr(X), _ptr(dZ), _ptr(W), _ptr(V), _ptr(WF), _ptr(WB), lr,
+                               gamma, sF, sB, momentum, _ptr(G_scratch), _ptr(work), ctypes.c_void_p(st.cuda_stream)))
+
+
 def softmax_ce_raw(logits: torch.Tensor, labels: torch.Tensor, loss: torch.Tensor, dlogits: torch.Tensor,
                    stream: Optional[torch.cuda.Stream] = None) -> None:
     B, C = logits.shape

@@ -151,3 +151,39 @@ def test_softmax_ce_vs_oracle(st, B, C):
     l64, d64 = O.loss_and_grad("softmax_ce", Z.astype(np.float64), y)
     assert loss.item() == pytest.approx(l64, rel=2e-6)
     np.testing.assert_allclose(d.cpu().numpy(), d64, rtol=1e-5, atol=1e-7 / B)
+
+
+@pytest.mark.parametrize("mode", ["fp32x3", "simt"])
+@pytest.mark.parametrize("B,n_in,n_out,sF,sB", [(128, 1024, 512, 0, 0), (32, 784, 256, 3, 1), (7, 264, 136, 2, 2),
+                                                (64, 256, 10, 1, 0), (128, 384, 640, 5, 2)])
+def test_dw_update_fused_vs_fp64(st, mode, B, n_in, n_out, sF, sB):
+    """dW fused with the K-B update (the st_run path): compare W, V, WF, WB with the
+    fp64 formulas applied to g = [Xᵀ·dZ ; Σ_b dZ] (Eq. 1, D1 apply, Eq. 4)."""
+    rng = np.random.default_rng(n_in + n_out + B)
+    dev = torch.device("cuda", 0)
+    P = n_in * n_out + n_out
+    X = rng.standard_normal((B, n_in)).astype(np.float32)
+    dZ = (rng.standard_normal((B, n_out)) / B).astype(np.float32)
+    W = rng.standard_normal(P).astype(np.float32)
+    V = (0.1 * rng.standard_normal(P)).astype(np.float32)
+    lr, gamma = 0.05, 0.9
+    t = lambda a: torch.from_numpy(a.copy()).to(dev)
+    tW, tV = t(W), t(V)
+    tF = torch.full((P,), 7.0, device=dev) if sF > 0 else None
+    tB = torch.full((P,), 9.0, device=dev) if (sB > 0 and sB != sF) else None
+    st.dw_update_raw(MODES[mode], t(X), t(dZ), tW, tV, tF, tB, lr, gamma, sF, sB)
+    torch.cuda.synchronize()
+    g = np.concatenate([(X.astype(np.float64).T @ dZ.astype(np.float64)).ravel(), dZ.astype(np.float64).sum(0)])
+    v64 = 0.9 * V.astype(np.float64) + 0.1 * g
+    w64 = W.astype(np.float64) - lr * v64
+    scale_g = np.concatenate([(np.abs(X.astype(np.float64)).T @ np.abs(dZ.astype(np.float64))).ravel(),
+                              np.abs(dZ.astype(np.float64)).sum(0)])
+    tol_v = 0.1 * 1e-5 * scale_g + 2e-7 * np.abs(v64) + 1e-30
+    assert np.all(np.abs(tV.cpu().numpy() - v64) <= tol_v)
+    assert np.all(np.abs(tW.cpu().numpy() - w64) <= lr * tol_v + 2e-7 * np.abs(w64))
+    if tF is not None:
+        ref = O.predict(w64, v64, sF, lr)
+        assert np.all(np.abs(tF.cpu().numpy() - ref) <= (sF + 1) * lr * tol_v + 4e-7 * np.abs(ref))
+    if tB is not None:
+        ref = O.predict(w64, v64, sB, lr)
+        assert np.all(np.abs(tB.cpu().numpy() - ref) <= (sB + 1) * lr * tol_v + 4e-7 * np.abs(ref))

@@ -192,7 +192,33 @@ def test_kernel_launch_accounting_and_profile(st):
     n0 = s.kernel_launches()
     s.run(4, torch.from_numpy(X).to(s.device), torch.from_numpy(Y).to(s.device))
     prof = s.profile()
-    assert prof["update"][1] == 4 and prof["gemm_fwd"][1] == 8 and prof["gemm_dw"][1] == 8
-    assert prof["update"][0] > 0
+    # st_run fuses the K-B update into each layer's dW (no standalone update launches)
+    assert prof["update"][1] == 0 and prof["gemm_fwd"][1] == 8 and prof["gemm_dw"][1] == 8
+    assert prof["gemm_dw"][0] > 0
     assert s.kernel_launches() - n0 >= 4 * (1 + 2 + 1 + 2 + 2)
     s.close()
+
+
+def test_fused_and_unfused_update_paths_agree(st):
+    """st_run (K-B fused into the dW epilogues) and the verb path (st_stage_backward
+    writes G, st_predict_and_update runs K-B) give the same weights bit for bit."""
+    model = sd.mlp([784, 256, 128, 10], cuts=[])
+    M, B, lr = 5, 64, 0.05
+    w0, X, Y = sd.parity_inputs(model, M, B, 11)
+    (a,) = build_pipeline(model, B, lr, gemm=gemm_mode(st), max_mb=M)
+    (b,) = build_pipeline(model, B, lr, gemm=gemm_mode(st), max_mb=M)
+    a.set_params(w0[0])
+    b.set_params(w0[0])
+    xs = torch.from_numpy(X).to(a.device)
+    ys = torch.from_numpy(Y).to(a.device)
+    a.run(M, xs, ys)
+    for i in range(M):
+        b.forward(i, xs[i], ys[i])
+        b.backward(i)
+        b.predict_and_update()
+    Wa, Va, _ = a.get_params()
+    Wb, Vb, _ = b.get_params()
+    np.testing.assert_array_equal(Wa, Wb)
+    np.testing.assert_array_equal(Va, Vb)
+    a.close()
+    b.close()

@@ -11,6 +11,19 @@ def t_op(op, mode, B, n_in, n_out, reps=10):
     dZ = torch.randn(B, n_out, device=dev)
     bias = torch.randn(n_out, device=dev)
     work = torch.zeros(int(st._lib.lib.st_gemm_workspace_bytes(B, n_in, n_out)), dtype=torch.uint8, device=dev)
+    if op == 3:
+        Wb = torch.randn(n_in * n_out + n_out, device=dev) * 0.01
+        Vb = torch.zeros_like(Wb)
+        Gs = torch.empty_like(Wb)
+        f = lambda: st.dw_update_raw(mode, X, dZ, Wb, Vb, None, None, 1e-3, 0.9, 0, 0, work=work, G_scratch=Gs)
+        f(); torch.cuda.synchronize()
+        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        torch.cuda._sleep(50_000_000)
+        e0.record()
+        for _ in range(reps): f()
+        e1.record(); torch.cuda.synchronize()
+        us = e0.elapsed_time(e1) * 1e3 / reps
+        return us, 2.0 * B * n_in * n_out / us / 1e6, 16.0 * n_in * n_out / us / 1e3
     if op == 0: args = (X, W, bias, None, torch.empty(B, n_out, device=dev))
     elif op == 1: args = (dZ, W, X, None, torch.empty(B, n_in, device=dev))
     else: args = (X, dZ, None, torch.empty(n_out, device=dev), torch.empty(n_in, n_out, device=dev))
@@ -27,9 +40,9 @@ def t_op(op, mode, B, n_in, n_out, reps=10):
     return us, flops / us / 1e6, byts / us / 1e3
 
 if __name__ == "__main__":
-    shapes = [(128, 8192, 8192), (128, 784, 8192), (128, 8192, 10)]
+    shapes = [(128, 8192, 8192)] + ([(128, 784, 8192), (128, 8192, 10)] if "--all" in sys.argv else [])
     for (B, i, o) in shapes:
         for mode, mname in ((0, "fp32x3"), (1, "tf32")):
-            for op, oname in ((0, "fwd"), (1, "dX"), (2, "dW")):
+            for op, oname in ((0, "fwd"), (1, "dX"), (2, "dW"), (3, "dWU")):
                 us, tf, gbs = t_op(op, mode, B, i, o)
                 print(f"{oname:3s} {mname:6s} B={B} in={i} out={o}: {us:8.1f} us  {tf:7.1f} TFLOP/s  weight-bytes {gbs:7.1f} GB/s")
