@@ -100,62 +100,155 @@ def stage_program(N: int, k: int, M: int) -> List[Tuple[int, int]]:
 # Dense stage forward / backward (§2.1; SPEC nn S:115-145)
 # --------------------------------------------------------------------------
 
-def unpack_stage(layers, flat: np.ndarray) -> List[Tuple[np.ndarray, np.ndarray]]:
-    """Stage flat layout: per layer W [in×out] row-major then b [out]."""
+def unpack_stage(layers, flat: np.ndarray):
+    """Stage flat layout: per layer, in order —
+    dense: W [in×out] row-major, then b [out] (if bias);
+    embed: E [vocab×dim];
+    lstm : W_ih [in×4h], W_hh [h×4h], b [4h]."""
     out, off = [], 0
+
+    def take(n, shape):
+        nonlocal off
+        a = flat[off:off + n].reshape(shape)
+        off += n
+        return a
+
     for L in layers:
-        W = flat[off:off + L.n_in * L.n_out].reshape(L.n_in, L.n_out)
-        off += L.n_in * L.n_out
-        if L.bias:
-            b = flat[off:off + L.n_out]
-            off += L.n_out
+        kind = getattr(L, "kind", "dense")
+        if kind == "embed":
+            out.append((take(L.n_in * L.n_out, (L.n_in, L.n_out)),))
+        elif kind == "lstm":
+            h = L.n_out
+            out.append((take(L.n_in * 4 * h, (L.n_in, 4 * h)), take(h * 4 * h, (h, 4 * h)), take(4 * h, (4 * h,))))
         else:
-            b = None
-        out.append((W, b))
+            W = take(L.n_in * L.n_out, (L.n_in, L.n_out))
+            b = take(L.n_out, (L.n_out,)) if L.bias else None
+            out.append((W, b))
     assert off == flat.size, (off, flat.size)
     return out
 
 
-def pack_stage(layers, parts: Sequence[Tuple[np.ndarray, np.ndarray]]) -> np.ndarray:
+def pack_stage(layers, parts) -> np.ndarray:
     chunks = []
-    for L, (gW, gb) in zip(layers, parts):
-        chunks.append(gW.reshape(-1))
-        if L.bias:
-            chunks.append(gb)
+    for L, part in zip(layers, parts):
+        for a in part:
+            if a is not None:
+                chunks.append(np.asarray(a).reshape(-1))
     return np.concatenate(chunks) if chunks else np.zeros(0)
 
 
-def stage_forward(layers, flat: np.ndarray, A: np.ndarray):
-    """Per layer: Z = A·W + b; A' = ReLU(Z) (identity when act == 'none').
-    Returns (stage output, stash of (A_in, Z) per layer)."""
+def _sigmoid(x):
+    return 1.0 / (1.0 + np.exp(-x))
+
+
+def lstm_forward(W_ih, W_hh, b, X, T):
+    """LSTM over T time-major steps of X [T·B × in] (reading D18):
+    G_t = X_t·W_ih + h_{t−1}·W_hh + b; i, f, o = σ(·), g = tanh(·) (order i, f, g, o);
+    c_t = f⊙c_{t−1} + i⊙g; h_t = o⊙tanh(c_t); h_{−1} = c_{−1} = 0."""
+    B = X.shape[0] // T
+    H = W_hh.shape[0]
+    Gx = X @ W_ih + b
+    h = np.zeros((B, H))
+    c = np.zeros((B, H))
+    outs, cache = [], []
+    for t in range(T):
+        G = Gx[t * B:(t + 1) * B] + h @ W_hh
+        i, f, g, o = _sigmoid(G[:, :H]), _sigmoid(G[:, H:2 * H]), np.tanh(G[:, 2 * H:3 * H]), _sigmoid(G[:, 3 * H:])
+        c_prev, h_prev = c, h
+        c = f * c_prev + i * g
+        h = o * np.tanh(c)
+        cache.append((i, f, g, o, c_prev, c, h_prev))
+        outs.append(h)
+    return np.concatenate(outs, axis=0), cache
+
+
+def lstm_backward(W_ih, W_hh, X, cache, dOut, T, need_dX=True):
+    """Backpropagation through time for lstm_forward; returns (gW_ih, gW_hh, gb, dX)."""
+    B = X.shape[0] // T
+    H = W_hh.shape[0]
+    dG_all = np.zeros((T * B, 4 * H))
+    dh_next = np.zeros((B, H))
+    dc_next = np.zeros((B, H))
+    gW_hh = np.zeros_like(W_hh)
+    for t in range(T - 1, -1, -1):
+        i, f, g, o, c_prev, c, h_prev = cache[t]
+        dh = dOut[t * B:(t + 1) * B] + dh_next
+        tc = np.tanh(c)
+        dc = dc_next + dh * o * (1.0 - tc * tc)
+        do = dh * tc
+        di = dc * g
+        dg = dc * i
+        df = dc * c_prev
+        dG = np.concatenate([di * i * (1 - i), df * f * (1 - f), dg * (1 - g * g), do * o * (1 - o)], axis=1)
+        dG_all[t * B:(t + 1) * B] = dG
+        gW_hh += h_prev.T @ dG
+        dh_next = dG @ W_hh.T
+        dc_next = dc * f
+    gW_ih = X.T @ dG_all
+    gb = dG_all.sum(axis=0)
+    dX = dG_all @ W_ih.T if need_dX else None
+    return gW_ih, gW_hh, gb, dX
+
+
+def stage_forward(layers, flat: np.ndarray, A, T: int = 1):
+    """Per layer: dense Z = A·W + b, A' = ReLU(Z) (identity when act ==
+    'none'); embed A' = E[tokens]; lstm A' = lstm_forward(A). Activations are
+    [T·B × width], time-major. Returns (stage output, stash per layer)."""
     stash = []
-    for L, (W, b) in zip(layers, unpack_stage(layers, flat)):
-        Z = A @ W
-        if b is not None:
-            Z = Z + b
-        stash.append((A, Z))
-        A = np.maximum(Z, 0.0) if L.act == "relu" else Z
+    for L, prm in zip(layers, unpack_stage(layers, flat)):
+        kind = getattr(L, "kind", "dense")
+        if kind == "embed":
+            (E,) = prm
+            tok = np.asarray(A).astype(np.int64).reshape(-1)
+            stash.append((tok,))
+            A = E[tok]
+        elif kind == "lstm":
+            W_ih, W_hh, b = prm
+            out, cache = lstm_forward(W_ih, W_hh, b, A, T)
+            stash.append((A, cache))
+            A = out
+        else:
+            W, b = prm
+            Z = A @ W
+            if b is not None:
+                Z = Z + b
+            stash.append((A, Z))
+            A = np.maximum(Z, 0.0) if L.act == "relu" else Z
     return A, stash
 
 
-def stage_backward(layers, flat: np.ndarray, stash, dA_out: np.ndarray, need_dA_in: bool = True):
-    """Reverse layers: dZ = dA ⊙ 1[Z>0] (D12: ReLU'(0)=0); g_W = Aᵀ·dZ;
-    g_b = Σ_rows dZ; dA_prev = dZ·Wᵀ.  Returns (flat gradient, dA_in or None)."""
+def stage_backward(layers, flat: np.ndarray, stash, dA_out: np.ndarray, need_dA_in: bool = True, T: int = 1):
+    """Reverse layers. dense: dZ = dA ⊙ 1[Z>0] (D12: ReLU'(0)=0); g_W = Aᵀ·dZ;
+    g_b = Σ_rows dZ; dA_prev = dZ·Wᵀ. embed: g_E[token] += dA rows. lstm: BPTT.
+    Returns (flat gradient, dA_in or None)."""
     params = unpack_stage(layers, flat)
     grads = [None] * len(layers)
     dA = dA_out
     for li in range(len(layers) - 1, -1, -1):
         L = layers[li]
-        W, b = params[li]
-        A_in, Z = stash[li]
-        dZ = dA * (Z > 0.0) if L.act == "relu" else dA
-        gW = A_in.T @ dZ
-        gb = dZ.sum(axis=0) if L.bias else None
-        grads[li] = (gW, gb)
-        if li > 0 or need_dA_in:
-            dA = dZ @ W.T
-        else:
+        kind = getattr(L, "kind", "dense")
+        need = li > 0 or need_dA_in
+        if kind == "embed":
+            (E,) = params[li]
+            (tok,) = stash[li]
+            gE = np.zeros_like(E)
+            np.add.at(gE, tok, dA)
+            grads[li] = (gE,)
             dA = None
+        elif kind == "lstm":
+            W_ih, W_hh, b = params[li]
+            X, cache = stash[li]
+            gW_ih, gW_hh, gb, dX = lstm_backward(W_ih, W_hh, X, cache, dA, T, need)
+            grads[li] = (gW_ih, gW_hh, gb)
+            dA = dX
+        else:
+            W, b = params[li]
+            A_in, Z = stash[li]
+            dZ = dA * (Z > 0.0) if L.act == "relu" else dA
+            gW = A_in.T @ dZ
+            gb = dZ.sum(axis=0) if L.bias else None
+            grads[li] = (gW, gb)
+            dA = dZ @ W.T if need else None
     return pack_stage(layers, grads), dA
 
 
@@ -227,6 +320,7 @@ def run(model, W0: Sequence[np.ndarray], X: np.ndarray, Y: np.ndarray, eta: floa
     test can show that)."""
     N = model.num_stages
     M = X.shape[0]
+    T = getattr(model, "seq_len", 1)
     W = [np.array(w, dtype=np.float64, copy=True) for w in W0]
     V = [np.zeros_like(w) for w in W]
     version = [0] * N
@@ -255,8 +349,11 @@ def run(model, W0: Sequence[np.ndarray], X: np.ndarray, Y: np.ndarray, eta: floa
         W_hat = predict(W[k], V[k], s, eta)
         trace[k].append(Event(k, pc[k], d, i, version[k], s))
         if d == FWD:
-            A_in = X[i].astype(np.float64) if k == 0 else act.pop((k - 1, i))
-            out, st = stage_forward(layers, W_hat, A_in)
+            if k == 0:
+                A_in = X[i] if getattr(layers[0], "kind", "dense") == "embed" else X[i].astype(np.float64)
+            else:
+                A_in = act.pop((k - 1, i))
+            out, st = stage_forward(layers, W_hat, A_in, T)
             stash[(k, i)] = st
             if k == N - 1:
                 losses[i], dlogits[i] = loss_and_grad(model.loss, out, Y[i])
@@ -264,7 +361,7 @@ def run(model, W0: Sequence[np.ndarray], X: np.ndarray, Y: np.ndarray, eta: floa
                 act[(k, i)] = out
         else:
             dA = dlogits.pop(i) if k == N - 1 else grad.pop((k + 1, i))
-            g, dA_in = stage_backward(layers, W_hat, stash.pop((k, i)), dA, need_dA_in=(k > 0))
+            g, dA_in = stage_backward(layers, W_hat, stash.pop((k, i)), dA, need_dA_in=(k > 0), T=T)
             if k > 0:
                 grad[(k, i)] = dA_in
             # Update after each B: Eq. 1, D1 apply, version += 1.

@@ -25,18 +25,32 @@ import numpy as np
 RELU = "relu"
 NONE = "none"
 
+DENSE = "dense"
+EMBED = "embed"
+LSTM = "lstm"
+
 
 @dataclasses.dataclass(frozen=True)
 class Layer:
-    """One dense layer `Z = A·W + b`, `A' = act(Z)`; W stored [in×out] row-major."""
+    """One layer of the chain.
+
+    dense: `Z = A·W + b`, `A' = act(Z)`; W [in×out] row-major, then b [out].
+    embed: token ids → rows of E [n_in = vocab × n_out = dim] (params: E only).
+    lstm : input n_in, hidden n_out; params W_ih [in×4h], W_hh [h×4h], b [4h]
+           (gate order i, f, g, o — reading D18)."""
 
     n_in: int
     n_out: int
     act: str = RELU
     bias: bool = True
+    kind: str = DENSE
 
     @property
     def n_params(self) -> int:
+        if self.kind == EMBED:
+            return self.n_in * self.n_out
+        if self.kind == LSTM:
+            return (self.n_in + self.n_out) * 4 * self.n_out + 4 * self.n_out
         return self.n_in * self.n_out + (self.n_out if self.bias else 0)
 
 
@@ -47,6 +61,7 @@ class Model:
     layers: Tuple[Layer, ...]
     cuts: Tuple[int, ...]  # N-1 strictly increasing layer indices; stage k = [cuts[k-1], cuts[k])
     loss: str = "softmax_ce"  # or "half_mse" (App. C scalar chain)
+    seq_len: int = 1  # T: activations are [T·B × width], time-major rows (t·B + b)
 
     @property
     def num_stages(self) -> int:
@@ -111,6 +126,21 @@ def config_wide_fcn(num_stages: int, width: int = 8192, hidden_layers: int = 8) 
     return mlp(widths, cuts=even_cuts(len(widths) - 1, num_stages))
 
 
+def lstm_lm(vocab: int, hidden: int, layers: int, cuts: Sequence[int], seq_len: int) -> Model:
+    """Embedding → `layers` × LSTM(hidden) → dense softmax over the vocabulary
+    (BJ configs[2]; reading D18: untied embedding / softmax, h0 = c0 = 0 per mini-batch)."""
+    ls = [Layer(vocab, hidden, NONE, False, EMBED)]
+    ls += [Layer(hidden, hidden, NONE, True, LSTM) for _ in range(layers)]
+    ls += [Layer(hidden, vocab, NONE, True, DENSE)]
+    return Model(tuple(ls), tuple(int(c) for c in cuts), "softmax_ce", seq_len)
+
+
+def config_lstm_lm(num_stages: int = 4, vocab: int = 10000, hidden: int = 1500, seq_len: int = 35) -> Model:
+    """BJ configs[2]: 2-layer LSTM LM, hidden 1500, seq 35, vocab 10k; 4 stages
+    {Emb}{LSTM1}{LSTM2}{Softmax}."""
+    return lstm_lm(vocab, hidden, 2, even_cuts(4, num_stages), seq_len)
+
+
 def config_large_fcn(num_stages: int, width: int = 16384, hidden_layers: int = 16) -> Model:
     """BJ configs[4]: large FCN 16 × 16384."""
     widths = [784] + [width] * hidden_layers + [10]
@@ -121,18 +151,46 @@ def config_large_fcn(num_stages: int, width: int = 16384, hidden_layers: int = 1
 
 def glorot_params(model: Model, seed: int) -> List[np.ndarray]:
     """Per-stage flat float64 parameter vectors in the stage layout
-    (layer-major: W_l [in×out] row-major, then b_l [out])."""
+    (layer-major: W_l [in×out] row-major, then b_l [out]).
+    Embedding: U(-0.1, 0.1). LSTM: W_ih, W_hh Glorot over (in, 4h) / (h, 4h), b = 0."""
     rng = np.random.default_rng(seed)
     out = []
     for k in range(model.num_stages):
         parts = []
         for layer in model.stage_layers(k):
-            r = math.sqrt(6.0 / (layer.n_in + layer.n_out))
-            parts.append(rng.uniform(-r, r, size=layer.n_in * layer.n_out))
-            if layer.bias:
-                parts.append(np.zeros(layer.n_out))
+            if layer.kind == EMBED:
+                parts.append(rng.uniform(-0.1, 0.1, size=layer.n_in * layer.n_out))
+            elif layer.kind == LSTM:
+                h = layer.n_out
+                r1 = math.sqrt(6.0 / (layer.n_in + 4 * h))
+                r2 = math.sqrt(6.0 / (h + 4 * h))
+                parts.append(rng.uniform(-r1, r1, size=layer.n_in * 4 * h))
+                parts.append(rng.uniform(-r2, r2, size=h * 4 * h))
+                parts.append(np.zeros(4 * h))
+            else:
+                r = math.sqrt(6.0 / (layer.n_in + layer.n_out))
+                parts.append(rng.uniform(-r, r, size=layer.n_in * layer.n_out))
+                if layer.bias:
+                    parts.append(np.zeros(layer.n_out))
         out.append(np.concatenate(parts) if parts else np.zeros(0))
     return out
+
+
+def tokens(vocab: int, num_batches: int, batch: int, seq_len: int, seed: int,
+           dist: str = "zipf") -> Tuple[np.ndarray, np.ndarray]:
+    """Synthetic LM data: X int32 [M, T·B] input tokens (time-major, row t·B + b),
+    Y int32 [M, T·B] next-token targets. Zipf(1.0)-like over the vocabulary
+    (tokens uniform or Zipf), or uniform."""
+    rng = np.random.default_rng(seed)
+    if dist == "zipf":
+        p = 1.0 / np.arange(1, vocab + 1)
+        p /= p.sum()
+        seq = rng.choice(vocab, size=(num_batches, batch, seq_len + 1), p=p)
+    else:
+        seq = rng.integers(0, vocab, size=(num_batches, batch, seq_len + 1))
+    x = seq[:, :, :-1].transpose(0, 2, 1).reshape(num_batches, seq_len * batch)
+    y = seq[:, :, 1:].transpose(0, 2, 1).reshape(num_batches, seq_len * batch)
+    return x.astype(np.int32), y.astype(np.int32)
 
 
 def images_and_labels(

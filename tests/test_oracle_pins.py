@@ -397,3 +397,105 @@ def test_spectrain_differs_from_vanilla_and_staleness_witness():
     assert not np.allclose(np.concatenate(a.W), np.concatenate(b.W), rtol=1e-9)
     assert any(f.base_version != bb.base_version for f in b.trace[0] for bb in b.trace[0]
                if f.dir == O.FWD and bb.dir == O.BWD and f.mb == bb.mb)
+
+
+# ---------------------------------------------------------------- LSTM LM (a8, a9)
+
+def _torch_lm_loss(model, flat, x_tok, y_tok):
+    """The same LM with torch library modules (nn.Embedding, nn.LSTM with PyTorch's
+    i, f, g, o gate order, nn.Linear), fp64, time-major [T, B]."""
+    T = model.seq_len
+    B = x_tok.shape[0] // T
+    off = 0
+    a = None
+    for L in model.layers:
+        if L.kind == sd.EMBED:
+            E = flat[off:off + L.n_in * L.n_out].view(L.n_in, L.n_out)
+            off += L.n_in * L.n_out
+            a = torch.nn.functional.embedding(x_tok.long(), E)
+        elif L.kind == sd.LSTM:
+            h = L.n_out
+            W_ih = flat[off:off + L.n_in * 4 * h].view(L.n_in, 4 * h)
+            off += L.n_in * 4 * h
+            W_hh = flat[off:off + h * 4 * h].view(h, 4 * h)
+            off += h * 4 * h
+            b = flat[off:off + 4 * h]
+            off += 4 * h
+            out = torch._VF.lstm(a.view(T, B, L.n_in), (torch.zeros(1, B, h, dtype=a.dtype), torch.zeros(1, B, h, dtype=a.dtype)),
+                                    [W_ih.t(), W_hh.t(), b, torch.zeros_like(b)], True, 1, 0.0, False, False, False)[0]
+            a = out.reshape(T * B, h)
+        else:
+            W = flat[off:off + L.n_in * L.n_out].view(L.n_in, L.n_out)
+            off += L.n_in * L.n_out
+            z = a @ W
+            if L.bias:
+                z = z + flat[off:off + L.n_out]
+                off += L.n_out
+            a = torch.relu(z) if L.act == sd.RELU else z
+    return torch.nn.functional.cross_entropy(a, y_tok.long())
+
+
+@pytest.mark.parametrize("cuts", [[], [1, 2, 3], [2]])
+def test_lstm_lm_grads_equal_torch_lstm(cuts):
+    """Embedding / LSTM / softmax stages composed stage by stage
+    == torch's LSTM + autograd on the monolithic model (library routine)."""
+    model = sd.lstm_lm(vocab=13, hidden=6, layers=2, cuts=cuts, seq_len=4)
+    w = np.concatenate(sd.glorot_params(model, 3))
+    w = w + 0.05 * np.random.default_rng(4).standard_normal(w.size)  # non-zero biases
+    X, Y = sd.tokens(13, 1, 3, 4, seed=5)
+    flats, off = [], 0
+    for k in range(model.num_stages):
+        n = model.stage_params(k)
+        flats.append(w[off:off + n])
+        off += n
+    a, stashes = X[0], []
+    for k in range(model.num_stages):
+        a, st = O.stage_forward(model.stage_layers(k), flats[k], a, model.seq_len)
+        stashes.append(st)
+    loss, d = O.loss_and_grad("softmax_ce", a, Y[0])
+    grads = [None] * model.num_stages
+    for k in range(model.num_stages - 1, -1, -1):
+        grads[k], d = O.stage_backward(model.stage_layers(k), flats[k], stashes[k], d, need_dA_in=k > 0,
+                                       T=model.seq_len)
+    tw = torch.tensor(w, dtype=torch.float64, requires_grad=True)
+    tl = _torch_lm_loss(model, tw, torch.tensor(X[0]), torch.tensor(Y[0]))
+    tl.backward()
+    assert loss == pytest.approx(tl.item(), rel=1e-12)
+    np.testing.assert_allclose(np.concatenate(grads), tw.grad.numpy(), rtol=1e-10, atol=1e-13)
+
+
+def test_lstm_finite_differences():
+    model = sd.lstm_lm(vocab=7, hidden=3, layers=1, cuts=[], seq_len=3)
+    w = np.concatenate(sd.glorot_params(model, 9)) + 0.05
+    X, Y = sd.tokens(7, 1, 2, 3, seed=10, dist="uniform")
+
+    def f(wv):
+        out, _ = O.stage_forward(model.layers, wv, X[0], 3)
+        return O.loss_and_grad("softmax_ce", out, Y[0])[0]
+
+    out, st = O.stage_forward(model.layers, w, X[0], 3)
+    _, dz = O.loss_and_grad("softmax_ce", out, Y[0])
+    g, _ = O.stage_backward(model.layers, w, st, dz, need_dA_in=False, T=3)
+    h = 1e-6
+    for i in range(w.size):
+        e = np.zeros_like(w)
+        e[i] = h
+        fd = (f(w + e) - f(w - e)) / (2 * h)
+        assert abs(fd - g[i]) <= 1e-6 * max(1e-2, abs(g[i])) + 1e-9, (i, fd, g[i])
+
+
+def test_lstm_lm_pipeline_single_stage_equals_torch_sgd():
+    """N=1 SpecTrain on the LM == torch.optim.SGD(momentum=γ, dampening=γ) driving
+    torch's LSTM (zero momentum buffer)."""
+    model = sd.lstm_lm(vocab=11, hidden=5, layers=2, cuts=[], seq_len=3)
+    w0 = np.concatenate(sd.glorot_params(model, 21))
+    X, Y = sd.tokens(11, 4, 2, 3, seed=22)
+    res = O.run(model, [w0], X, Y, 0.1, 0.9)
+    tw = torch.tensor(w0, dtype=torch.float64, requires_grad=True)
+    opt = torch.optim.SGD([tw], lr=0.1, momentum=0.9, dampening=0.9)
+    opt.state[tw]["momentum_buffer"] = torch.zeros_like(tw)
+    for i in range(4):
+        opt.zero_grad()
+        _torch_lm_loss(model, tw, torch.tensor(X[i]), torch.tensor(Y[i])).backward()
+        opt.step()
+    np.testing.assert_allclose(res.W[0], tw.detach().numpy(), rtol=1e-10, atol=1e-13)
