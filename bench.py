@@ -44,7 +44,7 @@ def parse():
     p.add_argument("--steps", type=int, default=30)
     p.add_argument("--warmup", type=int, default=5)
     p.add_argument("--impl", default="ours", choices=["ours", "reference"])
-    p.add_argument("--workload", default="wide_fcn", choices=["wide_fcn", "large_fcn", "mlp", "deep_mlp"])
+    p.add_argument("--workload", default="wide_fcn", choices=["wide_fcn", "large_fcn", "mlp", "deep_mlp", "lstm_lm"])
     p.add_argument("--stages", type=int, default=0, help="pipeline depth (default = --gpus); >N only with N=1")
     p.add_argument("--gemm", default=DEFAULT_GEMM, choices=["fp32x3", "tf32", "simt"])
     p.add_argument("--pred", default="spectrain", choices=["spectrain", "none"])
@@ -62,6 +62,8 @@ def workload(name: str, S: int):
         return sd.config_large_fcn(S), 128, "large_fcn_784-16x16384-10_b128"
     if name == "deep_mlp":
         return sd.config_deep_mlp(S), 128, "deep_mlp_784-8x1024-10_b128"
+    if name == "lstm_lm":
+        return sd.config_lstm_lm(min(S, 4)), 128, "lstm_lm_v10k_h1500_2layer_t35_b128"
     return sd.mlp([784, 256, 256, 10], cuts=sd.even_cuts(3, S)), 32, "mlp_784-256-256-10_b32"
 
 
@@ -222,20 +224,26 @@ def run_ours(args):
     model, B, wname = workload(args.workload, S)
     gemm = {"fp32x3": st.ST_GEMM_FP32X3, "tf32": st.ST_GEMM_TF32, "simt": st.ST_GEMM_SIMT}[args.gemm]
     pred = st.ST_PRED_SPECTRAIN if args.pred == "spectrain" else st.ST_PRED_NONE
-    layers = [(l.n_in, l.n_out, st.ST_ACT_RELU if l.act == sd.RELU else st.ST_ACT_NONE, 1) for l in model.layers]
+    kinds = {sd.DENSE: st.ST_LAYER_DENSE, sd.EMBED: st.ST_LAYER_EMBED, sd.LSTM: st.ST_LAYER_LSTM}
+    layers = [(l.n_in, l.n_out, st.ST_ACT_RELU if l.act == sd.RELU else st.ST_ACT_NONE, 1 if l.bias else 0,
+               kinds[l.kind]) for l in model.layers]
+    T = model.seq_len
+    R = B * T
     M = max(args.steps, args.warmup, 1)
 
     if N > 1:
         obj = [st.nccl_id() if rank == 0 else None]
         dist.broadcast_object_list(obj, src=0)
         my_stages = [st.Stage(layers, model.cuts, rank, B, args.lr, 0.9, pred=pred, gemm=gemm,
-                              transport=st.ST_TRANSPORT_NCCL, device=local, max_minibatches=M, nccl_id=obj[0])]
+                              transport=st.ST_TRANSPORT_NCCL, device=local, max_minibatches=M, nccl_id=obj[0],
+                              seq_len=T)]
     elif S == 1:
         my_stages = [st.Stage(layers, model.cuts, 0, B, args.lr, 0.9, pred=pred, gemm=gemm,
-                              transport=st.ST_TRANSPORT_NCCL, device=local, max_minibatches=M)]
+                              transport=st.ST_TRANSPORT_NCCL, device=local, max_minibatches=M, seq_len=T)]
     else:
         my_stages = [st.Stage(layers, model.cuts, k, B, args.lr, 0.9, pred=pred, gemm=gemm,
-                              transport=st.ST_TRANSPORT_LOCAL, device=local, max_minibatches=M) for k in range(S)]
+                              transport=st.ST_TRANSPORT_LOCAL, device=local, max_minibatches=M, seq_len=T)
+                     for k in range(S)]
         st.connect_local(my_stages)
 
     # parameters: Glorot on device (bench-only, SURVEY §8(d) seeds), labels uniform
@@ -244,20 +252,30 @@ def run_ours(args):
     for s in my_stages:
         w = torch.empty(s.params, device=dev)
         off = 0
-        for (n_in, n_out, act, bias) in s.layers[model.stage_bounds(s.k)[0]:model.stage_bounds(s.k)[1]]:
-            r = (6.0 / (n_in + n_out)) ** 0.5
-            w[off:off + n_in * n_out].uniform_(-r, r, generator=g)
-            off += n_in * n_out
-            if bias:
-                w[off:off + n_out].zero_()
-                off += n_out
+        for L in model.stage_layers(s.k):
+            if L.kind == sd.EMBED:
+                w[off:off + L.n_params].uniform_(-0.1, 0.1, generator=g)
+            elif L.kind == sd.LSTM:
+                h = L.n_out
+                r1, r2 = (6.0 / (L.n_in + 4 * h)) ** 0.5, (6.0 / (5 * h)) ** 0.5
+                w[off:off + L.n_in * 4 * h].uniform_(-r1, r1, generator=g)
+                w[off + L.n_in * 4 * h:off + (L.n_in + h) * 4 * h].uniform_(-r2, r2, generator=g)
+                w[off + (L.n_in + h) * 4 * h:off + L.n_params].zero_()
+            else:
+                r = (6.0 / (L.n_in + L.n_out)) ** 0.5
+                w[off:off + L.n_in * L.n_out].uniform_(-r, r, generator=g)
+                w[off + L.n_in * L.n_out:off + L.n_params].zero_()
+            off += L.n_params
         s.set_params(w.cpu().numpy())
         del w
     n_in, n_cls = model.layers[0].n_in, model.layers[-1].n_out
     first = my_stages[0].is_first
     last = my_stages[-1].is_last
-    xs = torch.rand(M, B, n_in, device=dev, generator=g) if first else None
-    ys = torch.randint(0, n_cls, (M, B), device=dev, dtype=torch.int32, generator=g) if last else None
+    if model.layers[0].kind == sd.EMBED:
+        xs = torch.randint(0, n_in, (M, R), device=dev, dtype=torch.int32, generator=g) if first else None
+    else:
+        xs = torch.rand(M, R, n_in, device=dev, generator=g) if first else None
+    ys = torch.randint(0, n_cls, (M, R), device=dev, dtype=torch.int32, generator=g) if last else None
 
     def barrier():
         torch.cuda.synchronize()
@@ -355,8 +373,9 @@ def run_ours(args):
             t = torch.tensor([ems], device=dev, dtype=torch.float64)
             dist.all_reduce(t, op=dist.ReduceOp.MAX)
             ems = float(t.item())
+        x_bytes = R * 4 if model.layers[0].kind == sd.EMBED else R * n_in * 4
         e2e = {"value": args.steps * B / (ems / 1e3), "unit": UNIT,
-               "h2d_bytes_per_step": B * n_in * 4 + B * 4, "d2h_bytes_per_step": 4,
+               "h2d_bytes_per_step": x_bytes + R * 4, "d2h_bytes_per_step": 4,
                "api": "st_run_host"}
 
     if rank == 0:
@@ -368,7 +387,7 @@ def run_ours(args):
             "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": N, "steps": args.steps,
             "warmup": args.warmup, "ms_per_step": t_max / args.steps, "higher_is_better": True,
             "scaling": "strong", "vs_baseline": None, "dtype": "f32", "data": "synthetic",
-            "config": {"workload": wname, "stages": S, "batch": B, "gemm": args.gemm, "pred": args.pred,
+            "config": {"workload": wname, "stages": S, "batch": B, "seq_len": T, "gemm": args.gemm, "pred": args.pred,
                        "parallelism": f"pp{S}", "l2": "no flush: per-step working set (weights) >> 126 MB L2",
                        "session": "warm-up and timed steps are separate 1F1B sessions (fill + drain included)"},
             "roofline": {"kernel": "k_gemm_tc.cu tc_dw_kernel<FP32X3, fused K-B update> (dW + Eq.1/apply/predict)",

@@ -35,8 +35,12 @@
  * (argument rejected before any state changed).
  *
  * Parameter layout (identical on host and device): stage-local flat fp32
- * array, layer-major; for each layer W_l [n_in × n_out] row-major, then b_l
- * [n_out] if the layer has a bias.
+ * array, layer-major; for each DENSE layer W_l [n_in × n_out] row-major, then b_l
+ * [n_out] if the layer has a bias; EMBED: E [vocab × dim]; LSTM: W_ih, W_hh, b.
+ *
+ * Rows. Every activation, message and label vector has R = batch·seq_len rows
+ * (seq_len = 1 for the FC models). Inputs of a stage whose first layer is EMBED are
+ * int32 token ids [R] passed through the float* x arguments (same byte size).
  */
 #ifndef SPECTRAIN_H_
 #define SPECTRAIN_H_
@@ -68,6 +72,12 @@ typedef enum {
 
 enum { ST_FWD = 0, ST_BWD = 1 };
 enum { ST_ACT_NONE = 0, ST_ACT_RELU = 1 };
+/* Layer kinds. DENSE: Z = A·W + b, act. EMBED (network
+ * layer 0 only): n_in = vocabulary, n_out = dimension, params E [n_in × n_out]; the
+ * stage-0 input is int32 token ids. LSTM: n_in inputs, n_out = hidden H; params
+ * W_ih [n_in × 4H], W_hh [H × 4H], b [4H], gate order i, f, g, o (reading D18),
+ * h_{-1} = c_{-1} = 0 per mini-batch. */
+enum { ST_LAYER_DENSE = 0, ST_LAYER_EMBED = 1, ST_LAYER_LSTM = 2 };
 enum { ST_PRED_SPECTRAIN = 0, ST_PRED_NONE = 1 };
 enum { ST_MOMENTUM_EMA = 0, ST_MOMENTUM_HEAVY_BALL = 1 };
 /* GEMM arithmetic. FP32X3 = 3xTF32 split (hi·hi + hi·lo + lo·hi) on tcgen05
@@ -86,7 +96,8 @@ typedef struct {
   int32_t n_in;
   int32_t n_out;
   int32_t act;   /* ST_ACT_RELU for hidden layers, ST_ACT_NONE for the network's last layer */
-  int32_t bias;  /* 1: the layer has a bias vector b_l [n_out] */
+  int32_t bias;  /* 1: the layer has a bias vector b_l [n_out] (DENSE) */
+  int32_t kind;  /* ST_LAYER_* */
 } st_layer;
 
 typedef struct {
@@ -96,6 +107,7 @@ typedef struct {
   const int32_t* cuts;      /* [N-1] strictly increasing; stage k owns layers [cuts[k-1], cuts[k]) */
   int32_t stage;            /* k, 0 ≤ k < N */
   int32_t batch;            /* B ≥ 1 (mini-batch size) */
+  int32_t seq_len;          /* T ≥ 1: activations are [T·B × width], time-major rows t·B + b */
   float lr;                 /* η > 0 */
   float gamma;              /* γ, 0 < γ ≤ 1 */
   int32_t pred;             /* ST_PRED_* */
@@ -212,9 +224,9 @@ ST_API st_status st_get_params(st_ctx* ctx, float* W, float* V, size_t n, int64_
 
 /* ---- the verbs of one pipeline task ---------------------------------------- */
 
-/* F(mb) with WF. Stage 0 reads x_dev [B × n_in] (device, copied into the
- * stash); other stages receive the activation from stage k−1. The last stage
- * reads labels y_dev [B] int32 and writes the loss to its on-device loss vector
+/* F(mb) with WF. Stage 0 reads x_dev [R × n_in] (device, copied into the
+ * stash; int32 tokens [R] for an EMBED layer); other stages receive the activation
+ * from stage k−1. The last stage reads labels y_dev [R] int32 and writes the loss to its on-device loss vector
  * at index mb; if loss_host ≠ NULL it synchronises and copies the loss out
  * (ST_ERR_DIVERGED if non-finite). Non-last stages send their output to k+1.
  * ST_ERR_STATE if F(mb) is not the next op of the program. */
@@ -235,8 +247,8 @@ ST_API st_status st_predict_and_update(st_ctx* ctx);
  * (stage 0 / last stage; others may pass NULL). */
 ST_API st_status st_step(st_ctx* ctx, const float* x_dev, const int32_t* y_dev, st_step_info* out);
 
-/* Whole M-mini-batch program from the current position. xs_dev [M × B × n_in]
- * (stage 0), ys_dev [M × B] (last stage); losses_host [M] (last stage, may be
+/* Whole M-mini-batch program from the current position. xs_dev [M × R × n_in]
+ * (stage 0; [M × R] int32 tokens for EMBED), ys_dev [M × R] (last stage); losses_host [M] (last stage, may be
  * NULL) — when non-NULL the call synchronises and checks finiteness. */
 ST_API st_status st_run(st_ctx* ctx, int64_t M, const float* xs_dev, const int32_t* ys_dev, float* losses_host);
 

@@ -19,6 +19,7 @@ LIB_PATH = os.path.join(HERE, "libspectrain.so")
 
 ST_FWD, ST_BWD = 0, 1
 ST_ACT_NONE, ST_ACT_RELU = 0, 1
+ST_LAYER_DENSE, ST_LAYER_EMBED, ST_LAYER_LSTM = 0, 1, 2
 ST_PRED_SPECTRAIN, ST_PRED_NONE = 0, 1
 ST_MOMENTUM_EMA, ST_MOMENTUM_HEAVY_BALL = 0, 1
 ST_GEMM_FP32X3, ST_GEMM_TF32, ST_GEMM_SIMT = 0, 1, 2
@@ -37,14 +38,15 @@ class SpecTrainError(RuntimeError):
 
 
 class StLayer(ctypes.Structure):
-    _fields_ = [("n_in", ctypes.c_int32), ("n_out", ctypes.c_int32), ("act", ctypes.c_int32), ("bias", ctypes.c_int32)]
+    _fields_ = [("n_in", ctypes.c_int32), ("n_out", ctypes.c_int32), ("act", ctypes.c_int32), ("bias", ctypes.c_int32),
+                ("kind", ctypes.c_int32)]
 
 
 class StConfig(ctypes.Structure):
     _fields_ = [
         ("num_layers", ctypes.c_int32), ("layers", ctypes.POINTER(StLayer)),
         ("num_stages", ctypes.c_int32), ("cuts", ctypes.POINTER(ctypes.c_int32)),
-        ("stage", ctypes.c_int32), ("batch", ctypes.c_int32),
+        ("stage", ctypes.c_int32), ("batch", ctypes.c_int32), ("seq_len", ctypes.c_int32),
         ("lr", ctypes.c_float), ("gamma", ctypes.c_float),
         ("pred", ctypes.c_int32), ("momentum", ctypes.c_int32), ("gemm", ctypes.c_int32),
         ("loss", ctypes.c_int32), ("transport", ctypes.c_int32), ("device", ctypes.c_int32),
@@ -173,12 +175,16 @@ def nccl_id() -> bytes:
     return bytes(buf)
 
 
-def make_config(layers: Sequence[Tuple[int, int, int, int]], cuts: Sequence[int], stage: int, batch: int,
+def make_config(layers, cuts: Sequence[int], stage: int, batch: int,
                 lr: float, gamma: float, pred: int = ST_PRED_SPECTRAIN, momentum: int = ST_MOMENTUM_EMA,
                 gemm: int = ST_GEMM_FP32X3, transport: int = ST_TRANSPORT_NCCL, device: int = 0,
-                max_minibatches: int = 256, nccl_id_bytes: Optional[bytes] = None):
-    """Returns (StConfig, keepalive) — keepalive holds the arrays the struct points to."""
-    L = (StLayer * len(layers))(*[StLayer(int(a), int(b), int(c), int(d)) for a, b, c, d in layers])
+                max_minibatches: int = 256, nccl_id_bytes: Optional[bytes] = None, seq_len: int = 1):
+    """layers: (n_in, n_out, act, bias[, kind]) tuples. Returns (StConfig, keepalive) —
+    keepalive holds the arrays the struct points to."""
+    def mk(t):
+        t = tuple(int(v) for v in t)
+        return StLayer(t[0], t[1], t[2], t[3], t[4] if len(t) > 4 else ST_LAYER_DENSE)
+    L = (StLayer * len(layers))(*[mk(t) for t in layers])
     C = (ctypes.c_int32 * max(1, len(cuts)))(*[int(c) for c in cuts]) if cuts else (ctypes.c_int32 * 1)()
     cfg = StConfig()
     cfg.num_layers = len(layers)
@@ -186,6 +192,7 @@ def make_config(layers: Sequence[Tuple[int, int, int, int]], cuts: Sequence[int]
     cfg.num_stages = len(cuts) + 1
     cfg.cuts = ctypes.cast(C, ctypes.POINTER(ctypes.c_int32))
     cfg.stage, cfg.batch, cfg.lr, cfg.gamma = stage, batch, lr, gamma
+    cfg.seq_len = seq_len
     cfg.pred, cfg.momentum, cfg.gemm, cfg.loss = pred, momentum, gemm, ST_LOSS_SOFTMAX_CE
     cfg.transport, cfg.device, cfg.max_minibatches = transport, device, max_minibatches
     if nccl_id_bytes is not None:

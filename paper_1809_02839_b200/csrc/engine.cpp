@@ -35,6 +35,10 @@ struct Layout {
   int64_t off_send_fwd = -1, off_recv_bwd = -1, off_send_bwd = -1, off_logits = -1, off_dlogits = -1;
   int64_t off_bufA = -1, off_bufB = -1, off_losses = -1, off_rowloss = -1, off_ring_fwd = -1, off_ring_bwd = -1;
   int64_t off_ws = -1, off_ystage = -1;
+  int64_t off_lrec = -1, off_ldh = -1, off_ldc = -1, off_ldG = -1, off_escr = -1;
+  int T = 1;
+  int64_t R = 1;
+  bool embed_first = false;
   size_t ring_fwd_elems = 0, ring_bwd_elems = 0;
   st_sizes sizes{};
 };
@@ -68,32 +72,75 @@ st_status validate_and_layout(const st_config* c, Layout* L) {
     bounds.push_back(c->cuts[i]);
   }
   bounds.push_back(c->num_layers);
+  if (c->seq_len < 1) return set_error(ST_ERR_INPUT, "seq_len must be >= 1");
   for (int l = 0; l < c->num_layers; ++l) {
     const st_layer& y = c->layers[l];
     if (y.n_in < 1 || y.n_out < 1) return set_error(ST_ERR_SHAPE, "layer %d: bad dims", l);
     if (y.act != ST_ACT_NONE && y.act != ST_ACT_RELU) return set_error(ST_ERR_INPUT, "layer %d: bad act", l);
+    if (y.kind != ST_LAYER_DENSE && y.kind != ST_LAYER_EMBED && y.kind != ST_LAYER_LSTM)
+      return set_error(ST_ERR_INPUT, "layer %d: bad kind %d", l, y.kind);
+    if (y.kind == ST_LAYER_EMBED && l != 0) return set_error(ST_ERR_INPUT, "EMBED must be the network's layer 0");
+    if (y.kind != ST_LAYER_DENSE && y.act != ST_ACT_NONE)
+      return set_error(ST_ERR_INPUT, "layer %d: EMBED / LSTM layers take act = NONE", l);
     if (l > 0 && c->layers[l - 1].n_out != y.n_in)
       return set_error(ST_ERR_SHAPE, "layer chain mismatch: layer %d out %d != layer %d in %d", l - 1,
                        c->layers[l - 1].n_out, l, y.n_in);
   }
+  if (c->layers[c->num_layers - 1].kind != ST_LAYER_DENSE)
+    return set_error(ST_ERR_INPUT, "the network's last layer must be DENSE (softmax CE)");
   const int l0 = bounds[k], l1 = bounds[k + 1];
   const int64_t B = c->batch;
+  const int64_t T = c->seq_len;
+  const int64_t R = B * T;
+  L->T = (int)T;
+  L->R = R;
   L->first = (k == 0);
   L->last = (k == N - 1);
   L->S = N - k;
   L->prev_act = (k > 0) ? c->layers[l0 - 1].act : ST_ACT_NONE;
+  L->embed_first = c->layers[l0].kind == ST_LAYER_EMBED;
   int64_t off = 0, soff = 0;
+  int max_h = 0, max_vocab = 0;
   for (int l = l0; l < l1; ++l) {
     const st_layer& y = c->layers[l];
-    LayerInfo li{y.n_in, y.n_out, y.act, y.bias ? 1 : 0, off, -1, soff};
-    off += (int64_t)y.n_in * y.n_out;
-    if (y.bias) {
+    LayerInfo li{y.n_in, y.n_out, y.act, (y.kind == ST_LAYER_DENSE && y.bias) ? 1 : 0, y.kind, off, -1, -1, 0, -1,
+                 -1, -1, -1};
+    if (y.kind == ST_LAYER_EMBED) {
+      off += (int64_t)y.n_in * y.n_out;
+      max_vocab = std::max(max_vocab, y.n_in);
+    } else if (y.kind == ST_LAYER_LSTM) {
+      const int64_t H = y.n_out;
+      off += (int64_t)y.n_in * 4 * H;
+      li.whh_off = off;
+      off += H * 4 * H;
       li.b_off = off;
-      off += y.n_out;
+      off += 4 * H;
+      max_h = std::max(max_h, (int)H);
+    } else {
+      off += (int64_t)y.n_in * y.n_out;
+      if (y.bias) {
+        li.b_off = off;
+        off += y.n_out;
+      }
     }
-    soff += align_up(B * y.n_in, kAlignFloats);
-    L->max_in = std::max(L->max_in, y.n_in);
-    L->max_out = std::max(L->max_out, y.n_out);
+    li.n_params = off - li.w_off;
+    // layer input: aliases the previous LSTM's h buffer when that layer is in this stage
+    const bool alias = (l > l0) && c->layers[l - 1].kind == ST_LAYER_LSTM;
+    if (!alias) {
+      li.stash_off = soff;
+      soff += align_up(y.kind == ST_LAYER_EMBED ? R : R * y.n_in, kAlignFloats);
+    }
+    if (y.kind == ST_LAYER_LSTM) {
+      const int64_t H = y.n_out;
+      li.gates_off = soff;
+      soff += align_up(R * 4 * H, kAlignFloats);
+      li.c_off = soff;
+      soff += align_up(R * H, kAlignFloats);
+      li.h_off = soff;
+      soff += align_up((R + B) * H, kAlignFloats);
+    }
+    L->max_in = std::max(L->max_in, y.kind == ST_LAYER_EMBED ? 1 : y.n_in);
+    L->max_out = std::max(L->max_out, y.kind == ST_LAYER_LSTM ? 4 * y.n_out : y.n_out);
     L->layers.push_back(li);
   }
   L->P = off;
@@ -112,31 +159,38 @@ st_status validate_and_layout(const st_config* c, Layout* L) {
   };
   const int64_t width = std::max(L->max_in, L->max_out);
   if (!L->last) {
-    L->off_send_fwd = take(B * L->out_last);
-    L->off_recv_bwd = take(B * L->out_last);
+    L->off_send_fwd = take(R * L->out_last);
+    L->off_recv_bwd = take(R * L->out_last);
   }
-  if (!L->first) L->off_send_bwd = take(B * L->in_first);
+  if (!L->first) L->off_send_bwd = take(R * L->in_first);
   if (L->last) {
-    L->off_logits = take(B * L->out_last);
-    L->off_dlogits = take(B * L->out_last);
-    L->off_rowloss = take(B);
-    L->off_ystage = take(B);
+    L->off_logits = take(R * L->out_last);
+    L->off_dlogits = take(R * L->out_last);
+    L->off_rowloss = take(R);
+    L->off_ystage = take(R);
   }
-  L->off_bufA = take(B * width);
-  L->off_bufB = take(B * width);
+  L->off_bufA = take(R * width);
+  L->off_bufB = take(R * width);
   L->off_losses = take(c->max_minibatches);
+  if (max_h > 0) {
+    L->off_lrec = take(B * 4 * max_h);
+    L->off_ldh = take(B * max_h);
+    L->off_ldc = take(B * max_h);
+    L->off_ldG = take(R * 4 * max_h);
+  }
+  if (max_vocab > 0) L->off_escr = take(embed_grad_scratch_bytes((int)R, max_vocab) / 4 + 1);
   if (c->transport == ST_TRANSPORT_LOCAL) {
     if (!L->last) {
-      L->ring_fwd_elems = (size_t)(B * L->out_last);
+      L->ring_fwd_elems = (size_t)(R * L->out_last);
       L->off_ring_fwd = take((int64_t)L->ring_fwd_elems * (N + 1));
     }
     if (!L->first) {
-      L->ring_bwd_elems = (size_t)(B * L->in_first);
+      L->ring_bwd_elems = (size_t)(R * L->in_first);
       L->off_ring_bwd = take((int64_t)L->ring_bwd_elems * (N + 1));
     }
   }
   L->off_ws = w;
-  w += align_up(gemm_workspace_bytes((int)B, L->max_in, L->max_out), kAlignBytes);
+  w += align_up(gemm_workspace_bytes((int)R, L->max_in, L->max_out), kAlignBytes);
 
   st_sizes& z = L->sizes;
   z.params = L->P;
@@ -217,6 +271,9 @@ st_status ctx_init(const st_config* cfg, const st_buffers* bufs, void* stream, s
   c->N = cfg->num_stages;
   c->k = cfg->stage;
   c->B = cfg->batch;
+  c->T = L.T;
+  c->R = L.R;
+  c->embed_first = L.embed_first;
   c->lr = cfg->lr;
   c->gamma = cfg->gamma;
   c->pred = cfg->pred;
@@ -256,6 +313,11 @@ st_status ctx_init(const st_config* cfg, const st_buffers* bufs, void* stream, s
   c->dlogits = at(L.off_dlogits);
   c->rowloss = at(L.off_rowloss);
   c->y_stage = reinterpret_cast<int32_t*>(at(L.off_ystage));
+  c->lstm_rec = at(L.off_lrec);
+  c->lstm_dh = at(L.off_ldh);
+  c->lstm_dc = at(L.off_ldc);
+  c->lstm_dG = at(L.off_ldG);
+  c->embed_scratch = at(L.off_escr);
   c->bufA = at(L.off_bufA);
   c->bufB = at(L.off_bufB);
   c->losses_dev = at(L.off_losses);
@@ -274,7 +336,7 @@ st_status ctx_init(const st_config* cfg, const st_buffers* bufs, void* stream, s
   ST_CUDA_TRY(cudaMemsetAsync(c->V, 0, (size_t)c->P * 4, c->stream));
   ST_CUDA_TRY(cudaMemsetAsync(c->losses_dev, 0xff, (size_t)c->max_mb * 4, c->stream));  // NaN
   // GEMM workspace: split-K tile counters must start at zero (they self-reset afterwards)
-  ST_CUDA_TRY(cudaMemsetAsync(c->gemm_ws, 0, (size_t)gemm_workspace_bytes(c->B, c->max_width_in, c->max_width_out),
+  ST_CUDA_TRY(cudaMemsetAsync(c->gemm_ws, 0, (size_t)gemm_workspace_bytes((int)c->R, c->max_width_in, c->max_width_out),
                               c->stream));
   begin_session(c.get(), c->max_mb);
   *out = c.release();
@@ -348,7 +410,7 @@ st_status ctx_get_params(st_ctx* c, float* W, float* V, size_t n, int64_t* versi
 // ---- communication --------------------------------------------------------------
 
 static CommOp comm_op(st_ctx* c, int kind, int64_t mb) {
-  const size_t nin = (size_t)c->B * c->in_first, nout = (size_t)c->B * c->out_last;
+  const size_t nin = (size_t)c->R * c->in_first, nout = (size_t)c->R * c->out_last;
   switch (kind) {
     case CK_SEND_FWD: return {kind, mb, c->send_fwd, nout};
     case CK_RECV_FWD:
@@ -412,13 +474,62 @@ static st_status comm_after_task(st_ctx* c, size_t n) {
 static GemmArgs gargs(st_ctx* c, const LayerInfo& L) {
   GemmArgs g;
   g.mode = c->gemm;
-  g.B = c->B;
+  g.B = (int)c->R;  // GEMM rows: batch · sequence length
   g.n_in = L.n_in;
   g.n_out = L.n_out;
   g.work = c->gemm_ws;
-  g.work_bytes = gemm_workspace_bytes(c->B, c->max_width_in, c->max_width_out);
+  g.work_bytes = gemm_workspace_bytes((int)c->R, c->max_width_in, c->max_width_out);
   g.stream = c->stream;
   return g;
+}
+
+// layer input pointer inside a stash slot (aliases the previous LSTM layer's h_t rows)
+static float* layer_in(st_ctx* c, float* slot, size_t l) {
+  const LayerInfo& L = c->layers[l];
+  if (L.stash_off >= 0) return slot + L.stash_off;
+  const LayerInfo& P = c->layers[l - 1];
+  return slot + P.h_off + (size_t)c->B * P.n_out;
+}
+
+static GemmArgs gargs_rows(st_ctx* c, int rows, int n_in, int n_out) {
+  GemmArgs g;
+  g.mode = c->gemm;
+  g.B = rows;
+  g.n_in = n_in;
+  g.n_out = n_out;
+  g.work = c->gemm_ws;
+  g.work_bytes = gemm_workspace_bytes((int)c->R, c->max_width_in, c->max_width_out);
+  g.stream = c->stream;
+  return g;
+}
+
+// LSTM forward over T steps (a8): Gx = X·W_ih + b for all steps in one GEMM, then per
+// step the recurrent GEMM h_{t−1}·W_hh and the fused cell kernel.
+static st_status lstm_forward(st_ctx* c, const LayerInfo& L, const float* Wh, const float* X, float* slot) {
+  const int B = c->B, H = L.n_out, T = c->T;
+  float* gates = slot + L.gates_off;
+  float* cbuf = slot + L.c_off;
+  float* hbuf = slot + L.h_off;
+  {
+    Timed t(c, KC_GEMM_FWD);
+    ST_TRY(gemm_fwd(gargs_rows(c, (int)c->R, L.n_in, 4 * H), X, Wh + L.w_off, Wh + L.b_off, gates, 0));
+    c->launches += gemm_last_launches();
+  }
+  ST_CUDA_TRY(cudaMemsetAsync(hbuf, 0, (size_t)B * H * 4, c->stream));  // h_{-1} = 0
+  for (int t = 0; t < T; ++t) {
+    float* h_prev = hbuf + (size_t)t * B * H;
+    {
+      Timed tt(c, KC_GEMM_FWD);
+      ST_TRY(gemm_fwd(gargs_rows(c, B, H, 4 * H), h_prev, Wh + L.whh_off, nullptr, c->lstm_rec, 0));
+      c->launches += gemm_last_launches();
+    }
+    Timed tt(c, KC_LOSS);
+    ST_TRY(launch_lstm_cell_fwd(gates + (size_t)t * B * 4 * H, c->lstm_rec,
+                                t ? cbuf + (size_t)(t - 1) * B * H : nullptr, cbuf + (size_t)t * B * H,
+                                hbuf + (size_t)(t + 1) * B * H, B, H, c->stream));
+    c->launches += 1;
+  }
+  return ST_OK;
 }
 
 static st_status forward_compute(st_ctx* c, int64_t mb, const float* x_dev, const int32_t* y_dev, bool host_io,
@@ -427,26 +538,45 @@ static st_status forward_compute(st_ctx* c, int64_t mb, const float* x_dev, cons
   const float* Wh = c->WF;  // Eq. 4 with s_F (aliases W when s_F = 0)
   if (c->first_stage) {
     if (!x_dev) return set_error(ST_ERR_INPUT, "stage 0 forward needs x");
-    ST_CUDA_TRY(cudaMemcpyAsync(slot + c->layers[0].stash_off, x_dev, (size_t)c->B * c->in_first * 4,
+    const size_t bytes = c->embed_first ? (size_t)c->R * 4 : (size_t)c->R * c->in_first * 4;
+    ST_CUDA_TRY(cudaMemcpyAsync(slot + c->layers[0].stash_off, x_dev, bytes,
                                 host_io ? cudaMemcpyHostToDevice : cudaMemcpyDeviceToDevice, c->stream));
   }
   if (c->last_stage && host_io && y_dev) {
-    ST_CUDA_TRY(cudaMemcpyAsync(c->y_stage, y_dev, (size_t)c->B * 4, cudaMemcpyHostToDevice, c->stream));
+    ST_CUDA_TRY(cudaMemcpyAsync(c->y_stage, y_dev, (size_t)c->R * 4, cudaMemcpyHostToDevice, c->stream));
     y_dev = c->y_stage;
   }
   const size_t nl = c->layers.size();
   for (size_t l = 0; l < nl; ++l) {
     const LayerInfo& L = c->layers[l];
-    float* out = (l + 1 < nl) ? slot + c->layers[l + 1].stash_off : (c->last_stage ? c->logits : c->send_fwd);
-    Timed t(c, KC_GEMM_FWD);
-    ST_TRY(gemm_fwd(gargs(c, L), slot + L.stash_off, Wh + L.w_off, L.bias ? Wh + L.b_off : nullptr, out,
-                    L.act == ST_ACT_RELU));
-    c->launches += gemm_last_launches();
+    const float* in = layer_in(c, slot, l);
+    // where this layer's output goes: the next layer's input stash, or the stage output
+    float* out = nullptr;
+    const bool next_aliases = (l + 1 < nl) && c->layers[l + 1].stash_off < 0;
+    if (l + 1 < nl && !next_aliases)
+      out = slot + c->layers[l + 1].stash_off;
+    else if (l + 1 == nl)
+      out = c->last_stage ? c->logits : c->send_fwd;
+    if (L.kind == ST_LAYER_EMBED) {
+      Timed t(c, KC_LOSS);
+      ST_TRY(launch_embed_gather(Wh + L.w_off, reinterpret_cast<const int32_t*>(in), (int)c->R, L.n_out, out,
+                                 c->stream));
+      c->launches += 1;
+    } else if (L.kind == ST_LAYER_LSTM) {
+      ST_TRY(lstm_forward(c, L, Wh, in, slot));
+      if (out)  // stage output / a non-aliasing consumer: copy h_0..h_{T−1}
+        ST_CUDA_TRY(cudaMemcpyAsync(out, slot + L.h_off + (size_t)c->B * L.n_out, (size_t)c->R * L.n_out * 4,
+                                    cudaMemcpyDeviceToDevice, c->stream));
+    } else {
+      Timed t(c, KC_GEMM_FWD);
+      ST_TRY(gemm_fwd(gargs(c, L), in, Wh + L.w_off, L.bias ? Wh + L.b_off : nullptr, out, L.act == ST_ACT_RELU));
+      c->launches += gemm_last_launches();
+    }
   }
   if (c->last_stage) {
     if (!y_dev) return set_error(ST_ERR_INPUT, "last stage forward needs y_dev");
     Timed t(c, KC_LOSS);
-    ST_TRY(launch_softmax_ce(c->logits, y_dev, c->B, c->out_last, c->rowloss, c->losses_dev + (mb % c->max_mb),
+    ST_TRY(launch_softmax_ce(c->logits, y_dev, (int)c->R, c->out_last, c->rowloss, c->losses_dev + (mb % c->max_mb),
                              c->dlogits, c->stream));
     c->launches += 2;
     if (loss_host)
@@ -469,6 +599,51 @@ static UpdateArgs block_update(st_ctx* c, int64_t off, const UpdateConsts& k) {
 // blocks in its epilogue (G never reaches HBM); the caller then only bumps the version.
 // Safe per layer: dX_l (which reads WB_l) is issued before dW_l on the same stream and
 // no later task of this backward touches layer l again.
+// LSTM backward through time (a8). dOut [R × H]: gradient w.r.t. the layer output.
+// Writes the layer's gradient block into G and, if D != NULL, dX = dG·W_ihᵀ into D.
+static st_status lstm_backward(st_ctx* c, const LayerInfo& L, const float* Wh, const float* X, float* slot,
+                               const float* dOut, float* D) {
+  const int B = c->B, H = L.n_out, T = c->T;
+  const float* gates = slot + L.gates_off;
+  const float* cbuf = slot + L.c_off;
+  const float* hbuf = slot + L.h_off;
+  for (int t = T - 1; t >= 0; --t) {
+    {
+      Timed tt(c, KC_LOSS);
+      ST_TRY(launch_lstm_cell_bwd(gates + (size_t)t * B * 4 * H, cbuf + (size_t)t * B * H,
+                                  t ? cbuf + (size_t)(t - 1) * B * H : nullptr, dOut + (size_t)t * B * H,
+                                  t < T - 1 ? c->lstm_dh : nullptr, c->lstm_dc, t == T - 1,
+                                  c->lstm_dG + (size_t)t * B * 4 * H, B, H, c->stream));
+      c->launches += 1;
+    }
+    if (t > 0) {  // dh_{t−1} = dG_t · W_hhᵀ
+      Timed tt(c, KC_GEMM_DX);
+      ST_TRY(gemm_dx(gargs_rows(c, B, H, 4 * H), c->lstm_dG + (size_t)t * B * 4 * H, Wh + L.whh_off, nullptr,
+                     c->lstm_dh));
+      c->launches += gemm_last_launches();
+    }
+  }
+  {
+    Timed tt(c, KC_GEMM_DW);
+    // g_W_ih = Xᵀ·dG (+ g_b = Σ dG); g_W_hh = H_prevᵀ·dG with H_prev = [0, h_0 .. h_{T−2}]
+    ST_TRY(gemm_dw(gargs_rows(c, (int)c->R, L.n_in, 4 * H), X, c->lstm_dG, c->G + L.w_off, c->G + L.b_off));
+    c->launches += gemm_last_launches();
+    ST_TRY(gemm_dw(gargs_rows(c, (int)c->R, H, 4 * H), hbuf, c->lstm_dG, c->G + L.whh_off, nullptr));
+    c->launches += gemm_last_launches();
+  }
+  if (D) {
+    Timed tt(c, KC_GEMM_DX);
+    ST_TRY(gemm_dx(gargs_rows(c, (int)c->R, L.n_in, 4 * H), c->lstm_dG, Wh + L.w_off, nullptr, D));
+    c->launches += gemm_last_launches();
+  }
+  return ST_OK;
+}
+
+// fused = true: each layer's parameters are updated right after its gradient is
+// known — inside the dW GEMM epilogue for TMA-friendly dense layers (G never reaches
+// HBM), otherwise by a K-B launch over the layer block. Safe per layer: the layer's
+// dX (which reads WB) is issued before its update on the same stream and no later
+// task of this backward touches the layer again.
 static st_status backward_compute(st_ctx* c, int64_t mb, bool fused = false) {
   const UpdateConsts kc = make_update_consts(c->lr, c->gamma, c->sF, c->sB, c->momentum);
   float* slot = c->stash + (size_t)(mb % c->S) * c->slot_elems;
@@ -479,18 +654,28 @@ static st_status backward_compute(st_ctx* c, int64_t mb, bool fused = false) {
   int next = 0;
   for (int l = nl - 1; l >= 0; --l) {
     const LayerInfo& L = c->layers[l];
-    const float* Ain = slot + L.stash_off;
+    float* Ain = layer_in(c, slot, (size_t)l);
+    const bool need_dx = !(c->first_stage && l == 0) && L.kind != ST_LAYER_EMBED;
     float* D = nullptr;
-    if (!(c->first_stage && l == 0)) {
+    if (need_dx) {
       D = (l == 0) ? c->send_bwd : pp[next];
       if (D == dZ) D = pp[next ^= 1];
-      // ReLU mask of the layer that produced Ain (D12: ReLU'(0) = 0): 1[Z>0] == 1[ReLU(Z)>0]
-      const int producer_act = (l > 0) ? c->layers[l - 1].act : c->prev_act;
-      Timed t(c, KC_GEMM_DX);
-      ST_TRY(gemm_dx(gargs(c, L), dZ, Wh + L.w_off, producer_act == ST_ACT_RELU ? Ain : nullptr, D));
-      c->launches += gemm_last_launches();
     }
-    {
+    if (L.kind == ST_LAYER_EMBED) {
+      Timed t(c, KC_GEMM_DW);
+      ST_TRY(launch_embed_grad(dZ, reinterpret_cast<const int32_t*>(Ain), (int)c->R, L.n_in, L.n_out, c->G + L.w_off,
+                               c->embed_scratch, c->stream));
+      c->launches += 5;
+    } else if (L.kind == ST_LAYER_LSTM) {
+      ST_TRY(lstm_backward(c, L, Wh, Ain, slot, dZ, D));
+    } else {
+      if (D) {
+        // ReLU mask of the layer that produced Ain (D12: ReLU'(0) = 0): 1[Z>0] == 1[ReLU(Z)>0]
+        const int producer_act = (l > 0) ? c->layers[l - 1].act : c->prev_act;
+        Timed t(c, KC_GEMM_DX);
+        ST_TRY(gemm_dx(gargs(c, L), dZ, Wh + L.w_off, producer_act == ST_ACT_RELU ? Ain : nullptr, D));
+        c->launches += gemm_last_launches();
+      }
       Timed t(c, KC_GEMM_DW);
       if (fused) {
         UpdateArgs bu{};
@@ -500,6 +685,12 @@ static st_status backward_compute(st_ctx* c, int64_t mb, bool fused = false) {
         ST_TRY(gemm_dw(gargs(c, L), Ain, dZ, c->G + L.w_off, L.bias ? c->G + L.b_off : nullptr));
       }
       c->launches += gemm_last_launches();
+    }
+    if (fused && L.kind != ST_LAYER_DENSE) {
+      Timed t(c, KC_UPDATE);
+      UpdateArgs u = block_update(c, L.w_off, kc);
+      ST_TRY(launch_update_predict(u.W, u.V, c->G + L.w_off, u.WF, u.WB, (size_t)L.n_params, kc, c->stream));
+      c->launches += 1;
     }
     if (D) {
       dZ = D;
@@ -587,10 +778,10 @@ st_status ctx_predict_and_update(st_ctx* c) {
 }
 
 static const float* x_of(st_ctx* c, const float* xs, int64_t mb) {
-  return (c->first_stage && xs) ? xs + (size_t)mb * c->B * c->in_first : nullptr;
+  return (c->first_stage && xs) ? xs + (size_t)mb * c->R * (c->embed_first ? 1 : c->in_first) : nullptr;
 }
 static const int32_t* y_of(st_ctx* c, const int32_t* ys, int64_t mb) {
-  return (c->last_stage && ys) ? ys + (size_t)mb * c->B : nullptr;
+  return (c->last_stage && ys) ? ys + (size_t)mb * c->R : nullptr;
 }
 
 st_status ctx_step(st_ctx* c, const float* x_dev, const int32_t* y_dev, st_step_info* info) {

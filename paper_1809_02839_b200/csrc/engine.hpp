@@ -47,11 +47,25 @@ std::unique_ptr<Transport> make_local_transport(std::shared_ptr<LocalLink> link,
 std::shared_ptr<LocalLink> make_local_link(int N);
 
 struct LayerInfo {
-  int n_in, n_out, act, bias;
-  int64_t w_off;      // offset of W_l in the stage arena (elements)
+  int n_in, n_out, act, bias, kind;
+  int64_t w_off;      // offset of W_l (dense), E (embed), W_ih (lstm) in the stage arena
+  int64_t whh_off;    // lstm: offset of W_hh (−1 otherwise)
   int64_t b_off;      // offset of b_l (−1 if none)
-  int64_t stash_off;  // offset of A_in of this layer inside one stash slot
+  int64_t n_params;   // parameters of the layer (a contiguous block from w_off)
+  int64_t stash_off;  // offset of the layer input inside one stash slot (−1: aliases the
+                      // previous LSTM layer's h buffer); embed: int32 tokens [R]
+  int64_t gates_off, c_off, h_off;  // lstm: gates [R×4H], c [R×H], h [(R+B)×H] per slot
 };
+
+// LSTM / embedding kernels (k_lstm.cu)
+st_status launch_lstm_cell_fwd(float* gates, const float* rec, const float* c_prev, float* c_out, float* h_out, int B,
+                               int H, cudaStream_t s);
+st_status launch_lstm_cell_bwd(const float* gates, const float* c_t, const float* c_prev, const float* dOut,
+                               const float* dh_next, float* dc, int first, float* dG, int B, int H, cudaStream_t s);
+st_status launch_embed_gather(const float* E, const int32_t* tok, int rows, int D, float* out, cudaStream_t s);
+int64_t embed_grad_scratch_bytes(int rows, int V);
+st_status launch_embed_grad(const float* dA, const int32_t* tok, int rows, int V, int D, float* gE, void* scratch,
+                            cudaStream_t s);
 
 struct Profiler {
   bool on = false;
@@ -70,6 +84,9 @@ struct Profiler {
 struct st_ctx {
   // configuration
   int N = 1, k = 0, B = 1;
+  int T = 1;           // sequence length
+  int64_t R = 1;       // activation rows = B·T
+  bool embed_first = false;
   float lr = 0.f, gamma = 0.f;
   int pred = ST_PRED_SPECTRAIN, momentum = ST_MOMENTUM_EMA, gemm = ST_GEMM_FP32X3, loss = ST_LOSS_SOFTMAX_CE;
   int transport_kind = ST_TRANSPORT_NCCL;
@@ -100,7 +117,12 @@ struct st_ctx {
   float* bufB = nullptr;
   float* losses_dev = nullptr;  // [max_mb]
   float* rowloss = nullptr;     // [B]
-  int32_t* y_stage = nullptr;   // [B] labels staged from host (st_run_host)
+  int32_t* y_stage = nullptr;   // [R] labels staged from host (st_run_host)
+  float* lstm_rec = nullptr;    // [B × 4H] h_{t−1}·W_hh
+  float* lstm_dh = nullptr;     // [B × H] dh_next
+  float* lstm_dc = nullptr;     // [B × H] dc_next
+  float* lstm_dG = nullptr;     // [R × 4H] gate gradients of all steps
+  void* embed_scratch = nullptr;
   float* ring_fwd = nullptr;    // LOCAL transport rings
   float* ring_bwd = nullptr;
   size_t ring_fwd_elems = 0, ring_bwd_elems = 0;

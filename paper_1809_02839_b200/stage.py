@@ -32,15 +32,16 @@ class Stage:
     def __init__(self, layers: Layers, cuts: Sequence[int], stage: int, batch: int, lr: float, gamma: float = 0.9,
                  pred: int = L.ST_PRED_SPECTRAIN, momentum: int = L.ST_MOMENTUM_EMA, gemm: int = L.ST_GEMM_FP32X3,
                  transport: int = L.ST_TRANSPORT_NCCL, device: int = 0, max_minibatches: int = 256,
-                 nccl_id: Optional[bytes] = None, stream: Optional[torch.cuda.Stream] = None):
+                 nccl_id: Optional[bytes] = None, stream: Optional[torch.cuda.Stream] = None, seq_len: int = 1):
         self.layers = [tuple(int(v) for v in l) for l in layers]
         self.cuts = list(cuts)
         self.k = stage
         self.N = len(cuts) + 1
         self.batch = batch
         self.device = torch.device("cuda", device)
+        self.seq_len = seq_len
         self.cfg, self._keep = L.make_config(self.layers, self.cuts, stage, batch, lr, gamma, pred, momentum, gemm,
-                                             transport, device, max_minibatches, nccl_id)
+                                             transport, device, max_minibatches, nccl_id, seq_len)
         self.sizes = L.query_sizes(self.cfg)
         self.stream = stream if stream is not None else torch.cuda.Stream(device=self.device)
 

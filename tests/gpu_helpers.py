@@ -12,8 +12,9 @@ from oracle import spectrain_oracle as O
 
 def layers_of(model: sd.Model):
     import paper_1809_02839_b200 as st
-    return [(l.n_in, l.n_out, st.ST_ACT_RELU if l.act == sd.RELU else st.ST_ACT_NONE, 1 if l.bias else 0)
-            for l in model.layers]
+    kinds = {sd.DENSE: st.ST_LAYER_DENSE, sd.EMBED: st.ST_LAYER_EMBED, sd.LSTM: st.ST_LAYER_LSTM}
+    return [(l.n_in, l.n_out, st.ST_ACT_RELU if l.act == sd.RELU else st.ST_ACT_NONE, 1 if l.bias else 0,
+             kinds[l.kind]) for l in model.layers]
 
 
 def rel_l2(a, b) -> float:
@@ -29,7 +30,8 @@ def build_pipeline(model: sd.Model, batch: int, lr: float, gamma: float = 0.9, p
     momentum = st.ST_MOMENTUM_EMA if momentum is None else momentum
     gemm = st.ST_GEMM_FP32X3 if gemm is None else gemm
     stages = [st.Stage(layers_of(model), model.cuts, k, batch, lr, gamma, pred=pred, momentum=momentum, gemm=gemm,
-                       transport=st.ST_TRANSPORT_LOCAL, device=device, max_minibatches=max_mb)
+                       transport=st.ST_TRANSPORT_LOCAL, device=device, max_minibatches=max_mb,
+                       seq_len=model.seq_len)
               for k in range(model.num_stages)]
     st.connect_local(stages)
     return stages
@@ -40,7 +42,7 @@ def run_pipeline(stages, w0, X, Y):
     for s, w in zip(stages, w0):
         s.set_params(w)
     dev = stages[0].device
-    xs = torch.from_numpy(np.ascontiguousarray(X, np.float32)).to(dev)
+    xs = torch.from_numpy(np.ascontiguousarray(X, np.int32 if X.dtype.kind in "iu" else np.float32)).to(dev)
     ys = torch.from_numpy(np.ascontiguousarray(Y, np.int32)).to(dev)
     losses = st.run_group(stages, X.shape[0], xs, ys, want_losses=True)
     out = [s.get_params() for s in stages]
@@ -49,7 +51,8 @@ def run_pipeline(stages, w0, X, Y):
 
 
 def oracle_run(model, w0, X, Y, lr, gamma=0.9, pred=O.PRED_SPECTRAIN, momentum=O.MOMENTUM_EMA):
-    return O.run(model, sd.widen(w0), X.astype(np.float64), Y, float(np.float32(lr)), float(np.float32(gamma)),
+    Xo = X if X.dtype.kind in "iu" else X.astype(np.float64)
+    return O.run(model, sd.widen(w0), Xo, Y, float(np.float32(lr)), float(np.float32(gamma)),
                  pred=pred, momentum=momentum)
 
 
