@@ -115,7 +115,13 @@ def unpack_stage(layers, flat: np.ndarray):
 
     for L in layers:
         kind = getattr(L, "kind", "dense")
-        if kind == "embed":
+        if kind == "pool":
+            out.append(())
+        elif kind == "conv":
+            W = take(9 * L.n_in * L.n_out, (3, 3, L.n_in, L.n_out))
+            b = take(L.n_out, (L.n_out,)) if L.bias else None
+            out.append((W, b))
+        elif kind == "embed":
             out.append((take(L.n_in * L.n_out, (L.n_in, L.n_out)),))
         elif kind == "lstm":
             h = L.n_out
@@ -190,6 +196,54 @@ def lstm_backward(W_ih, W_hh, X, cache, dOut, T, need_dX=True):
     return gW_ih, gW_hh, gb, dX
 
 
+def conv3x3_forward(W, b, X):
+    """3×3 convolution, stride 1, zero padding 1, NHWC:
+    Y[n,h,w,o] = b[o] + Σ_{kh,kw,c} Xpad[n, h+kh, w+kw, c] · W[kh, kw, c, o]."""
+    n, H, Wd, _ = X.shape
+    Xp = np.pad(X, ((0, 0), (1, 1), (1, 1), (0, 0)))
+    Y = np.zeros((n, H, Wd, W.shape[3]))
+    for kh in range(3):
+        for kw in range(3):
+            Y += Xp[:, kh:kh + H, kw:kw + Wd, :] @ W[kh, kw]
+    if b is not None:
+        Y += b
+    return Y
+
+
+def conv3x3_backward(W, X, dY, need_dX=True):
+    """Gradients of conv3x3_forward: gW[kh,kw] = Σ Xpad-shiftᵀ·dY, gb = Σ dY,
+    dX = the padded scatter of dY·W[kh,kw]ᵀ."""
+    n, H, Wd, C = X.shape
+    Xp = np.pad(X, ((0, 0), (1, 1), (1, 1), (0, 0)))
+    gW = np.zeros_like(W)
+    dXp = np.zeros_like(Xp)
+    dY2 = dY.reshape(-1, dY.shape[3])
+    for kh in range(3):
+        for kw in range(3):
+            gW[kh, kw] = Xp[:, kh:kh + H, kw:kw + Wd, :].reshape(-1, C).T @ dY2
+            if need_dX:
+                dXp[:, kh:kh + H, kw:kw + Wd, :] += dY @ W[kh, kw].T
+    gb = dY2.sum(axis=0)
+    return gW, gb, (dXp[:, 1:-1, 1:-1, :] if need_dX else None)
+
+
+def maxpool2_forward(X):
+    """2×2 max-pool, stride 2, NHWC. The routed position is the first maximum in
+    row-major window order (reading D21; ties only occur among ReLU zeros, where the
+    routed gradient is masked to 0 anyway)."""
+    n, H, Wd, C = X.shape
+    w4 = np.stack([X[:, 0::2, 0::2], X[:, 0::2, 1::2], X[:, 1::2, 0::2], X[:, 1::2, 1::2]], axis=0)
+    arg = np.argmax(w4, axis=0)  # numpy argmax: first occurrence
+    return w4.max(axis=0), arg
+
+
+def maxpool2_backward(arg, dY, shape):
+    dX = np.zeros(shape)
+    for q, (dh, dw) in enumerate(((0, 0), (0, 1), (1, 0), (1, 1))):
+        dX[:, dh::2, dw::2] += dY * (arg == q)
+    return dX
+
+
 def stage_forward(layers, flat: np.ndarray, A, T: int = 1):
     """Per layer: dense Z = A·W + b, A' = ReLU(Z) (identity when act ==
     'none'); embed A' = E[tokens]; lstm A' = lstm_forward(A). Activations are
@@ -197,7 +251,19 @@ def stage_forward(layers, flat: np.ndarray, A, T: int = 1):
     stash = []
     for L, prm in zip(layers, unpack_stage(layers, flat)):
         kind = getattr(L, "kind", "dense")
-        if kind == "embed":
+        if kind in ("conv", "pool"):
+            n = A.shape[0]
+            X = A.reshape(n, L.hw, L.hw, L.n_in)
+            if kind == "conv":
+                W, b = prm
+                Z = conv3x3_forward(W, b, X)
+                stash.append((X, Z))
+                Y = np.maximum(Z, 0.0) if L.act == "relu" else Z
+            else:
+                Y, arg = maxpool2_forward(X)
+                stash.append((X.shape, arg))
+            A = Y.reshape(n, -1)
+        elif kind == "embed":
             (E,) = prm
             tok = np.asarray(A).astype(np.int64).reshape(-1)
             stash.append((tok,))
@@ -228,7 +294,22 @@ def stage_backward(layers, flat: np.ndarray, stash, dA_out: np.ndarray, need_dA_
         L = layers[li]
         kind = getattr(L, "kind", "dense")
         need = li > 0 or need_dA_in
-        if kind == "embed":
+        if kind in ("conv", "pool"):
+            n = dA.shape[0]
+            if kind == "conv":
+                W, b = params[li]
+                X, Z = stash[li]
+                dZ = dA.reshape(Z.shape)
+                if L.act == "relu":
+                    dZ = dZ * (Z > 0.0)
+                gW, gb, dX = conv3x3_backward(W, X, dZ, need)
+                grads[li] = (gW, gb if L.bias else None)
+            else:
+                shape, arg = stash[li]
+                dX = maxpool2_backward(arg, dA.reshape(arg.shape), shape)
+                grads[li] = ()
+            dA = dX.reshape(n, -1) if dX is not None else None
+        elif kind == "embed":
             (E,) = params[li]
             (tok,) = stash[li]
             gE = np.zeros_like(E)

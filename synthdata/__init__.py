@@ -28,6 +28,8 @@ NONE = "none"
 DENSE = "dense"
 EMBED = "embed"
 LSTM = "lstm"
+CONV = "conv"
+POOL = "pool"
 
 
 @dataclasses.dataclass(frozen=True)
@@ -44,9 +46,27 @@ class Layer:
     act: str = RELU
     bias: bool = True
     kind: str = DENSE
+    hw: int = 1  # conv / pool: input spatial side (square, NHWC activations)
+
+    @property
+    def width_in(self) -> int:
+        """Per-sample activation width entering the layer."""
+        return self.hw * self.hw * self.n_in if self.kind in (CONV, POOL) else self.n_in
+
+    @property
+    def width_out(self) -> int:
+        if self.kind == CONV:
+            return self.hw * self.hw * self.n_out
+        if self.kind == POOL:
+            return (self.hw // 2) * (self.hw // 2) * self.n_out
+        return self.n_out
 
     @property
     def n_params(self) -> int:
+        if self.kind == POOL:
+            return 0
+        if self.kind == CONV:
+            return 9 * self.n_in * self.n_out + (self.n_out if self.bias else 0)
         if self.kind == EMBED:
             return self.n_in * self.n_out
         if self.kind == LSTM:
@@ -141,6 +161,47 @@ def config_lstm_lm(num_stages: int = 4, vocab: int = 10000, hidden: int = 1500, 
     return lstm_lm(vocab, hidden, 2, even_cuts(4, num_stages), seq_len)
 
 
+VGG16_CIFAR = (64, 64, "M", 128, 128, "M", 256, 256, 256, "M", 512, 512, 512, "M", 512, 512, 512, "M")
+
+
+def vgg(cfg=VGG16_CIFAR, fc=(512, 512), classes: int = 10, hw: int = 32, in_ch: int = 3,
+        cuts: Optional[Sequence[int]] = None) -> Model:
+    """VGG on hw×hw×in_ch images (reading D19: 13 conv 3×3 pad 1 + ReLU, 2×2 max-pool
+    at 'M', FC 512-512-10, no BN / dropout). NHWC activations; the flatten after the
+    last pool is implicit (1×1×512 → 512)."""
+    ls = []
+    c, s = in_ch, hw
+    for v in cfg:
+        if v == "M":
+            ls.append(Layer(c, c, NONE, False, POOL, s))
+            s //= 2
+        else:
+            ls.append(Layer(c, v, RELU, True, CONV, s))
+            c = v
+    w = c * s * s
+    for f in fc:
+        ls.append(Layer(w, f, RELU, True, DENSE))
+        w = f
+    ls.append(Layer(w, classes, NONE, True, DENSE))
+    return Model(tuple(ls), tuple(cuts or ()), "softmax_ce", 1)
+
+
+def vgg16_cuts_8() -> Tuple[int, ...]:
+    """SURVEY §8(d) row 4 TF32 (flop-balanced) 8-stage partition, pools attached to
+    their conv: {c1_1,c1_2,P}{c2_1}{c2_2,P}{c3_1,c3_2}{c3_3,P}{c4_1,c4_2}{c4_3,P}{c5_*,P,fc×3}.
+    Layer indices: c1_1 0, c1_2 1, P 2, c2_1 3, c2_2 4, P 5, c3_1 6, c3_2 7, c3_3 8, P 9,
+    c4_1 10, c4_2 11, c4_3 12, P 13, c5_1 14 ..."""
+    return (3, 4, 6, 8, 10, 12, 14)
+
+
+def config_vgg16(num_stages: int = 8) -> Model:
+    """BJ configs[3]: VGG-16 on 32×32×3 CIFAR-shaped images, batch 128, 8 stages."""
+    if num_stages == 8:
+        return vgg(cuts=vgg16_cuts_8())
+    n = len(vgg().layers)
+    return vgg(cuts=even_cuts(n, num_stages))
+
+
 def config_large_fcn(num_stages: int, width: int = 16384, hidden_layers: int = 16) -> Model:
     """BJ configs[4]: large FCN 16 × 16384."""
     widths = [784] + [width] * hidden_layers + [10]
@@ -160,6 +221,13 @@ def glorot_params(model: Model, seed: int) -> List[np.ndarray]:
         for layer in model.stage_layers(k):
             if layer.kind == EMBED:
                 parts.append(rng.uniform(-0.1, 0.1, size=layer.n_in * layer.n_out))
+            elif layer.kind == POOL:
+                pass
+            elif layer.kind == CONV:
+                r = math.sqrt(6.0 / (9 * layer.n_in + 9 * layer.n_out))
+                parts.append(rng.uniform(-r, r, size=9 * layer.n_in * layer.n_out))
+                if layer.bias:
+                    parts.append(np.zeros(layer.n_out))
             elif layer.kind == LSTM:
                 h = layer.n_out
                 r1 = math.sqrt(6.0 / (layer.n_in + 4 * h))
@@ -226,8 +294,9 @@ def widen(params_f32: Sequence[np.ndarray]) -> List[np.ndarray]:
 def parity_inputs(model: Model, num_batches: int, batch: int, seed: int = 0,
                   labels: str = "teacher") -> Tuple[List[np.ndarray], np.ndarray, np.ndarray]:
     """(W0 per stage as fp32, X as fp32 [M,B,in], Y int32 [M,B]) — fp32-representable
-    inputs so oracle (fp64) and GPU (fp32) start from bit-identical values."""
+    inputs so oracle (fp64) and GPU (fp32) start from bit-identical values. Images of
+    conv models are NHWC, flattened per sample."""
     w0 = to_f32_params(glorot_params(model, seed))
-    x, y = images_and_labels(model.layers[0].n_in, model.layers[-1].n_out, num_batches, batch,
+    x, y = images_and_labels(model.layers[0].width_in, model.layers[-1].n_out, num_batches, batch,
                              seed + 1, labels)
     return w0, x.astype(np.float32), y

@@ -499,3 +499,67 @@ def test_lstm_lm_pipeline_single_stage_equals_torch_sgd():
         _torch_lm_loss(model, tw, torch.tensor(X[i]), torch.tensor(Y[i])).backward()
         opt.step()
     np.testing.assert_allclose(res.W[0], tw.detach().numpy(), rtol=1e-10, atol=1e-13)
+
+
+# ---------------------------------------------------------------- VGG conv stages (a10)
+
+def _torch_vgg_loss(model, flat, x, y):
+    off = 0
+    a = x.view(x.shape[0], model.layers[0].hw, model.layers[0].hw, model.layers[0].n_in).permute(0, 3, 1, 2)
+    for L in model.layers:
+        if L.kind == sd.CONV:
+            W = flat[off:off + 9 * L.n_in * L.n_out].view(3, 3, L.n_in, L.n_out)
+            off += 9 * L.n_in * L.n_out
+            b = flat[off:off + L.n_out]
+            off += L.n_out
+            a = torch.nn.functional.conv2d(a, W.permute(3, 2, 0, 1), b, padding=1)
+            a = torch.relu(a) if L.act == sd.RELU else a
+        elif L.kind == sd.POOL:
+            a = torch.nn.functional.max_pool2d(a, 2)
+        else:
+            if a.dim() == 4:
+                a = a.permute(0, 2, 3, 1).reshape(a.shape[0], -1)
+            W = flat[off:off + L.n_in * L.n_out].view(L.n_in, L.n_out)
+            off += L.n_in * L.n_out
+            a = a @ W + flat[off:off + L.n_out]
+            off += L.n_out
+            a = torch.relu(a) if L.act == sd.RELU else a
+    return torch.nn.functional.cross_entropy(a, y.long())
+
+
+@pytest.mark.parametrize("cuts", [[], [2, 4], [1, 3, 5]])
+def test_vgg_stage_grads_equal_torch_conv(cuts):
+    """conv 3×3 (pad 1) + ReLU, 2×2 max-pool, FC head, composed stage by stage ==
+    torch.nn.functional.conv2d / max_pool2d + autograd (library routines)."""
+    model = sd.vgg(cfg=(4, "M", 6, 6, "M"), fc=(7,), classes=5, hw=8, in_ch=3, cuts=cuts)
+    w = np.concatenate(sd.glorot_params(model, 31))
+    w = w + 0.05 * np.random.default_rng(2).standard_normal(w.size)
+    X, Y = sd.images_and_labels(model.layers[0].width_in, 5, 1, 3, seed=33)
+    X = X - 0.5
+    flats, off = [], 0
+    for k in range(model.num_stages):
+        n = model.stage_params(k)
+        flats.append(w[off:off + n])
+        off += n
+    a, stashes = X[0], []
+    for k in range(model.num_stages):
+        a, st = O.stage_forward(model.stage_layers(k), flats[k], a)
+        stashes.append(st)
+    loss, d = O.loss_and_grad("softmax_ce", a, Y[0])
+    grads = [None] * model.num_stages
+    for k in range(model.num_stages - 1, -1, -1):
+        grads[k], d = O.stage_backward(model.stage_layers(k), flats[k], stashes[k], d, need_dA_in=k > 0)
+    tw = torch.tensor(w, dtype=torch.float64, requires_grad=True)
+    tl = _torch_vgg_loss(model, tw, torch.tensor(X[0]), torch.tensor(Y[0]))
+    tl.backward()
+    assert loss == pytest.approx(tl.item(), rel=1e-12)
+    np.testing.assert_allclose(np.concatenate(grads), tw.grad.numpy(), rtol=1e-10, atol=1e-13)
+
+
+def test_maxpool_tie_rule_first_in_row_major():
+    X = np.zeros((1, 2, 2, 1))
+    X[0, 0, 1, 0] = X[0, 1, 0, 0] = 1.0  # two equal maxima
+    Y, arg = O.maxpool2_forward(X)
+    assert Y[0, 0, 0, 0] == 1.0 and arg[0, 0, 0, 0] == 1
+    dX = O.maxpool2_backward(arg, np.ones((1, 1, 1, 1)), X.shape)
+    assert dX[0, 0, 1, 0] == 1.0 and dX.sum() == 1.0
