@@ -44,7 +44,7 @@ def parse():
     p.add_argument("--steps", type=int, default=30)
     p.add_argument("--warmup", type=int, default=5)
     p.add_argument("--impl", default="ours", choices=["ours", "reference"])
-    p.add_argument("--workload", default="wide_fcn", choices=["wide_fcn", "large_fcn", "mlp", "deep_mlp", "lstm_lm"])
+    p.add_argument("--workload", default="wide_fcn", choices=["wide_fcn", "large_fcn", "mlp", "deep_mlp", "lstm_lm", "vgg16"])
     p.add_argument("--stages", type=int, default=0, help="pipeline depth (default = --gpus); >N only with N=1")
     p.add_argument("--gemm", default=DEFAULT_GEMM, choices=["fp32x3", "tf32", "simt"])
     p.add_argument("--pred", default="spectrain", choices=["spectrain", "none"])
@@ -62,6 +62,8 @@ def workload(name: str, S: int):
         return sd.config_large_fcn(S), 128, "large_fcn_784-16x16384-10_b128"
     if name == "deep_mlp":
         return sd.config_deep_mlp(S), 128, "deep_mlp_784-8x1024-10_b128"
+    if name == "vgg16":
+        return sd.config_vgg16(S if S in (1, 8) else S), 128, "vgg16_cifar_32x32x3_b128"
     if name == "lstm_lm":
         return sd.config_lstm_lm(min(S, 4)), 128, "lstm_lm_v10k_h1500_2layer_t35_b128"
     return sd.mlp([784, 256, 256, 10], cuts=sd.even_cuts(3, S)), 32, "mlp_784-256-256-10_b32"
@@ -224,9 +226,10 @@ def run_ours(args):
     model, B, wname = workload(args.workload, S)
     gemm = {"fp32x3": st.ST_GEMM_FP32X3, "tf32": st.ST_GEMM_TF32, "simt": st.ST_GEMM_SIMT}[args.gemm]
     pred = st.ST_PRED_SPECTRAIN if args.pred == "spectrain" else st.ST_PRED_NONE
-    kinds = {sd.DENSE: st.ST_LAYER_DENSE, sd.EMBED: st.ST_LAYER_EMBED, sd.LSTM: st.ST_LAYER_LSTM}
+    kinds = {sd.DENSE: st.ST_LAYER_DENSE, sd.EMBED: st.ST_LAYER_EMBED, sd.LSTM: st.ST_LAYER_LSTM,
+             sd.CONV: st.ST_LAYER_CONV, sd.POOL: st.ST_LAYER_POOL}
     layers = [(l.n_in, l.n_out, st.ST_ACT_RELU if l.act == sd.RELU else st.ST_ACT_NONE, 1 if l.bias else 0,
-               kinds[l.kind]) for l in model.layers]
+               kinds[l.kind], l.hw) for l in model.layers]
     T = model.seq_len
     R = B * T
     M = max(args.steps, args.warmup, 1)
@@ -253,7 +256,13 @@ def run_ours(args):
         w = torch.empty(s.params, device=dev)
         off = 0
         for L in model.stage_layers(s.k):
-            if L.kind == sd.EMBED:
+            if L.kind == sd.POOL:
+                pass
+            elif L.kind == sd.CONV:
+                r = (6.0 / (9 * L.n_in + 9 * L.n_out)) ** 0.5
+                w[off:off + 9 * L.n_in * L.n_out].uniform_(-r, r, generator=g)
+                w[off + 9 * L.n_in * L.n_out:off + L.n_params].zero_()
+            elif L.kind == sd.EMBED:
                 w[off:off + L.n_params].uniform_(-0.1, 0.1, generator=g)
             elif L.kind == sd.LSTM:
                 h = L.n_out
@@ -268,7 +277,7 @@ def run_ours(args):
             off += L.n_params
         s.set_params(w.cpu().numpy())
         del w
-    n_in, n_cls = model.layers[0].n_in, model.layers[-1].n_out
+    n_in, n_cls = model.layers[0].width_in, model.layers[-1].n_out
     first = my_stages[0].is_first
     last = my_stages[-1].is_last
     if model.layers[0].kind == sd.EMBED:

@@ -77,7 +77,12 @@ enum { ST_ACT_NONE = 0, ST_ACT_RELU = 1 };
  * stage-0 input is int32 token ids. LSTM: n_in inputs, n_out = hidden H; params
  * W_ih [n_in × 4H], W_hh [H × 4H], b [4H], gate order i, f, g, o (reading D18),
  * h_{-1} = c_{-1} = 0 per mini-batch. */
-enum { ST_LAYER_DENSE = 0, ST_LAYER_EMBED = 1, ST_LAYER_LSTM = 2 };
+enum { ST_LAYER_DENSE = 0, ST_LAYER_EMBED = 1, ST_LAYER_LSTM = 2, ST_LAYER_CONV = 3, ST_LAYER_POOL = 4 };
+/* CONV: 3×3, stride 1, zero padding 1 on NHWC [hw × hw × n_in] → [hw × hw × n_out],
+ * params W [3·3·n_in × n_out] (HWIO, rows (kh, kw, c)), then b; act RELU or NONE.
+ * POOL: 2×2 max-pool stride 2, n_in = n_out = channels, hw even; no params. The
+ * per-sample activation width entering a CONV / POOL layer is hw·hw·n_in; a DENSE layer
+ * after the last POOL sees the flattened NHWC vector. (SURVEY §8(a) a10, D19, D21.) */
 enum { ST_PRED_SPECTRAIN = 0, ST_PRED_NONE = 1 };
 enum { ST_MOMENTUM_EMA = 0, ST_MOMENTUM_HEAVY_BALL = 1 };
 /* GEMM arithmetic. FP32X3 = 3xTF32 split (hi·hi + hi·lo + lo·hi) on tcgen05
@@ -98,6 +103,7 @@ typedef struct {
   int32_t act;   /* ST_ACT_RELU for hidden layers, ST_ACT_NONE for the network's last layer */
   int32_t bias;  /* 1: the layer has a bias vector b_l [n_out] (DENSE) */
   int32_t kind;  /* ST_LAYER_* */
+  int32_t hw;    /* CONV / POOL: input spatial side (square images); ignored otherwise */
 } st_layer;
 
 typedef struct {

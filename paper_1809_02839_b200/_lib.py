@@ -19,7 +19,7 @@ LIB_PATH = os.path.join(HERE, "libspectrain.so")
 
 ST_FWD, ST_BWD = 0, 1
 ST_ACT_NONE, ST_ACT_RELU = 0, 1
-ST_LAYER_DENSE, ST_LAYER_EMBED, ST_LAYER_LSTM = 0, 1, 2
+ST_LAYER_DENSE, ST_LAYER_EMBED, ST_LAYER_LSTM, ST_LAYER_CONV, ST_LAYER_POOL = 0, 1, 2, 3, 4
 ST_PRED_SPECTRAIN, ST_PRED_NONE = 0, 1
 ST_MOMENTUM_EMA, ST_MOMENTUM_HEAVY_BALL = 0, 1
 ST_GEMM_FP32X3, ST_GEMM_TF32, ST_GEMM_SIMT = 0, 1, 2
@@ -39,7 +39,7 @@ class SpecTrainError(RuntimeError):
 
 class StLayer(ctypes.Structure):
     _fields_ = [("n_in", ctypes.c_int32), ("n_out", ctypes.c_int32), ("act", ctypes.c_int32), ("bias", ctypes.c_int32),
-                ("kind", ctypes.c_int32)]
+                ("kind", ctypes.c_int32), ("hw", ctypes.c_int32)]
 
 
 class StConfig(ctypes.Structure):
@@ -179,11 +179,11 @@ def make_config(layers, cuts: Sequence[int], stage: int, batch: int,
                 lr: float, gamma: float, pred: int = ST_PRED_SPECTRAIN, momentum: int = ST_MOMENTUM_EMA,
                 gemm: int = ST_GEMM_FP32X3, transport: int = ST_TRANSPORT_NCCL, device: int = 0,
                 max_minibatches: int = 256, nccl_id_bytes: Optional[bytes] = None, seq_len: int = 1):
-    """layers: (n_in, n_out, act, bias[, kind]) tuples. Returns (StConfig, keepalive) —
+    """layers: (n_in, n_out, act, bias[, kind[, hw]]) tuples. Returns (StConfig, keepalive) —
     keepalive holds the arrays the struct points to."""
     def mk(t):
         t = tuple(int(v) for v in t)
-        return StLayer(t[0], t[1], t[2], t[3], t[4] if len(t) > 4 else ST_LAYER_DENSE)
+        return StLayer(t[0], t[1], t[2], t[3], t[4] if len(t) > 4 else ST_LAYER_DENSE, t[5] if len(t) > 5 else 1)
     L = (StLayer * len(layers))(*[mk(t) for t in layers])
     C = (ctypes.c_int32 * max(1, len(cuts)))(*[int(c) for c in cuts]) if cuts else (ctypes.c_int32 * 1)()
     cfg = StConfig()

@@ -35,13 +35,24 @@ struct Layout {
   int64_t off_send_fwd = -1, off_recv_bwd = -1, off_send_bwd = -1, off_logits = -1, off_dlogits = -1;
   int64_t off_bufA = -1, off_bufB = -1, off_losses = -1, off_rowloss = -1, off_ring_fwd = -1, off_ring_bwd = -1;
   int64_t off_ws = -1, off_ystage = -1;
-  int64_t off_lrec = -1, off_ldh = -1, off_ldc = -1, off_ldG = -1, off_escr = -1;
+  int64_t off_lrec = -1, off_ldh = -1, off_ldc = -1, off_ldG = -1, off_escr = -1, off_col = -1, off_dcol = -1;
+  int64_t gemm_rows = 1;
+  int gemm_in = 1, gemm_out = 1;  // largest GEMM operand widths (workspace sizing)
   int T = 1;
   int64_t R = 1;
   bool embed_first = false;
   size_t ring_fwd_elems = 0, ring_bwd_elems = 0;
   st_sizes sizes{};
 };
+
+int64_t layer_win(const st_layer& y) {
+  return (y.kind == ST_LAYER_CONV || y.kind == ST_LAYER_POOL) ? (int64_t)y.hw * y.hw * y.n_in : y.n_in;
+}
+int64_t layer_wout(const st_layer& y) {
+  if (y.kind == ST_LAYER_CONV) return (int64_t)y.hw * y.hw * y.n_out;
+  if (y.kind == ST_LAYER_POOL) return (int64_t)(y.hw / 2) * (y.hw / 2) * y.n_out;
+  return y.n_out;
+}
 
 st_status validate_and_layout(const st_config* c, Layout* L) {
   if (!c) return set_error(ST_ERR_INPUT, "config is NULL");
@@ -77,14 +88,19 @@ st_status validate_and_layout(const st_config* c, Layout* L) {
     const st_layer& y = c->layers[l];
     if (y.n_in < 1 || y.n_out < 1) return set_error(ST_ERR_SHAPE, "layer %d: bad dims", l);
     if (y.act != ST_ACT_NONE && y.act != ST_ACT_RELU) return set_error(ST_ERR_INPUT, "layer %d: bad act", l);
-    if (y.kind != ST_LAYER_DENSE && y.kind != ST_LAYER_EMBED && y.kind != ST_LAYER_LSTM)
+    if (y.kind < ST_LAYER_DENSE || y.kind > ST_LAYER_POOL)
       return set_error(ST_ERR_INPUT, "layer %d: bad kind %d", l, y.kind);
     if (y.kind == ST_LAYER_EMBED && l != 0) return set_error(ST_ERR_INPUT, "EMBED must be the network's layer 0");
-    if (y.kind != ST_LAYER_DENSE && y.act != ST_ACT_NONE)
-      return set_error(ST_ERR_INPUT, "layer %d: EMBED / LSTM layers take act = NONE", l);
-    if (l > 0 && c->layers[l - 1].n_out != y.n_in)
-      return set_error(ST_ERR_SHAPE, "layer chain mismatch: layer %d out %d != layer %d in %d", l - 1,
-                       c->layers[l - 1].n_out, l, y.n_in);
+    if ((y.kind == ST_LAYER_EMBED || y.kind == ST_LAYER_LSTM || y.kind == ST_LAYER_POOL) && y.act != ST_ACT_NONE)
+      return set_error(ST_ERR_INPUT, "layer %d: EMBED / LSTM / POOL layers take act = NONE", l);
+    if (y.kind == ST_LAYER_CONV || y.kind == ST_LAYER_POOL) {
+      if (y.hw < 1 || (y.kind == ST_LAYER_POOL && (y.hw % 2 || y.n_in != y.n_out)))
+        return set_error(ST_ERR_SHAPE, "layer %d: bad conv / pool geometry", l);
+      if (c->seq_len != 1) return set_error(ST_ERR_INPUT, "conv / pool layers need seq_len = 1");
+    }
+    if (l > 0 && layer_wout(c->layers[l - 1]) != layer_win(y))
+      return set_error(ST_ERR_SHAPE, "layer chain mismatch: layer %d out %lld != layer %d in %lld", l - 1,
+                       (long long)layer_wout(c->layers[l - 1]), l, (long long)layer_win(y));
   }
   if (c->layers[c->num_layers - 1].kind != ST_LAYER_DENSE)
     return set_error(ST_ERR_INPUT, "the network's last layer must be DENSE (softmax CE)");
@@ -101,11 +117,24 @@ st_status validate_and_layout(const st_config* c, Layout* L) {
   L->embed_first = c->layers[l0].kind == ST_LAYER_EMBED;
   int64_t off = 0, soff = 0;
   int max_h = 0, max_vocab = 0;
+  int64_t max_col = 0, gemm_rows = R;
   for (int l = l0; l < l1; ++l) {
     const st_layer& y = c->layers[l];
-    LayerInfo li{y.n_in, y.n_out, y.act, (y.kind == ST_LAYER_DENSE && y.bias) ? 1 : 0, y.kind, off, -1, -1, 0, -1,
-                 -1, -1, -1};
-    if (y.kind == ST_LAYER_EMBED) {
+    const bool has_bias = (y.kind == ST_LAYER_DENSE || y.kind == ST_LAYER_CONV) && y.bias;
+    LayerInfo li{y.n_in, y.n_out, y.act, has_bias ? 1 : 0, y.kind, y.hw, layer_win(y), layer_wout(y), off, -1, -1, 0,
+                 -1, -1, -1, -1};
+    if (y.kind == ST_LAYER_POOL) {
+      // no parameters
+    } else if (y.kind == ST_LAYER_CONV) {
+      off += (int64_t)9 * y.n_in * y.n_out;
+      if (y.bias) {
+        li.b_off = off;
+        off += y.n_out;
+      }
+      const int64_t P = B * y.hw * y.hw;
+      max_col = std::max(max_col, P * 9 * y.n_in);
+      gemm_rows = std::max(gemm_rows, P);
+    } else if (y.kind == ST_LAYER_EMBED) {
       off += (int64_t)y.n_in * y.n_out;
       max_vocab = std::max(max_vocab, y.n_in);
     } else if (y.kind == ST_LAYER_LSTM) {
@@ -128,7 +157,7 @@ st_status validate_and_layout(const st_config* c, Layout* L) {
     const bool alias = (l > l0) && c->layers[l - 1].kind == ST_LAYER_LSTM;
     if (!alias) {
       li.stash_off = soff;
-      soff += align_up(y.kind == ST_LAYER_EMBED ? R : R * y.n_in, kAlignFloats);
+      soff += align_up(y.kind == ST_LAYER_EMBED ? R : R * li.win, kAlignFloats);
     }
     if (y.kind == ST_LAYER_LSTM) {
       const int64_t H = y.n_out;
@@ -139,14 +168,26 @@ st_status validate_and_layout(const st_config* c, Layout* L) {
       li.h_off = soff;
       soff += align_up((R + B) * H, kAlignFloats);
     }
-    L->max_in = std::max(L->max_in, y.kind == ST_LAYER_EMBED ? 1 : y.n_in);
-    L->max_out = std::max(L->max_out, y.kind == ST_LAYER_LSTM ? 4 * y.n_out : y.n_out);
+    // buffer widths (messages, ping-pong) and GEMM operand widths
+    L->max_in = std::max<int>(L->max_in, y.kind == ST_LAYER_EMBED ? 1 : (int)li.win);
+    L->max_out = std::max<int>(L->max_out, y.kind == ST_LAYER_LSTM ? 4 * y.n_out : (int)li.wout);
+    if (y.kind == ST_LAYER_CONV) {
+      L->gemm_in = std::max(L->gemm_in, 9 * y.n_in);
+      L->gemm_out = std::max(L->gemm_out, y.n_out);
+    } else if (y.kind == ST_LAYER_LSTM) {
+      L->gemm_in = std::max(L->gemm_in, y.n_in);
+      L->gemm_out = std::max(L->gemm_out, 4 * y.n_out);
+    } else if (y.kind == ST_LAYER_DENSE) {
+      L->gemm_in = std::max(L->gemm_in, y.n_in);
+      L->gemm_out = std::max(L->gemm_out, y.n_out);
+    }
     L->layers.push_back(li);
   }
+  L->gemm_rows = gemm_rows;
   L->P = off;
   L->slot_elems = soff;
-  L->in_first = c->layers[l0].n_in;
-  L->out_last = c->layers[l1 - 1].n_out;
+  L->in_first = (int)layer_win(c->layers[l0]);
+  L->out_last = (int)layer_wout(c->layers[l1 - 1]);
   L->sF = c->pred == ST_PRED_NONE ? 0 : version_difference(k, N, ST_FWD);
   L->sB = c->pred == ST_PRED_NONE ? 0 : version_difference(k, N, ST_BWD);
 
@@ -179,6 +220,10 @@ st_status validate_and_layout(const st_config* c, Layout* L) {
     L->off_ldG = take(R * 4 * max_h);
   }
   if (max_vocab > 0) L->off_escr = take(embed_grad_scratch_bytes((int)R, max_vocab) / 4 + 1);
+  if (max_col > 0) {
+    L->off_col = take(max_col);
+    L->off_dcol = take(max_col);
+  }
   if (c->transport == ST_TRANSPORT_LOCAL) {
     if (!L->last) {
       L->ring_fwd_elems = (size_t)(R * L->out_last);
@@ -190,7 +235,7 @@ st_status validate_and_layout(const st_config* c, Layout* L) {
     }
   }
   L->off_ws = w;
-  w += align_up(gemm_workspace_bytes((int)R, L->max_in, L->max_out), kAlignBytes);
+  w += align_up(gemm_workspace_bytes((int)gemm_rows, L->gemm_in, L->gemm_out), kAlignBytes);
 
   st_sizes& z = L->sizes;
   z.params = L->P;
@@ -318,6 +363,11 @@ st_status ctx_init(const st_config* cfg, const st_buffers* bufs, void* stream, s
   c->lstm_dc = at(L.off_ldc);
   c->lstm_dG = at(L.off_ldG);
   c->embed_scratch = at(L.off_escr);
+  c->conv_col = at(L.off_col);
+  c->conv_dcol = at(L.off_dcol);
+  c->gemm_rows_max = L.gemm_rows;
+  c->gemm_in_max = L.gemm_in;
+  c->gemm_out_max = L.gemm_out;
   c->bufA = at(L.off_bufA);
   c->bufB = at(L.off_bufB);
   c->losses_dev = at(L.off_losses);
@@ -336,8 +386,7 @@ st_status ctx_init(const st_config* cfg, const st_buffers* bufs, void* stream, s
   ST_CUDA_TRY(cudaMemsetAsync(c->V, 0, (size_t)c->P * 4, c->stream));
   ST_CUDA_TRY(cudaMemsetAsync(c->losses_dev, 0xff, (size_t)c->max_mb * 4, c->stream));  // NaN
   // GEMM workspace: split-K tile counters must start at zero (they self-reset afterwards)
-  ST_CUDA_TRY(cudaMemsetAsync(c->gemm_ws, 0, (size_t)gemm_workspace_bytes((int)c->R, c->max_width_in, c->max_width_out),
-                              c->stream));
+  ST_CUDA_TRY(cudaMemsetAsync(c->gemm_ws, 0, 64 * 1024, c->stream));  // split-K counters
   begin_session(c.get(), c->max_mb);
   *out = c.release();
   return ST_OK;
@@ -380,10 +429,10 @@ void ctx_destroy(st_ctx* c) {
 }
 
 st_status ctx_set_params(st_ctx* c, const float* host, size_t n) {
-  if (!c || !host) return set_error(ST_ERR_INPUT, "NULL argument");
+  if (!c || (!host && n)) return set_error(ST_ERR_INPUT, "NULL argument");
   if ((int64_t)n != c->P) return set_error(ST_ERR_SHAPE, "set_params: n = %zu but stage has %lld", n, (long long)c->P);
   ST_CUDA_TRY(cudaSetDevice(c->device));
-  ST_CUDA_TRY(cudaMemcpyAsync(c->W, host, n * 4, cudaMemcpyHostToDevice, c->stream));
+  if (n) ST_CUDA_TRY(cudaMemcpyAsync(c->W, host, n * 4, cudaMemcpyHostToDevice, c->stream));
   ST_CUDA_TRY(cudaMemsetAsync(c->V, 0, n * 4, c->stream));
   if (c->WF_out) ST_CUDA_TRY(cudaMemcpyAsync(c->WF_out, c->W, n * 4, cudaMemcpyDeviceToDevice, c->stream));
   if (c->WB_out) ST_CUDA_TRY(cudaMemcpyAsync(c->WB_out, c->W, n * 4, cudaMemcpyDeviceToDevice, c->stream));
@@ -478,7 +527,7 @@ static GemmArgs gargs(st_ctx* c, const LayerInfo& L) {
   g.n_in = L.n_in;
   g.n_out = L.n_out;
   g.work = c->gemm_ws;
-  g.work_bytes = gemm_workspace_bytes((int)c->R, c->max_width_in, c->max_width_out);
+  g.work_bytes = gemm_workspace_bytes((int)c->gemm_rows_max, c->gemm_in_max, c->gemm_out_max);
   g.stream = c->stream;
   return g;
 }
@@ -498,7 +547,7 @@ static GemmArgs gargs_rows(st_ctx* c, int rows, int n_in, int n_out) {
   g.n_in = n_in;
   g.n_out = n_out;
   g.work = c->gemm_ws;
-  g.work_bytes = gemm_workspace_bytes((int)c->R, c->max_width_in, c->max_width_out);
+  g.work_bytes = gemm_workspace_bytes((int)c->gemm_rows_max, c->gemm_in_max, c->gemm_out_max);
   g.stream = c->stream;
   return g;
 }
@@ -557,7 +606,22 @@ static st_status forward_compute(st_ctx* c, int64_t mb, const float* x_dev, cons
       out = slot + c->layers[l + 1].stash_off;
     else if (l + 1 == nl)
       out = c->last_stage ? c->logits : c->send_fwd;
-    if (L.kind == ST_LAYER_EMBED) {
+    if (L.kind == ST_LAYER_CONV) {
+      const int P = c->B * L.hw * L.hw;
+      {
+        Timed t(c, KC_LOSS);
+        ST_TRY(launch_im2col(in, c->B, L.hw, L.hw, L.n_in, c->conv_col, c->stream));
+        c->launches += 1;
+      }
+      Timed t(c, KC_GEMM_FWD);
+      ST_TRY(gemm_fwd(gargs_rows(c, P, 9 * L.n_in, L.n_out), c->conv_col, Wh + L.w_off,
+                      L.bias ? Wh + L.b_off : nullptr, out, L.act == ST_ACT_RELU));
+      c->launches += gemm_last_launches();
+    } else if (L.kind == ST_LAYER_POOL) {
+      Timed t(c, KC_LOSS);
+      ST_TRY(launch_maxpool_fwd(in, c->B, L.hw, L.hw, L.n_in, out, c->stream));
+      c->launches += 1;
+    } else if (L.kind == ST_LAYER_EMBED) {
       Timed t(c, KC_LOSS);
       ST_TRY(launch_embed_gather(Wh + L.w_off, reinterpret_cast<const int32_t*>(in), (int)c->R, L.n_out, out,
                                  c->stream));
@@ -661,7 +725,39 @@ static st_status backward_compute(st_ctx* c, int64_t mb, bool fused = false) {
       D = (l == 0) ? c->send_bwd : pp[next];
       if (D == dZ) D = pp[next ^= 1];
     }
-    if (L.kind == ST_LAYER_EMBED) {
+    const int producer_act = (l > 0) ? c->layers[l - 1].act : c->prev_act;
+    if (L.kind == ST_LAYER_POOL) {
+      if (D) {
+        Timed t(c, KC_LOSS);
+        ST_TRY(launch_maxpool_bwd(Ain, dZ, c->B, L.hw, L.hw, L.n_in, producer_act == ST_ACT_RELU, D, c->stream));
+        c->launches += 1;
+      }
+    } else if (L.kind == ST_LAYER_CONV) {
+      const int P = c->B * L.hw * L.hw;
+      {
+        Timed t(c, KC_LOSS);
+        ST_TRY(launch_im2col(Ain, c->B, L.hw, L.hw, L.n_in, c->conv_col, c->stream));
+        c->launches += 1;
+      }
+      if (D) {  // dcol = dZ·Wᵀ, dX = col2im(dcol) ⊙ ReLU mask of the producer of Ain
+        Timed t(c, KC_GEMM_DX);
+        ST_TRY(gemm_dx(gargs_rows(c, P, 9 * L.n_in, L.n_out), dZ, Wh + L.w_off, nullptr, c->conv_dcol));
+        c->launches += gemm_last_launches();
+        ST_TRY(launch_col2im(c->conv_dcol, c->B, L.hw, L.hw, L.n_in, producer_act == ST_ACT_RELU ? Ain : nullptr, D,
+                             c->stream));
+        c->launches += 1;
+      }
+      Timed t(c, KC_GEMM_DW);
+      const GemmArgs gw = gargs_rows(c, P, 9 * L.n_in, L.n_out);
+      if (fused) {
+        UpdateArgs bu{};
+        if (L.bias) bu = block_update(c, L.b_off, kc);
+        ST_TRY(gemm_dw_update(gw, c->conv_col, dZ, block_update(c, L.w_off, kc), bu, c->G + L.w_off));
+      } else {
+        ST_TRY(gemm_dw(gw, c->conv_col, dZ, c->G + L.w_off, L.bias ? c->G + L.b_off : nullptr));
+      }
+      c->launches += gemm_last_launches();
+    } else if (L.kind == ST_LAYER_EMBED) {
       Timed t(c, KC_GEMM_DW);
       ST_TRY(launch_embed_grad(dZ, reinterpret_cast<const int32_t*>(Ain), (int)c->R, L.n_in, L.n_out, c->G + L.w_off,
                                c->embed_scratch, c->stream));
@@ -671,7 +767,6 @@ static st_status backward_compute(st_ctx* c, int64_t mb, bool fused = false) {
     } else {
       if (D) {
         // ReLU mask of the layer that produced Ain (D12: ReLU'(0) = 0): 1[Z>0] == 1[ReLU(Z)>0]
-        const int producer_act = (l > 0) ? c->layers[l - 1].act : c->prev_act;
         Timed t(c, KC_GEMM_DX);
         ST_TRY(gemm_dx(gargs(c, L), dZ, Wh + L.w_off, producer_act == ST_ACT_RELU ? Ain : nullptr, D));
         c->launches += gemm_last_launches();
@@ -686,7 +781,7 @@ static st_status backward_compute(st_ctx* c, int64_t mb, bool fused = false) {
       }
       c->launches += gemm_last_launches();
     }
-    if (fused && L.kind != ST_LAYER_DENSE) {
+    if (fused && (L.kind == ST_LAYER_EMBED || L.kind == ST_LAYER_LSTM)) {
       Timed t(c, KC_UPDATE);
       UpdateArgs u = block_update(c, L.w_off, kc);
       ST_TRY(launch_update_predict(u.W, u.V, c->G + L.w_off, u.WF, u.WB, (size_t)L.n_params, kc, c->stream));

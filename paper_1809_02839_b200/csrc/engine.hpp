@@ -48,6 +48,8 @@ std::shared_ptr<LocalLink> make_local_link(int N);
 
 struct LayerInfo {
   int n_in, n_out, act, bias, kind;
+  int hw;             // conv / pool: input spatial side
+  int64_t win, wout;  // per-sample activation width in / out
   int64_t w_off;      // offset of W_l (dense), E (embed), W_ih (lstm) in the stage arena
   int64_t whh_off;    // lstm: offset of W_hh (−1 otherwise)
   int64_t b_off;      // offset of b_l (−1 if none)
@@ -66,6 +68,12 @@ st_status launch_embed_gather(const float* E, const int32_t* tok, int rows, int 
 int64_t embed_grad_scratch_bytes(int rows, int V);
 st_status launch_embed_grad(const float* dA, const int32_t* tok, int rows, int V, int D, float* gE, void* scratch,
                             cudaStream_t s);
+// conv / pool kernels (k_conv.cu)
+st_status launch_im2col(const float* X, int B, int H, int W, int C, float* col, cudaStream_t s);
+st_status launch_col2im(const float* dcol, int B, int H, int W, int C, const float* mask, float* dX, cudaStream_t s);
+st_status launch_maxpool_fwd(const float* X, int B, int H, int W, int C, float* Y, cudaStream_t s);
+st_status launch_maxpool_bwd(const float* X, const float* dY, int B, int H, int W, int C, int relu_mask, float* dX,
+                             cudaStream_t s);
 
 struct Profiler {
   bool on = false;
@@ -123,6 +131,10 @@ struct st_ctx {
   float* lstm_dc = nullptr;     // [B × H] dc_next
   float* lstm_dG = nullptr;     // [R × 4H] gate gradients of all steps
   void* embed_scratch = nullptr;
+  float* conv_col = nullptr;    // [P × 9·C_in] im2col of the current conv layer
+  float* conv_dcol = nullptr;   // [P × 9·C_in] its gradient
+  int64_t gemm_rows_max = 1;    // largest GEMM row count (R or conv pixel rows)
+  int gemm_in_max = 1, gemm_out_max = 1;
   float* ring_fwd = nullptr;    // LOCAL transport rings
   float* ring_bwd = nullptr;
   size_t ring_fwd_elems = 0, ring_bwd_elems = 0;

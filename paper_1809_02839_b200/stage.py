@@ -51,7 +51,8 @@ class Stage:
             return torch.empty(int(nbytes), dtype=torch.uint8, device=self.device)
 
         s = self.sizes
-        self.W, self.V, self.G = buf(s.w_bytes), buf(s.v_bytes), buf(s.g_bytes)
+        # a parameter-free stage (e.g. a lone max-pool) still binds 256-byte arenas
+        self.W, self.V, self.G = buf(max(256, s.w_bytes)), buf(max(256, s.v_bytes)), buf(max(256, s.g_bytes))
         self.WF, self.WB = buf(s.wf_bytes), buf(s.wb_bytes)
         self.stash, self.work = buf(max(256, s.stash_bytes)), buf(max(256, s.work_bytes))
         bufs = L.StBuffers(_ptr(self.W), _ptr(self.V), _ptr(self.G), _ptr(self.WF), _ptr(self.WB),

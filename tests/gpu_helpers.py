@@ -12,9 +12,10 @@ from oracle import spectrain_oracle as O
 
 def layers_of(model: sd.Model):
     import paper_1809_02839_b200 as st
-    kinds = {sd.DENSE: st.ST_LAYER_DENSE, sd.EMBED: st.ST_LAYER_EMBED, sd.LSTM: st.ST_LAYER_LSTM}
+    kinds = {sd.DENSE: st.ST_LAYER_DENSE, sd.EMBED: st.ST_LAYER_EMBED, sd.LSTM: st.ST_LAYER_LSTM,
+             sd.CONV: st.ST_LAYER_CONV, sd.POOL: st.ST_LAYER_POOL}
     return [(l.n_in, l.n_out, st.ST_ACT_RELU if l.act == sd.RELU else st.ST_ACT_NONE, 1 if l.bias else 0,
-             kinds[l.kind]) for l in model.layers]
+             kinds[l.kind], l.hw) for l in model.layers]
 
 
 def rel_l2(a, b) -> float:

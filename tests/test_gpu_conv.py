@@ -1,0 +1,53 @@
+"""VGG conv stages on the GPU (-m gpu): 3×3 convolution (im2col + tcgen05 GEMMs,
+col2im gather), ReLU, 2×2 max-pool and the FC head through the C-ABI, against the
+fp64 oracle. Gates: trace bit-exact, W and loss ≤ 1e-4 rel-L2."""
+import numpy as np
+import pytest
+import torch
+
+import synthdata as sd
+from tests.gpu_helpers import assert_parity, build_pipeline, oracle_run, rel_l2, run_pipeline
+
+pytestmark = pytest.mark.gpu
+
+
+@pytest.fixture(scope="module")
+def st():
+    if not torch.cuda.is_available():
+        pytest.fail("CUDA device required for -m gpu tests")
+    import paper_1809_02839_b200 as st
+    return st
+
+
+def _vgg_parity(st, model, batch, M, lr, seed=0, gemm=None):
+    w0, X, Y = sd.parity_inputs(model, M, batch, seed)
+    stages = build_pipeline(model, batch, lr, gemm=gemm, max_mb=M)
+    try:
+        res = run_pipeline(stages, w0, X, Y)
+    finally:
+        for s in stages:
+            s.close()
+    ref = oracle_run(model, w0, X, Y, lr)
+    assert_parity(model, res, ref)
+    assert rel_l2(np.concatenate(ref.W), np.concatenate(sd.widen(w0))) > 1e-4
+
+
+def test_vgg_small_4stage_tma_widths(st):
+    """conv(4→8) pool conv(8→16) conv(16→16) pool FC — channel counts whose im2col
+    widths (9·C) take the TMA / tcgen05 path; pools at stage boundaries and inside."""
+    model = sd.vgg(cfg=(8, "M", 16, 16, "M"), fc=(32,), classes=10, hw=16, in_ch=4, cuts=[1, 3, 5])
+    _vgg_parity(st, model, 8, 10, 0.05)
+
+
+def test_vgg_small_single_stage_rgb(st):
+    """RGB input (9·3 = 27-wide im2col: CUDA-core GEMM path) on one stage, and a
+    stage that starts with a pool (mask of the previous stage's conv applied there)."""
+    model = sd.vgg(cfg=(8, 8, "M", 16, "M"), fc=(16,), classes=10, hw=8, in_ch=3, cuts=[])
+    _vgg_parity(st, model, 4, 8, 0.05, seed=1)
+    model = sd.vgg(cfg=(8, "M", 16, "M"), fc=(16,), classes=10, hw=8, in_ch=4, cuts=[1, 2])
+    _vgg_parity(st, model, 4, 8, 0.05, seed=2)
+
+
+def test_vgg_simt_mode(st):
+    model = sd.vgg(cfg=(8, "M", 16, "M"), fc=(16,), classes=10, hw=8, in_ch=4, cuts=[2])
+    _vgg_parity(st, model, 4, 6, 0.05, seed=3, gemm=st.ST_GEMM_SIMT)
