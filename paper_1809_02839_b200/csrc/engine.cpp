@@ -33,10 +33,11 @@ struct Layout {
   bool first = true, last = true;
   // work offsets (bytes)
   int64_t off_send_fwd = -1, off_recv_bwd = -1, off_send_bwd = -1, off_logits = -1, off_dlogits = -1;
-  int64_t off_bufA = -1, off_bufB = -1, off_losses = -1, off_rowloss = -1, off_ring_fwd = -1, off_ring_bwd = -1;
+  int64_t off_bufA = -1, off_bufB = -1, off_bufC = -1, off_losses = -1, off_rowloss = -1, off_ring_fwd = -1, off_ring_bwd = -1;
   int64_t off_ws = -1, off_ystage = -1;
   int64_t off_lrec = -1, off_ldh = -1, off_ldc = -1, off_ldG = -1, off_escr = -1, off_col = -1, off_dcol = -1;
   int64_t gemm_rows = 1;
+  int64_t off_ws2 = -1;
   int gemm_in = 1, gemm_out = 1;  // largest GEMM operand widths (workspace sizing)
   int T = 1;
   int64_t R = 1;
@@ -212,6 +213,7 @@ st_status validate_and_layout(const st_config* c, Layout* L) {
   }
   L->off_bufA = take(R * width);
   L->off_bufB = take(R * width);
+  L->off_bufC = take(R * width);
   L->off_losses = take(c->max_minibatches);
   if (max_h > 0) {
     L->off_lrec = take(B * 4 * max_h);
@@ -236,6 +238,9 @@ st_status validate_and_layout(const st_config* c, Layout* L) {
   }
   L->off_ws = w;
   w += align_up(gemm_workspace_bytes((int)gemm_rows, L->gemm_in, L->gemm_out), kAlignBytes);
+  // the side stream (dW + update overlapped with the next dX) gets its own GEMM workspace
+  L->off_ws2 = w;
+  w += align_up(gemm_workspace_bytes((int)gemm_rows, L->gemm_in, L->gemm_out), kAlignBytes);
 
   st_sizes& z = L->sizes;
   z.params = L->P;
@@ -253,16 +258,17 @@ st_status validate_and_layout(const st_config* c, Layout* L) {
 struct Timed {
   st_ctx* c;
   int cls;
+  cudaStream_t s;
   cudaEvent_t b = nullptr;
-  Timed(st_ctx* ctx, int k) : c(ctx), cls(k) {
+  Timed(st_ctx* ctx, int k, cudaStream_t stream = nullptr) : c(ctx), cls(k), s(stream ? stream : ctx->stream) {
     if (!c->prof.on) return;
     cudaEvent_t a = get();
     b = get();
-    cudaEventRecord(a, c->stream);
+    cudaEventRecord(a, s);
     c->prof.pairs.push_back({cls, a, b});
   }
   ~Timed() {
-    if (b) cudaEventRecord(b, c->stream);
+    if (b) cudaEventRecord(b, s);
   }
   cudaEvent_t get() {
     if (!c->prof.pool.empty()) {
@@ -370,12 +376,14 @@ st_status ctx_init(const st_config* cfg, const st_buffers* bufs, void* stream, s
   c->gemm_out_max = L.gemm_out;
   c->bufA = at(L.off_bufA);
   c->bufB = at(L.off_bufB);
+  c->bufC = at(L.off_bufC);
   c->losses_dev = at(L.off_losses);
   c->ring_fwd = at(L.off_ring_fwd);
   c->ring_bwd = at(L.off_ring_bwd);
   c->ring_fwd_elems = L.ring_fwd_elems;
   c->ring_bwd_elems = L.ring_bwd_elems;
   c->gemm_ws = w + L.off_ws;
+  c->gemm_ws2 = w + L.off_ws2;
   c->stream = static_cast<cudaStream_t>(stream);
 
   if (c->transport_kind == ST_TRANSPORT_NCCL) {
@@ -383,10 +391,15 @@ st_status ctx_init(const st_config* cfg, const st_buffers* bufs, void* stream, s
     c->tp = make_nccl_transport(cfg->nccl_id, c->N, c->k, c->device, &e);
     if (e != ST_OK) return e;
   }
+  ST_CUDA_TRY(cudaStreamCreateWithFlags(&c->side, cudaStreamNonBlocking));
+  c->side_events.resize(c->layers.size() + 1);
+  for (auto& e : c->side_events) ST_CUDA_TRY(cudaEventCreateWithFlags(&e, cudaEventDisableTiming));
+  if (const char* e = getenv("ST_DWU_SMS")) c->dwu_sms = std::max(1, atoi(e));
   ST_CUDA_TRY(cudaMemsetAsync(c->V, 0, (size_t)c->P * 4, c->stream));
   ST_CUDA_TRY(cudaMemsetAsync(c->losses_dev, 0xff, (size_t)c->max_mb * 4, c->stream));  // NaN
   // GEMM workspace: split-K tile counters must start at zero (they self-reset afterwards)
   ST_CUDA_TRY(cudaMemsetAsync(c->gemm_ws, 0, 64 * 1024, c->stream));  // split-K counters
+  ST_CUDA_TRY(cudaMemsetAsync(c->gemm_ws2, 0, 64 * 1024, c->stream));
   begin_session(c.get(), c->max_mb);
   *out = c.release();
   return ST_OK;
@@ -425,6 +438,11 @@ void ctx_destroy(st_ctx* c) {
     cudaEventDestroy(p.b);
   }
   for (auto e : c->prof.pool) cudaEventDestroy(e);
+  if (c->side) {
+    cudaStreamSynchronize(c->side);
+    cudaStreamDestroy(c->side);
+  }
+  for (auto e : c->side_events) cudaEventDestroy(e);
   delete c;
 }
 
@@ -714,16 +732,40 @@ static st_status backward_compute(st_ctx* c, int64_t mb, bool fused = false) {
   const float* Wh = c->WB;  // Eq. 4 with s_B (D5: re-predicted from the current state)
   const float* dZ = c->last_stage ? c->dlogits : c->recv_bwd;
   const int nl = (int)c->layers.size();
-  float* pp[2] = {c->bufA, c->bufB};
+  // Gradient buffers rotate over 3 so that the dW + update of layer l (side stream,
+  // reading dZ_l) can overlap the dX of layer l−1 (main stream, writing dZ_{l−2}).
+  float* pp[3] = {c->bufA, c->bufB, c->bufC};
+  int reader[3] = {-1, -1, -1};  // layer whose side-stream dW last read pp[i] (event index)
   int next = 0;
+  bool side_busy = false;
+  auto join_side = [&]() -> st_status {
+    if (!side_busy) return ST_OK;
+    ST_CUDA_TRY(cudaEventRecord(c->side_events[nl], c->side));
+    ST_CUDA_TRY(cudaStreamWaitEvent(c->stream, c->side_events[nl], 0));
+    side_busy = false;
+    reader[0] = reader[1] = reader[2] = -1;
+    return ST_OK;
+  };
   for (int l = nl - 1; l >= 0; --l) {
     const LayerInfo& L = c->layers[l];
     float* Ain = layer_in(c, slot, (size_t)l);
     const bool need_dx = !(c->first_stage && l == 0) && L.kind != ST_LAYER_EMBED;
+    const bool overlap = fused && L.kind == ST_LAYER_DENSE;
+    if (!overlap) ST_TRY(join_side());
     float* D = nullptr;
+    int dslot = -1;
     if (need_dx) {
-      D = (l == 0) ? c->send_bwd : pp[next];
-      if (D == dZ) D = pp[next ^= 1];
+      if (l == 0) {
+        D = c->send_bwd;
+      } else {
+        dslot = next;
+        next = (next + 1) % 3;
+        D = pp[dslot];
+        if (reader[dslot] >= 0) {  // a side-stream dW still reads this buffer
+          ST_CUDA_TRY(cudaStreamWaitEvent(c->stream, c->side_events[reader[dslot]], 0));
+          reader[dslot] = -1;
+        }
+      }
     }
     const int producer_act = (l > 0) ? c->layers[l - 1].act : c->prev_act;
     if (L.kind == ST_LAYER_POOL) {
@@ -767,19 +809,38 @@ static st_status backward_compute(st_ctx* c, int64_t mb, bool fused = false) {
     } else {
       if (D) {
         // ReLU mask of the layer that produced Ain (D12: ReLU'(0) = 0): 1[Z>0] == 1[ReLU(Z)>0]
+        GemmArgs gx = gargs(c, L);
+        if (side_busy) gx.max_ctas = std::max(1, 148 - c->dwu_sms);  // share the GPU with the running dW
         Timed t(c, KC_GEMM_DX);
-        ST_TRY(gemm_dx(gargs(c, L), dZ, Wh + L.w_off, producer_act == ST_ACT_RELU ? Ain : nullptr, D));
+        ST_TRY(gemm_dx(gx, dZ, Wh + L.w_off, producer_act == ST_ACT_RELU ? Ain : nullptr, D));
         c->launches += gemm_last_launches();
       }
-      Timed t(c, KC_GEMM_DW);
       if (fused) {
+        // dW + update on the side stream, after this layer's dX (which reads WB_l)
+        ST_CUDA_TRY(cudaEventRecord(c->side_events[l], c->stream));
+        ST_CUDA_TRY(cudaStreamWaitEvent(c->side, c->side_events[l], 0));
+        GemmArgs gw = gargs(c, L);
+        gw.stream = c->side;
+        gw.work = c->gemm_ws2;
+        // a dX of layer l−1 will run concurrently only if that layer is DENSE and needs one
+        const bool more_dx = l > 0 && c->layers[l - 1].kind == ST_LAYER_DENSE && !(c->first_stage && l == 1);
+        if (more_dx) gw.max_ctas = c->dwu_sms;
         UpdateArgs bu{};
         if (L.bias) bu = block_update(c, L.b_off, kc);
-        ST_TRY(gemm_dw_update(gargs(c, L), Ain, dZ, block_update(c, L.w_off, kc), bu, c->G + L.w_off));
+        {
+          Timed t(c, KC_GEMM_DW, c->side);
+          ST_TRY(gemm_dw_update(gw, Ain, dZ, block_update(c, L.w_off, kc), bu, c->G + L.w_off));
+        }
+        c->launches += gemm_last_launches();
+        ST_CUDA_TRY(cudaEventRecord(c->side_events[l], c->side));
+        side_busy = true;
+        for (int i = 0; i < 3; ++i)
+          if (dZ == pp[i]) reader[i] = l;
       } else {
+        Timed t(c, KC_GEMM_DW);
         ST_TRY(gemm_dw(gargs(c, L), Ain, dZ, c->G + L.w_off, L.bias ? c->G + L.b_off : nullptr));
+        c->launches += gemm_last_launches();
       }
-      c->launches += gemm_last_launches();
     }
     if (fused && (L.kind == ST_LAYER_EMBED || L.kind == ST_LAYER_LSTM)) {
       Timed t(c, KC_UPDATE);
@@ -787,11 +848,9 @@ static st_status backward_compute(st_ctx* c, int64_t mb, bool fused = false) {
       ST_TRY(launch_update_predict(u.W, u.V, c->G + L.w_off, u.WF, u.WB, (size_t)L.n_params, kc, c->stream));
       c->launches += 1;
     }
-    if (D) {
-      dZ = D;
-      next ^= 1;
-    }
+    if (D) dZ = D;
   }
+  ST_TRY(join_side());
   return ST_OK;
 }
 

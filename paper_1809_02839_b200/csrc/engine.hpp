@@ -121,8 +121,12 @@ struct st_ctx {
   float* send_bwd = nullptr;  // [B × in_first]  (k > 0)
   float* logits = nullptr;    // [B × C]         (last stage)
   float* dlogits = nullptr;   // [B × C]
-  float* bufA = nullptr;      // [B × max width] backward ping-pong
+  float* bufA = nullptr;      // [R × max width] backward gradient buffers (3-way rotation)
   float* bufB = nullptr;
+  float* bufC = nullptr;
+  cudaStream_t side = nullptr;          // library-owned: dW + update overlapped with the next dX
+  std::vector<cudaEvent_t> side_events; // one per layer (dW done) + join
+  int dwu_sms = 80;                     // SM budget of an overlapped dW + update (measured best)
   float* losses_dev = nullptr;  // [max_mb]
   float* rowloss = nullptr;     // [B]
   int32_t* y_stage = nullptr;   // [R] labels staged from host (st_run_host)
@@ -139,6 +143,7 @@ struct st_ctx {
   float* ring_bwd = nullptr;
   size_t ring_fwd_elems = 0, ring_bwd_elems = 0;
   void* gemm_ws = nullptr;
+  void* gemm_ws2 = nullptr;  // workspace of the side stream
   cudaStream_t stream = nullptr;
 
   // program state

@@ -15,6 +15,7 @@ st_status tc_dw(const GemmArgs& g, const float* X, const float* dZ, float* G, fl
 int64_t tc_workspace_bytes(int B, int max_in, int max_out);
 int tc_last_launches();
 bool tc_dw_fusable(const GemmArgs& g, const float* X, const float* dZ);
+bool tc_dw_update_aligned(const UpdateArgs& w);
 st_status tc_dw_update(const GemmArgs& g, const float* X, const float* dZ, const UpdateArgs& w, const UpdateArgs& b);
 int simt_last_launches();
 
@@ -70,7 +71,7 @@ st_status gemm_dw(const GemmArgs& g, const float* X, const float* dZ, float* G, 
 st_status gemm_dw_update(const GemmArgs& g, const float* X, const float* dZ, const UpdateArgs& w,
                          const UpdateArgs& b, float* G_scratch) {
   ST_TRY(check(g));
-  if (tc_dw_fusable(g, X, dZ)) {
+  if (tc_dw_fusable(g, X, dZ) && tc_dw_update_aligned(w)) {
     st_status s = tc_dw_update(g, X, dZ, w, b);
     g_last_launches = tc_last_launches();
     return s;

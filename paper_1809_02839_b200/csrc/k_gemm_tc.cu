@@ -1084,7 +1084,7 @@ st_status launch(const GemmArgs& g, int M, int N, int K, const CUtensorMap& ma, 
 bool tma_ok(const void* p, int pitch) { return aligned16(p) && (pitch % 4) == 0; }
 
 // split-K plan shared by both kernels
-void plan_splits(TcParams& p, int M, int N, int K) {
+void plan_splits(TcParams& p, int M, int N, int K, int budget) {
   p.M = M;
   p.N = N;
   p.K = K;
@@ -1092,7 +1092,7 @@ void plan_splits(TcParams& p, int M, int N, int K) {
   const int mt = (M + BM - 1) / BM, nt = (N + BNMAX - 1) / BNMAX;
   const int tiles = mt * nt;
   int splits = 1;
-  if (tiles < num_sms()) splits = std::min(num_sms() / tiles, p.kb_total);
+  if (tiles < budget) splits = std::min(budget / tiles, p.kb_total);
   if (splits < 1) splits = 1;
   const size_t part_bytes = (size_t)BNMAX * BM * 4;
   const size_t ws_cap = (size_t)2 * 148 * BNMAX * BM * 4;
@@ -1108,7 +1108,7 @@ template <int EPI, bool A_MN>
 st_status launch_ts(const GemmArgs& g, int M, int N, int K, const CUtensorMap& ma, const float* Bact, float* out,
                     const float* aux, int relu) {
   TcParams p{};
-  plan_splits(p, M, N, K);
+  plan_splits(p, M, N, K, g.max_ctas > 0 ? std::min(g.max_ctas, num_sms()) : num_sms());
   p.out = out;
   p.aux = aux;
   p.relu = relu;
@@ -1207,6 +1207,9 @@ bool tc_dw_fusable(const GemmArgs& g, const float* X, const float* dZ) {
 st_status tc_dw_update(const GemmArgs& g, const float* X, const float* dZ, const UpdateArgs& w, const UpdateArgs& b) {
   return tc_dw_impl(g, X, dZ, nullptr, nullptr, &w, b.W ? &b : nullptr);
 }
+bool tc_dw_update_aligned(const UpdateArgs& w) {
+  return aligned16(w.W) && aligned16(w.V) && (!w.WF || aligned16(w.WF)) && (!w.WB || aligned16(w.WB));
+}
 st_status tc_dw_impl(const GemmArgs& g, const float* X, const float* dZ, float* G, float* gb, const UpdateArgs* upd,
                      const UpdateArgs* gb_upd) {
   if (!tma_ok(dZ, g.n_out) || !tma_ok(X, g.n_in) || !get_encode()) {
@@ -1246,7 +1249,7 @@ st_status tc_dw_impl(const GemmArgs& g, const float* X, const float* dZ, float* 
     if (upd) p.upd = *upd;
     p.idesc = make_idesc(p.bn, false, true);  // A from TMEM, B MN-major
     const int mt = (g.n_out + BM - 1) / BM, nt = (g.n_in + BNMAX - 1) / BNMAX;
-    const int grid = std::min(mt * nt, num_sms());
+    const int grid = std::min(mt * nt, g.max_ctas > 0 ? std::min(g.max_ctas, num_sms()) : num_sms());
     auto kern = upd ? (x3 ? tc_dw_kernel<true, true> : tc_dw_kernel<false, true>)
                     : (x3 ? tc_dw_kernel<true, false> : tc_dw_kernel<false, false>);
     static bool attr_set[4] = {false, false, false, false};

@@ -41,6 +41,7 @@ struct GemmArgs {
   void* work;  // split-K workspace (gemm_workspace_bytes), 64 KB zeroed counters first
   int64_t work_bytes;
   cudaStream_t stream;
+  int max_ctas = 0;  // CTA budget of the launch (0 = every SM); used to share the GPU between streams
 };
 int64_t gemm_workspace_bytes(int B, int max_in, int max_out);
 st_status gemm_fwd(const GemmArgs& g, const float* X, const float* W, const float* bias, float* Z, int relu);
