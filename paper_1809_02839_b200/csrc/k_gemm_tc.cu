@@ -52,7 +52,8 @@ struct TcParams {
   float* ws;         // split-K partials [splits][tiles][BNMAX][BM]
   int* counters;     // [tiles]
   uint32_t idesc;
-  int dev_flags;     // development only (ST_GEMM_DEV_FLAGS): bit0 skip MMAs, bit1 skip converter math
+  int dev_flags;     // development only (ST_GEMM_DEV_FLAGS): bit0 skip MMAs, bit1 skip converter math,
+                     // bit2 / bit3 skip B / A loads, bit4 skip TMEM stores, bit5 skip tcgen05.wait::st
   UpdateArgs upd;    // dW fused with K-B: weight-block targets (index n·M + m, like out)
 };
 
@@ -164,6 +165,52 @@ __device__ __forceinline__ void make_lo(const char* raw, char* lo, int chunks, i
 }
 
 
+// Development timeline (ST_GEMM_DEV_FLAGS bit 7): %globaltimer at fixed points of each
+// CTA, written into the unused upper half of the split-K counter block.
+__device__ __forceinline__ void dbg_mark(const TcParams& p, int slot) {
+  if (p.dev_flags & 128) {
+    uint64_t t;
+    asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
+    const int cta = blockIdx.x + gridDim.x * (blockIdx.y + gridDim.y * blockIdx.z);
+    if (cta < 240) reinterpret_cast<uint64_t*>(reinterpret_cast<char*>(p.counters) + 32768)[cta * 16 + slot] = t;
+  }
+}
+
+__device__ __forceinline__ void dbg_put(const TcParams& p, int slot, uint64_t v) {
+  if (p.dev_flags & 128) {
+    const int cta = blockIdx.x + gridDim.x * (blockIdx.y + gridDim.y * blockIdx.z);
+    if (cta < 240) reinterpret_cast<uint64_t*>(reinterpret_cast<char*>(p.counters) + 32768)[cta * 16 + slot] = v;
+  }
+}
+
+// 16 output columns n0c .. n0c + 15 of row m: fused bias + ReLU (fwd) or ReLU mask (dX).
+// All mask loads are issued before any store (out and aux may not alias, but the
+// compiler cannot know that): one memory latency per 16 columns, not per column.
+template <int EPI>
+__device__ __forceinline__ void epilogue_store16(const TcParams& p, int m, int n0c, const float* acc, float bias) {
+  const int nv = min(16, p.N - n0c);
+  if (EPI == EPI_DX && p.aux) {
+    float mk[16];
+#pragma unroll
+    for (int j = 0; j < 16; ++j) mk[j] = (j < nv) ? __ldg(p.aux + (size_t)(n0c + j) * p.M + m) : 0.f;
+#pragma unroll
+    for (int j = 0; j < 16; ++j)
+      if (j < nv) p.out[(size_t)(n0c + j) * p.M + m] = (mk[j] > 0.f) ? acc[j] : 0.f;
+    return;
+  }
+#pragma unroll
+  for (int j = 0; j < 16; ++j) {
+    if (j < nv) {
+      float v = acc[j];
+      if (EPI == EPI_FWD) {
+        v += bias;
+        if (p.relu) v = fmaxf(v, 0.f);
+      }
+      p.out[(size_t)(n0c + j) * p.M + m] = v;
+    }
+  }
+}
+
 // Epilogue (4 warps, 128 threads): TMEM lane = m (the warp's quadrant), columns = n.
 // Fused: fwd bias + ReLU, dX ReLU mask; split-K partials reduced in fixed split order
 // by the last CTA of the tile (deterministic), counters self-reset.
@@ -174,6 +221,7 @@ __device__ __forceinline__ void epilogue(const TcParams& p, uint32_t tmem, int w
   tc_fence_after();
   const int bn = p.bn;
   const int ctid = (warp - 2) * 32 + lane;
+  if (ctid == 0) dbg_mark(p, 3);
   const int quad = warp & 3;
   const int m = m0 + quad * 32 + lane;
   const uint32_t trow = tmem + ((uint32_t)(quad * 32) << 16);
@@ -188,75 +236,67 @@ __device__ __forceinline__ void epilogue(const TcParams& p, uint32_t tmem, int w
     __threadfence();
     asm volatile("bar.sync 1, 128;" ::: "memory");
     if (ctid == 0) {
+      dbg_mark(p, 4);
       const int prev = atomicAdd(p.counters + tile, 1);
       *last_flag = (prev == p.splits - 1);
     }
     asm volatile("bar.sync 1, 128;" ::: "memory");
+    if (ctid == 0) dbg_mark(p, 5);
     if (*last_flag) {
       __threadfence();
       const float bias = (EPI == EPI_FWD && p.aux && m < p.M) ? p.aux[m] : 0.f;
       // Fixed split order 0..S−1 (deterministic); this CTA's own partial comes from
-      // TMEM, the others from the workspace with 16 independent loads in flight.
-      for (int c = 0; c < bn; c += 16) {
-        float acc[16], mine[16];
-        tc_ld16(trow + c, mine);
+      // TMEM, the others from the workspace. 32 columns per chunk with every global load
+      // of the chunk (partials, dX mask) issued before the first use: the fix-up is
+      // latency-bound, so the chunk count is what costs.
+      for (int c = 0; c < bn; c += 32) {
+        float acc[32], mk[32];
+        const int nv = min(32, p.N - (n0 + c));
+        if (EPI == EPI_DX && p.aux && m < p.M) {
 #pragma unroll
-        for (int j = 0; j < 16; ++j) acc[j] = 0.f;
+          for (int j = 0; j < 32; ++j) mk[j] = (j < nv) ? __ldg(p.aux + (size_t)(n0 + c + j) * p.M + m) : 0.f;
+        }
+#pragma unroll
+        for (int j = 0; j < 32; ++j) acc[j] = 0.f;
         for (int s = 0; s < p.splits; ++s) {
+          float v[32];
           if (s == split) {
-#pragma unroll
-            for (int j = 0; j < 16; ++j) acc[j] += mine[j];
+            tc_ld16_nowait(trow + c, reinterpret_cast<uint32_t*>(v));
+            tc_ld16_nowait(trow + c + 16, reinterpret_cast<uint32_t*>(v + 16));
+            tc_wait_ld();
           } else {
             const float* src = p.ws + ((size_t)s * tiles + tile) * (BNMAX * BM) + (size_t)c * BM + quad * 32 + lane;
-            float v[16];
 #pragma unroll
-            for (int j = 0; j < 16; ++j) v[j] = __ldcg(src + (size_t)j * BM);
-#pragma unroll
-            for (int j = 0; j < 16; ++j) acc[j] += v[j];
+            for (int j = 0; j < 32; ++j) v[j] = (c + j < BNMAX) ? __ldcg(src + (size_t)j * BM) : 0.f;
           }
+#pragma unroll
+          for (int j = 0; j < 32; ++j) acc[j] += v[j];
         }
         if (m < p.M) {
 #pragma unroll
-          for (int j = 0; j < 16; ++j) {
-            const int n = n0 + c + j;
-            if (n < p.N) {
-              const size_t o = (size_t)n * p.M + m;
+          for (int j = 0; j < 32; ++j) {
+            if (j < nv) {
               float v = acc[j];
               if (EPI == EPI_FWD) {
                 v += bias;
                 if (p.relu) v = fmaxf(v, 0.f);
               } else if (EPI == EPI_DX) {
-                if (p.aux && !(p.aux[o] > 0.f)) v = 0.f;
+                if (p.aux && !(mk[j] > 0.f)) v = 0.f;
               }
-              p.out[o] = v;
+              p.out[(size_t)(n0 + c + j) * p.M + m] = v;
             }
           }
         }
       }
       if (ctid == 0) p.counters[tile] = 0;  // self-reset for the next launch
+      if (ctid == 0) dbg_mark(p, 6);
     }
   } else {
     const float bias = (EPI == EPI_FWD && p.aux && m < p.M) ? p.aux[m] : 0.f;
     for (int c = 0; c < bn; c += 16) {
       float v[16];
       tc_ld16(trow + c, v);
-      if (m < p.M) {
-#pragma unroll
-        for (int j = 0; j < 16; ++j) {
-          const int n = n0 + c + j;
-          if (n < p.N) {
-            const size_t o = (size_t)n * p.M + m;
-            float x = v[j];
-            if (EPI == EPI_FWD) {
-              x += bias;
-              if (p.relu) x = fmaxf(x, 0.f);
-            } else if (EPI == EPI_DX) {
-              if (p.aux && !(p.aux[o] > 0.f)) x = 0.f;
-            }
-            p.out[o] = x;
-          }
-        }
-      }
+      if (m < p.M) epilogue_store16<EPI>(p, m, n0 + c, v, bias);
     }
   }
 }
@@ -398,7 +438,7 @@ __global__ void __launch_bounds__(kThreads, 1)
 // ============================================================================
 constexpr int TS_RA = 6;                 // weight (A) raw ring stages, 16 KB each
 constexpr int TS_RB = 3;                 // activation (B) ring stages, hi + lo ≤ 32 KB
-constexpr int TS_TA = 3;                 // TMEM A slots (64 columns: 32 hi + 32 lo)
+constexpr int TS_TA = 6;                 // TMEM A slots (64 columns: 32 hi + 32 lo): 128 + 6·64 = 512
 constexpr int TS_THREADS = 224;          // 7 warps
 constexpr int TS_B_STAGE = 2 * BNMAX * BK * 4;
 constexpr int ts_smem_bytes() { return TS_RA * TILE_BYTES + TS_RB * TS_B_STAGE + 1024 + 512; }
@@ -449,6 +489,7 @@ __global__ void __launch_bounds__(TS_THREADS, 1)
   const int kb0 = split * p.kb_per_split;
   const int nkb = min(p.kb_total, kb0 + p.kb_per_split) - kb0;
   const int bn = p.bn;
+  if (threadIdx.x == 0) dbg_mark(p, 0);
 
   if (threadIdx.x == 0) {
     for (int s = 0; s < TS_RA; ++s) {
@@ -478,6 +519,7 @@ __global__ void __launch_bounds__(TS_THREADS, 1)
   tc_fence_before();
   __syncthreads();
   tc_fence_after();
+  if (threadIdx.x == 0) dbg_mark(p, 1);
   const uint32_t tmem = *tmem_slot;      // accumulator: columns [0, 128)
   const uint32_t tmemA = tmem + BNMAX;   // A ring: columns [128, 128 + 64·TA)
 
@@ -544,6 +586,7 @@ __global__ void __launch_bounds__(TS_THREADS, 1)
         tc_commit(t_empty + 8 * ta);
       }
       tc_commit(acc_full);
+      dbg_mark(p, 2);
     }
   } else {
     // ---------------- converter (warps 2..5): raw weight tile → TMEM hi / lo
@@ -587,15 +630,18 @@ __global__ void __launch_bounds__(TS_THREADS, 1)
       mbar_wait(t_empty + 8 * ta, ((i / TS_TA) & 1) ^ 1);
       tc_fence_after();
       const uint32_t taddr = tmemA + ta * 64 + ((uint32_t)(quad * 32) << 16);
-      tc_st32(taddr, hi);
-      tc_st32(taddr + 32, lo);
-      asm volatile("tcgen05.wait::st.sync.aligned;" ::: "memory");
+      if (!(p.dev_flags & 16)) {
+        tc_st32(taddr, hi);
+        tc_st32(taddr + 32, lo);
+        if (!(p.dev_flags & 32)) asm volatile("tcgen05.wait::st.sync.aligned;" ::: "memory");
+      }
       tc_fence_before();
       __syncwarp();
       if (lane == 0) mbar_arrive(t_full + 8 * ta);
     }
     epilogue<EPI>(p, tmem, warp, lane, m0, n0, split, n_tile * gridDim.x + m_tile, gridDim.x * gridDim.y,
                   last_flag, acc_full);
+    if (threadIdx.x == 64) dbg_mark(p, 7);
   }
 
   tc_fence_before();
@@ -603,6 +649,277 @@ __global__ void __launch_bounds__(TS_THREADS, 1)
   if (warp == 1) {
     tc_fence_after();
     asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, 512;" ::"r"(tmem));
+    if (lane == 0) dbg_mark(p, 8);
+  }
+}
+
+// ============================================================================
+// FP32X3 forward / dX kernel, CTA-pair form (tcgen05.mma.cta_group::2).
+//
+// Same dataflow as tc_ts_kernel, but a 2-CTA cluster computes one 256 × bn tile:
+// each CTA converts ITS 128 weight rows into ITS TMEM (A-from-TMEM) and stages bn/2
+// activation rows (hi + lo) in its smem; the leader CTA (rank 0) issues M = 256 MMAs
+// that read both CTAs' operands and write each CTA's 128 accumulator lanes. Measured
+// (tools/probe_2cta.cu): 64 cycles per M=256, N=128, K=8 MMA — 128 × 128 × 8 per SM
+// every 64 cycles, against 94 for the single-CTA TS MMA.
+// Cross-CTA protocol: B TMA loads of both CTAs complete on the LEADER's b_full
+// (.cta_group::2 TMA), converters of both CTAs arrive remotely on the leader's t_full,
+// and the leader's commits multicast to the b_empty / t_empty / acc_full barriers of both.
+// ============================================================================
+constexpr int TS2_RB = 4;                         // activation ring stages (hi + lo of bn/2 rows ≤ 16 KB)
+constexpr int TS2_B_STAGE = 2 * (BNMAX / 2) * BK * 4;
+constexpr int ts2_smem_bytes() { return TS_RA * TILE_BYTES + TS2_RB * TS2_B_STAGE + 1024 + 512; }
+
+__device__ __forceinline__ uint32_t cluster_rank() {
+  uint32_t r;
+  asm volatile("mov.u32 %0, %%cluster_ctarank;" : "=r"(r));
+  return r;
+}
+// shared::cluster address of the same smem offset in CTA `rank` of the cluster
+__device__ __forceinline__ uint32_t map_to_rank(uint32_t saddr, uint32_t rank) {
+  uint32_t r;
+  asm volatile("mapa.shared::cluster.u32 %0, %1, %2;" : "=r"(r) : "r"(saddr), "r"(rank));
+  return r;
+}
+__device__ __forceinline__ void mbar_arrive_cluster(uint32_t cluster_bar) {
+  asm volatile("mbarrier.arrive.shared::cluster.b64 _, [%0];" ::"r"(cluster_bar) : "memory");
+}
+// TMA into this CTA's smem, completion signalled on an mbarrier of either CTA of the pair
+__device__ __forceinline__ void tma_load_2d_pair(uint32_t dst, const CUtensorMap* map, int c0, int c1,
+                                                 uint32_t cluster_bar) {
+  asm volatile(
+      "cp.async.bulk.tensor.2d.cta_group::2.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1, {%2, %3}], "
+      "[%4];" ::"r"(dst),
+      "l"(reinterpret_cast<uint64_t>(map)), "r"(c0), "r"(c1), "r"(cluster_bar)
+      : "memory");
+}
+__device__ __forceinline__ void tc_mma_ts2(uint32_t tmem_d, uint32_t tmem_a, uint64_t bdesc, uint32_t idesc,
+                                           uint32_t accum) {
+  asm volatile(
+      "{\n .reg .pred p;\n setp.ne.b32 p, %4, 0;\n tcgen05.mma.cta_group::2.kind::tf32 [%0], [%1], %2, %3, p;\n}" ::"r"(
+          tmem_d),
+      "r"(tmem_a), "l"(bdesc), "r"(idesc), "r"(accum)
+      : "memory");
+}
+__device__ __forceinline__ void tc_commit2(uint32_t bar) {
+  asm volatile(
+      "tcgen05.commit.cta_group::2.mbarrier::arrive::one.shared::cluster.multicast::cluster.b64 [%0], %1;" ::"r"(bar),
+      "h"((uint16_t)3)
+      : "memory");
+}
+__device__ __forceinline__ void cluster_sync_all() {
+  asm volatile("barrier.cluster.arrive.release.aligned;\nbarrier.cluster.wait.acquire.aligned;" ::: "memory");
+}
+
+template <int EPI, bool A_MN>
+__global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(TS_THREADS, 1)
+    tc_ts2_kernel(const __grid_constant__ CUtensorMap mapA, const __grid_constant__ CUtensorMap mapB,
+                  const __grid_constant__ CUtensorMap mapBlo, TcParams p) {
+  extern __shared__ __align__(1024) uint8_t smem_raw[];
+  char* smem = reinterpret_cast<char*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
+  char* ringA = smem;
+  char* ringB = smem + TS_RA * TILE_BYTES;
+  uint64_t* bars = reinterpret_cast<uint64_t*>(ringB + TS2_RB * TS2_B_STAGE);
+  const uint32_t a_full = smem_u32(bars);          // TMA landed (A, own)              [RA]
+  const uint32_t a_free = a_full + 8 * TS_RA;      // converter read it (own)          [RA]
+  const uint32_t b_full = a_free + 8 * TS_RA;      // B hi + lo of BOTH CTAs (leader)  [RB]
+  const uint32_t b_empty = b_full + 8 * TS2_RB;    // MMA done with B (multicast)      [RB]
+  const uint32_t t_full = b_empty + 8 * TS2_RB;    // TMEM A slots of both (leader)    [TA]
+  const uint32_t t_empty = t_full + 8 * TS_TA;     // MMA done with TMEM (multicast)   [TA]
+  const uint32_t acc_full = t_empty + 8 * TS_TA;   // accumulator complete (multicast)
+  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(bars + 2 * TS_RA + 2 * TS2_RB + 2 * TS_TA + 1);
+  int* last_flag = reinterpret_cast<int*>(tmem_slot + 1);
+
+  const int warp = threadIdx.x >> 5;
+  const int lane = threadIdx.x & 31;
+  const uint32_t rank = cluster_rank();
+  const int m_tile = blockIdx.x, n_tile = blockIdx.y, split = blockIdx.z;
+  const int m0 = m_tile * BM, n0 = n_tile * BNMAX;
+  const int kb0 = split * p.kb_per_split;
+  const int nkb = min(p.kb_total, kb0 + p.kb_per_split) - kb0;
+  const int bn = p.bn;
+  const int bh = bn / 2;  // activation rows staged by this CTA
+  if (threadIdx.x == 0) dbg_mark(p, 0);
+
+  if (threadIdx.x == 0) {
+    for (int s = 0; s < TS_RA; ++s) {
+      mbar_init(a_full + 8 * s, 1);
+      mbar_init(a_free + 8 * s, 4);
+    }
+    for (int s = 0; s < TS2_RB; ++s) {
+      mbar_init(b_full + 8 * s, 1);
+      mbar_init(b_empty + 8 * s, 1);
+    }
+    for (int s = 0; s < TS_TA; ++s) {
+      mbar_init(t_full + 8 * s, 8);
+      mbar_init(t_empty + 8 * s, 1);
+    }
+    mbar_init(acc_full, 1);
+    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+  }
+  if (warp == 1) {
+    asm volatile("tcgen05.alloc.cta_group::2.sync.aligned.shared::cta.b32 [%0], 512;" ::"r"(smem_u32(tmem_slot)));
+    asm volatile("tcgen05.relinquish_alloc_permit.cta_group::2.sync.aligned;");
+  }
+  if (warp == 0 && lane == 0) {
+    asm volatile("prefetch.tensormap [%0];" ::"l"(reinterpret_cast<uint64_t>(&mapA)) : "memory");
+    asm volatile("prefetch.tensormap [%0];" ::"l"(reinterpret_cast<uint64_t>(&mapB)) : "memory");
+    asm volatile("prefetch.tensormap [%0];" ::"l"(reinterpret_cast<uint64_t>(&mapBlo)) : "memory");
+  }
+  tc_fence_before();
+  cluster_sync_all();  // barriers of both CTAs initialised, TMEM allocated
+  tc_fence_after();
+  const uint32_t tmem = *tmem_slot;
+  const uint32_t tmemA = tmem + BNMAX;
+  if (threadIdx.x == 0) dbg_mark(p, 1);
+
+  if (warp == 0) {
+    // ---------------- TMA producer, weights (A): this CTA's 128 rows
+    if (lane == 0) {
+      const bool oob = m0 >= p.M;  // padding CTA of an odd tile count: rows masked at the end
+      uint64_t w_f = 0;
+      for (int i = 0; i < nkb; ++i) {
+        const int s = i % TS_RA;
+        const uint64_t c0 = clock64();
+        mbar_wait(a_free + 8 * s, ((i / TS_RA) & 1) ^ 1);
+        w_f += clock64() - c0;
+        const uint32_t full = a_full + 8 * s;
+        if (oob || (p.dev_flags & 8)) {
+          mbar_arrive(full);
+          continue;
+        }
+        mbar_expect_tx(full, TILE_BYTES);
+        const int k0 = (kb0 + i) * BK;
+        const uint32_t dA = smem_u32(ringA + s * TILE_BYTES);
+        if (A_MN) {
+#pragma unroll
+          for (int c = 0; c < BM / 32; ++c) tma_load_2d(dA + c * 4096, &mapA, m0 + 32 * c, k0, full);
+        } else {
+          tma_load_2d(dA, &mapA, k0, m0, full);
+        }
+      }
+      dbg_put(p, 15, w_f);
+    }
+  } else if (warp == 6) {
+    // ---------------- TMA producer, activations: rows n0 + rank·bn/2 .. +bn/2 (hi + lo)
+    if (lane == 0) {
+      const uint32_t bytes = (uint32_t)(2 * 2 * bh * BK * 4);  // both CTAs, hi + lo
+      for (int i = 0; i < nkb; ++i) {
+        const int s = i % TS2_RB;
+        mbar_wait(b_empty + 8 * s, ((i / TS2_RB) & 1) ^ 1);
+        const uint32_t full_leader = map_to_rank(b_full + 8 * s, 0);
+        if (rank == 0) mbar_expect_tx(b_full + 8 * s, bytes);
+        const int k0 = (kb0 + i) * BK;
+        const uint32_t dB = smem_u32(ringB + s * TS2_B_STAGE);
+        tma_load_2d_pair(dB, &mapB, k0, n0 + (int)rank * bh, full_leader);
+        tma_load_2d_pair(dB + (BNMAX / 2) * BK * 4, &mapBlo, k0, n0 + (int)rank * bh, full_leader);
+      }
+    }
+  } else if (warp == 1) {
+    // ---------------- MMA issuer (leader CTA only)
+    if (rank == 0 && lane == 0) {
+      uint64_t w_t = 0, w_b = 0, w_i = 0;
+      for (int i = 0; i < nkb; ++i) {
+        const int sb = i % TS2_RB, ta = i % TS_TA;
+        const uint64_t c0 = clock64();
+        mbar_wait(t_full + 8 * ta, (i / TS_TA) & 1);
+        const uint64_t c1 = clock64();
+        mbar_wait(b_full + 8 * sb, (i / TS2_RB) & 1);
+        const uint64_t c2 = clock64();
+        w_t += c1 - c0;
+        w_b += c2 - c1;
+        tc_fence_after();
+        const uint32_t b_hi = smem_u32(ringB + sb * TS2_B_STAGE), b_lo = b_hi + (BNMAX / 2) * BK * 4;
+        const uint32_t a_hi = tmemA + ta * 64, a_lo = a_hi + 32;
+#pragma unroll
+        for (int kk = 0; kk < BK / 8; ++kk) {
+          if (p.dev_flags & 1) break;
+          const uint32_t acc = (i > 0 || kk > 0) ? 1u : 0u;
+          tc_mma_ts2(tmem, a_hi + kk * 8, desc_kmajor(b_hi + kk * 32), p.idesc, acc);
+          tc_mma_ts2(tmem, a_lo + kk * 8, desc_kmajor(b_hi + kk * 32), p.idesc, 1u);
+          tc_mma_ts2(tmem, a_hi + kk * 8, desc_kmajor(b_lo + kk * 32), p.idesc, 1u);
+        }
+        tc_commit2(b_empty + 8 * sb);
+        tc_commit2(t_empty + 8 * ta);
+        w_i += clock64() - c2;
+      }
+      tc_commit2(acc_full);
+      dbg_mark(p, 2);
+      dbg_put(p, 9, w_t);
+      dbg_put(p, 10, w_b);
+      dbg_put(p, 11, w_i);
+    }
+  } else {
+    // ---------------- converter (warps 2..5): raw weight tile → this CTA's TMEM hi / lo
+    const int quad = warp & 3;
+    const int r = quad * 32 + lane;
+    uint64_t w_a = 0, w_e = 0, w_s = 0;
+    for (int i = 0; i < nkb; ++i) {
+      const int s = i % TS_RA, ta = i % TS_TA;
+      const uint64_t c0 = clock64();
+      mbar_wait(a_full + 8 * s, (i / TS_RA) & 1);
+      w_a += clock64() - c0;
+      const char* t = ringA + s * TILE_BYTES;
+      uint32_t hi[32], lo[32];
+      if (p.dev_flags & 2) {
+#pragma unroll
+        for (int k = 0; k < 32; ++k) hi[k] = lo[k] = 0;
+      } else if (A_MN) {
+        const char* box = t + (r >> 5) * 4096;
+#pragma unroll
+        for (int k = 0; k < 32; ++k) {
+          const float x = *reinterpret_cast<const float*>(box + k * 128 + ((((r & 31) >> 3) ^ (k & 3)) << 5) +
+                                                          (r & 7) * 4);
+          hi[k] = __float_as_uint(x);
+          lo[k] = __float_as_uint(lo_part(x));
+        }
+      } else {
+#pragma unroll
+        for (int j = 0; j < 8; ++j) {
+          const float4 v = *reinterpret_cast<const float4*>(t + r * 128 + ((j ^ (r & 7)) << 4));
+          hi[4 * j + 0] = __float_as_uint(v.x);
+          hi[4 * j + 1] = __float_as_uint(v.y);
+          hi[4 * j + 2] = __float_as_uint(v.z);
+          hi[4 * j + 3] = __float_as_uint(v.w);
+          lo[4 * j + 0] = __float_as_uint(lo_part(v.x));
+          lo[4 * j + 1] = __float_as_uint(lo_part(v.y));
+          lo[4 * j + 2] = __float_as_uint(lo_part(v.z));
+          lo[4 * j + 3] = __float_as_uint(lo_part(v.w));
+        }
+      }
+      __syncwarp();
+      if (lane == 0) mbar_arrive(a_free + 8 * s);
+      const uint64_t c1 = clock64();
+      mbar_wait(t_empty + 8 * ta, ((i / TS_TA) & 1) ^ 1);
+      const uint64_t c2 = clock64();
+      w_e += c2 - c1;
+      tc_fence_after();
+      const uint32_t taddr = tmemA + ta * 64 + ((uint32_t)(quad * 32) << 16);
+      if (!(p.dev_flags & 16)) {
+        tc_st32(taddr, hi);
+        tc_st32(taddr + 32, lo);
+        if (!(p.dev_flags & 32)) asm volatile("tcgen05.wait::st.sync.aligned;" ::: "memory");
+      }
+      tc_fence_before();
+      __syncwarp();
+      if (lane == 0) mbar_arrive_cluster(map_to_rank(t_full + 8 * ta, 0));
+      w_s += clock64() - c2;
+    }
+    if (threadIdx.x == 64) {
+      dbg_put(p, 12, w_a);
+      dbg_put(p, 13, w_e);
+      dbg_put(p, 14, w_s);
+    }
+    epilogue<EPI>(p, tmem, warp, lane, m0, n0, split, n_tile * gridDim.x + m_tile, gridDim.x * gridDim.y,
+                  last_flag, acc_full);
+    if (threadIdx.x == 64) dbg_mark(p, 7);
+  }
+
+  tc_fence_before();
+  cluster_sync_all();  // no CTA leaves while the pair's MMAs may still touch its smem / TMEM
+  if (warp == 1) {
+    tc_fence_after();
+    asm volatile("tcgen05.dealloc.cta_group::2.sync.aligned.b32 %0, 512;" ::"r"(tmem));
   }
 }
 
@@ -1010,7 +1327,7 @@ int num_sms() {
   return sms;
 }
 
-uint32_t make_idesc(int bn, bool a_mn, bool b_mn) {
+uint32_t make_idesc(int bn, bool a_mn, bool b_mn, int mma_m = BM) {
   uint32_t d = 0;
   d |= 1u << 4;                       // D format F32
   d |= 2u << 7;                       // A format TF32
@@ -1018,7 +1335,7 @@ uint32_t make_idesc(int bn, bool a_mn, bool b_mn) {
   d |= (a_mn ? 1u : 0u) << 15;        // A major (0 = K, 1 = MN)
   d |= (b_mn ? 1u : 0u) << 16;        // B major
   d |= (uint32_t)(bn >> 3) << 17;     // N >> 3
-  d |= (uint32_t)(BM >> 4) << 24;     // M >> 4
+  d |= (uint32_t)(mma_m >> 4) << 24;  // M >> 4
   return d;
 }
 
@@ -1102,19 +1419,36 @@ void plan_splits(TcParams& p, int M, int N, int K, int budget) {
   p.bn = bn_for(N);
 }
 
-// FP32X3 fwd / dX through the TMEM-A kernel. Bact: the activation operand [N rows × K]
+// CTA-pair kernel for fwd / dX (ST_GEMM_PAIR=1). Off by default: both forms run into the
+// 1000 W board power cap on these GEMMs (tools/gemm_power.py: ~1.72 GHz single, ~1.77 GHz
+// pair, same time per GEMM), so the pair's faster MMA issue buys no wall time.
+bool use_pair() {
+  static int f = -1;
+  if (f < 0) {
+    const char* e = getenv("ST_GEMM_PAIR");
+    f = e ? atoi(e) : 0;
+  }
+  return f != 0;
+}
+
+// FP32X3 fwd / dX through the TMEM-A kernels. Bact: the activation operand [N rows × K]
 // (row pitch K); its lo part goes to the workspace tail.
 template <int EPI, bool A_MN>
 st_status launch_ts(const GemmArgs& g, int M, int N, int K, const CUtensorMap& ma, const float* Bact, float* out,
                     const float* aux, int relu) {
   TcParams p{};
-  plan_splits(p, M, N, K, g.max_ctas > 0 ? std::min(g.max_ctas, num_sms()) : num_sms());
+  const bool pair = use_pair();
+  const int budget = g.max_ctas > 0 ? std::min(g.max_ctas, num_sms()) : num_sms();
+  // pair: the m-tile count is padded to even (the padding CTA's rows are masked)
+  const int mt = (M + BM - 1) / BM, mt_grid = pair ? (mt + 1) / 2 * 2 : mt;
+  plan_splits(p, mt_grid * BM, N, K, pair ? budget / 2 * 2 : budget);
+  p.M = M;
   p.out = out;
   p.aux = aux;
   p.relu = relu;
   p.counters = reinterpret_cast<int*>(g.work);
   p.ws = reinterpret_cast<float*>(static_cast<char*>(g.work) + kCounterBytes);
-  p.idesc = make_idesc(p.bn, false, false);
+  p.idesc = make_idesc(p.bn, false, false, pair ? 2 * BM : BM);
   p.dev_flags = dev_flags();
   float* blo = reinterpret_cast<float*>(static_cast<char*>(g.work) + kCounterBytes +
                                         (size_t)2 * 148 * BNMAX * BM * 4);
@@ -1122,18 +1456,29 @@ st_status launch_ts(const GemmArgs& g, int M, int N, int K, const CUtensorMap& m
   split_lo_kernel<<<std::min<size_t>(4 * 148, (n4 + 255) / 256), 256, 0, g.stream>>>(
       reinterpret_cast<const float4*>(Bact), reinterpret_cast<float4*>(blo), n4);
   ST_CUDA_TRY(cudaGetLastError());
+  const int brows = pair ? p.bn / 2 : p.bn;
   CUtensorMap mb, mblo;
-  if (!make_map(&mb, Bact, K, N, K, p.bn, false) || !make_map(&mblo, blo, K, N, K, p.bn, false))
+  if (!make_map(&mb, Bact, K, N, K, brows, false) || !make_map(&mblo, blo, K, N, K, brows, false))
     return set_error(ST_ERR_CUDA, "cuTensorMapEncodeTiled failed (activation operand)");
-  const int mt = (M + BM - 1) / BM, nt = (N + BNMAX - 1) / BNMAX;
-  dim3 grid(mt, nt, p.splits);
-  auto kern = tc_ts_kernel<EPI, A_MN>;
-  static bool attr_set = false;
-  if (!attr_set) {
-    ST_CUDA_TRY(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, ts_smem_bytes()));
-    attr_set = true;
+  const int nt = (N + BNMAX - 1) / BNMAX;
+  dim3 grid(mt_grid, nt, p.splits);
+  if (pair) {
+    auto kern = tc_ts2_kernel<EPI, A_MN>;
+    static bool attr_set = false;
+    if (!attr_set) {
+      ST_CUDA_TRY(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, ts2_smem_bytes()));
+      attr_set = true;
+    }
+    kern<<<grid, TS_THREADS, ts2_smem_bytes(), g.stream>>>(ma, mb, mblo, p);
+  } else {
+    auto kern = tc_ts_kernel<EPI, A_MN>;
+    static bool attr_set = false;
+    if (!attr_set) {
+      ST_CUDA_TRY(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, ts_smem_bytes()));
+      attr_set = true;
+    }
+    kern<<<grid, TS_THREADS, ts_smem_bytes(), g.stream>>>(ma, mb, mblo, p);
   }
-  kern<<<grid, TS_THREADS, ts_smem_bytes(), g.stream>>>(ma, mb, mblo, p);
   ST_CUDA_TRY(cudaGetLastError());
   g_launches = 2;
   return ST_OK;
