@@ -55,6 +55,7 @@ struct TcParams {
   int dev_flags;     // development only (ST_GEMM_DEV_FLAGS): bit0 skip MMAs, bit1 skip converter math,
                      // bit2 / bit3 skip B / A loads, bit4 skip TMEM stores, bit5 skip tcgen05.wait::st
   UpdateArgs upd;    // dW fused with K-B: weight-block targets (index n·M + m, like out)
+  int wv_stream;     // fused K-B: W / V chunks staged in smem by TMA (mapW / mapV valid)
 };
 
 // ------------------------------------------------------------------ PTX helpers
@@ -107,6 +108,11 @@ __device__ __forceinline__ void tc_ld16_nowait(uint32_t taddr, uint32_t* r) {
       : "=r"(r[0]), "=r"(r[1]), "=r"(r[2]), "=r"(r[3]), "=r"(r[4]), "=r"(r[5]), "=r"(r[6]), "=r"(r[7]), "=r"(r[8]),
         "=r"(r[9]), "=r"(r[10]), "=r"(r[11]), "=r"(r[12]), "=r"(r[13]), "=r"(r[14]), "=r"(r[15])
       : "r"(taddr));
+}
+__device__ __forceinline__ void tc_ld8_nowait(uint32_t taddr, uint32_t* r) {
+  asm volatile("tcgen05.ld.sync.aligned.32x32b.x8.b32 {%0,%1,%2,%3,%4,%5,%6,%7}, [%8];"
+               : "=r"(r[0]), "=r"(r[1]), "=r"(r[2]), "=r"(r[3]), "=r"(r[4]), "=r"(r[5]), "=r"(r[6]), "=r"(r[7])
+               : "r"(taddr));
 }
 __device__ __forceinline__ void tc_wait_ld() { asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory"); }
 __device__ __forceinline__ void tc_ld16(uint32_t taddr, float* v) {
@@ -1050,32 +1056,43 @@ __device__ __forceinline__ void update_block16_vec(const UpdateArgs& u, size_t M
 // Each CTA walks a contiguous range of 128 × 128 output tiles in m-major order.
 // The A operand (dZᵀ rows of the current m-tile, all of K) is staged once per m-tile
 // (TMA → smem), split by converter warps into hi / lo and kept RESIDENT IN TMEM
-// (A-from-TMEM MMA); B (X columns, hi + lo precomputed) streams through a 3-stage smem
-// ring. Keeping A out of smem holds the CTA at 160 KB of shared memory, which leaves
-// enough L1 for the epilogue's in-flight loads (tools/probe_tile_stream.cu: the same
-// stream runs at 5.4 TB/s with ≤ 160 KB of smem and 4.0 TB/s with 220 KB).
-// TMEM: accumulators [0, 256) (two buffers), A hi [256, 384), A lo [384, 512).
-// Epilogue: 16 warps in two groups, group g drains accumulator g (tiles local ≡ g mod 2);
-// with kUPD it applies the K-B update in place of storing G (float4 via quad transposes).
+// (A-from-TMEM MMA); B (X columns, hi + lo precomputed) streams through a 2-stage smem
+// ring. TMEM: accumulators [0, 256) (two buffers), A hi [256, 384), A lo [384, 512).
+// Epilogue: 16 warps in two groups, group g drains accumulator g (tiles local ≡ g mod 2).
+// With kUPD it applies the K-B update in place of storing G. The update is an HBM
+// stream (W, V read and written once): two loader warps keep W / V chunks
+// (128 rows × 16 columns, 16 KB) in flight by TMA into a 3-slot ring per group — 96 KB
+// continuously in flight per SM, independent of registers — and the epilogue reads them
+// from smem, applies Eq. 1 / apply / Eq. 4 with g from TMEM and stores from registers
+// (warp-coalesced, write-through). Register-staged loads (one 4 KB batch per warp in
+// flight) reached only ~4.7 TB/s on the same stream.
 // ============================================================================
 constexpr int DW_KMAX = 128;                       // K (= batch) capacity of the resident A
-constexpr int DW_RB = 3;                           // B ring stages (hi + lo, 32 KB)
+constexpr int DW_RB = 2;                           // B ring stages (hi + lo, 32 KB)
 constexpr int DW_EPI_WARPS = 16;                   // 2 groups × 2 warps per TMEM lane quadrant
 constexpr int DW_CONV_WARPS = 4;
-constexpr int DW_THREADS = 64 + 32 * (DW_EPI_WARPS + DW_CONV_WARPS);
+constexpr int DW_LOAD_WARPS = 2;                   // W / V stream loaders, one per group
+constexpr int DW_THREADS = 64 + 32 * (DW_EPI_WARPS + DW_CONV_WARPS + DW_LOAD_WARPS);
 constexpr int DW_A_BYTES = (DW_KMAX / BK) * TILE_BYTES;  // raw A staging: 64 KB
 constexpr int DW_B_STAGE = 2 * TILE_BYTES;
-constexpr int dw_smem_bytes() { return DW_A_BYTES + DW_RB * DW_B_STAGE + 1024 + 512; }
+constexpr int DW_WV_COLS = 16;                     // columns (n) per W / V chunk
+constexpr int DW_WV_SLOTS = 3;                     // ring slots per group
+constexpr int DW_WV_HALF = DW_WV_COLS * BM * 4;    // 8 KB: one tensor's chunk [16][128]
+constexpr int DW_WV_SLOT = 2 * DW_WV_HALF;         // W + V
+constexpr int DW_WV_BYTES = 2 * DW_WV_SLOTS * DW_WV_SLOT;  // 96 KB
+constexpr int dw_smem_bytes() { return DW_A_BYTES + DW_RB * DW_B_STAGE + DW_WV_BYTES + 1024 + 512; }
 
 template <bool kX3, bool kUPD>
 __global__ void __launch_bounds__(DW_THREADS, 1)
     tc_dw_kernel(const __grid_constant__ CUtensorMap mapA, const __grid_constant__ CUtensorMap mapB,
-                 const __grid_constant__ CUtensorMap mapBlo, TcParams p, int m_tiles, int n_tiles) {
+                 const __grid_constant__ CUtensorMap mapBlo, const __grid_constant__ CUtensorMap mapW,
+                 const __grid_constant__ CUtensorMap mapV, TcParams p, int m_tiles, int n_tiles) {
   extern __shared__ __align__(1024) uint8_t smem_raw[];
   char* smem = reinterpret_cast<char*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
   char* Astage = smem;
   char* ringB = smem + DW_A_BYTES;
-  uint64_t* bars = reinterpret_cast<uint64_t*>(ringB + DW_RB * DW_B_STAGE);
+  char* ringWV = ringB + DW_RB * DW_B_STAGE;  // [group][slot] W chunk, V chunk
+  uint64_t* bars = reinterpret_cast<uint64_t*>(ringWV + DW_WV_BYTES);
   const uint32_t a_full = smem_u32(bars);          // A staging landed (TMA)
   const uint32_t a_sfree = a_full + 8;             // converter done reading the staging (4 warps)
   const uint32_t a_tfull = a_sfree + 8;            // A hi / lo written to TMEM (4 warps)
@@ -1084,7 +1101,9 @@ __global__ void __launch_bounds__(DW_THREADS, 1)
   const uint32_t b_empty = b_full + 8 * DW_RB;     // [RB]
   const uint32_t c_full = b_empty + 8 * DW_RB;     // [2] accumulator ready
   const uint32_t c_empty = c_full + 16;            // [2] epilogue group drained it (8 warps)
-  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(bars + 4 + 2 * DW_RB + 4);
+  const uint32_t wv_full = c_empty + 16;           // [2][SLOTS] W / V chunk landed (TMA)
+  const uint32_t wv_empty = wv_full + 8 * 2 * DW_WV_SLOTS;  // [2][SLOTS] consumed (the group's 8 warps)
+  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(bars + 4 + 2 * DW_RB + 4 + 4 * DW_WV_SLOTS);
 
   const int warp = threadIdx.x >> 5;
   const int lane = threadIdx.x & 31;
@@ -1094,6 +1113,8 @@ __global__ void __launch_bounds__(DW_THREADS, 1)
   const int nkb = p.kb_total;  // K blocks (K ≤ 128)
   const int bn = p.bn;
   const int conv_w0 = 2 + DW_EPI_WARPS;
+  const int load_w0 = conv_w0 + DW_CONV_WARPS;
+  const int nch = (bn + DW_WV_COLS - 1) / DW_WV_COLS;  // W / V chunks per tile
 
   if (threadIdx.x == 0) {
     mbar_init(a_full, 1);
@@ -1107,6 +1128,10 @@ __global__ void __launch_bounds__(DW_THREADS, 1)
     for (int s = 0; s < 2; ++s) {
       mbar_init(c_full + 8 * s, 1);
       mbar_init(c_empty + 8 * s, DW_EPI_WARPS / 2);
+    }
+    for (int s = 0; s < 2 * DW_WV_SLOTS; ++s) {
+      mbar_init(wv_full + 8 * s, 1);
+      mbar_init(wv_empty + 8 * s, DW_EPI_WARPS / 2);
     }
     asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
   }
@@ -1189,6 +1214,25 @@ __global__ void __launch_bounds__(DW_THREADS, 1)
         tc_commit(c_full + 8 * buf);
       }
     }
+  } else if (warp >= load_w0) {
+    // ---------------- W / V stream loader of group (warp − load_w0): TMA into the ring
+    if (kUPD && p.wv_stream && lane == 0) {
+      const int group = warp - load_w0;
+      const uint32_t full0 = wv_full + 8 * DW_WV_SLOTS * group, empty0 = wv_empty + 8 * DW_WV_SLOTS * group;
+      char* ring = ringWV + group * DW_WV_SLOTS * DW_WV_SLOT;
+      int q = 0;
+      for (int t = t_begin + group; t < t_end; t += 2) {
+        const int m_t = t / n_tiles, n_t = t % n_tiles;
+        for (int c = 0; c < nch; ++c, ++q) {
+          const int sl = q % DW_WV_SLOTS;
+          mbar_wait(empty0 + 8 * sl, ((q / DW_WV_SLOTS) & 1) ^ 1);
+          mbar_expect_tx(full0 + 8 * sl, DW_WV_SLOT);
+          const uint32_t dst = smem_u32(ring + sl * DW_WV_SLOT);
+          tma_load_2d(dst, &mapW, m_t * BM, n_t * BNMAX + c * DW_WV_COLS, full0 + 8 * sl);
+          tma_load_2d(dst + DW_WV_HALF, &mapV, m_t * BM, n_t * BNMAX + c * DW_WV_COLS, full0 + 8 * sl);
+        }
+      }
+    }
   } else if (warp >= conv_w0) {
     // ---------------- converter: staged dZᵀ (MN-major boxes) → TMEM hi / lo, once per m-tile
     const int quad = warp & 3;
@@ -1229,8 +1273,63 @@ __global__ void __launch_bounds__(DW_THREADS, 1)
     // K-B update of W / V / WF / WB at the same index; g never leaves the chip.
     const int quad = warp & 3;
     const int group = (warp - 2) >> 3;       // accumulator / tile parity
-    const int half = ((warp - 2) >> 2) & 1;  // which 64 columns of the tile
+    const int half = ((warp - 2) >> 2) & 1;  // which 64 columns of the tile (G store) / 8 of each chunk's 16 (stream)
     int local = group;
+    if (kUPD && p.wv_stream) {
+      // W / V from the smem ring: every chunk is consumed by all 8 warps of the group
+      // (one consumer timeline per ring); this warp takes rows quad·32 + lane, columns
+      // half·8 .. half·8 + 7 of the chunk.
+      const uint32_t full0 = wv_full + 8 * DW_WV_SLOTS * group, empty0 = wv_empty + 8 * DW_WV_SLOTS * group;
+      const char* ring = ringWV + group * DW_WV_SLOTS * DW_WV_SLOT;
+      const UpdateArgs& u = p.upd;
+      int q = 0;
+      for (int t = t_begin + group; t < t_end; t += 2, local += 2) {
+        const int m_t = t / n_tiles, n_t = t % n_tiles;
+        mbar_wait(c_full + 8 * group, (local >> 1) & 1);
+        tc_fence_after();
+        const int m = m_t * BM + quad * 32 + lane;
+        const uint32_t trow = tmem + group * BNMAX + ((uint32_t)(quad * 32) << 16);
+        const int n0 = n_t * BNMAX;
+        for (int c = 0; c < nch; ++c, ++q) {
+          const int sl = q % DW_WV_SLOTS;
+          const int c0 = c * DW_WV_COLS + half * 8;  // first tile column of this warp
+          uint32_t rr[8];
+          tc_ld8_nowait(trow + c0, rr);
+          mbar_wait(full0 + 8 * sl, (q / DW_WV_SLOTS) & 1);
+          const float* sw = reinterpret_cast<const float*>(ring + sl * DW_WV_SLOT) + half * 8 * BM + quad * 32 + lane;
+          const float* sv = sw + DW_WV_HALF / 4;
+          float w[8], v[8];
+#pragma unroll
+          for (int j = 0; j < 8; ++j) {
+            w[j] = sw[j * BM];
+            v[j] = sv[j * BM];
+          }
+          __syncwarp();
+          if (lane == 0) mbar_arrive(empty0 + 8 * sl);  // slot refillable: values are in registers
+          tc_wait_ld();
+          if (p.dev_flags & 16) continue;
+          const int nc = n0 + c0;
+          if (m < p.M) {
+#pragma unroll
+            for (int j = 0; j < 8; ++j) {
+              if (nc + j < p.N) {
+                const float g = __uint_as_float(rr[j]);
+                const float vn = __fmaf_rn(u.c.c_gamma, v[j], __fmul_rn(u.c.c_one, g));
+                const float wn = __fmaf_rn(-u.c.c_eta, vn, w[j]);
+                const size_t o = (size_t)(nc + j) * p.M + m;
+                __stcs(u.W + o, wn);
+                __stcs(u.V + o, vn);
+                if (u.WF) __stcs(u.WF + o, __fmaf_rn(-u.c.c_f, vn, wn));
+                if (u.WB) __stcs(u.WB + o, __fmaf_rn(-u.c.c_b, vn, wn));
+              }
+            }
+          }
+        }
+        tc_fence_before();
+        __syncwarp();
+        if (lane == 0) mbar_arrive(c_empty + 8 * group);
+      }
+    } else
     for (int t = t_begin + group; t < t_end; t += 2, local += 2) {
       const int m_t = t / n_tiles, n_t = t % n_tiles;
       const int buf = group;
@@ -1312,6 +1411,21 @@ bool make_map(CUtensorMap* m, const float* base, int inner, int outer, int pitch
                    CU_TENSOR_MAP_INTERLEAVE_NONE,
                    mn_major ? CU_TENSOR_MAP_SWIZZLE_128B_ATOM_32B : CU_TENSOR_MAP_SWIZZLE_128B,
                    CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
+                   CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+  return r == CUDA_SUCCESS;
+}
+
+// 2D fp32 tensor [outer][inner] (row pitch = inner), box {box_inner, box_outer}, no swizzle
+// (plain row-major staging for the W / V stream of the fused update).
+bool make_plain_map(CUtensorMap* m, const float* base, int inner, int outer, int box_inner, int box_outer) {
+  EncodeFn enc = get_encode();
+  if (!enc || ((uintptr_t)base & 15u)) return false;
+  cuuint64_t dims[2] = {(cuuint64_t)inner, (cuuint64_t)outer};
+  cuuint64_t strides[1] = {(cuuint64_t)inner * 4};
+  cuuint32_t box[2] = {(cuuint32_t)box_inner, (cuuint32_t)box_outer};
+  cuuint32_t es[2] = {1, 1};
+  CUresult r = enc(m, CU_TENSOR_MAP_DATA_TYPE_FLOAT32, 2, const_cast<float*>(base), dims, strides, box, es,
+                   CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_NONE, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
                    CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
   return r == CUDA_SUCCESS;
 }
@@ -1591,7 +1705,15 @@ st_status tc_dw_impl(const GemmArgs& g, const float* X, const float* dZ, float* 
     p.bn = bn_for(g.n_in);
     p.out = G;
     p.dev_flags = dev_flags();
-    if (upd) p.upd = *upd;
+    CUtensorMap mw, mv;
+    memset(&mw, 0, sizeof(mw));
+    memset(&mv, 0, sizeof(mv));
+    if (upd) {
+      p.upd = *upd;
+      // W / V block [N rows][M cols] (element (n, m) at n·M + m), box 128 (m) × 16 (n), no swizzle
+      p.wv_stream = (g.n_out % 4 == 0) && make_plain_map(&mw, upd->W, g.n_out, g.n_in, BM, DW_WV_COLS) &&
+                    make_plain_map(&mv, upd->V, g.n_out, g.n_in, BM, DW_WV_COLS);
+    }
     p.idesc = make_idesc(p.bn, false, true);  // A from TMEM, B MN-major
     const int mt = (g.n_out + BM - 1) / BM, nt = (g.n_in + BNMAX - 1) / BNMAX;
     const int grid = std::min(mt * nt, g.max_ctas > 0 ? std::min(g.max_ctas, num_sms()) : num_sms());
@@ -1603,7 +1725,7 @@ st_status tc_dw_impl(const GemmArgs& g, const float* X, const float* dZ, float* 
       ST_CUDA_TRY(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, dw_smem_bytes()));
       attr_set[ai] = true;
     }
-    kern<<<grid, DW_THREADS, dw_smem_bytes(), g.stream>>>(ma, mb, mblo, p, mt, nt);
+    kern<<<grid, DW_THREADS, dw_smem_bytes(), g.stream>>>(ma, mb, mblo, mw, mv, p, mt, nt);
     ST_CUDA_TRY(cudaGetLastError());
     if (gb_upd) {
       ST_TRY(launch_bias_grad_update(dZ, g.B, g.n_out, *gb_upd, g.stream));

@@ -9,8 +9,13 @@ dev = torch.device("cuda", 0)
 X = torch.randn(B, n_in, device=dev); W = torch.randn(n_in, n_out, device=dev) * 0.01
 dZ = torch.randn(B, n_out, device=dev); bias = torch.randn(n_out, device=dev)
 work = torch.zeros(int(st._lib.lib.st_gemm_workspace_bytes(B, n_in, n_out)), dtype=torch.uint8, device=dev)
-args = (X, W, bias, None, torch.empty(B, n_out, device=dev)) if op == 0 else (dZ, W, X, None, torch.empty(B, n_in, device=dev))
-f = lambda: st.gemm_raw(op, 0, B, n_in, n_out, *args, relu=(op == 0), work=work)
+if op == 3:  # fused dW + K-B update
+    Wb = torch.randn(n_in * n_out + n_out, device=dev) * 0.01
+    Vb = torch.zeros_like(Wb); Gs = torch.empty_like(Wb)
+    f = lambda: st.dw_update_raw(0, X, dZ, Wb, Vb, None, None, 1e-3, 0.9, 0, 0, work=work, G_scratch=Gs)
+else:
+    args = (X, W, bias, None, torch.empty(B, n_out, device=dev)) if op == 0 else (dZ, W, X, None, torch.empty(B, n_in, device=dev))
+    f = lambda: st.gemm_raw(op, 0, B, n_in, n_out, *args, relu=(op == 0), work=work)
 pynvml.nvmlInit(); h = pynvml.nvmlDeviceGetHandleByIndex(0)
 samples, stop = [], False
 def sampler():
