@@ -41,7 +41,7 @@ DEFAULT_GEMM = "fp32x3"
 def parse():
     p = argparse.ArgumentParser()
     p.add_argument("--gpus", type=int, default=1)
-    p.add_argument("--steps", type=int, default=30)
+    p.add_argument("--steps", type=int, default=100)
     p.add_argument("--warmup", type=int, default=5)
     p.add_argument("--impl", default="ours", choices=["ours", "reference"])
     p.add_argument("--workload", default="wide_fcn", choices=["wide_fcn", "large_fcn", "mlp", "deep_mlp", "lstm_lm", "vgg16"])
@@ -124,7 +124,7 @@ class ClockSampler:
                         self.reasons.add(n)
             except Exception:
                 pass
-            time.sleep(0.1)
+            time.sleep(0.005)
 
     def __enter__(self):
         if self.ok:

@@ -2,6 +2,7 @@
 
   python tools/summarize_ncu.py launches <launches.csv>          per-kernel totals + shares
   python tools/summarize_ncu.py full <report.ncu-rep>            key metrics per captured kernel
+  python tools/summarize_ncu.py traffic <report.ncu-rep> <regex>  DRAM bytes summed over matching kernels
 """
 import csv
 import io
@@ -61,5 +62,36 @@ def full(path):
     return "\n".join(out)
 
 
+
+
+def traffic(path, regex):
+    """Σ (dram__bytes_read.sum + dram__bytes_write.sum) over captured kernels whose name
+    matches `regex` (one captured step → bytes per step)."""
+    import re
+    if path.endswith(".csv"):
+        raw = open(path).read()  # `ncu -i <rep> --page raw --csv` output
+    else:
+        raw = subprocess.run(["ncu", "-i", path, "--page", "raw", "--csv"], capture_output=True, text=True).stdout
+    rows = list(csv.reader(io.StringIO(raw)))
+    h, units = rows[0], rows[1]
+    ki, r_i, w_i, t_i = (h.index(x) for x in ("Kernel Name", "dram__bytes_read.sum", "dram__bytes_write.sum",
+                                              "gpu__time_duration.sum"))
+    scale = {"byte": 1, "Kbyte": 1e3, "Mbyte": 1e6, "Gbyte": 1e9, "B": 1, "KB": 1e3, "MB": 1e6, "GB": 1e9}
+    tscale = {"nsecond": 1e-9, "usecond": 1e-6, "msecond": 1e-3, "ns": 1e-9, "us": 1e-6, "ms": 1e-3}
+    tot, tot_t, n = 0.0, 0.0, 0
+    for r in rows[2:]:
+        if re.search(regex, r[ki]):
+            tot += float(r[r_i].replace(",", "")) * scale[units[r_i]] + float(r[w_i].replace(",", "")) * scale[units[w_i]]
+            tot_t += float(r[t_i].replace(",", "")) * tscale[units[t_i]]
+            n += 1
+    return n, tot, tot_t
+
+
 if __name__ == "__main__":
-    print(launches(sys.argv[2]) if sys.argv[1] == "launches" else full(sys.argv[2]))
+    if sys.argv[1] == "launches":
+        print(launches(sys.argv[2]))
+    elif sys.argv[1] == "traffic":
+        n, b, t = traffic(sys.argv[2], sys.argv[3])
+        print(f"{n} kernels, dram bytes {b:.6e}, duration {t * 1e6:.1f} us")
+    else:
+        print(full(sys.argv[2]))
