@@ -41,7 +41,6 @@ st_status ctx_run_group(st_ctx** ctxs, int n, int64_t M, const float* xs, const 
 st_status ctx_get_trace(st_ctx* c, st_event* out, size_t cap, size_t* n);
 st_status ctx_set_profiling(st_ctx* c, int on);
 st_status ctx_get_profile(st_ctx* c, double* total_ms, int64_t* launches);
-st_status launch_bias_grad(const float* dZ, int B, int n_out, float* gb, cudaStream_t s);
 
 }  // namespace st
 

@@ -123,12 +123,56 @@ __global__ void __launch_bounds__(256) bias_grad_kernel(const float* __restrict_
   }
 }
 
+// Tall column sums (conv layers: rows = B·H·W pixels): pass 1 gives each CTA a fixed
+// contiguous row block (block rb of `rpb` rows, 8 row groups, fixed combine) and writes
+// part[rb][o]; pass 2 sums the blocks in order. The partition depends only on the
+// shape, so the result is deterministic.
+__global__ void __launch_bounds__(256) colsum_partial_kernel(const float* __restrict__ dZ, int rows, int n_out,
+                                                             int rpb, float* __restrict__ part) {
+  __shared__ float sm[8][33];
+  const int tx = threadIdx.x & 31, ty = threadIdx.x >> 5;
+  const int o = blockIdx.x * 32 + tx;
+  const int r0 = blockIdx.y * rpb, r1 = min(rows, r0 + rpb);
+  float s = 0.f;
+  if (o < n_out)
+    for (int r = r0 + ty; r < r1; r += 8) s += dZ[(size_t)r * n_out + o];
+  sm[ty][tx] = s;
+  __syncthreads();
+  if (ty == 0 && o < n_out) {
+    float t = sm[0][tx];
+#pragma unroll
+    for (int q = 1; q < 8; ++q) t += sm[q][tx];
+    part[(size_t)blockIdx.y * n_out + o] = t;
+  }
+}
+
+__global__ void colsum_final_kernel(const float* __restrict__ part, int nb, int n_out, float* __restrict__ gb) {
+  const int o = blockIdx.x * blockDim.x + threadIdx.x;
+  if (o >= n_out) return;
+  float t = 0.f;
+  for (int b = 0; b < nb; ++b) t += part[(size_t)b * n_out + o];
+  gb[o] = t;
+}
+
 }  // namespace
 
-st_status launch_bias_grad(const float* dZ, int B, int n_out, float* gb, cudaStream_t s) {
-  bias_grad_kernel<<<(n_out + 31) / 32, 256, 0, s>>>(dZ, B, n_out, gb);
-  ST_CUDA_TRY(cudaGetLastError());
-  return ST_OK;
+// scratch: workspace whose bytes past the 64 KB counter block may be used for the
+// per-block partials of tall inputs (NULL: one-pass kernel). Returns the launch count.
+int launch_bias_grad(const float* dZ, int rows, int n_out, float* gb, void* work, int64_t work_bytes,
+                     cudaStream_t s) {
+  const int cb = (n_out + 31) / 32;
+  int nb = rows > 1024 ? std::min(1024, std::max(1, (4 * 148) / cb)) : 1;
+  nb = std::min(nb, (rows + 255) / 256);
+  if (nb > 1 && work && (int64_t)nb * n_out * 4 <= work_bytes - 64 * 1024) {
+    const int rpb = (rows + nb - 1) / nb;
+    nb = (rows + rpb - 1) / rpb;
+    float* part = reinterpret_cast<float*>(static_cast<char*>(work) + 64 * 1024);
+    colsum_partial_kernel<<<dim3(cb, nb), 256, 0, s>>>(dZ, rows, n_out, rpb, part);
+    colsum_final_kernel<<<(n_out + 127) / 128, 128, 0, s>>>(part, nb, n_out, gb);
+    return cudaGetLastError() == cudaSuccess ? 2 : -1;
+  }
+  bias_grad_kernel<<<cb, 256, 0, s>>>(dZ, rows, n_out, gb);
+  return cudaGetLastError() == cudaSuccess ? 1 : -1;
 }
 
 namespace {
@@ -187,8 +231,9 @@ st_status simt_dw(const GemmArgs& g, const float* X, const float* dZ, float* G, 
                         g.work, g.work_bytes));
   if (gb) {
     const int l = g_simt_launches;
-    ST_TRY(launch_bias_grad(dZ, g.B, g.n_out, gb, g.stream));
-    g_simt_launches = l + 1;
+    const int n = launch_bias_grad(dZ, g.B, g.n_out, gb, g.work, g.work_bytes, g.stream);
+    if (n < 0) return set_error(ST_ERR_CUDA, "bias gradient launch failed");
+    g_simt_launches = l + n;
   }
   return ST_OK;
 }

@@ -28,7 +28,8 @@
 namespace st {
 
 int64_t tc_workspace_bytes(int, int, int);
-st_status launch_bias_grad(const float* dZ, int B, int n_out, float* gb, cudaStream_t s);
+int launch_bias_grad(const float* dZ, int rows, int n_out, float* gb, void* work, int64_t work_bytes,
+                     cudaStream_t s);
 
 namespace {
 
@@ -56,6 +57,7 @@ struct TcParams {
                      // bit2 / bit3 skip B / A loads, bit4 skip TMEM stores, bit5 skip tcgen05.wait::st
   UpdateArgs upd;    // dW fused with K-B: weight-block targets (index n·M + m, like out)
   int wv_stream;     // fused K-B: W / V chunks staged in smem by TMA (mapW / mapV valid)
+  int ext_reduce;    // split-K: every CTA only writes its partial; splitk_epilogue_kernel reduces
 };
 
 // ------------------------------------------------------------------ PTX helpers
@@ -239,6 +241,7 @@ __device__ __forceinline__ void epilogue(const TcParams& p, uint32_t tmem, int w
 #pragma unroll
       for (int j = 0; j < 16; ++j) wsp[(size_t)(c + j) * BM + quad * 32 + lane] = v[j];
     }
+    if (p.ext_reduce) return;  // many splits: the parallel reduce kernel sums them
     __threadfence();
     asm volatile("bar.sync 1, 128;" ::: "memory");
     if (ctid == 0) {
@@ -929,6 +932,51 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(TS_THREADS, 1)
   }
 }
 
+// Split-K reduction for many splits (ext_reduce): one thread per output (n, m), the
+// partials of all splits loaded independently (4 at a time) and summed in fixed split
+// order 0..S−1 — the same order as the in-kernel fix-up — then the fused epilogue.
+// The last-CTA fix-up walks the splits serially (one memory latency per split and
+// chunk), which dominated GEMMs with a long K (e.g. the LSTM dh GEMM, K = 4H = 6000).
+template <int EPI>
+__global__ void splitk_epilogue_kernel(const float* __restrict__ ws, int splits, int tiles, int mt_grid, int M, int N,
+                                       float* __restrict__ out, const float* __restrict__ aux, int relu) {
+  const int64_t total = (int64_t)M * N;
+  const size_t split_stride = (size_t)tiles * BNMAX * BM;
+  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < total; i += (int64_t)gridDim.x * blockDim.x) {
+    const int m = (int)(i % M);
+    const int n = (int)(i / M);
+    const int tile = (n / BNMAX) * mt_grid + m / BM;
+    const float* src = ws + ((size_t)tile * BNMAX + n % BNMAX) * BM + m % BM;
+    float acc = 0.f;
+    int s = 0;
+    for (; s + 4 <= splits; s += 4) {
+      const float a0 = __ldcg(src + (size_t)s * split_stride), a1 = __ldcg(src + (size_t)(s + 1) * split_stride);
+      const float a2 = __ldcg(src + (size_t)(s + 2) * split_stride), a3 = __ldcg(src + (size_t)(s + 3) * split_stride);
+      acc += a0;
+      acc += a1;
+      acc += a2;
+      acc += a3;
+    }
+    for (; s < splits; ++s) acc += __ldcg(src + (size_t)s * split_stride);
+    if (EPI == EPI_FWD) {
+      if (aux) acc += aux[m];
+      if (relu) acc = fmaxf(acc, 0.f);
+    } else if (EPI == EPI_DX) {
+      if (aux && !(aux[i] > 0.f)) acc = 0.f;
+    }
+    out[i] = acc;
+  }
+}
+
+template <int EPI>
+st_status launch_splitk_epilogue(const TcParams& p, int tiles, int mt_grid, cudaStream_t s) {
+  const int64_t total = (int64_t)p.M * p.N;
+  const int blocks = (int)std::min<int64_t>((total + 255) / 256, 148 * 8);
+  splitk_epilogue_kernel<EPI><<<blocks, 256, 0, s>>>(p.ws, p.splits, tiles, mt_grid, p.M, p.N, p.out, p.aux, p.relu);
+  ST_CUDA_TRY(cudaGetLastError());
+  return ST_OK;
+}
+
 // lo = x − trunc_tf32(x) of a whole [rows × pitch] activation matrix (the B operand
 // of the FP32X3 forward / dX GEMMs), computed once per GEMM.
 __global__ void split_lo_kernel(const float4* __restrict__ x, float4* __restrict__ lo, size_t n4) {
@@ -1470,6 +1518,17 @@ bool aligned16(const void* p) { return ((uintptr_t)p & 15u) == 0; }
 
 static thread_local int g_launches = 0;
 constexpr size_t kCounterBytes = 64 * 1024;
+constexpr int kExtReduceSplits = 2;  // from this many K splits on, reduce in a separate parallel kernel (ST_EXT_REDUCE overrides)
+
+int ext_reduce_splits() {
+  static int f = -1;
+  if (f < 0) {
+    const char* e = getenv("ST_EXT_REDUCE");
+    f = e ? atoi(e) : kExtReduceSplits;
+  }
+  return f;
+}
+
 
 template <int EPI, bool A_MN, bool B_MN>
 st_status launch(const GemmArgs& g, int M, int N, int K, const CUtensorMap& ma, const CUtensorMap& mb, float* out,
@@ -1506,9 +1565,14 @@ st_status launch(const GemmArgs& g, int M, int N, int K, const CUtensorMap& ma, 
     ST_CUDA_TRY(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, smem_bytes(S)));
     attr_set[ai] = true;
   }
+  p.ext_reduce = p.splits >= ext_reduce_splits();
   kern<<<grid, kThreads, smem_bytes(S), g.stream>>>(ma, mb, p);
   ST_CUDA_TRY(cudaGetLastError());
   g_launches = 1;
+  if (p.ext_reduce) {
+    ST_TRY(launch_splitk_epilogue<EPI>(p, mt * nt, mt, g.stream));
+    g_launches = 2;
+  }
   return ST_OK;
 }
 
@@ -1564,6 +1628,7 @@ st_status launch_ts(const GemmArgs& g, int M, int N, int K, const CUtensorMap& m
   p.ws = reinterpret_cast<float*>(static_cast<char*>(g.work) + kCounterBytes);
   p.idesc = make_idesc(p.bn, false, false, pair ? 2 * BM : BM);
   p.dev_flags = dev_flags();
+  p.ext_reduce = p.splits >= ext_reduce_splits();
   float* blo = reinterpret_cast<float*>(static_cast<char*>(g.work) + kCounterBytes +
                                         (size_t)2 * 148 * BNMAX * BM * 4);
   const size_t n4 = (size_t)N * K / 4;
@@ -1595,6 +1660,10 @@ st_status launch_ts(const GemmArgs& g, int M, int N, int K, const CUtensorMap& m
   }
   ST_CUDA_TRY(cudaGetLastError());
   g_launches = 2;
+  if (p.ext_reduce) {
+    ST_TRY(launch_splitk_epilogue<EPI>(p, mt_grid * nt, mt_grid, g.stream));
+    g_launches = 3;
+  }
   return ST_OK;
 }
 
@@ -1731,8 +1800,9 @@ st_status tc_dw_impl(const GemmArgs& g, const float* X, const float* dZ, float* 
       ST_TRY(launch_bias_grad_update(dZ, g.B, g.n_out, *gb_upd, g.stream));
       ++launches;
     } else if (gb) {
-      ST_TRY(launch_bias_grad(dZ, g.B, g.n_out, gb, g.stream));
-      ++launches;
+      const int n = launch_bias_grad(dZ, g.B, g.n_out, gb, nullptr, 0, g.stream);
+      if (n < 0) return set_error(ST_ERR_CUDA, "bias gradient launch failed");
+      launches += n;
     }
     g_launches = launches;
     return ST_OK;
@@ -1742,8 +1812,10 @@ st_status tc_dw_impl(const GemmArgs& g, const float* X, const float* dZ, float* 
     return set_error(ST_ERR_CUDA, "cuTensorMapEncodeTiled failed (dW)");
   ST_TRY((launch<EPI_DW, true, true>(g, g.n_out, g.n_in, g.B, ma, mb, G, nullptr, 0)));
   if (gb) {
-    ST_TRY(launch_bias_grad(dZ, g.B, g.n_out, gb, g.stream));
-    g_launches = 2;
+    // the GEMM's split-K partials are consumed by the time this runs (same stream)
+    const int n = launch_bias_grad(dZ, g.B, g.n_out, gb, g.work, g.work_bytes, g.stream);
+    if (n < 0) return set_error(ST_ERR_CUDA, "bias gradient launch failed");
+    g_launches = 1 + n;
   }
   return ST_OK;
 }
