@@ -281,9 +281,11 @@ ST_API st_status st_sync(st_ctx* ctx);
 
 /* ---- measurement hooks ----------------------------------------------------- */
 
-/* Profiling: when on, the engine brackets every launch of each kernel class with
- * CUDA events on the compute stream. Classes: 0 update (K-B), 1 gemm_fwd,
- * 2 gemm_dx, 3 gemm_dw, 4 loss (CE + bias-grad), 5 comm. */
+/* Profiling: `on` is a bitmask of kernel classes (bit i = class i; 0 = off). The
+ * engine brackets every launch of a selected class with CUDA events on the stream
+ * it is launched on (events are pre-created by this call, so a timed region pays
+ * only the two records). Classes: 0 update (K-B), 1 gemm_fwd, 2 gemm_dx,
+ * 3 gemm_dw, 4 loss (CE + bias-grad), 5 comm. Resets the totals. */
 ST_API st_status st_set_profiling(st_ctx* ctx, int on);
 /* Per class: total milliseconds and launch count since profiling was switched on
  * (synchronises). arrays of length 6. */

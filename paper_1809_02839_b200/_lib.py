@@ -15,7 +15,8 @@ from typing import List, Optional, Sequence, Tuple
 import numpy as np
 
 HERE = os.path.dirname(os.path.abspath(__file__))
-LIB_PATH = os.path.join(HERE, "libspectrain.so")
+# ST_LIB_PATH: a development variant built by build.build(lib=...) (still in-tree, still loud if missing)
+LIB_PATH = os.environ.get("ST_LIB_PATH") or os.path.join(HERE, "libspectrain.so")
 
 ST_FWD, ST_BWD = 0, 1
 ST_ACT_NONE, ST_ACT_RELU = 0, 1

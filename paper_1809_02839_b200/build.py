@@ -38,13 +38,15 @@ def _needs(obj: str, src: str, deps) -> bool:
     return any(os.path.getmtime(p) > t for p in [src, *deps])
 
 
-def build(verbose: bool = False, force: bool = False) -> str:
+def build(verbose: bool = False, force: bool = False, defines=(), lib: str = LIB, build_dir: str = BUILD) -> str:
+    """defines / lib / build_dir: development variants (e.g. ring depths) built beside the product .so."""
     nccl_inc, nccl_lib = nccl_paths()
+    BUILD, LIB = build_dir, lib
     os.makedirs(BUILD, exist_ok=True)
     headers = [os.path.join(CSRC, f) for f in os.listdir(CSRC) if f.endswith((".hpp", ".cuh"))]
     headers.append(os.path.join(INCLUDE, "spectrain.h"))
     common = ["-O3", "-std=c++17", "-lineinfo", "-Xcompiler", "-fPIC,-fvisibility=hidden", f"-I{INCLUDE}",
-              f"-I{CSRC}", f"-I{nccl_inc}", *ARCH, "-Xptxas", "-v" if verbose else "-O3"]
+              f"-I{CSRC}", f"-I{nccl_inc}", *ARCH, "-Xptxas", "-v" if verbose else "-O3", *[f"-D{d}" for d in defines]]
     objs, jobs = [], []
     for src in sources():
         obj = os.path.join(BUILD, os.path.basename(src) + ".o")

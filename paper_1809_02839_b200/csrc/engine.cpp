@@ -261,7 +261,7 @@ struct Timed {
   cudaStream_t s;
   cudaEvent_t b = nullptr;
   Timed(st_ctx* ctx, int k, cudaStream_t stream = nullptr) : c(ctx), cls(k), s(stream ? stream : ctx->stream) {
-    if (!c->prof.on) return;
+    if (!c->prof.on || !((c->prof.mask >> cls) & 1u)) return;
     cudaEvent_t a = get();
     b = get();
     cudaEventRecord(a, s);
@@ -1038,7 +1038,17 @@ st_status ctx_set_profiling(st_ctx* c, int on) {
     c->prof.total_ms[i] = 0;
     c->prof.launches[i] = 0;
   }
+  // on: bitmask of kernel classes (1 << KC_*); nonzero enables. Events are created
+  // here, outside any timed region, so bracketing costs only the two records.
+  c->prof.mask = (unsigned)on;
   c->prof.on = on != 0;
+  if (c->prof.on) {
+    while (c->prof.pool.size() < 8192) {
+      cudaEvent_t e;
+      ST_CUDA_TRY(cudaEventCreate(&e));
+      c->prof.pool.push_back(e);
+    }
+  }
   return ST_OK;
 }
 

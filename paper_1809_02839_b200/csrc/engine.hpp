@@ -77,6 +77,7 @@ st_status launch_maxpool_bwd(const float* X, const float* dY, int B, int H, int 
 
 struct Profiler {
   bool on = false;
+  unsigned mask = 0;  // bit i: bracket kernel class i
   struct Pair {
     int cls;
     cudaEvent_t a, b;

@@ -445,8 +445,14 @@ __global__ void __launch_bounds__(kThreads, 1)
 // tiles by TMA (lo precomputed once per GEMM by split_lo_kernel). The MMA thread
 // issues A_hi·B_hi + A_lo·B_hi + A_hi·B_lo per K step of 8, reading only B from smem.
 // ============================================================================
-constexpr int TS_RA = 6;                 // weight (A) raw ring stages, 16 KB each
-constexpr int TS_RB = 3;                 // activation (B) ring stages, hi + lo ≤ 32 KB
+#ifndef ST_TS_RA
+#define ST_TS_RA 6
+#endif
+#ifndef ST_TS_RB
+#define ST_TS_RB 3
+#endif
+constexpr int TS_RA = ST_TS_RA;          // weight (A) raw ring stages, 16 KB each
+constexpr int TS_RB = ST_TS_RB;          // activation (B) ring stages, hi + lo ≤ 32 KB
 constexpr int TS_TA = 6;                 // TMEM A slots (64 columns: 32 hi + 32 lo): 128 + 6·64 = 512
 constexpr int TS_THREADS = 224;          // 7 warps
 constexpr int TS_B_STAGE = 2 * BNMAX * BK * 4;
@@ -589,7 +595,7 @@ __global__ void __launch_bounds__(TS_THREADS, 1)
           const uint32_t acc = (i > 0 || kk > 0) ? 1u : 0u;
           tc_mma_ts(tmem, a_hi + kk * 8, desc_kmajor(b_hi + kk * 32), p.idesc, acc);
           tc_mma_ts(tmem, a_lo + kk * 8, desc_kmajor(b_hi + kk * 32), p.idesc, 1u);
-          tc_mma_ts(tmem, a_hi + kk * 8, desc_kmajor(b_lo + kk * 32), p.idesc, 1u);
+          if (!(p.dev_flags & 256)) tc_mma_ts(tmem, a_hi + kk * 8, desc_kmajor(b_lo + kk * 32), p.idesc, 1u);
         }
         tc_commit(b_empty + 8 * sb);
         tc_commit(t_empty + 8 * ta);
@@ -846,7 +852,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(TS_THREADS, 1)
           const uint32_t acc = (i > 0 || kk > 0) ? 1u : 0u;
           tc_mma_ts2(tmem, a_hi + kk * 8, desc_kmajor(b_hi + kk * 32), p.idesc, acc);
           tc_mma_ts2(tmem, a_lo + kk * 8, desc_kmajor(b_hi + kk * 32), p.idesc, 1u);
-          tc_mma_ts2(tmem, a_hi + kk * 8, desc_kmajor(b_lo + kk * 32), p.idesc, 1u);
+          if (!(p.dev_flags & 256)) tc_mma_ts2(tmem, a_hi + kk * 8, desc_kmajor(b_lo + kk * 32), p.idesc, 1u);
         }
         tc_commit2(b_empty + 8 * sb);
         tc_commit2(t_empty + 8 * ta);
@@ -1254,7 +1260,7 @@ __global__ void __launch_bounds__(DW_THREADS, 1)
             tc_mma_ts(acc_t, tA_hi + ka, desc_mnmajor(b_hi + kk * 1024), p.idesc, acc);
             if (kX3) {
               tc_mma_ts(acc_t, tA_lo + ka, desc_mnmajor(b_hi + kk * 1024), p.idesc, 1u);
-              tc_mma_ts(acc_t, tA_hi + ka, desc_mnmajor(b_lo + kk * 1024), p.idesc, 1u);
+              if (!(p.dev_flags & 256)) tc_mma_ts(acc_t, tA_hi + ka, desc_mnmajor(b_lo + kk * 1024), p.idesc, 1u);
             }
           }
           tc_commit(b_empty + 8 * s);

@@ -139,8 +139,13 @@ class Stage:
     def losses_device_ptr(self) -> int:
         return lib.st_losses_device(self.ctx) or 0
 
-    def set_profiling(self, on: bool) -> None:
-        check(lib.st_set_profiling(self.ctx, 1 if on else 0))
+    def set_profiling(self, on, classes=None) -> None:
+        """on: bool; classes: kernel-class names to bracket (default: all)."""
+        mask = 0
+        if on:
+            names = L.KERNEL_CLASSES if classes is None else classes
+            mask = sum(1 << L.KERNEL_CLASSES.index(n) for n in names)
+        check(lib.st_set_profiling(self.ctx, mask))
 
     def profile(self):
         ms = (ctypes.c_double * 6)()
