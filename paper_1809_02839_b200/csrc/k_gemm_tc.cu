@@ -61,6 +61,13 @@ struct TcParams {
 };
 
 // ------------------------------------------------------------------ PTX helpers
+// 1024-B aligned base of the dynamic smem window. Pointer arithmetic on the __shared__
+// array itself (not a uintptr_t round trip) keeps the address space visible to the
+// compiler, so reads through it are LDS, not generic LD.
+__device__ __forceinline__ char* align_smem_1k(uint8_t* raw) {
+  const uint32_t a = (uint32_t)__cvta_generic_to_shared(raw);
+  return reinterpret_cast<char*>(raw) + ((1024u - (a & 1023u)) & 1023u);
+}
 __device__ __forceinline__ uint32_t smem_u32(const void* p) { return (uint32_t)__cvta_generic_to_shared(p); }
 
 __device__ __forceinline__ void mbar_init(uint32_t bar, uint32_t count) {
@@ -314,7 +321,7 @@ template <int EPI, bool A_MN, bool B_MN, bool kX3, int STAGES>
 __global__ void __launch_bounds__(kThreads, 1)
     tc_gemm_kernel(const __grid_constant__ CUtensorMap mapA, const __grid_constant__ CUtensorMap mapB, TcParams p) {
   extern __shared__ __align__(1024) uint8_t smem_raw[];
-  char* smem = reinterpret_cast<char*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
+  char* smem = align_smem_1k(smem_raw);
   uint64_t* bars = reinterpret_cast<uint64_t*>(smem + STAGES * STAGE_BYTES);
   const uint32_t b_full = smem_u32(bars);            // TMA landed        (1 arrive + tx)
   const uint32_t b_conv = b_full + 8 * STAGES;       // lo tiles written  (4 converter warps)
@@ -483,7 +490,7 @@ __global__ void __launch_bounds__(TS_THREADS, 1)
     tc_ts_kernel(const __grid_constant__ CUtensorMap mapA, const __grid_constant__ CUtensorMap mapB,
                  const __grid_constant__ CUtensorMap mapBlo, TcParams p) {
   extern __shared__ __align__(1024) uint8_t smem_raw[];
-  char* smem = reinterpret_cast<char*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
+  char* smem = align_smem_1k(smem_raw);
   char* ringA = smem;
   char* ringB = smem + TS_RA * TILE_BYTES;
   uint64_t* bars = reinterpret_cast<uint64_t*>(ringB + TS_RB * TS_B_STAGE);
@@ -731,7 +738,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(TS_THREADS, 1)
     tc_ts2_kernel(const __grid_constant__ CUtensorMap mapA, const __grid_constant__ CUtensorMap mapB,
                   const __grid_constant__ CUtensorMap mapBlo, TcParams p) {
   extern __shared__ __align__(1024) uint8_t smem_raw[];
-  char* smem = reinterpret_cast<char*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
+  char* smem = align_smem_1k(smem_raw);
   char* ringA = smem;
   char* ringB = smem + TS_RA * TILE_BYTES;
   uint64_t* bars = reinterpret_cast<uint64_t*>(ringB + TS2_RB * TS2_B_STAGE);
@@ -1122,7 +1129,10 @@ __device__ __forceinline__ void update_block16_vec(const UpdateArgs& u, size_t M
 // flight) reached only ~4.7 TB/s on the same stream.
 // ============================================================================
 constexpr int DW_KMAX = 128;                       // K (= batch) capacity of the resident A
-constexpr int DW_RB = 2;                           // B ring stages (hi + lo, 32 KB)
+#ifndef ST_DW_RB
+#define ST_DW_RB 4
+#endif
+constexpr int DW_RB = ST_DW_RB;                    // B ring stages (hi + lo, 32 KB)
 constexpr int DW_EPI_WARPS = 16;                   // 2 groups × 2 warps per TMEM lane quadrant
 constexpr int DW_CONV_WARPS = 4;
 constexpr int DW_LOAD_WARPS = 2;                   // W / V stream loaders, one per group
@@ -1130,11 +1140,20 @@ constexpr int DW_THREADS = 64 + 32 * (DW_EPI_WARPS + DW_CONV_WARPS + DW_LOAD_WAR
 constexpr int DW_A_BYTES = (DW_KMAX / BK) * TILE_BYTES;  // raw A staging: 64 KB
 constexpr int DW_B_STAGE = 2 * TILE_BYTES;
 constexpr int DW_WV_COLS = 16;                     // columns (n) per W / V chunk
-constexpr int DW_WV_SLOTS = 3;                     // ring slots per group
+#ifndef ST_DW_WV_SLOTS
+#define ST_DW_WV_SLOTS 3
+#endif
+constexpr int DW_WV_SLOTS = ST_DW_WV_SLOTS;        // ring slots per group
 constexpr int DW_WV_HALF = DW_WV_COLS * BM * 4;    // 8 KB: one tensor's chunk [16][128]
 constexpr int DW_WV_SLOT = 2 * DW_WV_HALF;         // W + V
 constexpr int DW_WV_BYTES = 2 * DW_WV_SLOTS * DW_WV_SLOT;  // 96 KB
-constexpr int dw_smem_bytes() { return DW_A_BYTES + DW_RB * DW_B_STAGE + DW_WV_BYTES + 1024 + 512; }
+// The A staging (needed once per m-tile, i.e. once or twice per CTA) ALIASES the B ring:
+// the producer drains the ring before loading A and resumes B only after the converter
+// has read A. The 64 KB this frees deepen the B ring (X hi + lo, 128 KB per tile from
+// L2: with 2 stages the MMAs starved on the L2 round trip and the epilogue waited on
+// the accumulator).
+static_assert(DW_RB * DW_B_STAGE >= DW_A_BYTES, "A staging aliases the B ring");
+constexpr int dw_smem_bytes() { return DW_RB * DW_B_STAGE + DW_WV_BYTES + 1024 + 512; }
 
 template <bool kX3, bool kUPD>
 __global__ void __launch_bounds__(DW_THREADS, 1)
@@ -1142,10 +1161,10 @@ __global__ void __launch_bounds__(DW_THREADS, 1)
                  const __grid_constant__ CUtensorMap mapBlo, const __grid_constant__ CUtensorMap mapW,
                  const __grid_constant__ CUtensorMap mapV, TcParams p, int m_tiles, int n_tiles) {
   extern __shared__ __align__(1024) uint8_t smem_raw[];
-  char* smem = reinterpret_cast<char*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
+  char* smem = align_smem_1k(smem_raw);
   char* Astage = smem;
-  char* ringB = smem + DW_A_BYTES;
-  char* ringWV = ringB + DW_RB * DW_B_STAGE;  // [group][slot] W chunk, V chunk
+  char* ringB = smem;  // aliased with the A staging (see dw_smem_bytes)
+  char* ringWV = smem + DW_RB * DW_B_STAGE;  // [group][slot] W chunk, V chunk
   uint64_t* bars = reinterpret_cast<uint64_t*>(ringWV + DW_WV_BYTES);
   const uint32_t a_full = smem_u32(bars);          // A staging landed (TMA)
   const uint32_t a_sfree = a_full + 8;             // converter done reading the staging (4 warps)
@@ -1206,13 +1225,16 @@ __global__ void __launch_bounds__(DW_THREADS, 1)
       for (int t = t_begin; t < t_end; ++t) {
         const int m_t = t / n_tiles, n_t = t % n_tiles;
         if (m_t != cur_m) {
-          mbar_wait(a_sfree, (a_loads & 1) ^ 1);
+          // drain the B ring (the staging aliases it): the MMAs of every issued B stage are done
+          for (int j = max(0, it - DW_RB); j < it; ++j) mbar_wait(b_empty + 8 * (j % DW_RB), (j / DW_RB) & 1);
           mbar_expect_tx(a_full, (uint32_t)(nkb * TILE_BYTES));
           for (int kb = 0; kb < nkb; ++kb) {
             const uint32_t dA = smem_u32(Astage + kb * TILE_BYTES);
 #pragma unroll
             for (int c = 0; c < BM / 32; ++c) tma_load_2d(dA + c * 4096, &mapA, m_t * BM + 32 * c, kb * BK, a_full);
           }
+          // B may overwrite the staging only once the converter has read it
+          mbar_wait(a_sfree, a_loads & 1);
           cur_m = m_t;
           ++a_loads;
         }
