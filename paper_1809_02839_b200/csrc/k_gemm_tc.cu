@@ -58,12 +58,21 @@ struct TcParams {
   UpdateArgs upd;    // dW fused with K-B: weight-block targets (index n·M + m, like out)
   int wv_stream;     // fused K-B: W / V chunks staged in smem by TMA (mapW / mapV valid)
   int ext_reduce;    // split-K: every CTA only writes its partial; splitk_epilogue_kernel reduces
+  int sk;            // stream-K (fwd / dX TS kernel): CTA b takes chunks [b·U/G, (b+1)·U/G) of
+                     // the tile-major (tile, K-block) space, U = tiles · kb_total, G = gridDim.x
+  int mt, tiles;     // stream-K: m tiles, total tiles (tile = n_tile · mt + m_tile)
 };
 
 // ------------------------------------------------------------------ PTX helpers
 // 1024-B aligned base of the dynamic smem window. Pointer arithmetic on the __shared__
 // array itself (not a uintptr_t round trip) keeps the address space visible to the
 // compiler, so reads through it are LDS, not generic LD.
+__device__ __forceinline__ bool elect_one() {
+  uint32_t pred = 0;
+  asm volatile(
+      "{\n .reg .pred p;\n elect.sync _|p, 0xffffffff;\n selp.u32 %0, 1, 0, p;\n}" : "=r"(pred)::"memory");
+  return pred != 0;
+}
 __device__ __forceinline__ char* align_smem_1k(uint8_t* raw) {
   const uint32_t a = (uint32_t)__cvta_generic_to_shared(raw);
   return reinterpret_cast<char*>(raw) + ((1024u - (a & 1023u)) & 1023u);
@@ -441,6 +450,108 @@ __global__ void __launch_bounds__(kThreads, 1)
 }
 
 
+// ---------------------------------------------------------------- stream-K
+// First chunk of CTA b's range (b = G gives U).
+__device__ __forceinline__ long long sk_begin(int b, int G, long long U) { return (long long)b * U / G; }
+// The CTA whose range holds chunk x.
+__device__ __forceinline__ int sk_owner(long long x, int G, long long U) {
+  int b = (int)(((x + 1) * G + U - 1) / U) - 1;
+  while (b + 1 < G && sk_begin(b + 1, G, U) <= x) ++b;
+  while (b > 0 && sk_begin(b, G, U) > x) --b;
+  return b;
+}
+// Partial slot of the segment (tile, CTA b): a CTA holds at most two partial segments,
+// the one its range starts in (2b) and the one it ends in (2b + 1).
+__device__ __forceinline__ size_t sk_slot(int tile, int b, int G, long long U, int kbt) {
+  return (size_t)(sk_begin(b, G, U) >= (long long)tile * kbt ? 2 * b : 2 * b + 1);
+}
+
+// Stream-K segment epilogue (the 4 converter warps). The tile's segments belong to the
+// consecutive CTAs b_first .. b_first + nseg − 1; a whole-tile segment stores directly,
+// otherwise every segment writes its partial and the last CTA to arrive sums them in
+// segment order (deterministic) and applies the fused epilogue. acc parity = segment
+// count of this CTA & 1.
+template <int EPI>
+__device__ __forceinline__ void epilogue_sk(const TcParams& p, uint32_t tmem, int warp, int lane, int tile,
+                                            long long U, int* last_flag, uint32_t b_acc_full, uint32_t parity) {
+  mbar_wait(b_acc_full, parity);
+  tc_fence_after();
+  const int G = gridDim.x, b = blockIdx.x, kbt = p.kb_total;
+  const int m0 = (tile % p.mt) * BM, n0 = (tile / p.mt) * BNMAX;
+  const int bn = p.bn;
+  const int ctid = (warp - 2) * 32 + lane;
+  const int quad = warp & 3;
+  const int m = m0 + quad * 32 + lane;
+  const uint32_t trow = tmem + ((uint32_t)(quad * 32) << 16);
+  const int b_first = sk_owner((long long)tile * kbt, G, U);
+  const int nseg = sk_owner((long long)tile * kbt + kbt - 1, G, U) - b_first + 1;
+  const float bias = (EPI == EPI_FWD && p.aux && m < p.M) ? p.aux[m] : 0.f;
+  if (nseg == 1) {
+    for (int c = 0; c < bn; c += 16) {
+      float v[16];
+      tc_ld16(trow + c, v);
+      if (m < p.M) epilogue_store16<EPI>(p, m, n0 + c, v, bias);
+    }
+    return;
+  }
+  float* wsp = p.ws + sk_slot(tile, b, G, U, kbt) * (BNMAX * BM);
+  for (int c = 0; c < bn; c += 16) {
+    float v[16];
+    tc_ld16(trow + c, v);
+#pragma unroll
+    for (int j = 0; j < 16; ++j) wsp[(size_t)(c + j) * BM + quad * 32 + lane] = v[j];
+  }
+  __threadfence();
+  asm volatile("bar.sync 1, 128;" ::: "memory");
+  if (ctid == 0) *last_flag = (atomicAdd(p.counters + tile, 1) == nseg - 1);
+  asm volatile("bar.sync 1, 128;" ::: "memory");
+  const bool last = *last_flag;
+  asm volatile("bar.sync 1, 128;" ::: "memory");  // the flag is reused by the next segment
+  if (!last) return;
+  __threadfence();
+  for (int c = 0; c < bn; c += 32) {
+    float acc[32], mk[32];
+    const int nv = min(32, p.N - (n0 + c));
+    if (EPI == EPI_DX && p.aux && m < p.M) {
+#pragma unroll
+      for (int j = 0; j < 32; ++j) mk[j] = (j < nv) ? __ldg(p.aux + (size_t)(n0 + c + j) * p.M + m) : 0.f;
+    }
+#pragma unroll
+    for (int j = 0; j < 32; ++j) acc[j] = 0.f;
+    for (int sgi = 0; sgi < nseg; ++sgi) {
+      const int bs = b_first + sgi;
+      float v[32];
+      if (bs == b) {
+        tc_ld16_nowait(trow + c, reinterpret_cast<uint32_t*>(v));
+        tc_ld16_nowait(trow + c + 16, reinterpret_cast<uint32_t*>(v + 16));
+        tc_wait_ld();
+      } else {
+        const float* src = p.ws + sk_slot(tile, bs, G, U, kbt) * (BNMAX * BM) + (size_t)c * BM + quad * 32 + lane;
+#pragma unroll
+        for (int j = 0; j < 32; ++j) v[j] = (c + j < BNMAX) ? __ldcg(src + (size_t)j * BM) : 0.f;
+      }
+#pragma unroll
+      for (int j = 0; j < 32; ++j) acc[j] += v[j];
+    }
+    if (m < p.M) {
+#pragma unroll
+      for (int j = 0; j < 32; ++j) {
+        if (j < nv) {
+          float v = acc[j];
+          if (EPI == EPI_FWD) {
+            v += bias;
+            if (p.relu) v = fmaxf(v, 0.f);
+          } else if (EPI == EPI_DX) {
+            if (p.aux && !(mk[j] > 0.f)) v = 0.f;
+          }
+          p.out[(size_t)(n0 + c + j) * p.M + m] = v;
+        }
+      }
+    }
+  }
+  if (ctid == 0) p.counters[tile] = 0;  // self-reset for the next launch
+}
+
 // ============================================================================
 // FP32X3 forward / dX kernel: weights through TMEM (tcgen05.mma A-from-TMEM).
 //
@@ -501,7 +612,8 @@ __global__ void __launch_bounds__(TS_THREADS, 1)
   const uint32_t t_full = b_empty + 8 * TS_RB;     // TMEM A slot written     [TA]
   const uint32_t t_empty = t_full + 8 * TS_TA;     // MMA done with TMEM slot [TA]
   const uint32_t acc_full = t_empty + 8 * TS_TA;
-  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(bars + 2 * TS_RA + 2 * TS_RB + 2 * TS_TA + 1);
+  const uint32_t acc_empty = acc_full + 8;         // stream-K: epilogue drained the accumulator
+  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(bars + 2 * TS_RA + 2 * TS_RB + 2 * TS_TA + 2);
   int* last_flag = reinterpret_cast<int*>(tmem_slot + 1);
 
   const int warp = threadIdx.x >> 5;
@@ -509,8 +621,14 @@ __global__ void __launch_bounds__(TS_THREADS, 1)
   const int m_tile = blockIdx.x, n_tile = blockIdx.y, split = blockIdx.z;
   const int m0 = m_tile * BM, n0 = n_tile * BNMAX;
   const int kb0 = split * p.kb_per_split;
-  const int nkb = min(p.kb_total, kb0 + p.kb_per_split) - kb0;
   const int bn = p.bn;
+  // this CTA's chunks g0 .. g0 + nkb − 1 of the tile-major (tile, K-block) space
+  const int kbt = p.kb_total;
+  const long long U = (long long)p.tiles * kbt;
+  const int g0 = p.sk ? (int)sk_begin(blockIdx.x, gridDim.x, U) : (n_tile * gridDim.x + m_tile) * kbt + kb0;
+  const int nkb = p.sk ? (int)sk_begin(blockIdx.x + 1, gridDim.x, U) - g0 : min(kbt, kb0 + p.kb_per_split) - kb0;
+  const int mt = p.sk ? p.mt : (int)gridDim.x;
+  const int tile0 = g0 / kbt, kbs0 = g0 - tile0 * kbt;  // first chunk: tile, K-block (walked incrementally)
   if (threadIdx.x == 0) dbg_mark(p, 0);
 
   if (threadIdx.x == 0) {
@@ -527,6 +645,7 @@ __global__ void __launch_bounds__(TS_THREADS, 1)
       mbar_init(t_empty + 8 * s, 1);
     }
     mbar_init(acc_full, 1);
+    mbar_init(acc_empty, 4);
     asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
   }
   if (warp == 1) {
@@ -548,7 +667,7 @@ __global__ void __launch_bounds__(TS_THREADS, 1)
   if (warp == 0) {
     // ---------------- TMA producer, weights (A)
     if (lane == 0) {
-      for (int i = 0; i < nkb; ++i) {
+      for (int i = 0, tile = tile0, kb = kbs0; i < nkb; ++i, kb = (kb + 1 == kbt) ? (++tile, 0) : kb + 1) {
         const int s = i % TS_RA;
         mbar_wait(a_free + 8 * s, ((i / TS_RA) & 1) ^ 1);
         const uint32_t full = a_full + 8 * s;
@@ -557,13 +676,13 @@ __global__ void __launch_bounds__(TS_THREADS, 1)
           continue;
         }
         mbar_expect_tx(full, TILE_BYTES);
-        const int k0 = (kb0 + i) * BK;
+        const int k0 = kb * BK, am0 = (tile % mt) * BM;
         const uint32_t dA = smem_u32(ringA + s * TILE_BYTES);
         if (A_MN) {
 #pragma unroll
-          for (int c = 0; c < BM / 32; ++c) tma_load_2d(dA + c * 4096, &mapA, m0 + 32 * c, k0, full);
+          for (int c = 0; c < BM / 32; ++c) tma_load_2d(dA + c * 4096, &mapA, am0 + 32 * c, k0, full);
         } else {
-          tma_load_2d(dA, &mapA, k0, m0, full);
+          tma_load_2d(dA, &mapA, k0, am0, full);
         }
       }
     }
@@ -571,7 +690,7 @@ __global__ void __launch_bounds__(TS_THREADS, 1)
     // ---------------- TMA producer, activations (B hi + lo)
     if (lane == 0) {
       const uint32_t bytes = (uint32_t)(2 * bn * BK * 4);
-      for (int i = 0; i < nkb; ++i) {
+      for (int i = 0, tile = tile0, kb = kbs0; i < nkb; ++i, kb = (kb + 1 == kbt) ? (++tile, 0) : kb + 1) {
         const int s = i % TS_RB;
         mbar_wait(b_empty + 8 * s, ((i / TS_RB) & 1) ^ 1);
         const uint32_t full = b_full + 8 * s;
@@ -580,41 +699,51 @@ __global__ void __launch_bounds__(TS_THREADS, 1)
           continue;
         }
         mbar_expect_tx(full, bytes);
-        const int k0 = (kb0 + i) * BK;
+        const int k0 = kb * BK, bn0 = (tile / mt) * BNMAX;
         const uint32_t dB = smem_u32(ringB + s * TS_B_STAGE);
-        tma_load_2d(dB, &mapB, k0, n0, full);
-        tma_load_2d(dB + BNMAX * BK * 4, &mapBlo, k0, n0, full);
+        tma_load_2d(dB, &mapB, k0, bn0, full);
+        tma_load_2d(dB + BNMAX * BK * 4, &mapBlo, k0, bn0, full);
       }
     }
   } else if (warp == 1) {
-    // ---------------- MMA issuer
-    if (lane == 0) {
-      for (int i = 0; i < nkb; ++i) {
+    // ---------------- MMA issuer: the whole warp walks the loop (warp-uniform operands
+    // stay in uniform registers), one elected lane issues
+    {
+      int seg = 0;
+      for (int i = 0, kb = kbs0; i < nkb; ++i, kb = (kb + 1 == kbt) ? 0 : kb + 1) {
         const int sb = i % TS_RB, ta = i % TS_TA;
+        const bool seg_start = (i == 0) || (kb == 0);
+        const bool seg_end = (i == nkb - 1) || (kb + 1 == kbt);
+        if (seg_start && seg > 0) mbar_wait(acc_empty, (seg - 1) & 1);  // stream-K: accumulator drained
         mbar_wait(t_full + 8 * ta, (i / TS_TA) & 1);
         mbar_wait(b_full + 8 * sb, (i / TS_RB) & 1);
         tc_fence_after();
         const uint32_t b_hi = smem_u32(ringB + sb * TS_B_STAGE), b_lo = b_hi + BNMAX * BK * 4;
         const uint32_t a_hi = tmemA + ta * 64, a_lo = a_hi + 32;
+        const uint32_t acc0 = seg_start ? 0u : 1u;
+        if (elect_one()) {
 #pragma unroll
-        for (int kk = 0; kk < BK / 8; ++kk) {
-          if (p.dev_flags & 1) break;
-          const uint32_t acc = (i > 0 || kk > 0) ? 1u : 0u;
-          tc_mma_ts(tmem, a_hi + kk * 8, desc_kmajor(b_hi + kk * 32), p.idesc, acc);
-          tc_mma_ts(tmem, a_lo + kk * 8, desc_kmajor(b_hi + kk * 32), p.idesc, 1u);
-          if (!(p.dev_flags & 256)) tc_mma_ts(tmem, a_hi + kk * 8, desc_kmajor(b_lo + kk * 32), p.idesc, 1u);
+          for (int kk = 0; kk < BK / 8; ++kk) {
+            if (p.dev_flags & 1) break;
+            tc_mma_ts(tmem, a_hi + kk * 8, desc_kmajor(b_hi + kk * 32), p.idesc, kk > 0 ? 1u : acc0);
+            tc_mma_ts(tmem, a_lo + kk * 8, desc_kmajor(b_hi + kk * 32), p.idesc, 1u);
+            if (!(p.dev_flags & 256)) tc_mma_ts(tmem, a_hi + kk * 8, desc_kmajor(b_lo + kk * 32), p.idesc, 1u);
+          }
+          tc_commit(b_empty + 8 * sb);
+          tc_commit(t_empty + 8 * ta);
+          if (seg_end) tc_commit(acc_full);
         }
-        tc_commit(b_empty + 8 * sb);
-        tc_commit(t_empty + 8 * ta);
+        __syncwarp();
+        if (seg_end) ++seg;
       }
-      tc_commit(acc_full);
-      dbg_mark(p, 2);
+      if (lane == 0) dbg_mark(p, 2);
     }
   } else {
     // ---------------- converter (warps 2..5): raw weight tile → TMEM hi / lo
     const int quad = warp & 3;
     const int r = quad * 32 + lane;  // tile row = TMEM lane
-    for (int i = 0; i < nkb; ++i) {
+    int sk_seg = 0;
+    for (int i = 0, tile = tile0, kb = kbs0; i < nkb; ++i, kb = (kb + 1 == kbt) ? (++tile, 0) : kb + 1) {
       const int s = i % TS_RA, ta = i % TS_TA;
       mbar_wait(a_full + 8 * s, (i / TS_RA) & 1);
       const char* t = ringA + s * TILE_BYTES;
@@ -660,9 +789,19 @@ __global__ void __launch_bounds__(TS_THREADS, 1)
       tc_fence_before();
       __syncwarp();
       if (lane == 0) mbar_arrive(t_full + 8 * ta);
+      if (p.sk) {
+        if (i == nkb - 1 || kb + 1 == kbt) {
+          epilogue_sk<EPI>(p, tmem, warp, lane, tile, U, last_flag, acc_full, (uint32_t)(sk_seg & 1));
+          tc_fence_before();
+          __syncwarp();
+          if (lane == 0) mbar_arrive(acc_empty);
+          ++sk_seg;
+        }
+      }
     }
-    epilogue<EPI>(p, tmem, warp, lane, m0, n0, split, n_tile * gridDim.x + m_tile, gridDim.x * gridDim.y,
-                  last_flag, acc_full);
+    if (!p.sk)
+      epilogue<EPI>(p, tmem, warp, lane, m0, n0, split, n_tile * gridDim.x + m_tile, gridDim.x * gridDim.y,
+                    last_flag, acc_full);
     if (threadIdx.x == 64) dbg_mark(p, 7);
   }
 
@@ -1254,13 +1393,17 @@ __global__ void __launch_bounds__(DW_THREADS, 1)
       }
     }
   } else if (warp == 1) {
-    // ---------------- MMA issuer: A (dZᵀ hi / lo) from TMEM, B (X hi / lo) from smem
-    if (lane == 0) {
+    // ---------------- MMA issuer: A (dZᵀ hi / lo) from TMEM, B (X hi / lo) from smem.
+    // The whole warp walks the loop (operands stay warp-uniform), one elected lane issues.
+    {
       int cur_m = -1, a_loads = 0, it = 0, local = 0;
       for (int t = t_begin; t < t_end; ++t, ++local) {
         const int m_t = t / n_tiles;
         if (m_t != cur_m) {
-          if (a_loads > 0) tc_commit(a_tempty);  // every MMA on the old A has been issued
+          if (a_loads > 0) {
+            if (elect_one()) tc_commit(a_tempty);  // every MMA on the old A has been issued
+            __syncwarp();
+          }
           mbar_wait(a_tfull, a_loads & 1);
           cur_m = m_t;
           ++a_loads;
@@ -1274,20 +1417,24 @@ __global__ void __launch_bounds__(DW_THREADS, 1)
           mbar_wait(b_full + 8 * s, (it / DW_RB) & 1);
           tc_fence_after();
           const uint32_t b_hi = smem_u32(ringB + s * DW_B_STAGE), b_lo = b_hi + TILE_BYTES;
+          const uint32_t acc0 = kb > 0 ? 1u : 0u;
+          if (elect_one()) {
 #pragma unroll
-          for (int kk = 0; kk < BK / 8; ++kk) {
-            if (p.dev_flags & 1) break;
-            const uint32_t acc = (kb > 0 || kk > 0) ? 1u : 0u;
-            const uint32_t ka = kb * BK + kk * 8;
-            tc_mma_ts(acc_t, tA_hi + ka, desc_mnmajor(b_hi + kk * 1024), p.idesc, acc);
-            if (kX3) {
-              tc_mma_ts(acc_t, tA_lo + ka, desc_mnmajor(b_hi + kk * 1024), p.idesc, 1u);
-              if (!(p.dev_flags & 256)) tc_mma_ts(acc_t, tA_hi + ka, desc_mnmajor(b_lo + kk * 1024), p.idesc, 1u);
+            for (int kk = 0; kk < BK / 8; ++kk) {
+              if (p.dev_flags & 1) break;
+              const uint32_t ka = kb * BK + kk * 8;
+              tc_mma_ts(acc_t, tA_hi + ka, desc_mnmajor(b_hi + kk * 1024), p.idesc, kk > 0 ? 1u : acc0);
+              if (kX3) {
+                tc_mma_ts(acc_t, tA_lo + ka, desc_mnmajor(b_hi + kk * 1024), p.idesc, 1u);
+                if (!(p.dev_flags & 256)) tc_mma_ts(acc_t, tA_hi + ka, desc_mnmajor(b_lo + kk * 1024), p.idesc, 1u);
+              }
             }
+            tc_commit(b_empty + 8 * s);
           }
-          tc_commit(b_empty + 8 * s);
+          __syncwarp();
         }
-        tc_commit(c_full + 8 * buf);
+        if (elect_one()) tc_commit(c_full + 8 * buf);
+        __syncwarp();
       }
     }
   } else if (warp >= load_w0) {
@@ -1628,6 +1775,19 @@ void plan_splits(TcParams& p, int M, int N, int K, int budget) {
 // CTA-pair kernel for fwd / dX (ST_GEMM_PAIR=1). Off by default: both forms run into the
 // 1000 W board power cap on these GEMMs (tools/gemm_power.py: ~1.72 GHz single, ~1.77 GHz
 // pair, same time per GEMM), so the pair's faster MMA issue buys no wall time.
+// Stream-K is opt-in (ST_STREAM_K=1): measured on the 8192² fwd / dX it is no faster
+// than the K-split grid (102 vs 105 µs standalone, 3.14 vs 3.18 ms per wide-FCN step) —
+// the GEMM is bound chip-wide, not by the 20 SMs the split leaves idle — and it loses
+// badly when a tile is cut into many segments (784-wide dX: 25 → 80 µs).
+bool stream_k_off() {
+  static int f = -1;
+  if (f < 0) {
+    const char* e = getenv("ST_STREAM_K");
+    f = (e && atoi(e) == 1) ? 0 : 1;
+  }
+  return f != 0;
+}
+
 bool use_pair() {
   static int f = -1;
   if (f < 0) {
@@ -1648,6 +1808,12 @@ st_status launch_ts(const GemmArgs& g, int M, int N, int K, const CUtensorMap& m
   // pair: the m-tile count is padded to even (the padding CTA's rows are masked)
   const int mt = (M + BM - 1) / BM, mt_grid = pair ? (mt + 1) / 2 * 2 : mt;
   plan_splits(p, mt_grid * BM, N, K, pair ? budget / 2 * 2 : budget);
+  const int nt = (N + BNMAX - 1) / BNMAX;
+  p.mt = mt_grid;
+  p.tiles = mt_grid * nt;
+  // stream-K when the tiles alone cannot fill the CTA budget: every CTA gets the same
+  // number of K-blocks (a K split leaves budget − tiles·splits SMs idle)
+  p.sk = (!pair && p.tiles < budget && !stream_k_off()) ? 1 : 0;
   p.M = M;
   p.out = out;
   p.aux = aux;
@@ -1667,8 +1833,13 @@ st_status launch_ts(const GemmArgs& g, int M, int N, int K, const CUtensorMap& m
   CUtensorMap mb, mblo;
   if (!make_map(&mb, Bact, K, N, K, brows, false) || !make_map(&mblo, blo, K, N, K, brows, false))
     return set_error(ST_ERR_CUDA, "cuTensorMapEncodeTiled failed (activation operand)");
-  const int nt = (N + BNMAX - 1) / BNMAX;
   dim3 grid(mt_grid, nt, p.splits);
+  if (p.sk) {
+    const long long U = (long long)p.tiles * p.kb_total;
+    grid = dim3((unsigned)std::min<long long>(budget, U), 1, 1);
+    p.splits = 1;
+    p.ext_reduce = 0;
+  }
   if (pair) {
     auto kern = tc_ts2_kernel<EPI, A_MN>;
     static bool attr_set = false;
