@@ -106,6 +106,16 @@ __device__ __forceinline__ void tma_load_2d(uint32_t dst, const CUtensorMap* map
       : "memory");
 }
 __device__ __forceinline__ void fence_proxy_async() { asm volatile("fence.proxy.async.shared::cta;" ::: "memory"); }
+// TMA store of a 2-D box from smem (bulk-group completion)
+__device__ __forceinline__ void tma_store_2d(const CUtensorMap* map, uint32_t src, int c0, int c1) {
+  asm volatile("cp.async.bulk.tensor.2d.global.shared::cta.bulk_group [%0, {%2, %3}], [%1];" ::"l"(
+                   reinterpret_cast<uint64_t>(map)),
+               "r"(src), "r"(c0), "r"(c1)
+               : "memory");
+}
+__device__ __forceinline__ void bulk_commit() { asm volatile("cp.async.bulk.commit_group;" ::: "memory"); }
+template <int N>
+__device__ __forceinline__ void bulk_wait_read() { asm volatile("cp.async.bulk.wait_group.read %0;" ::"n"(N) : "memory"); }
 __device__ __forceinline__ void tc_fence_before() { asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory"); }
 __device__ __forceinline__ void tc_fence_after() { asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory"); }
 
@@ -1269,7 +1279,7 @@ __device__ __forceinline__ void update_block16_vec(const UpdateArgs& u, size_t M
 // ============================================================================
 constexpr int DW_KMAX = 128;                       // K (= batch) capacity of the resident A
 #ifndef ST_DW_RB
-#define ST_DW_RB 4
+#define ST_DW_RB 3
 #endif
 constexpr int DW_RB = ST_DW_RB;                    // B ring stages (hi + lo, 32 KB)
 constexpr int DW_EPI_WARPS = 16;                   // 2 groups × 2 warps per TMEM lane quadrant
@@ -1280,7 +1290,7 @@ constexpr int DW_A_BYTES = (DW_KMAX / BK) * TILE_BYTES;  // raw A staging: 64 KB
 constexpr int DW_B_STAGE = 2 * TILE_BYTES;
 constexpr int DW_WV_COLS = 16;                     // columns (n) per W / V chunk
 #ifndef ST_DW_WV_SLOTS
-#define ST_DW_WV_SLOTS 3
+#define ST_DW_WV_SLOTS 4
 #endif
 constexpr int DW_WV_SLOTS = ST_DW_WV_SLOTS;        // ring slots per group
 constexpr int DW_WV_HALF = DW_WV_COLS * BM * 4;    // 8 KB: one tensor's chunk [16][128]
@@ -1343,7 +1353,7 @@ __global__ void __launch_bounds__(DW_THREADS, 1)
     }
     for (int s = 0; s < 2 * DW_WV_SLOTS; ++s) {
       mbar_init(wv_full + 8 * s, 1);
-      mbar_init(wv_empty + 8 * s, DW_EPI_WARPS / 2);
+      mbar_init(wv_empty + 8 * s, DW_EPI_WARPS / 2);  // the group's 8 warps wrote w', v' back
     }
     asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
   }
@@ -1383,6 +1393,10 @@ __global__ void __launch_bounds__(DW_THREADS, 1)
           const int s = it % DW_RB;
           mbar_wait(b_empty + 8 * s, ((it / DW_RB) & 1) ^ 1);
           const uint32_t full = b_full + 8 * s;
+          if (p.dev_flags & 4) {  // development: skip the B loads
+            mbar_arrive(full);
+            continue;
+          }
           mbar_expect_tx(full, bytes);
           const uint32_t dB = smem_u32(ringB + s * DW_B_STAGE);
           for (int c = 0; c < nbox; ++c) {
@@ -1438,23 +1452,50 @@ __global__ void __launch_bounds__(DW_THREADS, 1)
       }
     }
   } else if (warp >= load_w0) {
-    // ---------------- W / V stream loader of group (warp − load_w0): TMA into the ring
+    // ---------------- W / V stream of group (warp − load_w0), one thread: TMA loads into
+    // the ring and TMA stores of the updated chunks out of it. Chunk q lives in slot
+    // q % SLOTS; once the group's 8 warps have written w', v' back into it (wv_empty[q],
+    // 8 arrivals) the chunk is stored, and once that store has read the slot, chunk
+    // q + SLOTS is loaded into it. The epilogue warps never wait for one another.
     if (kUPD && p.wv_stream && lane == 0) {
       const int group = warp - load_w0;
-      const uint32_t full0 = wv_full + 8 * DW_WV_SLOTS * group, empty0 = wv_empty + 8 * DW_WV_SLOTS * group;
+      const uint32_t full0 = wv_full + 8 * DW_WV_SLOTS * group, done0 = wv_empty + 8 * DW_WV_SLOTS * group;
       char* ring = ringWV + group * DW_WV_SLOTS * DW_WV_SLOT;
-      int q = 0;
-      for (int t = t_begin + group; t < t_end; t += 2) {
-        const int m_t = t / n_tiles, n_t = t % n_tiles;
-        for (int c = 0; c < nch; ++c, ++q) {
-          const int sl = q % DW_WV_SLOTS;
-          mbar_wait(empty0 + 8 * sl, ((q / DW_WV_SLOTS) & 1) ^ 1);
-          mbar_expect_tx(full0 + 8 * sl, DW_WV_SLOT);
-          const uint32_t dst = smem_u32(ring + sl * DW_WV_SLOT);
-          tma_load_2d(dst, &mapW, m_t * BM, n_t * BNMAX + c * DW_WV_COLS, full0 + 8 * sl);
-          tma_load_2d(dst + DW_WV_HALF, &mapV, m_t * BM, n_t * BNMAX + c * DW_WV_COLS, full0 + 8 * sl);
+      const int my_tiles = (t_end - (t_begin + group) + 1) / 2;
+      const int nq = my_tiles > 0 ? my_tiles * nch : 0;
+      auto coords = [&](int q, int& cm, int& cn) {
+        const int t = t_begin + group + 2 * (q / nch), c = q % nch;
+        cm = (t / n_tiles) * BM;
+        cn = (t % n_tiles) * BNMAX + c * DW_WV_COLS;
+      };
+      auto load = [&](int q) {
+        const int sl = q % DW_WV_SLOTS;
+        if (p.dev_flags & 64) {  // development: skip the W / V loads
+          mbar_arrive(full0 + 8 * sl);
+          return;
         }
+        int cm, cn;
+        coords(q, cm, cn);
+        mbar_expect_tx(full0 + 8 * sl, DW_WV_SLOT);
+        const uint32_t dst = smem_u32(ring + sl * DW_WV_SLOT);
+        tma_load_2d(dst, &mapW, cm, cn, full0 + 8 * sl);
+        tma_load_2d(dst + DW_WV_HALF, &mapV, cm, cn, full0 + 8 * sl);
+      };
+      for (int q = 0; q < min(nq, DW_WV_SLOTS); ++q) load(q);
+      for (int q = 0; q < nq; ++q) {
+        const int sl = q % DW_WV_SLOTS;
+        mbar_wait(done0 + 8 * sl, (q / DW_WV_SLOTS) & 1);  // w', v' of chunk q are in the slot
+        int cm, cn;
+        coords(q, cm, cn);
+        const uint32_t src = smem_u32(ring + sl * DW_WV_SLOT);
+        tma_store_2d(&mapW, src, cm, cn);
+        tma_store_2d(&mapV, src + DW_WV_HALF, cm, cn);
+        bulk_commit();
+        // refill the slot of the previous chunk once its store has read it
+        bulk_wait_read<1>();
+        if (q >= 1 && q - 1 + DW_WV_SLOTS < nq) load(q - 1 + DW_WV_SLOTS);
       }
+      asm volatile("cp.async.bulk.wait_group 0;" ::: "memory");  // the updates are in memory before exit
     }
   } else if (warp >= conv_w0) {
     // ---------------- converter: staged dZᵀ (MN-major boxes) → TMEM hi / lo, once per m-tile
@@ -1501,9 +1542,12 @@ __global__ void __launch_bounds__(DW_THREADS, 1)
     if (kUPD && p.wv_stream) {
       // W / V from the smem ring: every chunk is consumed by all 8 warps of the group
       // (one consumer timeline per ring); this warp takes rows quad·32 + lane, columns
-      // half·8 .. half·8 + 7 of the chunk.
+      // half·8 .. half·8 + 7 of the chunk. w', v' are written back INTO the slot and leave
+      // by TMA store (issued by the group's stream thread once all 8 warps have arrived
+      // on wv_empty): no per-warp global stores for W / V. WF / WB (only when s > 0) are
+      // stored from registers.
       const uint32_t full0 = wv_full + 8 * DW_WV_SLOTS * group, empty0 = wv_empty + 8 * DW_WV_SLOTS * group;
-      const char* ring = ringWV + group * DW_WV_SLOTS * DW_WV_SLOT;
+      char* ring = ringWV + group * DW_WV_SLOTS * DW_WV_SLOT;
       const UpdateArgs& u = p.upd;
       int q = 0;
       for (int t = t_begin + group; t < t_end; t += 2, local += 2) {
@@ -1519,34 +1563,32 @@ __global__ void __launch_bounds__(DW_THREADS, 1)
           uint32_t rr[8];
           tc_ld8_nowait(trow + c0, rr);
           mbar_wait(full0 + 8 * sl, (q / DW_WV_SLOTS) & 1);
-          const float* sw = reinterpret_cast<const float*>(ring + sl * DW_WV_SLOT) + half * 8 * BM + quad * 32 + lane;
-          const float* sv = sw + DW_WV_HALF / 4;
+          float* sw = reinterpret_cast<float*>(ring + sl * DW_WV_SLOT) + half * 8 * BM + quad * 32 + lane;
+          float* sv = sw + DW_WV_HALF / 4;
           float w[8], v[8];
 #pragma unroll
           for (int j = 0; j < 8; ++j) {
             w[j] = sw[j * BM];
             v[j] = sv[j * BM];
           }
-          __syncwarp();
-          if (lane == 0) mbar_arrive(empty0 + 8 * sl);  // slot refillable: values are in registers
           tc_wait_ld();
-          if (p.dev_flags & 16) continue;
           const int nc = n0 + c0;
-          if (m < p.M) {
 #pragma unroll
-            for (int j = 0; j < 8; ++j) {
-              if (nc + j < p.N) {
-                const float g = __uint_as_float(rr[j]);
-                const float vn = __fmaf_rn(u.c.c_gamma, v[j], __fmul_rn(u.c.c_one, g));
-                const float wn = __fmaf_rn(-u.c.c_eta, vn, w[j]);
-                const size_t o = (size_t)(nc + j) * p.M + m;
-                __stcs(u.W + o, wn);
-                __stcs(u.V + o, vn);
-                if (u.WF) __stcs(u.WF + o, __fmaf_rn(-u.c.c_f, vn, wn));
-                if (u.WB) __stcs(u.WB + o, __fmaf_rn(-u.c.c_b, vn, wn));
-              }
+          for (int j = 0; j < 8; ++j) {
+            const float g = __uint_as_float(rr[j]);
+            const float vn = __fmaf_rn(u.c.c_gamma, v[j], __fmul_rn(u.c.c_one, g));
+            const float wn = __fmaf_rn(-u.c.c_eta, vn, w[j]);
+            sw[j * BM] = wn;  // out-of-range rows / columns are clipped by the TMA store
+            sv[j * BM] = vn;
+            if ((u.WF || u.WB) && m < p.M && nc + j < p.N) {
+              const size_t o = (size_t)(nc + j) * p.M + m;
+              if (u.WF) __stcs(u.WF + o, __fmaf_rn(-u.c.c_f, vn, wn));
+              if (u.WB) __stcs(u.WB + o, __fmaf_rn(-u.c.c_b, vn, wn));
             }
           }
+          fence_proxy_async();  // the generic-proxy writes above are read by the TMA store
+          __syncwarp();
+          if (lane == 0) mbar_arrive(empty0 + 8 * sl);  // this warp's part of chunk q is written back
         }
         tc_fence_before();
         __syncwarp();
