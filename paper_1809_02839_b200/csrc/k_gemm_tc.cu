@@ -945,8 +945,9 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(TS_THREADS, 1)
   if (threadIdx.x == 0) dbg_mark(p, 1);
 
   if (warp == 0) {
-    // ---------------- TMA producer, weights (A): this CTA's 128 rows
-    if (lane == 0) {
+    // ---------------- TMA producer, weights (A): this CTA's 128 rows (warp-converged loop,
+    // elected lane issues: the tensor-map coordinates stay in uniform registers)
+    {
       const bool oob = m0 >= p.M;  // padding CTA of an odd tile count: rows masked at the end
       uint64_t w_f = 0;
       for (int i = 0; i < nkb; ++i) {
@@ -955,35 +956,41 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(TS_THREADS, 1)
         mbar_wait(a_free + 8 * s, ((i / TS_RA) & 1) ^ 1);
         w_f += clock64() - c0;
         const uint32_t full = a_full + 8 * s;
-        if (oob || (p.dev_flags & 8)) {
-          mbar_arrive(full);
-          continue;
-        }
-        mbar_expect_tx(full, TILE_BYTES);
         const int k0 = (kb0 + i) * BK;
         const uint32_t dA = smem_u32(ringA + s * TILE_BYTES);
-        if (A_MN) {
+        if (elect_one()) {
+          if (oob || (p.dev_flags & 8)) {
+            mbar_arrive(full);
+          } else {
+            mbar_expect_tx(full, TILE_BYTES);
+            if (A_MN) {
 #pragma unroll
-          for (int c = 0; c < BM / 32; ++c) tma_load_2d(dA + c * 4096, &mapA, m0 + 32 * c, k0, full);
-        } else {
-          tma_load_2d(dA, &mapA, k0, m0, full);
+              for (int c = 0; c < BM / 32; ++c) tma_load_2d(dA + c * 4096, &mapA, m0 + 32 * c, k0, full);
+            } else {
+              tma_load_2d(dA, &mapA, k0, m0, full);
+            }
+          }
         }
+        __syncwarp();
       }
-      dbg_put(p, 15, w_f);
+      if (lane == 0) dbg_put(p, 15, w_f);
     }
   } else if (warp == 6) {
     // ---------------- TMA producer, activations: rows n0 + rank·bn/2 .. +bn/2 (hi + lo)
-    if (lane == 0) {
+    {
       const uint32_t bytes = (uint32_t)(2 * 2 * bh * BK * 4);  // both CTAs, hi + lo
       for (int i = 0; i < nkb; ++i) {
         const int s = i % TS2_RB;
         mbar_wait(b_empty + 8 * s, ((i / TS2_RB) & 1) ^ 1);
         const uint32_t full_leader = map_to_rank(b_full + 8 * s, 0);
-        if (rank == 0) mbar_expect_tx(b_full + 8 * s, bytes);
         const int k0 = (kb0 + i) * BK;
         const uint32_t dB = smem_u32(ringB + s * TS2_B_STAGE);
-        tma_load_2d_pair(dB, &mapB, k0, n0 + (int)rank * bh, full_leader);
-        tma_load_2d_pair(dB + (BNMAX / 2) * BK * 4, &mapBlo, k0, n0 + (int)rank * bh, full_leader);
+        if (elect_one()) {
+          if (rank == 0) mbar_expect_tx(b_full + 8 * s, bytes);
+          tma_load_2d_pair(dB, &mapB, k0, n0 + (int)rank * bh, full_leader);
+          tma_load_2d_pair(dB + (BNMAX / 2) * BK * 4, &mapBlo, k0, n0 + (int)rank * bh, full_leader);
+        }
+        __syncwarp();
       }
     }
   } else if (warp == 1) {
@@ -1375,19 +1382,23 @@ __global__ void __launch_bounds__(DW_THREADS, 1)
 
   if (warp == 0) {
     // ---------------- TMA producer: A staging per m-tile, B ring per tile × K-block
-    if (lane == 0) {
+    // (warp-converged loop, elected lane issues)
+    {
       int cur_m = -1, a_loads = 0, it = 0;
       for (int t = t_begin; t < t_end; ++t) {
         const int m_t = t / n_tiles, n_t = t % n_tiles;
         if (m_t != cur_m) {
           // drain the B ring (the staging aliases it): the MMAs of every issued B stage are done
           for (int j = max(0, it - DW_RB); j < it; ++j) mbar_wait(b_empty + 8 * (j % DW_RB), (j / DW_RB) & 1);
-          mbar_expect_tx(a_full, (uint32_t)(nkb * TILE_BYTES));
-          for (int kb = 0; kb < nkb; ++kb) {
-            const uint32_t dA = smem_u32(Astage + kb * TILE_BYTES);
+          if (elect_one()) {
+            mbar_expect_tx(a_full, (uint32_t)(nkb * TILE_BYTES));
+            for (int kb = 0; kb < nkb; ++kb) {
+              const uint32_t dA = smem_u32(Astage + kb * TILE_BYTES);
 #pragma unroll
-            for (int c = 0; c < BM / 32; ++c) tma_load_2d(dA + c * 4096, &mapA, m_t * BM + 32 * c, kb * BK, a_full);
+              for (int c = 0; c < BM / 32; ++c) tma_load_2d(dA + c * 4096, &mapA, m_t * BM + 32 * c, kb * BK, a_full);
+            }
           }
+          __syncwarp();
           // B may overwrite the staging only once the converter has read it
           mbar_wait(a_sfree, a_loads & 1);
           cur_m = m_t;
@@ -1399,16 +1410,19 @@ __global__ void __launch_bounds__(DW_THREADS, 1)
           const int s = it % DW_RB;
           mbar_wait(b_empty + 8 * s, ((it / DW_RB) & 1) ^ 1);
           const uint32_t full = b_full + 8 * s;
-          if (p.dev_flags & 4) {  // development: skip the B loads
-            mbar_arrive(full);
-            continue;
-          }
-          mbar_expect_tx(full, bytes);
           const uint32_t dB = smem_u32(ringB + s * DW_B_STAGE);
-          for (int c = 0; c < nbox; ++c) {
-            tma_load_2d(dB + c * 4096, &mapB, n_t * BNMAX + 32 * c, kb * BK, full);
-            if (kX3) tma_load_2d(dB + TILE_BYTES + c * 4096, &mapBlo, n_t * BNMAX + 32 * c, kb * BK, full);
+          if (elect_one()) {
+            if (p.dev_flags & 4) {  // development: skip the B loads
+              mbar_arrive(full);
+            } else {
+              mbar_expect_tx(full, bytes);
+              for (int c = 0; c < nbox; ++c) {
+                tma_load_2d(dB + c * 4096, &mapB, n_t * BNMAX + 32 * c, kb * BK, full);
+                if (kX3) tma_load_2d(dB + TILE_BYTES + c * 4096, &mapBlo, n_t * BNMAX + 32 * c, kb * BK, full);
+              }
+            }
           }
+          __syncwarp();
         }
       }
     }
@@ -1463,8 +1477,9 @@ __global__ void __launch_bounds__(DW_THREADS, 1)
     // q % SLOTS; once the group's 8 warps have written w', v' back into it (wv_empty[q],
     // 8 arrivals) the chunk is stored, and once that store has read the slot, chunk
     // q + SLOTS is loaded into it. The epilogue warps never wait for one another.
-    if (kUPD && p.wv_stream && lane == 0) {
+    if (kUPD && p.wv_stream) {
       const int group = warp - load_w0;
+      const bool leader = elect_one();
       const uint32_t full0 = wv_full + 8 * DW_WV_SLOTS * group, done0 = wv_empty + 8 * DW_WV_SLOTS * group;
       char* ring = ringWV + group * DW_WV_SLOTS * DW_WV_SLOT;
       const int my_tiles = (t_end - (t_begin + group) + 1) / 2;
@@ -1476,16 +1491,19 @@ __global__ void __launch_bounds__(DW_THREADS, 1)
       };
       auto load = [&](int q) {
         const int sl = q % DW_WV_SLOTS;
-        if (p.dev_flags & 64) {  // development: skip the W / V loads
-          mbar_arrive(full0 + 8 * sl);
-          return;
-        }
         int cm, cn;
         coords(q, cm, cn);
-        mbar_expect_tx(full0 + 8 * sl, DW_WV_SLOT);
         const uint32_t dst = smem_u32(ring + sl * DW_WV_SLOT);
-        tma_load_2d(dst, &mapW, cm, cn, full0 + 8 * sl);
-        tma_load_2d(dst + DW_WV_HALF, &mapV, cm, cn, full0 + 8 * sl);
+        if (leader) {
+          if (p.dev_flags & 64) {  // development: skip the W / V loads
+            mbar_arrive(full0 + 8 * sl);
+          } else {
+            mbar_expect_tx(full0 + 8 * sl, DW_WV_SLOT);
+            tma_load_2d(dst, &mapW, cm, cn, full0 + 8 * sl);
+            tma_load_2d(dst + DW_WV_HALF, &mapV, cm, cn, full0 + 8 * sl);
+          }
+        }
+        __syncwarp();
       };
       for (int q = 0; q < min(nq, DW_WV_SLOTS); ++q) load(q);
       for (int q = 0; q < nq; ++q) {
@@ -1494,14 +1512,18 @@ __global__ void __launch_bounds__(DW_THREADS, 1)
         int cm, cn;
         coords(q, cm, cn);
         const uint32_t src = smem_u32(ring + sl * DW_WV_SLOT);
-        tma_store_2d(&mapW, src, cm, cn);
-        tma_store_2d(&mapV, src + DW_WV_HALF, cm, cn);
-        bulk_commit();
-        // refill the slot of the previous chunk once its store has read it
-        bulk_wait_read<1>();
+        if (leader) {
+          tma_store_2d(&mapW, src, cm, cn);
+          tma_store_2d(&mapV, src + DW_WV_HALF, cm, cn);
+          bulk_commit();
+          // refill the slot of the previous chunk once its store has read it
+          bulk_wait_read<1>();
+        }
+        __syncwarp();
         if (q >= 1 && q - 1 + DW_WV_SLOTS < nq) load(q - 1 + DW_WV_SLOTS);
       }
-      asm volatile("cp.async.bulk.wait_group 0;" ::: "memory");  // the updates are in memory before exit
+      if (leader) asm volatile("cp.async.bulk.wait_group 0;" ::: "memory");  // updates in memory before exit
+      __syncwarp();
     }
   } else if (warp >= conv_w0) {
     // ---------------- converter: staged dZᵀ (MN-major boxes) → TMEM hi / lo, once per m-tile
