@@ -199,6 +199,21 @@ def test_kernel_launch_accounting_and_profile(st):
     s.close()
 
 
+def test_profiling_class_mask(st):
+    """st_set_profiling with a class mask brackets only the selected classes."""
+    model = sd.mlp([784, 256, 10], cuts=[])
+    (s,) = build_pipeline(model, 32, 0.05, gemm=gemm_mode(st), max_mb=4)
+    w0, X, Y = sd.parity_inputs(model, 4, 32, 9)
+    s.set_params(w0[0])
+    s.set_profiling(True, ["gemm_dw"])
+    s.run(4, torch.from_numpy(X).to(s.device), torch.from_numpy(Y).to(s.device))
+    prof = s.profile()
+    assert prof["gemm_dw"][1] == 8 and prof["gemm_dw"][0] > 0
+    assert all(prof[k][1] == 0 for k in prof if k != "gemm_dw")
+    s.set_profiling(False)
+    s.close()
+
+
 def test_fused_and_unfused_update_paths_agree(st):
     """st_run (K-B fused into the dW epilogues) and the verb path (st_stage_backward
     writes G, st_predict_and_update runs K-B) give the same weights bit for bit."""

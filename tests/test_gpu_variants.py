@@ -1,0 +1,28 @@
+"""The GEMM kernels behind the environment switches (ST_GEMM_PAIR=0: single-CTA fwd / dX
+kernel; ST_STREAM_K=1 with it: stream-K work split) against the same fp64 references and
+the same pipeline parity gate as the default CTA-pair path. The switches are read once
+per process, so each variant runs the existing tests in a child pytest."""
+import os
+import subprocess
+import sys
+
+import pytest
+
+ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+
+CASES = [
+    "tests/test_gpu_kernels.py::test_stage_gemms_vs_fp64",
+    "tests/test_gpu_pipeline.py::test_deep_mlp_8stage",
+    "tests/test_gpu_pipeline.py::test_ragged_shapes_and_M_smaller_than_depth",
+    "tests/test_gpu_pipeline.py::test_mlp_2stage_config0",
+]
+
+
+@pytest.mark.gpu
+@pytest.mark.parametrize("env", [{"ST_GEMM_PAIR": "0"}, {"ST_GEMM_PAIR": "0", "ST_STREAM_K": "1"}],
+                         ids=["single_cta", "stream_k"])
+def test_gemm_variants_pass_parity(env):
+    e = dict(os.environ, **env)
+    r = subprocess.run([sys.executable, "-m", "pytest", "-q", "-x", "-m", "gpu", "-p", "no:cacheprovider",
+                        "-k", "not tf32", *CASES], cwd=ROOT, env=e, capture_output=True, text=True, timeout=900)
+    assert r.returncode == 0, r.stdout[-3000:] + r.stderr[-2000:]
