@@ -1366,7 +1366,7 @@ __global__ void __launch_bounds__(DW_THREADS, 1)
     }
     for (int s = 0; s < 2 * DW_WV_SLOTS; ++s) {
       mbar_init(wv_full + 8 * s, 1);
-      mbar_init(wv_empty + 8 * s, DW_EPI_WARPS / 2);  // the group's 8 warps wrote w', v' back
+      mbar_init(wv_empty + 8 * s, DW_EPI_WARPS / 4);  // the chunk's 4 warps wrote w', v' back
     }
     asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
   }
@@ -1516,11 +1516,11 @@ __global__ void __launch_bounds__(DW_THREADS, 1)
           tma_store_2d(&mapW, src, cm, cn);
           tma_store_2d(&mapV, src + DW_WV_HALF, cm, cn);
           bulk_commit();
-          // refill the slot of the previous chunk once its store has read it
-          bulk_wait_read<1>();
+          // refill the slot as soon as its store has read it (the global writes stay in flight)
+          bulk_wait_read<0>();
         }
         __syncwarp();
-        if (q >= 1 && q - 1 + DW_WV_SLOTS < nq) load(q - 1 + DW_WV_SLOTS);
+        if (q + DW_WV_SLOTS < nq) load(q + DW_WV_SLOTS);
       }
       if (leader) asm volatile("cp.async.bulk.wait_group 0;" ::: "memory");  // updates in memory before exit
       __syncwarp();
@@ -1568,12 +1568,12 @@ __global__ void __launch_bounds__(DW_THREADS, 1)
     const int half = ((warp - 2) >> 2) & 1;  // which 64 columns of the tile (G store) / 8 of each chunk's 16 (stream)
     int local = group;
     if (kUPD && p.wv_stream) {
-      // W / V from the smem ring: every chunk is consumed by all 8 warps of the group
-      // (one consumer timeline per ring); this warp takes rows quad·32 + lane, columns
-      // half·8 .. half·8 + 7 of the chunk. w', v' are written back INTO the slot and leave
-      // by TMA store (issued by the group's stream thread once all 8 warps have arrived
-      // on wv_empty): no per-warp global stores for W / V. WF / WB (only when s > 0) are
-      // stored from registers.
+      // W / V from the smem ring: chunk c of a tile is consumed by the 4 warps (one per
+      // TMEM lane quadrant) of parity c & 1, so two chunks are in flight per group; this
+      // warp takes rows quad·32 + lane, all 16 columns. w', v' are written back INTO the
+      // slot and leave by TMA store (issued by the group's stream thread once the 4 warps
+      // have arrived on wv_empty): no per-warp global stores for W / V. WF / WB (only when
+      // s > 0) are stored from registers.
       const uint32_t full0 = wv_full + 8 * DW_WV_SLOTS * group, empty0 = wv_empty + 8 * DW_WV_SLOTS * group;
       char* ring = ringWV + group * DW_WV_SLOTS * DW_WV_SLOT;
       const UpdateArgs& u = p.upd;
@@ -1586,23 +1586,24 @@ __global__ void __launch_bounds__(DW_THREADS, 1)
         const uint32_t trow = tmem + group * BNMAX + ((uint32_t)(quad * 32) << 16);
         const int n0 = n_t * BNMAX;
         for (int c = 0; c < nch; ++c, ++q) {
+          if ((c & 1) != half) continue;
           const int sl = q % DW_WV_SLOTS;
-          const int c0 = c * DW_WV_COLS + half * 8;  // first tile column of this warp
-          uint32_t rr[8];
-          tc_ld8_nowait(trow + c0, rr);
+          const int c0 = c * DW_WV_COLS;  // first tile column of the chunk
+          uint32_t rr[16];
+          tc_ld16_nowait(trow + c0, rr);
           mbar_wait(full0 + 8 * sl, (q / DW_WV_SLOTS) & 1);
-          float* sw = reinterpret_cast<float*>(ring + sl * DW_WV_SLOT) + half * 8 * BM + quad * 32 + lane;
+          float* sw = reinterpret_cast<float*>(ring + sl * DW_WV_SLOT) + quad * 32 + lane;
           float* sv = sw + DW_WV_HALF / 4;
-          float w[8], v[8];
+          float w[16], v[16];
 #pragma unroll
-          for (int j = 0; j < 8; ++j) {
+          for (int j = 0; j < 16; ++j) {
             w[j] = sw[j * BM];
             v[j] = sv[j * BM];
           }
           tc_wait_ld();
           const int nc = n0 + c0;
 #pragma unroll
-          for (int j = 0; j < 8; ++j) {
+          for (int j = 0; j < 16; ++j) {
             const float g = __uint_as_float(rr[j]);
             const float vn = __fmaf_rn(u.c.c_gamma, v[j], __fmul_rn(u.c.c_one, g));
             const float wn = __fmaf_rn(-u.c.c_eta, vn, w[j]);
