@@ -624,7 +624,12 @@ static st_status forward_compute(st_ctx* c, int64_t mb, const float* x_dev, cons
       out = slot + c->layers[l + 1].stash_off;
     else if (l + 1 == nl)
       out = c->last_stage ? c->logits : c->send_fwd;
-    if (L.kind == ST_LAYER_CONV) {
+    if (L.kind == ST_LAYER_CONV && tc_conv_ok(c->gemm, L.hw, L.hw, L.n_in, L.n_out)) {
+      Timed t(c, KC_GEMM_FWD);  // implicit GEMM: the shifted windows come straight from `in`
+      ST_TRY(tc_conv_fwd(gargs_rows(c, c->B, 9 * L.n_in, L.n_out), in, L.hw, L.hw, L.n_in, L.n_out, Wh + L.w_off,
+                         L.bias ? Wh + L.b_off : nullptr, out, L.act == ST_ACT_RELU));
+      c->launches += tc_last_launches();
+    } else if (L.kind == ST_LAYER_CONV) {
       const int P = c->B * L.hw * L.hw;
       {
         Timed t(c, KC_LOSS);
@@ -772,6 +777,24 @@ static st_status backward_compute(st_ctx* c, int64_t mb, bool fused = false) {
       if (D) {
         Timed t(c, KC_LOSS);
         ST_TRY(launch_maxpool_bwd(Ain, dZ, c->B, L.hw, L.hw, L.n_in, producer_act == ST_ACT_RELU, D, c->stream));
+        c->launches += 1;
+      }
+    } else if (L.kind == ST_LAYER_CONV && tc_conv_ok(c->gemm, L.hw, L.hw, L.n_in, L.n_out)) {
+      // implicit GEMMs: dX = conv with the flipped kernel (ReLU mask of the producer of
+      // Ain fused), then dW = Σ_p window(Ain)ᵀ dZ (+ bias gradient) into G
+      if (D) {
+        Timed t(c, KC_GEMM_DX);
+        ST_TRY(tc_conv_dx(gargs_rows(c, c->B, 9 * L.n_in, L.n_out), dZ, L.hw, L.hw, L.n_in, L.n_out, Wh + L.w_off,
+                          producer_act == ST_ACT_RELU ? Ain : nullptr, D));
+        c->launches += tc_last_launches();
+      }
+      Timed t(c, KC_GEMM_DW);
+      ST_TRY(tc_conv_dw(gargs_rows(c, c->B, 9 * L.n_in, L.n_out), Ain, dZ, L.hw, L.hw, L.n_in, L.n_out,
+                        c->G + L.w_off, L.bias ? c->G + L.b_off : nullptr));
+      c->launches += tc_last_launches();
+      if (fused) {  // K-B over the layer's weight + bias block (contiguous, S:106 layout)
+        const UpdateArgs u = block_update(c, L.w_off, kc);
+        ST_TRY(launch_update_predict(u.W, u.V, c->G + L.w_off, u.WF, u.WB, (size_t)L.n_params, kc, c->stream));
         c->launches += 1;
       }
     } else if (L.kind == ST_LAYER_CONV) {

@@ -61,6 +61,8 @@ struct TcParams {
   int sk;            // stream-K (fwd / dX TS kernel): CTA b takes chunks [b·U/G, (b+1)·U/G) of
                      // the tile-major (tile, K-block) space, U = tiles · kb_total, G = gridDim.x
   int mt, tiles;     // stream-K: m tiles, total tiles (tile = n_tile · mt + m_tile)
+  int row;           // output element (m, n) at out[m·N + n] (implicit-GEMM conv fwd / dX), else out[n·M + m]
+  int cv_H, cv_W, cv_C;  // implicit-GEMM conv: NHWC image height, width, channels of the implicit operand
 };
 
 // ------------------------------------------------------------------ PTX helpers
@@ -103,6 +105,24 @@ __device__ __forceinline__ void tma_load_2d(uint32_t dst, const CUtensorMap* map
       "cp.async.bulk.tensor.2d.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1, {%2, %3}], [%4];" ::"r"(
           dst),
       "l"(reinterpret_cast<uint64_t>(map)), "r"(c0), "r"(c1), "r"(bar)
+      : "memory");
+}
+__device__ __forceinline__ void tma_load_3d(uint32_t dst, const CUtensorMap* map, int c0, int c1, int c2,
+                                            uint32_t bar) {
+  asm volatile(
+      "cp.async.bulk.tensor.3d.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1, {%2, %3, %4}], [%5];" ::
+          "r"(dst),
+      "l"(reinterpret_cast<uint64_t>(map)), "r"(c0), "r"(c1), "r"(c2), "r"(bar)
+      : "memory");
+}
+// 4-D box of an NHWC activation tensor (dims C, W, H, B); coordinates may be negative or
+// past the edge: TMA zero-fills those elements, which is exactly the conv's zero padding.
+__device__ __forceinline__ void tma_load_4d(uint32_t dst, const CUtensorMap* map, int c0, int c1, int c2, int c3,
+                                            uint32_t bar) {
+  asm volatile(
+      "cp.async.bulk.tensor.4d.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1, {%2, %3, %4, %5}], "
+      "[%6];" ::"r"(dst),
+      "l"(reinterpret_cast<uint64_t>(map)), "r"(c0), "r"(c1), "r"(c2), "r"(c3), "r"(bar)
       : "memory");
 }
 __device__ __forceinline__ void fence_proxy_async() { asm volatile("fence.proxy.async.shared::cta;" ::: "memory"); }
@@ -223,6 +243,45 @@ __device__ __forceinline__ void dbg_put(const TcParams& p, int slot, uint64_t v)
 template <int EPI>
 __device__ __forceinline__ void epilogue_store16(const TcParams& p, int m, int n0c, const float* acc, float bias) {
   const int nv = min(16, p.N - n0c);
+  if (p.row) {
+    // row-major output (implicit conv): this thread's 16 columns are contiguous; bias by
+    // column; the dX mask has the output's indexing. float4 when the row pitch allows it.
+    float v[16];
+    float* dst = p.out + (size_t)m * p.N + n0c;
+    const float* mk = (EPI == EPI_DX && p.aux) ? p.aux + (size_t)m * p.N + n0c : nullptr;
+    if (nv == 16 && (p.N & 3) == 0) {
+      float mv[16];
+      if (mk) {
+#pragma unroll
+        for (int j = 0; j < 16; j += 4) *reinterpret_cast<float4*>(mv + j) = __ldg(reinterpret_cast<const float4*>(mk + j));
+      }
+#pragma unroll
+      for (int j = 0; j < 16; ++j) {
+        float x = acc[j];
+        if (EPI == EPI_FWD) {
+          if (p.aux) x += __ldg(p.aux + n0c + j);
+          if (p.relu) x = fmaxf(x, 0.f);
+        } else if (EPI == EPI_DX && mk) {
+          x = (mv[j] > 0.f) ? x : 0.f;
+        }
+        v[j] = x;
+      }
+#pragma unroll
+      for (int j = 0; j < 16; j += 4) *reinterpret_cast<float4*>(dst + j) = *reinterpret_cast<const float4*>(v + j);
+    } else {
+      for (int j = 0; j < nv; ++j) {
+        float x = acc[j];
+        if (EPI == EPI_FWD) {
+          if (p.aux) x += p.aux[n0c + j];
+          if (p.relu) x = fmaxf(x, 0.f);
+        } else if (EPI == EPI_DX && mk) {
+          x = (mk[j] > 0.f) ? x : 0.f;
+        }
+        dst[j] = x;
+      }
+    }
+    return;
+  }
   if (EPI == EPI_DX && p.aux) {
     float mk[16];
 #pragma unroll
@@ -279,7 +338,7 @@ __device__ __forceinline__ void epilogue(const TcParams& p, uint32_t tmem, int w
     if (ctid == 0) dbg_mark(p, 5);
     if (*last_flag) {
       __threadfence();
-      const float bias = (EPI == EPI_FWD && p.aux && m < p.M) ? p.aux[m] : 0.f;
+      const float bias = (EPI == EPI_FWD && p.aux && m < p.M && !p.row) ? p.aux[m] : 0.f;
       // Fixed split order 0..S−1 (deterministic); this CTA's own partial comes from
       // TMEM, the others from the workspace. 32 columns per chunk with every global load
       // of the chunk (partials, dX mask) issued before the first use: the fix-up is
@@ -289,7 +348,9 @@ __device__ __forceinline__ void epilogue(const TcParams& p, uint32_t tmem, int w
         const int nv = min(32, p.N - (n0 + c));
         if (EPI == EPI_DX && p.aux && m < p.M) {
 #pragma unroll
-          for (int j = 0; j < 32; ++j) mk[j] = (j < nv) ? __ldg(p.aux + (size_t)(n0 + c + j) * p.M + m) : 0.f;
+          for (int j = 0; j < 32; ++j)
+            mk[j] = (j < nv) ? __ldg(p.aux + (p.row ? (size_t)m * p.N + (n0 + c + j) : (size_t)(n0 + c + j) * p.M + m))
+                             : 0.f;
         }
 #pragma unroll
         for (int j = 0; j < 32; ++j) acc[j] = 0.f;
@@ -313,12 +374,12 @@ __device__ __forceinline__ void epilogue(const TcParams& p, uint32_t tmem, int w
             if (j < nv) {
               float v = acc[j];
               if (EPI == EPI_FWD) {
-                v += bias;
+                v += p.row ? (p.aux ? p.aux[n0 + c + j] : 0.f) : bias;
                 if (p.relu) v = fmaxf(v, 0.f);
               } else if (EPI == EPI_DX) {
                 if (p.aux && !(mk[j] > 0.f)) v = 0.f;
               }
-              p.out[(size_t)(n0 + c + j) * p.M + m] = v;
+              p.out[p.row ? (size_t)m * p.N + (n0 + c + j) : (size_t)(n0 + c + j) * p.M + m] = v;
             }
           }
         }
@@ -327,7 +388,7 @@ __device__ __forceinline__ void epilogue(const TcParams& p, uint32_t tmem, int w
       if (ctid == 0) dbg_mark(p, 6);
     }
   } else {
-    const float bias = (EPI == EPI_FWD && p.aux && m < p.M) ? p.aux[m] : 0.f;
+    const float bias = (EPI == EPI_FWD && p.aux && m < p.M && !p.row) ? p.aux[m] : 0.f;
     for (int c = 0; c < bn; c += 16) {
       float v[16];
       tc_ld16(trow + c, v);
@@ -336,7 +397,20 @@ __device__ __forceinline__ void epilogue(const TcParams& p, uint32_t tmem, int w
   }
 }
 
-template <int EPI, bool A_MN, bool B_MN, bool kX3, int STAGES>
+// Implicit-GEMM 3×3 / pad-1 convolution (a10) on the same kernel: CV selects how the
+// producer addresses the operands (NHWC activations through 4-D TMA boxes whose
+// out-of-image part TMA zero-fills = the padding; no im2col buffer):
+//   CV_FWD: M = P pixels, N = Cout, K = 9·Cin in (kh, kw, ci) order.  A = X shifted by
+//           (kh−1, kw−1) [128 pixel rows × 32 ci, K-major]; B = W [K × Cout] MN-major.
+//   CV_DX : M = P, N = Cin, K = 9·Cout in (kh, kw, co) order.  A = dZ shifted by
+//           (1−kh, 1−kw) (the flipped kernel); B = W viewed as [9][Cin][Cout] (3-D map),
+//           box {32 co, bn ci, 1}: K-major.
+//   CV_DW : M = Cout, N = 9·Cin, K = P.  A = dZ [P × Cout] MN-major (2-D, as EPI_DW);
+//           B = X shifted by (kh−1, kw−1) [32 pixels × 32 ci boxes, MN-major].
+// CV_FWD / CV_DX write row-major (p.row): out[p·N + n] is NHWC.
+enum { CV_NONE = 0, CV_FWD = 1, CV_DX = 2, CV_DW = 3 };
+
+template <int EPI, bool A_MN, bool B_MN, bool kX3, int STAGES, int CV = CV_NONE>
 __global__ void __launch_bounds__(kThreads, 1)
     tc_gemm_kernel(const __grid_constant__ CUtensorMap mapA, const __grid_constant__ CUtensorMap mapB, TcParams p) {
   extern __shared__ __align__(1024) uint8_t smem_raw[];
@@ -395,6 +469,31 @@ __global__ void __launch_bounds__(kThreads, 1)
         const int k0 = (kb0 + i) * BK;
         const uint32_t dA = smem_u32(smem + s * STAGE_BYTES);
         const uint32_t dB = dA + TILE_BYTES;
+        if (CV == CV_FWD || CV == CV_DX) {
+          // K-block (kh, kw, c0): the 128-pixel tile [b0.., h0.., w0..] shifted by the tap
+          const int HW = p.cv_H * p.cv_W;
+          const int b0 = m0 / HW, r0 = m0 - b0 * HW, h0 = r0 / p.cv_W, w0 = r0 - h0 * p.cv_W;
+          const int q = k0 / p.cv_C, c0 = k0 - q * p.cv_C, kh = q / 3, kw = q - 3 * kh;
+          const int dh = (CV == CV_FWD) ? kh - 1 : 1 - kh, dw = (CV == CV_FWD) ? kw - 1 : 1 - kw;
+          tma_load_4d(dA, &mapA, c0, w0 + dw, h0 + dh, b0, full);
+          if (CV == CV_FWD) {
+            for (int c = 0; c < nbox_b; ++c) tma_load_2d(dB + c * 4096, &mapB, n0 + 32 * c, k0, full);
+          } else {
+            tma_load_3d(dB, &mapB, c0, n0, q, full);
+          }
+          continue;
+        }
+        if (CV == CV_DW) {
+#pragma unroll
+          for (int c = 0; c < BM / 32; ++c) tma_load_2d(dA + c * 4096, &mapA, m0 + 32 * c, k0, full);
+          const int HW = p.cv_H * p.cv_W;
+          const int b0 = k0 / HW, r0 = k0 - b0 * HW, h0 = r0 / p.cv_W, w0 = r0 - h0 * p.cv_W;
+          for (int c = 0; c < nbox_b; ++c) {
+            const int n = n0 + 32 * c, q = n / p.cv_C, ci0 = n - q * p.cv_C, kh = q / 3, kw = q - 3 * kh;
+            tma_load_4d(dB + c * 4096, &mapB, ci0, w0 + kw - 1, h0 + kh - 1, b0, full);
+          }
+          continue;
+        }
         if (A_MN) {
 #pragma unroll
           for (int c = 0; c < BM / 32; ++c) tma_load_2d(dA + c * 4096, &mapA, m0 + 32 * c, k0, full);
@@ -495,7 +594,7 @@ __device__ __forceinline__ void epilogue_sk(const TcParams& p, uint32_t tmem, in
   const uint32_t trow = tmem + ((uint32_t)(quad * 32) << 16);
   const int b_first = sk_owner((long long)tile * kbt, G, U);
   const int nseg = sk_owner((long long)tile * kbt + kbt - 1, G, U) - b_first + 1;
-  const float bias = (EPI == EPI_FWD && p.aux && m < p.M) ? p.aux[m] : 0.f;
+  const float bias = (EPI == EPI_FWD && p.aux && m < p.M && !p.row) ? p.aux[m] : 0.f;
   if (nseg == 1) {
     for (int c = 0; c < bn; c += 16) {
       float v[16];
@@ -1114,7 +1213,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(TS_THREADS, 1)
 // chunk), which dominated GEMMs with a long K (e.g. the LSTM dh GEMM, K = 4H = 6000).
 template <int EPI>
 __global__ void splitk_epilogue_kernel(const float* __restrict__ ws, int splits, int tiles, int mt_grid, int M, int N,
-                                       float* __restrict__ out, const float* __restrict__ aux, int relu) {
+                                       float* __restrict__ out, const float* __restrict__ aux, int relu, int row) {
   const int64_t total = (int64_t)M * N;
   const size_t split_stride = (size_t)tiles * BNMAX * BM;
   for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < total; i += (int64_t)gridDim.x * blockDim.x) {
@@ -1133,13 +1232,14 @@ __global__ void splitk_epilogue_kernel(const float* __restrict__ ws, int splits,
       acc += a3;
     }
     for (; s < splits; ++s) acc += __ldcg(src + (size_t)s * split_stride);
+    const int64_t o = row ? (int64_t)m * N + n : i;  // row: out[m·N + n]
     if (EPI == EPI_FWD) {
-      if (aux) acc += aux[m];
+      if (aux) acc += aux[row ? n : m];
       if (relu) acc = fmaxf(acc, 0.f);
     } else if (EPI == EPI_DX) {
-      if (aux && !(aux[i] > 0.f)) acc = 0.f;
+      if (aux && !(aux[o] > 0.f)) acc = 0.f;
     }
-    out[i] = acc;
+    out[o] = acc;
   }
 }
 
@@ -1147,7 +1247,8 @@ template <int EPI>
 st_status launch_splitk_epilogue(const TcParams& p, int tiles, int mt_grid, cudaStream_t s) {
   const int64_t total = (int64_t)p.M * p.N;
   const int blocks = (int)std::min<int64_t>((total + 255) / 256, 148 * 8);
-  splitk_epilogue_kernel<EPI><<<blocks, 256, 0, s>>>(p.ws, p.splits, tiles, mt_grid, p.M, p.N, p.out, p.aux, p.relu);
+  splitk_epilogue_kernel<EPI><<<blocks, 256, 0, s>>>(p.ws, p.splits, tiles, mt_grid, p.M, p.N, p.out, p.aux, p.relu,
+                                                    p.row);
   ST_CUDA_TRY(cudaGetLastError());
   return ST_OK;
 }
@@ -1776,10 +1877,14 @@ int ext_reduce_splits() {
 }
 
 
-template <int EPI, bool A_MN, bool B_MN>
+template <int EPI, bool A_MN, bool B_MN, int CV = CV_NONE>
 st_status launch(const GemmArgs& g, int M, int N, int K, const CUtensorMap& ma, const CUtensorMap& mb, float* out,
-                 const float* aux, int relu) {
+                 const float* aux, int relu, int cvH = 0, int cvW = 0, int cvC = 0) {
   TcParams p{};
+  p.row = (CV == CV_FWD || CV == CV_DX) ? 1 : 0;
+  p.cv_H = cvH;
+  p.cv_W = cvW;
+  p.cv_C = cvC;
   p.M = M;
   p.N = N;
   p.K = K;
@@ -1803,8 +1908,8 @@ st_status launch(const GemmArgs& g, int M, int N, int K, const CUtensorMap& ma, 
   p.idesc = make_idesc(p.bn, A_MN, B_MN);
   dim3 grid(mt, nt, p.splits);
   constexpr int S = 3;
-  auto kern = (g.mode == ST_GEMM_FP32X3) ? tc_gemm_kernel<EPI, A_MN, B_MN, true, S>
-                                         : tc_gemm_kernel<EPI, A_MN, B_MN, false, S>;
+  auto kern = (g.mode == ST_GEMM_FP32X3) ? tc_gemm_kernel<EPI, A_MN, B_MN, true, S, CV>
+                                         : tc_gemm_kernel<EPI, A_MN, B_MN, false, S, CV>;
   static bool attr_set[2] = {false, false};
   const int ai = g.mode == ST_GEMM_FP32X3 ? 1 : 0;
   if (!attr_set[ai]) {
@@ -2087,6 +2192,117 @@ st_status tc_dw_impl(const GemmArgs& g, const float* X, const float* dZ, float* 
     if (n < 0) return set_error(ST_ERR_CUDA, "bias gradient launch failed");
     g_launches = 1 + n;
   }
+  return ST_OK;
+}
+
+// ---------------------------------------------------------------- implicit-GEMM conv
+namespace {
+
+// Pixel box of `rows` consecutive NHWC pixels (a tile never straddles a partial image
+// row): {w, h, b} extents, or false when the geometry cannot be tiled that way.
+bool act_box(int H, int W, int rows, cuuint32_t* box) {
+  if (W >= rows) {
+    if (W % rows) return false;
+    box[0] = rows, box[1] = 1, box[2] = 1;
+  } else {
+    if (rows % W) return false;
+    const int hb = rows / W;
+    if (hb <= H) {
+      if (H % hb) return false;
+      box[0] = W, box[1] = hb, box[2] = 1;
+    } else {
+      if (hb % H) return false;
+      box[0] = W, box[1] = H, box[2] = hb / H;
+    }
+  }
+  return box[0] <= 256 && box[1] <= 256 && box[2] <= 256;
+}
+
+// NHWC tensor [B][H][W][C] (fp32) as a 4-D map (dims C, W, H, B), box {32 channels,
+// `rows` pixels}; SWIZZLE_128B (K-major operand) or SWIZZLE_128B_ATOM_32B (MN-major):
+// the box lands in smem exactly like the 2-D box {32, rows} of a [pixels × C] matrix.
+bool make_act_map(CUtensorMap* m, const float* base, int B, int H, int W, int C, int rows, bool mn_major) {
+  EncodeFn enc = get_encode();
+  cuuint32_t pb[3];
+  if (!enc || !aligned16(base) || (C % 32) || !act_box(H, W, rows, pb)) return false;
+  cuuint64_t dims[4] = {(cuuint64_t)C, (cuuint64_t)W, (cuuint64_t)H, (cuuint64_t)B};
+  cuuint64_t strides[3] = {(cuuint64_t)C * 4, (cuuint64_t)W * C * 4, (cuuint64_t)H * W * C * 4};
+  cuuint32_t box[4] = {32, pb[0], pb[1], pb[2]};
+  cuuint32_t es[4] = {1, 1, 1, 1};
+  CUresult r = enc(m, CU_TENSOR_MAP_DATA_TYPE_FLOAT32, 4, const_cast<float*>(base), dims, strides, box, es,
+                   CU_TENSOR_MAP_INTERLEAVE_NONE,
+                   mn_major ? CU_TENSOR_MAP_SWIZZLE_128B_ATOM_32B : CU_TENSOR_MAP_SWIZZLE_128B,
+                   CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+  return r == CUDA_SUCCESS;
+}
+
+// HWIO weights viewed as [9][Cin][Cout] (dims Cout, Cin, 9), box {32 co, bn ci, 1 tap}:
+// the K-major B operand of the conv dX (K = (tap, co)).
+bool make_w3_map(CUtensorMap* m, const float* base, int Cin, int Cout, int bn) {
+  EncodeFn enc = get_encode();
+  if (!enc || !aligned16(base) || (Cout % 4)) return false;
+  cuuint64_t dims[3] = {(cuuint64_t)Cout, (cuuint64_t)Cin, 9};
+  cuuint64_t strides[2] = {(cuuint64_t)Cout * 4, (cuuint64_t)Cin * Cout * 4};
+  cuuint32_t box[3] = {32, (cuuint32_t)bn, 1};
+  cuuint32_t es[3] = {1, 1, 1};
+  CUresult r = enc(m, CU_TENSOR_MAP_DATA_TYPE_FLOAT32, 3, const_cast<float*>(base), dims, strides, box, es,
+                   CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
+                   CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+  return r == CUDA_SUCCESS;
+}
+
+bool implicit_conv_off() {
+  static int f = -1;
+  if (f < 0) {
+    const char* e = getenv("ST_CONV_IM2COL");
+    f = (e && atoi(e) == 1) ? 1 : 0;
+  }
+  return f != 0;
+}
+
+}  // namespace
+
+bool tc_conv_ok(int mode, int H, int W, int Cin, int Cout) {
+  cuuint32_t b[3];
+  return !implicit_conv_off() && (mode == ST_GEMM_FP32X3 || mode == ST_GEMM_TF32) && get_encode() &&
+         Cin % 32 == 0 && Cout % 32 == 0 && act_box(H, W, BM, b) && act_box(H, W, 32, b);
+}
+
+// Y[P × Cout] = conv3x3(X) + b, optional ReLU (NHWC; g.B = images)
+st_status tc_conv_fwd(const GemmArgs& g, const float* X, int H, int W, int Cin, int Cout, const float* Wt,
+                      const float* bias, float* Y, int relu) {
+  const int P = g.B * H * W;
+  CUtensorMap ma, mb;
+  if (!make_act_map(&ma, X, g.B, H, W, Cin, BM, false) || !make_map(&mb, Wt, Cout, 9 * Cin, Cout, 32, true))
+    return set_error(ST_ERR_CUDA, "cuTensorMapEncodeTiled failed (conv fwd)");
+  return launch<EPI_FWD, false, true, CV_FWD>(g, P, Cout, 9 * Cin, ma, mb, Y, bias, relu, H, W, Cin);
+}
+
+// D[P × Cin] = conv3x3ᵀ(dZ) ⊙ 1[mask > 0] (mask may be null)
+st_status tc_conv_dx(const GemmArgs& g, const float* dZ, int H, int W, int Cin, int Cout, const float* Wt,
+                     const float* mask, float* D) {
+  const int P = g.B * H * W;
+  CUtensorMap ma, mb;
+  if (!make_act_map(&ma, dZ, g.B, H, W, Cout, BM, false) || !make_w3_map(&mb, Wt, Cin, Cout, bn_for(Cin)))
+    return set_error(ST_ERR_CUDA, "cuTensorMapEncodeTiled failed (conv dX)");
+  return launch<EPI_DX, false, false, CV_DX>(g, P, Cin, 9 * Cout, ma, mb, D, mask, 0, H, W, Cout);
+}
+
+// G[9·Cin × Cout] = Σ_p col(X)[p]ᵀ dZ[p]; gb[Cout] = Σ_p dZ[p] (gb may be null)
+st_status tc_conv_dw(const GemmArgs& g, const float* X, const float* dZ, int H, int W, int Cin, int Cout, float* G,
+                     float* gb) {
+  const int P = g.B * H * W;
+  CUtensorMap ma, mb;
+  if (!make_map(&ma, dZ, Cout, P, Cout, 32, true) || !make_act_map(&mb, X, g.B, H, W, Cin, 32, true))
+    return set_error(ST_ERR_CUDA, "cuTensorMapEncodeTiled failed (conv dW)");
+  ST_TRY((launch<EPI_DW, true, true, CV_DW>(g, Cout, 9 * Cin, P, ma, mb, G, nullptr, 0, H, W, Cin)));
+  int launches = g_launches;
+  if (gb) {
+    const int n = launch_bias_grad(dZ, P, Cout, gb, g.work, g.work_bytes, g.stream);
+    if (n < 0) return set_error(ST_ERR_CUDA, "bias gradient launch failed");
+    launches += n;
+  }
+  g_launches = launches;
   return ST_OK;
 }
 

@@ -52,8 +52,21 @@ st_status gemm_dw(const GemmArgs& g, const float* X, const float* dZ, float* G, 
 // bias block `b` (b.W == NULL: no bias). G_scratch is used only by the fallback path.
 st_status gemm_dw_update(const GemmArgs& g, const float* X, const float* dZ, const UpdateArgs& w,
                          const UpdateArgs& b, float* G_scratch);
-// number of kernel launches the last gemm_* call issued on this thread
+// number of kernel launches the last gemm_* / tc_conv_* call issued on this thread
 int gemm_last_launches();
+
+// ---- 3×3 / pad-1 convolution as implicit tcgen05 GEMMs (a10; k_gemm_tc.cu) ----------
+// NHWC activations [g.B images][H][W][C], HWIO weights [3][3][Cin][Cout]. The shifted
+// windows are 4-D TMA boxes (zero-filled outside the image), so no im2col buffer exists.
+// tc_conv_ok: Cin, Cout multiples of 32, tileable H × W, tensor-core mode, ST_CONV_IM2COL≠1.
+bool tc_conv_ok(int mode, int H, int W, int Cin, int Cout);
+st_status tc_conv_fwd(const GemmArgs& g, const float* X, int H, int W, int Cin, int Cout, const float* Wt,
+                      const float* bias, float* Y, int relu);
+st_status tc_conv_dx(const GemmArgs& g, const float* dZ, int H, int W, int Cin, int Cout, const float* Wt,
+                     const float* mask, float* D);
+st_status tc_conv_dw(const GemmArgs& g, const float* X, const float* dZ, int H, int W, int Cin, int Cout, float* G,
+                     float* gb);
+int tc_last_launches();
 
 // ---- softmax cross-entropy, batch mean (D11) -----------------------------------
 // loss_out[0] = mean_b −log softmax(Z_b)[y_b];  dZ = (softmax − onehot)/B.

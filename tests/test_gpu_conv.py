@@ -51,3 +51,26 @@ def test_vgg_small_single_stage_rgb(st):
 def test_vgg_simt_mode(st):
     model = sd.vgg(cfg=(8, "M", 16, "M"), fc=(16,), classes=10, hw=8, in_ch=4, cuts=[2])
     _vgg_parity(st, model, 4, 6, 0.05, seed=3, gemm=st.ST_GEMM_SIMT)
+
+
+# Implicit-GEMM conv path (channel counts multiples of 32: 4-D TMA windows, no im2col).
+# Geometries: 16×16 (pixel box 8 rows × 16), 8×8 (2 images × 8 × 8), 4×4 (8 images),
+# 2×2 (32 images); batch 3 makes every P = 3·H·W tile ragged except at 16×16.
+
+def test_vgg_implicit_conv_3stage(st):
+    model = sd.vgg(cfg=(32, 32, "M", 64, "M", 64, "M", 32, "M"), fc=(32,), classes=10, hw=16, in_ch=32,
+                   cuts=[2, 5])
+    _vgg_parity(st, model, 3, 10, 0.05, seed=4)
+
+
+def test_vgg_implicit_after_rgb(st):
+    """3-channel first conv (CUDA-core im2col path) feeding implicit convs; dX of the
+    implicit conv carries the ReLU mask of its producer across a stage boundary."""
+    model = sd.vgg(cfg=(32, "M", 32, 64, "M", 64), fc=(16,), classes=10, hw=8, in_ch=3, cuts=[1, 3])
+    _vgg_parity(st, model, 5, 8, 0.05, seed=5)
+
+
+def test_vgg_implicit_batch1(st):
+    """FP32X3 (the parity mode) at batch 1 — single-image tiles, P < 128 everywhere."""
+    model = sd.vgg(cfg=(32, "M", 64, "M"), fc=(16,), classes=10, hw=8, in_ch=32, cuts=[])
+    _vgg_parity(st, model, 1, 6, 0.05, seed=6)
