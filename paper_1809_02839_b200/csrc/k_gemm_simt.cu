@@ -146,12 +146,63 @@ __global__ void __launch_bounds__(256) colsum_partial_kernel(const float* __rest
   }
 }
 
-__global__ void colsum_final_kernel(const float* __restrict__ part, int nb, int n_out, float* __restrict__ gb) {
-  const int o = blockIdx.x * blockDim.x + threadIdx.x;
-  if (o >= n_out) return;
-  float t = 0.f;
-  for (int b = 0; b < nb; ++b) t += part[(size_t)b * n_out + o];
-  gb[o] = t;
+// float4 variant (n_out % 4 == 0, 16-B aligned): 8 threads × 4 columns = 32 columns per
+// CTA, 32 row groups, each thread 4 independent accumulators (rows r ≡ j mod 4 of its
+// group) combined in fixed order, then the 32 groups in fixed order — deterministic, and
+// 16 B × 4 loads in flight per thread instead of one 4-B load.
+__global__ void __launch_bounds__(256) colsum4_partial_kernel(const float* __restrict__ dZ, int rows, int n_out,
+                                                              int rpb, float* __restrict__ part) {
+  __shared__ float4 sm[32][9];
+  const int tx = threadIdx.x & 7, ty = threadIdx.x >> 3;
+  const int o = blockIdx.x * 32 + tx * 4;
+  const int r0 = blockIdx.y * rpb, r1 = min(rows, r0 + rpb);
+  float4 a[4];
+#pragma unroll
+  for (int j = 0; j < 4; ++j) a[j] = make_float4(0.f, 0.f, 0.f, 0.f);
+  if (o < n_out) {
+    const float* base = dZ + o;
+    int r = r0 + ty;
+    for (; r + 96 < r1; r += 128) {
+      float4 v[4];
+#pragma unroll
+      for (int j = 0; j < 4; ++j) v[j] = __ldg(reinterpret_cast<const float4*>(base + (size_t)(r + 32 * j) * n_out));
+#pragma unroll
+      for (int j = 0; j < 4; ++j) {
+        a[j].x += v[j].x;
+        a[j].y += v[j].y;
+        a[j].z += v[j].z;
+        a[j].w += v[j].w;
+      }
+    }
+    for (int j = 0; r < r1; r += 32, ++j) {
+      const float4 v = __ldg(reinterpret_cast<const float4*>(base + (size_t)r * n_out));
+      a[j & 3].x += v.x;
+      a[j & 3].y += v.y;
+      a[j & 3].z += v.z;
+      a[j & 3].w += v.w;
+    }
+  }
+  float4 t = a[0];
+#pragma unroll
+  for (int j = 1; j < 4; ++j) {
+    t.x += a[j].x;
+    t.y += a[j].y;
+    t.z += a[j].z;
+    t.w += a[j].w;
+  }
+  sm[ty][tx] = t;
+  __syncthreads();
+  if (ty == 0 && o < n_out) {
+    float4 u = sm[0][tx];
+    for (int q = 1; q < 32; ++q) {
+      const float4 w = sm[q][tx];
+      u.x += w.x;
+      u.y += w.y;
+      u.z += w.z;
+      u.w += w.w;
+    }
+    *reinterpret_cast<float4*>(part + (size_t)blockIdx.y * n_out + o) = u;
+  }
 }
 
 }  // namespace
@@ -161,14 +212,20 @@ __global__ void colsum_final_kernel(const float* __restrict__ part, int nb, int 
 int launch_bias_grad(const float* dZ, int rows, int n_out, float* gb, void* work, int64_t work_bytes,
                      cudaStream_t s) {
   const int cb = (n_out + 31) / 32;
-  int nb = rows > 1024 ? std::min(1024, std::max(1, (4 * 148) / cb)) : 1;
+  int nb = rows > 1024 ? std::min(1024, std::max(1, (2 * 148) / cb)) : 1;
   nb = std::min(nb, (rows + 255) / 256);
   if (nb > 1 && work && (int64_t)nb * n_out * 4 <= work_bytes - 64 * 1024) {
     const int rpb = (rows + nb - 1) / nb;
     nb = (rows + rpb - 1) / rpb;
     float* part = reinterpret_cast<float*>(static_cast<char*>(work) + 64 * 1024);
-    colsum_partial_kernel<<<dim3(cb, nb), 256, 0, s>>>(dZ, rows, n_out, rpb, part);
-    colsum_final_kernel<<<(n_out + 127) / 128, 128, 0, s>>>(part, nb, n_out, gb);
+    // pass 2 is the same column sum over the [nb × n_out] partials as one row block
+    if ((n_out & 3) == 0 && (((uintptr_t)dZ | (uintptr_t)gb) & 15) == 0) {
+      colsum4_partial_kernel<<<dim3(cb, nb), 256, 0, s>>>(dZ, rows, n_out, rpb, part);
+      colsum4_partial_kernel<<<dim3(cb, 1), 256, 0, s>>>(part, nb, n_out, nb, gb);
+    } else {
+      colsum_partial_kernel<<<dim3(cb, nb), 256, 0, s>>>(dZ, rows, n_out, rpb, part);
+      colsum_partial_kernel<<<dim3(cb, 1), 256, 0, s>>>(part, nb, n_out, nb, gb);
+    }
     return cudaGetLastError() == cudaSuccess ? 2 : -1;
   }
   bias_grad_kernel<<<cb, 256, 0, s>>>(dZ, rows, n_out, gb);

@@ -410,6 +410,50 @@ __device__ __forceinline__ void epilogue(const TcParams& p, uint32_t tmem, int w
 // CV_FWD / CV_DX write row-major (p.row): out[p·N + n] is NHWC.
 enum { CV_NONE = 0, CV_FWD = 1, CV_DX = 2, CV_DW = 3 };
 
+// One ring stage of operand tiles: K-block k0 of the (m0, n0) tile, TMA into dA / dB,
+// completing on `full` (plain 2-D operands, or the implicit-conv windows of CV).
+template <bool A_MN, bool B_MN, int CV>
+__device__ __forceinline__ void load_stage(const TcParams& p, const CUtensorMap* mA, const CUtensorMap* mB,
+                                           uint32_t dA, uint32_t dB, uint32_t full, int m0, int n0, int k0,
+                                           int nbox_b) {
+  if (CV == CV_FWD || CV == CV_DX) {
+    // K-block (kh, kw, c0): the 128-pixel tile [b0.., h0.., w0..] shifted by the tap
+    const int HW = p.cv_H * p.cv_W;
+    const int b0 = m0 / HW, r0 = m0 - b0 * HW, h0 = r0 / p.cv_W, w0 = r0 - h0 * p.cv_W;
+    const int q = k0 / p.cv_C, c0 = k0 - q * p.cv_C, kh = q / 3, kw = q - 3 * kh;
+    const int dh = (CV == CV_FWD) ? kh - 1 : 1 - kh, dw = (CV == CV_FWD) ? kw - 1 : 1 - kw;
+    tma_load_4d(dA, mA, c0, w0 + dw, h0 + dh, b0, full);
+    if (CV == CV_FWD) {
+      for (int c = 0; c < nbox_b; ++c) tma_load_2d(dB + c * 4096, mB, n0 + 32 * c, k0, full);
+    } else {
+      tma_load_3d(dB, mB, c0, n0, q, full);
+    }
+    return;
+  }
+  if (CV == CV_DW) {
+#pragma unroll
+    for (int c = 0; c < BM / 32; ++c) tma_load_2d(dA + c * 4096, mA, m0 + 32 * c, k0, full);
+    const int HW = p.cv_H * p.cv_W;
+    const int b0 = k0 / HW, r0 = k0 - b0 * HW, h0 = r0 / p.cv_W, w0 = r0 - h0 * p.cv_W;
+    for (int c = 0; c < nbox_b; ++c) {
+      const int n = n0 + 32 * c, q = n / p.cv_C, ci0 = n - q * p.cv_C, kh = q / 3, kw = q - 3 * kh;
+      tma_load_4d(dB + c * 4096, mB, ci0, w0 + kw - 1, h0 + kh - 1, b0, full);
+    }
+    return;
+  }
+  if (A_MN) {
+#pragma unroll
+    for (int c = 0; c < BM / 32; ++c) tma_load_2d(dA + c * 4096, mA, m0 + 32 * c, k0, full);
+  } else {
+    tma_load_2d(dA, mA, k0, m0, full);
+  }
+  if (B_MN) {
+    for (int c = 0; c < nbox_b; ++c) tma_load_2d(dB + c * 4096, mB, n0 + 32 * c, k0, full);
+  } else {
+    tma_load_2d(dB, mB, k0, n0, full);
+  }
+}
+
 template <int EPI, bool A_MN, bool B_MN, bool kX3, int STAGES, int CV = CV_NONE>
 __global__ void __launch_bounds__(kThreads, 1)
     tc_gemm_kernel(const __grid_constant__ CUtensorMap mapA, const __grid_constant__ CUtensorMap mapB, TcParams p) {
@@ -469,42 +513,7 @@ __global__ void __launch_bounds__(kThreads, 1)
         const int k0 = (kb0 + i) * BK;
         const uint32_t dA = smem_u32(smem + s * STAGE_BYTES);
         const uint32_t dB = dA + TILE_BYTES;
-        if (CV == CV_FWD || CV == CV_DX) {
-          // K-block (kh, kw, c0): the 128-pixel tile [b0.., h0.., w0..] shifted by the tap
-          const int HW = p.cv_H * p.cv_W;
-          const int b0 = m0 / HW, r0 = m0 - b0 * HW, h0 = r0 / p.cv_W, w0 = r0 - h0 * p.cv_W;
-          const int q = k0 / p.cv_C, c0 = k0 - q * p.cv_C, kh = q / 3, kw = q - 3 * kh;
-          const int dh = (CV == CV_FWD) ? kh - 1 : 1 - kh, dw = (CV == CV_FWD) ? kw - 1 : 1 - kw;
-          tma_load_4d(dA, &mapA, c0, w0 + dw, h0 + dh, b0, full);
-          if (CV == CV_FWD) {
-            for (int c = 0; c < nbox_b; ++c) tma_load_2d(dB + c * 4096, &mapB, n0 + 32 * c, k0, full);
-          } else {
-            tma_load_3d(dB, &mapB, c0, n0, q, full);
-          }
-          continue;
-        }
-        if (CV == CV_DW) {
-#pragma unroll
-          for (int c = 0; c < BM / 32; ++c) tma_load_2d(dA + c * 4096, &mapA, m0 + 32 * c, k0, full);
-          const int HW = p.cv_H * p.cv_W;
-          const int b0 = k0 / HW, r0 = k0 - b0 * HW, h0 = r0 / p.cv_W, w0 = r0 - h0 * p.cv_W;
-          for (int c = 0; c < nbox_b; ++c) {
-            const int n = n0 + 32 * c, q = n / p.cv_C, ci0 = n - q * p.cv_C, kh = q / 3, kw = q - 3 * kh;
-            tma_load_4d(dB + c * 4096, &mapB, ci0, w0 + kw - 1, h0 + kh - 1, b0, full);
-          }
-          continue;
-        }
-        if (A_MN) {
-#pragma unroll
-          for (int c = 0; c < BM / 32; ++c) tma_load_2d(dA + c * 4096, &mapA, m0 + 32 * c, k0, full);
-        } else {
-          tma_load_2d(dA, &mapA, k0, m0, full);
-        }
-        if (B_MN) {
-          for (int c = 0; c < nbox_b; ++c) tma_load_2d(dB + c * 4096, &mapB, n0 + 32 * c, k0, full);
-        } else {
-          tma_load_2d(dB, &mapB, k0, n0, full);
-        }
+        load_stage<A_MN, B_MN, CV>(p, &mapA, &mapB, dA, dB, full, m0, n0, k0, nbox_b);
       }
     }
   } else if (warp == 1) {
@@ -558,6 +567,337 @@ __global__ void __launch_bounds__(kThreads, 1)
   }
 }
 
+
+// Persistent variant for the implicit-conv fwd / dX GEMMs (M = pixels: hundreds of
+// small tiles, no K split). One CTA per SM walks tiles t = blockIdx.x + j·gridDim.x
+// (m fastest: concurrent CTAs share the weight tile in L2); the operand ring runs on
+// across tiles, and two TMEM accumulators let the epilogue of tile j (warps 6..9)
+// overlap the MMAs of tile j+1. Warp 0 TMA, warp 1 MMA (warp-converged, elected
+// issuing lane), warps 2..5 lo converters (3xTF32), warps 6..9 epilogue.
+constexpr int kPThreads = 320;
+
+template <int EPI, bool A_MN, bool B_MN, bool kX3, int STAGES, int CV>
+__global__ void __launch_bounds__(kPThreads, 1)
+    tc_gemm_persistent_kernel(const __grid_constant__ CUtensorMap mapA, const __grid_constant__ CUtensorMap mapB,
+                              TcParams p, int mt, int tiles) {
+  extern __shared__ __align__(1024) uint8_t smem_raw[];
+  char* smem = align_smem_1k(smem_raw);
+  uint64_t* bars = reinterpret_cast<uint64_t*>(smem + STAGES * STAGE_BYTES);
+  const uint32_t b_full = smem_u32(bars);
+  const uint32_t b_conv = b_full + 8 * STAGES;
+  const uint32_t b_empty = b_conv + 8 * STAGES;
+  const uint32_t acc_full = b_empty + 8 * STAGES;  // [2]
+  const uint32_t acc_empty = acc_full + 16;        // [2]
+  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(bars + 3 * STAGES + 4);
+
+  const int warp = threadIdx.x >> 5;
+  const int lane = threadIdx.x & 31;
+  const int nkb = p.kb_total;
+  const int bn = p.bn;
+  const int nbox_b = (bn + 31) / 32;
+  const int b_chunks = B_MN ? nbox_b * 256 : bn * 8;
+
+  if (threadIdx.x == 0) {
+    for (int s = 0; s < STAGES; ++s) {
+      mbar_init(b_full + 8 * s, 1);
+      mbar_init(b_conv + 8 * s, 4);
+      mbar_init(b_empty + 8 * s, 1);
+    }
+    for (int a = 0; a < 2; ++a) {
+      mbar_init(acc_full + 8 * a, 1);
+      mbar_init(acc_empty + 8 * a, 4);
+    }
+    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+  }
+  if (warp == 1) {
+    asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], %1;" ::"r"(smem_u32(tmem_slot)),
+                 "r"(2 * BNMAX));
+    asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;");
+  }
+  if (warp == 0 && lane == 0) {
+    asm volatile("prefetch.tensormap [%0];" ::"l"(reinterpret_cast<uint64_t>(&mapA)) : "memory");
+    asm volatile("prefetch.tensormap [%0];" ::"l"(reinterpret_cast<uint64_t>(&mapB)) : "memory");
+  }
+  tc_fence_before();
+  __syncthreads();
+  tc_fence_after();
+  const uint32_t tmem = *tmem_slot;
+
+  if (warp == 0) {
+    // ---------------- TMA producer (ring continues across tiles)
+    const uint32_t bytes = (uint32_t)(TILE_BYTES + (B_MN ? nbox_b * 4096 : bn * BK * 4));
+    int it = 0;
+    for (int t = blockIdx.x; t < tiles; t += gridDim.x) {
+      const int m0 = (t % mt) * BM, n0 = (t / mt) * BNMAX;
+      for (int kb = 0; kb < nkb; ++kb, ++it) {
+        const int s = it % STAGES;
+        mbar_wait(b_empty + 8 * s, ((it / STAGES) & 1) ^ 1);
+        const uint32_t full = b_full + 8 * s;
+        const uint32_t dA = smem_u32(smem + s * STAGE_BYTES);
+        if (elect_one()) {
+          mbar_expect_tx(full, bytes);
+          load_stage<A_MN, B_MN, CV>(p, &mapA, &mapB, dA, dA + TILE_BYTES, full, m0, n0, kb * BK, nbox_b);
+        }
+        __syncwarp();
+      }
+    }
+  } else if (warp == 1) {
+    // ---------------- MMA issuer
+    int it = 0, j = 0;
+    for (int t = blockIdx.x; t < tiles; t += gridDim.x, ++j) {
+      const int buf = j & 1;
+      const uint32_t d = tmem + (uint32_t)(buf * BNMAX);
+      mbar_wait(acc_empty + 8 * buf, ((j >> 1) & 1) ^ 1);
+      tc_fence_after();
+      for (int kb = 0; kb < nkb; ++kb, ++it) {
+        const int s = it % STAGES;
+        mbar_wait((kX3 ? b_conv : b_full) + 8 * s, (it / STAGES) & 1);
+        tc_fence_after();
+        const uint32_t a_hi = smem_u32(smem + s * STAGE_BYTES), b_hi = a_hi + TILE_BYTES;
+        const uint32_t a_lo = a_hi + 2 * TILE_BYTES, b_lo = a_hi + 3 * TILE_BYTES;
+        if (elect_one()) {
+#pragma unroll
+          for (int kk = 0; kk < BK / 8; ++kk) {
+            const uint32_t acc = (kb > 0 || kk > 0) ? 1u : 0u;
+            tc_mma(d, op_desc<A_MN>(a_hi, kk), op_desc<B_MN>(b_hi, kk), p.idesc, acc);
+            if (kX3) {
+              tc_mma(d, op_desc<A_MN>(a_lo, kk), op_desc<B_MN>(b_hi, kk), p.idesc, 1u);
+              tc_mma(d, op_desc<A_MN>(a_hi, kk), op_desc<B_MN>(b_lo, kk), p.idesc, 1u);
+            }
+          }
+          tc_commit(b_empty + 8 * s);
+          if (kb == nkb - 1) tc_commit(acc_full + 8 * buf);
+        }
+        __syncwarp();
+      }
+    }
+  } else if (warp < 6) {
+    // ---------------- converters (warps 2..5): lo tiles for the 3xTF32 split
+    if (kX3) {
+      const int ctid = threadIdx.x - 64;
+      int it = 0;
+      for (int t = blockIdx.x; t < tiles; t += gridDim.x) {
+        for (int kb = 0; kb < nkb; ++kb, ++it) {
+          const int s = it % STAGES;
+          mbar_wait(b_full + 8 * s, (it / STAGES) & 1);
+          char* st = smem + s * STAGE_BYTES;
+          make_lo(st, st + 2 * TILE_BYTES, TILE_BYTES / 16, ctid);
+          make_lo(st + TILE_BYTES, st + 3 * TILE_BYTES, b_chunks, ctid);
+          fence_proxy_async();
+          __syncwarp();
+          if (lane == 0) mbar_arrive(b_conv + 8 * s);
+        }
+      }
+    }
+  } else {
+    // ---------------- epilogue (warps 6..9 → TMEM quadrants 2, 3, 0, 1)
+    const int quad = warp & 3;
+    int j = 0;
+    for (int t = blockIdx.x; t < tiles; t += gridDim.x, ++j) {
+      const int buf = j & 1;
+      const int m0 = (t % mt) * BM, n0 = (t / mt) * BNMAX;
+      mbar_wait(acc_full + 8 * buf, (j >> 1) & 1);
+      tc_fence_after();
+      const int m = m0 + quad * 32 + lane;
+      const uint32_t trow = tmem + (uint32_t)(buf * BNMAX) + ((uint32_t)(quad * 32) << 16);
+      const float bias = (EPI == EPI_FWD && p.aux && m < p.M && !p.row) ? p.aux[m] : 0.f;
+      for (int c = 0; c < bn; c += 16) {
+        float v[16];
+        tc_ld16(trow + c, v);
+        if (m < p.M) epilogue_store16<EPI>(p, m, n0 + c, v, bias);
+      }
+      tc_fence_before();
+      __syncwarp();
+      if (lane == 0) mbar_arrive(acc_empty + 8 * buf);
+    }
+  }
+
+  tc_fence_before();
+  __syncthreads();
+  if (warp == 1) {
+    tc_fence_after();
+    asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(tmem), "r"(2 * BNMAX));
+  }
+}
+
+__device__ __forceinline__ void tc_mma_ts(uint32_t tmem_d, uint32_t tmem_a, uint64_t bdesc, uint32_t idesc,
+                                          uint32_t accum);
+__device__ __forceinline__ void tc_st32(uint32_t taddr, const uint32_t* v);
+
+// FP32X3 implicit-conv fwd / dX with the activation window in TMEM (A-from-TMEM MMAs).
+// With A and B both read from smem by three MMAs per K step (plus the converter's
+// passes), the persistent kernel above is bound by shared-memory bandwidth (~144 KB of
+// smem traffic per 128 × 64 × 32 K-block vs ~576 MMA cycles). Here the converter warps
+// read each raw window tile once and write hi / lo into a TMEM slot (tcgen05.st), and
+// compute the weight lo tile in smem; the MMAs then read only the weight tiles from smem.
+// Ring: CS stages × (A raw 16 KB + B raw 16 KB + B lo 16 KB), TMEM slot s ↔ stage s
+// (64 columns: 32 hi + 32 lo), 2 accumulators × 128 columns: 256 + CS·64 ≤ 512.
+constexpr int CS = 4;
+constexpr int CS_STAGE = 3 * TILE_BYTES;
+constexpr int cs_smem_bytes() { return CS * CS_STAGE + 1024 + 256; }
+
+template <int EPI, bool B_MN, int CV>
+__global__ void __launch_bounds__(kPThreads, 1)
+    tc_conv_ts_kernel(const __grid_constant__ CUtensorMap mapA, const __grid_constant__ CUtensorMap mapB,
+                      TcParams p, int mt, int tiles) {
+  extern __shared__ __align__(1024) uint8_t smem_raw[];
+  char* smem = align_smem_1k(smem_raw);
+  uint64_t* bars = reinterpret_cast<uint64_t*>(smem + CS * CS_STAGE);
+  const uint32_t b_full = smem_u32(bars);          // TMA landed (A + B)           [CS]
+  const uint32_t b_ready = b_full + 8 * CS;        // TMEM hi/lo + B lo written    [CS] (4 warps)
+  const uint32_t b_empty = b_ready + 8 * CS;       // MMAs done with stage + slot  [CS]
+  const uint32_t acc_full = b_empty + 8 * CS;      // [2]
+  const uint32_t acc_empty = acc_full + 16;        // [2] (4 epilogue warps)
+  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(bars + 3 * CS + 4);
+
+  const int warp = threadIdx.x >> 5;
+  const int lane = threadIdx.x & 31;
+  const int nkb = p.kb_total;
+  const int bn = p.bn;
+  const int nbox_b = (bn + 31) / 32;
+  const int b_chunks = B_MN ? nbox_b * 256 : bn * 8;
+
+  if (threadIdx.x == 0) {
+    for (int s = 0; s < CS; ++s) {
+      mbar_init(b_full + 8 * s, 1);
+      mbar_init(b_ready + 8 * s, 4);
+      mbar_init(b_empty + 8 * s, 1);
+    }
+    for (int a = 0; a < 2; ++a) {
+      mbar_init(acc_full + 8 * a, 1);
+      mbar_init(acc_empty + 8 * a, 4);
+    }
+    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+  }
+  if (warp == 1) {
+    asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], %1;" ::"r"(smem_u32(tmem_slot)),
+                 "r"(512));
+    asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;");
+  }
+  if (warp == 0 && lane == 0) {
+    asm volatile("prefetch.tensormap [%0];" ::"l"(reinterpret_cast<uint64_t>(&mapA)) : "memory");
+    asm volatile("prefetch.tensormap [%0];" ::"l"(reinterpret_cast<uint64_t>(&mapB)) : "memory");
+  }
+  tc_fence_before();
+  __syncthreads();
+  tc_fence_after();
+  const uint32_t tmem = *tmem_slot;
+  const uint32_t tmemA = tmem + 2 * BNMAX;  // CS slots of 64 columns
+
+  if (warp == 0) {
+    // ---------------- TMA producer
+    const uint32_t bytes = (uint32_t)(TILE_BYTES + (B_MN ? nbox_b * 4096 : bn * BK * 4));
+    int it = 0;
+    for (int t = blockIdx.x; t < tiles; t += gridDim.x) {
+      const int m0 = (t % mt) * BM, n0 = (t / mt) * BNMAX;
+      for (int kb = 0; kb < nkb; ++kb, ++it) {
+        const int s = it % CS;
+        mbar_wait(b_empty + 8 * s, ((it / CS) & 1) ^ 1);
+        const uint32_t full = b_full + 8 * s;
+        const uint32_t dA = smem_u32(smem + s * CS_STAGE);
+        if (elect_one()) {
+          mbar_expect_tx(full, bytes);
+          load_stage<false, B_MN, CV>(p, &mapA, &mapB, dA, dA + TILE_BYTES, full, m0, n0, kb * BK, nbox_b);
+        }
+        __syncwarp();
+      }
+    }
+  } else if (warp == 1) {
+    // ---------------- MMA issuer (A hi / lo from TMEM slot s, B hi / lo from smem)
+    int it = 0, j = 0;
+    for (int t = blockIdx.x; t < tiles; t += gridDim.x, ++j) {
+      const int buf = j & 1;
+      const uint32_t d = tmem + (uint32_t)(buf * BNMAX);
+      mbar_wait(acc_empty + 8 * buf, ((j >> 1) & 1) ^ 1);
+      tc_fence_after();
+      for (int kb = 0; kb < nkb; ++kb, ++it) {
+        const int s = it % CS;
+        mbar_wait(b_ready + 8 * s, (it / CS) & 1);
+        tc_fence_after();
+        const uint32_t b_hi = smem_u32(smem + s * CS_STAGE) + TILE_BYTES, b_lo = b_hi + TILE_BYTES;
+        const uint32_t a_hi = tmemA + s * 64, a_lo = a_hi + 32;
+        if (elect_one()) {
+#pragma unroll
+          for (int kk = 0; kk < BK / 8; ++kk) {
+            const uint32_t acc = (kb > 0 || kk > 0) ? 1u : 0u;
+            tc_mma_ts(d, a_hi + kk * 8, op_desc<B_MN>(b_hi, kk), p.idesc, acc);
+            tc_mma_ts(d, a_lo + kk * 8, op_desc<B_MN>(b_hi, kk), p.idesc, 1u);
+            tc_mma_ts(d, a_hi + kk * 8, op_desc<B_MN>(b_lo, kk), p.idesc, 1u);
+          }
+          tc_commit(b_empty + 8 * s);
+          if (kb == nkb - 1) tc_commit(acc_full + 8 * buf);
+        }
+        __syncwarp();
+      }
+    }
+  } else if (warp < 6) {
+    // ---------------- converters (warps 2..5): window row r → TMEM lane r (hi, lo);
+    // weight tile lo in smem
+    const int quad = warp & 3;
+    const int r = quad * 32 + lane;
+    const int ctid = threadIdx.x - 64;
+    int it = 0;
+    for (int t = blockIdx.x; t < tiles; t += gridDim.x) {
+      for (int kb = 0; kb < nkb; ++kb, ++it) {
+        const int s = it % CS;
+        mbar_wait(b_full + 8 * s, (it / CS) & 1);
+        char* st = smem + s * CS_STAGE;
+        uint32_t hi[32], lo[32];
+#pragma unroll
+        for (int c = 0; c < 8; ++c) {
+          const float4 v = *reinterpret_cast<const float4*>(st + r * 128 + ((c ^ (r & 7)) << 4));
+          hi[4 * c + 0] = __float_as_uint(v.x);
+          hi[4 * c + 1] = __float_as_uint(v.y);
+          hi[4 * c + 2] = __float_as_uint(v.z);
+          hi[4 * c + 3] = __float_as_uint(v.w);
+          lo[4 * c + 0] = __float_as_uint(lo_part(v.x));
+          lo[4 * c + 1] = __float_as_uint(lo_part(v.y));
+          lo[4 * c + 2] = __float_as_uint(lo_part(v.z));
+          lo[4 * c + 3] = __float_as_uint(lo_part(v.w));
+        }
+        make_lo(st + TILE_BYTES, st + 2 * TILE_BYTES, b_chunks, ctid);
+        fence_proxy_async();
+        // the slot's previous MMAs are done: the producer refilled this stage only after
+        // b_empty[s], which commits after every MMA that read TMEM slot s
+        tc_fence_after();
+        const uint32_t taddr = tmemA + s * 64 + ((uint32_t)(quad * 32) << 16);
+        tc_st32(taddr, hi);
+        tc_st32(taddr + 32, lo);
+        asm volatile("tcgen05.wait::st.sync.aligned;" ::: "memory");
+        tc_fence_before();
+        __syncwarp();
+        if (lane == 0) mbar_arrive(b_ready + 8 * s);
+      }
+    }
+  } else {
+    // ---------------- epilogue (warps 6..9 → TMEM quadrants 2, 3, 0, 1), row-major
+    const int quad = warp & 3;
+    int j = 0;
+    for (int t = blockIdx.x; t < tiles; t += gridDim.x, ++j) {
+      const int buf = j & 1;
+      const int m0 = (t % mt) * BM, n0 = (t / mt) * BNMAX;
+      mbar_wait(acc_full + 8 * buf, (j >> 1) & 1);
+      tc_fence_after();
+      const int m = m0 + quad * 32 + lane;
+      const uint32_t trow = tmem + (uint32_t)(buf * BNMAX) + ((uint32_t)(quad * 32) << 16);
+      for (int c = 0; c < bn; c += 16) {
+        float v[16];
+        tc_ld16(trow + c, v);
+        if (m < p.M) epilogue_store16<EPI>(p, m, n0 + c, v, 0.f);
+      }
+      tc_fence_before();
+      __syncwarp();
+      if (lane == 0) mbar_arrive(acc_empty + 8 * buf);
+    }
+  }
+
+  tc_fence_before();
+  __syncthreads();
+  if (warp == 1) {
+    tc_fence_after();
+    asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(tmem), "r"(512));
+  }
+}
 
 // ---------------------------------------------------------------- stream-K
 // First chunk of CTA b's range (b = G gives U).
@@ -1877,6 +2217,26 @@ int ext_reduce_splits() {
 }
 
 
+// ST_CONV_TS=0: FP32X3 implicit-conv fwd / dX without the TMEM-A kernel (A/B timing)
+bool conv_ts_on() {
+  static int f = -1;
+  if (f < 0) {
+    const char* e = getenv("ST_CONV_TS");
+    f = (e && atoi(e) == 0) ? 0 : 1;
+  }
+  return f != 0;
+}
+
+// ST_CONV_PERSISTENT=0: implicit-conv fwd / dX on the one-tile-per-CTA kernel (A/B timing)
+bool conv_persistent_off() {
+  static int f = -1;
+  if (f < 0) {
+    const char* e = getenv("ST_CONV_PERSISTENT");
+    f = (e && atoi(e) == 0) ? 1 : 0;
+  }
+  return f != 0;
+}
+
 template <int EPI, bool A_MN, bool B_MN, int CV = CV_NONE>
 st_status launch(const GemmArgs& g, int M, int N, int K, const CUtensorMap& ma, const CUtensorMap& mb, float* out,
                  const float* aux, int relu, int cvH = 0, int cvW = 0, int cvC = 0) {
@@ -1917,6 +2277,34 @@ st_status launch(const GemmArgs& g, int M, int N, int K, const CUtensorMap& ma, 
     attr_set[ai] = true;
   }
   p.ext_reduce = p.splits >= ext_reduce_splits();
+  if ((CV == CV_FWD || CV == CV_DX) && p.splits == 1 && g.mode == ST_GEMM_FP32X3 && conv_ts_on()) {
+    auto ck = tc_conv_ts_kernel<EPI, B_MN, CV>;
+    static bool cattr_set = false;
+    if (!cattr_set) {
+      ST_CUDA_TRY(cudaFuncSetAttribute(ck, cudaFuncAttributeMaxDynamicSharedMemorySize, cs_smem_bytes()));
+      cattr_set = true;
+    }
+    p.idesc = make_idesc(p.bn, false, B_MN);
+    const int budget = g.max_ctas > 0 ? std::min(g.max_ctas, num_sms()) : num_sms();
+    ck<<<std::min(tiles, budget), kPThreads, cs_smem_bytes(), g.stream>>>(ma, mb, p, mt, tiles);
+    ST_CUDA_TRY(cudaGetLastError());
+    g_launches = 1;
+    return ST_OK;
+  }
+  if ((CV == CV_FWD || CV == CV_DX) && p.splits == 1 && !conv_persistent_off()) {
+    auto pk = (g.mode == ST_GEMM_FP32X3) ? tc_gemm_persistent_kernel<EPI, A_MN, B_MN, true, S, CV>
+                                         : tc_gemm_persistent_kernel<EPI, A_MN, B_MN, false, S, CV>;
+    static bool pattr_set[2] = {false, false};
+    if (!pattr_set[ai]) {
+      ST_CUDA_TRY(cudaFuncSetAttribute(pk, cudaFuncAttributeMaxDynamicSharedMemorySize, smem_bytes(S)));
+      pattr_set[ai] = true;
+    }
+    const int budget = g.max_ctas > 0 ? std::min(g.max_ctas, num_sms()) : num_sms();
+    pk<<<std::min(tiles, budget), kPThreads, smem_bytes(S), g.stream>>>(ma, mb, p, mt, tiles);
+    ST_CUDA_TRY(cudaGetLastError());
+    g_launches = 1;
+    return ST_OK;
+  }
   kern<<<grid, kThreads, smem_bytes(S), g.stream>>>(ma, mb, p);
   ST_CUDA_TRY(cudaGetLastError());
   g_launches = 1;
