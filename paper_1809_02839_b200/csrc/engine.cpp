@@ -133,7 +133,7 @@ st_status validate_and_layout(const st_config* c, Layout* L) {
         off += y.n_out;
       }
       const int64_t P = B * y.hw * y.hw;
-      max_col = std::max(max_col, P * 9 * y.n_in);
+      max_col = std::max(max_col, P * std::max<int64_t>(9 * y.n_in, 32));  // ≥ 32: padded first-conv im2col
       gemm_rows = std::max(gemm_rows, P);
     } else if (y.kind == ST_LAYER_EMBED) {
       off += (int64_t)y.n_in * y.n_out;
@@ -629,6 +629,16 @@ static st_status forward_compute(st_ctx* c, int64_t mb, const float* x_dev, cons
       ST_TRY(tc_conv_fwd(gargs_rows(c, c->B, 9 * L.n_in, L.n_out), in, L.hw, L.hw, L.n_in, L.n_out, Wh + L.w_off,
                          L.bias ? Wh + L.b_off : nullptr, out, L.act == ST_ACT_RELU));
       c->launches += tc_last_launches();
+    } else if (L.kind == ST_LAYER_CONV && tc_conv_small_ok(c->gemm, L.n_in, L.n_out)) {
+      {
+        Timed t(c, KC_LOSS);
+        ST_TRY(launch_im2col_pad32(in, c->B, L.hw, L.hw, L.n_in, c->conv_col, c->stream));
+        c->launches += 1;
+      }
+      Timed t(c, KC_GEMM_FWD);
+      ST_TRY(tc_conv_small_fwd(gargs_rows(c, c->B, 9 * L.n_in, L.n_out), c->conv_col, L.hw, L.hw, L.n_in, L.n_out,
+                               Wh + L.w_off, L.bias ? Wh + L.b_off : nullptr, out, L.act == ST_ACT_RELU));
+      c->launches += tc_last_launches();
     } else if (L.kind == ST_LAYER_CONV) {
       const int P = c->B * L.hw * L.hw;
       {
@@ -793,6 +803,30 @@ static st_status backward_compute(st_ctx* c, int64_t mb, bool fused = false) {
                         c->G + L.w_off, L.bias ? c->G + L.b_off : nullptr));
       c->launches += tc_last_launches();
       if (fused) {  // K-B over the layer's weight + bias block (contiguous, S:106 layout)
+        const UpdateArgs u = block_update(c, L.w_off, kc);
+        ST_TRY(launch_update_predict(u.W, u.V, c->G + L.w_off, u.WF, u.WB, (size_t)L.n_params, kc, c->stream));
+        c->launches += 1;
+      }
+    } else if (L.kind == ST_LAYER_CONV && tc_conv_small_ok(c->gemm, L.n_in, L.n_out)) {
+      const int P = c->B * L.hw * L.hw;
+      if (D) {  // dcol = dZ·Wᵀ [P × 9·Cin], dX = col2im(dcol) ⊙ mask (9·Cin < 32: CUDA-core GEMM)
+        Timed t(c, KC_GEMM_DX);
+        ST_TRY(gemm_dx(gargs_rows(c, P, 9 * L.n_in, L.n_out), dZ, Wh + L.w_off, nullptr, c->conv_dcol));
+        c->launches += gemm_last_launches();
+        ST_TRY(launch_col2im(c->conv_dcol, c->B, L.hw, L.hw, L.n_in, producer_act == ST_ACT_RELU ? Ain : nullptr, D,
+                             c->stream));
+        c->launches += 1;
+      }
+      {
+        Timed t(c, KC_LOSS);
+        ST_TRY(launch_im2col_pad32(Ain, c->B, L.hw, L.hw, L.n_in, c->conv_col, c->stream));
+        c->launches += 1;
+      }
+      Timed t(c, KC_GEMM_DW);
+      ST_TRY(tc_conv_small_dw(gargs_rows(c, c->B, 9 * L.n_in, L.n_out), c->conv_col, dZ, L.hw, L.hw, L.n_in,
+                              L.n_out, c->G + L.w_off, L.bias ? c->G + L.b_off : nullptr));
+      c->launches += tc_last_launches();
+      if (fused) {
         const UpdateArgs u = block_update(c, L.w_off, kc);
         ST_TRY(launch_update_predict(u.W, u.V, c->G + L.w_off, u.WF, u.WB, (size_t)L.n_params, kc, c->stream));
         c->launches += 1;

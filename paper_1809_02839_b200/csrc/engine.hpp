@@ -70,6 +70,8 @@ st_status launch_embed_grad(const float* dA, const int32_t* tok, int rows, int V
                             cudaStream_t s);
 // conv / pool kernels (k_conv.cu)
 st_status launch_im2col(const float* X, int B, int H, int W, int C, float* col, cudaStream_t s);
+// rows padded to 32 columns (9·C ≤ 32), zeros after the window: the first conv's TMA path
+st_status launch_im2col_pad32(const float* X, int B, int H, int W, int C, float* col, cudaStream_t s);
 st_status launch_col2im(const float* dcol, int B, int H, int W, int C, const float* mask, float* dX, cudaStream_t s);
 st_status launch_maxpool_fwd(const float* X, int B, int H, int W, int C, float* Y, cudaStream_t s);
 st_status launch_maxpool_bwd(const float* X, const float* dY, int B, int H, int W, int C, int relu_mask, float* dX,

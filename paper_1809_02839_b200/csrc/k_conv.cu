@@ -86,6 +86,31 @@ __global__ void col2im_kernel(const float* __restrict__ dcol, int B, int H, int 
   }
 }
 
+// col[p][0..31]: the 9·C (≤ 32) window values of pixel p in (kh, kw, c) order, zeros
+// after them; one thread per pixel, eight float4 stores (C a template: static indices).
+template <int C>
+__global__ void im2col_pad32_kernel(const float* __restrict__ X, int B, int H, int W, float* __restrict__ col) {
+  const int total = B * H * W;
+  for (int p = blockIdx.x * blockDim.x + threadIdx.x; p < total; p += gridDim.x * blockDim.x) {
+    const int w = p % W, h = (p / W) % H, b = p / (W * H);
+    float v[32];
+#pragma unroll
+    for (int k = 0; k < 32; ++k) v[k] = 0.f;
+#pragma unroll
+    for (int q = 0; q < 9; ++q) {
+      const int hh = h + q / 3 - 1, ww = w + q % 3 - 1;
+      if (hh >= 0 && hh < H && ww >= 0 && ww < W) {
+        const float* x = X + (((int64_t)b * H + hh) * W + ww) * C;
+#pragma unroll
+        for (int c = 0; c < C; ++c) v[q * C + c] = __ldg(x + c);
+      }
+    }
+    float4* dst = reinterpret_cast<float4*>(col + (int64_t)p * 32);
+#pragma unroll
+    for (int k = 0; k < 8; ++k) dst[k] = make_float4(v[4 * k], v[4 * k + 1], v[4 * k + 2], v[4 * k + 3]);
+  }
+}
+
 template <typename IDX>
 __global__ void maxpool_fwd_kernel(const float* __restrict__ X, int B, int H, int W, int C, float* __restrict__ Y) {
   const int Ho = H / 2, Wo = W / 2;
@@ -157,6 +182,18 @@ st_status launch_im2col(const float* X, int B, int H, int W, int C, float* col, 
   } else {
     if (nv < kI32) im2col_kernel<int, 1><<<blocks_for(nv), 256, 0, s>>>(X, B, H, W, C, col);
     else im2col_kernel<int64_t, 1><<<blocks_for(nv), 256, 0, s>>>(X, B, H, W, C, col);
+  }
+  ST_CUDA_TRY(cudaGetLastError());
+  return ST_OK;
+}
+
+st_status launch_im2col_pad32(const float* X, int B, int H, int W, int C, float* col, cudaStream_t s) {
+  if (9 * C > 32) return set_error(ST_ERR_INPUT, "im2col_pad32: 9·C = %d > 32", 9 * C);
+  const int64_t n = (int64_t)B * H * W;
+  switch (C) {
+    case 1: im2col_pad32_kernel<1><<<blocks_for(n), 256, 0, s>>>(X, B, H, W, col); break;
+    case 2: im2col_pad32_kernel<2><<<blocks_for(n), 256, 0, s>>>(X, B, H, W, col); break;
+    default: im2col_pad32_kernel<3><<<blocks_for(n), 256, 0, s>>>(X, B, H, W, col); break;
   }
   ST_CUDA_TRY(cudaGetLastError());
   return ST_OK;

@@ -408,7 +408,12 @@ __device__ __forceinline__ void epilogue(const TcParams& p, uint32_t tmem, int w
 //   CV_DW : M = Cout, N = 9·Cin, K = P.  A = dZ [P × Cout] MN-major (2-D, as EPI_DW);
 //           B = X shifted by (kh−1, kw−1) [32 pixels × 32 ci boxes, MN-major].
 // CV_FWD / CV_DX write row-major (p.row): out[p·N + n] is NHWC.
-enum { CV_NONE = 0, CV_FWD = 1, CV_DX = 2, CV_DW = 3 };
+//   CV_ROWS: plain 2-D operands (A K-major [M × K], B as B_MN says), row-major output —
+//           the padded-im2col first conv (Cin = 3: 27 taps·channels padded to 32).
+//   CV_DWT: dW with M = 9·Cin, N = Cout, K = P (for Cout < 128: no half-empty M tile).
+//           A = X window boxes (MN-major, 32 ci × 32 pixels), B = dZ [P × Cout]
+//           MN-major; row-major output = G[(tap, ci)·Cout + co].
+enum { CV_NONE = 0, CV_FWD = 1, CV_DX = 2, CV_DW = 3, CV_ROWS = 4, CV_DWT = 5 };
 
 // One ring stage of operand tiles: K-block k0 of the (m0, n0) tile, TMA into dA / dB,
 // completing on `full` (plain 2-D operands, or the implicit-conv windows of CV).
@@ -428,6 +433,17 @@ __device__ __forceinline__ void load_stage(const TcParams& p, const CUtensorMap*
     } else {
       tma_load_3d(dB, mB, c0, n0, q, full);
     }
+    return;
+  }
+  if (CV == CV_DWT) {
+    const int HW = p.cv_H * p.cv_W;
+    const int b0 = k0 / HW, r0 = k0 - b0 * HW, h0 = r0 / p.cv_W, w0 = r0 - h0 * p.cv_W;
+#pragma unroll
+    for (int c = 0; c < BM / 32; ++c) {
+      const int m = m0 + 32 * c, q = m / p.cv_C, ci0 = m - q * p.cv_C, kh = q / 3, kw = q - 3 * kh;
+      tma_load_4d(dA + c * 4096, mA, ci0, w0 + kw - 1, h0 + kh - 1, b0, full);
+    }
+    for (int c = 0; c < nbox_b; ++c) tma_load_2d(dB + c * 4096, mB, n0 + 32 * c, k0, full);
     return;
   }
   if (CV == CV_DW) {
@@ -2241,7 +2257,7 @@ template <int EPI, bool A_MN, bool B_MN, int CV = CV_NONE>
 st_status launch(const GemmArgs& g, int M, int N, int K, const CUtensorMap& ma, const CUtensorMap& mb, float* out,
                  const float* aux, int relu, int cvH = 0, int cvW = 0, int cvC = 0) {
   TcParams p{};
-  p.row = (CV == CV_FWD || CV == CV_DX) ? 1 : 0;
+  p.row = (CV == CV_FWD || CV == CV_DX || CV == CV_ROWS || CV == CV_DWT) ? 1 : 0;
   p.cv_H = cvH;
   p.cv_W = cvW;
   p.cv_C = cvC;
@@ -2277,7 +2293,7 @@ st_status launch(const GemmArgs& g, int M, int N, int K, const CUtensorMap& ma, 
     attr_set[ai] = true;
   }
   p.ext_reduce = p.splits >= ext_reduce_splits();
-  if ((CV == CV_FWD || CV == CV_DX) && p.splits == 1 && g.mode == ST_GEMM_FP32X3 && conv_ts_on()) {
+  if ((CV == CV_FWD || CV == CV_DX || CV == CV_ROWS) && p.splits == 1 && g.mode == ST_GEMM_FP32X3 && conv_ts_on()) {
     auto ck = tc_conv_ts_kernel<EPI, B_MN, CV>;
     static bool cattr_set = false;
     if (!cattr_set) {
@@ -2291,7 +2307,7 @@ st_status launch(const GemmArgs& g, int M, int N, int K, const CUtensorMap& ma, 
     g_launches = 1;
     return ST_OK;
   }
-  if ((CV == CV_FWD || CV == CV_DX) && p.splits == 1 && !conv_persistent_off()) {
+  if ((CV == CV_FWD || CV == CV_DX || CV == CV_ROWS) && p.splits == 1 && !conv_persistent_off()) {
     auto pk = (g.mode == ST_GEMM_FP32X3) ? tc_gemm_persistent_kernel<EPI, A_MN, B_MN, true, S, CV>
                                          : tc_gemm_persistent_kernel<EPI, A_MN, B_MN, false, S, CV>;
     static bool pattr_set[2] = {false, false};
@@ -2676,14 +2692,55 @@ st_status tc_conv_dx(const GemmArgs& g, const float* dZ, int H, int W, int Cin, 
   return launch<EPI_DX, false, false, CV_DX>(g, P, Cin, 9 * Cout, ma, mb, D, mask, 0, H, W, Cout);
 }
 
-// G[9·Cin × Cout] = Σ_p col(X)[p]ᵀ dZ[p]; gb[Cout] = Σ_p dZ[p] (gb may be null)
+// G[9·Cin × Cout] = Σ_p col(X)[p]ᵀ dZ[p]; gb[Cout] = Σ_p dZ[p] (gb may be null).
+// Cout ≥ 128: M = Cout (full 128-row tiles), N = 9·Cin; else M = 9·Cin, N = Cout.
 st_status tc_conv_dw(const GemmArgs& g, const float* X, const float* dZ, int H, int W, int Cin, int Cout, float* G,
                      float* gb) {
   const int P = g.B * H * W;
   CUtensorMap ma, mb;
-  if (!make_map(&ma, dZ, Cout, P, Cout, 32, true) || !make_act_map(&mb, X, g.B, H, W, Cin, 32, true))
-    return set_error(ST_ERR_CUDA, "cuTensorMapEncodeTiled failed (conv dW)");
-  ST_TRY((launch<EPI_DW, true, true, CV_DW>(g, Cout, 9 * Cin, P, ma, mb, G, nullptr, 0, H, W, Cin)));
+  if (Cout < BM) {
+    if (!make_act_map(&ma, X, g.B, H, W, Cin, 32, true) || !make_map(&mb, dZ, Cout, P, Cout, 32, true))
+      return set_error(ST_ERR_CUDA, "cuTensorMapEncodeTiled failed (conv dW)");
+    ST_TRY((launch<EPI_DW, true, true, CV_DWT>(g, 9 * Cin, Cout, P, ma, mb, G, nullptr, 0, H, W, Cin)));
+  } else {
+    if (!make_map(&ma, dZ, Cout, P, Cout, 32, true) || !make_act_map(&mb, X, g.B, H, W, Cin, 32, true))
+      return set_error(ST_ERR_CUDA, "cuTensorMapEncodeTiled failed (conv dW)");
+    ST_TRY((launch<EPI_DW, true, true, CV_DW>(g, Cout, 9 * Cin, P, ma, mb, G, nullptr, 0, H, W, Cin)));
+  }
+  int launches = g_launches;
+  if (gb) {
+    const int n = launch_bias_grad(dZ, P, Cout, gb, g.work, g.work_bytes, g.stream);
+    if (n < 0) return set_error(ST_ERR_CUDA, "bias gradient launch failed");
+    launches += n;
+  }
+  g_launches = launches;
+  return ST_OK;
+}
+
+// First conv (Cin·9 < 32, e.g. RGB): explicit im2col into rows padded to 32 columns
+// (col[p][k], k ≥ 9·Cin zero) so both GEMMs take the TMA / tcgen05 path; the weight
+// rows past 9·Cin are outside the [9·Cin × Cout] map, so TMA zero-fills them.
+bool tc_conv_small_ok(int mode, int Cin, int Cout) {
+  return !implicit_conv_off() && (mode == ST_GEMM_FP32X3 || mode == ST_GEMM_TF32) && get_encode() && 9 * Cin <= 32 &&
+         Cout % 4 == 0;
+}
+
+st_status tc_conv_small_fwd(const GemmArgs& g, const float* col, int H, int W, int Cin, int Cout, const float* Wt,
+                            const float* bias, float* Y, int relu) {
+  const int P = g.B * H * W;
+  CUtensorMap ma, mb;
+  if (!make_map(&ma, col, 32, P, 32, BM, false) || !make_map(&mb, Wt, Cout, 9 * Cin, Cout, 32, true))
+    return set_error(ST_ERR_CUDA, "cuTensorMapEncodeTiled failed (first conv fwd)");
+  return launch<EPI_FWD, false, true, CV_ROWS>(g, P, Cout, 32, ma, mb, Y, bias, relu);
+}
+
+st_status tc_conv_small_dw(const GemmArgs& g, const float* col, const float* dZ, int H, int W, int Cin, int Cout,
+                           float* G, float* gb) {
+  const int P = g.B * H * W;
+  CUtensorMap ma, mb;
+  if (!make_map(&ma, dZ, Cout, P, Cout, 32, true) || !make_map(&mb, col, 9 * Cin, P, 32, 32, true))
+    return set_error(ST_ERR_CUDA, "cuTensorMapEncodeTiled failed (first conv dW)");
+  ST_TRY((launch<EPI_DW, true, true>(g, Cout, 9 * Cin, P, ma, mb, G, nullptr, 0)));
   int launches = g_launches;
   if (gb) {
     const int n = launch_bias_grad(dZ, P, Cout, gb, g.work, g.work_bytes, g.stream);

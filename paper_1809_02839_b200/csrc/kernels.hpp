@@ -66,6 +66,12 @@ st_status tc_conv_dx(const GemmArgs& g, const float* dZ, int H, int W, int Cin, 
                      const float* mask, float* D);
 st_status tc_conv_dw(const GemmArgs& g, const float* X, const float* dZ, int H, int W, int Cin, int Cout, float* G,
                      float* gb);
+// first conv with 9·Cin ≤ 32 (RGB): col [P × 32] from launch_im2col_pad32, TMA GEMMs
+bool tc_conv_small_ok(int mode, int Cin, int Cout);
+st_status tc_conv_small_fwd(const GemmArgs& g, const float* col, int H, int W, int Cin, int Cout, const float* Wt,
+                            const float* bias, float* Y, int relu);
+st_status tc_conv_small_dw(const GemmArgs& g, const float* col, const float* dZ, int H, int W, int Cin, int Cout,
+                           float* G, float* gb);
 int tc_last_launches();
 
 // ---- softmax cross-entropy, batch mean (D11) -----------------------------------
