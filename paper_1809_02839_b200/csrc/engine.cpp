@@ -36,6 +36,7 @@ struct Layout {
   int64_t off_bufA = -1, off_bufB = -1, off_bufC = -1, off_losses = -1, off_rowloss = -1, off_ring_fwd = -1, off_ring_bwd = -1;
   int64_t off_ws = -1, off_ystage = -1;
   int64_t off_lrec = -1, off_ldh = -1, off_ldc = -1, off_ldG = -1, off_escr = -1, off_col = -1, off_dcol = -1;
+  int64_t off_lhlo = -1, off_ldglo = -1;
   int64_t gemm_rows = 1;
   int64_t off_ws2 = -1;
   int gemm_in = 1, gemm_out = 1;  // largest GEMM operand widths (workspace sizing)
@@ -220,6 +221,8 @@ st_status validate_and_layout(const st_config* c, Layout* L) {
     L->off_ldh = take(B * max_h);
     L->off_ldc = take(B * max_h);
     L->off_ldG = take(R * 4 * max_h);
+    L->off_lhlo = take(B * max_h);
+    L->off_ldglo = take(B * 4 * max_h);
   }
   if (max_vocab > 0) L->off_escr = take(embed_grad_scratch_bytes((int)R, max_vocab) / 4 + 1);
   if (max_col > 0) {
@@ -368,6 +371,8 @@ st_status ctx_init(const st_config* cfg, const st_buffers* bufs, void* stream, s
   c->lstm_dh = at(L.off_ldh);
   c->lstm_dc = at(L.off_ldc);
   c->lstm_dG = at(L.off_ldG);
+  c->lstm_hlo = at(L.off_lhlo);
+  c->lstm_dglo = at(L.off_ldglo);
   c->embed_scratch = at(L.off_escr);
   c->conv_col = at(L.off_col);
   c->conv_dcol = at(L.off_dcol);
@@ -582,18 +587,25 @@ static st_status lstm_forward(st_ctx* c, const LayerInfo& L, const float* Wh, co
     ST_TRY(gemm_fwd(gargs_rows(c, (int)c->R, L.n_in, 4 * H), X, Wh + L.w_off, Wh + L.b_off, gates, 0));
     c->launches += gemm_last_launches();
   }
-  ST_CUDA_TRY(cudaMemsetAsync(hbuf, 0, (size_t)B * H * 4, c->stream));  // h_{-1} = 0
+  ST_CUDA_TRY(cudaMemsetAsync(hbuf, 0, (size_t)B * H * 4, c->stream));          // h_{-1} = 0
+  ST_CUDA_TRY(cudaMemsetAsync(c->lstm_hlo, 0, (size_t)B * H * 4, c->stream));  // its tf32 lo
   for (int t = 0; t < T; ++t) {
     float* h_prev = hbuf + (size_t)t * B * H;
+    // G_t = Gx_t + h_{t−1}·W_hh: the GEMM takes h_{t−1}'s lo from the previous cell step and
+    // leaves its K-split partials to the cell kernel (two launches per step fewer)
+    SplitPlan plan;
     {
       Timed tt(c, KC_GEMM_FWD);
-      ST_TRY(gemm_fwd(gargs_rows(c, B, H, 4 * H), h_prev, Wh + L.whh_off, nullptr, c->lstm_rec, 0));
+      GemmArgs g = gargs_rows(c, B, H, 4 * H);
+      g.act_lo = c->lstm_hlo;
+      g.defer = &plan;
+      ST_TRY(gemm_fwd(g, h_prev, Wh + L.whh_off, nullptr, c->lstm_rec, 0));
       c->launches += gemm_last_launches();
     }
     Timed tt(c, KC_LOSS);
-    ST_TRY(launch_lstm_cell_fwd(gates + (size_t)t * B * 4 * H, c->lstm_rec,
+    ST_TRY(launch_lstm_cell_fwd(gates + (size_t)t * B * 4 * H, c->lstm_rec, &plan,
                                 t ? cbuf + (size_t)(t - 1) * B * H : nullptr, cbuf + (size_t)t * B * H,
-                                hbuf + (size_t)(t + 1) * B * H, B, H, c->stream));
+                                hbuf + (size_t)(t + 1) * B * H, c->lstm_hlo, B, H, c->stream));
     c->launches += 1;
   }
   return ST_OK;
@@ -704,19 +716,23 @@ static st_status lstm_backward(st_ctx* c, const LayerInfo& L, const float* Wh, c
   const float* gates = slot + L.gates_off;
   const float* cbuf = slot + L.c_off;
   const float* hbuf = slot + L.h_off;
+  SplitPlan plan;  // dh_next of the step after t (splits = 0: none at t = T−1)
   for (int t = T - 1; t >= 0; --t) {
     {
       Timed tt(c, KC_LOSS);
       ST_TRY(launch_lstm_cell_bwd(gates + (size_t)t * B * 4 * H, cbuf + (size_t)t * B * H,
                                   t ? cbuf + (size_t)(t - 1) * B * H : nullptr, dOut + (size_t)t * B * H,
-                                  t < T - 1 ? c->lstm_dh : nullptr, c->lstm_dc, t == T - 1,
-                                  c->lstm_dG + (size_t)t * B * 4 * H, B, H, c->stream));
+                                  t < T - 1 ? c->lstm_dh : nullptr, &plan, c->lstm_dc, t == T - 1,
+                                  c->lstm_dG + (size_t)t * B * 4 * H, t > 0 ? c->lstm_dglo : nullptr, B, H,
+                                  c->stream));
       c->launches += 1;
     }
-    if (t > 0) {  // dh_{t−1} = dG_t · W_hhᵀ
+    if (t > 0) {  // dh_{t−1} = dG_t · W_hhᵀ (dG_t's lo from the cell, partials left to the next cell)
       Timed tt(c, KC_GEMM_DX);
-      ST_TRY(gemm_dx(gargs_rows(c, B, H, 4 * H), c->lstm_dG + (size_t)t * B * 4 * H, Wh + L.whh_off, nullptr,
-                     c->lstm_dh));
+      GemmArgs g = gargs_rows(c, B, H, 4 * H);
+      g.act_lo = c->lstm_dglo;
+      g.defer = &plan;
+      ST_TRY(gemm_dx(g, c->lstm_dG + (size_t)t * B * 4 * H, Wh + L.whh_off, nullptr, c->lstm_dh));
       c->launches += gemm_last_launches();
     }
   }

@@ -60,10 +60,13 @@ struct LayerInfo {
 };
 
 // LSTM / embedding kernels (k_lstm.cu)
-st_status launch_lstm_cell_fwd(float* gates, const float* rec, const float* c_prev, float* c_out, float* h_out, int B,
-                               int H, cudaStream_t s);
+// rec / dh_next: the recurrent GEMM output, or (plan with splits > 1) its deferred
+// split-K partials; h_lo / dG_lo (nullable): tf32 lo halves for the next recurrent GEMM
+st_status launch_lstm_cell_fwd(float* gates, const float* rec, const SplitPlan* rp, const float* c_prev, float* c_out,
+                               float* h_out, float* h_lo, int B, int H, cudaStream_t s);
 st_status launch_lstm_cell_bwd(const float* gates, const float* c_t, const float* c_prev, const float* dOut,
-                               const float* dh_next, float* dc, int first, float* dG, int B, int H, cudaStream_t s);
+                               const float* dh_next, const SplitPlan* hp, float* dc, int first, float* dG,
+                               float* dG_lo, int B, int H, cudaStream_t s);
 st_status launch_embed_gather(const float* E, const int32_t* tok, int rows, int D, float* out, cudaStream_t s);
 int64_t embed_grad_scratch_bytes(int rows, int V);
 st_status launch_embed_grad(const float* dA, const int32_t* tok, int rows, int V, int D, float* gE, void* scratch,
@@ -135,6 +138,8 @@ struct st_ctx {
   int32_t* y_stage = nullptr;   // [R] labels staged from host (st_run_host)
   float* lstm_rec = nullptr;    // [B × 4H] h_{t−1}·W_hh
   float* lstm_dh = nullptr;     // [B × H] dh_next
+  float* lstm_hlo = nullptr;    // [B × H] tf32 lo of h_{t−1} (3xTF32 operand of the recurrent GEMM)
+  float* lstm_dglo = nullptr;   // [B × 4H] tf32 lo of dG_t (operand of the dh GEMM)
   float* lstm_dc = nullptr;     // [B × H] dc_next
   float* lstm_dG = nullptr;     // [R × 4H] gate gradients of all steps
   void* embed_scratch = nullptr;

@@ -34,6 +34,7 @@ static st_status check(const GemmArgs& g) {
 
 st_status gemm_fwd(const GemmArgs& g, const float* X, const float* W, const float* bias, float* Z, int relu) {
   ST_TRY(check(g));
+  if (g.defer) g.defer->splits = 1;  // overridden when the TMEM-A kernel defers its reduce
   if (g.mode == ST_GEMM_SIMT) {
     st_status s = simt_fwd(g, X, W, bias, Z, relu);
     g_last_launches = simt_last_launches();
@@ -46,6 +47,7 @@ st_status gemm_fwd(const GemmArgs& g, const float* X, const float* W, const floa
 
 st_status gemm_dx(const GemmArgs& g, const float* dZ, const float* W, const float* mask, float* D) {
   ST_TRY(check(g));
+  if (g.defer) g.defer->splits = 1;  // overridden when the TMEM-A kernel defers its reduce
   if (g.mode == ST_GEMM_SIMT) {
     st_status s = simt_dx(g, dZ, W, mask, D);
     g_last_launches = simt_last_launches();

@@ -2405,10 +2405,16 @@ st_status launch_ts(const GemmArgs& g, int M, int N, int K, const CUtensorMap& m
   p.ext_reduce = p.splits >= ext_reduce_splits();
   float* blo = reinterpret_cast<float*>(static_cast<char*>(g.work) + kCounterBytes +
                                         (size_t)2 * 148 * BNMAX * BM * 4);
-  const size_t n4 = (size_t)N * K / 4;
-  split_lo_kernel<<<std::min<size_t>(4 * 148, (n4 + 255) / 256), 256, 0, g.stream>>>(
-      reinterpret_cast<const float4*>(Bact), reinterpret_cast<float4*>(blo), n4);
-  ST_CUDA_TRY(cudaGetLastError());
+  int launches = 1;
+  if (g.act_lo) {
+    blo = const_cast<float*>(g.act_lo);  // the producer already split the operand
+  } else {
+    const size_t n4 = (size_t)N * K / 4;
+    split_lo_kernel<<<std::min<size_t>(4 * 148, (n4 + 255) / 256), 256, 0, g.stream>>>(
+        reinterpret_cast<const float4*>(Bact), reinterpret_cast<float4*>(blo), n4);
+    ST_CUDA_TRY(cudaGetLastError());
+    ++launches;
+  }
   const int brows = pair ? p.bn / 2 : p.bn;
   CUtensorMap mb, mblo;
   if (!make_map(&mb, Bact, K, N, K, brows, false) || !make_map(&mblo, blo, K, N, K, brows, false))
@@ -2438,10 +2444,17 @@ st_status launch_ts(const GemmArgs& g, int M, int N, int K, const CUtensorMap& m
     kern<<<grid, TS_THREADS, ts_smem_bytes(), g.stream>>>(ma, mb, mblo, p);
   }
   ST_CUDA_TRY(cudaGetLastError());
-  g_launches = 2;
-  if (p.ext_reduce) {
+  g_launches = launches;
+  if (p.ext_reduce && g.defer) {
+    g.defer->ws = p.ws;
+    g.defer->splits = p.splits;
+    g.defer->tiles = mt_grid * nt;
+    g.defer->mt = mt_grid;
+    g.defer->bm = BM;
+    g.defer->bn = BNMAX;
+  } else if (p.ext_reduce) {
     ST_TRY(launch_splitk_epilogue<EPI>(p, mt_grid * nt, mt_grid, g.stream));
-    g_launches = 3;
+    g_launches = launches + 1;
   }
   return ST_OK;
 }

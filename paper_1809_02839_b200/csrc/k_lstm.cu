@@ -15,20 +15,67 @@ namespace {
 
 __device__ __forceinline__ float sigm(float x) { return 1.0f / (1.0f + expf(-x)); }
 
+// x − trunc_tf32(x): the lo half of the 3xTF32 split of the next GEMM's activation
+// operand (the same expression as k_gemm_tc.cu split_lo_kernel, written independently)
+__device__ __forceinline__ float tf32_lo(float x) { return x - __uint_as_float(__float_as_uint(x) & 0xFFFFE000u); }
+
+// Elements (row n, columns m + j·step, j < J) of a GEMM output [rows × ld]: direct, or
+// the sums of the deferred split-K partials (SplitPlan, kernels.hpp) — each in split order
+// from 0.f (bit-identical to the reduce kernel), with every load of a 4-split group issued
+// before its adds (the partials come from L2: latency, not bandwidth, bounds this).
+template <int J>
+__device__ __forceinline__ void gemm_out(const float* direct, const SplitPlan& p, int n, int m, int step, int ld,
+                                         float* out) {
+  if (p.splits <= 1) {
+#pragma unroll
+    for (int j = 0; j < J; ++j) out[j] = direct[(size_t)n * ld + m + j * step];
+    return;
+  }
+  const size_t stride = (size_t)p.tiles * p.bn * p.bm;
+  const float* src[J];
+#pragma unroll
+  for (int j = 0; j < J; ++j) {
+    const int mj = m + j * step;
+    src[j] = p.ws + ((size_t)((n / p.bn) * p.mt + mj / p.bm) * p.bn + n % p.bn) * p.bm + mj % p.bm;
+    out[j] = 0.f;
+  }
+  int s = 0;
+  for (; s + 4 <= p.splits; s += 4) {
+    float v[4][J];
+#pragma unroll
+    for (int u = 0; u < 4; ++u)
+#pragma unroll
+      for (int j = 0; j < J; ++j) v[u][j] = __ldcg(src[j] + (size_t)(s + u) * stride);
+#pragma unroll
+    for (int u = 0; u < 4; ++u)
+#pragma unroll
+      for (int j = 0; j < J; ++j) out[j] += v[u][j];
+  }
+  for (; s < p.splits; ++s) {
+    float v[J];
+#pragma unroll
+    for (int j = 0; j < J; ++j) v[j] = __ldcg(src[j] + (size_t)s * stride);
+#pragma unroll
+    for (int j = 0; j < J; ++j) out[j] += v[j];
+  }
+}
+
 // gates [B × 4H]: in = Gx_t (pre-activation input projection incl. bias), overwritten
-// with the activated i, f, g, o; rec [B × 4H] = h_{t−1}·W_hh.
-__global__ void lstm_cell_fwd_kernel(float* __restrict__ gates, const float* __restrict__ rec,
+// with the activated i, f, g, o; rec [B × 4H] = h_{t−1}·W_hh (or its deferred partials).
+// h_lo (optional): tf32 lo of h_t for the next step's recurrent GEMM.
+__global__ void lstm_cell_fwd_kernel(float* __restrict__ gates, const float* __restrict__ rec, SplitPlan rp,
                                      const float* __restrict__ c_prev, float* __restrict__ c_out,
-                                     float* __restrict__ h_out, int B, int H) {
+                                     float* __restrict__ h_out, float* __restrict__ h_lo, int B, int H) {
   const int idx = blockIdx.x * blockDim.x + threadIdx.x;
   if (idx >= B * H) return;
   const int b = idx / H, j = idx % H;
   float* g = gates + (size_t)b * 4 * H;
-  const float* r = rec + (size_t)b * 4 * H;
-  const float gi = sigm(g[j] + r[j]);
-  const float gf = sigm(g[H + j] + r[H + j]);
-  const float gg = tanhf(g[2 * H + j] + r[2 * H + j]);
-  const float go = sigm(g[3 * H + j] + r[3 * H + j]);
+  float r[4];
+  gemm_out<4>(rec, rp, b, j, H, 4 * H, r);
+  const float gi = sigm(g[j] + r[0]);
+  const float gf = sigm(g[H + j] + r[1]);
+  const float gg = tanhf(g[2 * H + j] + r[2]);
+  const float go = sigm(g[3 * H + j] + r[3]);
   const float cp = c_prev ? c_prev[idx] : 0.f;
   const float c = gf * cp + gi * gg;
   g[j] = gi;
@@ -36,15 +83,18 @@ __global__ void lstm_cell_fwd_kernel(float* __restrict__ gates, const float* __r
   g[2 * H + j] = gg;
   g[3 * H + j] = go;
   c_out[idx] = c;
-  h_out[idx] = go * tanhf(c);
+  const float h = go * tanhf(c);
+  h_out[idx] = h;
+  if (h_lo) h_lo[idx] = tf32_lo(h);
 }
 
-// dOut_t [B × H] (gradient w.r.t. h_t from above), dh_next [B × H] (from step t+1,
-// NULL at t = T−1), dc [B × H] in: dc_next (ignored when first), out: dc⊙f for step t−1.
+// dOut_t [B × H] (gradient w.r.t. h_t from above), dh_next [B × H] (from step t+1, or its
+// deferred partials; NULL with splits = 0 at t = T−1), dc [B × H] in: dc_next (ignored when
+// first), out: dc⊙f for step t−1. dG_lo (optional): tf32 lo of dG_t for the dh GEMM.
 __global__ void lstm_cell_bwd_kernel(const float* __restrict__ gates, const float* __restrict__ c_t,
                                      const float* __restrict__ c_prev, const float* __restrict__ dOut,
-                                     const float* __restrict__ dh_next, float* __restrict__ dc, int first,
-                                     float* __restrict__ dG, int B, int H) {
+                                     const float* __restrict__ dh_next, SplitPlan hp, float* __restrict__ dc,
+                                     int first, float* __restrict__ dG, float* __restrict__ dG_lo, int B, int H) {
   const int idx = blockIdx.x * blockDim.x + threadIdx.x;
   if (idx >= B * H) return;
   const int b = idx / H, j = idx % H;
@@ -52,14 +102,27 @@ __global__ void lstm_cell_bwd_kernel(const float* __restrict__ gates, const floa
   const float gi = g[j], gf = g[H + j], gg = g[2 * H + j], go = g[3 * H + j];
   const float c = c_t[idx];
   const float cp = c_prev ? c_prev[idx] : 0.f;
-  const float dh = dOut[idx] + (dh_next ? dh_next[idx] : 0.f);
+  float dhn = 0.f;
+  if (dh_next || hp.splits > 1) gemm_out<1>(dh_next, hp, b, j, 0, H, &dhn);
+  const float dh = dOut[idx] + dhn;
   const float tc = tanhf(c);
   const float dcv = (first ? 0.f : dc[idx]) + dh * go * (1.f - tc * tc);
   float* d = dG + (size_t)b * 4 * H;
-  d[j] = dcv * gg * gi * (1.f - gi);
-  d[H + j] = dcv * cp * gf * (1.f - gf);
-  d[2 * H + j] = dcv * gi * (1.f - gg * gg);
-  d[3 * H + j] = dh * tc * go * (1.f - go);
+  const float d0 = dcv * gg * gi * (1.f - gi);
+  const float d1 = dcv * cp * gf * (1.f - gf);
+  const float d2 = dcv * gi * (1.f - gg * gg);
+  const float d3 = dh * tc * go * (1.f - go);
+  d[j] = d0;
+  d[H + j] = d1;
+  d[2 * H + j] = d2;
+  d[3 * H + j] = d3;
+  if (dG_lo) {
+    float* l = dG_lo + (size_t)b * 4 * H;
+    l[j] = tf32_lo(d0);
+    l[H + j] = tf32_lo(d1);
+    l[2 * H + j] = tf32_lo(d2);
+    l[3 * H + j] = tf32_lo(d3);
+  }
   dc[idx] = dcv * gf;
 }
 
@@ -140,18 +203,22 @@ __global__ void embed_grad_kernel(const float* __restrict__ dA, const int* __res
 
 }  // namespace
 
-st_status launch_lstm_cell_fwd(float* gates, const float* rec, const float* c_prev, float* c_out, float* h_out, int B,
-                               int H, cudaStream_t s) {
+st_status launch_lstm_cell_fwd(float* gates, const float* rec, const SplitPlan* rp, const float* c_prev, float* c_out,
+                               float* h_out, float* h_lo, int B, int H, cudaStream_t s) {
   const int n = B * H;
-  lstm_cell_fwd_kernel<<<(n + 255) / 256, 256, 0, s>>>(gates, rec, c_prev, c_out, h_out, B, H);
+  const SplitPlan p = rp ? *rp : SplitPlan{};
+  lstm_cell_fwd_kernel<<<(n + 255) / 256, 256, 0, s>>>(gates, rec, p, c_prev, c_out, h_out, h_lo, B, H);
   ST_CUDA_TRY(cudaGetLastError());
   return ST_OK;
 }
 
 st_status launch_lstm_cell_bwd(const float* gates, const float* c_t, const float* c_prev, const float* dOut,
-                               const float* dh_next, float* dc, int first, float* dG, int B, int H, cudaStream_t s) {
+                               const float* dh_next, const SplitPlan* hp, float* dc, int first, float* dG,
+                               float* dG_lo, int B, int H, cudaStream_t s) {
   const int n = B * H;
-  lstm_cell_bwd_kernel<<<(n + 255) / 256, 256, 0, s>>>(gates, c_t, c_prev, dOut, dh_next, dc, first, dG, B, H);
+  const SplitPlan p = hp ? *hp : SplitPlan{};
+  lstm_cell_bwd_kernel<<<(n + 255) / 256, 256, 0, s>>>(gates, c_t, c_prev, dOut, dh_next, p, dc, first, dG, dG_lo,
+                                                        B, H);
   ST_CUDA_TRY(cudaGetLastError());
   return ST_OK;
 }

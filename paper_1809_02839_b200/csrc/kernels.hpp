@@ -35,6 +35,15 @@ st_status launch_bias_grad_update(const float* dZ, int B, int n_out, const Updat
 // fwd: Z[B×out] = X[B×in]·W[in×out] + b, optional ReLU
 // dX : D[B×in]  = (dZ[B×out]·Wᵀ) ⊙ 1[mask > 0] (mask may be null)
 // dW : G[in×out] = Xᵀ·dZ ; gb[out] = Σ_b dZ (gb may be null)
+// Split-K partials left unreduced for a consumer kernel (the LSTM cells): output element
+// (m, n) = Σ_{s < splits} ws[s·tiles·bn·bm + (((n / bn)·mt + m / bm)·bn + n % bn)·bm + m % bm],
+// summed in split order from 0.f (bit-identical to the reduce kernel). splits ≤ 1: the
+// GEMM wrote its output normally.
+struct SplitPlan {
+  const float* ws = nullptr;
+  int splits = 0, tiles = 0, mt = 0, bm = 128, bn = 128;
+};
+
 struct GemmArgs {
   int mode;  // ST_GEMM_*
   int B, n_in, n_out;
@@ -42,6 +51,10 @@ struct GemmArgs {
   int64_t work_bytes;
   cudaStream_t stream;
   int max_ctas = 0;  // CTA budget of the launch (0 = every SM); used to share the GPU between streams
+  // FP32X3 fwd / dX (TMEM-A kernels): lo = x − trunc_tf32(x) of the activation operand,
+  // already computed by its producer (same pitch as the operand); NULL: split here
+  const float* act_lo = nullptr;
+  SplitPlan* defer = nullptr;  // non-NULL: K-split partials are left for the consumer (see SplitPlan)
 };
 int64_t gemm_workspace_bytes(int B, int max_in, int max_out);
 st_status gemm_fwd(const GemmArgs& g, const float* X, const float* W, const float* bias, float* Z, int relu);
