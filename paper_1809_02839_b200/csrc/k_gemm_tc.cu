@@ -740,7 +740,8 @@ __device__ __forceinline__ void tc_mma_ts(uint32_t tmem_d, uint32_t tmem_a, uint
                                           uint32_t accum);
 __device__ __forceinline__ void tc_st32(uint32_t taddr, const uint32_t* v);
 
-// FP32X3 implicit-conv fwd / dX with the activation window in TMEM (A-from-TMEM MMAs).
+// FP32X3 persistent GEMM with the A operand in TMEM (A-from-TMEM MMAs): the implicit-conv
+// fwd / dX / dW and the tall dense dW (LSTM / LM softmax: K = T·B rows).
 // With A and B both read from smem by three MMAs per K step (plus the converter's
 // passes), the persistent kernel above is bound by shared-memory bandwidth (~144 KB of
 // smem traffic per 128 × 64 × 32 K-block vs ~576 MMA cycles). Here the converter warps
@@ -748,13 +749,16 @@ __device__ __forceinline__ void tc_st32(uint32_t taddr, const uint32_t* v);
 // compute the weight lo tile in smem; the MMAs then read only the weight tiles from smem.
 // Ring: CS stages × (A raw 16 KB + B raw 16 KB + B lo 16 KB), TMEM slot s ↔ stage s
 // (64 columns: 32 hi + 32 lo), 2 accumulators × 128 columns: 256 + CS·64 ≤ 512.
+// Work units u = split·tiles + tile (tile m-fastest); with p.splits > 1 every unit covers
+// kb_per_split K-blocks and writes its partial tile to the workspace (the split-K layout
+// of epilogue()), reduced in fixed split order by splitk_epilogue_kernel.
 constexpr int CS = 4;
 constexpr int CS_STAGE = 3 * TILE_BYTES;
 constexpr int cs_smem_bytes() { return CS * CS_STAGE + 1024 + 256; }
 
-template <int EPI, bool B_MN, int CV>
+template <int EPI, bool A_MN, bool B_MN, int CV>
 __global__ void __launch_bounds__(kPThreads, 1)
-    tc_conv_ts_kernel(const __grid_constant__ CUtensorMap mapA, const __grid_constant__ CUtensorMap mapB,
+    tc_tsg_kernel(const __grid_constant__ CUtensorMap mapA, const __grid_constant__ CUtensorMap mapB,
                       TcParams p, int mt, int tiles) {
   extern __shared__ __align__(1024) uint8_t smem_raw[];
   char* smem = align_smem_1k(smem_raw);
@@ -768,7 +772,13 @@ __global__ void __launch_bounds__(kPThreads, 1)
 
   const int warp = threadIdx.x >> 5;
   const int lane = threadIdx.x & 31;
-  const int nkb = p.kb_total;
+  const int units = tiles * p.splits;
+  // K-block range of unit u
+  auto kb_range = [&](int u, int& k0, int& k1) {
+    const int sp = u / tiles;
+    k0 = sp * p.kb_per_split;
+    k1 = min(p.kb_total, k0 + p.kb_per_split);
+  };
   const int bn = p.bn;
   const int nbox_b = (bn + 31) / 32;
   const int b_chunks = B_MN ? nbox_b * 256 : bn * 8;
@@ -804,16 +814,18 @@ __global__ void __launch_bounds__(kPThreads, 1)
     // ---------------- TMA producer
     const uint32_t bytes = (uint32_t)(TILE_BYTES + (B_MN ? nbox_b * 4096 : bn * BK * 4));
     int it = 0;
-    for (int t = blockIdx.x; t < tiles; t += gridDim.x) {
-      const int m0 = (t % mt) * BM, n0 = (t / mt) * BNMAX;
-      for (int kb = 0; kb < nkb; ++kb, ++it) {
+    for (int u = blockIdx.x; u < units; u += gridDim.x) {
+      const int t = u % tiles, m0 = (t % mt) * BM, n0 = (t / mt) * BNMAX;
+      int kb0, kb1;
+      kb_range(u, kb0, kb1);
+      for (int kb = kb0; kb < kb1; ++kb, ++it) {
         const int s = it % CS;
         mbar_wait(b_empty + 8 * s, ((it / CS) & 1) ^ 1);
         const uint32_t full = b_full + 8 * s;
         const uint32_t dA = smem_u32(smem + s * CS_STAGE);
         if (elect_one()) {
           mbar_expect_tx(full, bytes);
-          load_stage<false, B_MN, CV>(p, &mapA, &mapB, dA, dA + TILE_BYTES, full, m0, n0, kb * BK, nbox_b);
+          load_stage<A_MN, B_MN, CV>(p, &mapA, &mapB, dA, dA + TILE_BYTES, full, m0, n0, kb * BK, nbox_b);
         }
         __syncwarp();
       }
@@ -821,12 +833,14 @@ __global__ void __launch_bounds__(kPThreads, 1)
   } else if (warp == 1) {
     // ---------------- MMA issuer (A hi / lo from TMEM slot s, B hi / lo from smem)
     int it = 0, j = 0;
-    for (int t = blockIdx.x; t < tiles; t += gridDim.x, ++j) {
+    for (int u = blockIdx.x; u < units; u += gridDim.x, ++j) {
       const int buf = j & 1;
       const uint32_t d = tmem + (uint32_t)(buf * BNMAX);
+      int kb0, kb1;
+      kb_range(u, kb0, kb1);
       mbar_wait(acc_empty + 8 * buf, ((j >> 1) & 1) ^ 1);
       tc_fence_after();
-      for (int kb = 0; kb < nkb; ++kb, ++it) {
+      for (int kb = kb0; kb < kb1; ++kb, ++it) {
         const int s = it % CS;
         mbar_wait(b_ready + 8 * s, (it / CS) & 1);
         tc_fence_after();
@@ -835,41 +849,54 @@ __global__ void __launch_bounds__(kPThreads, 1)
         if (elect_one()) {
 #pragma unroll
           for (int kk = 0; kk < BK / 8; ++kk) {
-            const uint32_t acc = (kb > 0 || kk > 0) ? 1u : 0u;
+            const uint32_t acc = (kb > kb0 || kk > 0) ? 1u : 0u;
             tc_mma_ts(d, a_hi + kk * 8, op_desc<B_MN>(b_hi, kk), p.idesc, acc);
             tc_mma_ts(d, a_lo + kk * 8, op_desc<B_MN>(b_hi, kk), p.idesc, 1u);
             tc_mma_ts(d, a_hi + kk * 8, op_desc<B_MN>(b_lo, kk), p.idesc, 1u);
           }
           tc_commit(b_empty + 8 * s);
-          if (kb == nkb - 1) tc_commit(acc_full + 8 * buf);
+          if (kb == kb1 - 1) tc_commit(acc_full + 8 * buf);
         }
         __syncwarp();
       }
     }
   } else if (warp < 6) {
-    // ---------------- converters (warps 2..5): window row r → TMEM lane r (hi, lo);
-    // weight tile lo in smem
+    // ---------------- converters (warps 2..5): A row r → TMEM lane r (hi, lo); B lo in smem
     const int quad = warp & 3;
     const int r = quad * 32 + lane;
     const int ctid = threadIdx.x - 64;
     int it = 0;
-    for (int t = blockIdx.x; t < tiles; t += gridDim.x) {
-      for (int kb = 0; kb < nkb; ++kb, ++it) {
+    for (int u = blockIdx.x; u < units; u += gridDim.x) {
+      int kb0, kb1;
+      kb_range(u, kb0, kb1);
+      for (int kb = kb0; kb < kb1; ++kb, ++it) {
         const int s = it % CS;
         mbar_wait(b_full + 8 * s, (it / CS) & 1);
         char* st = smem + s * CS_STAGE;
         uint32_t hi[32], lo[32];
+        if (A_MN) {
+          // element (k, r): box r/32, row k (128 B), 32-byte atoms swizzled by k % 4
+          const char* box = st + (r >> 5) * 4096;
 #pragma unroll
-        for (int c = 0; c < 8; ++c) {
-          const float4 v = *reinterpret_cast<const float4*>(st + r * 128 + ((c ^ (r & 7)) << 4));
-          hi[4 * c + 0] = __float_as_uint(v.x);
-          hi[4 * c + 1] = __float_as_uint(v.y);
-          hi[4 * c + 2] = __float_as_uint(v.z);
-          hi[4 * c + 3] = __float_as_uint(v.w);
-          lo[4 * c + 0] = __float_as_uint(lo_part(v.x));
-          lo[4 * c + 1] = __float_as_uint(lo_part(v.y));
-          lo[4 * c + 2] = __float_as_uint(lo_part(v.z));
-          lo[4 * c + 3] = __float_as_uint(lo_part(v.w));
+          for (int q = 0; q < 32; ++q) {
+            const float x =
+                *reinterpret_cast<const float*>(box + q * 128 + ((((r & 31) >> 3) ^ (q & 3)) << 5) + (r & 7) * 4);
+            hi[q] = __float_as_uint(x);
+            lo[q] = __float_as_uint(lo_part(x));
+          }
+        } else {
+#pragma unroll
+          for (int c = 0; c < 8; ++c) {
+            const float4 v = *reinterpret_cast<const float4*>(st + r * 128 + ((c ^ (r & 7)) << 4));
+            hi[4 * c + 0] = __float_as_uint(v.x);
+            hi[4 * c + 1] = __float_as_uint(v.y);
+            hi[4 * c + 2] = __float_as_uint(v.z);
+            hi[4 * c + 3] = __float_as_uint(v.w);
+            lo[4 * c + 0] = __float_as_uint(lo_part(v.x));
+            lo[4 * c + 1] = __float_as_uint(lo_part(v.y));
+            lo[4 * c + 2] = __float_as_uint(lo_part(v.z));
+            lo[4 * c + 3] = __float_as_uint(lo_part(v.w));
+          }
         }
         make_lo(st + TILE_BYTES, st + 2 * TILE_BYTES, b_chunks, ctid);
         fence_proxy_async();
@@ -886,20 +913,31 @@ __global__ void __launch_bounds__(kPThreads, 1)
       }
     }
   } else {
-    // ---------------- epilogue (warps 6..9 → TMEM quadrants 2, 3, 0, 1), row-major
+    // ---------------- epilogue (warps 6..9 → TMEM quadrants 2, 3, 0, 1)
     const int quad = warp & 3;
     int j = 0;
-    for (int t = blockIdx.x; t < tiles; t += gridDim.x, ++j) {
+    for (int u = blockIdx.x; u < units; u += gridDim.x, ++j) {
       const int buf = j & 1;
-      const int m0 = (t % mt) * BM, n0 = (t / mt) * BNMAX;
+      const int t = u % tiles, m0 = (t % mt) * BM, n0 = (t / mt) * BNMAX;
       mbar_wait(acc_full + 8 * buf, (j >> 1) & 1);
       tc_fence_after();
       const int m = m0 + quad * 32 + lane;
       const uint32_t trow = tmem + (uint32_t)(buf * BNMAX) + ((uint32_t)(quad * 32) << 16);
-      for (int c = 0; c < bn; c += 16) {
-        float v[16];
-        tc_ld16(trow + c, v);
-        if (m < p.M) epilogue_store16<EPI>(p, m, n0 + c, v, 0.f);
+      if (p.splits > 1) {
+        float* wsp = p.ws + ((size_t)(u / tiles) * tiles + t) * (BNMAX * BM);
+        for (int c = 0; c < bn; c += 16) {
+          float v[16];
+          tc_ld16(trow + c, v);
+#pragma unroll
+          for (int q = 0; q < 16; ++q) wsp[(size_t)(c + q) * BM + quad * 32 + lane] = v[q];
+        }
+      } else {
+        const float bias = (EPI == EPI_FWD && p.aux && m < p.M && !p.row) ? p.aux[m] : 0.f;
+        for (int c = 0; c < bn; c += 16) {
+          float v[16];
+          tc_ld16(trow + c, v);
+          if (m < p.M) epilogue_store16<EPI>(p, m, n0 + c, v, bias);
+        }
       }
       tc_fence_before();
       __syncwarp();
@@ -2293,18 +2331,24 @@ st_status launch(const GemmArgs& g, int M, int N, int K, const CUtensorMap& ma, 
     attr_set[ai] = true;
   }
   p.ext_reduce = p.splits >= ext_reduce_splits();
-  if ((CV == CV_FWD || CV == CV_DX || CV == CV_ROWS) && p.splits == 1 && g.mode == ST_GEMM_FP32X3 && conv_ts_on()) {
-    auto ck = tc_conv_ts_kernel<EPI, B_MN, CV>;
+  if (g.mode == ST_GEMM_FP32X3 && conv_ts_on() && (CV != CV_NONE || EPI == EPI_DW)) {
+    // persistent TMEM-A kernel: implicit conv (all passes) and the tall dense dW
+    auto ck = tc_tsg_kernel<EPI, A_MN, B_MN, CV>;
     static bool cattr_set = false;
     if (!cattr_set) {
       ST_CUDA_TRY(cudaFuncSetAttribute(ck, cudaFuncAttributeMaxDynamicSharedMemorySize, cs_smem_bytes()));
       cattr_set = true;
     }
     p.idesc = make_idesc(p.bn, false, B_MN);
+    p.ext_reduce = p.splits > 1;
     const int budget = g.max_ctas > 0 ? std::min(g.max_ctas, num_sms()) : num_sms();
-    ck<<<std::min(tiles, budget), kPThreads, cs_smem_bytes(), g.stream>>>(ma, mb, p, mt, tiles);
+    ck<<<std::min(tiles * p.splits, budget), kPThreads, cs_smem_bytes(), g.stream>>>(ma, mb, p, mt, tiles);
     ST_CUDA_TRY(cudaGetLastError());
     g_launches = 1;
+    if (p.ext_reduce) {
+      ST_TRY(launch_splitk_epilogue<EPI>(p, tiles, mt, g.stream));
+      g_launches = 2;
+    }
     return ST_OK;
   }
   if ((CV == CV_FWD || CV == CV_DX || CV == CV_ROWS) && p.splits == 1 && !conv_persistent_off()) {
