@@ -31,6 +31,10 @@ BWD = 1
 
 PRED_SPECTRAIN = "spectrain"
 PRED_NONE = "none"  # vanilla pipelining, s ≡ 0 (D-A8)
+# PipeDream weight stashing (Fig. 6c): the forward of a mini-batch uses the
+# stage's current weights and its backward uses the SAME (stashed) weights; no prediction
+# (SURVEY §8(f) NEXT-2). The trace records, for a backward, the version its forward used.
+PRED_STASH = "stash"
 
 MOMENTUM_EMA = "ema"  # Eq. 1 literally: v = γ v + (1-γ) g
 MOMENTUM_HEAVY_BALL = "heavy_ball"  # v = γ v + g (TF MomentumOptimizer, D2 flag)
@@ -415,7 +419,9 @@ def run(model, W0: Sequence[np.ndarray], X: np.ndarray, Y: np.ndarray, eta: floa
     trace: List[List[Event]] = [[] for _ in range(N)]
 
     def s_of(k: int, d: int) -> int:
-        return 0 if pred == PRED_NONE else version_difference(k, N, d)
+        return 0 if pred in (PRED_NONE, PRED_STASH) else version_difference(k, N, d)
+
+    wstash: Dict[Tuple[int, int], Tuple[np.ndarray, int]] = {}  # PRED_STASH: (k, i) → (W, version) of F(i)
 
     def ready(k: int) -> bool:
         d, i = progs[k][pc[k]]
@@ -428,7 +434,13 @@ def run(model, W0: Sequence[np.ndarray], X: np.ndarray, Y: np.ndarray, eta: floa
         layers = model.stage_layers(k)
         s = s_of(k, d)
         W_hat = predict(W[k], V[k], s, eta)
-        trace[k].append(Event(k, pc[k], d, i, version[k], s))
+        base = version[k]
+        if pred == PRED_STASH:
+            if d == FWD:
+                wstash[(k, i)] = (W_hat.copy(), version[k])  # s = 0: W_hat is the current W
+            else:
+                W_hat, base = wstash.pop((k, i))  # the forward's weights and their version
+        trace[k].append(Event(k, pc[k], d, i, base, s))
         if d == FWD:
             if k == 0:
                 A_in = X[i] if getattr(layers[0], "kind", "dense") == "embed" else X[i].astype(np.float64)

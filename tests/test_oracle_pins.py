@@ -563,3 +563,65 @@ def test_maxpool_tie_rule_first_in_row_major():
     assert Y[0, 0, 0, 0] == 1.0 and arg[0, 0, 0, 0] == 1
     dX = O.maxpool2_backward(arg, np.ones((1, 1, 1, 1)), X.shape)
     assert dX[0, 0, 1, 0] == 1.0 and dX.sum() == 1.0
+
+
+# ---------------------------------------------------------------- PipeDream weight stashing (NEXT-2)
+
+def _stash_version_indexed(model, W0, X, Y, eta, gamma):
+    """Weight stashing written from its definition, independently of the
+    oracle's interpreter: mini-batch j sees, at every stage k, the single version
+    c_F(j, k) = max(0, j − (N−k−1)) in BOTH passes (1F1B base version of its forward,
+    D8), so its gradient is plain autograd of the whole model with the stage weights at
+    those versions; stage k's update j then gives version j+1 (Eq. 1, D1)."""
+    N = model.num_stages
+    hist = [[torch.tensor(w, dtype=torch.float64)] for w in W0]  # hist[k][v] = stage k at version v
+    V = [torch.zeros_like(h[0]) for h in hist]
+    losses = []
+    for j in range(X.shape[0]):
+        used = [hist[k][max(0, j - (N - k - 1))].clone().requires_grad_(True) for k in range(N)]
+        loss = _torch_model_loss(model, torch.cat(used), torch.tensor(X[j], dtype=torch.float64),
+                                 torch.tensor(Y[j]))
+        grads = torch.autograd.grad(loss, used)
+        losses.append(float(loss.detach()))
+        for k in range(N):
+            V[k] = gamma * V[k] + (1.0 - gamma) * grads[k]
+            hist[k].append(hist[k][-1] - eta * V[k])
+    return [h[-1].numpy() for h in hist], np.array(losses)
+
+
+@pytest.mark.parametrize("cuts", [[2], [2, 3], [1, 2, 3]])
+def test_stash_equals_version_indexed_autograd(cuts):
+    model = sd.mlp([20, 16, 12, 12, 5], cuts=cuts)
+    w0, X, Y = sd.parity_inputs(model, 9, 4, seed=3)
+    W0 = sd.widen(w0)
+    res = O.run(model, W0, X.astype(np.float64), Y, 0.05, 0.9, pred=O.PRED_STASH)
+    Wr, lr = _stash_version_indexed(model, W0, X.astype(np.float64), Y, 0.05, 0.9)
+    for a, b in zip(res.W, Wr):
+        np.testing.assert_allclose(a, b, rtol=0, atol=1e-12)
+    np.testing.assert_allclose(res.losses, lr, rtol=1e-12)
+    # the trace: s ≡ 0, the forward base version is c_F, and the backward records the
+    # version its forward used (the stashed copy)
+    N = model.num_stages
+    for k in range(N):
+        fwd_base = {}
+        for e in res.trace[k]:
+            assert e.s == 0 and e.target == e.base_version
+            if e.dir == O.FWD:
+                assert e.base_version == max(0, e.mb - (N - k - 1))
+                fwd_base[e.mb] = e.base_version
+            else:
+                assert e.base_version == fwd_base[e.mb]
+
+
+def test_stash_single_stage_is_sequential_sgd_and_differs_from_vanilla():
+    model = sd.mlp([20, 16, 12, 5], cuts=[])
+    w0, X, Y = sd.parity_inputs(model, 6, 4, seed=4)
+    res = O.run(model, sd.widen(w0), X.astype(np.float64), Y, 0.05, 0.9, pred=O.PRED_STASH)
+    W, losses = O.sequential_momentum_sgd(model, np.concatenate(sd.widen(w0)), X, Y, 0.05, 0.9)
+    np.testing.assert_array_equal(np.concatenate(res.W), W)
+    # N = 3 with multi-layer early stages: stashing changes the backward weights
+    model = sd.mlp([20, 16, 12, 12, 5], cuts=[2, 3])
+    w0, X, Y = sd.parity_inputs(model, 8, 4, seed=5)
+    a = O.run(model, sd.widen(w0), X.astype(np.float64), Y, 0.05, 0.9, pred=O.PRED_STASH)
+    b = O.run(model, sd.widen(w0), X.astype(np.float64), Y, 0.05, 0.9, pred=O.PRED_NONE)
+    assert np.linalg.norm(np.concatenate(a.W) - np.concatenate(b.W)) > 1e-6
