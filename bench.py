@@ -47,7 +47,7 @@ def parse():
     p.add_argument("--workload", default="wide_fcn", choices=["wide_fcn", "large_fcn", "mlp", "deep_mlp", "lstm_lm", "vgg16"])
     p.add_argument("--stages", type=int, default=0, help="pipeline depth (default = --gpus); >N only with N=1")
     p.add_argument("--gemm", default=DEFAULT_GEMM, choices=["fp32x3", "tf32", "simt"])
-    p.add_argument("--pred", default="spectrain", choices=["spectrain", "none"])
+    p.add_argument("--pred", default="spectrain", choices=["spectrain", "none", "stash"])
     p.add_argument("--no-e2e", action="store_true")
     p.add_argument("--no-cpu", action="store_true")
     p.add_argument("--lr", type=float, default=1e-3)
@@ -104,6 +104,8 @@ def stage_work(model, k: int, B: int, pred: str):
     sF = (k // 2 + N - k - 1) if pred == "spectrain" else 0
     sB = (k // 2) if pred == "spectrain" else 0
     upd = 16 + (4 if sF > 0 else 0) + (4 if (sB > 0 and sB != sF) else 0)
+    if pred == "stash":  # PipeDream weight stashing: the update writes W' into the stash slot
+        upd = 20
     T = model.seq_len
     R = B * T
     byts, flops = 0.0, 0.0
@@ -289,7 +291,7 @@ def run_ours(args):
         dist.init_process_group("nccl", device_id=dev)
     model, B, wname = workload(args.workload, S)
     gemm = {"fp32x3": st.ST_GEMM_FP32X3, "tf32": st.ST_GEMM_TF32, "simt": st.ST_GEMM_SIMT}[args.gemm]
-    pred = st.ST_PRED_SPECTRAIN if args.pred == "spectrain" else st.ST_PRED_NONE
+    pred = {"spectrain": st.ST_PRED_SPECTRAIN, "none": st.ST_PRED_NONE, "stash": st.ST_PRED_STASH}[args.pred]
     kinds = {sd.DENSE: st.ST_LAYER_DENSE, sd.EMBED: st.ST_LAYER_EMBED, sd.LSTM: st.ST_LAYER_LSTM,
              sd.CONV: st.ST_LAYER_CONV, sd.POOL: st.ST_LAYER_POOL}
     layers = [(l.n_in, l.n_out, st.ST_ACT_RELU if l.act == sd.RELU else st.ST_ACT_NONE, 1 if l.bias else 0,
@@ -424,7 +426,7 @@ def run_ours(args):
     # (operand reads of dZ and X, ~B·(in+out)·8 B, are left out: < 1%).
     kb_bytes, kb_ms, kb_n, stage_ms = 0.0, 0.0, 0, 0.0
     for s, pr in zip(my_stages, profs):
-        bpp = 16 + (4 if s.sizes.s_fwd > 0 else 0) + (4 if (s.sizes.s_bwd > 0 and s.sizes.s_bwd != s.sizes.s_fwd) else 0)
+        bpp = 16 + (4 if s.sizes.wf_bytes > 0 else 0) + (4 if s.sizes.wb_bytes > 0 else 0)  # + WF / WB (or stash) writes
         ms_k, n_k = pr["gemm_dw"]
         kb_bytes += bpp * s.params * args.steps
         kb_ms += ms_k

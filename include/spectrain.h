@@ -83,7 +83,13 @@ enum { ST_LAYER_DENSE = 0, ST_LAYER_EMBED = 1, ST_LAYER_LSTM = 2, ST_LAYER_CONV 
  * POOL: 2×2 max-pool stride 2, n_in = n_out = channels, hw even; no params. The
  * per-sample activation width entering a CONV / POOL layer is hw·hw·n_in; a DENSE layer
  * after the last POOL sees the flattened NHWC vector. (SURVEY §8(a) a10, D19, D21.) */
-enum { ST_PRED_SPECTRAIN = 0, ST_PRED_NONE = 1 };
+/* ST_PRED_STASH: PipeDream weight stashing (Fig. 6c) — no
+ * prediction (s = 0); the forward of a mini-batch uses the stage's current W and its
+ * backward the same stashed copy. The WF buffer then holds the stash: N−k slots of P
+ * floats at a pitch of P rounded up to 64 (wf_bytes says how much); the update after
+ * B(mb) writes W' into B(mb)'s slot, whose next user is F(mb + N − k). Trace: a
+ * backward's base_version is the version its forward used. */
+enum { ST_PRED_SPECTRAIN = 0, ST_PRED_NONE = 1, ST_PRED_STASH = 2 };
 enum { ST_MOMENTUM_EMA = 0, ST_MOMENTUM_HEAVY_BALL = 1 };
 /* GEMM arithmetic. FP32X3 = 3xTF32 split (hi·hi + hi·lo + lo·hi) on tcgen05
  * tensor cores, fp32 accumulate in TMEM — the parity mode.
@@ -132,7 +138,7 @@ typedef struct {
   int64_t w_bytes;      /* W  — current weights */
   int64_t v_bytes;      /* V  — smoothed gradient, Eq. 1 */
   int64_t g_bytes;      /* G  — gradient of the last backward */
-  int64_t wf_bytes;     /* WF — Ŵ for the next forward (0 if s_F = 0) */
+  int64_t wf_bytes;     /* WF — Ŵ for the next forward (0 if s_F = 0); ST_PRED_STASH: the weight stash */
   int64_t wb_bytes;     /* WB — Ŵ for the next backward (0 if s_B = 0 or s_B = s_F) */
   int64_t stash_bytes;  /* activation stash: N−k slots × Σ_l B·n_in_l fp32 */
   int64_t work_bytes;   /* messages, logits, split-K workspace, counters, losses */

@@ -16,6 +16,11 @@
 using st::set_error;
 
 namespace st {
+
+// ST_PRED_STASH slot pitch: P rounded up to 64 floats (256 B), so every slot keeps the
+// alignment of the arena (the fused dW + update writes its WF block with float4 / TMA)
+static int64_t stash_pitch(int64_t P) { return (P + 63) / 64 * 64; }
+
 namespace {
 
 int64_t align_up(int64_t x, int64_t a) { return (x + a - 1) / a * a; }
@@ -67,7 +72,8 @@ st_status validate_and_layout(const st_config* c, Layout* L) {
   if (c->batch < 1) return set_error(ST_ERR_INPUT, "batch must be >= 1");
   if (!(c->lr > 0.f) || !std::isfinite(c->lr)) return set_error(ST_ERR_INPUT, "lr must be > 0");
   if (!(c->gamma > 0.f && c->gamma <= 1.f)) return set_error(ST_ERR_INPUT, "gamma must be in (0, 1]");
-  if (c->pred != ST_PRED_SPECTRAIN && c->pred != ST_PRED_NONE) return set_error(ST_ERR_INPUT, "bad pred");
+  if (c->pred != ST_PRED_SPECTRAIN && c->pred != ST_PRED_NONE && c->pred != ST_PRED_STASH)
+    return set_error(ST_ERR_INPUT, "bad pred");
   if (c->momentum != ST_MOMENTUM_EMA && c->momentum != ST_MOMENTUM_HEAVY_BALL)
     return set_error(ST_ERR_INPUT, "bad momentum");
   if (c->gemm != ST_GEMM_FP32X3 && c->gemm != ST_GEMM_TF32 && c->gemm != ST_GEMM_SIMT)
@@ -190,8 +196,9 @@ st_status validate_and_layout(const st_config* c, Layout* L) {
   L->slot_elems = soff;
   L->in_first = (int)layer_win(c->layers[l0]);
   L->out_last = (int)layer_wout(c->layers[l1 - 1]);
-  L->sF = c->pred == ST_PRED_NONE ? 0 : version_difference(k, N, ST_FWD);
-  L->sB = c->pred == ST_PRED_NONE ? 0 : version_difference(k, N, ST_BWD);
+  const bool no_pred = c->pred == ST_PRED_NONE || c->pred == ST_PRED_STASH;
+  L->sF = no_pred ? 0 : version_difference(k, N, ST_FWD);
+  L->sB = no_pred ? 0 : version_difference(k, N, ST_BWD);
 
   // work carve-up
   int64_t w = 0;
@@ -248,7 +255,8 @@ st_status validate_and_layout(const st_config* c, Layout* L) {
   st_sizes& z = L->sizes;
   z.params = L->P;
   z.w_bytes = z.v_bytes = z.g_bytes = align_up(L->P * 4, kAlignBytes);
-  z.wf_bytes = L->sF > 0 ? z.w_bytes : 0;
+  // ST_PRED_STASH: WF is the weight stash, one W copy per mini-batch in flight (N−k slots)
+  z.wf_bytes = c->pred == ST_PRED_STASH ? stash_pitch(L->P) * 4 * L->S : (L->sF > 0 ? z.w_bytes : 0);
   z.wb_bytes = (L->sB > 0 && L->sB != L->sF) ? z.w_bytes : 0;
   z.stash_bytes = (int64_t)L->S * L->slot_elems * 4;
   z.work_bytes = w;
@@ -313,7 +321,7 @@ st_status ctx_init(const st_config* cfg, const st_buffers* bufs, void* stream, s
   ST_TRY(validate_and_layout(cfg, &L));
   if (!bufs || !bufs->W || !bufs->V || !bufs->G || !bufs->stash || !bufs->work)
     return set_error(ST_ERR_INPUT, "missing buffer (W, V, G, stash, work are required)");
-  if (L.sizes.wf_bytes && !bufs->WF) return set_error(ST_ERR_INPUT, "WF buffer required (s_F = %d)", L.sF);
+  if (L.sizes.wf_bytes && !bufs->WF) return set_error(ST_ERR_INPUT, "WF buffer required (s_F = %d / stash)", L.sF);
   if (L.sizes.wb_bytes && !bufs->WB) return set_error(ST_ERR_INPUT, "WB buffer required (s_B = %d)", L.sB);
   auto misaligned = [](const void* p) { return p && ((uintptr_t)p % kAlignBytes) != 0; };
   if (misaligned(bufs->W) || misaligned(bufs->V) || misaligned(bufs->G) || misaligned(bufs->WF) ||
@@ -355,6 +363,8 @@ st_status ctx_init(const st_config* cfg, const st_buffers* bufs, void* stream, s
   c->WB_out = (L.sB > 0 && L.sB != L.sF) ? bufs->WB : nullptr;
   c->WF = L.sF > 0 ? bufs->WF : bufs->W;
   c->WB = L.sB == 0 ? bufs->W : (L.sB == L.sF ? c->WF : bufs->WB);
+  c->wstash = c->pred == ST_PRED_STASH ? bufs->WF : nullptr;
+  c->stash_ver.assign((size_t)L.S, 0);
   c->stash = static_cast<float*>(bufs->stash);
   c->slot_elems = L.slot_elems;
   c->S = L.S;
@@ -458,6 +468,8 @@ st_status ctx_set_params(st_ctx* c, const float* host, size_t n) {
   if (n) ST_CUDA_TRY(cudaMemcpyAsync(c->W, host, n * 4, cudaMemcpyHostToDevice, c->stream));
   ST_CUDA_TRY(cudaMemsetAsync(c->V, 0, n * 4, c->stream));
   if (c->WF_out) ST_CUDA_TRY(cudaMemcpyAsync(c->WF_out, c->W, n * 4, cudaMemcpyDeviceToDevice, c->stream));
+  for (int slot = 0; c->wstash && slot < c->S; ++slot)  // every in-flight forward before the first update sees W0
+    ST_CUDA_TRY(cudaMemcpyAsync(c->wstash + (size_t)slot * stash_pitch(c->P), c->W, n * 4, cudaMemcpyDeviceToDevice, c->stream));
   if (c->WB_out) ST_CUDA_TRY(cudaMemcpyAsync(c->WB_out, c->W, n * 4, cudaMemcpyDeviceToDevice, c->stream));
   ST_CUDA_TRY(cudaMemsetAsync(c->losses_dev, 0xff, (size_t)c->max_mb * 4, c->stream));
   ST_CUDA_TRY(cudaStreamSynchronize(c->stream));
@@ -614,7 +626,9 @@ static st_status lstm_forward(st_ctx* c, const LayerInfo& L, const float* Wh, co
 static st_status forward_compute(st_ctx* c, int64_t mb, const float* x_dev, const int32_t* y_dev, bool host_io,
                                  float* loss_host) {
   float* slot = c->stash + (size_t)(mb % c->S) * c->slot_elems;
-  const float* Wh = c->WF;  // Eq. 4 with s_F (aliases W when s_F = 0)
+  // Eq. 4 with s_F (aliases W when s_F = 0); weight stashing: this mini-batch's stash slot,
+  // written with the current W by the update that preceded this forward (or W0)
+  const float* Wh = c->wstash ? c->wstash + (size_t)(mb % c->S) * stash_pitch(c->P) : c->WF;
   if (c->first_stage) {
     if (!x_dev) return set_error(ST_ERR_INPUT, "stage 0 forward needs x");
     const size_t bytes = c->embed_first ? (size_t)c->R * 4 : (size_t)c->R * c->in_first * 4;
@@ -760,7 +774,11 @@ static st_status lstm_backward(st_ctx* c, const LayerInfo& L, const float* Wh, c
 static st_status backward_compute(st_ctx* c, int64_t mb, bool fused = false) {
   const UpdateConsts kc = make_update_consts(c->lr, c->gamma, c->sF, c->sB, c->momentum);
   float* slot = c->stash + (size_t)(mb % c->S) * c->slot_elems;
-  const float* Wh = c->WB;  // Eq. 4 with s_B (D5: re-predicted from the current state)
+  // Eq. 4 with s_B (D5: re-predicted from the current state); weight stashing: the
+  // forward's copy. The update after this backward refills the same slot with W' for the
+  // next forward, F(mb + N − k), which is the slot's next user.
+  const float* Wh = c->wstash ? c->wstash + (size_t)(mb % c->S) * stash_pitch(c->P) : c->WB;
+  if (c->wstash) c->WF_out = c->wstash + (size_t)(mb % c->S) * stash_pitch(c->P);
   const float* dZ = c->last_stage ? c->dlogits : c->recv_bwd;
   const int nl = (int)c->layers.size();
   // Gradient buffers rotate over 3 so that the dW + update of layer l (side stream,
@@ -940,6 +958,10 @@ static st_status run_task(st_ctx* c, const float* x_dev, const int32_t* y_dev, b
   e.dir = t.dir;
   e.mb = t.mb;
   e.base_version = c->version;
+  if (c->wstash) {  // the backward records the version its forward used (the stashed copy)
+    if (t.dir == ST_FWD) c->stash_ver[(size_t)(t.mb % c->S)] = c->version;
+    else e.base_version = c->stash_ver[(size_t)(t.mb % c->S)];
+  }
   e.s = t.dir == ST_FWD ? c->sF : c->sB;
   e.target = e.base_version + e.s;
   c->trace.push_back(e);

@@ -138,6 +138,8 @@ struct st_ctx {
   int32_t* y_stage = nullptr;   // [R] labels staged from host (st_run_host)
   float* lstm_rec = nullptr;    // [B × 4H] h_{t−1}·W_hh
   float* lstm_dh = nullptr;     // [B × H] dh_next
+  float* wstash = nullptr;      // ST_PRED_STASH: S slots of P floats (the WF buffer)
+  std::vector<int64_t> stash_ver;  // ST_PRED_STASH: version each slot's forward used
   float* lstm_hlo = nullptr;    // [B × H] tf32 lo of h_{t−1} (3xTF32 operand of the recurrent GEMM)
   float* lstm_dglo = nullptr;   // [B × 4H] tf32 lo of dG_t (operand of the dh GEMM)
   float* lstm_dc = nullptr;     // [B × H] dc_next

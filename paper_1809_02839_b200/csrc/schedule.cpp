@@ -46,8 +46,10 @@ std::vector<st_event> program_events(int N, int k, int64_t M, int pred) {
   std::vector<st_event> ev;
   ev.reserve(p.size());
   int64_t version = 0;
-  const int64_t sF = pred == ST_PRED_NONE ? 0 : version_difference(k, N, ST_FWD);
-  const int64_t sB = pred == ST_PRED_NONE ? 0 : version_difference(k, N, ST_BWD);
+  const bool no_pred = pred == ST_PRED_NONE || pred == ST_PRED_STASH;
+  const int64_t sF = no_pred ? 0 : version_difference(k, N, ST_FWD);
+  const int64_t sB = no_pred ? 0 : version_difference(k, N, ST_BWD);
+  std::vector<int64_t> fwd_version((size_t)std::max<int64_t>(M, 0), 0);  // ST_PRED_STASH
   for (size_t n = 0; n < p.size(); ++n) {
     st_event e{};
     e.stage = k;
@@ -55,6 +57,10 @@ std::vector<st_event> program_events(int N, int k, int64_t M, int pred) {
     e.dir = p[n].dir;
     e.mb = p[n].mb;
     e.base_version = version;
+    if (pred == ST_PRED_STASH) {  // a backward runs on the weights its forward stashed
+      if (p[n].dir == ST_FWD) fwd_version[(size_t)p[n].mb] = version;
+      else e.base_version = fwd_version[(size_t)p[n].mb];
+    }
     e.s = p[n].dir == ST_FWD ? sF : sB;
     e.target = e.base_version + e.s;
     ev.push_back(e);

@@ -31,7 +31,7 @@ def gemm_mode(st):
 
 def _parity(st, model, batch, M, lr, seed=0, pred=O.PRED_SPECTRAIN, momentum=O.MOMENTUM_EMA, labels="teacher"):
     w0, X, Y = sd.parity_inputs(model, M, batch, seed, labels)
-    cpred = st.ST_PRED_SPECTRAIN if pred == O.PRED_SPECTRAIN else st.ST_PRED_NONE
+    cpred = {O.PRED_SPECTRAIN: st.ST_PRED_SPECTRAIN, O.PRED_NONE: st.ST_PRED_NONE, O.PRED_STASH: st.ST_PRED_STASH}[pred]
     cmom = st.ST_MOMENTUM_EMA if momentum == O.MOMENTUM_EMA else st.ST_MOMENTUM_HEAVY_BALL
     stages = build_pipeline(model, batch, lr, pred=cpred, momentum=cmom, gemm=gemm_mode(st), max_mb=M)
     try:
@@ -78,6 +78,21 @@ def test_vanilla_and_heavy_ball(st):
     res, ref = _parity(st, model, 32, 20, 0.05, pred=O.PRED_NONE)
     assert all(e[5] == 0 for tr in res[3] for e in tr)
     _parity(st, model, 32, 20, 0.02, momentum=O.MOMENTUM_HEAVY_BALL)
+
+
+def test_weight_stashing(st):
+    """PipeDream weight stashing (NEXT-2): each backward runs on its forward's
+    stashed weights; the update refills that slot for the next forward. Trace bit-exact
+    (a backward records its forward's version), W / loss within the gate — 3 and 4 stages
+    with multi-layer early stages (fused dW + update writing the stash slot), ragged
+    widths (unfused K-B fallback) and M < N."""
+    model = sd.mlp([784, 128, 96, 64, 10], cuts=[2, 3])
+    res, ref = _parity(st, model, 32, 20, 0.05, pred=O.PRED_STASH)
+    assert all(e[5] == 0 for tr in res[3] for e in tr)
+    _parity(st, sd.mlp([784, 160, 128, 96, 64, 10], cuts=[2, 3, 4]), 24, 20, 0.05, seed=2, pred=O.PRED_STASH)
+    model = sd.mlp([77, 45, 31, 29, 13, 5], cuts=[2, 4])
+    _parity(st, model, 7, 11, 0.05, seed=7, pred=O.PRED_STASH)
+    _parity(st, model, 7, 2, 0.05, seed=8, pred=O.PRED_STASH)
 
 
 def test_ragged_shapes_and_M_smaller_than_depth(st):
