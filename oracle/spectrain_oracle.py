@@ -84,6 +84,16 @@ def predict(W: np.ndarray, v: np.ndarray, s: int, eta: float) -> np.ndarray:
     return W - s * eta * v
 
 
+
+def prediction_rmse(W_old: np.ndarray, V_old: np.ndarray, W_now: np.ndarray, s: int, eta: float):
+    """Prediction accuracy (Fig. 7): with (W_old, V_old) the stage state s
+    updates before W_now (V_old = the smoothed gradient stored next to W_old, i.e.
+    v_{t−s−1} in the paper's indexing, D4), the predicted weights are
+    Ŵ_t = W_old − s·η·V_old (Eq. 4) and the stale ones W_{t−s} = W_old. Returns
+    (RMSE(Ŵ_t, W_t), RMSE(W_{t−s}, W_t)) over all elements."""
+    W_hat = predict(W_old, V_old, s, eta)
+    return float(np.sqrt(np.mean((W_hat - W_now) ** 2))), float(np.sqrt(np.mean((W_old - W_now) ** 2)))
+
 # --------------------------------------------------------------------------
 # §3.1 schedule: PipeDream 1F1B round-robin (P:210-213), D8
 # --------------------------------------------------------------------------

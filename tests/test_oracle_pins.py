@@ -625,3 +625,35 @@ def test_stash_single_stage_is_sequential_sgd_and_differs_from_vanilla():
     a = O.run(model, sd.widen(w0), X.astype(np.float64), Y, 0.05, 0.9, pred=O.PRED_STASH)
     b = O.run(model, sd.widen(w0), X.astype(np.float64), Y, 0.05, 0.9, pred=O.PRED_NONE)
     assert np.linalg.norm(np.concatenate(a.W) - np.concatenate(b.W)) > 1e-6
+
+
+# ---------------------------------------------------------------- Fig. 7 prediction accuracy (NEXT-2)
+
+def test_prediction_rmse_closed_forms():
+    """A constant gradient g with γ = 0 makes v = g after one step, so the weights move by
+    exactly η·g per update: the prediction W_{t−s} − sηv is exact (RMSE 0) and the stale
+    weights are off by sηg (RMSE = sη·rms(g)). With γ > 0, v → g geometrically, so the
+    prediction error decays to 0 while the stale error stays sη·rms(g)."""
+    rng = np.random.default_rng(0)
+    g = rng.standard_normal(50)
+    eta = 0.1
+    for gamma, exact in ((0.0, True), (0.9, False)):
+        W, V = np.zeros(50), np.zeros(50)
+        hist = [(W.copy(), V.copy())]
+        for _ in range(200):
+            V = O.update_smoothed(V, g, gamma)
+            W = W - eta * V
+            hist.append((W.copy(), V.copy()))
+        for s_ in (1, 2, 3):
+            t = len(hist) - 1
+            rp, rs = O.prediction_rmse(hist[t - s_][0], hist[t - s_][1], hist[t][0], s_, eta)
+            np.testing.assert_allclose(rs, s_ * eta * np.sqrt(np.mean(g ** 2)), rtol=1e-6 if not exact else 1e-12)
+            assert rp < 1e-9 * rs
+        # early on (t = 3, γ = 0.9: v far from g) the prediction is worse than at the end
+        if not exact:
+            rp_early, _ = O.prediction_rmse(hist[2][0], hist[2][1], hist[3][0], 1, eta)
+            assert rp_early > 1e-3
+    # s = 0: both errors are the plain distance
+    a, b = rng.standard_normal(7), rng.standard_normal(7)
+    rp, rs = O.prediction_rmse(a, rng.standard_normal(7), b, 0, 0.1)
+    assert rp == rs == pytest.approx(np.sqrt(np.mean((a - b) ** 2)), rel=1e-15)
