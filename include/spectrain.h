@@ -301,6 +301,17 @@ ST_API int64_t st_kernel_launches(st_ctx* ctx);
 
 /* ---- raw kernels (test and bench hooks on caller arenas) --------------------- */
 
+/* Prediction accuracy of Fig. 7. W_old / V_old: a
+ * stage's weights and stored smoothed gradient s updates before W_now (device fp32,
+ * n elements each). out_host[0] = Σ (W_old − s·lr·V_old − W_now)² (the Eq. 4
+ * prediction's error), out_host[1] = Σ (W_old − W_now)² (the stale weights' error), both
+ * accumulated in fp64 in a fixed order (RMSE = sqrt(sum / n)). work: device scratch of
+ * st_prediction_error_work_bytes() bytes, 8-byte aligned. Stream-ordered, then syncs the
+ * stream to return the sums. Errors: ST_ERR_INPUT (NULL buffer, s < 0), ST_ERR_CUDA. */
+ST_API int64_t st_prediction_error_work_bytes(void);
+ST_API st_status st_prediction_error_raw(const float* W_old, const float* V_old, const float* W_now, size_t n, int s,
+                                         float lr, double* out_host, void* work, void* stream);
+
 /* K-B on caller arenas of n fp32: v' = γv + (1−γ)g (HEAVY_BALL: γv + g),
  * w' = w − η v', WF = w' − s_F η v' (if WF ≠ NULL), WB = w' − s_B η v' (if WB ≠ NULL).
  * All pointers 16-byte aligned device pointers; n = 0 is a no-op.

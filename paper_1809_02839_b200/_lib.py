@@ -114,6 +114,8 @@ def _load() -> ctypes.CDLL:
         "st_get_profile": (S, [P, P, P]),
         "st_kernel_launches": (I64, [P]),
         "st_update_predict_raw": (S, [P, P, P, P, P, U, F, F, I, I, I, P]),
+        "st_prediction_error_work_bytes": (I64, []),
+        "st_prediction_error_raw": (S, [P, P, P, U, I, F, ctypes.POINTER(ctypes.c_double), P, P]),
         "st_gemm_raw": (S, [I, I, I, I, I, P, P, P, P, P, I, P, P]),
         "st_gemm_workspace_bytes": (I64, [I, I, I]),
         "st_softmax_ce_raw": (S, [P, P, I, I, P, P, P, P]),
@@ -133,7 +135,7 @@ EXPORTED = ("st_version_difference", "st_program", "st_comm_plan", "st_query_siz
             "st_connect_local", "st_destroy", "st_set_params", "st_get_params", "st_stage_forward",
             "st_stage_backward", "st_predict_and_update", "st_step", "st_run", "st_run_host", "st_run_group", "st_get_trace",
             "st_losses_device", "st_sync", "st_set_profiling", "st_get_profile", "st_kernel_launches",
-            "st_update_predict_raw", "st_gemm_raw", "st_gemm_workspace_bytes", "st_softmax_ce_raw", "st_dw_update_raw",
+            "st_update_predict_raw", "st_prediction_error_work_bytes", "st_prediction_error_raw", "st_gemm_raw", "st_gemm_workspace_bytes", "st_softmax_ce_raw", "st_dw_update_raw",
             "st_last_error", "st_version")
 
 

@@ -221,6 +221,26 @@ st_status st_update_predict_raw(float* W, float* V, const float* G, float* WF, f
   })
 }
 
+int64_t st_prediction_error_work_bytes(void) { return prediction_error_work_bytes(); }
+
+st_status st_prediction_error_raw(const float* W_old, const float* V_old, const float* W_now, size_t n, int s,
+                                  float lr, double* out_host, void* work, void* stream) {
+  GUARD({
+    if (!out_host) return set_error(ST_ERR_INPUT, "prediction_error_raw: out_host required");
+    out_host[0] = out_host[1] = 0.0;
+    if (n == 0) return ST_OK;
+    if (!W_old || !V_old || !W_now || !work) return set_error(ST_ERR_INPUT, "prediction_error_raw: NULL buffer");
+    if (s < 0) return set_error(ST_ERR_INPUT, "prediction_error_raw: s must be >= 0");
+    cudaStream_t st = static_cast<cudaStream_t>(stream);
+    double* w = static_cast<double*>(work);
+    ST_TRY(launch_prediction_error(W_old, V_old, W_now, n, (double)s * (double)lr, w, st));
+    const int64_t off = prediction_error_work_bytes() / 8 - 2;
+    ST_CUDA_TRY(cudaMemcpyAsync(out_host, w + off, 2 * sizeof(double), cudaMemcpyDeviceToHost, st));
+    ST_CUDA_TRY(cudaStreamSynchronize(st));
+    return ST_OK;
+  })
+}
+
 int64_t st_gemm_workspace_bytes(int B, int n_in, int n_out) { return gemm_workspace_bytes(B, n_in, n_out); }
 
 st_status st_gemm_raw(int op, int gemm_mode, int B, int n_in, int n_out, const float* a, const float* b,

@@ -180,3 +180,69 @@ st_status launch_bias_grad_update(const float* dZ, int B, int n_out, const Updat
 }
 
 }  // namespace st
+
+// ---- Fig. 7 prediction accuracy -----------------------
+// e_pred = W_old − s·η·V_old − W_now (Eq. 4 prediction vs the actual weights s updates
+// later), e_stale = W_old − W_now; Σ e² of both in fp64. Pass 1: CTA b sums a fixed
+// contiguous chunk (per-thread strided sums, then a fixed smem tree); pass 2: one thread
+// adds the CTA partials in order — deterministic for a given n.
+namespace st {
+namespace {
+
+constexpr int kErrBlocks = 592;
+
+__global__ void __launch_bounds__(256) pred_err_partial_kernel(const float* __restrict__ Wo,
+                                                               const float* __restrict__ Vo,
+                                                               const float* __restrict__ Wn, size_t n, double c,
+                                                               double* __restrict__ part) {
+  __shared__ double sp[256], ss[256];
+  const size_t chunk = (n + gridDim.x - 1) / gridDim.x;
+  const size_t i0 = (size_t)blockIdx.x * chunk, i1 = min(n, i0 + chunk);
+  double ap = 0.0, as = 0.0;
+  for (size_t i = i0 + threadIdx.x; i < i1; i += blockDim.x) {
+    const double wo = Wo[i], wn = Wn[i];
+    const double ep = (wo - c * (double)Vo[i]) - wn, es = wo - wn;
+    ap += ep * ep;
+    as += es * es;
+  }
+  sp[threadIdx.x] = ap;
+  ss[threadIdx.x] = as;
+  __syncthreads();
+  for (int h = 128; h > 0; h >>= 1) {
+    if (threadIdx.x < h) {
+      sp[threadIdx.x] += sp[threadIdx.x + h];
+      ss[threadIdx.x] += ss[threadIdx.x + h];
+    }
+    __syncthreads();
+  }
+  if (threadIdx.x == 0) {
+    part[2 * blockIdx.x] = sp[0];
+    part[2 * blockIdx.x + 1] = ss[0];
+  }
+}
+
+__global__ void pred_err_final_kernel(const double* __restrict__ part, int nb, double* __restrict__ out) {
+  if (threadIdx.x != 0 || blockIdx.x != 0) return;
+  double p = 0.0, q = 0.0;
+  for (int b = 0; b < nb; ++b) {
+    p += part[2 * b];
+    q += part[2 * b + 1];
+  }
+  out[0] = p;
+  out[1] = q;
+}
+
+}  // namespace
+
+int64_t prediction_error_work_bytes() { return (int64_t)(2 * kErrBlocks + 2) * 8; }
+
+st_status launch_prediction_error(const float* W_old, const float* V_old, const float* W_now, size_t n, double s_eta,
+                                  double* work, cudaStream_t s) {
+  const int nb = (int)std::min<size_t>(kErrBlocks, std::max<size_t>(1, (n + 255) / 256));
+  pred_err_partial_kernel<<<nb, 256, 0, s>>>(W_old, V_old, W_now, n, s_eta, work);
+  pred_err_final_kernel<<<1, 32, 0, s>>>(work, nb, work + 2 * kErrBlocks);
+  ST_CUDA_TRY(cudaGetLastError());
+  return ST_OK;
+}
+
+}  // namespace st

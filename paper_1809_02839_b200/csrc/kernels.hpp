@@ -19,6 +19,12 @@ UpdateConsts make_update_consts(float lr, float gamma, int sF, int sB, int momen
 st_status launch_update_predict(float* W, float* V, const float* G, float* WF, float* WB, size_t n,
                                 const UpdateConsts& c, cudaStream_t s);
 
+// Fig. 7 prediction accuracy: work[2·592] partials, then work[2·592 + 0/1] =
+// Σ (W_old − s_eta·V_old − W_now)², Σ (W_old − W_now)² (fp64, deterministic order).
+int64_t prediction_error_work_bytes();
+st_status launch_prediction_error(const float* W_old, const float* V_old, const float* W_now, size_t n, double s_eta,
+                                  double* work, cudaStream_t s);
+
 // In-place K-B targets of one parameter block (a layer's weight matrix or bias):
 // pointers at the block's offset in the stage arenas; WF / WB NULL when aliased.
 struct UpdateArgs {

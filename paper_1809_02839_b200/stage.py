@@ -180,6 +180,17 @@ def update_predict_raw(W: torch.Tensor, V: torch.Tensor, G: torch.Tensor, WF: Op
                                     momentum, ctypes.c_void_p(st.cuda_stream)))
 
 
+def prediction_error_raw(W_old: torch.Tensor, V_old: torch.Tensor, W_now: torch.Tensor, s: int, lr: float,
+                         stream: Optional[torch.cuda.Stream] = None) -> Tuple[float, float]:
+    """Fig. 7 (P:346-355): (Σ (W_old − s·lr·V_old − W_now)², Σ (W_old − W_now)²), fp64."""
+    st = stream or torch.cuda.current_stream(W_old.device)
+    work = torch.empty(int(lib.st_prediction_error_work_bytes()), dtype=torch.uint8, device=W_old.device)
+    out = (ctypes.c_double * 2)()
+    check(lib.st_prediction_error_raw(_ptr(W_old), _ptr(V_old), _ptr(W_now), W_old.numel(), s, lr, out, _ptr(work),
+                                      ctypes.c_void_p(st.cuda_stream)))
+    return float(out[0]), float(out[1])
+
+
 def gemm_raw(op: int, mode: int, B: int, n_in: int, n_out: int, a: torch.Tensor, b: torch.Tensor,
              aux: Optional[torch.Tensor], aux_out: Optional[torch.Tensor], out: torch.Tensor, relu: bool = False,
              work: Optional[torch.Tensor] = None, stream: Optional[torch.cuda.Stream] = None) -> None:

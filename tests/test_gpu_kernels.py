@@ -1,5 +1,6 @@
 """Kernel-level parity on the GPU (-m gpu): K-B fused update/prediction, the
 stage GEMMs and softmax-CE against NumPy (fp64 / exact-product emulation)."""
+import math
 import numpy as np
 import pytest
 import torch
@@ -187,3 +188,25 @@ def test_dw_update_fused_vs_fp64(st, mode, B, n_in, n_out, sF, sB):
     if tB is not None:
         ref = O.predict(w64, v64, sB, lr)
         assert np.all(np.abs(tB.cpu().numpy() - ref) <= (sB + 1) * lr * tol_v + 4e-7 * np.abs(ref))
+
+
+@pytest.mark.parametrize("n", [0, 5, 1_000_003])
+def test_prediction_error_kernel_vs_oracle(st, n):
+    """Fig. 7 prediction-accuracy sums against the oracle's RMSE on the same
+    fp32 arrays (fp64 accumulation on both sides; only the summation order differs)."""
+    rng = np.random.default_rng(n)
+    Wo = rng.standard_normal(n).astype(np.float32)
+    Vo = (0.1 * rng.standard_normal(n)).astype(np.float32)
+    Wn = (Wo - 0.02 * rng.standard_normal(n)).astype(np.float32)
+    lr = 0.05
+    dev = torch.device("cuda", 0)
+    t = [torch.from_numpy(a).to(dev) for a in (Wo, Vo, Wn)]
+    for s_ in (0, 1, 2, 3):
+        sp, ss = st.prediction_error_raw(t[0], t[1], t[2], s_, lr)
+        if n == 0:
+            assert sp == ss == 0.0
+            continue
+        rp, rs = O.prediction_rmse(Wo.astype(np.float64), Vo.astype(np.float64), Wn.astype(np.float64), s_,
+                                   float(np.float32(lr)))
+        assert math.sqrt(sp / n) == pytest.approx(rp, rel=1e-12)
+        assert math.sqrt(ss / n) == pytest.approx(rs, rel=1e-12)
