@@ -51,6 +51,8 @@ def parse():
     p.add_argument("--no-e2e", action="store_true")
     p.add_argument("--no-cpu", action="store_true")
     p.add_argument("--lr", type=float, default=1e-3)
+    p.add_argument("--parallel", default="pp", choices=["pp", "dp"],
+                   help="pp: the SpecTrain pipeline (default); dp: the data-parallel comparator (NEXT-1)")
     return p.parse_args()
 
 
@@ -269,6 +271,109 @@ def run_reference(args):
 
 # ----------------------------------------------------------------------------- GPU arm
 
+def init_params(s, layers, dev, g):
+    """Bench-only device-side Glorot / embedding / LSTM init of one stage's arena."""
+    import torch
+    import synthdata as sd
+    w = torch.empty(s.params, device=dev)
+    off = 0
+    for L in layers:
+        if L.kind == sd.POOL:
+            pass
+        elif L.kind == sd.CONV:
+            r = (6.0 / (9 * L.n_in + 9 * L.n_out)) ** 0.5
+            w[off:off + 9 * L.n_in * L.n_out].uniform_(-r, r, generator=g)
+            w[off + 9 * L.n_in * L.n_out:off + L.n_params].zero_()
+        elif L.kind == sd.EMBED:
+            w[off:off + L.n_params].uniform_(-0.1, 0.1, generator=g)
+        elif L.kind == sd.LSTM:
+            h = L.n_out
+            r1, r2 = (6.0 / (L.n_in + 4 * h)) ** 0.5, (6.0 / (5 * h)) ** 0.5
+            w[off:off + L.n_in * 4 * h].uniform_(-r1, r1, generator=g)
+            w[off + L.n_in * 4 * h:off + (L.n_in + h) * 4 * h].uniform_(-r2, r2, generator=g)
+            w[off + (L.n_in + h) * 4 * h:off + L.n_params].zero_()
+        else:
+            r = (6.0 / (L.n_in + L.n_out)) ** 0.5
+            w[off:off + L.n_in * L.n_out].uniform_(-r, r, generator=g)
+            w[off + L.n_in * L.n_out:off + L.n_params].zero_()
+        off += L.n_params
+    s.set_params(w.cpu().numpy())
+    del w
+
+
+def run_dp(args):
+    """NEXT-1 comparator (paper_1809_02839_b200/dp.py): N data-parallel replicas of the
+    whole model, per-rank batch B (weak scaling: global batch N·B), G averaged by an
+    NCCL all-reduce (one bucket) before the K-B update; s ≡ 0."""
+    import torch
+    import torch.distributed as dist
+
+    import paper_1809_02839_b200 as st
+    import synthdata as sd
+    from paper_1809_02839_b200.dp import DataParallelStage
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    N = args.gpus
+    if world != N:
+        raise SystemExit(f"--gpus {N} but WORLD_SIZE={world}: launch N>1 with torchrun")
+    torch.cuda.set_device(local)
+    dev = torch.device("cuda", local)
+    if N > 1:
+        dist.init_process_group("nccl", device_id=dev)
+    model, B, wname = workload(args.workload, 1)
+    if model.seq_len != 1 or any(l.kind != sd.DENSE for l in model.layers):
+        raise SystemExit("--parallel dp: dense workloads only")
+    layers = [(l.n_in, l.n_out, st.ST_ACT_RELU if l.act == sd.RELU else st.ST_ACT_NONE, 1 if l.bias else 0)
+              for l in model.layers]
+    K, W_ = args.steps, args.warmup
+    r = DataParallelStage(layers, B, args.lr, 0.9, device=local, max_minibatches=K + W_)
+    g = torch.Generator(device=dev)
+    g.manual_seed(1234)  # identical replicas
+    init_params(r.stage, model.layers, dev, g)
+    g.manual_seed(99 + rank)  # each rank its own shard
+    xs = torch.rand(K + W_, B, model.layers[0].n_in, device=dev, generator=g)
+    ys = torch.randint(0, model.layers[-1].n_out, (K + W_, B), device=dev, dtype=torch.int32, generator=g)
+
+    def barrier():
+        torch.cuda.synchronize()
+        if N > 1:
+            dist.barrier()
+        torch.cuda.synchronize()
+
+    for i in range(W_):
+        r.step(xs[i], ys[i])
+    barrier()
+    l0 = r.stage.kernel_launches()
+    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    sampler = ClockSampler(local)
+    with sampler:
+        e0.record(r.stream)
+        for i in range(W_, W_ + K):
+            r.step(xs[i], ys[i])
+        e1.record(r.stream)
+        torch.cuda.synchronize()
+    ms = e0.elapsed_time(e1)
+    launches = r.stage.kernel_launches() - l0
+    if N > 1:
+        t = torch.tensor([ms], device=dev, dtype=torch.float64)
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        ms = float(t.item())
+    value = N * B * K / (ms / 1e3)
+    if rank == 0:
+        print(json.dumps({
+            "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": N, "steps": K, "warmup": W_,
+            "ms_per_step": ms / K, "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f32",
+            "data": "synthetic",
+            "config": {"workload": wname, "parallelism": f"dp{N}", "batch_per_rank": B, "global_batch": N * B,
+                       "gemm": args.gemm, "allreduce": "one NCCL all-reduce (AVG) of the whole G per step",
+                       "role": "NEXT-1 comparator (data parallelism on the same kernels), not the headline"},
+            "gpu_launches": launches, "clocks": sampler.summary()}), flush=True)
+    r.close()
+    if N > 1:
+        dist.destroy_process_group()
+
+
 def run_ours(args):
     import torch
     import torch.distributed as dist
@@ -319,30 +424,7 @@ def run_ours(args):
     g = torch.Generator(device=dev)
     g.manual_seed(1234 + rank)
     for s in my_stages:
-        w = torch.empty(s.params, device=dev)
-        off = 0
-        for L in model.stage_layers(s.k):
-            if L.kind == sd.POOL:
-                pass
-            elif L.kind == sd.CONV:
-                r = (6.0 / (9 * L.n_in + 9 * L.n_out)) ** 0.5
-                w[off:off + 9 * L.n_in * L.n_out].uniform_(-r, r, generator=g)
-                w[off + 9 * L.n_in * L.n_out:off + L.n_params].zero_()
-            elif L.kind == sd.EMBED:
-                w[off:off + L.n_params].uniform_(-0.1, 0.1, generator=g)
-            elif L.kind == sd.LSTM:
-                h = L.n_out
-                r1, r2 = (6.0 / (L.n_in + 4 * h)) ** 0.5, (6.0 / (5 * h)) ** 0.5
-                w[off:off + L.n_in * 4 * h].uniform_(-r1, r1, generator=g)
-                w[off + L.n_in * 4 * h:off + (L.n_in + h) * 4 * h].uniform_(-r2, r2, generator=g)
-                w[off + (L.n_in + h) * 4 * h:off + L.n_params].zero_()
-            else:
-                r = (6.0 / (L.n_in + L.n_out)) ** 0.5
-                w[off:off + L.n_in * L.n_out].uniform_(-r, r, generator=g)
-                w[off + L.n_in * L.n_out:off + L.n_params].zero_()
-            off += L.n_params
-        s.set_params(w.cpu().numpy())
-        del w
+        init_params(s, model.stage_layers(s.k), dev, g)
     n_in, n_cls = model.layers[0].width_in, model.layers[-1].n_out
     first = my_stages[0].is_first
     last = my_stages[-1].is_last
@@ -543,6 +625,8 @@ def main():
     faulthandler.dump_traceback_later(float(os.environ.get("ST_BENCH_WATCHDOG_S", "240")), repeat=True)
     if args.impl == "reference":
         run_reference(args)
+    elif args.parallel == "dp":
+        run_dp(args)
     else:
         run_ours(args)
 

@@ -657,3 +657,31 @@ def test_prediction_rmse_closed_forms():
     a, b = rng.standard_normal(7), rng.standard_normal(7)
     rp, rs = O.prediction_rmse(a, rng.standard_normal(7), b, 0, 0.1)
     assert rp == rs == pytest.approx(np.sqrt(np.mean((a - b) ** 2)), rel=1e-15)
+
+
+# ---------------------------------------------------------------- data-parallel comparator (NEXT-1)
+
+def test_data_parallel_equals_global_batch_sgd():
+    """Reading D23: averaging the batch-mean gradients of equal shards is the gradient of
+    the global batch mean, so 2-way data parallelism (each replica: forward + backward on
+    its half, gradients averaged, the same Eq. 1 / D1 update) equals the oracle's 1-stage
+    run on the whole batch — checked with the oracle's per-stage building blocks."""
+    model = sd.mlp([20, 16, 12, 5], cuts=[])
+    w0, X, Y = sd.parity_inputs(model, 6, 8, seed=9)
+    W = np.concatenate(sd.widen(w0))
+    V = np.zeros_like(W)
+    losses = []
+    for i in range(X.shape[0]):
+        gs, ls = [], []
+        for half in (slice(0, 4), slice(4, 8)):
+            out, stash = O.stage_forward(model.layers, W, X[i][half].astype(np.float64))
+            loss, dZ = O.loss_and_grad(model.loss, out, Y[i][half])
+            g, _ = O.stage_backward(model.layers, W, stash, dZ, need_dA_in=False)
+            gs.append(g)
+            ls.append(loss)
+        V = O.update_smoothed(V, 0.5 * (gs[0] + gs[1]), 0.9)
+        W = O.apply_update(W, V, None, 0.05, O.APPLY_MOMENTUM)
+        losses.append(0.5 * (ls[0] + ls[1]))
+    ref = O.run(model, sd.widen(w0), X.astype(np.float64), Y, 0.05, 0.9)
+    np.testing.assert_allclose(W, np.concatenate(ref.W), rtol=0, atol=1e-13)
+    np.testing.assert_allclose(losses, ref.losses, rtol=1e-13)
