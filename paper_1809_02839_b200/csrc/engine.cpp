@@ -787,6 +787,7 @@ static st_status backward_compute(st_ctx* c, int64_t mb, bool fused = false) {
   int reader[3] = {-1, -1, -1};  // layer whose side-stream dW last read pp[i] (event index)
   int next = 0;
   bool side_busy = false;
+  int64_t side_params = 0;  // parameters of the dW + update last issued on the side stream
   auto join_side = [&]() -> st_status {
     if (!side_busy) return ST_OK;
     ST_CUDA_TRY(cudaEventRecord(c->side_events[nl], c->side));
@@ -901,7 +902,9 @@ static st_status backward_compute(st_ctx* c, int64_t mb, bool fused = false) {
       if (D) {
         // ReLU mask of the layer that produced Ain (D12: ReLU'(0) = 0): 1[Z>0] == 1[ReLU(Z)>0]
         GemmArgs gx = gargs(c, L);
-        if (side_busy) gx.max_ctas = std::max(1, 148 - c->dwu_sms);  // share the GPU with the running dW
+        // share the GPU with the running dW + update — unless that one is small (e.g. the
+        // 10-wide output layer's), when this dX would otherwise run alone on part of the GPU
+        if (side_busy && side_params >= (int64_t)1 << 22) gx.max_ctas = std::max(1, 148 - c->dwu_sms);
         Timed t(c, KC_GEMM_DX);
         ST_TRY(gemm_dx(gx, dZ, Wh + L.w_off, producer_act == ST_ACT_RELU ? Ain : nullptr, D));
         c->launches += gemm_last_launches();
@@ -925,6 +928,7 @@ static st_status backward_compute(st_ctx* c, int64_t mb, bool fused = false) {
         c->launches += gemm_last_launches();
         ST_CUDA_TRY(cudaEventRecord(c->side_events[l], c->side));
         side_busy = true;
+        side_params = L.n_params;
         for (int i = 0; i < 3; ++i)
           if (dZ == pp[i]) reader[i] = l;
       } else {

@@ -57,6 +57,8 @@ struct TcParams {
                      // bit2 / bit3 skip B / A loads, bit4 skip TMEM stores, bit5 skip tcgen05.wait::st
   UpdateArgs upd;    // dW fused with K-B: weight-block targets (index n·M + m, like out)
   int wv_stream;     // fused K-B: W / V chunks staged in smem by TMA (mapW / mapV valid)
+  int lockstep;      // dW: CTA b owns m-tile b % m_tiles and the (b / m_tiles)-th part of its n-tiles, so
+                     // concurrent CTAs stream adjacent 512-B segments of the same W / V rows
   int ext_reduce;    // split-K: every CTA only writes its partial; splitk_epilogue_kernel reduces
   int sk;            // stream-K (fwd / dX TS kernel): CTA b takes chunks [b·U/G, (b+1)·U/G) of
                      // the tile-major (tile, K-block) space, U = tiles · kb_total, G = gridDim.x
@@ -1838,8 +1840,13 @@ __global__ void __launch_bounds__(DW_THREADS, 1)
   const int warp = threadIdx.x >> 5;
   const int lane = threadIdx.x & 31;
   const int tiles = m_tiles * n_tiles;
-  const int t_begin = (int)((long long)blockIdx.x * tiles / gridDim.x);
-  const int t_end = (int)((long long)(blockIdx.x + 1) * tiles / gridDim.x);
+  int t_begin = (int)((long long)blockIdx.x * tiles / gridDim.x);
+  int t_end = (int)((long long)(blockIdx.x + 1) * tiles / gridDim.x);
+  if (p.lockstep) {
+    const int parts = gridDim.x / m_tiles, m_t = blockIdx.x % m_tiles, part = blockIdx.x / m_tiles;
+    t_begin = m_t * n_tiles + part * n_tiles / parts;
+    t_end = m_t * n_tiles + (part + 1) * n_tiles / parts;
+  }
   const int nkb = p.kb_total;  // K blocks (K ≤ 128)
   const int bn = p.bn;
   const int conv_w0 = 2 + DW_EPI_WARPS;
@@ -2271,6 +2278,16 @@ int ext_reduce_splits() {
 }
 
 
+// ST_DW_LOCKSTEP=1: fused dW + update with m-tile-aligned CTA ranges (TcParams::lockstep)
+bool dw_lockstep() {
+  static int f = -1;
+  if (f < 0) {
+    const char* e = getenv("ST_DW_LOCKSTEP");
+    f = e ? atoi(e) : 0;
+  }
+  return f != 0;
+}
+
 // ST_CONV_TS=0: FP32X3 implicit-conv fwd / dX without the TMEM-A kernel (A/B timing)
 bool conv_ts_on() {
   static int f = -1;
@@ -2621,7 +2638,12 @@ st_status tc_dw_impl(const GemmArgs& g, const float* X, const float* dZ, float* 
     }
     p.idesc = make_idesc(p.bn, false, true);  // A from TMEM, B MN-major
     const int mt = (g.n_out + BM - 1) / BM, nt = (g.n_in + BNMAX - 1) / BNMAX;
-    const int grid = std::min(mt * nt, g.max_ctas > 0 ? std::min(g.max_ctas, num_sms()) : num_sms());
+    const int budget = g.max_ctas > 0 ? std::min(g.max_ctas, num_sms()) : num_sms();
+    int grid = std::min(mt * nt, budget);
+    if (dw_lockstep() && mt <= budget && nt >= budget / mt) {
+      grid = (budget / mt) * mt;  // whole m-tile columns (see TcParams::lockstep)
+      p.lockstep = 1;
+    }
     auto kern = upd ? (x3 ? tc_dw_kernel<true, true> : tc_dw_kernel<false, true>)
                     : (x3 ? tc_dw_kernel<true, false> : tc_dw_kernel<false, false>);
     static bool attr_set[4] = {false, false, false, false};
