@@ -202,6 +202,15 @@ ST_API int st_version_difference(int k, int N, int dir);
  * GPU. out may be NULL to query the count (*n = 2M). ST_ERR_INPUT if cap < 2M. */
 ST_API st_status st_program(int N, int k, int64_t M, int pred, st_event* out, size_t cap, size_t* n);
 
+/* Layer-to-stage partition (stage imbalance bounds a pipeline,
+ * P:146): contiguous cuts of n_layers layers with per-layer costs
+ * cost[0..n_layers) (≥ 0, e.g. measured or roofline times) into N non-empty stages that
+ * minimise the maximum stage cost; among optimal partitions the lexicographically
+ * smallest cut vector. cuts_out[0..N−1) receives the first layer of stages 1..N−1 (the
+ * st_config.cuts convention); *max_cost_out (may be NULL) the optimum. Host only.
+ * Errors: ST_ERR_INPUT (N < 1, N > n_layers, negative / non-finite cost, NULL). */
+ST_API st_status st_partition(const double* cost, int n_layers, int N, int32_t* cuts_out, double* max_cost_out);
+
 /* The communication plan of stage k (order of grouped sends/receives the engine
  * issues). Host only. out may be NULL to query the count. */
 ST_API st_status st_comm_plan(int N, int k, int64_t M, st_comm_group* out, size_t cap, size_t* n);

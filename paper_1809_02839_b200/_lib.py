@@ -92,6 +92,8 @@ def _load() -> ctypes.CDLL:
     sig = {
         "st_version_difference": (I, [I, I, I]),
         "st_program": (S, [I, I, I64, I, ctypes.POINTER(StEvent), U, ctypes.POINTER(U)]),
+        "st_partition": (S, [ctypes.POINTER(ctypes.c_double), I, I, ctypes.POINTER(ctypes.c_int32),
+                             ctypes.POINTER(ctypes.c_double)]),
         "st_comm_plan": (S, [I, I, I64, ctypes.POINTER(StCommGroup), U, ctypes.POINTER(U)]),
         "st_query_sizes": (S, [ctypes.POINTER(StConfig), ctypes.POINTER(StSizes)]),
         "st_get_nccl_id": (S, [ctypes.POINTER(ctypes.c_uint8 * 128)]),
@@ -131,7 +133,7 @@ def _load() -> ctypes.CDLL:
 
 
 lib = _load()
-EXPORTED = ("st_version_difference", "st_program", "st_comm_plan", "st_query_sizes", "st_get_nccl_id", "st_init",
+EXPORTED = ("st_version_difference", "st_program", "st_partition", "st_comm_plan", "st_query_sizes", "st_get_nccl_id", "st_init",
             "st_connect_local", "st_destroy", "st_set_params", "st_get_params", "st_stage_forward",
             "st_stage_backward", "st_predict_and_update", "st_step", "st_run", "st_run_host", "st_run_group", "st_get_trace",
             "st_losses_device", "st_sync", "st_set_profiling", "st_get_profile", "st_kernel_launches",
@@ -161,6 +163,16 @@ def program(N: int, k: int, M: int, pred: int = ST_PRED_SPECTRAIN):
     arr = (StEvent * max(1, n.value))()
     check(lib.st_program(N, k, M, pred, arr, n.value, ctypes.byref(n)))
     return _events(arr, n.value)
+
+
+def partition(costs, N: int):
+    """(cuts, max stage cost): min-max contiguous partition of per-layer costs into N
+    stages (st_partition; cuts in the st_config convention, first layer of stages 1..N−1)."""
+    c = (ctypes.c_double * max(1, len(costs)))(*[float(x) for x in costs])
+    cuts = (ctypes.c_int32 * max(1, N - 1))()
+    best = ctypes.c_double()
+    check(lib.st_partition(c, len(costs), N, cuts, ctypes.byref(best)))
+    return [int(cuts[i]) for i in range(N - 1)], best.value
 
 
 def comm_plan(N: int, k: int, M: int):

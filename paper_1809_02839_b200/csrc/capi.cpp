@@ -90,6 +90,10 @@ st_status st_program(int N, int k, int64_t M, int pred, st_event* out, size_t ca
   })
 }
 
+st_status st_partition(const double* cost, int n_layers, int N, int32_t* cuts_out, double* max_cost_out) {
+  GUARD({ return partition_layers(cost, n_layers, N, cuts_out, max_cost_out); })
+}
+
 st_status st_comm_plan(int N, int k, int64_t M, st_comm_group* out, size_t cap, size_t* n) {
   GUARD({
     if (N < 1 || k < 0 || k >= N || M < 0 || !n) return set_error(ST_ERR_INPUT, "st_comm_plan: bad arguments");

@@ -21,6 +21,7 @@ int version_difference(int k, int N, int dir);
 std::vector<Task> build_program(int N, int k, int64_t M);
 std::vector<st_event> program_events(int N, int k, int64_t M, int pred);
 std::vector<CommGroup> build_comm_plan(int N, int k, int64_t M);
+st_status partition_layers(const double* cost, int L, int N, int32_t* cuts, double* max_cost);
 
 // One communication op of a group: device buffer + element count.
 struct CommOp {

@@ -18,6 +18,8 @@
 // send is issued first as its own group.
 #include <vector>
 
+#include <limits>
+
 #include "engine.hpp"
 
 namespace st {
@@ -102,6 +104,44 @@ std::vector<CommGroup> build_comm_plan(int N, int k, int64_t M) {
     }
   }
   return plan;
+}
+
+// Min-max contiguous partition (P:146, P:380, P:404 — stage
+// imbalance bounds a pipeline): f[k][j] = the least possible maximum stage cost when
+// layers j..L−1 form k non-empty contiguous stages (suffix DP over prefix sums); the
+// cuts are then chosen front to back as the smallest index whose stage and best
+// remaining suffix both stay within the global optimum, i.e. the lexicographically
+// smallest optimal cut vector.
+st_status partition_layers(const double* cost, int L, int N, int32_t* cuts, double* max_cost) {
+  if (!cost || L < 1 || N < 1 || N > L || (N > 1 && !cuts))
+    return set_error(ST_ERR_INPUT, "partition: need 1 <= N <= L and a cost per layer");
+  std::vector<double> pre((size_t)L + 1, 0.0);
+  for (int i = 0; i < L; ++i) {
+    if (!(cost[i] >= 0.0)) return set_error(ST_ERR_INPUT, "partition: cost[%d] must be finite and >= 0", i);
+    pre[(size_t)i + 1] = pre[(size_t)i] + cost[i];
+  }
+  const double inf = std::numeric_limits<double>::infinity();
+  std::vector<std::vector<double>> f((size_t)N + 1, std::vector<double>((size_t)L + 1, inf));
+  for (int j = 0; j < L; ++j) f[1][(size_t)j] = pre[(size_t)L] - pre[(size_t)j];
+  for (int k = 2; k <= N; ++k)
+    for (int j = 0; j + k <= L; ++j)
+      for (int i = j + 1; i + (k - 1) <= L; ++i)
+        f[(size_t)k][(size_t)j] = std::min(f[(size_t)k][(size_t)j], std::max(pre[(size_t)i] - pre[(size_t)j], f[(size_t)k - 1][(size_t)i]));
+  const double opt = f[(size_t)N][0];
+  int start = 0;
+  for (int k = N; k >= 2; --k) {
+    int pick = -1;
+    for (int i = start + 1; i + (k - 1) <= L; ++i)
+      if (std::max(pre[(size_t)i] - pre[(size_t)start], f[(size_t)k - 1][(size_t)i]) <= opt) {
+        pick = i;
+        break;
+      }
+    if (pick < 0) return set_error(ST_ERR_STATE, "partition: no cut reproduces the optimum (internal)");
+    cuts[N - k] = pick;
+    start = pick;
+  }
+  if (max_cost) *max_cost = opt;
+  return ST_OK;
 }
 
 }  // namespace st

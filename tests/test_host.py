@@ -168,3 +168,45 @@ def test_query_sizes_and_validation(st):
         z = L.query_sizes(c)
         assert (z.s_fwd, z.s_bwd) == (sf, sb)
         assert (z.wb_bytes > 0) == (0 < sb != sf)
+
+
+# ---------------------------------------------------------------- st_partition (NEXT-4)
+
+def _brute_partition(cost, N):
+    import itertools
+    L = len(cost)
+    best, best_cuts = None, None
+    for cuts in itertools.combinations(range(1, L), N - 1):  # lexicographic order
+        b = (0,) + cuts + (L,)
+        m = max(sum(cost[b[i]:b[i + 1]]) for i in range(N))
+        if best is None or m < best:
+            best, best_cuts = m, list(cuts)
+    return best_cuts, best
+
+
+def test_partition_brute_force(st):
+    """Integer costs (exact in double): the optimum and the lexicographically smallest
+    optimal cut vector equal exhaustive search; every stage non-empty."""
+    rng = np.random.default_rng(0)
+    for _ in range(300):
+        L = int(rng.integers(1, 9))
+        N = int(rng.integers(1, L + 1))
+        cost = [int(x) for x in rng.integers(0, 20, L)]
+        cuts, best = st.partition(cost, N)
+        bc, bb = _brute_partition(cost, N)
+        assert best == bb and cuts == bc, (cost, N, cuts, best, bc, bb)
+        assert all(a < b for a, b in zip([0] + cuts, cuts + [L]))
+
+
+def test_partition_errors_and_vgg_flops(st):
+    with pytest.raises(st.SpecTrainError, match="INPUT"):
+        st.partition([1.0, 2.0], 3)
+    with pytest.raises(st.SpecTrainError, match="INPUT"):
+        st.partition([1.0, -2.0], 1)
+    # the flop-balanced VGG-16 8-stage partition of SURVEY §8(d) row 4 is optimal
+    m = sd.config_vgg16(8)
+    c = [2.0 * 128 * L.hw * L.hw * L.n_in * L.n_out * 9 if L.kind == sd.CONV else
+         (2.0 * 128 * L.n_in * L.n_out if L.kind == sd.DENSE else 0.0) for L in m.layers]
+    _, best = st.partition(c, 8)
+    b = (0,) + tuple(m.cuts) + (len(c),)
+    assert best == pytest.approx(max(sum(c[b[i]:b[i + 1]]) for i in range(8)), rel=1e-12)
