@@ -608,7 +608,7 @@ def run_ours(args):
                         "algorithmic_bytes_per_step": kb_bytes / args.steps}
     if rank == 0:
         cpu = None
-        if not args.no_cpu:
+        if not args.no_cpu and N == 1:  # the oracle baseline: rank 0 at N = 1 only
             rate, desc, threads, _ = oracle_sample_rate(model, B, 1)
             cpu = {"value": rate, "unit": UNIT, "cores": threads, "kind": "oracle", "sample": desc}
         line = {
