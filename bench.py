@@ -249,18 +249,28 @@ def run_reference(args):
         return
     S = args.stages or args.gpus
     model, B, wname = workload(args.workload, S)
-    for _ in range(args.warmup):
+    # the oracle takes seconds per mini-batch on the wide FCN slice: warm-up and timed steps
+    # share a wall-clock budget (ST_REF_BUDGET_S, default 150 s) so the arm ends within a few
+    # minutes; at least one warm-up and one timed step always run, the count is reported
+    budget = float(os.environ.get("ST_REF_BUDGET_S", "150"))
+    t_start = time.perf_counter()
+    for i in range(max(1, args.warmup)):
+        if i > 0 and time.perf_counter() - t_start > budget / 3:
+            break
         oracle_sample_rate(model, B, 1)
     rates, step_s = [], []
     desc, threads = "", 1
-    for _ in range(args.steps):
+    for i in range(args.steps):
+        if i > 0 and time.perf_counter() - t_start > budget:
+            break
         r, desc, threads, s = oracle_sample_rate(model, B, 1)
         rates.append(r)
         step_s.append(s)
     value = float(statistics.mean(rates))
+    desc += f"; {len(rates)} timed step(s) of the requested {args.steps} (wall-clock budget {budget:.0f} s)"
     line = {
         "impl": "reference", "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": args.gpus,
-        "steps": args.steps, "warmup": args.warmup, "ms_per_step": B / value * 1e3, "higher_is_better": True,
+        "steps": args.steps, "timed_steps": len(rates), "warmup": args.warmup, "ms_per_step": B / value * 1e3, "higher_is_better": True,
         "scaling": "strong", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
         "config": {"workload": wname, "stages": S, "batch": B, "parallelism": f"pp{S}"},
         "cpu_baseline": {"value": value, "unit": UNIT, "cores": threads, "kind": "oracle", "sample": desc},
