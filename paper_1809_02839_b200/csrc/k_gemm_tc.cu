@@ -835,12 +835,15 @@ __global__ void __launch_bounds__(kPThreads, 1)
   } else if (warp == 1) {
     // ---------------- MMA issuer (A hi / lo from TMEM slot s, B hi / lo from smem)
     int it = 0, j = 0;
+    const bool sa = (p.dev_flags & 1024) != 0;  // small terms in their own accumulator
     for (int u = blockIdx.x; u < units; u += gridDim.x, ++j) {
-      const int buf = j & 1;
+      const int buf = sa ? 0 : (j & 1);
+      const uint32_t par = sa ? (uint32_t)(j & 1) : (uint32_t)((j >> 1) & 1);
       const uint32_t d = tmem + (uint32_t)(buf * BNMAX);
+      const uint32_t d2 = sa ? tmem + (uint32_t)BNMAX : d;
       int kb0, kb1;
       kb_range(u, kb0, kb1);
-      mbar_wait(acc_empty + 8 * buf, ((j >> 1) & 1) ^ 1);
+      mbar_wait(acc_empty + 8 * buf, par ^ 1);
       tc_fence_after();
       for (int kb = kb0; kb < kb1; ++kb, ++it) {
         const int s = it % CS;
@@ -853,8 +856,8 @@ __global__ void __launch_bounds__(kPThreads, 1)
           for (int kk = 0; kk < BK / 8; ++kk) {
             const uint32_t acc = (kb > kb0 || kk > 0) ? 1u : 0u;
             tc_mma_ts(d, a_hi + kk * 8, op_desc<B_MN>(b_hi, kk), p.idesc, acc);
-            tc_mma_ts(d, a_lo + kk * 8, op_desc<B_MN>(b_hi, kk), p.idesc, 1u);
-            tc_mma_ts(d, a_hi + kk * 8, op_desc<B_MN>(b_lo, kk), p.idesc, 1u);
+            tc_mma_ts(d2, a_lo + kk * 8, op_desc<B_MN>(b_hi, kk), p.idesc, sa ? acc : 1u);
+            tc_mma_ts(d2, a_hi + kk * 8, op_desc<B_MN>(b_lo, kk), p.idesc, 1u);
           }
           tc_commit(b_empty + 8 * s);
           if (kb == kb1 - 1) tc_commit(acc_full + 8 * buf);
@@ -918,18 +921,26 @@ __global__ void __launch_bounds__(kPThreads, 1)
     // ---------------- epilogue (warps 6..9 → TMEM quadrants 2, 3, 0, 1)
     const int quad = warp & 3;
     int j = 0;
+    const bool sa = (p.dev_flags & 1024) != 0;
     for (int u = blockIdx.x; u < units; u += gridDim.x, ++j) {
-      const int buf = j & 1;
+      const int buf = sa ? 0 : (j & 1);
       const int t = u % tiles, m0 = (t % mt) * BM, n0 = (t / mt) * BNMAX;
-      mbar_wait(acc_full + 8 * buf, (j >> 1) & 1);
+      mbar_wait(acc_full + 8 * buf, sa ? (uint32_t)(j & 1) : (uint32_t)((j >> 1) & 1));
       tc_fence_after();
       const int m = m0 + quad * 32 + lane;
       const uint32_t trow = tmem + (uint32_t)(buf * BNMAX) + ((uint32_t)(quad * 32) << 16);
+      const uint32_t trow2 = tmem + (uint32_t)BNMAX + ((uint32_t)(quad * 32) << 16);
       if (p.splits > 1) {
         float* wsp = p.ws + ((size_t)(u / tiles) * tiles + t) * (BNMAX * BM);
         for (int c = 0; c < bn; c += 16) {
           float v[16];
           tc_ld16(trow + c, v);
+          if (sa) {
+            float w2[16];
+            tc_ld16(trow2 + c, w2);
+#pragma unroll
+            for (int q = 0; q < 16; ++q) v[q] += w2[q];
+          }
 #pragma unroll
           for (int q = 0; q < 16; ++q) wsp[(size_t)(c + q) * BM + quad * 32 + lane] = v[q];
         }
@@ -938,6 +949,12 @@ __global__ void __launch_bounds__(kPThreads, 1)
         for (int c = 0; c < bn; c += 16) {
           float v[16];
           tc_ld16(trow + c, v);
+          if (sa) {
+            float w2[16];
+            tc_ld16(trow2 + c, w2);
+#pragma unroll
+            for (int q = 0; q < 16; ++q) v[q] += w2[q];
+          }
           if (m < p.M) epilogue_store16<EPI>(p, m, n0 + c, v, bias);
         }
       }
@@ -2315,6 +2332,7 @@ template <int EPI, bool A_MN, bool B_MN, int CV = CV_NONE>
 st_status launch(const GemmArgs& g, int M, int N, int K, const CUtensorMap& ma, const CUtensorMap& mb, float* out,
                  const float* aux, int relu, int cvH = 0, int cvW = 0, int cvC = 0) {
   TcParams p{};
+  p.dev_flags = dev_flags();
   p.row = (CV == CV_FWD || CV == CV_DX || CV == CV_ROWS || CV == CV_DWT) ? 1 : 0;
   p.cv_H = cvH;
   p.cv_W = cvW;
