@@ -410,6 +410,7 @@ st_status ctx_init(const st_config* cfg, const st_buffers* bufs, void* stream, s
   c->side_events.resize(c->layers.size() + 1);
   for (auto& e : c->side_events) ST_CUDA_TRY(cudaEventCreateWithFlags(&e, cudaEventDisableTiming));
   if (const char* e = getenv("ST_DWU_SMS")) c->dwu_sms = std::max(1, atoi(e));
+  if (const char* e = getenv("ST_CONV_OVERLAP")) c->conv_overlap = atoi(e) != 0;
   ST_CUDA_TRY(cudaMemsetAsync(c->V, 0, (size_t)c->P * 4, c->stream));
   ST_CUDA_TRY(cudaMemsetAsync(c->losses_dev, 0xff, (size_t)c->max_mb * 4, c->stream));  // NaN
   // GEMM workspace: split-K tile counters must start at zero (they self-reset afterwards)
@@ -800,7 +801,11 @@ static st_status backward_compute(st_ctx* c, int64_t mb, bool fused = false) {
     const LayerInfo& L = c->layers[l];
     float* Ain = layer_in(c, slot, (size_t)l);
     const bool need_dx = !(c->first_stage && l == 0) && L.kind != ST_LAYER_EMBED;
-    const bool overlap = fused && L.kind == ST_LAYER_DENSE;
+    // implicit convs and pools also overlap: a conv's dW + update runs on the side stream
+    // while the next layers' dX / max-pool backward run on the main stream
+    const bool conv_ov = c->conv_overlap && (L.kind == ST_LAYER_POOL ||
+                                             (L.kind == ST_LAYER_CONV && tc_conv_ok(c->gemm, L.hw, L.hw, L.n_in, L.n_out)));
+    const bool overlap = fused && (L.kind == ST_LAYER_DENSE || conv_ov);
     if (!overlap) ST_TRY(join_side());
     float* D = nullptr;
     int dslot = -1;
@@ -828,19 +833,48 @@ static st_status backward_compute(st_ctx* c, int64_t mb, bool fused = false) {
       // implicit GEMMs: dX = conv with the flipped kernel (ReLU mask of the producer of
       // Ain fused), then dW = Σ_p window(Ain)ᵀ dZ (+ bias gradient) into G
       if (D) {
+        GemmArgs gx = gargs_rows(c, c->B, 9 * L.n_in, L.n_out);
+        if (side_busy) gx.max_ctas = std::max(1, 148 - c->dwu_sms);  // a conv dW is running on the side
         Timed t(c, KC_GEMM_DX);
-        ST_TRY(tc_conv_dx(gargs_rows(c, c->B, 9 * L.n_in, L.n_out), dZ, L.hw, L.hw, L.n_in, L.n_out, Wh + L.w_off,
-                          producer_act == ST_ACT_RELU ? Ain : nullptr, D));
+        ST_TRY(tc_conv_dx(gx, dZ, L.hw, L.hw, L.n_in, L.n_out, Wh + L.w_off, producer_act == ST_ACT_RELU ? Ain : nullptr,
+                          D));
         c->launches += tc_last_launches();
       }
-      Timed t(c, KC_GEMM_DW);
-      ST_TRY(tc_conv_dw(gargs_rows(c, c->B, 9 * L.n_in, L.n_out), Ain, dZ, L.hw, L.hw, L.n_in, L.n_out,
-                        c->G + L.w_off, L.bias ? c->G + L.b_off : nullptr));
-      c->launches += tc_last_launches();
-      if (fused) {  // K-B over the layer's weight + bias block (contiguous, S:106 layout)
-        const UpdateArgs u = block_update(c, L.w_off, kc);
-        ST_TRY(launch_update_predict(u.W, u.V, c->G + L.w_off, u.WF, u.WB, (size_t)L.n_params, kc, c->stream));
-        c->launches += 1;
+      if (overlap) {
+        // dW + bias gradient + K-B update on the side stream, after this layer's dX (which
+        // reads WB_l); its own GEMM workspace; a CTA budget while more conv dX follow
+        ST_CUDA_TRY(cudaEventRecord(c->side_events[l], c->stream));
+        ST_CUDA_TRY(cudaStreamWaitEvent(c->side, c->side_events[l], 0));
+        GemmArgs gw = gargs_rows(c, c->B, 9 * L.n_in, L.n_out);
+        gw.stream = c->side;
+        gw.work = c->gemm_ws2;
+        bool more_dx = false;
+        for (int q = l - 1; q >= 0 && !more_dx; --q)
+          more_dx = c->layers[q].kind == ST_LAYER_CONV && !(c->first_stage && q == 0);
+        if (more_dx) gw.max_ctas = c->dwu_sms;
+        {
+          Timed t(c, KC_GEMM_DW, c->side);
+          ST_TRY(tc_conv_dw(gw, Ain, dZ, L.hw, L.hw, L.n_in, L.n_out, c->G + L.w_off, L.bias ? c->G + L.b_off : nullptr));
+          c->launches += tc_last_launches();
+          const UpdateArgs u = block_update(c, L.w_off, kc);
+          ST_TRY(launch_update_predict(u.W, u.V, c->G + L.w_off, u.WF, u.WB, (size_t)L.n_params, kc, c->side));
+          c->launches += 1;
+        }
+        ST_CUDA_TRY(cudaEventRecord(c->side_events[l], c->side));
+        side_busy = true;
+        side_params = L.n_params;
+        for (int i = 0; i < 3; ++i)
+          if (dZ == pp[i]) reader[i] = l;
+      } else {
+        Timed t(c, KC_GEMM_DW);
+        ST_TRY(tc_conv_dw(gargs_rows(c, c->B, 9 * L.n_in, L.n_out), Ain, dZ, L.hw, L.hw, L.n_in, L.n_out,
+                          c->G + L.w_off, L.bias ? c->G + L.b_off : nullptr));
+        c->launches += tc_last_launches();
+        if (fused) {  // K-B over the layer's weight + bias block (contiguous, S:106 layout)
+          const UpdateArgs u = block_update(c, L.w_off, kc);
+          ST_TRY(launch_update_predict(u.W, u.V, c->G + L.w_off, u.WF, u.WB, (size_t)L.n_params, kc, c->stream));
+          c->launches += 1;
+        }
       }
     } else if (L.kind == ST_LAYER_CONV && tc_conv_small_ok(c->gemm, L.n_in, L.n_out)) {
       const int P = c->B * L.hw * L.hw;

@@ -139,6 +139,8 @@ struct st_ctx {
   int32_t* y_stage = nullptr;   // [R] labels staged from host (st_run_host)
   float* lstm_rec = nullptr;    // [B × 4H] h_{t−1}·W_hh
   float* lstm_dh = nullptr;     // [B × H] dh_next
+  bool conv_overlap = false;    // implicit-conv dW + update on the side stream (ST_CONV_OVERLAP=1; measured
+                                // slower: VGG-16 58.9k -> 53.0k samples/s with an 80 / 68 SM split)
   float* wstash = nullptr;      // ST_PRED_STASH: S slots of P floats (the WF buffer)
   std::vector<int64_t> stash_ver;  // ST_PRED_STASH: version each slot's forward used
   float* lstm_hlo = nullptr;    // [B × H] tf32 lo of h_{t−1} (3xTF32 operand of the recurrent GEMM)
