@@ -782,19 +782,30 @@ constexpr int CS = 4;
 constexpr int CS_STAGE = 3 * TILE_BYTES;
 constexpr int cs_smem_bytes() { return CS * CS_STAGE + 1024 + 256; }
 
-template <int EPI, bool A_MN, bool B_MN, int CV>
+// NARROW (MMA N ≤ 64, e.g. the 64-channel conv layers): B tiles are half size, so the ring
+// is 6 stages of 32 KB and the accumulators 64 columns wide (TMEM 2·64 + 6·64 = 512).
+template <bool NARROW>
+constexpr int tsg_stage_bytes() { return TILE_BYTES + 2 * (NARROW ? TILE_BYTES / 2 : TILE_BYTES); }
+template <bool NARROW>
+constexpr int tsg_smem_bytes() { return (NARROW ? 6 : CS) * tsg_stage_bytes<NARROW>() + 1024 + 256; }
+
+template <int EPI, bool A_MN, bool B_MN, int CV, bool NARROW = false>
 __global__ void __launch_bounds__(kPThreads, 1)
     tc_tsg_kernel(const __grid_constant__ CUtensorMap mapA, const __grid_constant__ CUtensorMap mapB,
                       TcParams p, int mt, int tiles) {
+  constexpr int NS = NARROW ? 6 : CS;                     // ring stages = TMEM A slots
+  constexpr int BT = NARROW ? TILE_BYTES / 2 : TILE_BYTES;  // B raw / B lo tile bytes
+  constexpr int STG = TILE_BYTES + 2 * BT;
+  constexpr uint32_t AW = NARROW ? 64 : BNMAX;             // accumulator columns
   extern __shared__ __align__(1024) uint8_t smem_raw[];
   char* smem = align_smem_1k(smem_raw);
-  uint64_t* bars = reinterpret_cast<uint64_t*>(smem + CS * CS_STAGE);
-  const uint32_t b_full = smem_u32(bars);          // TMA landed (A + B)           [CS]
-  const uint32_t b_ready = b_full + 8 * CS;        // TMEM hi/lo + B lo written    [CS] (4 warps)
-  const uint32_t b_empty = b_ready + 8 * CS;       // MMAs done with stage + slot  [CS]
-  const uint32_t acc_full = b_empty + 8 * CS;      // [2]
+  uint64_t* bars = reinterpret_cast<uint64_t*>(smem + NS * STG);
+  const uint32_t b_full = smem_u32(bars);          // TMA landed (A + B)           [NS]
+  const uint32_t b_ready = b_full + 8 * NS;        // TMEM hi/lo + B lo written    [NS] (4 warps)
+  const uint32_t b_empty = b_ready + 8 * NS;       // MMAs done with stage + slot  [NS]
+  const uint32_t acc_full = b_empty + 8 * NS;      // [2]
   const uint32_t acc_empty = acc_full + 16;        // [2] (4 epilogue warps)
-  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(bars + 3 * CS + 4);
+  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(bars + 3 * NS + 4);
 
   const int warp = threadIdx.x >> 5;
   const int lane = threadIdx.x & 31;
@@ -810,7 +821,7 @@ __global__ void __launch_bounds__(kPThreads, 1)
   const int b_chunks = B_MN ? nbox_b * 256 : bn * 8;
 
   if (threadIdx.x == 0) {
-    for (int s = 0; s < CS; ++s) {
+    for (int s = 0; s < NS; ++s) {
       mbar_init(b_full + 8 * s, 1);
       mbar_init(b_ready + 8 * s, 4);
       mbar_init(b_empty + 8 * s, 1);
@@ -834,7 +845,7 @@ __global__ void __launch_bounds__(kPThreads, 1)
   __syncthreads();
   tc_fence_after();
   const uint32_t tmem = *tmem_slot;
-  const uint32_t tmemA = tmem + 2 * BNMAX;  // CS slots of 64 columns
+  const uint32_t tmemA = tmem + 2 * AW;  // NS slots of 64 columns
 
   if (warp == 0) {
     // ---------------- TMA producer
@@ -845,10 +856,10 @@ __global__ void __launch_bounds__(kPThreads, 1)
       int kb0, kb1;
       kb_range(u, kb0, kb1);
       for (int kb = kb0; kb < kb1; ++kb, ++it) {
-        const int s = it % CS;
-        mbar_wait(b_empty + 8 * s, ((it / CS) & 1) ^ 1);
+        const int s = it % NS;
+        mbar_wait(b_empty + 8 * s, ((it / NS) & 1) ^ 1);
         const uint32_t full = b_full + 8 * s;
-        const uint32_t dA = smem_u32(smem + s * CS_STAGE);
+        const uint32_t dA = smem_u32(smem + s * STG);
         if (elect_one()) {
           mbar_expect_tx(full, bytes);
           load_stage<A_MN, B_MN, CV>(p, &mapA, &mapB, dA, dA + TILE_BYTES, full, m0, n0, kb * BK, nbox_b);
@@ -863,17 +874,17 @@ __global__ void __launch_bounds__(kPThreads, 1)
     for (int u = blockIdx.x; u < units; u += gridDim.x, ++j) {
       const int buf = sa ? 0 : (j & 1);
       const uint32_t par = sa ? (uint32_t)(j & 1) : (uint32_t)((j >> 1) & 1);
-      const uint32_t d = tmem + (uint32_t)(buf * BNMAX);
-      const uint32_t d2 = sa ? tmem + (uint32_t)BNMAX : d;
+      const uint32_t d = tmem + (uint32_t)buf * AW;
+      const uint32_t d2 = sa ? tmem + AW : d;
       int kb0, kb1;
       kb_range(u, kb0, kb1);
       mbar_wait(acc_empty + 8 * buf, par ^ 1);
       tc_fence_after();
       for (int kb = kb0; kb < kb1; ++kb, ++it) {
-        const int s = it % CS;
-        mbar_wait(b_ready + 8 * s, (it / CS) & 1);
+        const int s = it % NS;
+        mbar_wait(b_ready + 8 * s, (it / NS) & 1);
         tc_fence_after();
-        const uint32_t b_hi = smem_u32(smem + s * CS_STAGE) + TILE_BYTES, b_lo = b_hi + TILE_BYTES;
+        const uint32_t b_hi = smem_u32(smem + s * STG) + TILE_BYTES, b_lo = b_hi + BT;
         const uint32_t a_hi = tmemA + s * 64, a_lo = a_hi + 32;
         if (elect_one()) {
 #pragma unroll
@@ -899,9 +910,9 @@ __global__ void __launch_bounds__(kPThreads, 1)
       int kb0, kb1;
       kb_range(u, kb0, kb1);
       for (int kb = kb0; kb < kb1; ++kb, ++it) {
-        const int s = it % CS;
-        mbar_wait(b_full + 8 * s, (it / CS) & 1);
-        char* st = smem + s * CS_STAGE;
+        const int s = it % NS;
+        mbar_wait(b_full + 8 * s, (it / NS) & 1);
+        char* st = smem + s * STG;
         uint32_t hi[32], lo[32];
         if (A_MN) {
           // element (k, r): box r/32, row k (128 B), 32-byte atoms swizzled by k % 4
@@ -927,7 +938,7 @@ __global__ void __launch_bounds__(kPThreads, 1)
             lo[4 * c + 3] = __float_as_uint(lo_part(v.w));
           }
         }
-        make_lo(st + TILE_BYTES, st + 2 * TILE_BYTES, b_chunks, ctid);
+        make_lo(st + TILE_BYTES, st + TILE_BYTES + BT, b_chunks, ctid);
         fence_proxy_async();
         // the slot's previous MMAs are done: the producer refilled this stage only after
         // b_empty[s], which commits after every MMA that read TMEM slot s
@@ -952,8 +963,8 @@ __global__ void __launch_bounds__(kPThreads, 1)
       mbar_wait(acc_full + 8 * buf, sa ? (uint32_t)(j & 1) : (uint32_t)((j >> 1) & 1));
       tc_fence_after();
       const int m = m0 + quad * 32 + lane;
-      const uint32_t trow = tmem + (uint32_t)(buf * BNMAX) + ((uint32_t)(quad * 32) << 16);
-      const uint32_t trow2 = tmem + (uint32_t)BNMAX + ((uint32_t)(quad * 32) << 16);
+      const uint32_t trow = tmem + (uint32_t)buf * AW + ((uint32_t)(quad * 32) << 16);
+      const uint32_t trow2 = tmem + AW + ((uint32_t)(quad * 32) << 16);
       if (p.splits > 1) {
         float* wsp = p.ws + ((size_t)(u / tiles) * tiles + t) * (BNMAX * BM);
         for (int c = 0; c < bn; c += 16) {
@@ -2336,6 +2347,16 @@ int dw_lockstep_mode() {
   return f;
 }
 
+// ST_TSG_NARROW=0: N ≤ 64 TMEM-A launches on the 4-stage ring (A/B timing)
+bool tsg_narrow_on() {
+  static int f = -1;
+  if (f < 0) {
+    const char* e = getenv("ST_TSG_NARROW");
+    f = (e && atoi(e) == 0) ? 0 : 1;
+  }
+  return f != 0;
+}
+
 // ST_CONV_TS=0: FP32X3 implicit-conv fwd / dX without the TMEM-A kernel (A/B timing)
 bool conv_ts_on() {
   static int f = -1;
@@ -2399,11 +2420,13 @@ st_status launch(const GemmArgs& g, int M, int N, int K, const CUtensorMap& ma, 
   p.ext_reduce = p.splits >= ext_reduce_splits();
   if (g.mode == ST_GEMM_FP32X3 && conv_ts_on() && (CV != CV_NONE || EPI == EPI_DW)) {
     // persistent TMEM-A kernel: implicit conv (all passes) and the tall dense dW
-    auto ck = tc_tsg_kernel<EPI, A_MN, B_MN, CV>;
-    static bool cattr_set = false;
-    if (!cattr_set) {
-      ST_CUDA_TRY(cudaFuncSetAttribute(ck, cudaFuncAttributeMaxDynamicSharedMemorySize, cs_smem_bytes()));
-      cattr_set = true;
+    const bool narrow = p.bn <= 64 && tsg_narrow_on();
+    auto ck = narrow ? tc_tsg_kernel<EPI, A_MN, B_MN, CV, true> : tc_tsg_kernel<EPI, A_MN, B_MN, CV, false>;
+    const int smem = narrow ? tsg_smem_bytes<true>() : tsg_smem_bytes<false>();
+    static bool cattr_set[2] = {false, false};
+    if (!cattr_set[narrow]) {
+      ST_CUDA_TRY(cudaFuncSetAttribute(ck, cudaFuncAttributeMaxDynamicSharedMemorySize, smem));
+      cattr_set[narrow] = true;
     }
     p.idesc = make_idesc(p.bn, false, B_MN);
     p.ext_reduce = p.splits > 1;
@@ -2412,7 +2435,7 @@ st_status launch(const GemmArgs& g, int M, int N, int K, const CUtensorMap& ma, 
     // accumulators that overlap the epilogue (ST_GEMM_DEV_FLAGS=1024 forces it everywhere)
     p.split_acc = (EPI == EPI_DW || (p.dev_flags & 1024)) ? 1 : 0;
     const int budget = g.max_ctas > 0 ? std::min(g.max_ctas, num_sms()) : num_sms();
-    ck<<<std::min(tiles * p.splits, budget), kPThreads, cs_smem_bytes(), g.stream>>>(ma, mb, p, mt, tiles);
+    ck<<<std::min(tiles * p.splits, budget), kPThreads, smem, g.stream>>>(ma, mb, p, mt, tiles);
     ST_CUDA_TRY(cudaGetLastError());
     g_launches = 1;
     if (p.ext_reduce) {
