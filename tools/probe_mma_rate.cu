@@ -82,7 +82,7 @@ int main() {
   cudaFuncSetAttribute(rate, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
   long long* out; float* sink;
   cudaMallocManaged(&out, 16); cudaMallocManaged(&sink, 4);
-  for (int N : {128, 256})
+  for (int N : {32, 64, 128, 256})
     for (int ts = 0; ts < 2; ++ts)
       for (int noise = 0; noise < 2; ++noise) {
         for (int rep = 0; rep < 2; ++rep) {
