@@ -1411,6 +1411,15 @@ __device__ __forceinline__ void tma_load_2d_pair(uint32_t dst, const CUtensorMap
       "l"(reinterpret_cast<uint64_t>(map)), "r"(c0), "r"(c1), "r"(cluster_bar)
       : "memory");
 }
+// 4-D (NHWC window) variant: coordinates (c, w, h, b), zero fill outside the image
+__device__ __forceinline__ void tma_load_4d_pair(uint32_t dst, const CUtensorMap* map, int c0, int c1, int c2, int c3,
+                                                 uint32_t cluster_bar) {
+  asm volatile(
+      "cp.async.bulk.tensor.4d.cta_group::2.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1, {%2, %3, "
+      "%4, %5}], [%6];" ::"r"(dst),
+      "l"(reinterpret_cast<uint64_t>(map)), "r"(c0), "r"(c1), "r"(c2), "r"(c3), "r"(cluster_bar)
+      : "memory");
+}
 __device__ __forceinline__ void tc_mma_ts2(uint32_t tmem_d, uint32_t tmem_a, uint64_t bdesc, uint32_t idesc,
                                            uint32_t accum) {
   asm volatile(
@@ -1431,7 +1440,10 @@ __device__ __forceinline__ void cluster_sync_all() {
 
 // SA: the two small 3xTF32 terms go to a second TMEM accumulator (4 A slots instead of 6),
 // added to the hi·hi accumulator in fp32 by the epilogue (reading D24)
-template <int EPI, bool A_MN, bool SA = false>
+// CONV: B is the implicit 3×3 window of an NHWC activation (CV_FWD addressing, 64-pixel
+// 4-D boxes per CTA) and its precomputed lo — the conv forward with the weights on M
+// (Cout ≥ 256: full 256-row pair tiles), pixels on N, output NHWC as out[p·Cout + co].
+template <int EPI, bool A_MN, bool SA = false, bool CONV = false>
 __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(TS_THREADS, 1)
     tc_ts2_kernel(const __grid_constant__ CUtensorMap mapA, const __grid_constant__ CUtensorMap mapB,
                   const __grid_constant__ CUtensorMap mapBlo, TcParams p) {
@@ -1537,8 +1549,16 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(TS_THREADS, 1)
         const uint32_t dB = smem_u32(ringB + s * TS2_B_STAGE);
         if (elect_one()) {
           if (rank == 0) mbar_expect_tx(b_full + 8 * s, bytes);
-          tma_load_2d_pair(dB, &mapB, k0, n0 + (int)rank * bh, full_leader);
-          tma_load_2d_pair(dB + (BNMAX / 2) * BK * 4, &mapBlo, k0, n0 + (int)rank * bh, full_leader);
+          if (CONV) {
+            const int HW = p.cv_H * p.cv_W, p0 = n0 + (int)rank * bh;
+            const int b0 = p0 / HW, r0 = p0 - b0 * HW, h0 = r0 / p.cv_W, w0 = r0 - h0 * p.cv_W;
+            const int q = k0 / p.cv_C, c0 = k0 - q * p.cv_C, kh = q / 3, kw = q - 3 * kh;
+            tma_load_4d_pair(dB, &mapB, c0, w0 + kw - 1, h0 + kh - 1, b0, full_leader);
+            tma_load_4d_pair(dB + (BNMAX / 2) * BK * 4, &mapBlo, c0, w0 + kw - 1, h0 + kh - 1, b0, full_leader);
+          } else {
+            tma_load_2d_pair(dB, &mapB, k0, n0 + (int)rank * bh, full_leader);
+            tma_load_2d_pair(dB + (BNMAX / 2) * BK * 4, &mapBlo, k0, n0 + (int)rank * bh, full_leader);
+          }
         }
         __syncwarp();
       }
@@ -2840,10 +2860,81 @@ bool tc_conv_ok(int mode, int H, int W, int Cin, int Cout) {
          Cin % 32 == 0 && Cout % 32 == 0 && act_box(H, W, BM, b) && act_box(H, W, 32, b);
 }
 
+// Conv forward on the CTA-pair TMEM-A kernel (tc_ts2_kernel<…, CONV>): weights on M
+// (Cout ≥ 256, so every pair tile is full), pixels on N — the pair's MMAs run at ~1.5× the
+// per-SM rate of the single-CTA N ≤ 128 ones (profiles/r1_probe_mma_rate_tf32.txt). The
+// activation lo is split once into the workspace tail. Opt-in (ST_CONV_PAIR=1): in the
+// serialised, cache-flushed ncu list its conv3–5 forwards are ~25% faster, but in the warm
+// step the forward class is unchanged (0.638 vs 0.644 ms; VGG-16 58.9k vs 59.0k samples/s).
+bool conv_pair_on() {
+  static int f = -1;
+  if (f < 0) {
+    const char* e = getenv("ST_CONV_PAIR");
+    f = (e && atoi(e) == 1) ? 1 : 0;
+  }
+  return f != 0;
+}
+
+st_status tc_conv_fwd_pair(const GemmArgs& g, const float* X, int H, int W, int Cin, int Cout, const float* Wt,
+                           const float* bias, float* Y, int relu) {
+  const int P = g.B * H * W, K = 9 * Cin;
+  TcParams p{};
+  const int budget = g.max_ctas > 0 ? std::min(g.max_ctas, num_sms()) : num_sms();
+  const int mt = (Cout + BM - 1) / BM, mt_grid = (mt + 1) / 2 * 2;
+  plan_splits(p, mt_grid * BM, P, K, budget / 2 * 2);
+  const int nt = (P + BNMAX - 1) / BNMAX;
+  if (p.bn != BNMAX) return set_error(ST_ERR_INPUT, "conv fwd pair: needs P >= %d pixels (got %d)", BNMAX, P);
+  p.mt = mt_grid;
+  p.tiles = mt_grid * nt;
+  p.M = Cout;
+  p.out = Y;
+  p.aux = bias;
+  p.relu = relu;
+  p.cv_H = H;
+  p.cv_W = W;
+  p.cv_C = Cin;
+  p.counters = reinterpret_cast<int*>(g.work);
+  p.ws = reinterpret_cast<float*>(static_cast<char*>(g.work) + kCounterBytes);
+  p.idesc = make_idesc(p.bn, false, false, 2 * BM);
+  p.dev_flags = dev_flags();
+  p.ext_reduce = p.splits >= ext_reduce_splits();
+  float* xlo = reinterpret_cast<float*>(static_cast<char*>(g.work) + kCounterBytes +
+                                        (size_t)2 * 148 * BNMAX * BM * 4);
+  const size_t n4 = (size_t)P * Cin / 4;
+  split_lo_kernel<<<std::min<size_t>(4 * 148, (n4 + 255) / 256), 256, 0, g.stream>>>(
+      reinterpret_cast<const float4*>(X), reinterpret_cast<float4*>(xlo), n4);
+  ST_CUDA_TRY(cudaGetLastError());
+  CUtensorMap ma, mb, mblo;
+  if (!make_map(&ma, Wt, Cout, K, Cout, 32, true) || !make_act_map(&mb, X, g.B, H, W, Cin, BNMAX / 2, false) ||
+      !make_act_map(&mblo, xlo, g.B, H, W, Cin, BNMAX / 2, false))
+    return set_error(ST_ERR_CUDA, "cuTensorMapEncodeTiled failed (conv fwd, pair)");
+  auto kern = ts_split_acc() ? tc_ts2_kernel<EPI_FWD, true, true, true> : tc_ts2_kernel<EPI_FWD, true, false, true>;
+  static bool attr_set[2] = {false, false};
+  if (!attr_set[ts_split_acc()]) {
+    ST_CUDA_TRY(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, ts2_smem_bytes()));
+    attr_set[ts_split_acc()] = true;
+  }
+  dim3 grid(mt_grid, nt, p.splits);
+  kern<<<grid, TS_THREADS, ts2_smem_bytes(), g.stream>>>(ma, mb, mblo, p);
+  ST_CUDA_TRY(cudaGetLastError());
+  g_launches = 2;
+  if (p.ext_reduce) {
+    ST_TRY(launch_splitk_epilogue<EPI_FWD>(p, mt_grid * nt, mt_grid, g.stream));
+    g_launches = 3;
+  }
+  return ST_OK;
+}
+
 // Y[P × Cout] = conv3x3(X) + b, optional ReLU (NHWC; g.B = images)
 st_status tc_conv_fwd(const GemmArgs& g, const float* X, int H, int W, int Cin, int Cout, const float* Wt,
                       const float* bias, float* Y, int relu) {
   const int P = g.B * H * W;
+  cuuint32_t pb[3];
+  // P ≥ 128: the pair's N tile is the full 128 pixels, so each CTA's window box is exactly the
+  // 64 pixels its TMA map describes (a narrower tile would expect fewer bytes than it loads)
+  if (g.mode == ST_GEMM_FP32X3 && Cout >= 2 * BM && P >= BNMAX && use_pair() && conv_pair_on() &&
+      act_box(H, W, BNMAX / 2, pb))
+    return tc_conv_fwd_pair(g, X, H, W, Cin, Cout, Wt, bias, Y, relu);
   CUtensorMap ma, mb;
   if (!make_act_map(&ma, X, g.B, H, W, Cin, BM, false) || !make_map(&mb, Wt, Cout, 9 * Cin, Cout, 32, true))
     return set_error(ST_ERR_CUDA, "cuTensorMapEncodeTiled failed (conv fwd)");

@@ -74,3 +74,14 @@ def test_vgg_implicit_batch1(st):
     """FP32X3 (the parity mode) at batch 1 — single-image tiles, P < 128 everywhere."""
     model = sd.vgg(cfg=(32, "M", 64, "M"), fc=(16,), classes=10, hw=8, in_ch=32, cuts=[])
     _vgg_parity(st, model, 1, 6, 0.05, seed=6)
+
+
+def test_vgg_wide_conv_pair_kernel(st):
+    """Cout ≥ 256 (256 / 384 channels). With ST_CONV_PAIR=1 (tests/test_gpu_variants.py
+    runs this in a child process) the conv forward is the CTA-pair TMEM-A kernel (weights on M,
+    64-pixel window boxes per CTA, activation lo split once); 384 output channels leave a
+    padding CTA in the last pair; 8×8 and 4×4 images, ragged pixel tiles (batch 3)."""
+    model = sd.vgg(cfg=(32, 384, "M", 256, "M"), fc=(16,), classes=10, hw=8, in_ch=32, cuts=[2])
+    _vgg_parity(st, model, 3, 8, 0.02, seed=7)  # 4×4 stage: P = 48 < 128 → single-CTA kernel
+    model = sd.vgg(cfg=(32, 256, 256, "M"), fc=(16,), classes=10, hw=8, in_ch=32, cuts=[1])
+    _vgg_parity(st, model, 5, 6, 0.02, seed=8)  # P = 320: two full and one ragged pixel tile

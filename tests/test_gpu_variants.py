@@ -26,3 +26,19 @@ def test_gemm_variants_pass_parity(env):
     r = subprocess.run([sys.executable, "-m", "pytest", "-q", "-x", "-m", "gpu", "-p", "no:cacheprovider",
                         "-k", "not tf32", *CASES], cwd=ROOT, env=e, capture_output=True, text=True, timeout=900)
     assert r.returncode == 0, r.stdout[-3000:] + r.stderr[-2000:]
+
+
+CONV_CASES = ["tests/test_gpu_conv.py"]
+
+
+@pytest.mark.gpu
+@pytest.mark.parametrize("env", [{"ST_CONV_PAIR": "1"}, {"ST_CONV_OVERLAP": "1"}, {"ST_TS_SPLIT_ACC": "0"},
+                                 {"ST_TSG_NARROW": "0"}],
+                         ids=["conv_pair", "conv_overlap", "one_accumulator", "tsg_4_stages"])
+def test_conv_variants_pass_parity(env):
+    """Opt-in conv paths: the CTA-pair conv forward, side-stream overlap of the conv dW +
+    update, the single-accumulator pair kernel, the 4-stage TMEM-A ring for N ≤ 64."""
+    e = dict(os.environ, **env)
+    r = subprocess.run([sys.executable, "-m", "pytest", "-q", "-x", "-m", "gpu", "-p", "no:cacheprovider",
+                        *CONV_CASES], cwd=ROOT, env=e, capture_output=True, text=True, timeout=900)
+    assert r.returncode == 0, r.stdout[-3000:] + r.stderr[-2000:]
