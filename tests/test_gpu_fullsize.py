@@ -97,3 +97,24 @@ def test_wide_fcn_full_size_two_stages_with_prediction(st):
         for s in stages:
             s.close()
     _check(model, w0, X, Y, [o[0] for o in out], [o[1] for o in out], losses, trs, v_hidden_tol=3e-2)
+
+
+def test_vgg16_full_size_single_stage_bench_path(st):
+    """BJ configs[3] at full size: VGG-16 on 32×32×3 images, batch 128, one stage through
+    st_run (RGB first conv via the padded im2col, implicit-GEMM convs on the TMEM-A
+    kernel, max-pools, FC head). Max-pool choices, like ReLU decisions, are taken in fp32
+    here and in fp64 by the oracle (D24), so V gets the same loose hidden-layer gate."""
+    model = sd.config_vgg16(1)
+    M, B = 2, 128
+    w0, X, Y = sd.parity_inputs(model, M, B, seed=0)
+    dev = torch.device("cuda", 0)
+    s = st.Stage(layers_of(model), model.cuts, 0, B, LR, 0.9, transport=st.ST_TRANSPORT_NCCL, device=0,
+                 max_minibatches=M)
+    try:
+        s.set_params(w0[0])
+        losses = s.run(M, torch.from_numpy(X).to(dev), torch.from_numpy(Y).to(dev), want_losses=True)
+        W, V, _ = s.get_params()
+        tr = s.trace()
+    finally:
+        s.close()
+    _check(model, w0, X, Y, [W], [V], losses, [tr], v_hidden_tol=3e-2)
