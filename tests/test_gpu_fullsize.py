@@ -118,3 +118,30 @@ def test_vgg16_full_size_single_stage_bench_path(st):
     finally:
         s.close()
     _check(model, w0, X, Y, [W], [V], losses, [tr], v_hidden_tol=3e-2)
+
+
+def test_lstm_lm_full_size_single_stage_bench_path(st):
+    """BJ configs[2] at full size: embedding 10k × 1500 → 2 × LSTM(1500) → softmax over
+    10k, T = 35, batch 128 (4480 token rows), one stage through st_run (recurrent GEMMs
+    with split-K partials summed by the cell kernels, TMEM-A dW, the 4480 × 10 000 CE).
+    No ReLU or max decisions on this path, so V is gated tightly (measured 1.2e-5)."""
+    model = sd.config_lstm_lm(1)
+    M, B = 2, 128
+    w0 = sd.to_f32_params(sd.glorot_params(model, 0))
+    X, Y = sd.tokens(model.layers[0].n_in, M, B, model.seq_len, 1)
+    dev = torch.device("cuda", 0)
+    s = st.Stage(layers_of(model), model.cuts, 0, B, LR, 0.9, transport=st.ST_TRANSPORT_NCCL, device=0,
+                 max_minibatches=M, seq_len=model.seq_len)
+    try:
+        s.set_params(w0[0])
+        losses = s.run(M, torch.from_numpy(X).to(dev), torch.from_numpy(Y).to(dev), want_losses=True)
+        W, V, _ = s.get_params()
+        tr = s.trace()
+    finally:
+        s.close()
+    ref = O.run(model, sd.widen(w0), X, Y, float(np.float32(LR)), float(np.float32(0.9)))
+    assert tr == [e.as_tuple() for e in ref.trace[0]]
+    assert rel_l2(losses, ref.losses) <= 1e-4
+    assert rel_l2(W, ref.W[0]) <= 1e-4
+    rv = rel_l2(V, ref.V[0])
+    assert rv <= 1e-4, rv
