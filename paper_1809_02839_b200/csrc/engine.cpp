@@ -411,6 +411,7 @@ st_status ctx_init(const st_config* cfg, const st_buffers* bufs, void* stream, s
   for (auto& e : c->side_events) ST_CUDA_TRY(cudaEventCreateWithFlags(&e, cudaEventDisableTiming));
   if (const char* e = getenv("ST_DWU_SMS")) c->dwu_sms = std::max(1, atoi(e));
   if (const char* e = getenv("ST_CONV_OVERLAP")) c->conv_overlap = atoi(e) != 0;
+  if (const char* e = getenv("ST_PDL")) c->pdl = atoi(e) != 0;
   ST_CUDA_TRY(cudaMemsetAsync(c->V, 0, (size_t)c->P * 4, c->stream));
   ST_CUDA_TRY(cudaMemsetAsync(c->losses_dev, 0xff, (size_t)c->max_mb * 4, c->stream));  // NaN
   // GEMM workspace: split-K tile counters must start at zero (they self-reset afterwards)
@@ -612,6 +613,7 @@ static st_status lstm_forward(st_ctx* c, const LayerInfo& L, const float* Wh, co
       GemmArgs g = gargs_rows(c, B, H, 4 * H);
       g.act_lo = c->lstm_hlo;
       g.defer = &plan;
+      g.pdl = c->pdl;
       ST_TRY(gemm_fwd(g, h_prev, Wh + L.whh_off, nullptr, c->lstm_rec, 0));
       c->launches += gemm_last_launches();
     }
@@ -747,6 +749,7 @@ static st_status lstm_backward(st_ctx* c, const LayerInfo& L, const float* Wh, c
       GemmArgs g = gargs_rows(c, B, H, 4 * H);
       g.act_lo = c->lstm_dglo;
       g.defer = &plan;
+      g.pdl = c->pdl;
       ST_TRY(gemm_dx(g, c->lstm_dG + (size_t)t * B * 4 * H, Wh + L.whh_off, nullptr, c->lstm_dh));
       c->launches += gemm_last_launches();
     }

@@ -1452,6 +1452,11 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(TS_THREADS, 1)
   char* smem = align_smem_1k(smem_raw);
   char* ringA = smem;
   char* ringB = smem + TS_RA * TILE_BYTES;
+  // programmatic dependent launch (GemmArgs::pdl): let the next kernel of the stream launch
+  // now; this kernel's own dependency on its predecessor is waited for by the B producer
+  // only (the weights — operand A — are not written by the preceding kernel). Both are
+  // no-ops without the launch attribute.
+  if (threadIdx.x == 0) asm volatile("griddepcontrol.launch_dependents;" ::: "memory");
   uint64_t* bars = reinterpret_cast<uint64_t*>(ringB + TS2_RB * TS2_B_STAGE);
   const uint32_t a_full = smem_u32(bars);          // TMA landed (A, own)              [RA]
   const uint32_t a_free = a_full + 8 * TS_RA;      // converter read it (own)          [RA]
@@ -1540,6 +1545,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(TS_THREADS, 1)
   } else if (warp == 6) {
     // ---------------- TMA producer, activations: rows n0 + rank·bn/2 .. +bn/2 (hi + lo)
     {
+      asm volatile("griddepcontrol.wait;" ::: "memory");  // the activations come from the previous kernel
       const uint32_t bytes = (uint32_t)(2 * 2 * bh * BK * 4);  // both CTAs, hi + lo
       for (int i = 0; i < nkb; ++i) {
         const int s = i % TS2_RB;
@@ -2602,7 +2608,21 @@ st_status launch_ts(const GemmArgs& g, int M, int N, int K, const CUtensorMap& m
       ST_CUDA_TRY(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, ts2_smem_bytes()));
       attr_set[ts_split_acc()] = true;
     }
-    kern<<<grid, TS_THREADS, ts2_smem_bytes(), g.stream>>>(ma, mb, mblo, p);
+    if (g.pdl) {
+      cudaLaunchConfig_t cfg = {};
+      cfg.gridDim = grid;
+      cfg.blockDim = dim3(TS_THREADS);
+      cfg.dynamicSmemBytes = ts2_smem_bytes();
+      cfg.stream = g.stream;
+      cudaLaunchAttribute at[1];
+      at[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+      at[0].val.programmaticStreamSerializationAllowed = 1;
+      cfg.attrs = at;
+      cfg.numAttrs = 1;
+      ST_CUDA_TRY(cudaLaunchKernelEx(&cfg, kern, ma, mb, mblo, p));
+    } else {
+      kern<<<grid, TS_THREADS, ts2_smem_bytes(), g.stream>>>(ma, mb, mblo, p);
+    }
   } else {
     auto kern = tc_ts_kernel<EPI, A_MN>;
     static bool attr_set = false;

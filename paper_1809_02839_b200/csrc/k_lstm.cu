@@ -66,6 +66,10 @@ __device__ __forceinline__ void gemm_out(const float* direct, const SplitPlan& p
 __global__ void lstm_cell_fwd_kernel(float* __restrict__ gates, const float* __restrict__ rec, SplitPlan rp,
                                      const float* __restrict__ c_prev, float* __restrict__ c_out,
                                      float* __restrict__ h_out, float* __restrict__ h_lo, int B, int H) {
+  // programmatic dependent launch: the next recurrent GEMM may launch now; this kernel's
+  // inputs (the previous GEMM's partials) are complete only after the wait
+  asm volatile("griddepcontrol.launch_dependents;" ::: "memory");
+  asm volatile("griddepcontrol.wait;" ::: "memory");
   const int idx = blockIdx.x * blockDim.x + threadIdx.x;
   if (idx >= B * H) return;
   const int b = idx / H, j = idx % H;
@@ -95,6 +99,10 @@ __global__ void lstm_cell_bwd_kernel(const float* __restrict__ gates, const floa
                                      const float* __restrict__ c_prev, const float* __restrict__ dOut,
                                      const float* __restrict__ dh_next, SplitPlan hp, float* __restrict__ dc,
                                      int first, float* __restrict__ dG, float* __restrict__ dG_lo, int B, int H) {
+  // programmatic dependent launch: the next recurrent GEMM may launch now; this kernel's
+  // inputs (the previous GEMM's partials) are complete only after the wait
+  asm volatile("griddepcontrol.launch_dependents;" ::: "memory");
+  asm volatile("griddepcontrol.wait;" ::: "memory");
   const int idx = blockIdx.x * blockDim.x + threadIdx.x;
   if (idx >= B * H) return;
   const int b = idx / H, j = idx % H;
@@ -184,6 +192,10 @@ __device__ __forceinline__ void gemm_out4(const float* direct, const SplitPlan& 
 __global__ void lstm_cell_fwd4_kernel(float* __restrict__ gates, const float* __restrict__ rec, SplitPlan rp,
                                       const float* __restrict__ c_prev, float* __restrict__ c_out,
                                       float* __restrict__ h_out, float* __restrict__ h_lo, int B, int H) {
+  // programmatic dependent launch: the next recurrent GEMM may launch now; this kernel's
+  // inputs (the previous GEMM's partials) are complete only after the wait
+  asm volatile("griddepcontrol.launch_dependents;" ::: "memory");
+  asm volatile("griddepcontrol.wait;" ::: "memory");
   const int H4 = H / 4;
   const int idx = blockIdx.x * blockDim.x + threadIdx.x;
   if (idx >= B * H4) return;
@@ -224,6 +236,10 @@ __global__ void lstm_cell_bwd4_kernel(const float* __restrict__ gates, const flo
                                       const float* __restrict__ c_prev, const float* __restrict__ dOut,
                                       const float* __restrict__ dh_next, SplitPlan hp, float* __restrict__ dc,
                                       int first, float* __restrict__ dG, float* __restrict__ dG_lo, int B, int H) {
+  // programmatic dependent launch: the next recurrent GEMM may launch now; this kernel's
+  // inputs (the previous GEMM's partials) are complete only after the wait
+  asm volatile("griddepcontrol.launch_dependents;" ::: "memory");
+  asm volatile("griddepcontrol.wait;" ::: "memory");
   const int H4 = H / 4;
   const int idx = blockIdx.x * blockDim.x + threadIdx.x;
   if (idx >= B * H4) return;
@@ -342,16 +358,35 @@ __global__ void embed_grad_kernel(const float* __restrict__ dA, const int* __res
 
 }  // namespace
 
+// 256-thread launch of a cell kernel as a programmatic dependent of the preceding kernel
+static cudaLaunchConfig_t pdl_config(int blocks, cudaStream_t s) {
+  cudaLaunchConfig_t cfg = {};
+  cfg.gridDim = dim3(blocks);
+  cfg.blockDim = dim3(256);
+  cfg.dynamicSmemBytes = 0;
+  cfg.stream = s;
+  return cfg;
+}
+static void pdl_attr(cudaLaunchConfig_t& cfg, cudaLaunchAttribute* at) {
+  at[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+  at[0].val.programmaticStreamSerializationAllowed = 1;
+  cfg.attrs = at;
+  cfg.numAttrs = 1;
+}
+
 st_status launch_lstm_cell_fwd(float* gates, const float* rec, const SplitPlan* rp, const float* c_prev, float* c_out,
                                float* h_out, float* h_lo, int B, int H, cudaStream_t s) {
   const int n = B * H;
   const SplitPlan p = rp ? *rp : SplitPlan{};
   const bool v4 = H % 4 == 0 && ((uintptr_t)gates | (uintptr_t)rec | (uintptr_t)c_prev | (uintptr_t)c_out |
                                  (uintptr_t)h_out | (uintptr_t)h_lo | (uintptr_t)p.ws) % 16 == 0;
+  cudaLaunchConfig_t cfg = pdl_config(v4 ? (n / 4 + 255) / 256 : (n + 255) / 256, s);
+  cudaLaunchAttribute at[1];
+  pdl_attr(cfg, at);
   if (v4)
-    lstm_cell_fwd4_kernel<<<(n / 4 + 255) / 256, 256, 0, s>>>(gates, rec, p, c_prev, c_out, h_out, h_lo, B, H);
+    ST_CUDA_TRY(cudaLaunchKernelEx(&cfg, lstm_cell_fwd4_kernel, gates, rec, p, c_prev, c_out, h_out, h_lo, B, H));
   else
-    lstm_cell_fwd_kernel<<<(n + 255) / 256, 256, 0, s>>>(gates, rec, p, c_prev, c_out, h_out, h_lo, B, H);
+    ST_CUDA_TRY(cudaLaunchKernelEx(&cfg, lstm_cell_fwd_kernel, gates, rec, p, c_prev, c_out, h_out, h_lo, B, H));
   ST_CUDA_TRY(cudaGetLastError());
   return ST_OK;
 }
@@ -364,12 +399,15 @@ st_status launch_lstm_cell_bwd(const float* gates, const float* c_t, const float
   const bool v4 = H % 4 == 0 && ((uintptr_t)gates | (uintptr_t)c_t | (uintptr_t)c_prev | (uintptr_t)dOut |
                                  (uintptr_t)dh_next | (uintptr_t)dc | (uintptr_t)dG | (uintptr_t)dG_lo |
                                  (uintptr_t)p.ws) % 16 == 0;
+  cudaLaunchConfig_t cfg = pdl_config(v4 ? (n / 4 + 255) / 256 : (n + 255) / 256, s);
+  cudaLaunchAttribute at[1];
+  pdl_attr(cfg, at);
   if (v4)
-    lstm_cell_bwd4_kernel<<<(n / 4 + 255) / 256, 256, 0, s>>>(gates, c_t, c_prev, dOut, dh_next, p, dc, first, dG,
-                                                               dG_lo, B, H);
+    ST_CUDA_TRY(cudaLaunchKernelEx(&cfg, lstm_cell_bwd4_kernel, gates, c_t, c_prev, dOut, dh_next, p, dc, first, dG,
+                                   dG_lo, B, H));
   else
-    lstm_cell_bwd_kernel<<<(n + 255) / 256, 256, 0, s>>>(gates, c_t, c_prev, dOut, dh_next, p, dc, first, dG, dG_lo,
-                                                          B, H);
+    ST_CUDA_TRY(cudaLaunchKernelEx(&cfg, lstm_cell_bwd_kernel, gates, c_t, c_prev, dOut, dh_next, p, dc, first, dG,
+                                   dG_lo, B, H));
   ST_CUDA_TRY(cudaGetLastError());
   return ST_OK;
 }

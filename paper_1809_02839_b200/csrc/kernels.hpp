@@ -61,6 +61,9 @@ struct GemmArgs {
   // already computed by its producer (same pitch as the operand); NULL: split here
   const float* act_lo = nullptr;
   SplitPlan* defer = nullptr;  // non-NULL: K-split partials are left for the consumer (see SplitPlan)
+  // CTA-pair fwd / dX: launch as a programmatic dependent (the weights stream in while the
+  // previous kernel — e.g. the LSTM cell producing this step's h — finishes)
+  bool pdl = false;
 };
 int64_t gemm_workspace_bytes(int B, int max_in, int max_out);
 st_status gemm_fwd(const GemmArgs& g, const float* X, const float* W, const float* bias, float* Z, int relu);
