@@ -412,6 +412,7 @@ st_status ctx_init(const st_config* cfg, const st_buffers* bufs, void* stream, s
   if (const char* e = getenv("ST_DWU_SMS")) c->dwu_sms = std::max(1, atoi(e));
   if (const char* e = getenv("ST_CONV_OVERLAP")) c->conv_overlap = atoi(e) != 0;
   if (const char* e = getenv("ST_PDL")) c->pdl = atoi(e) != 0;
+  if (const char* e = getenv("ST_PDL_DENSE")) c->pdl_dense = atoi(e) != 0;
   ST_CUDA_TRY(cudaMemsetAsync(c->V, 0, (size_t)c->P * 4, c->stream));
   ST_CUDA_TRY(cudaMemsetAsync(c->losses_dev, 0xff, (size_t)c->max_mb * 4, c->stream));  // NaN
   // GEMM workspace: split-K tile counters must start at zero (they self-reset afterwards)
@@ -566,6 +567,7 @@ static GemmArgs gargs(st_ctx* c, const LayerInfo& L) {
   g.work = c->gemm_ws;
   g.work_bytes = gemm_workspace_bytes((int)c->gemm_rows_max, c->gemm_in_max, c->gemm_out_max);
   g.stream = c->stream;
+  g.pdl = c->pdl_dense;  // dense fwd / dX chains on the main stream (split-lo → GEMM → reduce)
   return g;
 }
 

@@ -1692,6 +1692,8 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(TS_THREADS, 1)
 template <int EPI>
 __global__ void splitk_epilogue_kernel(const float* __restrict__ ws, int splits, int tiles, int mt_grid, int M, int N,
                                        float* __restrict__ out, const float* __restrict__ aux, int relu, int row) {
+  asm volatile("griddepcontrol.launch_dependents;" ::: "memory");
+  asm volatile("griddepcontrol.wait;" ::: "memory");  // the partials of the preceding GEMM
   const int64_t total = (int64_t)M * N;
   const size_t split_stride = (size_t)tiles * BNMAX * BM;
   for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < total; i += (int64_t)gridDim.x * blockDim.x) {
@@ -1721,19 +1723,41 @@ __global__ void splitk_epilogue_kernel(const float* __restrict__ ws, int splits,
   }
 }
 
+// cudaLaunchKernelEx with programmatic stream serialization when pdl (GemmArgs::pdl)
+template <typename... KArgs, typename... Args>
+st_status launch_maybe_pdl(bool pdl, void (*kern)(KArgs...), dim3 grid, dim3 block, size_t smem, cudaStream_t s,
+                           Args... args) {
+  cudaLaunchConfig_t cfg = {};
+  cfg.gridDim = grid;
+  cfg.blockDim = block;
+  cfg.dynamicSmemBytes = smem;
+  cfg.stream = s;
+  cudaLaunchAttribute at[1];
+  if (pdl) {
+    at[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+    at[0].val.programmaticStreamSerializationAllowed = 1;
+    cfg.attrs = at;
+    cfg.numAttrs = 1;
+  }
+  ST_CUDA_TRY(cudaLaunchKernelEx(&cfg, kern, static_cast<KArgs>(args)...));
+  return ST_OK;
+}
+
 template <int EPI>
-st_status launch_splitk_epilogue(const TcParams& p, int tiles, int mt_grid, cudaStream_t s) {
+st_status launch_splitk_epilogue(const TcParams& p, int tiles, int mt_grid, cudaStream_t s, bool pdl = false) {
   const int64_t total = (int64_t)p.M * p.N;
   const int blocks = (int)std::min<int64_t>((total + 255) / 256, 148 * 8);
-  splitk_epilogue_kernel<EPI><<<blocks, 256, 0, s>>>(p.ws, p.splits, tiles, mt_grid, p.M, p.N, p.out, p.aux, p.relu,
-                                                    p.row);
-  ST_CUDA_TRY(cudaGetLastError());
-  return ST_OK;
+  return launch_maybe_pdl(pdl, splitk_epilogue_kernel<EPI>, dim3(blocks), dim3(256), 0, s, p.ws, p.splits, tiles,
+                          mt_grid, p.M, p.N, p.out, p.aux, p.relu, p.row);
 }
 
 // lo = x − trunc_tf32(x) of a whole [rows × pitch] activation matrix (the B operand
 // of the FP32X3 forward / dX GEMMs), computed once per GEMM.
 __global__ void split_lo_kernel(const float4* __restrict__ x, float4* __restrict__ lo, size_t n4) {
+  // programmatic dependent launch (no-ops without the attribute): successor may launch;
+  // x is complete only after the wait
+  asm volatile("griddepcontrol.launch_dependents;" ::: "memory");
+  asm volatile("griddepcontrol.wait;" ::: "memory");
   for (size_t i = blockIdx.x * (size_t)blockDim.x + threadIdx.x; i < n4; i += (size_t)gridDim.x * blockDim.x) {
     const float4 v = x[i];
     lo[i] = make_float4(lo_part(v.x), lo_part(v.y), lo_part(v.z), lo_part(v.w));
@@ -2585,9 +2609,9 @@ st_status launch_ts(const GemmArgs& g, int M, int N, int K, const CUtensorMap& m
     blo = const_cast<float*>(g.act_lo);  // the producer already split the operand
   } else {
     const size_t n4 = (size_t)N * K / 4;
-    split_lo_kernel<<<std::min<size_t>(4 * 148, (n4 + 255) / 256), 256, 0, g.stream>>>(
-        reinterpret_cast<const float4*>(Bact), reinterpret_cast<float4*>(blo), n4);
-    ST_CUDA_TRY(cudaGetLastError());
+    ST_TRY(launch_maybe_pdl(g.pdl, split_lo_kernel, dim3((unsigned)std::min<size_t>(4 * 148, (n4 + 255) / 256)),
+                            dim3(256), 0, g.stream, reinterpret_cast<const float4*>(Bact),
+                            reinterpret_cast<float4*>(blo), n4));
     ++launches;
   }
   const int brows = pair ? p.bn / 2 : p.bn;
@@ -2642,7 +2666,7 @@ st_status launch_ts(const GemmArgs& g, int M, int N, int K, const CUtensorMap& m
     g.defer->bm = BM;
     g.defer->bn = BNMAX;
   } else if (p.ext_reduce) {
-    ST_TRY(launch_splitk_epilogue<EPI>(p, mt_grid * nt, mt_grid, g.stream));
+    ST_TRY(launch_splitk_epilogue<EPI>(p, mt_grid * nt, mt_grid, g.stream, g.pdl));
     g_launches = launches + 1;
   }
   return ST_OK;
