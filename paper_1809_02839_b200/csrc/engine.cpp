@@ -588,6 +588,7 @@ static GemmArgs gargs_rows(st_ctx* c, int rows, int n_in, int n_out) {
   g.work = c->gemm_ws;
   g.work_bytes = gemm_workspace_bytes((int)c->gemm_rows_max, c->gemm_in_max, c->gemm_out_max);
   g.stream = c->stream;
+  g.pdl = c->pdl_dense;
   return g;
 }
 

@@ -1,6 +1,8 @@
 // GEMM dispatch for the stage path: tcgen05 tensor-core kernels (k_gemm_tc.cu)
 // for ST_GEMM_FP32X3 / ST_GEMM_TF32, CUDA-core fp32 (k_gemm_simt.cu) for
 // ST_GEMM_SIMT. Same contract for every mode (kernels.hpp).
+#include <cstdlib>
+
 #include "kernels.hpp"
 
 namespace st {
@@ -20,6 +22,15 @@ st_status tc_dw_update(const GemmArgs& g, const float* X, const float* dZ, const
 int simt_last_launches();
 
 static thread_local int g_last_launches = 0;
+
+bool pdl_enabled() {
+  static int f = -1;
+  if (f < 0) {
+    const char* e = getenv("ST_PDL_DENSE");
+    f = (e && atoi(e) == 0) ? 0 : 1;
+  }
+  return f != 0;
+}
 int gemm_last_launches() { return g_last_launches; }
 
 int64_t gemm_workspace_bytes(int B, int max_in, int max_out) { return tc_workspace_bytes(B, max_in, max_out); }

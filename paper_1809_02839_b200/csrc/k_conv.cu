@@ -90,6 +90,7 @@ __global__ void col2im_kernel(const float* __restrict__ dcol, int B, int H, int 
 // after them; one thread per pixel, eight float4 stores (C a template: static indices).
 template <int C>
 __global__ void im2col_pad32_kernel(const float* __restrict__ X, int B, int H, int W, float* __restrict__ col) {
+  PDL_PROLOGUE();
   const int total = B * H * W;
   for (int p = blockIdx.x * blockDim.x + threadIdx.x; p < total; p += gridDim.x * blockDim.x) {
     const int w = p % W, h = (p / W) % H, b = p / (W * H);
@@ -113,6 +114,7 @@ __global__ void im2col_pad32_kernel(const float* __restrict__ X, int B, int H, i
 
 template <typename IDX>
 __global__ void maxpool_fwd_kernel(const float* __restrict__ X, int B, int H, int W, int C, float* __restrict__ Y) {
+  PDL_PROLOGUE();
   const int Ho = H / 2, Wo = W / 2;
   const IDX total = (IDX)B * Ho * Wo * C;
   for (IDX i = blockIdx.x * (IDX)blockDim.x + threadIdx.x; i < total; i += (IDX)gridDim.x * blockDim.x) {
@@ -134,6 +136,7 @@ __global__ void maxpool_fwd_kernel(const float* __restrict__ X, int B, int H, in
 template <typename IDX>
 __global__ void maxpool_bwd_kernel(const float* __restrict__ X, const float* __restrict__ dY, int B, int H, int W,
                                    int C, int relu_mask, float* __restrict__ dX) {
+  PDL_PROLOGUE();
   const int Ho = H / 2, Wo = W / 2;
   const IDX total = (IDX)B * Ho * Wo * C;
   for (IDX i = blockIdx.x * (IDX)blockDim.x + threadIdx.x; i < total; i += (IDX)gridDim.x * blockDim.x) {
@@ -191,9 +194,9 @@ st_status launch_im2col_pad32(const float* X, int B, int H, int W, int C, float*
   if (9 * C > 32) return set_error(ST_ERR_INPUT, "im2col_pad32: 9·C = %d > 32", 9 * C);
   const int64_t n = (int64_t)B * H * W;
   switch (C) {
-    case 1: im2col_pad32_kernel<1><<<blocks_for(n), 256, 0, s>>>(X, B, H, W, col); break;
-    case 2: im2col_pad32_kernel<2><<<blocks_for(n), 256, 0, s>>>(X, B, H, W, col); break;
-    default: im2col_pad32_kernel<3><<<blocks_for(n), 256, 0, s>>>(X, B, H, W, col); break;
+    case 1: ST_TRY(launch_pdl(pdl_enabled(), im2col_pad32_kernel<1>, dim3(blocks_for(n)), dim3(256), 0, s, X, B, H, W, col)); break;
+    case 2: ST_TRY(launch_pdl(pdl_enabled(), im2col_pad32_kernel<2>, dim3(blocks_for(n)), dim3(256), 0, s, X, B, H, W, col)); break;
+    default: ST_TRY(launch_pdl(pdl_enabled(), im2col_pad32_kernel<3>, dim3(blocks_for(n)), dim3(256), 0, s, X, B, H, W, col)); break;
   }
   ST_CUDA_TRY(cudaGetLastError());
   return ST_OK;
@@ -216,8 +219,8 @@ st_status launch_col2im(const float* dcol, int B, int H, int W, int C, const flo
 
 st_status launch_maxpool_fwd(const float* X, int B, int H, int W, int C, float* Y, cudaStream_t s) {
   const int64_t n = (int64_t)B * (H / 2) * (W / 2) * C;
-  if (n * 4 < kI32) maxpool_fwd_kernel<int><<<blocks_for(n), 256, 0, s>>>(X, B, H, W, C, Y);
-  else maxpool_fwd_kernel<int64_t><<<blocks_for(n), 256, 0, s>>>(X, B, H, W, C, Y);
+  if (n * 4 < kI32) ST_TRY(launch_pdl(pdl_enabled(), maxpool_fwd_kernel<int>, dim3(blocks_for(n)), dim3(256), 0, s, X, B, H, W, C, Y));
+  else ST_TRY(launch_pdl(pdl_enabled(), maxpool_fwd_kernel<int64_t>, dim3(blocks_for(n)), dim3(256), 0, s, X, B, H, W, C, Y));
   ST_CUDA_TRY(cudaGetLastError());
   return ST_OK;
 }
@@ -225,8 +228,12 @@ st_status launch_maxpool_fwd(const float* X, int B, int H, int W, int C, float* 
 st_status launch_maxpool_bwd(const float* X, const float* dY, int B, int H, int W, int C, int relu_mask, float* dX,
                              cudaStream_t s) {
   const int64_t n = (int64_t)B * (H / 2) * (W / 2) * C;
-  if (n * 4 < kI32) maxpool_bwd_kernel<int><<<blocks_for(n), 256, 0, s>>>(X, dY, B, H, W, C, relu_mask, dX);
-  else maxpool_bwd_kernel<int64_t><<<blocks_for(n), 256, 0, s>>>(X, dY, B, H, W, C, relu_mask, dX);
+  if (n * 4 < kI32)
+    ST_TRY(launch_pdl(pdl_enabled(), maxpool_bwd_kernel<int>, dim3(blocks_for(n)), dim3(256), 0, s, X, dY, B, H, W, C,
+                      relu_mask, dX));
+  else
+    ST_TRY(launch_pdl(pdl_enabled(), maxpool_bwd_kernel<int64_t>, dim3(blocks_for(n)), dim3(256), 0, s, X, dY, B, H,
+                      W, C, relu_mask, dX));
   ST_CUDA_TRY(cudaGetLastError());
   return ST_OK;
 }

@@ -153,6 +153,7 @@ __global__ void __launch_bounds__(256) colsum_partial_kernel(const float* __rest
 __global__ void __launch_bounds__(256) colsum4_partial_kernel(const float* __restrict__ dZ, int rows, int n_out,
                                                               int rpb, float* __restrict__ part) {
   __shared__ float4 sm[32][9];
+  PDL_PROLOGUE();
   const int tx = threadIdx.x & 7, ty = threadIdx.x >> 3;
   const int o = blockIdx.x * 32 + tx * 4;
   const int r0 = blockIdx.y * rpb, r1 = min(rows, r0 + rpb);
@@ -220,8 +221,11 @@ int launch_bias_grad(const float* dZ, int rows, int n_out, float* gb, void* work
     float* part = reinterpret_cast<float*>(static_cast<char*>(work) + 64 * 1024);
     // pass 2 is the same column sum over the [nb × n_out] partials as one row block
     if ((n_out & 3) == 0 && (((uintptr_t)dZ | (uintptr_t)gb) & 15) == 0) {
-      colsum4_partial_kernel<<<dim3(cb, nb), 256, 0, s>>>(dZ, rows, n_out, rpb, part);
-      colsum4_partial_kernel<<<dim3(cb, 1), 256, 0, s>>>(part, nb, n_out, nb, gb);
+      if (launch_pdl(pdl_enabled(), colsum4_partial_kernel, dim3(cb, nb), dim3(256), 0, s, dZ, rows, n_out, rpb,
+                     part) != ST_OK ||
+          launch_pdl(pdl_enabled(), colsum4_partial_kernel, dim3(cb, 1), dim3(256), 0, s, part, nb, n_out, nb, gb) !=
+              ST_OK)
+        return -1;
     } else {
       colsum_partial_kernel<<<dim3(cb, nb), 256, 0, s>>>(dZ, rows, n_out, rpb, part);
       colsum_partial_kernel<<<dim3(cb, 1), 256, 0, s>>>(part, nb, n_out, nb, gb);

@@ -847,8 +847,11 @@ __global__ void __launch_bounds__(kPThreads, 1)
   const uint32_t tmem = *tmem_slot;
   const uint32_t tmemA = tmem + 2 * AW;  // NS slots of 64 columns
 
+  if (threadIdx.x == 0) asm volatile("griddepcontrol.launch_dependents;" ::: "memory");
   if (warp == 0) {
-    // ---------------- TMA producer
+    // ---------------- TMA producer (programmatic dependent launch: operands only after the
+    // predecessor completed; a no-op without the launch attribute)
+    asm volatile("griddepcontrol.wait;" ::: "memory");
     const uint32_t bytes = (uint32_t)(TILE_BYTES + (B_MN ? nbox_b * 4096 : bn * BK * 4));
     int it = 0;
     for (int u = blockIdx.x; u < units; u += gridDim.x) {
@@ -2485,11 +2488,11 @@ st_status launch(const GemmArgs& g, int M, int N, int K, const CUtensorMap& ma, 
     // accumulators that overlap the epilogue (ST_GEMM_DEV_FLAGS=1024 forces it everywhere)
     p.split_acc = (EPI == EPI_DW || (p.dev_flags & 1024)) ? 1 : 0;
     const int budget = g.max_ctas > 0 ? std::min(g.max_ctas, num_sms()) : num_sms();
-    ck<<<std::min(tiles * p.splits, budget), kPThreads, smem, g.stream>>>(ma, mb, p, mt, tiles);
-    ST_CUDA_TRY(cudaGetLastError());
+    ST_TRY(launch_maybe_pdl(g.pdl, ck, dim3(std::min(tiles * p.splits, budget)), dim3(kPThreads), (size_t)smem,
+                            g.stream, ma, mb, p, mt, tiles));
     g_launches = 1;
     if (p.ext_reduce) {
-      ST_TRY(launch_splitk_epilogue<EPI>(p, tiles, mt, g.stream));
+      ST_TRY(launch_splitk_epilogue<EPI>(p, tiles, mt, g.stream, g.pdl));
       g_launches = 2;
     }
     return ST_OK;

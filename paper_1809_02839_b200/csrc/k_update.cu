@@ -53,6 +53,7 @@ __global__ void __launch_bounds__(kThreads) update_predict_kernel(float4* __rest
                                                                   float* __restrict__ Vs, const float* __restrict__ Gs,
                                                                   float* __restrict__ WFs, float* __restrict__ WBs,
                                                                   int head, size_t tail0, int tail) {
+  PDL_PROLOGUE();
   const size_t stride = (size_t)gridDim.x * kThreads * kUnroll;
   for (size_t base = (size_t)blockIdx.x * kThreads * kUnroll + threadIdx.x; base < n4; base += stride) {
     float4 w[kUnroll], v[kUnroll], g[kUnroll], wf[kUnroll], wb[kUnroll];
@@ -127,18 +128,20 @@ st_status launch_update_predict(float* W, float* V, const float* G, float* WF, f
   auto G4 = reinterpret_cast<const float4*>(G + head);
   auto F4 = WF ? reinterpret_cast<float4*>(WF + head) : nullptr;
   auto B4 = WB ? reinterpret_cast<float4*>(WB + head) : nullptr;
+  st_status st = ST_OK;
   if (WF && WB)
-    update_predict_kernel<true, true><<<grid, kThreads, 0, s>>>(W4, V4, G4, F4, B4, n4, c, W, V, G, WF, WB, head,
+    st = launch_pdl(pdl_enabled(), update_predict_kernel<true, true>, dim3(grid), dim3(kThreads), 0, s, W4, V4, G4, F4, B4, n4, c, W, V, G, WF, WB, head,
                                                                 tail0, tail);
   else if (WF)
-    update_predict_kernel<true, false><<<grid, kThreads, 0, s>>>(W4, V4, G4, F4, B4, n4, c, W, V, G, WF, WB, head,
+    st = launch_pdl(pdl_enabled(), update_predict_kernel<true, false>, dim3(grid), dim3(kThreads), 0, s, W4, V4, G4, F4, B4, n4, c, W, V, G, WF, WB, head,
                                                                  tail0, tail);
   else if (WB)
-    update_predict_kernel<false, true><<<grid, kThreads, 0, s>>>(W4, V4, G4, F4, B4, n4, c, W, V, G, WF, WB, head,
+    st = launch_pdl(pdl_enabled(), update_predict_kernel<false, true>, dim3(grid), dim3(kThreads), 0, s, W4, V4, G4, F4, B4, n4, c, W, V, G, WF, WB, head,
                                                                  tail0, tail);
   else
-    update_predict_kernel<false, false><<<grid, kThreads, 0, s>>>(W4, V4, G4, F4, B4, n4, c, W, V, G, WF, WB, head,
+    st = launch_pdl(pdl_enabled(), update_predict_kernel<false, false>, dim3(grid), dim3(kThreads), 0, s, W4, V4, G4, F4, B4, n4, c, W, V, G, WF, WB, head,
                                                                   tail0, tail);
+  ST_TRY(st);
   ST_CUDA_TRY(cudaGetLastError());
   return ST_OK;
 }

@@ -6,6 +6,36 @@
 
 namespace st {
 
+// ---- programmatic dependent launch -------------------------------------------------
+// Kernels that begin with PDL_PROLOGUE (trigger the successor, then wait for the
+// predecessor's completion before touching memory) may be launched with programmatic
+// stream serialization: their launch and ramp overlap the predecessor's tail.
+// ST_PDL_DENSE=0 disables it for the stage paths.
+#define PDL_PROLOGUE()                                               \
+  do {                                                               \
+    asm volatile("griddepcontrol.launch_dependents;" ::: "memory"); \
+    asm volatile("griddepcontrol.wait;" ::: "memory");              \
+  } while (0)
+bool pdl_enabled();
+template <typename... KArgs, typename... Args>
+inline st_status launch_pdl(bool pdl, void (*kern)(KArgs...), dim3 grid, dim3 block, size_t smem, cudaStream_t s,
+                            Args... args) {
+  cudaLaunchConfig_t cfg = {};
+  cfg.gridDim = grid;
+  cfg.blockDim = block;
+  cfg.dynamicSmemBytes = smem;
+  cfg.stream = s;
+  cudaLaunchAttribute at[1];
+  if (pdl) {
+    at[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+    at[0].val.programmaticStreamSerializationAllowed = 1;
+    cfg.attrs = at;
+    cfg.numAttrs = 1;
+  }
+  ST_CUDA_TRY(cudaLaunchKernelEx(&cfg, kern, static_cast<KArgs>(args)...));
+  return ST_OK;
+}
+
 // ---- K-B: fused smoothed-gradient update + apply + weight prediction --------
 // (Eq. 1, D1 apply, Eq. 4 P:326-328 for s_F and s_B)
 struct UpdateConsts {
