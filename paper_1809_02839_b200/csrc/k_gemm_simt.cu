@@ -21,6 +21,7 @@ __global__ void __launch_bounds__(256) sgemm_kernel(int M, int N, int K, const f
                                                     int64_t a_sk, const float* __restrict__ Bm, int64_t b_sk,
                                                     int64_t b_sn, float* __restrict__ C, int64_t c_sm, int64_t c_sn,
                                                     const float* __restrict__ aux, int relu, int k_chunk) {
+  PDL_PROLOGUE();
   __shared__ float As[TK][TM + 4];
   __shared__ float Bs[TK][TN + 4];
   const int tid = threadIdx.x;
@@ -90,6 +91,7 @@ __global__ void __launch_bounds__(256) sgemm_kernel(int M, int N, int K, const f
 // Fixed-order reduction of split-K partials + the real epilogue.
 __global__ void splitk_reduce_kernel(const float* __restrict__ ws, int splits, int M, int N, float* __restrict__ C,
                                      int64_t c_sm, int64_t c_sn, int epi, const float* __restrict__ aux, int relu) {
+  PDL_PROLOGUE();
   const int idx = blockIdx.x * blockDim.x + threadIdx.x;
   if (idx >= M * N) return;
   const int m = idx / N, n = idx % N;
@@ -107,6 +109,7 @@ __global__ void splitk_reduce_kernel(const float* __restrict__ ws, int splits, i
 // g_b[o] = Σ_b dZ[b][o]: 32 columns per CTA × 8 row groups, fixed-order combine.
 __global__ void __launch_bounds__(256) bias_grad_kernel(const float* __restrict__ dZ, int B, int n_out,
                                                         float* __restrict__ gb) {
+  PDL_PROLOGUE();
   __shared__ float part[8][33];
   const int tx = threadIdx.x & 31, ty = threadIdx.x >> 5;
   const int o = blockIdx.x * 32 + tx;
@@ -232,7 +235,7 @@ int launch_bias_grad(const float* dZ, int rows, int n_out, float* gb, void* work
     }
     return cudaGetLastError() == cudaSuccess ? 2 : -1;
   }
-  bias_grad_kernel<<<cb, 256, 0, s>>>(dZ, rows, n_out, gb);
+  if (launch_pdl(pdl_enabled(), bias_grad_kernel, dim3(cb), dim3(256), 0, s, dZ, rows, n_out, gb) != ST_OK) return -1;
   return cudaGetLastError() == cudaSuccess ? 1 : -1;
 }
 
@@ -254,8 +257,8 @@ st_status run(int M, int N, int K, const float* A, int64_t a_sm, int64_t a_sk, c
   while (splits > 1 && need > work_bytes - 64 * 1024) --splits;
   dim3 grid((N + TN - 1) / TN, (M + TM - 1) / TM, std::max(1, splits));
   if (splits <= 1) {
-    sgemm_kernel<EPI><<<grid, 256, 0, s>>>(M, N, K, A, a_sm, a_sk, Bm, b_sk, b_sn, C, c_sm, c_sn, aux, relu, K);
-    ST_CUDA_TRY(cudaGetLastError());
+    ST_TRY(launch_pdl(pdl_enabled(), sgemm_kernel<EPI>, grid, dim3(256), 0, s, M, N, K, A, a_sm, a_sk, Bm, b_sk, b_sn,
+                      C, c_sm, c_sn, aux, relu, K));
     g_simt_launches = 1;
     return ST_OK;
   }
@@ -263,11 +266,10 @@ st_status run(int M, int N, int K, const float* A, int64_t a_sm, int64_t a_sk, c
   splits = (K + chunk - 1) / chunk;
   grid.z = splits;
   float* ws = reinterpret_cast<float*>(static_cast<char*>(work) + 64 * 1024);
-  sgemm_kernel<EPI_PARTIAL><<<grid, 256, 0, s>>>(M, N, K, A, a_sm, a_sk, Bm, b_sk, b_sn, ws, c_sm, c_sn, nullptr, 0,
-                                                 chunk);
-  ST_CUDA_TRY(cudaGetLastError());
-  splitk_reduce_kernel<<<(M * N + 255) / 256, 256, 0, s>>>(ws, splits, M, N, C, c_sm, c_sn, EPI, aux, relu);
-  ST_CUDA_TRY(cudaGetLastError());
+  ST_TRY(launch_pdl(pdl_enabled(), sgemm_kernel<EPI_PARTIAL>, grid, dim3(256), 0, s, M, N, K, A, a_sm, a_sk, Bm, b_sk,
+                    b_sn, ws, c_sm, c_sn, (const float*)nullptr, 0, chunk));
+  ST_TRY(launch_pdl(pdl_enabled(), splitk_reduce_kernel, dim3((M * N + 255) / 256), dim3(256), 0, s, ws, splits, M, N,
+                    C, c_sm, c_sn, EPI, aux, relu));
   g_simt_launches = 2;
   return ST_OK;
 }

@@ -22,6 +22,7 @@ __device__ __forceinline__ float warp_sum(float v) {
 __global__ void __launch_bounds__(256) ce_rows_kernel(const float* __restrict__ Z, const int32_t* __restrict__ y,
                                                       int B, int C, float inv_b, float* __restrict__ rowloss,
                                                       float* __restrict__ dZ) {
+  PDL_PROLOGUE();
   const int warp = (blockIdx.x * blockDim.x + threadIdx.x) >> 5;
   const int lane = threadIdx.x & 31;
   if (warp >= B) return;
@@ -44,6 +45,7 @@ __global__ void __launch_bounds__(256) ce_rows_kernel(const float* __restrict__ 
 
 __global__ void __launch_bounds__(1024) mean_kernel(const float* __restrict__ rowloss, int B, float inv_b,
                                                     float* __restrict__ out) {
+  PDL_PROLOGUE();
   // fixed-order: thread t sums rows t, t+1024, ...; then a fixed tree
   __shared__ float part[1024];
   float acc = 0.f;
@@ -64,11 +66,9 @@ st_status launch_softmax_ce(const float* Z, const int32_t* y, int B, int C, floa
   if (B <= 0 || C <= 0) return set_error(ST_ERR_INPUT, "softmax_ce: B=%d C=%d", B, C);
   const float inv_b = 1.0f / (float)B;
   const int warps_per_cta = 8;
-  ce_rows_kernel<<<(B + warps_per_cta - 1) / warps_per_cta, 32 * warps_per_cta, 0, s>>>(Z, y, B, C, inv_b,
-                                                                                       rowloss, dZ);
-  ST_CUDA_TRY(cudaGetLastError());
-  mean_kernel<<<1, 1024, 0, s>>>(rowloss, B, inv_b, loss_out);
-  ST_CUDA_TRY(cudaGetLastError());
+  ST_TRY(launch_pdl(pdl_enabled(), ce_rows_kernel, dim3((B + warps_per_cta - 1) / warps_per_cta),
+                    dim3(32 * warps_per_cta), 0, s, Z, y, B, C, inv_b, rowloss, dZ));
+  ST_TRY(launch_pdl(pdl_enabled(), mean_kernel, dim3(1), dim3(1024), 0, s, rowloss, B, inv_b, loss_out));
   return ST_OK;
 }
 
