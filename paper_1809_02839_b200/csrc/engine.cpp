@@ -413,6 +413,13 @@ st_status ctx_init(const st_config* cfg, const st_buffers* bufs, void* stream, s
   if (const char* e = getenv("ST_CONV_OVERLAP")) c->conv_overlap = atoi(e) != 0;
   if (const char* e = getenv("ST_PDL")) c->pdl = atoi(e) != 0;
   if (const char* e = getenv("ST_PDL_DENSE")) c->pdl_dense = atoi(e) != 0;
+  // several stage contexts sharing one GPU (LOCAL transport): their kernels interleave
+  // across streams and waiting dependents would hold SMs the other stages need
+  // (wide FCN at 2 co-located stages 45.8k → 41.8k samples/s with it)
+  if (c->transport_kind == ST_TRANSPORT_LOCAL && c->N > 1) {
+    c->pdl_dense = false;
+    c->pdl = false;
+  }
   ST_CUDA_TRY(cudaMemsetAsync(c->V, 0, (size_t)c->P * 4, c->stream));
   ST_CUDA_TRY(cudaMemsetAsync(c->losses_dev, 0xff, (size_t)c->max_mb * 4, c->stream));  // NaN
   // GEMM workspace: split-K tile counters must start at zero (they self-reset afterwards)
@@ -567,7 +574,7 @@ static GemmArgs gargs(st_ctx* c, const LayerInfo& L) {
   g.work = c->gemm_ws;
   g.work_bytes = gemm_workspace_bytes((int)c->gemm_rows_max, c->gemm_in_max, c->gemm_out_max);
   g.stream = c->stream;
-  g.pdl = c->pdl_dense;  // dense fwd / dX chains on the main stream (split-lo → GEMM → reduce)
+  g.pdl = c->pdl_now;  // programmatic dependent launches for this task (see run_task)
   return g;
 }
 
@@ -588,7 +595,7 @@ static GemmArgs gargs_rows(st_ctx* c, int rows, int n_in, int n_out) {
   g.work = c->gemm_ws;
   g.work_bytes = gemm_workspace_bytes((int)c->gemm_rows_max, c->gemm_in_max, c->gemm_out_max);
   g.stream = c->stream;
-  g.pdl = c->pdl_dense;
+  g.pdl = c->pdl_now;
   return g;
 }
 
@@ -805,6 +812,12 @@ static st_status backward_compute(st_ctx* c, int64_t mb, bool fused = false) {
   };
   for (int l = nl - 1; l >= 0; --l) {
     const LayerInfo& L = c->layers[l];
+    // Programmatic dependent launches pay off on one in-order stream; for a large dense
+    // layer the main-stream dX overlaps the side-stream dW + update, and early-launched
+    // CTAs waiting on their predecessor hold SMs the other stream needs (large FCN −5%),
+    // so those layers launch normally
+    c->pdl_now = c->pdl_dense && !(fused && L.kind == ST_LAYER_DENSE && L.n_params >= ((int64_t)1 << 22));
+    set_thread_pdl(c->pdl_now ? 1 : 0);
     float* Ain = layer_in(c, slot, (size_t)l);
     const bool need_dx = !(c->first_stage && l == 0) && L.kind != ST_LAYER_EMBED;
     // implicit convs and pools also overlap: a conv's dW + update runs on the side stream
@@ -995,6 +1008,9 @@ static st_status run_task(st_ctx* c, const float* x_dev, const int32_t* y_dev, b
   if (c->pending_update)
     return set_error(ST_ERR_STATE, "stage %d: predict_and_update must follow every backward", c->k);
   const Task t = c->program[c->pc];
+  // programmatic dependent launches for this task (the backward refines it per layer)
+  c->pdl_now = c->pdl_dense;
+  set_thread_pdl(c->pdl_now ? 1 : 0);
   ST_TRY(comm_before_task(c, c->pc));
   st_event e{};
   e.stage = c->k;

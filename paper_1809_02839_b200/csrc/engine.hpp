@@ -139,6 +139,7 @@ struct st_ctx {
   int32_t* y_stage = nullptr;   // [R] labels staged from host (st_run_host)
   float* lstm_rec = nullptr;    // [B × 4H] h_{t−1}·W_hh
   float* lstm_dh = nullptr;     // [B × H] dh_next
+  bool pdl_now = false;         // this task's launches (run_task)
   bool pdl_dense = true;        // dense fwd / dX kernels as programmatic dependent launches (ST_PDL_DENSE=0: off)
   bool pdl = true;              // LSTM recurrence: GEMM ↔ cell as programmatic dependent launches (ST_PDL=0: off)
   bool conv_overlap = false;    // implicit-conv dW + update on the side stream (ST_CONV_OVERLAP=1; measured

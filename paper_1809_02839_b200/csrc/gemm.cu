@@ -23,7 +23,11 @@ int simt_last_launches();
 
 static thread_local int g_last_launches = 0;
 
+// per host thread (one stage context per thread): the engine sets it per task
+static thread_local int tl_pdl = -1;
+void set_thread_pdl(int on) { tl_pdl = on; }
 bool pdl_enabled() {
+  if (tl_pdl >= 0) return tl_pdl != 0;
   static int f = -1;
   if (f < 0) {
     const char* e = getenv("ST_PDL_DENSE");
