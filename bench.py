@@ -51,6 +51,8 @@ def parse():
     p.add_argument("--no-e2e", action="store_true")
     p.add_argument("--no-cpu", action="store_true")
     p.add_argument("--lr", type=float, default=1e-3)
+    p.add_argument("--partition", default="fixed", choices=["fixed", "auto"],
+                   help="fixed: the BJ / SURVEY §8(d) stage cuts; auto: st_partition over per-layer roofline times")
     p.add_argument("--parallel", default="pp", choices=["pp", "dp"],
                    help="pp: the SpecTrain pipeline (default); dp: the data-parallel comparator (NEXT-1)")
     return p.parse_args()
@@ -131,6 +133,31 @@ def stage_work(model, k: int, B: int, pred: str):
     if k == N - 1:
         byts += 12.0 * R * model.layers[-1].n_out
     return byts, flops
+
+
+def auto_partition(model, B: int, S: int, hbm_gbs: float, tf32x3_tflops: float):
+    """NEXT-4: stage cuts from st_partition over per-layer roofline times (the stage_work
+    model for each layer alone: max(bytes / HBM, fp32 FLOPs / 3xTF32 peak), vanilla
+    16 B/param update) instead of the fixed BJ partitions."""
+    import dataclasses
+
+    import paper_1809_02839_b200 as st
+    import synthdata as sd
+    costs = []
+    for i, L in enumerate(model.layers):
+        one = sd.Model((L,), (), model.loss, model.seq_len)
+        b, f = stage_work(one, 0, B, "none")
+        if i != 0:  # stage_work treats its first layer as the network's first (no dX)
+            b += 4.0 * L.n_params
+            if L.kind == sd.DENSE:
+                f += 2.0 * B * model.seq_len * L.n_in * L.n_out
+            elif L.kind == sd.CONV:
+                f += 2.0 * B * L.hw * L.hw * L.n_in * L.n_out * 9
+            elif L.kind == sd.LSTM:
+                f += 2.0 * B * model.seq_len * (L.n_in + L.n_out) * 4 * L.n_out
+        costs.append(max(b / (hbm_gbs * 1e9), f / (tf32x3_tflops * 1e12)))
+    cuts, _ = st.partition(costs, S)
+    return dataclasses.replace(model, cuts=tuple(cuts))
 
 
 def pipeline_roofline(model, B: int, pred: str, hbm_gbs: float, tf32x3_tflops: float):
@@ -405,6 +432,9 @@ def run_ours(args):
     if N > 1:
         dist.init_process_group("nccl", device_id=dev)
     model, B, wname = workload(args.workload, S)
+    if args.partition == "auto" and S > 1:
+        hbm_, _ = measured_peaks()
+        model = auto_partition(model, B, S, hbm_, measured_tensor_peak()[2])
     gemm = {"fp32x3": st.ST_GEMM_FP32X3, "tf32": st.ST_GEMM_TF32, "simt": st.ST_GEMM_SIMT}[args.gemm]
     pred = {"spectrain": st.ST_PRED_SPECTRAIN, "none": st.ST_PRED_NONE, "stash": st.ST_PRED_STASH}[args.pred]
     kinds = {sd.DENSE: st.ST_LAYER_DENSE, sd.EMBED: st.ST_LAYER_EMBED, sd.LSTM: st.ST_LAYER_LSTM,
@@ -626,6 +656,7 @@ def run_ours(args):
             "warmup": args.warmup, "ms_per_step": t_max / args.steps, "higher_is_better": True,
             "scaling": "strong", "vs_baseline": None, "dtype": "f32", "data": "synthetic",
             "config": {"workload": wname, "stages": S, "batch": B, "seq_len": T, "gemm": args.gemm, "pred": args.pred,
+                       "cuts": list(model.cuts), "partition": args.partition,
                        "parallelism": f"pp{S}", "l2": "no flush: per-step working set (weights) >> 126 MB L2",
                        "session": "warm-up and timed steps are separate 1F1B sessions (fill + drain included)"},
             "roofline": roofline_key,
