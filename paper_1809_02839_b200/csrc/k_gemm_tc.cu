@@ -1990,10 +1990,15 @@ __global__ void __launch_bounds__(DW_THREADS, 1)
   tc_fence_after();
   const uint32_t tmem = *tmem_slot;
   const uint32_t tA_hi = tmem + 256, tA_lo = tmem + 384;
+  // programmatic dependent launch (no-ops without the attribute): the successor may launch;
+  // dZ / X / X-lo are read only after the predecessor completed (warp 0), while the W / V
+  // stream — written by no earlier kernel still in flight — may start at once
+  if (threadIdx.x == 0) asm volatile("griddepcontrol.launch_dependents;" ::: "memory");
 
   if (warp == 0) {
     // ---------------- TMA producer: A staging per m-tile, B ring per tile × K-block
     // (warp-converged loop, elected lane issues)
+    asm volatile("griddepcontrol.wait;" ::: "memory");
     {
       int cur_m = -1, a_loads = 0, it = 0;
       for (int t = t_begin; t < t_end; ++t) {
@@ -2764,9 +2769,9 @@ st_status tc_dw_impl(const GemmArgs& g, const float* X, const float* dZ, float* 
     (void)dzlo;
     if (x3) {
       const size_t n4b = (size_t)g.B * g.n_in / 4;
-      split_lo_kernel<<<std::min<size_t>(4 * 148, (n4b + 255) / 256), 256, 0, g.stream>>>(
-          reinterpret_cast<const float4*>(X), reinterpret_cast<float4*>(xlo), n4b);
-      ST_CUDA_TRY(cudaGetLastError());
+      ST_TRY(launch_maybe_pdl(g.pdl, split_lo_kernel, dim3((unsigned)std::min<size_t>(4 * 148, (n4b + 255) / 256)),
+                              dim3(256), 0, g.stream, reinterpret_cast<const float4*>(X),
+                              reinterpret_cast<float4*>(xlo), n4b));
       launches += 1;
     }
     CUtensorMap ma, mb, mblo;
@@ -2808,8 +2813,8 @@ st_status tc_dw_impl(const GemmArgs& g, const float* X, const float* dZ, float* 
       ST_CUDA_TRY(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, dw_smem_bytes()));
       attr_set[ai] = true;
     }
-    kern<<<grid, DW_THREADS, dw_smem_bytes(), g.stream>>>(ma, mb, mblo, mw, mv, p, mt, nt);
-    ST_CUDA_TRY(cudaGetLastError());
+    ST_TRY(launch_maybe_pdl(g.pdl, kern, dim3(grid), dim3(DW_THREADS), (size_t)dw_smem_bytes(), g.stream, ma, mb,
+                            mblo, mw, mv, p, mt, nt));
     if (gb_upd) {
       ST_TRY(launch_bias_grad_update(dZ, g.B, g.n_out, *gb_upd, g.stream));
       ++launches;

@@ -151,6 +151,7 @@ namespace {
 // the same K-B arithmetic as update_predict_kernel on the bias entries.
 __global__ void __launch_bounds__(256) bias_grad_update_kernel(const float* __restrict__ dZ, int B, int n_out,
                                                                UpdateArgs u) {
+  PDL_PROLOGUE();
   __shared__ float part[8][33];
   const int tx = threadIdx.x & 31, ty = threadIdx.x >> 5;
   const int o = blockIdx.x * 32 + tx;
@@ -177,7 +178,8 @@ __global__ void __launch_bounds__(256) bias_grad_update_kernel(const float* __re
 }  // namespace
 
 st_status launch_bias_grad_update(const float* dZ, int B, int n_out, const UpdateArgs& u, cudaStream_t s) {
-  bias_grad_update_kernel<<<(n_out + 31) / 32, 256, 0, s>>>(dZ, B, n_out, u);
+  ST_TRY(launch_pdl(pdl_enabled(), bias_grad_update_kernel, dim3((n_out + 31) / 32), dim3(256), 0, s, dZ, B, n_out,
+                    u));
   ST_CUDA_TRY(cudaGetLastError());
   return ST_OK;
 }
