@@ -409,7 +409,10 @@ st_status ctx_init(const st_config* cfg, const st_buffers* bufs, void* stream, s
   ST_CUDA_TRY(cudaStreamCreateWithFlags(&c->side, cudaStreamNonBlocking));
   c->side_events.resize(c->layers.size() + 1);
   for (auto& e : c->side_events) ST_CUDA_TRY(cudaEventCreateWithFlags(&e, cudaEventDisableTiming));
-  if (const char* e = getenv("ST_DWU_SMS")) c->dwu_sms = std::max(1, atoi(e));
+  if (const char* e = getenv("ST_DWU_SMS")) {
+    c->dwu_sms = std::max(1, atoi(e));
+    c->dwu_env = true;
+  }
   if (const char* e = getenv("ST_CONV_OVERLAP")) c->conv_overlap = atoi(e) != 0;
   if (const char* e = getenv("ST_PDL")) c->pdl = atoi(e) != 0;
   if (const char* e = getenv("ST_PDL_DENSE")) c->pdl_dense = atoi(e) != 0;
@@ -802,6 +805,7 @@ static st_status backward_compute(st_ctx* c, int64_t mb, bool fused = false) {
   int next = 0;
   bool side_busy = false;
   int64_t side_params = 0;  // parameters of the dW + update last issued on the side stream
+  int side_dwu = c->dwu_sms;  // its SM budget
   auto join_side = [&]() -> st_status {
     if (!side_busy) return ST_OK;
     ST_CUDA_TRY(cudaEventRecord(c->side_events[nl], c->side));
@@ -957,7 +961,7 @@ static st_status backward_compute(st_ctx* c, int64_t mb, bool fused = false) {
         GemmArgs gx = gargs(c, L);
         // share the GPU with the running dW + update — unless that one is small (e.g. the
         // 10-wide output layer's), when this dX would otherwise run alone on part of the GPU
-        if (side_busy && side_params >= (int64_t)1 << 22) gx.max_ctas = std::max(1, 148 - c->dwu_sms);
+        if (side_busy && side_params >= (int64_t)1 << 22) gx.max_ctas = std::max(1, 148 - side_dwu);
         Timed t(c, KC_GEMM_DX);
         ST_TRY(gemm_dx(gx, dZ, Wh + L.w_off, producer_act == ST_ACT_RELU ? Ain : nullptr, D));
         c->launches += gemm_last_launches();
@@ -971,7 +975,13 @@ static st_status backward_compute(st_ctx* c, int64_t mb, bool fused = false) {
         gw.work = c->gemm_ws2;
         // a dX of layer l−1 will run concurrently only if that layer is DENSE and needs one
         const bool more_dx = l > 0 && c->layers[l - 1].kind == ST_LAYER_DENSE && !(c->first_stage && l == 1);
-        if (more_dx) gw.max_ctas = c->dwu_sms;
+        // SM budget of the overlapped dW + update: 80 (swept on 8192-wide layers); a layer
+        // with 100–140 output tiles gets one CTA per tile, so every CTA owns a whole m-tile
+        // column (no dZ re-staging, adjacent W / V rows streamed together): 16384-wide
+        // layers 80 → 128 CTAs, large FCN 5.2k → 5.9k samples/s. ST_DWU_SMS overrides.
+        const int m_tiles = (L.n_out + 127) / 128;
+        side_dwu = c->dwu_env ? c->dwu_sms : ((m_tiles >= 100 && m_tiles <= 140) ? m_tiles : c->dwu_sms);
+        if (more_dx) gw.max_ctas = side_dwu;
         UpdateArgs bu{};
         if (L.bias) bu = block_update(c, L.b_off, kc);
         {

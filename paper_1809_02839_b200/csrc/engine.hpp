@@ -133,6 +133,7 @@ struct st_ctx {
   float* bufC = nullptr;
   cudaStream_t side = nullptr;          // library-owned: dW + update overlapped with the next dX
   std::vector<cudaEvent_t> side_events; // one per layer (dW done) + join
+  bool dwu_env = false;                 // ST_DWU_SMS given: one budget for every layer
   int dwu_sms = 80;                     // SM budget of an overlapped dW + update (measured best)
   float* losses_dev = nullptr;  // [max_mb]
   float* rowloss = nullptr;     // [B]
