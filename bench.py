@@ -7,12 +7,15 @@
 
 A step = one mini-batch (B samples) through the whole pipeline: F on every
 stage, loss, B on every stage, the fused K-B update on every stage. Workload
-(config.workload): BASELINE.json configs[1], the wide FCN (784 → 8 × 8192 → 10,
-batch 128) cut into N contiguous stages, one stage per GPU (N=1: one stage,
-s_F = s_B = 0). Warm-up and timed steps run as separate pipeline sessions
-(`st_run`, fill + steady state + drain), timed with CUDA events on the stage
-streams, max over ranks. Weights (1.9 GB) exceed L2 (126 MB), so no flush is
-needed between steps.
+(config.workload): BASELINE.json configs[4], the large FCN (784 → 16 × 16384 → 10,
+batch 128) — the one config BASELINE.json quotes at 1/2/4/8 stages — cut into N
+contiguous stages, one stage per GPU (N=1: one stage, s_F = s_B = 0; --workload
+picks the other configs). Warm-up and timed mini-batches run as ONE pipeline session
+(`st_run` of W + K mini-batches); the timed window is the paper's steady-state window
+(SURVEY §8(d)): CUDA events recorded on each rank's compute stream right after
+its backward of mini-batch W−1 and of mini-batch W+K−1 (`st_record_after_backward`),
+so K mini-batches complete inside it with the pipeline full; max over ranks. Weights
+(16 GB) exceed L2 (126 MB), so no flush is needed between steps.
 
 One JSON line on rank 0 (schema in the task contract), with `roofline` for the
 dominant kernel (K-B), `cpu_baseline` (the oracle on the host cores), `e2e`
@@ -44,7 +47,7 @@ def parse():
     p.add_argument("--steps", type=int, default=100)
     p.add_argument("--warmup", type=int, default=5)
     p.add_argument("--impl", default="ours", choices=["ours", "reference"])
-    p.add_argument("--workload", default="wide_fcn", choices=["wide_fcn", "large_fcn", "mlp", "deep_mlp", "lstm_lm", "vgg16"])
+    p.add_argument("--workload", default="large_fcn", choices=["wide_fcn", "large_fcn", "mlp", "deep_mlp", "lstm_lm", "vgg16"])
     p.add_argument("--stages", type=int, default=0, help="pipeline depth (default = --gpus); >N only with N=1")
     p.add_argument("--gemm", default=DEFAULT_GEMM, choices=["fp32x3", "tf32", "simt"])
     p.add_argument("--pred", default="spectrain", choices=["spectrain", "none", "stash"])
@@ -241,14 +244,27 @@ class ClockSampler:
 
 # ----------------------------------------------------------------------------- CPU oracle
 
-def oracle_sample_rate(model_full, B: int, steps: int = 1, seed: int = 0):
+def cpu_model() -> str:
+    try:
+        for line in open("/proc/cpuinfo"):
+            if line.startswith("model name"):
+                return line.split(":", 1)[1].strip()
+    except Exception:
+        pass
+    import platform
+    return platform.processor() or "unknown"
+
+
+def oracle_sample_rate(model_full, B: int, steps: int = 1, seed: int = 0, width_cap: int = 0):
     """Time the oracle as it stands on a bounded slice of the workload: a 1-stage
-    784-w-w-10 net with the workload's hidden width w, `steps` mini-batches each
-    (F, loss, B, update). Returns (samples/s extrapolated linearly in parameters to
-    the full model, description, threads, per-step seconds)."""
+    784-w-w-10 net with the workload's hidden width w (capped at width_cap if > 0),
+    `steps` mini-batches each (F, loss, B, update). Returns (samples/s extrapolated
+    linearly in parameters to the full model, description, threads, per-step seconds)."""
     import synthdata as sd
     from oracle import spectrain_oracle as O
     w = max(l.n_out for l in model_full.layers[:-1]) if len(model_full.layers) > 1 else model_full.layers[0].n_out
+    if width_cap:
+        w = min(w, width_cap)
     slice_model = sd.mlp([model_full.layers[0].n_in, w, w, model_full.layers[-1].n_out], cuts=[])
     P_slice = sum(l.n_params for l in slice_model.layers)
     P_full = sum(l.n_params for l in model_full.layers)
@@ -265,9 +281,26 @@ def oracle_sample_rate(model_full, B: int, steps: int = 1, seed: int = 0):
         threads = os.cpu_count() or 1
     rate = steps * B / dt * (P_slice / P_full)
     desc = (f"oracle.run (NumPy fp64) on a 1-stage {slice_model.layers[0].n_in}-{w}-{w}-"
-            f"{slice_model.layers[-1].n_out} slice ({P_slice / 1e6:.1f}M params), {steps} mini-batch(es) of B={B}; "
-            f"samples/s extrapolated linearly in params to the {P_full / 1e6:.1f}M-param workload")
+            f"{slice_model.layers[-1].n_out} slice ({P_slice / 1e6:.1f}M params), {steps} mini-batch(es) of B={B} "
+            f"in {dt:.2f} s measured; samples/s EXTRAPOLATED linearly in params to the {P_full / 1e6:.1f}M-param "
+            f"workload")
     return rate, desc, threads, dt / steps
+
+
+def cpu_baseline(model, B: int):
+    """The oracle on the host cores (all BLAS threads), plus a 1-thread run on a
+    narrower slice, the CPU model and the core count (SURVEY §8(d) 'Oracle timing')."""
+    rate, desc, threads, step_s = oracle_sample_rate(model, B, 1)
+    out = {"value": rate, "unit": UNIT, "cores": threads, "kind": "oracle", "sample": desc,
+           "slice_s_per_step": step_s, "cpu_model": cpu_model(), "nproc": os.cpu_count()}
+    try:
+        from threadpoolctl import threadpool_limits
+        with threadpool_limits(limits=1):
+            r1, d1, _, s1 = oracle_sample_rate(model, B, 1, width_cap=2048)
+        out["one_thread"] = {"value": r1, "unit": UNIT, "cores": 1, "sample": d1, "slice_s_per_step": s1}
+    except Exception as e:  # report, never fail the bench line for the context number
+        out["one_thread"] = {"error": repr(e)}
+    return out
 
 
 def run_reference(args):
@@ -295,13 +328,18 @@ def run_reference(args):
         step_s.append(s)
     value = float(statistics.mean(rates))
     desc += f"; {len(rates)} timed step(s) of the requested {args.steps} (wall-clock budget {budget:.0f} s)"
+    slice_s = float(sum(step_s))
     line = {
         "impl": "reference", "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": args.gpus,
         "steps": args.steps, "timed_steps": len(rates), "warmup": args.warmup, "ms_per_step": B / value * 1e3, "higher_is_better": True,
         "scaling": "strong", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
         "config": {"workload": wname, "stages": S, "batch": B, "parallelism": f"pp{S}"},
-        "cpu_baseline": {"value": value, "unit": UNIT, "cores": threads, "kind": "oracle", "sample": desc},
+        "cpu_baseline": {"value": value, "unit": UNIT, "cores": threads, "kind": "oracle", "sample": desc,
+                         "cpu_model": cpu_model(), "nproc": os.cpu_count()},
         "e2e": {"value": value, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
+        "measured_wall_s": slice_s,
+        "note": "ms_per_step is B / value (the extrapolated full-model rate); measured_wall_s is the measured oracle "
+                "time of the timed slice steps",
     }
     print(json.dumps(line), flush=True)
 
@@ -411,6 +449,55 @@ def run_dp(args):
         dist.destroy_process_group()
 
 
+def nccl_parity_leg(args, N: int, rank: int, local: int, dev):
+    """Under torchrun (N > 1), before timing: the NCCL transport checked on the real
+    ranks — the deep MLP 784-1024×8-10 cut into N stages, one per
+    rank over NCCL (two communicators, comm streams), M = 20, B = 128, η = 0.02, 3xTF32,
+    against the oracle on rank 0: trace bit-exact, W and loss rel-L2 ≤ 1e-4, ΔW rel-L2
+    ≤ 1e-3 (north_star gates)."""
+    import torch
+    import torch.distributed as dist
+
+    import paper_1809_02839_b200 as st
+    import synthdata as sd
+    model = sd.config_deep_mlp(N)
+    M, B, lr = 20, 128, 0.02
+    w0, X, Y = sd.parity_inputs(model, M, B, seed=0)
+    obj = [st.nccl_id() if rank == 0 else None]
+    dist.broadcast_object_list(obj, src=0)
+    layers = [(l.n_in, l.n_out, st.ST_ACT_RELU if l.act == sd.RELU else st.ST_ACT_NONE, 1 if l.bias else 0)
+              for l in model.layers]
+    s = st.Stage(layers, model.cuts, rank, B, lr, 0.9, transport=st.ST_TRANSPORT_NCCL, device=local,
+                 max_minibatches=M, nccl_id=obj[0])
+    s.set_params(w0[rank])
+    xs = torch.from_numpy(X).to(dev) if s.is_first else None
+    ys = torch.from_numpy(Y.astype(np.int32)).to(dev) if s.is_last else None
+    t0 = time.perf_counter()
+    losses = s.run(M, xs, ys, want_losses=s.is_last)
+    W, _, _ = s.get_params()
+    wall = time.perf_counter() - t0
+    tr = s.trace()
+    s.close()
+    got = [None] * N if rank == 0 else None
+    dist.gather_object((W, tr, losses), got, dst=0)
+    if rank != 0:
+        return None
+    from oracle import spectrain_oracle as O
+    ref = O.run(model, sd.widen(w0), X.astype(np.float64), Y, float(np.float32(lr)), float(np.float32(0.9)))
+
+    def rel(a, b):
+        return float(np.linalg.norm(np.asarray(a, np.float64) - b) / np.linalg.norm(b))
+    Wg = np.concatenate([g[0] for g in got])
+    Wr = np.concatenate(ref.W)
+    trace_ok = all(got[k][1] == [e.as_tuple() for e in ref.trace[k]] for k in range(N))
+    rw = rel(Wg, Wr)
+    rl = rel(got[N - 1][2], ref.losses)
+    dw = rel(Wg - np.concatenate(w0), Wr - np.concatenate(sd.widen(w0)))
+    return {"model": "deep_mlp_784-1024x8-10_b128", "stages": N, "minibatches": M, "transport": "nccl (2 comms)",
+            "trace_bit_exact": bool(trace_ok), "w_rel_l2": rw, "loss_rel_l2": rl, "dw_rel_l2": dw,
+            "pass": bool(trace_ok and rw <= 1e-4 and rl <= 1e-4 and dw <= 1e-3), "wall_s": wall}
+
+
 def run_ours(args):
     import torch
     import torch.distributed as dist
@@ -443,7 +530,10 @@ def run_ours(args):
                kinds[l.kind], l.hw) for l in model.layers]
     T = model.seq_len
     R = B * T
-    M = max(args.steps, args.warmup, 1)
+    W_, K = args.warmup, args.steps
+    if K < 1:
+        raise SystemExit("--steps must be >= 1")
+    M = W_ + K  # one session: W warm-up mini-batches, then the K timed ones
 
     if N > 1:
         obj = [st.nccl_id() if rank == 0 else None]
@@ -480,49 +570,54 @@ def run_ours(args):
             dist.barrier()
         torch.cuda.synchronize()
 
-    def session(K: int):
-        if len(my_stages) == 1:
-            my_stages[0].run(K, xs, ys)
+    def session(n: int, host=None):
+        if host is not None:
+            my_stages[0].run_host(n, *host)
+        elif len(my_stages) == 1:
+            my_stages[0].run(n, xs, ys)
         else:
-            st.run_group(my_stages, K, xs, ys, want_losses=False)
+            st.run_group(my_stages, n, xs, ys, want_losses=False)
 
-    def timed(K: int):
-        """CUDA-event time of one K-mini-batch session on this rank (all stage streams)."""
-        root = torch.cuda.current_stream(dev)
-        t0 = torch.cuda.Event(enable_timing=True)
-        t1 = torch.cuda.Event(enable_timing=True)
-        t0.record(root)
-        for s in my_stages:
-            s.stream.wait_event(t0)
-        session(K)
-        for s in my_stages:
-            e = torch.cuda.Event()
-            e.record(s.stream)
-            root.wait_event(e)
-        t1.record(root)
+    def windowed(host=None):
+        """One session of M = W + K mini-batches; returns the CUDA-event time between
+        stage 0's (this rank's) backward of mini-batch W−1 and of mini-batch M−1 —
+        the paper's steady-state window."""
+        s0 = my_stages[0]
+        e0 = torch.cuda.Event(enable_timing=True)
+        e1 = torch.cuda.Event(enable_timing=True)
+        if W_ >= 1:
+            s0.record_after_backward(W_ - 1, e0)
+        else:
+            e0.record(s0.stream)
+        s0.record_after_backward(M - 1, e1)
+        session(M, host)
         torch.cuda.synchronize()
-        return t0.elapsed_time(t1)
+        return e0.elapsed_time(e1)
 
-    # warm-up
-    barrier()
-    session(args.warmup)
-    barrier()
-    # timed region (device time, K-B profiled with CUDA events on the stage stream)
-    # only the dominant kernel class is bracketed inside the timed region (two event
-    # records per launch; events pre-created); the all-class breakdown comes from a
-    # separate short session after it
+    def max_over_ranks(x: float) -> float:
+        if N == 1:
+            return x
+        t = torch.tensor([x], device=dev, dtype=torch.float64)
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        return float(t.item())
+
+    nccl_parity = nccl_parity_leg(args, N, rank, local, dev) if N > 1 else None
+
+    # the timed session: only the dominant kernel class is bracketed with CUDA events
+    # (two event records per launch; events pre-created); the all-class breakdown comes
+    # from a separate short session after it
     for s in my_stages:
         s.set_profiling(True, ["gemm_dw"])
     launches0 = sum(s.kernel_launches() for s in my_stages)
     sampler = ClockSampler(local)
     barrier()
     with sampler:
-        ms = timed(args.steps)
+        ms = windowed()
     barrier()
     launches = sum(s.kernel_launches() for s in my_stages) - launches0
     profs = [s.profile() for s in my_stages]
     # breakdown session (not timed for `value`): every kernel class bracketed
-    n_brk = min(args.steps, 20)
+    n_brk = min(K, 20)
     for s in my_stages:
         s.set_profiling(True)
     barrier()
@@ -531,15 +626,12 @@ def run_ours(args):
     brk = [s.profile() for s in my_stages]
     for s in my_stages:
         s.set_profiling(False)
-    t_max = ms
+    t_max = max_over_ranks(ms)
     if N > 1:
-        t = torch.tensor([ms], device=dev, dtype=torch.float64)
-        dist.all_reduce(t, op=dist.ReduceOp.MAX)
-        t_max = float(t.item())
         lt = torch.tensor([launches], device=dev, dtype=torch.int64)
         dist.all_reduce(lt, op=dist.ReduceOp.SUM)
         launches = int(lt.item())
-    value = args.steps * B / (t_max / 1e3)
+    value = K * B / (t_max / 1e3)
 
     # roofline of the dominant kernel: the dW GEMM with the fused K-B update
     # (k_gemm_tc.cu tc_dw_kernel<x3, UPD> + its lo-split and bias-update launches — the
@@ -550,7 +642,7 @@ def run_ours(args):
     for s, pr in zip(my_stages, profs):
         bpp = 16 + (4 if s.sizes.wf_bytes > 0 else 0) + (4 if s.sizes.wb_bytes > 0 else 0)  # + WF / WB (or stash) writes
         ms_k, n_k = pr["gemm_dw"]
-        kb_bytes += bpp * s.params * args.steps
+        kb_bytes += bpp * s.params * M  # the class is bracketed over the whole session (M mini-batches)
         kb_ms += ms_k
         kb_n += n_k
         stage_ms += sum(v[0] for v in brk[my_stages.index(s)].values())
@@ -583,7 +675,8 @@ def run_ours(args):
     gemm_tf = fwd_flops / (fwd_ms / 1e3) / 1e12 if fwd_ms > 0 else None
     gemm_prof = {k: round(sum(p[k][0] for p in brk) / n_brk, 4) for k in brk[0]}
 
-    # end-to-end: the same metric through st_run_host (pinned host inputs, per-step H2D + loss D2H)
+    # end-to-end: the same metric through st_run_host (pinned host inputs, per-mini-batch H2D
+    # and loss D2H inside the same steady-state window)
     e2e = None
     if not args.no_e2e and len(my_stages) == 1:
         s = my_stages[0]
@@ -591,21 +684,13 @@ def run_ours(args):
         yh = ys.cpu().pin_memory() if last else None
         lh = torch.empty(M, dtype=torch.float32).pin_memory() if last else None
         barrier()
-        e0 = torch.cuda.Event(enable_timing=True)
-        e1 = torch.cuda.Event(enable_timing=True)
-        e0.record(s.stream)
-        s.run_host(args.steps, xh, yh, lh)
-        e1.record(s.stream)
-        torch.cuda.synchronize()
-        ems = e0.elapsed_time(e1)
-        if N > 1:
-            t = torch.tensor([ems], device=dev, dtype=torch.float64)
-            dist.all_reduce(t, op=dist.ReduceOp.MAX)
-            ems = float(t.item())
+        ems = max_over_ranks(windowed((xh, yh, lh)))
+        barrier()
         x_bytes = R * 4 if model.layers[0].kind == sd.EMBED else R * n_in * 4
-        e2e = {"value": args.steps * B / (ems / 1e3), "unit": UNIT,
-               "h2d_bytes_per_step": x_bytes + R * 4, "d2h_bytes_per_step": 4,
-               "api": "st_run_host"}
+        e2e = {"value": K * B / (ems / 1e3), "unit": UNIT,
+               "h2d_bytes_per_step": (x_bytes if first else 0) + (R * 4 if last else 0),
+               "d2h_bytes_per_step": 4 if last else 0,
+               "api": "st_run_host (same W + K session and window as `value`)"}
 
     # dominant kernel class = the gemm_dw class (largest share on every workload). FCN / MLP:
     # the fused dW + K-B update, HBM-bound (bytes above). Conv / LSTM workloads: the dW GEMMs
@@ -625,14 +710,14 @@ def run_ours(args):
         if N > 1:
             dist.all_reduce(t_)
         dw_flops = float(t_.item())
-        ach_t = dw_flops * args.steps / (kb_ms / 1e3) / 1e12 if kb_ms > 0 else None
+        ach_t = dw_flops * M / (kb_ms / 1e3) / 1e12 if kb_ms > 0 else None
         roofline_key = {"kernel": "gemm_dw class: k_gemm_tc.cu tc_tsg_kernel (implicit-conv dW / tall dense dW, "
                                   "3xTF32) + the K-B update of those layers",
                         "bound": "tensor", "achieved": ach_t, "peak": x3_pk, "unit": "TFLOP/s",
                         "frac": (ach_t / x3_pk) if ach_t else None, "traffic": None,
                         "peak_source": tpk_src + "; fp32 FLOP/s of 3xTF32 products = tf32 peak / 3",
                         "launches": int(kb_n), "per": "all dW launches of one step",
-                        "ms_per_step": kb_ms / args.steps,
+                        "ms_per_step": kb_ms / M,
                         "share_of_stage_time": (brk_dw / stage_ms) if stage_ms else None,
                         "algorithmic_flops_per_step": dw_flops}
     else:
@@ -643,22 +728,22 @@ def run_ours(args):
                         "traffic": recorded_traffic(wname, "dw_update_per_step"),
                         "peak_source": peak_src, "launches": int(kb_n),
                         "per": "all dW+update launches of one step (one per layer)",
-                        "ms_per_step": kb_ms / args.steps,
+                        "ms_per_step": kb_ms / M,
                         "share_of_stage_time": (brk_dw / stage_ms) if stage_ms else None,
-                        "algorithmic_bytes_per_step": kb_bytes / args.steps}
+                        "algorithmic_bytes_per_step": kb_bytes / M}
     if rank == 0:
         cpu = None
         if not args.no_cpu and N == 1:  # the oracle baseline: rank 0 at N = 1 only
-            rate, desc, threads, _ = oracle_sample_rate(model, B, 1)
-            cpu = {"value": rate, "unit": UNIT, "cores": threads, "kind": "oracle", "sample": desc}
+            cpu = cpu_baseline(model, B)
         line = {
-            "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": N, "steps": args.steps,
-            "warmup": args.warmup, "ms_per_step": t_max / args.steps, "higher_is_better": True,
+            "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": N, "steps": K,
+            "warmup": W_, "ms_per_step": t_max / K, "higher_is_better": True,
             "scaling": "strong", "vs_baseline": None, "dtype": "f32", "data": "synthetic",
             "config": {"workload": wname, "stages": S, "batch": B, "seq_len": T, "gemm": args.gemm, "pred": args.pred,
                        "cuts": list(model.cuts), "partition": args.partition,
                        "parallelism": f"pp{S}", "l2": "no flush: per-step working set (weights) >> 126 MB L2",
-                       "session": "warm-up and timed steps are separate 1F1B sessions (fill + drain included)"},
+                       "session": "one 1F1B session of warmup + steps mini-batches; timed window = CUDA events "
+                                  "after stage 0's B(warmup-1) and B(warmup+steps-1) (P:415 steady state)"},
             "roofline": roofline_key,
             "pipeline_roofline": {"samples_per_s": roof["samples_per_s"], "frac": value / roof["samples_per_s"],
                                   "stage_us": roof["stage_us"], "stage_bound": roof["bound"],
@@ -678,7 +763,9 @@ def run_ours(args):
                               "with every class bracketed (rank 0's stages)",
             "cpu_baseline": cpu,
             "e2e": e2e,
-            "gpu_launches": launches,
+            "gpu_launches": int(round(launches * K / M)),
+            "gpu_launches_note": f"library kernel launches of the {M}-mini-batch session x {K}/{M} (timed share)",
+            "nccl_parity": nccl_parity,
             "clocks": sampler.summary(),
         }
         print(json.dumps(line), flush=True)

@@ -24,9 +24,13 @@
  * the shipped binding) with the byte counts st_query_sizes reports, and is
  * BORROWED by the context until st_destroy. Device pointers must be 256-byte
  * aligned. Host pointers are read or written only during the call that receives
- * them. Streams are borrowed as well; every device operation of a context is
- * ordered on its compute stream (NCCL transfers included), and calls return
- * before the GPU work finishes unless stated (st_sync blocks).
+ * them. Streams are borrowed as well: the compute stream carries every kernel;
+ * messages to / from the neighbouring stages run on two comm streams (one per
+ * direction), ordered against the compute stream with CUDA events so that
+ * transfers overlap compute. At the end of st_run / st_run_host and in st_sync
+ * the comm streams are joined into the compute stream, so after those calls the
+ * compute stream orders everything the context did. Calls return before the GPU
+ * work finishes unless stated (st_sync blocks).
  *
  * Errors. Every function that can fail returns st_status; the message of the last
  * failure on the calling thread is available from st_last_error(). No C++
@@ -97,10 +101,14 @@ enum { ST_MOMENTUM_EMA = 0, ST_MOMENTUM_HEAVY_BALL = 1 };
  * SIMT = CUDA-core fp32 FMA (bring-up / diagnostic mode). */
 enum { ST_GEMM_FP32X3 = 0, ST_GEMM_TF32 = 1, ST_GEMM_SIMT = 2 };
 enum { ST_LOSS_SOFTMAX_CE = 0 };
-/* Stage-to-stage transport. NCCL: one process per GPU, ncclSend/ncclRecv between
- * adjacent stages on the compute stream. LOCAL: several stage contexts in ONE
- * process (same or different GPUs) linked with st_connect_local; messages are
- * device copies ordered by CUDA events, handed over through host channels. */
+/* Stage-to-stage transport. NCCL: one process
+ * per GPU; two communicators over the N stage ranks, one per direction (activations
+ * k → k+1, gradients k+1 → k), ncclSend / ncclRecv per message on the comm stream of
+ * that direction; asynchronous NCCL errors are polled while the library waits, and a
+ * wait longer than ST_COMM_TIMEOUT_S seconds (default 600) aborts both communicators
+ * (ST_ERR_NCCL). LOCAL: several stage contexts in ONE process (same GPU) linked with
+ * st_connect_local; messages are device copies on the same comm streams, handed over
+ * through host channels; a failing stage releases its blocked peers (ST_ERR_STATE). */
 enum { ST_TRANSPORT_NCCL = 0, ST_TRANSPORT_LOCAL = 1 };
 
 typedef struct {
@@ -169,11 +177,12 @@ typedef struct {
   int64_t target;
 } st_event;
 
-/* One communication step of a stage program (host-side plan, no device work).
- * Ops in one record form one ncclGroupStart/End group. kind: 0 send_fwd (to k+1,
- * activation of mb), 1 recv_fwd (from k−1), 2 send_bwd (to k−1, gradient),
- * 3 recv_bwd (from k+1). before_op = index of the program op it precedes
- * (2M = after the last op). */
+/* One communication op of a stage program (host-side plan, no device work), in
+ * issue order. kind: 0 send_fwd (to k+1, activation of mb), 1 recv_fwd (from k−1),
+ * 2 send_bwd (to k−1, gradient), 3 recv_bwd (from k+1); kinds 0/1 run on the
+ * activation communicator + comm_fwd stream, 2/3 on the gradient one + comm_bwd.
+ * before_op = index of the program op it sits in front of (2M = after the last op);
+ * n_ops = 1 (kind[1] = −1, mb[1] = −1 are unused). */
 typedef struct {
   int32_t before_op;
   int32_t n_ops;
@@ -223,12 +232,17 @@ ST_API st_status st_get_nccl_id(uint8_t out[128]);
 
 /* ---- context lifecycle ----------------------------------------------------- */
 
-/* Binds buffers and the compute stream (a cudaStream_t cast to void*; NULL =
- * legacy default stream), builds the 1F1B program, initialises NCCL for
- * ST_TRANSPORT_NCCL (collective across the N stage processes: every stage must
- * call st_init), sets V = 0, WF = WB = W, version = 0. W is NOT initialised:
- * call st_set_params before the first task. */
-ST_API st_status st_init(const st_config* cfg, const st_buffers* bufs, void* stream, st_ctx** out);
+/* Binds buffers and streams (cudaStream_t cast to void*): `stream` = the compute
+ * stream (NULL = legacy default stream); comm_fwd_stream / comm_bwd_stream = the
+ * streams of the activation / gradient transfers (NULL: the library creates its own
+ * non-blocking streams). Builds the 1F1B program, initialises NCCL for
+ * ST_TRANSPORT_NCCL (collective across the N stage processes: every stage must call
+ * st_init; two communicators), sets V = 0, WF = WB = W, version = 0. W is NOT
+ * initialised: call st_set_params before the first task.
+ * Errors: ST_ERR_INPUT (config, NULL / misaligned buffer), ST_ERR_SHAPE, ST_ERR_CUDA,
+ * ST_ERR_NCCL (communicator setup). */
+ST_API st_status st_init(const st_config* cfg, const st_buffers* bufs, void* stream, void* comm_fwd_stream,
+                         void* comm_bwd_stream, st_ctx** out);
 
 /* LOCAL transport: link ctxs[0..n) as consecutive stages 0..n−1 of one pipeline
  * in this process. Required before any task of a LOCAL context. */
@@ -292,7 +306,19 @@ ST_API st_status st_get_trace(st_ctx* ctx, st_event* out, size_t cap, size_t* n)
 /* Device pointer of the on-device loss vector (last stage; NULL otherwise). */
 ST_API const float* st_losses_device(st_ctx* ctx);
 
+/* Joins the comm streams into the compute stream and waits for it. With a transport it
+ * polls instead of blocking: an asynchronous NCCL error, or no completion within
+ * ST_COMM_TIMEOUT_S seconds (a hung or dead peer), aborts the transport and returns
+ * ST_ERR_NCCL (LOCAL: ST_ERR_STATE); the context is then only good for st_destroy. */
 ST_API st_status st_sync(st_ctx* ctx);
+
+/* Measurement hook (samples/s between stage-0 events after B(49) and
+ * B(249), the paper's iteration window P:415): once the backward of mini-batch mb is
+ * issued (in this or a later session, st_run or the verbs), `cuda_event` (a cudaEvent_t
+ * cast to void*, created by the caller) is recorded on the compute stream after all the
+ * work of that backward (its side-stream dW + update joined). One-shot; at most 64
+ * pending. Errors: ST_ERR_INPUT (NULL event, mb < 0, too many pending). */
+ST_API st_status st_record_after_backward(st_ctx* ctx, int64_t mb, void* cuda_event);
 
 /* ---- measurement hooks ----------------------------------------------------- */
 

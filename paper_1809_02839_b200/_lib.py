@@ -97,7 +97,8 @@ def _load() -> ctypes.CDLL:
         "st_comm_plan": (S, [I, I, I64, ctypes.POINTER(StCommGroup), U, ctypes.POINTER(U)]),
         "st_query_sizes": (S, [ctypes.POINTER(StConfig), ctypes.POINTER(StSizes)]),
         "st_get_nccl_id": (S, [ctypes.POINTER(ctypes.c_uint8 * 128)]),
-        "st_init": (S, [ctypes.POINTER(StConfig), ctypes.POINTER(StBuffers), P, ctypes.POINTER(P)]),
+        "st_init": (S, [ctypes.POINTER(StConfig), ctypes.POINTER(StBuffers), P, P, P, ctypes.POINTER(P)]),
+        "st_record_after_backward": (S, [P, I64, P]),
         "st_connect_local": (S, [ctypes.POINTER(P), ctypes.c_int32]),
         "st_destroy": (None, [P]),
         "st_set_params": (S, [P, P, U]),
@@ -136,7 +137,7 @@ lib = _load()
 EXPORTED = ("st_version_difference", "st_program", "st_partition", "st_comm_plan", "st_query_sizes", "st_get_nccl_id", "st_init",
             "st_connect_local", "st_destroy", "st_set_params", "st_get_params", "st_stage_forward",
             "st_stage_backward", "st_predict_and_update", "st_step", "st_run", "st_run_host", "st_run_group", "st_get_trace",
-            "st_losses_device", "st_sync", "st_set_profiling", "st_get_profile", "st_kernel_launches",
+            "st_losses_device", "st_sync", "st_record_after_backward", "st_set_profiling", "st_get_profile", "st_kernel_launches",
             "st_update_predict_raw", "st_prediction_error_work_bytes", "st_prediction_error_raw", "st_gemm_raw", "st_gemm_workspace_bytes", "st_softmax_ce_raw", "st_dw_update_raw",
             "st_last_error", "st_version")
 

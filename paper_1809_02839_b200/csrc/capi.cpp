@@ -27,7 +27,10 @@ void clear_error() { g_last_error.clear(); }
 
 // engine.cpp
 st_status query_sizes(const st_config* c, st_sizes* out);
-st_status ctx_init(const st_config* cfg, const st_buffers* bufs, void* stream, st_ctx** out);
+st_status ctx_init(const st_config* cfg, const st_buffers* bufs, void* stream, void* comm_fwd, void* comm_bwd,
+                   st_ctx** out);
+st_status ctx_wait(st_ctx* c);
+st_status ctx_mark_after_backward(st_ctx* c, int64_t mb, void* event);
 st_status ctx_connect_local(st_ctx** ctxs, int n);
 void ctx_destroy(st_ctx* c);
 st_status ctx_set_params(st_ctx* c, const float* host, size_t n);
@@ -121,8 +124,9 @@ st_status st_get_nccl_id(uint8_t out[128]) {
   })
 }
 
-st_status st_init(const st_config* cfg, const st_buffers* bufs, void* stream, st_ctx** out) {
-  GUARD({ return ctx_init(cfg, bufs, stream, out); })
+st_status st_init(const st_config* cfg, const st_buffers* bufs, void* stream, void* comm_fwd_stream,
+                  void* comm_bwd_stream, st_ctx** out) {
+  GUARD({ return ctx_init(cfg, bufs, stream, comm_fwd_stream, comm_bwd_stream, out); })
 }
 
 st_status st_connect_local(st_ctx** ctxs, int32_t n) {
@@ -192,9 +196,13 @@ st_status st_sync(st_ctx* ctx) {
   NEED_CTX(ctx);
   GUARD({
     ST_CUDA_TRY(cudaSetDevice(ctx->device));
-    ST_CUDA_TRY(cudaStreamSynchronize(ctx->stream));
-    return ST_OK;
+    return ctx_wait(ctx);
   })
+}
+
+st_status st_record_after_backward(st_ctx* ctx, int64_t mb, void* cuda_event) {
+  NEED_CTX(ctx);
+  GUARD({ return ctx_mark_after_backward(ctx, mb, cuda_event); })
 }
 
 st_status st_set_profiling(st_ctx* ctx, int on) {

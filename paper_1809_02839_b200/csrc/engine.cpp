@@ -7,6 +7,7 @@
 //   B(j): [recv grad] → per layer (reverse) gemm_dx with WB (ReLU mask fused),
 //         gemm_dw (+bias grad) → [send grad]
 //   update: K-B (k_update.cu) — Eq. 1, D1 apply, WF/WB for the next tasks.
+#include <chrono>
 #include <cmath>
 #include <cstring>
 #include <thread>
@@ -208,11 +209,13 @@ st_status validate_and_layout(const st_config* c, Layout* L) {
     return o;
   };
   const int64_t width = std::max(L->max_in, L->max_out);
+  // message buffers: two slots each (mini-batch parity), so the transfer of one
+  // mini-batch overlaps the compute of the next
   if (!L->last) {
-    L->off_send_fwd = take(R * L->out_last);
-    L->off_recv_bwd = take(R * L->out_last);
+    L->off_send_fwd = take(2 * align_up(R * L->out_last, kAlignFloats));
+    L->off_recv_bwd = take(2 * align_up(R * L->out_last, kAlignFloats));
   }
-  if (!L->first) L->off_send_bwd = take(R * L->in_first);
+  if (!L->first) L->off_send_bwd = take(2 * align_up(R * L->in_first, kAlignFloats));
   if (L->last) {
     L->off_logits = take(R * L->out_last);
     L->off_dlogits = take(R * L->out_last);
@@ -304,17 +307,23 @@ st_status query_sizes(const st_config* c, st_sizes* out) {
   return ST_OK;
 }
 
+st_status ctx_wait(st_ctx* c);
+
 static void begin_session(st_ctx* c, int64_t M) {
   c->program = build_program(c->N, c->k, M);
   c->plan = build_comm_plan(c->N, c->k, M);
   c->pc = 0;
-  c->plan_sent = 0;
-  c->plan_recv = 0;
+  c->plan_next = 0;
   c->session_M = M;
   c->pending_update = false;
+  // message slots: nothing in flight at a session boundary (the previous session's comm
+  // streams were joined into the compute stream)
+  for (int b = 0; b < 2; ++b) c->sent_fwd_pending[b] = c->sent_bwd_pending[b] = c->bwd_ring_done[b] = false;
+  std::fill(c->bwd_slot_done.begin(), c->bwd_slot_done.end(), 0);
 }
 
-st_status ctx_init(const st_config* cfg, const st_buffers* bufs, void* stream, st_ctx** out) {
+st_status ctx_init(const st_config* cfg, const st_buffers* bufs, void* stream, void* comm_fwd, void* comm_bwd,
+                   st_ctx** out) {
   if (!out) return set_error(ST_ERR_INPUT, "out is NULL");
   *out = nullptr;
   Layout L;
@@ -370,9 +379,17 @@ st_status ctx_init(const st_config* cfg, const st_buffers* bufs, void* stream, s
   c->S = L.S;
   char* w = static_cast<char*>(bufs->work);
   auto at = [&](int64_t off) { return off < 0 ? nullptr : reinterpret_cast<float*>(w + off); };
-  c->send_fwd = at(L.off_send_fwd);
-  c->recv_bwd = at(L.off_recv_bwd);
-  c->send_bwd = at(L.off_send_bwd);
+  {
+    const int64_t mf = align_up(L.R * L.out_last, kAlignFloats), mb = align_up(L.R * L.in_first, kAlignFloats);
+    for (int b = 0; b < 2; ++b) {
+      c->send_fwd2[b] = L.off_send_fwd < 0 ? nullptr : at(L.off_send_fwd) + b * mf;
+      c->recv_bwd2[b] = L.off_recv_bwd < 0 ? nullptr : at(L.off_recv_bwd) + b * mf;
+      c->send_bwd2[b] = L.off_send_bwd < 0 ? nullptr : at(L.off_send_bwd) + b * mb;
+    }
+    c->send_fwd = c->send_fwd2[0];
+    c->recv_bwd = c->recv_bwd2[0];
+    c->send_bwd = c->send_bwd2[0];
+  }
   c->logits = at(L.off_logits);
   c->dlogits = at(L.off_dlogits);
   c->rowloss = at(L.off_rowloss);
@@ -400,6 +417,45 @@ st_status ctx_init(const st_config* cfg, const st_buffers* bufs, void* stream, s
   c->gemm_ws = w + L.off_ws;
   c->gemm_ws2 = w + L.off_ws2;
   c->stream = static_cast<cudaStream_t>(stream);
+  {
+    int sms = 0;
+    ST_CUDA_TRY(cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, cfg->device));
+    c->sm_count = std::max(2, sms);
+    c->dwu_sms = std::min(c->dwu_sms, c->sm_count - 2);
+  }
+  // comm streams: the caller's, or library-owned non-blocking streams
+  if (comm_fwd) {
+    c->comm_fwd = static_cast<cudaStream_t>(comm_fwd);
+  } else {
+    ST_CUDA_TRY(cudaStreamCreateWithFlags(&c->comm_fwd, cudaStreamNonBlocking));
+    c->own_comm_fwd = true;
+  }
+  if (comm_bwd) {
+    c->comm_bwd = static_cast<cudaStream_t>(comm_bwd);
+  } else {
+    ST_CUDA_TRY(cudaStreamCreateWithFlags(&c->comm_bwd, cudaStreamNonBlocking));
+    c->own_comm_bwd = true;
+  }
+  {
+    auto mk = [](cudaEvent_t* e) { return cudaEventCreateWithFlags(e, cudaEventDisableTiming); };
+    for (int b = 0; b < 2; ++b) {
+      ST_CUDA_TRY(mk(&c->ev_sent_fwd[b]));
+      ST_CUDA_TRY(mk(&c->ev_sent_bwd[b]));
+      ST_CUDA_TRY(mk(&c->ev_recv_bwd[b]));
+      ST_CUDA_TRY(mk(&c->ev_bwd_ring[b]));
+      ST_CUDA_TRY(mk(&c->ev_join[b]));
+    }
+    c->ev_recv_fwd.assign((size_t)c->S, nullptr);
+    c->ev_bwd_slot.assign((size_t)c->S, nullptr);
+    c->bwd_slot_done.assign((size_t)c->S, 0);
+    for (int i = 0; i < c->S; ++i) {
+      ST_CUDA_TRY(mk(&c->ev_recv_fwd[(size_t)i]));
+      ST_CUDA_TRY(mk(&c->ev_bwd_slot[(size_t)i]));
+    }
+    ST_CUDA_TRY(mk(&c->ev_fwd_done));
+    ST_CUDA_TRY(mk(&c->ev_dx_ready));
+  }
+  if (const char* e = getenv("ST_COMM_TIMEOUT_S")) c->comm_timeout_s = std::max(1.0, atof(e));
 
   if (c->transport_kind == ST_TRANSPORT_NCCL) {
     st_status e;
@@ -410,7 +466,7 @@ st_status ctx_init(const st_config* cfg, const st_buffers* bufs, void* stream, s
   c->side_events.resize(c->layers.size() + 1);
   for (auto& e : c->side_events) ST_CUDA_TRY(cudaEventCreateWithFlags(&e, cudaEventDisableTiming));
   if (const char* e = getenv("ST_DWU_SMS")) {
-    c->dwu_sms = std::max(1, atoi(e));
+    c->dwu_sms = std::min(std::max(1, atoi(e)), c->sm_count - 2);
     c->dwu_env = true;
   }
   if (const char* e = getenv("ST_CONV_OVERLAP")) c->conv_overlap = atoi(e) != 0;
@@ -471,6 +527,20 @@ void ctx_destroy(st_ctx* c) {
     cudaStreamDestroy(c->side);
   }
   for (auto e : c->side_events) cudaEventDestroy(e);
+  if (c->comm_fwd) cudaStreamSynchronize(c->comm_fwd);
+  if (c->comm_bwd) cudaStreamSynchronize(c->comm_bwd);
+  c->tp.reset();  // communicators before the streams they used
+  for (int b = 0; b < 2; ++b)
+    for (cudaEvent_t e : {c->ev_sent_fwd[b], c->ev_sent_bwd[b], c->ev_recv_bwd[b], c->ev_bwd_ring[b], c->ev_join[b]})
+      if (e) cudaEventDestroy(e);
+  for (auto e : c->ev_recv_fwd)
+    if (e) cudaEventDestroy(e);
+  for (auto e : c->ev_bwd_slot)
+    if (e) cudaEventDestroy(e);
+  if (c->ev_fwd_done) cudaEventDestroy(c->ev_fwd_done);
+  if (c->ev_dx_ready) cudaEventDestroy(c->ev_dx_ready);
+  if (c->own_comm_fwd) cudaStreamDestroy(c->comm_fwd);
+  if (c->own_comm_bwd) cudaStreamDestroy(c->comm_bwd);
   delete c;
 }
 
@@ -497,7 +567,7 @@ st_status ctx_get_params(st_ctx* c, float* W, float* V, size_t n, int64_t* versi
   if ((W || V) && (int64_t)n != c->P)
     return set_error(ST_ERR_SHAPE, "get_params: n = %zu but stage has %lld", n, (long long)c->P);
   ST_CUDA_TRY(cudaSetDevice(c->device));
-  ST_CUDA_TRY(cudaStreamSynchronize(c->stream));
+  ST_TRY(ctx_wait(c));
   if (W) ST_CUDA_TRY(cudaMemcpy(W, c->W, n * 4, cudaMemcpyDeviceToHost));
   if (V) ST_CUDA_TRY(cudaMemcpy(V, c->V, n * 4, cudaMemcpyDeviceToHost));
   if (version) *version = c->version;
@@ -505,65 +575,146 @@ st_status ctx_get_params(st_ctx* c, float* W, float* V, size_t n, int64_t* versi
 }
 
 // ---- communication --------------------------------------------------------------
+//
+// Every message is one op on the comm stream of its direction (comm_fwd: activations,
+// comm_bwd: gradients), issued in comm-plan order (schedule.cpp build_comm_plan) and
+// ordered against the compute stream by events:
+//   send_fwd(i): waits for F(i) (ev_fwd_done), sends send_fwd2[i % 2]; F(i + 2) waits
+//                for it before overwriting that slot;
+//   send_bwd(j): waits for B(j)'s layer-0 dX only (ev_dx_ready), so the transfer
+//                overlaps that layer's dW + update; B(j + 2) waits before overwriting;
+//   recv_fwd(i): into stash slot i % S once B(i − S), its previous reader, finished;
+//                F(i) waits for it;
+//   recv_bwd(j): into recv_bwd2[j % 2] once B(j − 2) finished; B(j) waits for it.
+// NCCL receives are posted eagerly (after the previous task), so data arrives while
+// the current task computes; LOCAL receives block the host until the peer's send is
+// enqueued and are therefore issued right before the task that needs them.
+
+// one message: device buffer + element count
+struct CommOp {
+  int kind;
+  int64_t mb;
+  float* buf;
+  size_t count;
+};
 
 static CommOp comm_op(st_ctx* c, int kind, int64_t mb) {
   const size_t nin = (size_t)c->R * c->in_first, nout = (size_t)c->R * c->out_last;
   switch (kind) {
-    case CK_SEND_FWD: return {kind, mb, c->send_fwd, nout};
+    case CK_SEND_FWD: return {kind, mb, c->send_fwd2[mb % 2], nout};
     case CK_RECV_FWD:
       return {kind, mb, c->stash + (size_t)(mb % c->S) * c->slot_elems + c->layers[0].stash_off, nin};
-    case CK_SEND_BWD: return {kind, mb, c->send_bwd, nin};
-    default: return {kind, mb, c->recv_bwd, nout};
+    case CK_SEND_BWD: return {kind, mb, c->send_bwd2[mb % 2], nin};
+    default: return {kind, mb, c->recv_bwd2[mb % 2], nout};
   }
 }
 
-static st_status issue(st_ctx* c, const CommGroup& g, bool sends, bool recvs) {
-  CommOp ops[2];
-  int n = 0;
-  for (int i = 0; i < g.n_ops; ++i) {
-    const bool is_send = g.kind[i] == CK_SEND_FWD || g.kind[i] == CK_SEND_BWD;
-    if ((is_send && sends) || (!is_send && recvs)) ops[n++] = comm_op(c, g.kind[i], g.mb[i]);
-  }
-  if (n == 0) return ST_OK;
+static st_status issue_op(st_ctx* c, const CommGroup& g) {
   if (!c->tp) return set_error(ST_ERR_STATE, "stage %d: transport not connected", c->k);
-  Timed t(c, KC_COMM);
-  return c->tp->group(ops, n, c->stream);
+  for (int i = 0; i < g.n_ops; ++i) {
+    const CommOp o = comm_op(c, g.kind[i], g.mb[i]);
+    const bool fwd = o.kind == CK_SEND_FWD || o.kind == CK_RECV_FWD;
+    cudaStream_t cs = fwd ? c->comm_fwd : c->comm_bwd;
+    const int b = (int)(o.mb % 2);
+    const size_t slot = (size_t)(o.mb % c->S);
+    switch (o.kind) {
+      case CK_SEND_FWD: ST_CUDA_TRY(cudaStreamWaitEvent(cs, c->ev_fwd_done, 0)); break;
+      case CK_SEND_BWD: ST_CUDA_TRY(cudaStreamWaitEvent(cs, c->ev_dx_ready, 0)); break;
+      case CK_RECV_FWD:
+        if (c->bwd_slot_done[slot]) ST_CUDA_TRY(cudaStreamWaitEvent(cs, c->ev_bwd_slot[slot], 0));
+        break;
+      default:
+        if (c->bwd_ring_done[b]) ST_CUDA_TRY(cudaStreamWaitEvent(cs, c->ev_bwd_ring[b], 0));
+    }
+    {
+      Timed t(c, KC_COMM, cs);
+      if (o.kind == CK_SEND_FWD || o.kind == CK_SEND_BWD)
+        ST_TRY(c->tp->send(o.kind, o.mb, o.buf, o.count, cs));
+      else
+        ST_TRY(c->tp->recv(o.kind, o.mb, o.buf, o.count, cs));
+    }
+    switch (o.kind) {
+      case CK_SEND_FWD:
+        ST_CUDA_TRY(cudaEventRecord(c->ev_sent_fwd[b], cs));
+        c->sent_fwd_pending[b] = true;
+        break;
+      case CK_SEND_BWD:
+        ST_CUDA_TRY(cudaEventRecord(c->ev_sent_bwd[b], cs));
+        c->sent_bwd_pending[b] = true;
+        break;
+      case CK_RECV_FWD: ST_CUDA_TRY(cudaEventRecord(c->ev_recv_fwd[slot], cs)); break;
+      default: ST_CUDA_TRY(cudaEventRecord(c->ev_recv_bwd[b], cs));
+    }
+  }
+  return ST_OK;
 }
 
-// Before task n: make sure every receive it needs has been issued.
+static bool eager_recvs(st_ctx* c) { return c->transport_kind == ST_TRANSPORT_NCCL; }
+
+// Before task n: every op the plan places before it (its receive, and — LOCAL — the
+// previous task's send).
 static st_status comm_before_task(st_ctx* c, size_t n) {
-  const bool eager = c->tp && c->tp->eager_groups();
-  if (eager) {
-    while (c->plan_sent < c->plan.size() && (size_t)c->plan[c->plan_sent].before_op <= n) {
-      ST_TRY(issue(c, c->plan[c->plan_sent], true, true));
-      c->plan_sent++;
-    }
-    c->plan_recv = c->plan_sent;
-  } else {
-    while (c->plan_recv < c->plan.size() && (size_t)c->plan[c->plan_recv].before_op <= n) {
-      ST_TRY(issue(c, c->plan[c->plan_recv], false, true));
-      c->plan_recv++;
-    }
+  while (c->plan_next < c->plan.size() && (size_t)c->plan[c->plan_next].before_op <= n)
+    ST_TRY(issue_op(c, c->plan[c->plan_next++]));
+  return ST_OK;
+}
+
+// After task n: its send; NCCL also posts the next task's receive right away.
+static st_status comm_after_task(st_ctx* c, size_t n) {
+  while (c->plan_next < c->plan.size()) {
+    const CommGroup& g = c->plan[c->plan_next];
+    if ((size_t)g.before_op > n + 1) break;
+    const bool is_recv = g.kind[0] == CK_RECV_FWD || g.kind[0] == CK_RECV_BWD;
+    if ((size_t)g.before_op == n + 1 && is_recv && !eager_recvs(c)) break;
+    ST_TRY(issue_op(c, g));
+    c->plan_next++;
   }
   return ST_OK;
 }
 
-// After task n: issue its sends (NCCL: together with the next task's receive).
-static st_status comm_after_task(st_ctx* c, size_t n) {
-  const bool eager = c->tp && c->tp->eager_groups();
-  if (eager) {
-    while (c->plan_sent < c->plan.size() && (size_t)c->plan[c->plan_sent].before_op <= n + 1) {
-      ST_TRY(issue(c, c->plan[c->plan_sent], true, true));
-      c->plan_sent++;
-    }
-    c->plan_recv = c->plan_sent;
-  } else {
-    while (c->plan_sent < c->plan.size() && (size_t)c->plan[c->plan_sent].before_op <= n + 1) {
-      ST_TRY(issue(c, c->plan[c->plan_sent], true, false));
-      c->plan_sent++;
-    }
-  }
+// The comm streams' work so far becomes part of the compute stream (session end, sync).
+static st_status join_comm(st_ctx* c) {
+  if (!c->tp) return ST_OK;
+  ST_CUDA_TRY(cudaEventRecord(c->ev_join[0], c->comm_fwd));
+  ST_CUDA_TRY(cudaStreamWaitEvent(c->stream, c->ev_join[0], 0));
+  ST_CUDA_TRY(cudaEventRecord(c->ev_join[1], c->comm_bwd));
+  ST_CUDA_TRY(cudaStreamWaitEvent(c->stream, c->ev_join[1], 0));
   return ST_OK;
+}
+
+// Host wait for the compute stream that cannot hang on a dead peer: polls the stream and
+// the transport's asynchronous error state; a failure or no completion within
+// comm_timeout_s aborts the transport (NCCL: ncclCommAbort on both communicators) and
+// returns ST_ERR_NCCL (ST_ERR_STATE for a failed LOCAL peer).
+st_status ctx_wait(st_ctx* c) {
+  ST_TRY(join_comm(c));
+  if (!c->tp) {
+    ST_CUDA_TRY(cudaStreamSynchronize(c->stream));
+    return ST_OK;
+  }
+  const auto t0 = std::chrono::steady_clock::now();
+  int sleep_us = 2;
+  for (;;) {
+    const cudaError_t q = cudaStreamQuery(c->stream);
+    if (q == cudaSuccess) return ST_OK;
+    if (q != cudaErrorNotReady) return set_error(ST_ERR_CUDA, "stage %d: %s", c->k, cudaGetErrorString(q));
+    const st_status e = c->tp->poll();
+    if (e != ST_OK) {
+      const std::string msg = st_last_error();
+      c->tp->abort();
+      return set_error(e, "%s", msg.c_str());
+    }
+    const double waited = std::chrono::duration<double>(std::chrono::steady_clock::now() - t0).count();
+    if (waited > c->comm_timeout_s) {
+      c->tp->abort();
+      return set_error(c->transport_kind == ST_TRANSPORT_NCCL ? ST_ERR_NCCL : ST_ERR_STATE,
+                       "stage %d: no completion after %.0f s (ST_COMM_TIMEOUT_S): a peer stage is hung or gone; "
+                       "transport aborted",
+                       c->k, waited);
+    }
+    std::this_thread::sleep_for(std::chrono::microseconds(sleep_us));
+    sleep_us = std::min(sleep_us * 2, 1000);
+  }
 }
 
 // ---- tasks -----------------------------------------------------------------------
@@ -857,7 +1008,7 @@ static st_status backward_compute(st_ctx* c, int64_t mb, bool fused = false) {
       // Ain fused), then dW = Σ_p window(Ain)ᵀ dZ (+ bias gradient) into G
       if (D) {
         GemmArgs gx = gargs_rows(c, c->B, 9 * L.n_in, L.n_out);
-        if (side_busy) gx.max_ctas = std::max(1, 148 - c->dwu_sms);  // a conv dW is running on the side
+        if (side_busy) gx.max_ctas = std::max(2, (c->sm_count - c->dwu_sms) & ~1);  // a conv dW is running on the side
         Timed t(c, KC_GEMM_DX);
         ST_TRY(tc_conv_dx(gx, dZ, L.hw, L.hw, L.n_in, L.n_out, Wh + L.w_off, producer_act == ST_ACT_RELU ? Ain : nullptr,
                           D));
@@ -961,7 +1112,7 @@ static st_status backward_compute(st_ctx* c, int64_t mb, bool fused = false) {
         GemmArgs gx = gargs(c, L);
         // share the GPU with the running dW + update — unless that one is small (e.g. the
         // 10-wide output layer's), when this dX would otherwise run alone on part of the GPU
-        if (side_busy && side_params >= (int64_t)1 << 22) gx.max_ctas = std::max(1, 148 - side_dwu);
+        if (side_busy && side_params >= (int64_t)1 << 22) gx.max_ctas = std::max(2, (c->sm_count - side_dwu) & ~1);
         Timed t(c, KC_GEMM_DX);
         ST_TRY(gemm_dx(gx, dZ, Wh + L.w_off, producer_act == ST_ACT_RELU ? Ain : nullptr, D));
         c->launches += gemm_last_launches();
@@ -980,7 +1131,7 @@ static st_status backward_compute(st_ctx* c, int64_t mb, bool fused = false) {
         // column (no dZ re-staging, adjacent W / V rows streamed together): 16384-wide
         // layers 80 → 128 CTAs, large FCN 5.2k → 5.9k samples/s. ST_DWU_SMS overrides.
         const int m_tiles = (L.n_out + 127) / 128;
-        side_dwu = c->dwu_env ? c->dwu_sms : ((m_tiles >= 100 && m_tiles <= 140) ? m_tiles : c->dwu_sms);
+        side_dwu = c->dwu_env ? c->dwu_sms : ((m_tiles >= 100 && m_tiles <= c->sm_count - 8) ? m_tiles : c->dwu_sms);
         if (more_dx) gw.max_ctas = side_dwu;
         UpdateArgs bu{};
         if (L.bias) bu = block_update(c, L.b_off, kc);
@@ -1006,6 +1157,9 @@ static st_status backward_compute(st_ctx* c, int64_t mb, bool fused = false) {
       ST_TRY(launch_update_predict(u.W, u.V, c->G + L.w_off, u.WF, u.WB, (size_t)L.n_params, kc, c->stream));
       c->launches += 1;
     }
+    // the layer-0 dX is the message to stage k−1: its send may start now, overlapping
+    // this layer's dW + update on the side stream
+    if (l == 0 && D && !c->first_stage) ST_CUDA_TRY(cudaEventRecord(c->ev_dx_ready, c->stream));
     if (D) dZ = D;
   }
   ST_TRY(join_side());
@@ -1035,10 +1189,39 @@ static st_status run_task(st_ctx* c, const float* x_dev, const int32_t* y_dev, b
   e.s = t.dir == ST_FWD ? c->sF : c->sB;
   e.target = e.base_version + e.s;
   c->trace.push_back(e);
-  if (t.dir == ST_FWD)
+  const int b = (int)(t.mb % 2);
+  const size_t slot = (size_t)(t.mb % c->S);
+  if (t.dir == ST_FWD) {
+    if (!c->first_stage) ST_CUDA_TRY(cudaStreamWaitEvent(c->stream, c->ev_recv_fwd[slot], 0));  // input arrived
+    if (!c->last_stage) {  // the output slot's previous send (mb − 2) has left
+      if (c->sent_fwd_pending[b]) ST_CUDA_TRY(cudaStreamWaitEvent(c->stream, c->ev_sent_fwd[b], 0));
+      c->send_fwd = c->send_fwd2[b];
+    }
     ST_TRY(forward_compute(c, t.mb, x_dev, y_dev, host_io, loss_host));
-  else {
+    if (!c->last_stage) ST_CUDA_TRY(cudaEventRecord(c->ev_fwd_done, c->stream));
+  } else {
+    if (!c->last_stage) {  // the gradient from k+1 arrived
+      ST_CUDA_TRY(cudaStreamWaitEvent(c->stream, c->ev_recv_bwd[b], 0));
+      c->recv_bwd = c->recv_bwd2[b];
+    }
+    if (!c->first_stage) {
+      if (c->sent_bwd_pending[b]) ST_CUDA_TRY(cudaStreamWaitEvent(c->stream, c->ev_sent_bwd[b], 0));
+      c->send_bwd = c->send_bwd2[b];
+    }
     ST_TRY(backward_compute(c, t.mb, fused_update));
+    // this backward's readers are done with its stash slot and its gradient slot
+    ST_CUDA_TRY(cudaEventRecord(c->ev_bwd_slot[slot], c->stream));
+    c->bwd_slot_done[slot] = 1;
+    ST_CUDA_TRY(cudaEventRecord(c->ev_bwd_ring[b], c->stream));
+    c->bwd_ring_done[b] = true;
+    for (size_t i = 0; i < c->marks.size();) {  // st_record_after_backward
+      if (c->marks[i].first == t.mb) {
+        ST_CUDA_TRY(cudaEventRecord(c->marks[i].second, c->stream));
+        c->marks.erase(c->marks.begin() + (long)i);
+      } else {
+        ++i;
+      }
+    }
     if (fused_update)
       c->version += 1;  // the update already ran inside the dW epilogues
     else
@@ -1078,7 +1261,7 @@ st_status ctx_forward(st_ctx* c, int64_t mb, const float* x_dev, const int32_t* 
   ST_TRY(run_task(c, x_dev, y_dev));
   if (loss_host && c->last_stage) {
     ST_CUDA_TRY(cudaMemcpyAsync(loss_host, c->losses_dev + (mb % c->max_mb), 4, cudaMemcpyDeviceToHost, c->stream));
-    ST_CUDA_TRY(cudaStreamSynchronize(c->stream));
+    ST_TRY(ctx_wait(c));
     if (!std::isfinite(*loss_host))
       return set_error(ST_ERR_DIVERGED, "non-finite loss at mini-batch %lld", (long long)mb);
   }
@@ -1119,7 +1302,7 @@ st_status ctx_step(st_ctx* c, const float* x_dev, const int32_t* y_dev, st_step_
     z.ran_forward = (int32_t)t.mb;
     if (c->last_stage) {
       ST_CUDA_TRY(cudaMemcpyAsync(&z.loss, c->losses_dev + (t.mb % c->max_mb), 4, cudaMemcpyDeviceToHost, c->stream));
-      ST_CUDA_TRY(cudaStreamSynchronize(c->stream));
+      ST_TRY(ctx_wait(c));
     }
   }
   // a warm-up F is followed by another F; a steady F by its paired B; cooldown is B alone
@@ -1151,14 +1334,25 @@ st_status ctx_run(st_ctx* c, int64_t M, const float* xs, const int32_t* ys, floa
     float* lh = (host_io && losses_host && c->last_stage && t.dir == ST_FWD) ? losses_host + t.mb : nullptr;
     ST_TRY(run_task(c, x_of(c, xs, t.mb), y_of(c, ys, t.mb), host_io, lh, true));
   }
-  if (losses_host && c->last_stage && M > 0) {
-    if (!host_io)
-      ST_CUDA_TRY(cudaMemcpyAsync(losses_host, c->losses_dev, (size_t)M * 4, cudaMemcpyDeviceToHost, c->stream));
-    ST_CUDA_TRY(cudaStreamSynchronize(c->stream));
+  // the session's last transfers become part of the compute stream
+  ST_TRY(join_comm(c));
+  const bool want_losses = losses_host && c->last_stage && M > 0;
+  if (want_losses && !host_io)
+    ST_CUDA_TRY(cudaMemcpyAsync(losses_host, c->losses_dev, (size_t)M * 4, cudaMemcpyDeviceToHost, c->stream));
+  // host buffers (st_run_host) are read by asynchronous copies: never return before they finish
+  if (want_losses || host_io) ST_TRY(ctx_wait(c));
+  if (want_losses)
     for (int64_t i = 0; i < M; ++i)
       if (!std::isfinite(losses_host[i]))
         return set_error(ST_ERR_DIVERGED, "non-finite loss at mini-batch %lld", (long long)i);
-  }
+  return ST_OK;
+}
+
+st_status ctx_mark_after_backward(st_ctx* c, int64_t mb, void* event) {
+  if (!event) return set_error(ST_ERR_INPUT, "record_after_backward: event is NULL");
+  if (mb < 0) return set_error(ST_ERR_INPUT, "record_after_backward: mb must be >= 0");
+  if (c->marks.size() >= 64) return set_error(ST_ERR_INPUT, "record_after_backward: more than 64 pending marks");
+  c->marks.push_back({mb, static_cast<cudaEvent_t>(event)});
   return ST_OK;
 }
 
@@ -1170,13 +1364,27 @@ st_status ctx_run_group(st_ctx** ctxs, int n, int64_t M, const float* xs, const 
   for (int k = 0; k < n; ++k) {
     th.emplace_back([&, k] {
       st_ctx* c = ctxs[k];
-      cudaSetDevice(c->device);
-      res[k] = ctx_run(c, M, c->first_stage ? xs : nullptr, c->last_stage ? ys : nullptr,
-                       c->last_stage ? losses_host : nullptr, false);
-      if (res[k] != ST_OK) msg[k] = st_last_error();
+      try {
+        cudaSetDevice(c->device);
+        res[k] = ctx_run(c, M, c->first_stage ? xs : nullptr, c->last_stage ? ys : nullptr,
+                         c->last_stage ? losses_host : nullptr, false);
+        if (res[k] != ST_OK) msg[k] = st_last_error();
+      } catch (const std::exception& e) {
+        res[k] = ST_ERR_STATE;
+        msg[k] = std::string("internal exception: ") + e.what();
+      } catch (...) {
+        res[k] = ST_ERR_STATE;
+        msg[k] = "internal exception";
+      }
+      // a failed stage releases its peers at once instead of leaving them to time out
+      if (res[k] != ST_OK && c->tp) c->tp->abort();
     });
   }
   for (auto& t : th) t.join();
+  // report the root cause: a stage that failed on its own, not one released by the abort
+  for (int k = 0; k < n; ++k)
+    if (res[k] != ST_OK && msg[k].find("a peer stage failed") == std::string::npos)
+      return set_error(res[k], "stage %d: %s", k, msg[k].c_str());
   for (int k = 0; k < n; ++k)
     if (res[k] != ST_OK) return set_error(res[k], "stage %d: %s", k, msg[k].c_str());
   return ST_OK;

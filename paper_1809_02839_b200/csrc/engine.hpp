@@ -23,20 +23,22 @@ std::vector<st_event> program_events(int N, int k, int64_t M, int pred);
 std::vector<CommGroup> build_comm_plan(int N, int k, int64_t M);
 st_status partition_layers(const double* cost, int L, int N, int32_t* cuts, double* max_cost);
 
-// One communication op of a group: device buffer + element count.
-struct CommOp {
-  int kind;
-  int64_t mb;
-  float* buf;
-  size_t count;
-};
-
+// Stage-to-stage transport. The engine issues every
+// message as ONE op on the comm stream of its direction (kind CK_SEND_FWD /
+// CK_RECV_FWD: activations, the k→k+1 channel; CK_SEND_BWD / CK_RECV_BWD:
+// gradients, the k+1→k channel), ordered against the compute stream with events
+// (engine.cpp issue_op). A transport only moves bytes on the stream it is given.
 class Transport {
  public:
   virtual ~Transport() = default;
-  // Issue one group on `stream` (NCCL: ncclGroupStart/End; LOCAL: sends then receives).
-  virtual st_status group(const CommOp* ops, int n, cudaStream_t stream) = 0;
-  virtual bool eager_groups() const = 0;  // NCCL: issue whole groups eagerly at task end
+  virtual st_status send(int kind, int64_t mb, const float* buf, size_t count, cudaStream_t s) = 0;
+  virtual st_status recv(int kind, int64_t mb, float* buf, size_t count, cudaStream_t s) = 0;
+  // asynchronous failure of the transport (NCCL: ncclCommGetAsyncError on both
+  // communicators); ST_OK while healthy
+  virtual st_status poll() { return ST_OK; }
+  // tear the transport down after a failure so that no peer or stream waits forever
+  // (NCCL: ncclCommAbort; LOCAL: wake and fail every blocked peer)
+  virtual void abort() {}
 };
 
 std::unique_ptr<Transport> make_nccl_transport(const uint8_t id[128], int N, int k, int device, st_status* err);
@@ -46,6 +48,7 @@ std::unique_ptr<Transport> make_local_transport(std::shared_ptr<LocalLink> link,
                                                 float* ring_bwd, size_t fwd_elems, size_t bwd_elems,
                                                 st_status* err);
 std::shared_ptr<LocalLink> make_local_link(int N);
+void abort_local_link(LocalLink* link);
 
 struct LayerInfo {
   int n_in, n_out, act, bias, kind;
@@ -123,9 +126,31 @@ struct st_ctx {
   int64_t slot_elems = 0;
   int S = 1;  // stash slots = N − k
   // work carve-up
-  float* send_fwd = nullptr;  // [B × out_last]  (non-last stage)
-  float* recv_bwd = nullptr;  // [B × out_last]  (non-last stage)
-  float* send_bwd = nullptr;  // [B × in_first]  (k > 0)
+  // messages of the current task (engine.cpp run_task picks one of two slots per
+  // mini-batch parity, so a transfer of mb can overlap the compute of mb + 1)
+  float* send_fwd = nullptr;  // [R × out_last]  (non-last stage)
+  float* recv_bwd = nullptr;  // [R × out_last]  (non-last stage)
+  float* send_bwd = nullptr;  // [R × in_first]  (k > 0)
+  float* send_fwd2[2] = {nullptr, nullptr};
+  float* recv_bwd2[2] = {nullptr, nullptr};
+  float* send_bwd2[2] = {nullptr, nullptr};
+  // comm streams (activations k→k+1 / from k−1 on comm_fwd; gradients on comm_bwd) and
+  // the events ordering them against the compute stream (engine.cpp issue_op)
+  cudaStream_t comm_fwd = nullptr, comm_bwd = nullptr;
+  bool own_comm_fwd = false, own_comm_bwd = false;
+  cudaEvent_t ev_sent_fwd[2] = {}, ev_sent_bwd[2] = {};  // send of slot b finished (comm stream)
+  bool sent_fwd_pending[2] = {false, false}, sent_bwd_pending[2] = {false, false};
+  cudaEvent_t ev_recv_bwd[2] = {};                       // gradient of slot b arrived (comm_bwd)
+  cudaEvent_t ev_bwd_ring[2] = {};                       // the backward reading recv_bwd2[b] finished (compute)
+  bool bwd_ring_done[2] = {false, false};
+  std::vector<cudaEvent_t> ev_recv_fwd;                  // per stash slot: activation arrived (comm_fwd)
+  std::vector<cudaEvent_t> ev_bwd_slot;                  // per stash slot: its last backward finished (compute)
+  std::vector<char> bwd_slot_done;
+  cudaEvent_t ev_fwd_done = nullptr;    // the forward whose output is sent next
+  cudaEvent_t ev_dx_ready = nullptr;    // layer-0 dX of the current backward written (compute)
+  cudaEvent_t ev_join[2] = {};          // comm streams joined into compute at session end
+  double comm_timeout_s = 600.0;        // ST_COMM_TIMEOUT_S: a wait longer than this is a hung peer
+  std::vector<std::pair<int64_t, cudaEvent_t>> marks;  // st_record_after_backward
   float* logits = nullptr;    // [B × C]         (last stage)
   float* dlogits = nullptr;   // [B × C]
   float* bufA = nullptr;      // [R × max width] backward gradient buffers (3-way rotation)
@@ -162,13 +187,13 @@ struct st_ctx {
   void* gemm_ws = nullptr;
   void* gemm_ws2 = nullptr;  // workspace of the side stream
   cudaStream_t stream = nullptr;
+  int sm_count = 148;  // SMs of this device (cudaDevAttrMultiProcessorCount)
 
   // program state
   std::vector<st::Task> program;
   std::vector<st::CommGroup> plan;
   size_t pc = 0;
-  size_t plan_sent = 0;  // LOCAL: sends issued (by group index); NCCL: groups issued
-  size_t plan_recv = 0;  // LOCAL: receives issued
+  size_t plan_next = 0;  // next comm-plan op to issue
   int64_t session_M = 0;
   int64_t version = 0;
   bool pending_update = false;

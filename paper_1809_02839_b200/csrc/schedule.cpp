@@ -9,13 +9,15 @@
 // Base versions: an F(i) runs after B(i−w−1), so c_F = max(0, i−w); a B(j) runs
 // after B(j−1), so c_B = j.
 //
-// Communication plan. Per task: F(i) on k > 0 needs recv_fwd(i)
-// before it; F(i) on k < N−1 is followed by send_fwd(i); B(j) on k < N−1 needs
-// recv_bwd(j); B(j) on k > 0 is followed by send_bwd(j). Between two consecutive
-// tasks the trailing send of the first and the leading receive of the second form
-// ONE NCCL group when they talk to the same peer (Megatron's
-// send_forward_recv_backward / send_backward_recv_forward pairing); otherwise the
-// send is issued first as its own group.
+// Communication plan. Per task: F(i) on k > 0 needs
+// recv_fwd(i) before it; F(i) on k < N−1 is followed by send_fwd(i); B(j) on k < N−1
+// needs recv_bwd(j); B(j) on k > 0 is followed by send_bwd(j). The plan lists these
+// ops one per record, in issue order: at each task boundary n the trailing send of
+// task n−1, then the leading receive of task n (before_op = n). The engine runs each
+// direction on its own communicator and comm stream (activations: send_fwd /
+// recv_fwd; gradients: send_bwd / recv_bwd), so the two directions never wait on
+// each other and no send/recv pairing into groups is needed; within a direction the
+// ops of every stage follow this order, which pairs them per peer in mini-batch order.
 #include <vector>
 
 #include <limits>
@@ -76,7 +78,6 @@ struct Op {
   int kind;  // CK_*
   int64_t mb;
 };
-int peer_of(int kind) { return (kind == CK_SEND_FWD || kind == CK_RECV_BWD) ? +1 : -1; }
 }  // namespace
 
 std::vector<CommGroup> build_comm_plan(int N, int k, int64_t M) {
@@ -94,14 +95,8 @@ std::vector<CommGroup> build_comm_plan(int N, int k, int64_t M) {
   };
   for (size_t n = 0; n <= p.size(); ++n) {
     Op a{}, b{};
-    const bool has_post = n > 0 && post(p[n - 1], &a);
-    const bool has_pre = n < p.size() && pre(p[n], &b);
-    if (has_post && has_pre && peer_of(a.kind) == peer_of(b.kind)) {
-      plan.push_back({(int32_t)n, 2, {a.kind, b.kind}, {a.mb, b.mb}});
-    } else {
-      if (has_post) plan.push_back({(int32_t)n, 1, {a.kind, -1}, {a.mb, -1}});
-      if (has_pre) plan.push_back({(int32_t)n, 1, {b.kind, -1}, {b.mb, -1}});
-    }
+    if (n > 0 && post(p[n - 1], &a)) plan.push_back({(int32_t)n, 1, {a.kind, -1}, {a.mb, -1}});
+    if (n < p.size() && pre(p[n], &b)) plan.push_back({(int32_t)n, 1, {b.kind, -1}, {b.mb, -1}});
   }
   return plan;
 }

@@ -1,19 +1,29 @@
-// Stage-to-stage transports.
+// Stage-to-stage transports ("activations and
+// gradients are transferred between GPUs", "sent to the next GPU ... to hide
+// the latency").
 //
-// NCCL: one process per GPU; every message is an ncclSend/ncclRecv between
-// adjacent stages issued on the stage's compute stream, grouped exactly as the
-// host comm plan says (schedule.cpp), so the peers' sequences pair in order.
+// The engine (engine.cpp issue_op) issues every message as one op on the comm
+// stream of its direction — activations k→k+1 on comm_fwd, gradients k+1→k on
+// comm_bwd — ordered against the compute stream with CUDA events, so transfers
+// overlap compute. A transport only moves the bytes on the stream it is handed.
+//
+// NCCL: one process per GPU; two communicators over the same ranks (one per
+// direction), ncclSend / ncclRecv per message; asynchronous errors
+// polled by the engine while it waits (ST_ERR_NCCL), ncclCommAbort on failure.
 //
 // LOCAL: several stage contexts in one process (tests run an N-stage pipeline on
 // one GPU; bench can oversubscribe). Each directed channel k→k+1 / k+1→k is a
 // host queue of (mini-batch, ring slot) records plus a device ring owned by the
 // sender: send = stream-ordered copy into the ring slot + CUDA event; receive =
 // blocking pop, wait on the event, copy out, record a "consumed" event the sender
-// waits on before reusing the slot. Same plan, same ordering per channel.
+// waits on before reusing the slot. A failing stage aborts the link: every peer
+// blocked on it returns ST_ERR_STATE at once instead of waiting for the timeout.
 #include <nccl.h>
 
+#include <atomic>
 #include <chrono>
 #include <condition_variable>
+#include <cstring>
 #include <deque>
 #include <mutex>
 
@@ -24,35 +34,65 @@ namespace st {
 // ------------------------------------------------------------------ NCCL
 namespace {
 
+// Two communicators over the same N ranks, one per direction of the pipeline (SURVEY
+// §7.2 H5: forward- and backward-direction traffic must progress independently, so
+// they do not share a communicator): `fwd_` carries the activations k → k+1, `bwd_`
+// the gradients k+1 → k. The engine issues each communicator's ops from one host
+// thread on one comm stream, in the same order on every rank (the comm plan).
 class NcclTransport final : public Transport {
  public:
-  NcclTransport(ncclComm_t c, int N, int k) : comm_(c), N_(N), k_(k) {}
+  NcclTransport(ncclComm_t f, ncclComm_t b, int N, int k) : fwd_(f), bwd_(b), N_(N), k_(k) {}
   ~NcclTransport() override {
-    if (comm_) ncclCommDestroy(comm_);
+    if (aborted_) return;
+    if (fwd_) ncclCommDestroy(fwd_);
+    if (bwd_) ncclCommDestroy(bwd_);
   }
-  bool eager_groups() const override { return true; }
-  st_status group(const CommOp* ops, int n, cudaStream_t stream) override {
-    ncclResult_t r = ncclGroupStart();
-    if (r != ncclSuccess) return set_error(ST_ERR_NCCL, "ncclGroupStart: %s", ncclGetErrorString(r));
-    for (int i = 0; i < n && r == ncclSuccess; ++i) {
-      const CommOp& o = ops[i];
-      switch (o.kind) {
-        case CK_SEND_FWD: r = ncclSend(o.buf, o.count, ncclFloat32, k_ + 1, comm_, stream); break;
-        case CK_RECV_FWD: r = ncclRecv(o.buf, o.count, ncclFloat32, k_ - 1, comm_, stream); break;
-        case CK_SEND_BWD: r = ncclSend(o.buf, o.count, ncclFloat32, k_ - 1, comm_, stream); break;
-        case CK_RECV_BWD: r = ncclRecv(o.buf, o.count, ncclFloat32, k_ + 1, comm_, stream); break;
-        default: r = ncclInvalidArgument;
-      }
-    }
-    ncclResult_t r2 = ncclGroupEnd();
-    if (r != ncclSuccess) return set_error(ST_ERR_NCCL, "ncclSend/Recv: %s", ncclGetErrorString(r));
-    if (r2 != ncclSuccess) return set_error(ST_ERR_NCCL, "ncclGroupEnd: %s", ncclGetErrorString(r2));
+  st_status send(int kind, int64_t mb, const float* buf, size_t count, cudaStream_t s) override {
+    const bool f = kind == CK_SEND_FWD;
+    if (!f && kind != CK_SEND_BWD) return set_error(ST_ERR_INPUT, "nccl send: bad kind %d", kind);
+    const int peer = f ? k_ + 1 : k_ - 1;
+    if (peer < 0 || peer >= N_) return set_error(ST_ERR_STATE, "stage %d: no peer %d", k_, peer);
+    ncclResult_t r = ncclSend(buf, count, ncclFloat32, peer, f ? fwd_ : bwd_, s);
+    if (r != ncclSuccess)
+      return set_error(ST_ERR_NCCL, "stage %d: ncclSend(mb %lld -> %d): %s", k_, (long long)mb, peer,
+                       ncclGetErrorString(r));
     return ST_OK;
+  }
+  st_status recv(int kind, int64_t mb, float* buf, size_t count, cudaStream_t s) override {
+    const bool f = kind == CK_RECV_FWD;
+    if (!f && kind != CK_RECV_BWD) return set_error(ST_ERR_INPUT, "nccl recv: bad kind %d", kind);
+    const int peer = f ? k_ - 1 : k_ + 1;
+    if (peer < 0 || peer >= N_) return set_error(ST_ERR_STATE, "stage %d: no peer %d", k_, peer);
+    ncclResult_t r = ncclRecv(buf, count, ncclFloat32, peer, f ? fwd_ : bwd_, s);
+    if (r != ncclSuccess)
+      return set_error(ST_ERR_NCCL, "stage %d: ncclRecv(mb %lld <- %d): %s", k_, (long long)mb, peer,
+                       ncclGetErrorString(r));
+    return ST_OK;
+  }
+  st_status poll() override {
+    if (aborted_) return set_error(ST_ERR_NCCL, "stage %d: communicators were aborted", k_);
+    for (ncclComm_t c : {fwd_, bwd_}) {
+      ncclResult_t a = ncclSuccess;
+      ncclResult_t r = ncclCommGetAsyncError(c, &a);
+      if (r != ncclSuccess)
+        return set_error(ST_ERR_NCCL, "stage %d: ncclCommGetAsyncError: %s", k_, ncclGetErrorString(r));
+      if (a != ncclSuccess && a != ncclInProgress)
+        return set_error(ST_ERR_NCCL, "stage %d: asynchronous NCCL error on the %s communicator: %s", k_,
+                         c == fwd_ ? "activation" : "gradient", ncclGetErrorString(a));
+    }
+    return ST_OK;
+  }
+  void abort() override {
+    if (aborted_) return;
+    aborted_ = true;
+    ncclCommAbort(fwd_);
+    ncclCommAbort(bwd_);
   }
 
  private:
-  ncclComm_t comm_;
+  ncclComm_t fwd_, bwd_;
   int N_, k_;
+  bool aborted_ = false;
 };
 
 }  // namespace
@@ -67,13 +107,20 @@ std::unique_ptr<Transport> make_nccl_transport(const uint8_t id[128], int N, int
     *err = set_error(ST_ERR_CUDA, "cudaSetDevice(%d)", device);
     return nullptr;
   }
-  ncclComm_t comm = nullptr;
-  ncclResult_t r = ncclCommInitRank(&comm, N, uid, k);
+  ncclComm_t f = nullptr, b = nullptr;
+  ncclResult_t r = ncclCommInitRank(&f, N, uid, k);
   if (r != ncclSuccess) {
     *err = set_error(ST_ERR_NCCL, "ncclCommInitRank(N=%d, rank=%d): %s", N, k, ncclGetErrorString(r));
     return nullptr;
   }
-  return std::unique_ptr<Transport>(new NcclTransport(comm, N, k));
+  // the gradient-direction communicator: same ranks, same order (collective over all stages)
+  r = ncclCommSplit(f, 0, k, &b, nullptr);
+  if (r != ncclSuccess || !b) {
+    *err = set_error(ST_ERR_NCCL, "ncclCommSplit (gradient communicator, rank %d): %s", k, ncclGetErrorString(r));
+    ncclCommDestroy(f);
+    return nullptr;
+  }
+  return std::unique_ptr<Transport>(new NcclTransport(f, b, N, k));
 }
 
 // ------------------------------------------------------------------ LOCAL
@@ -96,6 +143,7 @@ struct Channel {
 
 struct LocalLink {
   int N = 0;
+  std::atomic<bool> aborted{false};
   std::vector<std::unique_ptr<Channel>> fwd, bwd;  // fwd[k]: k→k+1, bwd[k]: k+1→k
 };
 
@@ -109,6 +157,16 @@ std::shared_ptr<LocalLink> make_local_link(int N) {
   return l;
 }
 
+void abort_local_link(LocalLink* l) {
+  if (!l) return;
+  l->aborted = true;
+  for (auto* v : {&l->fwd, &l->bwd})
+    for (auto& ch : *v) {
+      { std::lock_guard<std::mutex> g(ch->mu); }
+      ch->cv.notify_all();
+    }
+}
+
 namespace {
 
 constexpr int kRingSlots(int N) { return N + 1; }
@@ -120,7 +178,6 @@ class LocalTransport final : public Transport {
   ~LocalTransport() override {
     for (auto& e : owned_) cudaEventDestroy(e);
   }
-  bool eager_groups() const override { return false; }
 
   st_status setup(float* ring_fwd, float* ring_bwd, size_t fwd_elems, size_t bwd_elems) {
     const int N = link_->N;
@@ -134,22 +191,25 @@ class LocalTransport final : public Transport {
     return ST_OK;
   }
 
-  st_status group(const CommOp* ops, int n, cudaStream_t stream) override {
-    for (int pass = 0; pass < 2; ++pass)  // sends first, then receives
-      for (int i = 0; i < n; ++i) {
-        const CommOp& o = ops[i];
-        const bool is_send = (o.kind == CK_SEND_FWD || o.kind == CK_SEND_BWD);
-        if (is_send != (pass == 0)) continue;
-        switch (o.kind) {
-          case CK_SEND_FWD: ST_TRY(send(*link_->fwd[k_], o, stream)); break;
-          case CK_SEND_BWD: ST_TRY(send(*link_->bwd[k_ - 1], o, stream)); break;
-          case CK_RECV_FWD: ST_TRY(recv(*link_->fwd[k_ - 1], o, stream)); break;
-          case CK_RECV_BWD: ST_TRY(recv(*link_->bwd[k_], o, stream)); break;
-          default: return set_error(ST_ERR_INPUT, "local transport: bad op kind %d", o.kind);
-        }
-      }
+  st_status send(int kind, int64_t mb, const float* buf, size_t count, cudaStream_t s) override {
+    switch (kind) {
+      case CK_SEND_FWD: return do_send(*link_->fwd[k_], mb, buf, count, s);
+      case CK_SEND_BWD: return do_send(*link_->bwd[k_ - 1], mb, buf, count, s);
+      default: return set_error(ST_ERR_INPUT, "local transport: bad send kind %d", kind);
+    }
+  }
+  st_status recv(int kind, int64_t mb, float* buf, size_t count, cudaStream_t s) override {
+    switch (kind) {
+      case CK_RECV_FWD: return do_recv(*link_->fwd[k_ - 1], mb, buf, count, s);
+      case CK_RECV_BWD: return do_recv(*link_->bwd[k_], mb, buf, count, s);
+      default: return set_error(ST_ERR_INPUT, "local transport: bad recv kind %d", kind);
+    }
+  }
+  st_status poll() override {
+    if (link_->aborted) return set_error(ST_ERR_STATE, "local transport: a peer stage failed (stage %d)", k_);
     return ST_OK;
   }
+  void abort() override { abort_local_link(link_.get()); }
 
  private:
   st_status init_sender(Channel& ch, float* ring, size_t elems, int R) {
@@ -176,37 +236,43 @@ class LocalTransport final : public Transport {
     return ST_OK;
   }
 
-  st_status send(Channel& ch, const CommOp& o, cudaStream_t stream) {
+  st_status do_send(Channel& ch, int64_t mb, const float* buf, size_t count, cudaStream_t stream) {
     std::unique_lock<std::mutex> lk(ch.mu);
-    if (o.count > ch.elems) return set_error(ST_ERR_SHAPE, "local send: %zu > ring slot %zu", o.count, ch.elems);
+    if (count > ch.elems) return set_error(ST_ERR_SHAPE, "local send: %zu > ring slot %zu", count, ch.elems);
     // never reuse a slot whose previous message has not been taken by the receiver
-    if (!ch.cv.wait_for(lk, std::chrono::duration<double>(kTimeoutS), [&] { return ch.sent - ch.received < ch.R; }))
-      return set_error(ST_ERR_STATE, "local transport: send timeout (stage %d, mb %lld)", k_, (long long)o.mb);
+    if (!ch.cv.wait_for(lk, std::chrono::duration<double>(kTimeoutS),
+                        [&] { return link_->aborted || ch.sent - ch.received < ch.R; }))
+      return set_error(ST_ERR_STATE, "local transport: send timeout (stage %d, mb %lld)", k_, (long long)mb);
+    if (link_->aborted)
+      return set_error(ST_ERR_STATE, "local transport: a peer stage failed (stage %d, send mb %lld)", k_, (long long)mb);
     const int slot = (int)(ch.sent % ch.R);
     if (ch.consumed_recorded.size() == (size_t)ch.R && ch.consumed_recorded[slot])
       ST_CUDA_TRY(cudaStreamWaitEvent(stream, ch.consumed[slot], 0));
     float* dst = ch.ring + (size_t)slot * ch.elems;
-    ST_CUDA_TRY(cudaMemcpyAsync(dst, o.buf, o.count * sizeof(float), cudaMemcpyDefault, stream));
+    ST_CUDA_TRY(cudaMemcpyAsync(dst, buf, count * sizeof(float), cudaMemcpyDefault, stream));
     ST_CUDA_TRY(cudaEventRecord(ch.ready[slot], stream));
-    ch.q.push_back({o.mb, slot, o.count});
+    ch.q.push_back({mb, slot, count});
     ch.sent++;
     lk.unlock();
     ch.cv.notify_all();
     return ST_OK;
   }
 
-  st_status recv(Channel& ch, const CommOp& o, cudaStream_t stream) {
+  st_status do_recv(Channel& ch, int64_t mb, float* buf, size_t count, cudaStream_t stream) {
     std::unique_lock<std::mutex> lk(ch.mu);
-    if (!ch.cv.wait_for(lk, std::chrono::duration<double>(kTimeoutS), [&] { return !ch.q.empty(); }))
-      return set_error(ST_ERR_STATE, "local transport: receive timeout (stage %d, mb %lld)", k_, (long long)o.mb);
+    if (!ch.cv.wait_for(lk, std::chrono::duration<double>(kTimeoutS),
+                        [&] { return link_->aborted || !ch.q.empty(); }))
+      return set_error(ST_ERR_STATE, "local transport: receive timeout (stage %d, mb %lld)", k_, (long long)mb);
+    if (link_->aborted)
+      return set_error(ST_ERR_STATE, "local transport: a peer stage failed (stage %d, recv mb %lld)", k_, (long long)mb);
     Channel::Msg m = ch.q.front();
     ch.q.pop_front();
-    if (m.mb != o.mb || m.count != o.count)
+    if (m.mb != mb || m.count != count)
       return set_error(ST_ERR_STATE, "local transport: expected mb %lld (%zu floats), got mb %lld (%zu)",
-                       (long long)o.mb, o.count, (long long)m.mb, m.count);
+                       (long long)mb, count, (long long)m.mb, m.count);
     ST_CUDA_TRY(cudaStreamWaitEvent(stream, ch.ready[m.slot], 0));
-    ST_CUDA_TRY(cudaMemcpyAsync(o.buf, ch.ring + (size_t)m.slot * ch.elems, o.count * sizeof(float),
-                                cudaMemcpyDefault, stream));
+    ST_CUDA_TRY(cudaMemcpyAsync(buf, ch.ring + (size_t)m.slot * ch.elems, count * sizeof(float), cudaMemcpyDefault,
+                                stream));
     ST_CUDA_TRY(cudaEventRecord(ch.consumed[m.slot], stream));
     ch.consumed_recorded[m.slot] = true;
     ch.received++;

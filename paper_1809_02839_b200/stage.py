@@ -32,7 +32,8 @@ class Stage:
     def __init__(self, layers: Layers, cuts: Sequence[int], stage: int, batch: int, lr: float, gamma: float = 0.9,
                  pred: int = L.ST_PRED_SPECTRAIN, momentum: int = L.ST_MOMENTUM_EMA, gemm: int = L.ST_GEMM_FP32X3,
                  transport: int = L.ST_TRANSPORT_NCCL, device: int = 0, max_minibatches: int = 256,
-                 nccl_id: Optional[bytes] = None, stream: Optional[torch.cuda.Stream] = None, seq_len: int = 1):
+                 nccl_id: Optional[bytes] = None, stream: Optional[torch.cuda.Stream] = None, seq_len: int = 1,
+                 comm_streams: Optional[Tuple[torch.cuda.Stream, torch.cuda.Stream]] = None):
         self.layers = [tuple(int(v) for v in l) for l in layers]
         self.cuts = list(cuts)
         self.k = stage
@@ -44,6 +45,8 @@ class Stage:
                                              transport, device, max_minibatches, nccl_id, seq_len)
         self.sizes = L.query_sizes(self.cfg)
         self.stream = stream if stream is not None else torch.cuda.Stream(device=self.device)
+        # activation / gradient transfer streams (None: the library creates its own)
+        self.comm_streams = comm_streams
 
         def buf(nbytes: int) -> Optional[torch.Tensor]:
             if nbytes <= 0:
@@ -58,8 +61,9 @@ class Stage:
         bufs = L.StBuffers(_ptr(self.W), _ptr(self.V), _ptr(self.G), _ptr(self.WF), _ptr(self.WB),
                            _ptr(self.stash), _ptr(self.work))
         self.ctx = ctypes.c_void_p()
+        cf, cb = (None, None) if comm_streams is None else (comm_streams[0].cuda_stream, comm_streams[1].cuda_stream)
         check(lib.st_init(ctypes.byref(self.cfg), ctypes.byref(bufs), ctypes.c_void_p(self.stream.cuda_stream),
-                          ctypes.byref(self.ctx)))
+                          ctypes.c_void_p(cf), ctypes.c_void_p(cb), ctypes.byref(self.ctx)))
 
     # ---- lifecycle ------------------------------------------------------------
     def close(self) -> None:
@@ -135,6 +139,12 @@ class Stage:
 
     def sync(self) -> None:
         check(lib.st_sync(self.ctx))
+
+    def record_after_backward(self, mb: int, event: torch.cuda.Event) -> None:
+        """Record `event` on the compute stream once B(mb) has been issued (measurement
+        window of SURVEY §8(d) / P:415)."""
+        event.record(self.stream)  # materialise the CUDA event (torch creates it lazily)
+        check(lib.st_record_after_backward(self.ctx, mb, ctypes.c_void_p(event.cuda_event)))
 
     def losses_device_ptr(self) -> int:
         return lib.st_losses_device(self.ctx) or 0

@@ -1,18 +1,29 @@
-"""Parity at BASELINE.json's full size (-m gpu), in the launch configuration bench.py
-times: the wide FCN 784 → 8 × 8192 → 10 (configs[1], 476M parameters), batch 128, through
-`Stage.run` (st_run: fused dW + K-B update overlapped with the next layer's dX on SM
-budgets, CTA-pair forward / dX GEMMs, 3xTF32) and, for two co-located stages,
-`run_group` (LOCAL transport, SpecTrain predictions active on stage 0: s_F = 1).
+"""Parity at BASELINE.json's full sizes (-m gpu), in the launch configuration bench.py
+times (`Stage.run` = st_run: fused dW + K-B update overlapped with the next layer's dX
+on SM budgets, CTA-pair forward / dX GEMMs, 3xTF32), north_star's 20 mini-batches:
 
-The oracle runs the same mini-batches in fp64 on the host. Gates: the trace bit-exact;
-W and the loss within 1e-4 rel-L2 (the north-star gate). V — the smoothed gradient,
-stored directly in fp32 and not masked by the weights' magnitude like W — is checked
-loosely (reading D24): through 8 ReLU layers of width 8192, a pre-activation within the
-fp32 accumulation error of 0 (K = 8192 terms: ~1e-5 of the operand scale on the tensor
-cores, ~1e-6 with fp32 FMAs) takes the other ReLU decision than in fp64, and each such
-flip moves a whole gradient row; measured V rel-L2 ~7e-3 (3xTF32) and ~2e-3 (CUDA-core
-fp32) against the fp64 oracle, while the output layer (no ReLU decision after its input)
-stays at ~1e-4. Gates: output layer ≤ 1e-3, all layers ≤ 3e-2."""
+- the wide FCN 784 → 8 × 8192 → 10 (configs[1], 476M parameters), batch 128, at 1 stage
+  (3xTF32 and CUDA-core fp32) and at 2 co-located stages (LOCAL transport, SpecTrain
+  prediction on stage 0: s_F = 1);
+- a 16384-wide FCN 784 → 3 × 16384 → 10 (550M parameters: the large FCN's layer shape,
+  configs[4]) at 1 stage — its second 16384² layer takes the one-CTA-per-m-tile dW budget
+  (128 CTAs) the large FCN runs with — and at 2 co-located stages.
+
+The oracle runs the same mini-batches in fp64 on the host. Gates (north_star: trace
+bit-exact, W and loss ≤ 1e-4 rel-L2), plus gates that see the gradient:
+- ΔW = W_M − W_0 against the oracle's ΔW: a skipped update gives 1.0;
+- V (the smoothed gradient, stored directly): whole-vector rel-L2 and, per layer, the
+  MEDIAN over weight rows of the row rel-error. Reading D24: a pre-activation within
+  fp32 rounding of 0 takes the other ReLU branch than in fp64 and moves a whole gradient
+  row, so the rel-L2 of V / ΔW at full width is set by a few flipped rows — the same
+  spread a plain NumPy float32 run of the oracle's own arithmetic shows against fp64
+  (tools/d24_fp32_vs_fp64.py → profiles/r2_d24_fp32_vs_fp64.json, no GPU involved). The
+  gates are 2× that CPU figure. A systematic error moves every row: the row-median gate
+  (1e-3) catches a 1% gradient error that a rel-L2 gate at the D24 level would not.
+Measured figures are appended to gpurun_out/fullsize_metrics.jsonl."""
+import json
+import os
+
 import numpy as np
 import pytest
 import torch
@@ -23,7 +34,14 @@ from tests.gpu_helpers import layers_of, rel_l2
 
 pytestmark = pytest.mark.gpu
 
-LR = 0.01  # material but stable for this width (the bench uses 1e-3)
+LR = 0.01  # material but stable for these widths (the bench uses 1e-3)
+M_FULL = 20  # north_star: "after 20 steps"
+# 2x the NumPy-float32-vs-float64 spread of the oracle's own arithmetic at full width (D24)
+GATE_V = 3e-2
+GATE_DW = 3e-2
+GATE_ROW_MEDIAN = 1e-3
+
+_ORACLE = {}
 
 
 @pytest.fixture(scope="module")
@@ -34,31 +52,65 @@ def st():
     return st
 
 
-def _check(model, w0, X, Y, Ws, Vs, losses, traces, v_hidden_tol):
-    ref = O.run(model, sd.widen(w0), X.astype(np.float64), Y, float(np.float32(LR)), float(np.float32(0.9)))
+def _oracle(key, model, w0, X, Y):
+    if key not in _ORACLE:
+        _ORACLE[key] = O.run(model, sd.widen(w0), X.astype(np.float64), Y, float(np.float32(LR)),
+                             float(np.float32(0.9)))
+    return _ORACLE[key]
+
+
+def _row_median(a, b, n_in, n_out):
+    a = np.asarray(a, np.float64).reshape(n_in, n_out)
+    b = np.asarray(b, np.float64).reshape(n_in, n_out)
+    nb = np.linalg.norm(b, axis=1)
+    ok = nb > 0
+    return float(np.median(np.linalg.norm(a - b, axis=1)[ok] / nb[ok]))
+
+
+def _record(name, d):
+    try:
+        root = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+        os.makedirs(os.path.join(root, "gpurun_out"), exist_ok=True)
+        with open(os.path.join(root, "gpurun_out", "fullsize_metrics.jsonl"), "a") as f:
+            f.write(json.dumps({"test": name, **d}) + "\n")
+    except OSError:
+        pass
+
+
+def _check(name, model, w0, ref, Ws, Vs, losses, traces, v_tol=GATE_V, dw_tol=GATE_DW):
     for k in range(model.num_stages):
         assert traces[k] == [e.as_tuple() for e in ref.trace[k]], f"trace mismatch at stage {k}"
-    assert rel_l2(losses, ref.losses) <= 1e-4
     W, Wr = np.concatenate(Ws), np.concatenate(ref.W)
     V, Vr = np.concatenate(Vs), np.concatenate(ref.V)
-    assert rel_l2(W, Wr) <= 1e-4
-    # the weights moved (a few mini-batches at init move 476M weights by only ~4e-6 of their
-    # norm, which is why V, not W, carries the gradient check here)
-    assert rel_l2(Wr, np.concatenate(sd.widen(w0))) > 1e-6
+    W0 = np.concatenate(sd.widen(w0))
+    m = {"loss": rel_l2(losses, ref.losses), "w": rel_l2(W, Wr), "dw": rel_l2(W - W0, Wr - W0),
+         "v": rel_l2(V, Vr)}
+    # per dense layer: V row medians (the flat arena is the layers' blocks in order)
+    rows, off = [], 0
+    for L in model.layers:
+        if L.kind == sd.DENSE:
+            n = L.n_in * L.n_out
+            rows.append(_row_median(V[off:off + n], Vr[off:off + n], L.n_in, L.n_out))
+        off += L.n_params
+    m["v_row_median"] = rows
     n_out = model.layers[-1].n_params  # the output layer's block ends the last stage's arena
-    rv_out = rel_l2(Vs[-1][-n_out:], ref.V[-1][-n_out:])
-    rv = rel_l2(V, Vr)
-    assert rv_out <= 1e-3, rv_out
-    assert rv <= v_hidden_tol, rv
+    m["v_out"] = rel_l2(Vs[-1][-n_out:], ref.V[-1][-n_out:])
+    _record(name, m)
+    assert m["loss"] <= 1e-4, m
+    assert m["w"] <= 1e-4, m
+    assert m["dw"] <= dw_tol, m
+    assert m["v"] <= v_tol, m
+    assert max(rows) <= GATE_ROW_MEDIAN, m
+    assert m["v_out"] <= 1e-3, m
+    return m
 
 
-def _single_stage(st, gemm, seed):
-    model = sd.config_wide_fcn(1)
-    M, B = 2, 128
+def _run_single(st, model, M, seed, gemm=None):
+    B = 128
     w0, X, Y = sd.parity_inputs(model, M, B, seed=seed)
     dev = torch.device("cuda", 0)
     s = st.Stage(layers_of(model), model.cuts, 0, B, LR, 0.9, transport=st.ST_TRANSPORT_NCCL, device=0,
-                 max_minibatches=M, gemm=gemm)
+                 max_minibatches=M, gemm=st.ST_GEMM_FP32X3 if gemm is None else gemm)
     try:
         s.set_params(w0[0])
         losses = s.run(M, torch.from_numpy(X).to(dev), torch.from_numpy(Y).to(dev), want_losses=True)
@@ -66,27 +118,18 @@ def _single_stage(st, gemm, seed):
         tr = s.trace()
     finally:
         s.close()
-    return model, w0, X, Y, [W], [V], losses, [tr]
+    return w0, X, Y, [W], [V], losses, [tr]
 
 
-def test_wide_fcn_full_size_single_stage_bench_path(st):
-    _check(*_single_stage(st, st.ST_GEMM_FP32X3, seed=0), v_hidden_tol=3e-2)
-
-
-def test_wide_fcn_full_size_single_stage_fp32_simt(st):
-    _check(*_single_stage(st, st.ST_GEMM_SIMT, seed=0), v_hidden_tol=3e-2)
-
-
-def test_wide_fcn_full_size_two_stages_with_prediction(st):
-    model = sd.config_wide_fcn(2)
-    M, B = 3, 128
-    w0, X, Y = sd.parity_inputs(model, M, B, seed=1)
+def _run_local(st, model, M, seed):
+    B = 128
+    w0, X, Y = sd.parity_inputs(model, M, B, seed=seed)
     dev = torch.device("cuda", 0)
     stages = [st.Stage(layers_of(model), model.cuts, k, B, LR, 0.9, transport=st.ST_TRANSPORT_LOCAL, device=0,
-                       max_minibatches=M) for k in range(2)]
+                       max_minibatches=M) for k in range(model.num_stages)]
     try:
         st.connect_local(stages)
-        assert stages[0].sizes.s_fwd == 1
+        assert stages[0].sizes.s_fwd == model.num_stages - 1
         for s, w in zip(stages, w0):
             s.set_params(w)
         losses = st.run_group(stages, M, torch.from_numpy(X).to(dev), torch.from_numpy(Y).to(dev),
@@ -96,7 +139,48 @@ def test_wide_fcn_full_size_two_stages_with_prediction(st):
     finally:
         for s in stages:
             s.close()
-    _check(model, w0, X, Y, [o[0] for o in out], [o[1] for o in out], losses, trs, v_hidden_tol=3e-2)
+    return w0, X, Y, [o[0] for o in out], [o[1] for o in out], losses, trs
+
+
+def test_wide_fcn_full_size_single_stage_bench_path(st):
+    model = sd.config_wide_fcn(1)
+    w0, X, Y, Ws, Vs, losses, trs = _run_single(st, model, M_FULL, seed=0)
+    ref = _oracle(("wide", 1), model, w0, X, Y)
+    _check("wide_fcn_1stage_fp32x3", model, w0, ref, Ws, Vs, losses, trs)
+
+
+def test_wide_fcn_full_size_single_stage_fp32_simt(st):
+    model = sd.config_wide_fcn(1)
+    w0, X, Y, Ws, Vs, losses, trs = _run_single(st, model, M_FULL, seed=0, gemm=st.ST_GEMM_SIMT)
+    ref = _oracle(("wide", 1), model, w0, X, Y)
+    _check("wide_fcn_1stage_simt", model, w0, ref, Ws, Vs, losses, trs)
+
+
+def test_wide_fcn_full_size_two_stages_with_prediction(st):
+    model = sd.config_wide_fcn(2)
+    w0, X, Y, Ws, Vs, losses, trs = _run_local(st, model, M_FULL, seed=1)
+    ref = _oracle(("wide", 2), model, w0, X, Y)
+    _check("wide_fcn_2stages", model, w0, ref, Ws, Vs, losses, trs)
+
+
+def _fcn16k(stages):
+    return sd.mlp([784, 16384, 16384, 16384, 10], cuts=sd.even_cuts(4, stages))
+
+
+def test_fcn_16384_wide_single_stage_bench_path(st):
+    """The large FCN's 16384² layer shape (configs[4]): 16384-wide TMA maps, the fused
+    dW + update at one CTA per m-tile (128 CTAs) overlapped with the next layer's dX."""
+    model = _fcn16k(1)
+    w0, X, Y, Ws, Vs, losses, trs = _run_single(st, model, M_FULL, seed=2)
+    ref = _oracle(("16k", 1), model, w0, X, Y)
+    _check("fcn16k_1stage", model, w0, ref, Ws, Vs, losses, trs)
+
+
+def test_fcn_16384_wide_two_stages_with_prediction(st):
+    model = _fcn16k(2)
+    w0, X, Y, Ws, Vs, losses, trs = _run_local(st, model, M_FULL, seed=3)
+    ref = _oracle(("16k", 2), model, w0, X, Y)
+    _check("fcn16k_2stages", model, w0, ref, Ws, Vs, losses, trs)
 
 
 def test_vgg16_full_size_single_stage_bench_path(st):
@@ -117,7 +201,8 @@ def test_vgg16_full_size_single_stage_bench_path(st):
         tr = s.trace()
     finally:
         s.close()
-    _check(model, w0, X, Y, [W], [V], losses, [tr], v_hidden_tol=3e-2)
+    ref = _oracle(("vgg16", 1), model, w0, X, Y)
+    _check("vgg16_1stage", model, w0, ref, [W], [V], losses, [tr], dw_tol=5e-2)
 
 
 def test_lstm_lm_full_size_single_stage_bench_path(st):
@@ -143,5 +228,9 @@ def test_lstm_lm_full_size_single_stage_bench_path(st):
     assert tr == [e.as_tuple() for e in ref.trace[0]]
     assert rel_l2(losses, ref.losses) <= 1e-4
     assert rel_l2(W, ref.W[0]) <= 1e-4
+    W0 = sd.widen(w0)[0]
+    rdw = rel_l2(W - W0, ref.W[0] - W0)
     rv = rel_l2(V, ref.V[0])
+    _record("lstm_lm_1stage", {"dw": rdw, "v": rv})
     assert rv <= 1e-4, rv
+    assert rdw <= 1e-2, rdw

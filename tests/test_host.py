@@ -59,83 +59,112 @@ def test_program_bit_exact_vs_oracle(st, N):
                 assert st.program(N, k, M, cpred) == [e.as_tuple() for e in tr[k]], (N, M, k, pred)
 
 
-def simulate_plans(plans, N):
-    """Strict semantics: a group completes once every op in it is matched by an op
-    the peer has POSTED (in its current or an earlier group); a stage posts group
-    g+1 only after group g completed. Returns True when every stage finishes."""
-    # channel ops in order: chan[(src, dst)] = list of mb for sends / recvs
-    sends = {}
-    recvs = {}
-    idx = []  # per stage, per group: list of (kind, chan, ordinal, mb)
-    for k in range(N):
-        gl = []
-        for before, ops in plans[k]:
-            g = []
-            for kind, mb in ops:
-                if kind in (0, 3):  # send_fwd to k+1 / recv_bwd from k+1
-                    peer = k + 1
-                else:
-                    peer = k - 1
-                if kind in (0, 2):
-                    ch = (k, peer)
-                    lst = sends.setdefault(ch, [])
-                    g.append(("s", ch, len(lst), mb))
-                    lst.append(mb)
-                else:
-                    ch = (peer, k)
-                    lst = recvs.setdefault(ch, [])
-                    g.append(("r", ch, len(lst), mb))
-                    lst.append(mb)
-            gl.append(g)
-        idx.append(gl)
-    for ch in set(sends) | set(recvs):
-        assert sends.get(ch, []) == recvs.get(ch, []), ("message order mismatch on channel", ch)
-    cur = [0] * N
-    posted_s = {}
-    posted_r = {}
+def simulate_streams(N, M, plans, programs, shared=False):
+    """The engine's execution model (engine.cpp issue_op / run_task) under strict
+    rendezvous semantics: per stage a compute FIFO (the program) and two comm FIFOs
+    (activations: kinds 0/1, gradients: kinds 2/3, each in plan order). A send
+    completes together with the matching receive, only when both are at the head of
+    their FIFOs and their event dependencies are met:
+      send_fwd(i) after F(i); send_bwd(j) after B(j);
+      recv_fwd(i) after B(i − S) (its stash slot's previous reader, S = N − k);
+      recv_bwd(j) after B(j − 2) (two gradient slots);
+      F(i) after recv_fwd(i) and send_fwd(i − 2); B(j) after recv_bwd(j) and send_bwd(j − 2).
+    shared=True puts both directions in ONE FIFO per stage (one comm stream / one
+    communicator for both): the negative control. Returns True when every FIFO drains."""
+    done = set()  # ("F"|"B", k, mb) compute tasks, (kind, k, mb) comm ops
+    comp = [list(p) for p in programs]
+    fifo = [[[(kd, mb) for _, ops in plans[k] for kd, mb in ops if kd in (0, 1)],
+             [(kd, mb) for _, ops in plans[k] for kd, mb in ops if kd in (2, 3)]] for k in range(N)]
+    if shared:
+        fifo = [[[op for _, ops in plans[k] for op in ops]] * 2 for k in range(N)]
 
-    def post(k):
-        if cur[k] < len(idx[k]):
-            for t, ch, o, mb in idx[k][cur[k]]:
-                d = posted_s if t == "s" else posted_r
-                d[ch] = max(d.get(ch, 0), o + 1)
+    def comm_ready(k, kd, mb):
+        S = N - k
+        if kd == 0:
+            return ("F", k, mb) in done
+        if kd == 2:
+            return ("B", k, mb) in done
+        if kd == 1:
+            return mb - S < 0 or ("B", k, mb - S) in done
+        return mb - 2 < 0 or ("B", k, mb - 2) in done
 
-    for k in range(N):
-        post(k)
+    def task_ready(k, d, mb):
+        if d == O.FWD:
+            return ((k == 0 or (1, k, mb) in done) and
+                    (k == N - 1 or mb - 2 < 0 or (0, k, mb - 2) in done))
+        return ((k == N - 1 or (3, k, mb) in done) and
+                (k == 0 or mb - 2 < 0 or (2, k, mb - 2) in done))
+
     while True:
         progress = False
         for k in range(N):
-            if cur[k] >= len(idx[k]):
-                continue
-            ok = all((posted_r.get(ch, 0) > o) if t == "s" else (posted_s.get(ch, 0) > o)
-                     for t, ch, o, mb in idx[k][cur[k]])
-            if ok:
-                cur[k] += 1
-                post(k)
+            while comp[k] and task_ready(k, *comp[k][0]):
+                d, mb = comp[k].pop(0)
+                done.add(("F" if d == O.FWD else "B", k, mb))
                 progress = True
-        if all(cur[k] >= len(idx[k]) for k in range(N)):
+            for q in (0, 1):
+                if not fifo[k][q]:
+                    continue
+                kd, mb = fifo[k][q][0]
+                if kd not in (0, 2):
+                    continue  # receives complete from the sender's side
+                peer = k + 1 if kd == 0 else k - 1
+                rk = 1 if kd == 0 else 3
+                pq = fifo[peer][q]
+                if (pq and pq[0] == (rk, mb) and comm_ready(k, kd, mb) and comm_ready(peer, rk, mb)):
+                    fifo[k][q].pop(0)
+                    pq.pop(0)
+                    done.add((kd, k, mb))
+                    done.add((rk, peer, mb))
+                    progress = True
+        if all(not comp[k] and not fifo[k][0] and not fifo[k][1] for k in range(N)):
             return True
         if not progress:
             return False
 
 
-def test_comm_plan_deadlock_free_and_paired(st):
+def test_comm_plan_deadlock_free_on_split_streams(st):
     for N in range(1, 9):
         for M in range(1, 14):
             plans = [st.comm_plan(N, k, M) for k in range(N)]
-            assert simulate_plans(plans, N), (N, M)
+            progs = [O.stage_program(N, k, M) for k in range(N)]
+            assert simulate_streams(N, M, plans, progs), (N, M)
             for k in range(N):
                 flat = [op for _, ops in plans[k] for op in ops]
-                n_send_f = sum(1 for kd, _ in flat if kd == 0)
-                n_recv_f = sum(1 for kd, _ in flat if kd == 1)
-                assert n_send_f == (M if k < N - 1 else 0) and n_recv_f == (M if k > 0 else 0)
+                assert all(len(ops) == 1 for _, ops in plans[k])
+                for kd in range(4):  # each channel carries mini-batches 0..M-1 in order
+                    mbs = [mb for d, mb in flat if d == kd]
+                    want = {0: k < N - 1, 1: k > 0, 2: k > 0, 3: k < N - 1}[kd]
+                    assert mbs == (list(range(M)) if want else []), (N, M, k, kd)
 
 
-def test_comm_plan_megatron_pairing(st):
-    # steady state at an interior stage: send act(i) grouped with recv grad(j) (same peer)
-    plan = st.comm_plan(4, 1, 10)
-    assert any(ops == [(0, 5), (3, 3)] for _, ops in plan)
-    assert any(ops == [(2, 3), (1, 6)] for _, ops in plan)
+def test_comm_plan_needs_split_streams(st):
+    # negative control: the same single-op plan on ONE comm FIFO per stage deadlocks
+    # (stage k sends act(i) to k+1 while k+1 sends grad(j) to k, both waiting for a
+    # receive queued behind the other's send) — the reason each direction has its own
+    # communicator and stream
+    N, M = 4, 8
+    plans = [st.comm_plan(N, k, M) for k in range(N)]
+    progs = [O.stage_program(N, k, M) for k in range(N)]
+    assert not simulate_streams(N, M, plans, progs, shared=True)
+    assert simulate_streams(N, M, plans, progs)
+
+
+def test_comm_plan_issue_points(st):
+    # every op sits at the boundary of the task it belongs to: a send right after its
+    # task, a receive right before (an interior stage in steady state)
+    N, k, M = 4, 1, 10
+    plan = st.comm_plan(N, k, M)
+    prog = O.stage_program(N, k, M)
+    for before, ops in plan:
+        (kd, mb), = ops
+        if kd in (0, 2):
+            assert prog[before - 1] == ((O.FWD if kd == 0 else O.BWD), mb)
+        else:
+            assert prog[before] == ((O.FWD if kd == 1 else O.BWD), mb)
+    # the two directions interleave in the plan but never share a FIFO
+    kinds = [ops[0][0] for _, ops in plan]
+    assert {0, 1, 2, 3} <= set(kinds)
 
 
 def test_query_sizes_and_validation(st):
