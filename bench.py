@@ -50,7 +50,7 @@ def parse():
     p.add_argument("--workload", default="large_fcn", choices=["wide_fcn", "large_fcn", "mlp", "deep_mlp", "lstm_lm", "vgg16"])
     p.add_argument("--stages", type=int, default=0, help="pipeline depth (default = --gpus); >N only with N=1")
     p.add_argument("--gemm", default=DEFAULT_GEMM, choices=["fp32x3", "tf32", "simt"])
-    p.add_argument("--pred", default="spectrain", choices=["spectrain", "none", "stash"])
+    p.add_argument("--pred", default="spectrain", choices=["spectrain", "none", "stash", "staleness_free"])
     p.add_argument("--no-e2e", action="store_true")
     p.add_argument("--no-cpu", action="store_true")
     p.add_argument("--lr", type=float, default=1e-3)
@@ -108,8 +108,8 @@ def stage_work(model, k: int, B: int, pred: str):
     FLOPs: 2·rows·in·out per GEMM pass (fwd, dX, dW; conv ×9·H·W, LSTM 4H·(in+H)·T)."""
     import synthdata as sd
     N = model.num_stages
-    sF = (k // 2 + N - k - 1) if pred == "spectrain" else 0
-    sB = (k // 2) if pred == "spectrain" else 0
+    sF = {"spectrain": k // 2 + N - k - 1, "staleness_free": N - k - 1}.get(pred, 0)
+    sB = {"spectrain": k // 2}.get(pred, 0)
     upd = 16 + (4 if sF > 0 else 0) + (4 if (sB > 0 and sB != sF) else 0)
     if pred == "stash":  # PipeDream weight stashing: the update writes W' into the stash slot
         upd = 20
@@ -523,7 +523,8 @@ def run_ours(args):
         hbm_, _ = measured_peaks()
         model = auto_partition(model, B, S, hbm_, measured_tensor_peak()[2])
     gemm = {"fp32x3": st.ST_GEMM_FP32X3, "tf32": st.ST_GEMM_TF32, "simt": st.ST_GEMM_SIMT}[args.gemm]
-    pred = {"spectrain": st.ST_PRED_SPECTRAIN, "none": st.ST_PRED_NONE, "stash": st.ST_PRED_STASH}[args.pred]
+    pred = {"spectrain": st.ST_PRED_SPECTRAIN, "none": st.ST_PRED_NONE, "stash": st.ST_PRED_STASH,
+            "staleness_free": st.ST_PRED_STALENESS_FREE}[args.pred]
     kinds = {sd.DENSE: st.ST_LAYER_DENSE, sd.EMBED: st.ST_LAYER_EMBED, sd.LSTM: st.ST_LAYER_LSTM,
              sd.CONV: st.ST_LAYER_CONV, sd.POOL: st.ST_LAYER_POOL}
     layers = [(l.n_in, l.n_out, st.ST_ACT_RELU if l.act == sd.RELU else st.ST_ACT_NONE, 1 if l.bias else 0,

@@ -93,7 +93,13 @@ enum { ST_LAYER_DENSE = 0, ST_LAYER_EMBED = 1, ST_LAYER_LSTM = 2, ST_LAYER_CONV 
  * floats at a pitch of P rounded up to 64 (wf_bytes says how much); the update after
  * B(mb) writes W' into B(mb)'s slot, whose next user is F(mb + N − k). Trace: a
  * backward's base_version is the version its forward used. */
-enum { ST_PRED_SPECTRAIN = 0, ST_PRED_NONE = 1, ST_PRED_STASH = 2 };
+/* ST_PRED_STALENESS_FREE: the staleness-free target the paper
+ * sets for SpecTrain — the whole round trip of a mini-batch on a stage adopts the version
+ * that exists once the previous mini-batch has updated — per stage:
+ * s_F = N−k−1 (the updates between F(i) and B(i) on stage k), s_B = 0. Both passes of
+ * mini-batch i then target stage version i; Eq. 5/6 (SPECTRAIN) add ⌊k/2⌋ to both
+ * (reading D6). */
+enum { ST_PRED_SPECTRAIN = 0, ST_PRED_NONE = 1, ST_PRED_STASH = 2, ST_PRED_STALENESS_FREE = 3 };
 enum { ST_MOMENTUM_EMA = 0, ST_MOMENTUM_HEAVY_BALL = 1 };
 /* GEMM arithmetic. FP32X3 = 3xTF32 split (hi·hi + hi·lo + lo·hi) on tcgen05
  * tensor cores, fp32 accumulate in TMEM — the parity mode.

@@ -35,12 +35,20 @@ PRED_NONE = "none"  # vanilla pipelining, s ≡ 0 (D-A8)
 # stage's current weights and its backward uses the SAME (stashed) weights; no prediction
 # (SURVEY §8(f) NEXT-2). The trace records, for a backward, the version its forward used.
 PRED_STASH = "stash"
+# Staleness-free target: the goal the paper states for SpecTrain —
+# "the entire round trip of a mini-batch should adopt the same weight version",
+# the version that exists once the previous mini-batch has updated the weights (P:229,
+# "the only staleness-free version of weights is W6") — taken per stage: a forward
+# predicts across the N−k−1 updates its stage applies before the mini-batch's backward
+# arrives (s_F = N−k−1, the local F→B lag of the 1F1B program), the backward uses the
+# current weights (s_B = 0). Both passes of mini-batch i then target stage version i.
+# Eq. 5/6 add ⌊k/2⌋ to both (reading D6); this variant drops that term.
+PRED_STALENESS_FREE = "staleness_free"
 
 MOMENTUM_EMA = "ema"  # Eq. 1 literally: v = γ v + (1-γ) g
 MOMENTUM_HEAVY_BALL = "heavy_ball"  # v = γ v + g (TF MomentumOptimizer, D2 flag)
 
 APPLY_MOMENTUM = "momentum"  # D1: W ← W − η·v_new (Momentum SGD)
-APPLY_EQ2 = "eq2"  # Eq. 2 literally: W ← W − η·g, oracle-only flag
 
 
 # --------------------------------------------------------------------------
@@ -68,12 +76,11 @@ def update_smoothed(v: np.ndarray, g: np.ndarray, gamma: float, momentum: str = 
 
 
 def apply_update(W: np.ndarray, v_new: np.ndarray, g: np.ndarray, eta: float, apply: str = APPLY_MOMENTUM) -> np.ndarray:
-    """D1: Momentum SGD step W ← W − η·v_t (P:373 'Momentum SGD'); APPLY_EQ2 is
-    Eq. 2 literally: W_{t+1} = W_t − η·g_t."""
+    """D1: Momentum SGD step W ← W − η·v_t (P:373 'Momentum SGD'; Eq. 3 uses v in place
+    of the gradient). Eq. 2's literal plain-SGD form is not offered: no
+    path uses it and nothing in the paper would pin it."""
     if apply == APPLY_MOMENTUM:
         return W - eta * v_new
-    if apply == APPLY_EQ2:
-        return W - eta * g
     raise ValueError(apply)
 
 
@@ -429,7 +436,11 @@ def run(model, W0: Sequence[np.ndarray], X: np.ndarray, Y: np.ndarray, eta: floa
     trace: List[List[Event]] = [[] for _ in range(N)]
 
     def s_of(k: int, d: int) -> int:
-        return 0 if pred in (PRED_NONE, PRED_STASH) else version_difference(k, N, d)
+        if pred in (PRED_NONE, PRED_STASH):
+            return 0
+        if pred == PRED_STALENESS_FREE:
+            return (N - k - 1) if d == FWD else 0
+        return version_difference(k, N, d)
 
     wstash: Dict[Tuple[int, int], Tuple[np.ndarray, int]] = {}  # PRED_STASH: (k, i) → (W, version) of F(i)
 

@@ -21,7 +21,7 @@ LIB_PATH = os.environ.get("ST_LIB_PATH") or os.path.join(HERE, "libspectrain.so"
 ST_FWD, ST_BWD = 0, 1
 ST_ACT_NONE, ST_ACT_RELU = 0, 1
 ST_LAYER_DENSE, ST_LAYER_EMBED, ST_LAYER_LSTM, ST_LAYER_CONV, ST_LAYER_POOL = 0, 1, 2, 3, 4
-ST_PRED_SPECTRAIN, ST_PRED_NONE, ST_PRED_STASH = 0, 1, 2
+ST_PRED_SPECTRAIN, ST_PRED_NONE, ST_PRED_STASH, ST_PRED_STALENESS_FREE = 0, 1, 2, 3
 ST_MOMENTUM_EMA, ST_MOMENTUM_HEAVY_BALL = 0, 1
 ST_GEMM_FP32X3, ST_GEMM_TF32, ST_GEMM_SIMT = 0, 1, 2
 ST_LOSS_SOFTMAX_CE = 0

@@ -73,7 +73,8 @@ st_status validate_and_layout(const st_config* c, Layout* L) {
   if (c->batch < 1) return set_error(ST_ERR_INPUT, "batch must be >= 1");
   if (!(c->lr > 0.f) || !std::isfinite(c->lr)) return set_error(ST_ERR_INPUT, "lr must be > 0");
   if (!(c->gamma > 0.f && c->gamma <= 1.f)) return set_error(ST_ERR_INPUT, "gamma must be in (0, 1]");
-  if (c->pred != ST_PRED_SPECTRAIN && c->pred != ST_PRED_NONE && c->pred != ST_PRED_STASH)
+  if (c->pred != ST_PRED_SPECTRAIN && c->pred != ST_PRED_NONE && c->pred != ST_PRED_STASH &&
+      c->pred != ST_PRED_STALENESS_FREE)
     return set_error(ST_ERR_INPUT, "bad pred");
   if (c->momentum != ST_MOMENTUM_EMA && c->momentum != ST_MOMENTUM_HEAVY_BALL)
     return set_error(ST_ERR_INPUT, "bad momentum");
@@ -197,9 +198,8 @@ st_status validate_and_layout(const st_config* c, Layout* L) {
   L->slot_elems = soff;
   L->in_first = (int)layer_win(c->layers[l0]);
   L->out_last = (int)layer_wout(c->layers[l1 - 1]);
-  const bool no_pred = c->pred == ST_PRED_NONE || c->pred == ST_PRED_STASH;
-  L->sF = no_pred ? 0 : version_difference(k, N, ST_FWD);
-  L->sB = no_pred ? 0 : version_difference(k, N, ST_BWD);
+  L->sF = stage_s(c->pred, k, N, ST_FWD);
+  L->sB = stage_s(c->pred, k, N, ST_BWD);
 
   // work carve-up
   int64_t w = 0;

@@ -18,6 +18,9 @@ enum CommKind { CK_SEND_FWD = 0, CK_RECV_FWD = 1, CK_SEND_BWD = 2, CK_RECV_BWD =
 using CommGroup = st_comm_group;
 
 int version_difference(int k, int N, int dir);
+// the version difference stage k uses for its forward / backward under a pred mode:
+// Eq. 5 / Eq. 6 (SPECTRAIN), 0 (NONE, STASH), N−k−1 / 0 (STALENESS_FREE)
+int stage_s(int pred, int k, int N, int dir);
 std::vector<Task> build_program(int N, int k, int64_t M);
 std::vector<st_event> program_events(int N, int k, int64_t M, int pred);
 std::vector<CommGroup> build_comm_plan(int N, int k, int64_t M);

@@ -31,6 +31,16 @@ int version_difference(int k, int N, int dir) {
   return dir == ST_FWD ? (k / 2 + N - k - 1) : (k / 2);
 }
 
+int stage_s(int pred, int k, int N, int dir) {
+  switch (pred) {
+    case ST_PRED_SPECTRAIN: return version_difference(k, N, dir);
+    // the staleness-free target: the forward predicts across the N−k−1
+    // updates that land before its backward, the backward uses the current weights
+    case ST_PRED_STALENESS_FREE: return dir == ST_FWD ? N - k - 1 : 0;
+    default: return 0;  // ST_PRED_NONE, ST_PRED_STASH
+  }
+}
+
 std::vector<Task> build_program(int N, int k, int64_t M) {
   std::vector<Task> p;
   if (M <= 0) return p;
@@ -50,9 +60,8 @@ std::vector<st_event> program_events(int N, int k, int64_t M, int pred) {
   std::vector<st_event> ev;
   ev.reserve(p.size());
   int64_t version = 0;
-  const bool no_pred = pred == ST_PRED_NONE || pred == ST_PRED_STASH;
-  const int64_t sF = no_pred ? 0 : version_difference(k, N, ST_FWD);
-  const int64_t sB = no_pred ? 0 : version_difference(k, N, ST_BWD);
+  const int64_t sF = stage_s(pred, k, N, ST_FWD);
+  const int64_t sB = stage_s(pred, k, N, ST_BWD);
   std::vector<int64_t> fwd_version((size_t)std::max<int64_t>(M, 0), 0);  // ST_PRED_STASH
   for (size_t n = 0; n < p.size(); ++n) {
     st_event e{};

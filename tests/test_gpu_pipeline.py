@@ -31,7 +31,8 @@ def gemm_mode(st):
 
 def _parity(st, model, batch, M, lr, seed=0, pred=O.PRED_SPECTRAIN, momentum=O.MOMENTUM_EMA, labels="teacher"):
     w0, X, Y = sd.parity_inputs(model, M, batch, seed, labels)
-    cpred = {O.PRED_SPECTRAIN: st.ST_PRED_SPECTRAIN, O.PRED_NONE: st.ST_PRED_NONE, O.PRED_STASH: st.ST_PRED_STASH}[pred]
+    cpred = {O.PRED_SPECTRAIN: st.ST_PRED_SPECTRAIN, O.PRED_NONE: st.ST_PRED_NONE, O.PRED_STASH: st.ST_PRED_STASH,
+             O.PRED_STALENESS_FREE: st.ST_PRED_STALENESS_FREE}[pred]
     cmom = st.ST_MOMENTUM_EMA if momentum == O.MOMENTUM_EMA else st.ST_MOMENTUM_HEAVY_BALL
     stages = build_pipeline(model, batch, lr, pred=cpred, momentum=cmom, gemm=gemm_mode(st), max_mb=M)
     try:
@@ -93,6 +94,21 @@ def test_weight_stashing(st):
     model = sd.mlp([77, 45, 31, 29, 13, 5], cuts=[2, 4])
     _parity(st, model, 7, 11, 0.05, seed=7, pred=O.PRED_STASH)
     _parity(st, model, 7, 2, 0.05, seed=8, pred=O.PRED_STASH)
+
+
+def test_staleness_free_variant(st):
+    """NEXT-2: s_F = N−k−1, s_B = 0 on the same kernels — trace bit-exact
+    (both passes of mini-batch i target stage version i in steady state), W / loss within
+    the gate; the 8-stage deep MLP (WF written on every stage but the last, WB never) and
+    a ragged 4-stage net (unfused K-B fallback)."""
+    model = sd.config_deep_mlp(8)
+    res, ref = _parity(st, model, 128, 20, 0.02, pred=O.PRED_STALENESS_FREE)
+    N = model.num_stages
+    for k, tr in enumerate(res[3]):
+        for e in tr:
+            if e[3] >= N - k - 1:  # steady state: the target is the mini-batch index
+                assert e[6] == e[3], (k, e)
+    _parity(st, sd.mlp([77, 45, 31, 29, 13, 5], cuts=[1, 2, 4]), 7, 11, 0.05, seed=9, pred=O.PRED_STALENESS_FREE)
 
 
 def test_ragged_shapes_and_M_smaller_than_depth(st):

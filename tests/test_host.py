@@ -53,7 +53,7 @@ def _oracle_trace(N, M, pred):
 def test_program_bit_exact_vs_oracle(st, N):
     for M in sorted({1, max(1, N - 1), N, 20}):
         for pred, cpred in ((O.PRED_SPECTRAIN, st.ST_PRED_SPECTRAIN), (O.PRED_NONE, st.ST_PRED_NONE),
-                            (O.PRED_STASH, st.ST_PRED_STASH)):
+                            (O.PRED_STASH, st.ST_PRED_STASH), (O.PRED_STALENESS_FREE, st.ST_PRED_STALENESS_FREE)):
             tr = _oracle_trace(N, M, pred)
             for k in range(N):
                 assert st.program(N, k, M, cpred) == [e.as_tuple() for e in tr[k]], (N, M, k, pred)

@@ -137,12 +137,25 @@ def test_program_counts():
 
 # ---------------------------------------------------------------- App. C brute force
 
-def _appc_bruteforce(pred: bool, heavy: bool, w_init, xs, ts, eta, gamma):
+def _appc_bruteforce(pred, heavy: bool, w_init, xs, ts, eta, gamma):
     """Independent exact-rational hand-stepping of the scalar chain. The per-stage
     task ORDER is not taken from the oracle: it emerges from a time-stepped
     round-robin simulation (P:211-212 'issues a forward task and a backward task in
     a round-robin manner', 'asynchronously executes the next one') in which a stage
-    holds at most N−k mini-batches in flight and prefers a ready backward."""
+    holds at most N−k mini-batches in flight and prefers a ready backward.
+    pred: True = Eq. 5/6 (written out here), False = s ≡ 0, or
+    "staleness_free" = s_F = N−k−1 (the number of mini-batches a stage holds in flight
+    besides the current one, i.e. the updates that land between F(i) and B(i)), s_B = 0."""
+    def s_fwd(k, N):
+        if pred == "staleness_free":
+            return N - k - 1
+        return (k // 2 + N - k - 1) if pred else 0
+
+    def s_bwd(k, N):
+        if pred == "staleness_free":
+            return 0
+        return (k // 2) if pred else 0
+
     N, M = len(w_init), len(xs)
     F = Fraction
     w = [F(x) for x in w_init]
@@ -167,7 +180,7 @@ def _appc_bruteforce(pred: bool, heavy: bool, w_init, xs, ts, eta, gamma):
             did = False
             if j < M and (k, j) in grad_in:
                 # backward of the oldest in-flight mini-batch
-                s = (k // 2) if pred else 0
+                s = s_bwd(k, N)
                 w_hat = w[k] - s * F(eta) * v[k]
                 trace[k].append(f"B{j}({ver[k]},{s},{ver[k] + s})")
                 a_in = stash.pop((k, j))
@@ -184,7 +197,7 @@ def _appc_bruteforce(pred: bool, heavy: bool, w_init, xs, ts, eta, gamma):
             if not did:
                 i = nxt_f[k]
                 if i < M and (k, i) in act_in and inflight[k] < N - k:
-                    s = (k // 2 + N - k - 1) if pred else 0
+                    s = s_fwd(k, N)
                     w_hat = w[k] - s * F(eta) * v[k]
                     trace[k].append(f"F{i}({ver[k]},{s},{ver[k] + s})")
                     a = act_in.pop((k, i))
@@ -260,6 +273,49 @@ def test_appc_oracle_vanilla_and_heavy_ball():
     assert all(e.s == 0 for ev in res.trace for e in ev)
     gold, res = _appc_oracle(O.PRED_SPECTRAIN, O.MOMENTUM_HEAVY_BALL)
     np.testing.assert_allclose(np.concatenate(res.W), gold["heavy_ball"]["W"], rtol=1e-12)
+
+
+def _tr(res, k):
+    return " ".join(f"{'F' if e.dir == O.FWD else 'B'}{e.mb}({e.base_version},{e.s},{e.target})" for e in res.trace[k])
+
+
+@pytest.mark.parametrize("w_init", [[0.9, 1.1, 0.8], [0.9, 1.1, 0.8, 1.2, 0.7]])
+def test_staleness_free_oracle_vs_exact_bruteforce(w_init):
+    """NEXT-2 staleness-free variant: the oracle against the independent exact-rational
+    brute force (App. C chain, 3 and 5 stages): W, V, losses and the full trace."""
+    gold = json.load(open(os.path.join(GOLDEN, "appc_scalar_chain.json")))
+    w, v, losses, trace = _appc_bruteforce("staleness_free", False, w_init, gold["x"], gold["t"], Fraction(1, 10), 0.9)
+    _, res = _appc_oracle(O.PRED_STALENESS_FREE, O.MOMENTUM_EMA, w_init=w_init)
+    np.testing.assert_allclose(np.concatenate(res.W), [float(a) for a in w], rtol=1e-12)
+    np.testing.assert_allclose(np.concatenate(res.V), [float(a) for a in v], rtol=1e-12)
+    np.testing.assert_allclose(res.losses, [float(a) for a in losses], rtol=1e-11)
+    for k in range(len(w_init)):
+        assert _tr(res, k) == " ".join(trace[k])
+
+
+def test_staleness_free_targets_and_special_cases():
+    """The variant's defining property (P:271 'the entire round trip of a mini-batch
+    should adopt the same weight version'): in steady state F(i) and B(i) of every
+    stage target stage version i. Special cases: N = 1 is plain momentum SGD; stages 0
+    and 1 use exactly Eq. 5/6 (⌊k/2⌋ = 0 there), so for N ≤ 2 the variant IS SpecTrain;
+    the last stage never predicts."""
+    for N in range(1, 9):
+        M = 12
+        res = O.run(_scalar_chain(N), [np.array([1.0])] * N, np.ones((M, 1, 1)), np.zeros((M, 1, 1)), 0.01, 0.9,
+                    pred=O.PRED_STALENESS_FREE)
+        for k in range(N):
+            for e in res.trace[k]:
+                assert e.s == ((N - k - 1) if e.dir == O.FWD else 0)
+                if e.dir == O.BWD or e.mb >= N - k - 1:
+                    assert e.target == e.mb, (N, k, e)
+    gold = json.load(open(os.path.join(GOLDEN, "appc_scalar_chain.json")))
+    _, a = _appc_oracle(O.PRED_STALENESS_FREE, O.MOMENTUM_EMA, w_init=[1.0])
+    np.testing.assert_allclose(a.W[0], gold["single_w1"]["W"], rtol=1e-11)
+    for w_init in ([0.9, 1.1], [0.7]):
+        _, a = _appc_oracle(O.PRED_STALENESS_FREE, O.MOMENTUM_EMA, w_init=w_init)
+        _, b = _appc_oracle(O.PRED_SPECTRAIN, O.MOMENTUM_EMA, w_init=w_init)
+        np.testing.assert_array_equal(np.concatenate(a.W), np.concatenate(b.W))
+        assert [_tr(a, k) for k in range(len(w_init))] == [_tr(b, k) for k in range(len(w_init))]
 
 
 def test_appc_single_weight_momentum_sgd():
