@@ -73,5 +73,17 @@ def build(verbose: bool = False, force: bool = False, defines=(), lib: str = LIB
     return LIB
 
 
+DEV_DIR = os.path.join(HERE, "_var", "dev")
+DEV_LIB = os.path.join(DEV_DIR, "libspectrain.so")
+
+
+def build_dev(verbose: bool = False, force: bool = False) -> str:
+    """The development variant: the same sources with -DST_DEV_KNOBS (csrc/knobs.hpp), so
+    the A/B switches and opt-in kernel variants are read from the environment. Used by
+    tests/test_gpu_variants.py (ST_LIB_PATH); the product library reads no knobs."""
+    return build(verbose=verbose, force=force, defines=("ST_DEV_KNOBS",), lib=DEV_LIB,
+                 build_dir=os.path.join(DEV_DIR, "_build"))
+
+
 if __name__ == "__main__":
     print(build(verbose="-v" in sys.argv, force="-f" in sys.argv))

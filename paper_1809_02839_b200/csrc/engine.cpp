@@ -13,6 +13,7 @@
 #include <thread>
 
 #include "engine.hpp"
+#include "knobs.hpp"
 
 using st::set_error;
 
@@ -465,13 +466,13 @@ st_status ctx_init(const st_config* cfg, const st_buffers* bufs, void* stream, v
   ST_CUDA_TRY(cudaStreamCreateWithFlags(&c->side, cudaStreamNonBlocking));
   c->side_events.resize(c->layers.size() + 1);
   for (auto& e : c->side_events) ST_CUDA_TRY(cudaEventCreateWithFlags(&e, cudaEventDisableTiming));
-  if (const char* e = getenv("ST_DWU_SMS")) {
-    c->dwu_sms = std::min(std::max(1, atoi(e)), c->sm_count - 2);
+  if (const int v = dev_knob("ST_DWU_SMS", 0)) {  // one dW + update budget for every layer (sweeps)
+    c->dwu_sms = std::min(std::max(1, v), c->sm_count - 2);
     c->dwu_env = true;
   }
-  if (const char* e = getenv("ST_CONV_OVERLAP")) c->conv_overlap = atoi(e) != 0;
-  if (const char* e = getenv("ST_PDL")) c->pdl = atoi(e) != 0;
-  if (const char* e = getenv("ST_PDL_DENSE")) c->pdl_dense = atoi(e) != 0;
+  c->conv_overlap = dev_knob("ST_CONV_OVERLAP", 0) != 0;
+  c->pdl = dev_knob("ST_PDL", 1) != 0;
+  c->pdl_dense = dev_knob("ST_PDL_DENSE", 1) != 0;
   // several stage contexts sharing one GPU (LOCAL transport): their kernels interleave
   // across streams and waiting dependents would hold SMs the other stages need
   // (wide FCN at 2 co-located stages 45.8k → 41.8k samples/s with it)

@@ -3,6 +3,7 @@
 // ST_GEMM_SIMT. Same contract for every mode (kernels.hpp).
 #include <cstdlib>
 
+#include "knobs.hpp"
 #include "kernels.hpp"
 
 namespace st {
@@ -30,8 +31,7 @@ bool pdl_enabled() {
   if (tl_pdl >= 0) return tl_pdl != 0;
   static int f = -1;
   if (f < 0) {
-    const char* e = getenv("ST_PDL_DENSE");
-    f = (e && atoi(e) == 0) ? 0 : 1;
+    f = dev_knob("ST_PDL_DENSE", 1) != 0 ? 1 : 0;
   }
   return f != 0;
 }

@@ -23,6 +23,7 @@
 #include <cstdlib>
 #include <mutex>
 
+#include "knobs.hpp"
 #include "kernels.hpp"
 
 namespace st {
@@ -2370,8 +2371,7 @@ int bn_for(int N) { return std::max(16, (std::min(N, BNMAX) + 15) / 16 * 16); }
 int dev_flags() {
   static int f = -1;
   if (f < 0) {
-    const char* e = getenv("ST_GEMM_DEV_FLAGS");
-    f = e ? atoi(e) : 0;
+    f = dev_knob("ST_GEMM_DEV_FLAGS", 0);
   }
   return f;
 }
@@ -2385,8 +2385,7 @@ constexpr int kExtReduceSplits = 2;  // from this many K splits on, reduce in a 
 int ext_reduce_splits() {
   static int f = -1;
   if (f < 0) {
-    const char* e = getenv("ST_EXT_REDUCE");
-    f = e ? atoi(e) : kExtReduceSplits;
+    f = dev_knob("ST_EXT_REDUCE", kExtReduceSplits);
   }
   return f;
 }
@@ -2399,8 +2398,7 @@ int ext_reduce_splits() {
 int dw_lockstep_mode() {
   static int f = -1;
   if (f < 0) {
-    const char* e = getenv("ST_DW_LOCKSTEP");
-    f = e ? atoi(e) : 2;
+    f = dev_knob("ST_DW_LOCKSTEP", 2);
   }
   return f;
 }
@@ -2409,8 +2407,7 @@ int dw_lockstep_mode() {
 bool tsg_narrow_on() {
   static int f = -1;
   if (f < 0) {
-    const char* e = getenv("ST_TSG_NARROW");
-    f = (e && atoi(e) == 0) ? 0 : 1;
+    f = dev_knob("ST_TSG_NARROW", 1) != 0 ? 1 : 0;
   }
   return f != 0;
 }
@@ -2419,8 +2416,7 @@ bool tsg_narrow_on() {
 bool conv_ts_on() {
   static int f = -1;
   if (f < 0) {
-    const char* e = getenv("ST_CONV_TS");
-    f = (e && atoi(e) == 0) ? 0 : 1;
+    f = dev_knob("ST_CONV_TS", 1) != 0 ? 1 : 0;
   }
   return f != 0;
 }
@@ -2429,8 +2425,7 @@ bool conv_ts_on() {
 bool conv_persistent_off() {
   static int f = -1;
   if (f < 0) {
-    const char* e = getenv("ST_CONV_PERSISTENT");
-    f = (e && atoi(e) == 0) ? 1 : 0;
+    f = dev_knob("ST_CONV_PERSISTENT", 1) == 0 ? 1 : 0;
   }
   return f != 0;
 }
@@ -2557,8 +2552,7 @@ void plan_splits(TcParams& p, int M, int N, int K, int budget) {
 bool stream_k_off() {
   static int f = -1;
   if (f < 0) {
-    const char* e = getenv("ST_STREAM_K");
-    f = (e && atoi(e) == 1) ? 0 : 1;
+    f = dev_knob("ST_STREAM_K", 0) == 1 ? 0 : 1;
   }
   return f != 0;
 }
@@ -2569,8 +2563,7 @@ bool stream_k_off() {
 int ts_split_acc() {
   static int f = -1;
   if (f < 0) {
-    const char* e = getenv("ST_TS_SPLIT_ACC");
-    f = (e && atoi(e) == 0) ? 0 : 1;
+    f = dev_knob("ST_TS_SPLIT_ACC", 1) != 0 ? 1 : 0;
   }
   return f;
 }
@@ -2578,8 +2571,7 @@ int ts_split_acc() {
 bool use_pair() {
   static int f = -1;
   if (f < 0) {
-    const char* e = getenv("ST_GEMM_PAIR");
-    f = e ? atoi(e) : 1;
+    f = dev_knob("ST_GEMM_PAIR", 1);
   }
   return f != 0;
 }
@@ -2898,8 +2890,7 @@ bool make_w3_map(CUtensorMap* m, const float* base, int Cin, int Cout, int bn) {
 bool implicit_conv_off() {
   static int f = -1;
   if (f < 0) {
-    const char* e = getenv("ST_CONV_IM2COL");
-    f = (e && atoi(e) == 1) ? 1 : 0;
+    f = dev_knob("ST_CONV_IM2COL", 0) == 1 ? 1 : 0;
   }
   return f != 0;
 }
@@ -2921,8 +2912,7 @@ bool tc_conv_ok(int mode, int H, int W, int Cin, int Cout) {
 bool conv_pair_on() {
   static int f = -1;
   if (f < 0) {
-    const char* e = getenv("ST_CONV_PAIR");
-    f = (e && atoi(e) == 1) ? 1 : 0;
+    f = dev_knob("ST_CONV_PAIR", 0) == 1 ? 1 : 0;
   }
   return f != 0;
 }

@@ -1,7 +1,8 @@
-"""The GEMM kernels behind the environment switches (ST_GEMM_PAIR=0: single-CTA fwd / dX
-kernel; ST_STREAM_K=1 with it: stream-K work split) against the same fp64 references and
-the same pipeline parity gate as the default CTA-pair path. The switches are read once
-per process, so each variant runs the existing tests in a child pytest."""
+"""The kernel variants behind the development knobs (ST_GEMM_PAIR=0: single-CTA fwd / dX
+kernel; ST_STREAM_K=1 with it: stream-K work split; the opt-in conv paths) against the
+same fp64 references and the same pipeline parity gate as the default path. The product
+library reads no knobs (csrc/knobs.hpp): these run the existing tests in a child pytest
+against the development build (build.build_dev(), loaded through ST_LIB_PATH)."""
 import os
 import subprocess
 import sys
@@ -9,6 +10,15 @@ import sys
 import pytest
 
 ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+
+
+def _dev_env(env):
+    import importlib.util
+    spec = importlib.util.spec_from_file_location("_st_build", os.path.join(ROOT, "paper_1809_02839_b200", "build.py"))
+    b = importlib.util.module_from_spec(spec)
+    spec.loader.exec_module(b)
+    lib = b.build_dev()
+    return dict(os.environ, ST_LIB_PATH=lib, **env)
 
 CASES = [
     "tests/test_gpu_kernels.py::test_stage_gemms_vs_fp64",
@@ -22,7 +32,7 @@ CASES = [
 @pytest.mark.parametrize("env", [{"ST_GEMM_PAIR": "0"}, {"ST_GEMM_PAIR": "0", "ST_STREAM_K": "1"}],
                          ids=["single_cta", "stream_k"])
 def test_gemm_variants_pass_parity(env):
-    e = dict(os.environ, **env)
+    e = _dev_env(env)
     r = subprocess.run([sys.executable, "-m", "pytest", "-q", "-x", "-m", "gpu", "-p", "no:cacheprovider",
                         "-k", "not tf32", *CASES], cwd=ROOT, env=e, capture_output=True, text=True, timeout=900)
     assert r.returncode == 0, r.stdout[-3000:] + r.stderr[-2000:]
@@ -38,7 +48,7 @@ CONV_CASES = ["tests/test_gpu_conv.py"]
 def test_conv_variants_pass_parity(env):
     """Opt-in conv paths: the CTA-pair conv forward, side-stream overlap of the conv dW +
     update, the single-accumulator pair kernel, the 4-stage TMEM-A ring for N ≤ 64."""
-    e = dict(os.environ, **env)
+    e = _dev_env(env)
     r = subprocess.run([sys.executable, "-m", "pytest", "-q", "-x", "-m", "gpu", "-p", "no:cacheprovider",
                         *CONV_CASES], cwd=ROOT, env=e, capture_output=True, text=True, timeout=900)
     assert r.returncode == 0, r.stdout[-3000:] + r.stderr[-2000:]
