@@ -256,8 +256,8 @@ ST_API st_status st_connect_local(st_ctx** ctxs, int32_t n);
 
 ST_API void st_destroy(st_ctx* ctx);
 
-/* W ← host[0..n) (n must equal P_k), V ← 0, WF = WB = W, version ← 0, program
- * restarted. Synchronous. ST_ERR_SHAPE on n mismatch. */
+/* W ← host[0..n) (n must equal P_k; host or device memory of this GPU — UVA), V ← 0,
+ * WF = WB = W, version ← 0, program restarted. Synchronous. ST_ERR_SHAPE on n mismatch. */
 ST_API st_status st_set_params(st_ctx* ctx, const float* host, size_t n);
 
 /* Copies W and V (either may be NULL) to host and the version counter. Synchronous. */

@@ -549,7 +549,8 @@ st_status ctx_set_params(st_ctx* c, const float* host, size_t n) {
   if (!c || (!host && n)) return set_error(ST_ERR_INPUT, "NULL argument");
   if ((int64_t)n != c->P) return set_error(ST_ERR_SHAPE, "set_params: n = %zu but stage has %lld", n, (long long)c->P);
   ST_CUDA_TRY(cudaSetDevice(c->device));
-  if (n) ST_CUDA_TRY(cudaMemcpyAsync(c->W, host, n * 4, cudaMemcpyHostToDevice, c->stream));
+  // host or device memory (UVA): a model too large to stage on the host is uploaded layer by layer
+  if (n) ST_CUDA_TRY(cudaMemcpyAsync(c->W, host, n * 4, cudaMemcpyDefault, c->stream));
   ST_CUDA_TRY(cudaMemsetAsync(c->V, 0, n * 4, c->stream));
   if (c->WF_out) ST_CUDA_TRY(cudaMemcpyAsync(c->WF_out, c->W, n * 4, cudaMemcpyDeviceToDevice, c->stream));
   for (int slot = 0; c->wstash && slot < c->S; ++slot)  // every in-flight forward before the first update sees W0

@@ -168,7 +168,7 @@ __global__ void maxpool_bwd_kernel(const float* __restrict__ X, const float* __r
 
 int blocks_for(int64_t n) {
   const int64_t b = (n + 255) / 256;
-  return (int)std::min<int64_t>(b, 148 * 32);
+  return (int)std::min<int64_t>(b, (int64_t)device_sm_count() * 32);
 }
 
 }  // namespace

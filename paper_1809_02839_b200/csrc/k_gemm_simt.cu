@@ -216,7 +216,7 @@ __global__ void __launch_bounds__(256) colsum4_partial_kernel(const float* __res
 int launch_bias_grad(const float* dZ, int rows, int n_out, float* gb, void* work, int64_t work_bytes,
                      cudaStream_t s) {
   const int cb = (n_out + 31) / 32;
-  int nb = rows > 1024 ? std::min(1024, std::max(1, (2 * 148) / cb)) : 1;
+  int nb = rows > 1024 ? std::min(1024, std::max(1, (2 * device_sm_count()) / cb)) : 1;
   nb = std::min(nb, (rows + 255) / 256);
   if (nb > 1 && work && (int64_t)nb * n_out * 4 <= work_bytes - 64 * 1024) {
     const int rpb = (rows + nb - 1) / nb;
@@ -252,7 +252,7 @@ st_status run(int M, int N, int K, const float* A, int64_t a_sm, int64_t a_sk, c
               void* work, int64_t work_bytes) {
   const int tiles = ((N + TN - 1) / TN) * ((M + TM - 1) / TM);
   int splits = 1;
-  if (work && tiles < 74 && K >= 8 * TK) splits = std::min(148 / tiles, K / (4 * TK));
+  if (work && tiles < 74 && K >= 8 * TK) splits = std::min(device_sm_count() / tiles, K / (4 * TK));
   const int64_t need = (int64_t)splits * M * N * 4;
   while (splits > 1 && need > work_bytes - 64 * 1024) --splits;
   dim3 grid((N + TN - 1) / TN, (M + TM - 1) / TM, std::max(1, splits));

@@ -18,6 +18,10 @@
 //               FP32X3 issues hi·hi + lo·hi + hi·lo
 //   warps 2..5  epilogue: tcgen05.ld → fused bias/ReLU (fwd), ReLU mask (dX) → global;
 //               split-K partials are reduced in fixed split order by the last CTA.
+#include <atomic>
+#include <mutex>
+#include <set>
+#include <tuple>
 #include <cuda.h>
 
 #include <cstdlib>
@@ -1750,7 +1754,7 @@ st_status launch_maybe_pdl(bool pdl, void (*kern)(KArgs...), dim3 grid, dim3 blo
 template <int EPI>
 st_status launch_splitk_epilogue(const TcParams& p, int tiles, int mt_grid, cudaStream_t s, bool pdl = false) {
   const int64_t total = (int64_t)p.M * p.N;
-  const int blocks = (int)std::min<int64_t>((total + 255) / 256, 148 * 8);
+  const int blocks = (int)std::min<int64_t>((total + 255) / 256, (int64_t)device_sm_count() * 8);
   return launch_maybe_pdl(pdl, splitk_epilogue_kernel<EPI>, dim3(blocks), dim3(256), 0, s, p.ws, p.splits, tiles,
                           mt_grid, p.M, p.N, p.out, p.aux, p.relu, p.row);
 }
@@ -2341,15 +2345,39 @@ bool make_plain_map(CUtensorMap* m, const float* base, int inner, int outer, int
   return r == CUDA_SUCCESS;
 }
 
+// Upper bound on the CTAs of one persistent / split-K launch: workspace_bytes sizes the
+// partial-tile buffers for it, independent of the device it is queried on.
+constexpr int kWsSms = 160;
+
+// SM count of the current device (cached per device ordinal: contexts may live on
+// different GPUs of one process)
 int num_sms() {
-  static int sms = 0;
-  if (!sms) {
-    int dev = 0;
-    cudaGetDevice(&dev);
+  static std::atomic<int> cache[64];
+  int dev = 0;
+  cudaGetDevice(&dev);
+  if (dev < 0 || dev >= 64) dev = 0;
+  int sms = cache[dev].load(std::memory_order_relaxed);
+  if (sms <= 0) {
     cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
     if (sms <= 0) sms = 148;
+    sms = std::min(sms, kWsSms);  // the split-K workspaces are sized for at most kWsSms CTAs
+    cache[dev].store(sms, std::memory_order_relaxed);
   }
   return sms;
+}
+
+// cudaFuncAttributeMaxDynamicSharedMemorySize is a per-device setting: opt each kernel in
+// once per (device, kernel, size), thread-safe (stage threads launch concurrently).
+st_status ensure_max_smem(const void* fn, int bytes) {
+  static std::mutex mu;
+  static std::set<std::tuple<int, const void*, int>> done;
+  int dev = 0;
+  ST_CUDA_TRY(cudaGetDevice(&dev));
+  std::lock_guard<std::mutex> lk(mu);
+  if (done.count(std::make_tuple(dev, fn, bytes))) return ST_OK;
+  ST_CUDA_TRY(cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, bytes));
+  done.insert(std::make_tuple(dev, fn, bytes));
+  return ST_OK;
 }
 
 uint32_t make_idesc(int bn, bool a_mn, bool b_mn, int mma_m = BM) {
@@ -2449,7 +2477,7 @@ st_status launch(const GemmArgs& g, int M, int N, int K, const CUtensorMap& ma, 
   if (tiles < num_sms()) splits = std::min(num_sms() / tiles, p.kb_total);
   if (splits < 1) splits = 1;
   const size_t part_bytes = (size_t)BNMAX * BM * 4;
-  const size_t ws_cap = (size_t)2 * 148 * BNMAX * BM * 4;
+  const size_t ws_cap = (size_t)2 * kWsSms * BNMAX * BM * 4;
   while (splits > 1 && ((size_t)splits * tiles * part_bytes > ws_cap || tiles > (int)(kCounterBytes / 4))) --splits;
   p.kb_per_split = (p.kb_total + splits - 1) / splits;
   p.splits = (p.kb_total + p.kb_per_split - 1) / p.kb_per_split;
@@ -2464,23 +2492,16 @@ st_status launch(const GemmArgs& g, int M, int N, int K, const CUtensorMap& ma, 
   constexpr int S = 3;
   auto kern = (g.mode == ST_GEMM_FP32X3) ? tc_gemm_kernel<EPI, A_MN, B_MN, true, S, CV>
                                          : tc_gemm_kernel<EPI, A_MN, B_MN, false, S, CV>;
-  static bool attr_set[2] = {false, false};
   const int ai = g.mode == ST_GEMM_FP32X3 ? 1 : 0;
-  if (!attr_set[ai]) {
-    ST_CUDA_TRY(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, smem_bytes(S)));
-    attr_set[ai] = true;
-  }
+  (void)ai;
+  ST_TRY(ensure_max_smem((const void*)kern, smem_bytes(S)));
   p.ext_reduce = p.splits >= ext_reduce_splits();
   if (g.mode == ST_GEMM_FP32X3 && conv_ts_on() && (CV != CV_NONE || EPI == EPI_DW)) {
     // persistent TMEM-A kernel: implicit conv (all passes) and the tall dense dW
     const bool narrow = p.bn <= 64 && tsg_narrow_on();
     auto ck = narrow ? tc_tsg_kernel<EPI, A_MN, B_MN, CV, true> : tc_tsg_kernel<EPI, A_MN, B_MN, CV, false>;
     const int smem = narrow ? tsg_smem_bytes<true>() : tsg_smem_bytes<false>();
-    static bool cattr_set[2] = {false, false};
-    if (!cattr_set[narrow]) {
-      ST_CUDA_TRY(cudaFuncSetAttribute(ck, cudaFuncAttributeMaxDynamicSharedMemorySize, smem));
-      cattr_set[narrow] = true;
-    }
+    ST_TRY(ensure_max_smem((const void*)ck, smem));
     p.idesc = make_idesc(p.bn, false, B_MN);
     p.ext_reduce = p.splits > 1;
     // dW: K = pixels / T·B rows, long accumulation chains (measured error 2.9e-5 → 9.7e-6
@@ -2500,11 +2521,7 @@ st_status launch(const GemmArgs& g, int M, int N, int K, const CUtensorMap& ma, 
   if ((CV == CV_FWD || CV == CV_DX || CV == CV_ROWS) && p.splits == 1 && !conv_persistent_off()) {
     auto pk = (g.mode == ST_GEMM_FP32X3) ? tc_gemm_persistent_kernel<EPI, A_MN, B_MN, true, S, CV>
                                          : tc_gemm_persistent_kernel<EPI, A_MN, B_MN, false, S, CV>;
-    static bool pattr_set[2] = {false, false};
-    if (!pattr_set[ai]) {
-      ST_CUDA_TRY(cudaFuncSetAttribute(pk, cudaFuncAttributeMaxDynamicSharedMemorySize, smem_bytes(S)));
-      pattr_set[ai] = true;
-    }
+    ST_TRY(ensure_max_smem((const void*)pk, smem_bytes(S)));
     const int budget = g.max_ctas > 0 ? std::min(g.max_ctas, num_sms()) : num_sms();
     pk<<<std::min(tiles, budget), kPThreads, smem_bytes(S), g.stream>>>(ma, mb, p, mt, tiles);
     ST_CUDA_TRY(cudaGetLastError());
@@ -2535,7 +2552,7 @@ void plan_splits(TcParams& p, int M, int N, int K, int budget) {
   if (tiles < budget) splits = std::min(budget / tiles, p.kb_total);
   if (splits < 1) splits = 1;
   const size_t part_bytes = (size_t)BNMAX * BM * 4;
-  const size_t ws_cap = (size_t)2 * 148 * BNMAX * BM * 4;
+  const size_t ws_cap = (size_t)2 * kWsSms * BNMAX * BM * 4;
   while (splits > 1 && ((size_t)splits * tiles * part_bytes > ws_cap || tiles > (int)(kCounterBytes / 4))) --splits;
   p.kb_per_split = (p.kb_total + splits - 1) / splits;
   p.splits = (p.kb_total + p.kb_per_split - 1) / p.kb_per_split;
@@ -2603,13 +2620,13 @@ st_status launch_ts(const GemmArgs& g, int M, int N, int K, const CUtensorMap& m
   p.dev_flags = dev_flags();
   p.ext_reduce = p.splits >= ext_reduce_splits();
   float* blo = reinterpret_cast<float*>(static_cast<char*>(g.work) + kCounterBytes +
-                                        (size_t)2 * 148 * BNMAX * BM * 4);
+                                        (size_t)2 * kWsSms * BNMAX * BM * 4);
   int launches = 1;
   if (g.act_lo) {
     blo = const_cast<float*>(g.act_lo);  // the producer already split the operand
   } else {
     const size_t n4 = (size_t)N * K / 4;
-    ST_TRY(launch_maybe_pdl(g.pdl, split_lo_kernel, dim3((unsigned)std::min<size_t>(4 * 148, (n4 + 255) / 256)),
+    ST_TRY(launch_maybe_pdl(g.pdl, split_lo_kernel, dim3((unsigned)std::min<size_t>(4 * (size_t)num_sms(), (n4 + 255) / 256)),
                             dim3(256), 0, g.stream, reinterpret_cast<const float4*>(Bact),
                             reinterpret_cast<float4*>(blo), n4));
     ++launches;
@@ -2627,11 +2644,7 @@ st_status launch_ts(const GemmArgs& g, int M, int N, int K, const CUtensorMap& m
   }
   if (pair) {
     auto kern = ts_split_acc() ? tc_ts2_kernel<EPI, A_MN, true> : tc_ts2_kernel<EPI, A_MN, false>;
-    static bool attr_set[2] = {false, false};
-    if (!attr_set[ts_split_acc()]) {
-      ST_CUDA_TRY(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, ts2_smem_bytes()));
-      attr_set[ts_split_acc()] = true;
-    }
+    ST_TRY(ensure_max_smem((const void*)kern, ts2_smem_bytes()));
     if (g.pdl) {
       cudaLaunchConfig_t cfg = {};
       cfg.gridDim = grid;
@@ -2649,11 +2662,7 @@ st_status launch_ts(const GemmArgs& g, int M, int N, int K, const CUtensorMap& m
     }
   } else {
     auto kern = tc_ts_kernel<EPI, A_MN>;
-    static bool attr_set = false;
-    if (!attr_set) {
-      ST_CUDA_TRY(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, ts_smem_bytes()));
-      attr_set = true;
-    }
+    ST_TRY(ensure_max_smem((const void*)kern, ts_smem_bytes()));
     kern<<<grid, TS_THREADS, ts_smem_bytes(), g.stream>>>(ma, mb, mblo, p);
   }
   ST_CUDA_TRY(cudaGetLastError());
@@ -2674,6 +2683,8 @@ st_status launch_ts(const GemmArgs& g, int M, int N, int K, const CUtensorMap& m
 
 }  // namespace
 
+int device_sm_count() { return num_sms(); }
+
 int tc_last_launches() { return g_launches; }
 // counters (64 KB, zero-initialised by the owner, self-resetting) + split-K partials
 // for up to 2 × #SMs output tiles of 128 × 128 fp32.
@@ -2681,7 +2692,7 @@ int tc_last_launches() { return g_launches; }
 // lo tails: dW needs both dZ and X (B × (out + in), each padded to 64 floats).
 int64_t tc_workspace_bytes(int B, int max_in, int max_out) {
   const int64_t lo = ((int64_t)B * max_out + 63) / 64 * 64 + ((int64_t)B * max_in + 63) / 64 * 64;
-  return (int64_t)kCounterBytes + (int64_t)2 * 148 * BNMAX * BM * 4 + std::max<int64_t>(64, lo) * 4 + 256;
+  return (int64_t)kCounterBytes + (int64_t)2 * kWsSms * BNMAX * BM * 4 + std::max<int64_t>(64, lo) * 4 + 256;
 }
 
 st_status simt_fwd(const GemmArgs& g, const float* X, const float* W, const float* bias, float* Z, int relu);
@@ -2754,14 +2765,14 @@ st_status tc_dw_impl(const GemmArgs& g, const float* X, const float* dZ, float* 
     // persistent kernel: lo of dZ and X precomputed into the workspace tail
     const bool x3 = g.mode == ST_GEMM_FP32X3;
     float* lo_base = reinterpret_cast<float*>(static_cast<char*>(g.work) + kCounterBytes +
-                                              (size_t)2 * 148 * BNMAX * BM * 4);
+                                              (size_t)2 * kWsSms * BNMAX * BM * 4);
     float* dzlo = lo_base;
     float* xlo = lo_base + (((size_t)g.B * g.n_out + 63) / 64 * 64);
     int launches = 1;
     (void)dzlo;
     if (x3) {
       const size_t n4b = (size_t)g.B * g.n_in / 4;
-      ST_TRY(launch_maybe_pdl(g.pdl, split_lo_kernel, dim3((unsigned)std::min<size_t>(4 * 148, (n4b + 255) / 256)),
+      ST_TRY(launch_maybe_pdl(g.pdl, split_lo_kernel, dim3((unsigned)std::min<size_t>(4 * (size_t)num_sms(), (n4b + 255) / 256)),
                               dim3(256), 0, g.stream, reinterpret_cast<const float4*>(X),
                               reinterpret_cast<float4*>(xlo), n4b));
       launches += 1;
@@ -2799,12 +2810,7 @@ st_status tc_dw_impl(const GemmArgs& g, const float* X, const float* dZ, float* 
     }
     auto kern = upd ? (x3 ? tc_dw_kernel<true, true> : tc_dw_kernel<false, true>)
                     : (x3 ? tc_dw_kernel<true, false> : tc_dw_kernel<false, false>);
-    static bool attr_set[4] = {false, false, false, false};
-    const int ai = (x3 ? 1 : 0) + (upd ? 2 : 0);
-    if (!attr_set[ai]) {
-      ST_CUDA_TRY(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, dw_smem_bytes()));
-      attr_set[ai] = true;
-    }
+    ST_TRY(ensure_max_smem((const void*)kern, dw_smem_bytes()));
     ST_TRY(launch_maybe_pdl(g.pdl, kern, dim3(grid), dim3(DW_THREADS), (size_t)dw_smem_bytes(), g.stream, ma, mb,
                             mblo, mw, mv, p, mt, nt));
     if (gb_upd) {
@@ -2941,9 +2947,9 @@ st_status tc_conv_fwd_pair(const GemmArgs& g, const float* X, int H, int W, int 
   p.dev_flags = dev_flags();
   p.ext_reduce = p.splits >= ext_reduce_splits();
   float* xlo = reinterpret_cast<float*>(static_cast<char*>(g.work) + kCounterBytes +
-                                        (size_t)2 * 148 * BNMAX * BM * 4);
+                                        (size_t)2 * kWsSms * BNMAX * BM * 4);
   const size_t n4 = (size_t)P * Cin / 4;
-  split_lo_kernel<<<std::min<size_t>(4 * 148, (n4 + 255) / 256), 256, 0, g.stream>>>(
+  split_lo_kernel<<<std::min<size_t>(4 * (size_t)num_sms(), (n4 + 255) / 256), 256, 0, g.stream>>>(
       reinterpret_cast<const float4*>(X), reinterpret_cast<float4*>(xlo), n4);
   ST_CUDA_TRY(cudaGetLastError());
   CUtensorMap ma, mb, mblo;
@@ -2951,11 +2957,7 @@ st_status tc_conv_fwd_pair(const GemmArgs& g, const float* X, int H, int W, int 
       !make_act_map(&mblo, xlo, g.B, H, W, Cin, BNMAX / 2, false))
     return set_error(ST_ERR_CUDA, "cuTensorMapEncodeTiled failed (conv fwd, pair)");
   auto kern = ts_split_acc() ? tc_ts2_kernel<EPI_FWD, true, true, true> : tc_ts2_kernel<EPI_FWD, true, false, true>;
-  static bool attr_set[2] = {false, false};
-  if (!attr_set[ts_split_acc()]) {
-    ST_CUDA_TRY(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, ts2_smem_bytes()));
-    attr_set[ts_split_acc()] = true;
-  }
+  ST_TRY(ensure_max_smem((const void*)kern, ts2_smem_bytes()));
   dim3 grid(mt_grid, nt, p.splits);
   kern<<<grid, TS_THREADS, ts2_smem_bytes(), g.stream>>>(ma, mb, mblo, p);
   ST_CUDA_TRY(cudaGetLastError());

@@ -94,13 +94,7 @@ __global__ void __launch_bounds__(kThreads) update_predict_kernel(float4* __rest
 }
 
 int grid_for(size_t n4) {
-  static int sms = 0;
-  if (sms == 0) {
-    int dev = 0;
-    cudaGetDevice(&dev);
-    cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
-    if (sms <= 0) sms = 148;
-  }
+  const int sms = device_sm_count();
   // persistent grid-stride: up to 8 resident 256-thread CTAs per SM
   const size_t per_cta = (size_t)kThreads * kUnroll;
   size_t want = (n4 + per_cta - 1) / per_cta;

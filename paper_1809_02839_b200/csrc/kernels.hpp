@@ -17,6 +17,8 @@ namespace st {
     asm volatile("griddepcontrol.wait;" ::: "memory");              \
   } while (0)
 bool pdl_enabled();
+// SMs of the current device (cached per device ordinal; grid sizing of every launcher)
+int device_sm_count();
 void set_thread_pdl(int on);  // this host thread's launches (−1: the ST_PDL_DENSE default)
 template <typename... KArgs, typename... Args>
 inline st_status launch_pdl(bool pdl, void (*kern)(KArgs...), dim3 grid, dim3 block, size_t smem, cudaStream_t s,

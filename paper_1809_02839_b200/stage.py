@@ -89,7 +89,13 @@ class Stage:
     def is_last(self) -> bool:
         return self.k == self.N - 1
 
-    def set_params(self, host: np.ndarray) -> None:
+    def set_params(self, host) -> None:
+        """host: a float32 numpy array, or a contiguous float32 CUDA tensor on this device."""
+        if isinstance(host, torch.Tensor):
+            assert host.dtype == torch.float32 and host.is_contiguous()
+            torch.cuda.synchronize(host.device)
+            check(lib.st_set_params(self.ctx, host.data_ptr(), host.numel()))
+            return
         a = np.ascontiguousarray(host, dtype=np.float32)
         check(lib.st_set_params(self.ctx, a.ctypes.data, a.size))
 

@@ -244,6 +244,21 @@ def glorot_params(model: Model, seed: int) -> List[np.ndarray]:
     return out
 
 
+def glorot_dense_layer_f32(layer: Layer, seed: int, index: int) -> np.ndarray:
+    """One dense layer's flat block [W (Glorot-U ±√(6/(in+out))) row-major, b = 0] as
+    float32, from its own stream PCG64([seed, index]) — for models too large to draw
+    whole on the host (the large FCN: 4.04G parameters); the same block can be redrawn
+    layer by layer."""
+    rng = np.random.default_rng([seed, index])
+    r = np.float32(math.sqrt(6.0 / (layer.n_in + layer.n_out)))
+    w = rng.random(layer.n_in * layer.n_out, dtype=np.float32)
+    w *= 2 * r
+    w -= r
+    if layer.bias:
+        return np.concatenate([w, np.zeros(layer.n_out, np.float32)])
+    return w
+
+
 def tokens(vocab: int, num_batches: int, batch: int, seq_len: int, seed: int,
            dist: str = "zipf") -> Tuple[np.ndarray, np.ndarray]:
     """Synthetic LM data: X int32 [M, T·B] input tokens (time-major, row t·B + b),
