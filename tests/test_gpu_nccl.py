@@ -38,6 +38,9 @@ def _nccl_env(rank: int):
 
 
 def _worker(rank, world, port, model_name, M, B, lr, out_dir, fail_rank, timeout_s):
+    import faulthandler
+    # diagnostics only: a stuck stage prints its Python stack (the parent kills it)
+    faulthandler.dump_traceback_later(timeout_s + 60 if fail_rank >= 0 else 500, exit=False)
     _nccl_env(rank)
     os.environ["ST_COMM_TIMEOUT_S"] = str(timeout_s)
     os.environ["MASTER_ADDR"] = "127.0.0.1"
@@ -98,9 +101,14 @@ def _spawn(world, model_name, M, B, lr, tmp_path, fail_rank=-1, timeout_s=600):
                                                  timeout_s)) for r in range(world)]
     for p in procs:
         p.start()
+    hung = []
     for p in procs:
-        p.join(600)
-        assert not p.is_alive(), "stage process hung"
+        p.join(max(120, 4 * timeout_s) if fail_rank >= 0 else 600)
+        if p.is_alive():
+            hung.append(p.pid)
+            p.kill()
+            p.join(10)
+    assert not hung, f"stage process(es) {hung} hung (killed)"
     return [p.exitcode for p in procs]
 
 
