@@ -26,6 +26,7 @@
 #include <cstring>
 #include <deque>
 #include <mutex>
+#include <thread>
 
 #include "engine.hpp"
 
@@ -82,11 +83,20 @@ class NcclTransport final : public Transport {
     }
     return ST_OK;
   }
+  // ncclCommAbort of one communicator waits for the device work in flight, and a kernel of
+  // the other communicator may be what that work waits on (the compute stream waits on
+  // both comm streams): abort both concurrently so both abort flags are raised at once.
   void abort() override {
     if (aborted_) return;
     aborted_ = true;
+    int dev = 0;
+    cudaGetDevice(&dev);
+    std::thread t([this, dev] {
+      cudaSetDevice(dev);
+      ncclCommAbort(bwd_);
+    });
     ncclCommAbort(fwd_);
-    ncclCommAbort(bwd_);
+    t.join();
   }
 
  private:
