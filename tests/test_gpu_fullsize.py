@@ -248,10 +248,12 @@ def test_large_fcn_full_size_one_step_sampled(st):
     stage_backward on that one layer — stage composition equals the monolithic model,
     pinned in test_oracle_pins), and per layer 512 random weights plus the bias are
     compared. After one update from V = 0: V = (1 − γ)·g and W = W0 − η·V (Eq. 1, D1).
-    Gates: loss 1e-5; sampled W 1e-6 (dominated by W0 — addressing); sampled V per layer
-    2e-2 (one mini-batch: the few ReLU decisions taken on pre-activations within
-    rounding of 0, reading D24, profiles/r2_d24_fp32_vs_fp64.json: 6e-4 from a single flip
-    in plain fp32 at 8192 wide)."""
+    Gates: loss 1e-5; sampled V per layer 2e-2 (one mini-batch: the few ReLU decisions
+    taken on pre-activations within rounding of 0, reading D24,
+    profiles/r2_d24_fp32_vs_fp64.json: 6e-4 from a single flip in plain fp32 at 8192
+    wide); sampled W per layer 1e-6 + 2e-2·‖η·V‖/‖W‖ — W = W0 − η·V, so the V error
+    allowed above reaches W scaled by the update's size (layer 15, the last 16384²
+    layer, has the largest ‖η·V‖/‖W‖: 3.5e-6 measured), plus fp32 storage of W0."""
     model = sd.config_large_fcn(1)
     L = model.layers
     B, seed = 128, 11
@@ -307,8 +309,10 @@ def test_large_fcn_full_size_one_step_sampled(st):
         w_ref = flat[sel] - eta * v_ref
         rv = rel_l2(v_got, v_ref)
         rw = rel_l2(w_got, w_ref)
-        worst.append((i, rv, rw))
-        assert rw <= 1e-6, (i, rw)
-        assert rv <= 2e-2, (i, rv)
+        tol_w = 1e-6 + 2e-2 * eta * np.linalg.norm(v_ref) / np.linalg.norm(w_ref)
+        worst.append((i, rv, rw, tol_w))
     _record("large_fcn_full_1step_sampled", {"loss": float(losses[0]), "loss_ref": loss,
-                                              "per_layer_v_w": [(i, rv, rw) for i, rv, rw in worst]})
+                                              "per_layer_v_w_tolw": worst})
+    for i, rv, rw, tol_w in worst:
+        assert rw <= tol_w, (i, rw, tol_w)
+        assert rv <= 2e-2, (i, rv)
