@@ -54,8 +54,9 @@ def parse():
     p.add_argument("--no-e2e", action="store_true")
     p.add_argument("--no-cpu", action="store_true")
     p.add_argument("--lr", type=float, default=1e-3)
-    p.add_argument("--partition", default="fixed", choices=["fixed", "auto"],
-                   help="fixed: the BJ / SURVEY §8(d) stage cuts; auto: st_partition over per-layer roofline times")
+    p.add_argument("--partition", default="fixed", choices=["fixed", "auto", "profiled"],
+                   help="fixed: the BJ / SURVEY §8(d) stage cuts; auto: st_partition over per-layer roofline "
+                        "times; profiled: st_partition over per-layer times measured on this GPU (NEXT-4)")
     p.add_argument("--parallel", default="pp", choices=["pp", "dp"],
                    help="pp: the SpecTrain pipeline (default); dp: the data-parallel comparator (NEXT-1)")
     return p.parse_args()
@@ -161,6 +162,51 @@ def auto_partition(model, B: int, S: int, hbm_gbs: float, tf32x3_tflops: float):
         costs.append(max(b / (hbm_gbs * 1e9), f / (tf32x3_tflops * 1e12)))
     cuts, _ = st.partition(costs, S)
     return dataclasses.replace(model, cuts=tuple(cuts))
+
+
+def profiled_partition(model, B: int, S: int, dev, lr: float, gemm: int, warm: int = 3, reps: int = 3):
+    """NEXT-4, PipeDream-style: profile each layer on this GPU, then cut.
+    The whole model runs as one library stage; with ST_PROF_LAYERS the engine brackets
+    every layer's forward and (serialised) backward work with CUDA events
+    (st_get_layer_profile); the per-layer cost is its mean forward + backward time over
+    `reps` profiled mini-batches after `warm` unprofiled ones, and st_partition (min-max
+    contiguous DP) turns the costs into S stages. Returns the re-cut model and the
+    per-layer costs in µs."""
+    import dataclasses
+
+    import torch
+
+    import paper_1809_02839_b200 as st
+    import synthdata as sd
+    kinds = {sd.DENSE: st.ST_LAYER_DENSE, sd.EMBED: st.ST_LAYER_EMBED, sd.LSTM: st.ST_LAYER_LSTM,
+             sd.CONV: st.ST_LAYER_CONV, sd.POOL: st.ST_LAYER_POOL}
+    layers = [(l.n_in, l.n_out, st.ST_ACT_RELU if l.act == sd.RELU else st.ST_ACT_NONE, 1 if l.bias else 0,
+               kinds[l.kind], l.hw) for l in model.layers]
+    whole = dataclasses.replace(model, cuts=())
+    T = model.seq_len
+    R = B * T
+    M = warm + reps
+    s = st.Stage(layers, [], 0, B, lr, 0.9, pred=st.ST_PRED_NONE, gemm=gemm, transport=st.ST_TRANSPORT_NCCL,
+                 device=dev.index or 0, max_minibatches=M, seq_len=T)
+    try:
+        g = torch.Generator(device=dev)
+        g.manual_seed(4321)
+        init_params(s, whole.layers, dev, g)
+        if model.layers[0].kind == sd.EMBED:
+            xs = torch.randint(0, model.layers[0].n_in, (M, R), device=dev, dtype=torch.int32, generator=g)
+        else:
+            xs = torch.rand(M, R, model.layers[0].width_in, device=dev, generator=g)
+        ys = torch.randint(0, model.layers[-1].n_out, (M, R), device=dev, dtype=torch.int32, generator=g)
+        s.run(warm, xs[:warm], ys[:warm])
+        s.set_layer_profiling(True)
+        s.run(reps, xs[warm:], ys[warm:])
+        ms, cnt = s.layer_profile()
+        s.set_layer_profiling(False)
+    finally:
+        s.close()
+    costs = [float(ms[i, 0] / max(1, cnt[i, 0]) + ms[i, 1] / max(1, cnt[i, 1])) for i in range(len(layers))]
+    cuts, _ = st.partition(costs, S)
+    return dataclasses.replace(model, cuts=tuple(cuts)), [round(c * 1e3, 1) for c in costs]
 
 
 def pipeline_roofline(model, B: int, pred: str, hbm_gbs: float, tf32x3_tflops: float):
@@ -519,10 +565,19 @@ def run_ours(args):
     if N > 1:
         dist.init_process_group("nccl", device_id=dev)
     model, B, wname = workload(args.workload, S)
+    gemm = {"fp32x3": st.ST_GEMM_FP32X3, "tf32": st.ST_GEMM_TF32, "simt": st.ST_GEMM_SIMT}[args.gemm]
+    layer_cost_us = None
     if args.partition == "auto" and S > 1:
         hbm_, _ = measured_peaks()
         model = auto_partition(model, B, S, hbm_, measured_tensor_peak()[2])
-    gemm = {"fp32x3": st.ST_GEMM_FP32X3, "tf32": st.ST_GEMM_TF32, "simt": st.ST_GEMM_SIMT}[args.gemm]
+    elif args.partition == "profiled" and S > 1:
+        # every rank profiles the same model on its own GPU; rank 0's cut is broadcast
+        model_p, layer_cost_us = profiled_partition(model, B, S, dev, args.lr, gemm)
+        obj = [list(model_p.cuts) if rank == 0 else None]
+        if N > 1:
+            dist.broadcast_object_list(obj, src=0)
+        import dataclasses
+        model = dataclasses.replace(model, cuts=tuple(obj[0]))
     pred = {"spectrain": st.ST_PRED_SPECTRAIN, "none": st.ST_PRED_NONE, "stash": st.ST_PRED_STASH,
             "staleness_free": st.ST_PRED_STALENESS_FREE}[args.pred]
     kinds = {sd.DENSE: st.ST_LAYER_DENSE, sd.EMBED: st.ST_LAYER_EMBED, sd.LSTM: st.ST_LAYER_LSTM,
@@ -627,6 +682,20 @@ def run_ours(args):
     brk = [s.profile() for s in my_stages]
     for s in my_stages:
         s.set_profiling(False)
+    # per-stage busy time (compute classes, comm excluded) of the breakdown session
+    busy_local = [(s.k, sum(p[c][0] for c in ("update", "gemm_fwd", "gemm_dx", "gemm_dw", "loss")) / n_brk)
+                  for s, p in zip(my_stages, brk)]
+    if N > 1:
+        allb = [None] * N
+        dist.all_gather_object(allb, busy_local)
+        busy_local = [b for part in allb for b in part]
+    busy_ms = [b for _, b in sorted(busy_local)]
+    stage_busy = {"ms_per_minibatch": [round(b, 4) for b in busy_ms],
+                  "imbalance_max_over_mean": round(max(busy_ms) * len(busy_ms) / sum(busy_ms), 3) if sum(busy_ms) > 0
+                  else None,
+                  "note": "per stage: its fwd / dX / dW+update GEMM, loss and update kernel time per mini-batch "
+                          "(CUDA events, breakdown session, comm excluded); the step can be no faster than the "
+                          "busiest stage (P:460-470)"}
     t_max = max_over_ranks(ms)
     if N > 1:
         lt = torch.tensor([launches], device=dev, dtype=torch.int64)
@@ -742,6 +811,7 @@ def run_ours(args):
             "scaling": "strong", "vs_baseline": None, "dtype": "f32", "data": "synthetic",
             "config": {"workload": wname, "stages": S, "batch": B, "seq_len": T, "gemm": args.gemm, "pred": args.pred,
                        "cuts": list(model.cuts), "partition": args.partition,
+                       **({"layer_cost_us": layer_cost_us} if layer_cost_us else {}),
                        "parallelism": f"pp{S}", "l2": "no flush: per-step working set (weights) >> 126 MB L2",
                        "session": "one 1F1B session of warmup + steps mini-batches; timed window = CUDA events "
                                   "after stage 0's B(warmup-1) and B(warmup+steps-1) (P:415 steady state)"},
@@ -760,6 +830,7 @@ def run_ours(args):
                              "8.91x best (FCN/RNN), 3.10x FCN/RNN average, +98.5% average over 6 models; "
                              "no absolute samples/s published",
             "kernel_ms_per_step": gemm_prof,
+            "stage_busy": stage_busy,
             "kernel_ms_note": f"per kernel class, ms per mini-batch, from a separate {n_brk}-mini-batch session "
                               "with every class bracketed (rank 0's stages)",
             "cpu_baseline": cpu,

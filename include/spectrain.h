@@ -334,6 +334,15 @@ ST_API st_status st_record_after_backward(st_ctx* ctx, int64_t mb, void* cuda_ev
  * only the two records). Classes: 0 update (K-B), 1 gemm_fwd, 2 gemm_dx,
  * 3 gemm_dw, 4 loss (CE + bias-grad), 5 comm. Resets the totals. */
 ST_API st_status st_set_profiling(st_ctx* ctx, int on);
+/* Bit of `on` (st_set_profiling) that brackets each layer's whole forward and
+ * backward work instead (PipeDream-style per-layer profile; SURVEY §8(f)
+ * NEXT-4): while set, the backward runs serialised (each layer's dW + update is joined
+ * before the next layer starts), so a bracket is that layer's cost alone. */
+#define ST_PROF_LAYERS (1 << 30)
+/* Per layer l of the stage: ms[2l] / ms[2l+1] = total milliseconds of its forward /
+ * backward work since profiling was switched on, counts[...] = passes bracketed
+ * (either may be NULL). n ≥ 2·(layers of the stage), else ST_ERR_INPUT. Synchronises. */
+ST_API st_status st_get_layer_profile(st_ctx* ctx, double* ms, int64_t* counts, size_t n);
 /* Per class: total milliseconds and launch count since profiling was switched on
  * (synchronises). arrays of length 6. */
 ST_API st_status st_get_profile(st_ctx* ctx, double* total_ms, int64_t* launches);

@@ -115,6 +115,7 @@ def _load() -> ctypes.CDLL:
         "st_sync": (S, [P]),
         "st_set_profiling": (S, [P, I]),
         "st_get_profile": (S, [P, P, P]),
+        "st_get_layer_profile": (S, [P, P, P, U]),
         "st_kernel_launches": (I64, [P]),
         "st_update_predict_raw": (S, [P, P, P, P, P, U, F, F, I, I, I, P]),
         "st_prediction_error_work_bytes": (I64, []),
@@ -137,9 +138,12 @@ lib = _load()
 EXPORTED = ("st_version_difference", "st_program", "st_partition", "st_comm_plan", "st_query_sizes", "st_get_nccl_id", "st_init",
             "st_connect_local", "st_destroy", "st_set_params", "st_get_params", "st_stage_forward",
             "st_stage_backward", "st_predict_and_update", "st_step", "st_run", "st_run_host", "st_run_group", "st_get_trace",
-            "st_losses_device", "st_sync", "st_record_after_backward", "st_set_profiling", "st_get_profile", "st_kernel_launches",
+            "st_losses_device", "st_sync", "st_record_after_backward", "st_set_profiling", "st_get_profile", "st_get_layer_profile", "st_kernel_launches",
             "st_update_predict_raw", "st_prediction_error_work_bytes", "st_prediction_error_raw", "st_gemm_raw", "st_gemm_workspace_bytes", "st_softmax_ce_raw", "st_dw_update_raw",
             "st_last_error", "st_version")
+
+
+ST_PROF_LAYERS = 1 << 30  # st_set_profiling bit: per-layer brackets (include/spectrain.h)
 
 
 def check(status: int) -> None:

@@ -44,6 +44,7 @@ st_status ctx_run_group(st_ctx** ctxs, int n, int64_t M, const float* xs, const 
 st_status ctx_get_trace(st_ctx* c, st_event* out, size_t cap, size_t* n);
 st_status ctx_set_profiling(st_ctx* c, int on);
 st_status ctx_get_profile(st_ctx* c, double* total_ms, int64_t* launches);
+st_status ctx_get_layer_profile(st_ctx* c, double* ms, int64_t* counts, size_t n);
 
 }  // namespace st
 
@@ -213,6 +214,11 @@ st_status st_set_profiling(st_ctx* ctx, int on) {
 st_status st_get_profile(st_ctx* ctx, double* total_ms, int64_t* launches) {
   NEED_CTX(ctx);
   GUARD({ return ctx_get_profile(ctx, total_ms, launches); })
+}
+
+st_status st_get_layer_profile(st_ctx* ctx, double* ms, int64_t* counts, size_t n) {
+  NEED_CTX(ctx);
+  GUARD({ return ctx_get_layer_profile(ctx, ms, counts, n); })
 }
 
 int64_t st_kernel_launches(st_ctx* ctx) { return ctx ? ctx->launches : -1; }

@@ -7,6 +7,7 @@
 //   B(j): [recv grad] → per layer (reverse) gemm_dx with WB (ReLU mask fused),
 //         gemm_dw (+bias grad) → [send grad]
 //   update: K-B (k_update.cu) — Eq. 1, D1 apply, WF/WB for the next tasks.
+#include <nvtx3/nvToolsExt.h>
 #include <chrono>
 #include <cmath>
 #include <cstring>
@@ -270,6 +271,17 @@ st_status validate_and_layout(const st_config* c, Layout* L) {
 }
 
 // ---- profiling helpers ----------------------------------------------------------
+// NVTX range for a timeline tool (nsys / ncu --nvtx); header-only NVTX v3, a no-op
+// unless a tool is attached
+struct NvtxRange {
+  explicit NvtxRange(const char* fmt, int a, long long b) {
+    char name[64];
+    snprintf(name, sizeof name, fmt, a, b);
+    nvtxRangePushA(name);
+  }
+  ~NvtxRange() { nvtxRangePop(); }
+};
+
 struct Timed {
   st_ctx* c;
   int cls;
@@ -286,6 +298,36 @@ struct Timed {
     if (b) cudaEventRecord(b, s);
   }
   cudaEvent_t get() {
+    if (!c->prof.pool.empty()) {
+      cudaEvent_t e = c->prof.pool.back();
+      c->prof.pool.pop_back();
+      return e;
+    }
+    cudaEvent_t e;
+    cudaEventCreate(&e);
+    return e;
+  }
+};
+
+// Per-layer bracket (ST_PROF_LAYERS): one event pair around all of layer l's work of
+// one pass (dir 0 forward, 1 backward) on stream s; backward brackets on the main and
+// the side stream are both counted (the profiled backward runs serialised).
+struct TimedLayer {
+  st_ctx* c;
+  cudaStream_t s;
+  cudaEvent_t b = nullptr;
+  TimedLayer(st_ctx* ctx, size_t l, int dir, cudaStream_t stream = nullptr)
+      : c(ctx), s(stream ? stream : ctx->stream) {
+    if (!c->prof.layers) return;
+    cudaEvent_t a = take();
+    b = take();
+    cudaEventRecord(a, s);
+    c->prof.lpairs.push_back({(int)(2 * l + dir), a, b});
+  }
+  ~TimedLayer() {
+    if (b) cudaEventRecord(b, s);
+  }
+  cudaEvent_t take() {
     if (!c->prof.pool.empty()) {
       cudaEvent_t e = c->prof.pool.back();
       c->prof.pool.pop_back();
@@ -630,6 +672,9 @@ static st_status issue_op(st_ctx* c, const CommGroup& g) {
     }
     {
       Timed t(c, KC_COMM, cs);
+      static const char* names[4] = {"stage %d send_fwd(%lld)", "stage %d recv_fwd(%lld)", "stage %d send_bwd(%lld)",
+                                     "stage %d recv_bwd(%lld)"};
+      NvtxRange range(names[o.kind & 3], c->k, (long long)o.mb);
       if (o.kind == CK_SEND_FWD || o.kind == CK_SEND_BWD)
         ST_TRY(c->tp->send(o.kind, o.mb, o.buf, o.count, cs));
       else
@@ -811,6 +856,7 @@ static st_status forward_compute(st_ctx* c, int64_t mb, const float* x_dev, cons
   const size_t nl = c->layers.size();
   for (size_t l = 0; l < nl; ++l) {
     const LayerInfo& L = c->layers[l];
+    TimedLayer tl(c, l, 0);
     const float* in = layer_in(c, slot, l);
     // where this layer's output goes: the next layer's input stash, or the stage output
     float* out = nullptr;
@@ -969,6 +1015,8 @@ static st_status backward_compute(st_ctx* c, int64_t mb, bool fused = false) {
   };
   for (int l = nl - 1; l >= 0; --l) {
     const LayerInfo& L = c->layers[l];
+    TimedLayer tl(c, (size_t)l, 1);  // ST_PROF_LAYERS: the side stream is joined below, so
+                                     // this bracket covers the layer's dW + update too
     // Programmatic dependent launches pay off on one in-order stream; for a large dense
     // layer the main-stream dX overlaps the side-stream dW + update, and early-launched
     // CTAs waiting on their predecessor hold SMs the other stream needs (large FCN −5%),
@@ -1163,6 +1211,7 @@ static st_status backward_compute(st_ctx* c, int64_t mb, bool fused = false) {
     // this layer's dW + update on the side stream
     if (l == 0 && D && !c->first_stage) ST_CUDA_TRY(cudaEventRecord(c->ev_dx_ready, c->stream));
     if (D) dZ = D;
+    if (c->prof.layers) ST_TRY(join_side());  // per-layer profile: no cross-layer overlap
   }
   ST_TRY(join_side());
   return ST_OK;
@@ -1174,6 +1223,7 @@ static st_status run_task(st_ctx* c, const float* x_dev, const int32_t* y_dev, b
   if (c->pending_update)
     return set_error(ST_ERR_STATE, "stage %d: predict_and_update must follow every backward", c->k);
   const Task t = c->program[c->pc];
+  NvtxRange range(t.dir == ST_FWD ? "stage %d F(%lld)" : "stage %d B(%lld)", c->k, (long long)t.mb);
   // programmatic dependent launches for this task (the backward refines it per layer)
   c->pdl_now = c->pdl_dense;
   set_thread_pdl(c->pdl_now ? 1 : 0);
@@ -1235,6 +1285,7 @@ static st_status run_task(st_ctx* c, const float* x_dev, const int32_t* y_dev, b
 }
 
 st_status ctx_update(st_ctx* c) {
+  NvtxRange range("stage %d update(v%lld)", c->k, (long long)c->version);
   if (!c->pending_update) return set_error(ST_ERR_STATE, "stage %d: no backward pending", c->k);
   const UpdateConsts k = make_update_consts(c->lr, c->gamma, c->sF, c->sB, c->momentum);
   {
@@ -1415,14 +1466,44 @@ st_status ctx_set_profiling(st_ctx* c, int on) {
   }
   // on: bitmask of kernel classes (1 << KC_*); nonzero enables. Events are created
   // here, outside any timed region, so bracketing costs only the two records.
+  for (auto& p : c->prof.lpairs) {
+    c->prof.pool.push_back(p.a);
+    c->prof.pool.push_back(p.b);
+  }
+  c->prof.lpairs.clear();
+  c->prof.layer_ms.assign(2 * c->layers.size(), 0.0);
+  c->prof.layer_n.assign(2 * c->layers.size(), 0);
+  c->prof.layers = (on & ST_PROF_LAYERS) != 0;
+  on &= ~ST_PROF_LAYERS;
   c->prof.mask = (unsigned)on;
   c->prof.on = on != 0;
-  if (c->prof.on) {
+  if (c->prof.on || c->prof.layers) {
     while (c->prof.pool.size() < 8192) {
       cudaEvent_t e;
       ST_CUDA_TRY(cudaEventCreate(&e));
       c->prof.pool.push_back(e);
     }
+  }
+  return ST_OK;
+}
+
+st_status ctx_get_layer_profile(st_ctx* c, double* ms, int64_t* counts, size_t n) {
+  if (n < 2 * c->layers.size()) return set_error(ST_ERR_INPUT, "layer profile needs 2 x %zu entries", c->layers.size());
+  ST_CUDA_TRY(cudaSetDevice(c->device));
+  ST_CUDA_TRY(cudaStreamSynchronize(c->stream));
+  ST_CUDA_TRY(cudaStreamSynchronize(c->side));
+  for (auto& p : c->prof.lpairs) {
+    float t = 0.f;
+    ST_CUDA_TRY(cudaEventElapsedTime(&t, p.a, p.b));
+    c->prof.layer_ms[p.cls] += t;
+    c->prof.layer_n[p.cls] += 1;
+    c->prof.pool.push_back(p.a);
+    c->prof.pool.push_back(p.b);
+  }
+  c->prof.lpairs.clear();
+  for (size_t i = 0; i < 2 * c->layers.size(); ++i) {
+    if (ms) ms[i] = c->prof.layer_ms[i];
+    if (counts) counts[i] = c->prof.layer_n[i];
   }
   return ST_OK;
 }

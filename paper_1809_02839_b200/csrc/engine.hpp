@@ -98,6 +98,12 @@ struct Profiler {
   std::vector<cudaEvent_t> pool;
   double total_ms[KC_COUNT] = {};
   int64_t launches[KC_COUNT] = {};
+  // ST_PROF_LAYERS: per-layer brackets (cls = 2·layer + dir) of the whole forward /
+  // backward work of each layer; the backward runs serialised (no side-stream overlap)
+  bool layers = false;
+  std::vector<Pair> lpairs;
+  std::vector<double> layer_ms;  // [2·L]: fwd, bwd per layer
+  std::vector<int64_t> layer_n;
 };
 
 }  // namespace st

@@ -169,6 +169,21 @@ class Stage:
         check(lib.st_get_profile(self.ctx, ms, n))
         return {name: (ms[i], n[i]) for i, name in enumerate(L.KERNEL_CLASSES)}
 
+    def set_layer_profiling(self, on: bool) -> None:
+        """Per-layer forward / backward brackets (ST_PROF_LAYERS; the backward runs
+        serialised while on)."""
+        check(lib.st_set_profiling(self.ctx, L.ST_PROF_LAYERS if on else 0))
+
+    def layer_profile(self) -> np.ndarray:
+        """[n_layers × 2] total ms of each layer's forward / backward work since
+        set_layer_profiling(True), and [n_layers × 2] pass counts."""
+        bounds = [0] + self.cuts + [len(self.layers)]
+        n = 2 * (bounds[self.k + 1] - bounds[self.k])
+        ms = (ctypes.c_double * n)()
+        cnt = (ctypes.c_int64 * n)()
+        check(lib.st_get_layer_profile(self.ctx, ms, cnt, n))
+        return np.array(ms[:]).reshape(-1, 2), np.array(cnt[:]).reshape(-1, 2)
+
     def kernel_launches(self) -> int:
         return int(lib.st_kernel_launches(self.ctx))
 
