@@ -114,8 +114,24 @@ enum { ST_LOSS_SOFTMAX_CE = 0 };
  * wait longer than ST_COMM_TIMEOUT_S seconds (default 600) aborts both communicators
  * (ST_ERR_NCCL). LOCAL: several stage contexts in ONE process (same GPU) linked with
  * st_connect_local; messages are device copies on the same comm streams, handed over
- * through host channels; a failing stage releases its blocked peers (ST_ERR_STATE). */
-enum { ST_TRANSPORT_NCCL = 0, ST_TRANSPORT_LOCAL = 1 };
+ * through host channels; a failing stage releases its blocked peers (ST_ERR_STATE).
+ * P2P (transfer fused into compute over peer memory): no copy and
+ * no send — stage k's last forward GEMM writes its output straight into stage k+1's
+ * stash slot, stage k+1's layer-0 dX GEMM writes the gradient straight into stage k's
+ * gradient ring; peer buffers are mapped with CUDA IPC (one process per GPU over
+ * NVLink / NVSwitch, or processes sharing a GPU) or used directly (contexts of one
+ * process); completion is handed over by flags in the waiter's memory (system-scope
+ * release / acquire, one-thread kernels on the compute stream). Connect with
+ * st_p2p_export + st_p2p_connect before the first task. A wait longer than
+ * ST_COMM_TIMEOUT_S releases the spinning kernels and returns ST_ERR_STATE. */
+enum { ST_TRANSPORT_NCCL = 0, ST_TRANSPORT_LOCAL = 1, ST_TRANSPORT_P2P = 2 };
+
+/* Opaque, trivially copyable descriptor of one P2P stage's exported buffers (its stash,
+ * gradient ring and flag block: CUDA IPC handles + offsets, geometry, owner pid).
+ * Exchange it between processes as 1024 raw bytes (e.g. torch.distributed). */
+typedef struct {
+  uint8_t bytes[1024];
+} st_p2p_desc;
 
 typedef struct {
   int32_t n_in;
@@ -144,6 +160,18 @@ typedef struct {
   int32_t device;           /* CUDA device ordinal of this stage */
   int64_t max_minibatches;  /* capacity of the on-device loss vector (≥ the M of st_run) */
   uint8_t nccl_id[128];     /* ST_TRANSPORT_NCCL: ncclUniqueId from st_get_nccl_id on stage 0 */
+  /* Hybrid data × pipeline parallelism: replicas[s] ≥ 1
+   * contexts share stage s (NULL = one each). A replicated stage splits the mini-batch
+   * by rows — replica r computes rows [r·B/R, (r+1)·B/R) with batch B/R (`batch` stays
+   * the GLOBAL B on every context) — and its replicas sum their gradients before the
+   * identical K-B update (NCCL all-reduce over the stage's replicas, or an in-place
+   * reduce across co-located replica contexts), so the pipeline computes exactly what
+   * the unreplicated one does. The neighbours exchange row slices with each replica.
+   * Limits (ST_ERR_INPUT): the last stage and adjacent stages cannot both / at all be
+   * replicated, seq_len = 1, B divisible by R, not with ST_TRANSPORT_P2P. NCCL ranks
+   * are stage-major: rank(s, r) = Σ_{j<s} replicas[j] + r. */
+  const int32_t* replicas;  /* [N] or NULL */
+  int32_t replica;          /* this context's index within its stage, 0 ≤ replica < replicas[stage] */
 } st_config;
 
 /* Byte counts the caller must allocate (0 = not needed: the buffer aliases W). */
@@ -249,6 +277,18 @@ ST_API st_status st_get_nccl_id(uint8_t out[128]);
  * ST_ERR_NCCL (communicator setup). */
 ST_API st_status st_init(const st_config* cfg, const st_buffers* bufs, void* stream, void* comm_fwd_stream,
                          void* comm_bwd_stream, st_ctx** out);
+
+/* P2P transport: describe this context's peer-writable buffers (the stash and work
+ * arenas must be cudaMalloc-backed allocations: CUDA IPC cannot export expandable /
+ * VMM segments — ST_ERR_INPUT). The flag block is a small library-owned cudaMalloc
+ * (freed by st_destroy). Errors: ST_ERR_STATE (not a P2P context), ST_ERR_INPUT. */
+ST_API st_status st_p2p_export(st_ctx* ctx, st_p2p_desc* out);
+/* P2P transport: map the neighbours' buffers (prev = stage k−1's descriptor, NULL for
+ * k = 0; next = stage k+1's, NULL for k = N−1). Same-process descriptors are used as
+ * plain pointers, others are opened with cudaIpcOpenMemHandle (closed by st_destroy).
+ * Errors: ST_ERR_INPUT (missing / bad descriptor), ST_ERR_SHAPE (the descriptors do not
+ * describe the adjacent stages of this pipeline), ST_ERR_CUDA (IPC open failed). */
+ST_API st_status st_p2p_connect(st_ctx* ctx, const st_p2p_desc* prev, const st_p2p_desc* next);
 
 /* LOCAL transport: link ctxs[0..n) as consecutive stages 0..n−1 of one pipeline
  * in this process. Required before any task of a LOCAL context. */

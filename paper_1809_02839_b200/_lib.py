@@ -25,7 +25,8 @@ ST_PRED_SPECTRAIN, ST_PRED_NONE, ST_PRED_STASH, ST_PRED_STALENESS_FREE = 0, 1, 2
 ST_MOMENTUM_EMA, ST_MOMENTUM_HEAVY_BALL = 0, 1
 ST_GEMM_FP32X3, ST_GEMM_TF32, ST_GEMM_SIMT = 0, 1, 2
 ST_LOSS_SOFTMAX_CE = 0
-ST_TRANSPORT_NCCL, ST_TRANSPORT_LOCAL = 0, 1
+ST_TRANSPORT_NCCL, ST_TRANSPORT_LOCAL, ST_TRANSPORT_P2P = 0, 1, 2
+P2P_DESC_BYTES = 1024  # sizeof(st_p2p_desc)
 KERNEL_CLASSES = ("update", "gemm_fwd", "gemm_dx", "gemm_dw", "loss", "comm")
 
 STATUS = {0: "ST_OK", 1: "ST_ERR_INPUT", 2: "ST_ERR_SHAPE", 3: "ST_ERR_STATE", 4: "ST_ERR_CUDA",
@@ -52,6 +53,7 @@ class StConfig(ctypes.Structure):
         ("pred", ctypes.c_int32), ("momentum", ctypes.c_int32), ("gemm", ctypes.c_int32),
         ("loss", ctypes.c_int32), ("transport", ctypes.c_int32), ("device", ctypes.c_int32),
         ("max_minibatches", ctypes.c_int64), ("nccl_id", ctypes.c_uint8 * 128),
+        ("replicas", ctypes.POINTER(ctypes.c_int32)), ("replica", ctypes.c_int32),
     ]
 
 
@@ -114,6 +116,8 @@ def _load() -> ctypes.CDLL:
         "st_losses_device": (P, [P]),
         "st_sync": (S, [P]),
         "st_set_profiling": (S, [P, I]),
+        "st_p2p_export": (S, [P, P]),
+        "st_p2p_connect": (S, [P, P, P]),
         "st_get_profile": (S, [P, P, P]),
         "st_get_layer_profile": (S, [P, P, P, U]),
         "st_kernel_launches": (I64, [P]),
@@ -138,7 +142,7 @@ lib = _load()
 EXPORTED = ("st_version_difference", "st_program", "st_partition", "st_comm_plan", "st_query_sizes", "st_get_nccl_id", "st_init",
             "st_connect_local", "st_destroy", "st_set_params", "st_get_params", "st_stage_forward",
             "st_stage_backward", "st_predict_and_update", "st_step", "st_run", "st_run_host", "st_run_group", "st_get_trace",
-            "st_losses_device", "st_sync", "st_record_after_backward", "st_set_profiling", "st_get_profile", "st_get_layer_profile", "st_kernel_launches",
+            "st_losses_device", "st_sync", "st_record_after_backward", "st_p2p_export", "st_p2p_connect", "st_set_profiling", "st_get_profile", "st_get_layer_profile", "st_kernel_launches",
             "st_update_predict_raw", "st_prediction_error_work_bytes", "st_prediction_error_raw", "st_gemm_raw", "st_gemm_workspace_bytes", "st_softmax_ce_raw", "st_dw_update_raw",
             "st_last_error", "st_version")
 
@@ -198,7 +202,8 @@ def nccl_id() -> bytes:
 def make_config(layers, cuts: Sequence[int], stage: int, batch: int,
                 lr: float, gamma: float, pred: int = ST_PRED_SPECTRAIN, momentum: int = ST_MOMENTUM_EMA,
                 gemm: int = ST_GEMM_FP32X3, transport: int = ST_TRANSPORT_NCCL, device: int = 0,
-                max_minibatches: int = 256, nccl_id_bytes: Optional[bytes] = None, seq_len: int = 1):
+                max_minibatches: int = 256, nccl_id_bytes: Optional[bytes] = None, seq_len: int = 1,
+                replicas: Optional[Sequence[int]] = None, replica: int = 0):
     """layers: (n_in, n_out, act, bias[, kind[, hw]]) tuples. Returns (StConfig, keepalive) —
     keepalive holds the arrays the struct points to."""
     def mk(t):
@@ -217,7 +222,12 @@ def make_config(layers, cuts: Sequence[int], stage: int, batch: int,
     cfg.transport, cfg.device, cfg.max_minibatches = transport, device, max_minibatches
     if nccl_id_bytes is not None:
         ctypes.memmove(cfg.nccl_id, nccl_id_bytes, 128)
-    return cfg, (L, C)
+    Rp = None
+    if replicas is not None:
+        Rp = (ctypes.c_int32 * len(replicas))(*[int(r) for r in replicas])
+        cfg.replicas = ctypes.cast(Rp, ctypes.POINTER(ctypes.c_int32))
+    cfg.replica = int(replica)
+    return cfg, (L, C, Rp)
 
 
 def query_sizes(cfg: StConfig) -> StSizes:

@@ -206,6 +206,17 @@ st_status st_record_after_backward(st_ctx* ctx, int64_t mb, void* cuda_event) {
   GUARD({ return ctx_mark_after_backward(ctx, mb, cuda_event); })
 }
 
+st_status st_p2p_export(st_ctx* ctx, st_p2p_desc* out) {
+  NEED_CTX(ctx);
+  if (!out) return set_error(ST_ERR_INPUT, "p2p_export: out is NULL");
+  GUARD({ return st::p2p_export(ctx, out); })
+}
+
+st_status st_p2p_connect(st_ctx* ctx, const st_p2p_desc* prev, const st_p2p_desc* next) {
+  NEED_CTX(ctx);
+  GUARD({ return st::p2p_connect(ctx, prev, next); })
+}
+
 st_status st_set_profiling(st_ctx* ctx, int on) {
   NEED_CTX(ctx);
   GUARD({ return ctx_set_profiling(ctx, on); })

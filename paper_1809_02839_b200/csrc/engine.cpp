@@ -50,6 +50,7 @@ struct Layout {
   int gemm_in = 1, gemm_out = 1;  // largest GEMM operand widths (workspace sizing)
   int T = 1;
   int64_t R = 1;
+  int rep_prev = 1, rep_self = 1, rep_next = 1;  // replicas of stages k−1, k, k+1 (NEXT-4)
   bool embed_first = false;
   size_t ring_fwd_elems = 0, ring_bwd_elems = 0;
   st_sizes sizes{};
@@ -83,7 +84,7 @@ st_status validate_and_layout(const st_config* c, Layout* L) {
   if (c->gemm != ST_GEMM_FP32X3 && c->gemm != ST_GEMM_TF32 && c->gemm != ST_GEMM_SIMT)
     return set_error(ST_ERR_INPUT, "bad gemm mode");
   if (c->loss != ST_LOSS_SOFTMAX_CE) return set_error(ST_ERR_INPUT, "bad loss");
-  if (c->transport != ST_TRANSPORT_NCCL && c->transport != ST_TRANSPORT_LOCAL)
+  if (c->transport != ST_TRANSPORT_NCCL && c->transport != ST_TRANSPORT_LOCAL && c->transport != ST_TRANSPORT_P2P)
     return set_error(ST_ERR_INPUT, "bad transport");
   if (c->max_minibatches < 1) return set_error(ST_ERR_INPUT, "max_minibatches must be >= 1");
   const int N = c->num_stages, k = c->stage;
@@ -117,7 +118,24 @@ st_status validate_and_layout(const st_config* c, Layout* L) {
   if (c->layers[c->num_layers - 1].kind != ST_LAYER_DENSE)
     return set_error(ST_ERR_INPUT, "the network's last layer must be DENSE (softmax CE)");
   const int l0 = bounds[k], l1 = bounds[k + 1];
-  const int64_t B = c->batch;
+  // hybrid DP × PP: replicas per stage (NEXT-4)
+  auto rep = [&](int s) -> int { return (c->replicas && s >= 0 && s < N) ? c->replicas[s] : 1; };
+  for (int s = 0; s < N; ++s) {
+    if (rep(s) < 1) return set_error(ST_ERR_INPUT, "replicas[%d] = %d must be >= 1", s, rep(s));
+    if (rep(s) == 1) continue;
+    if (s == N - 1) return set_error(ST_ERR_INPUT, "the last stage cannot be replicated (it owns the batch-mean loss)");
+    if ((s > 0 && rep(s - 1) > 1) || rep(s + 1) > 1)
+      return set_error(ST_ERR_INPUT, "adjacent stages %d and %d cannot both be replicated", s, rep(s - 1) > 1 ? s - 1 : s + 1);
+    if (c->seq_len != 1) return set_error(ST_ERR_INPUT, "replicated stages need seq_len = 1 (row slices per sample)");
+    if (c->batch % rep(s)) return set_error(ST_ERR_INPUT, "batch %d not divisible by replicas[%d] = %d", c->batch, s, rep(s));
+    if (c->transport == ST_TRANSPORT_P2P) return set_error(ST_ERR_INPUT, "replicated stages need NCCL or LOCAL transport");
+  }
+  if (c->replica < 0 || c->replica >= rep(k))
+    return set_error(ST_ERR_INPUT, "replica %d outside [0, %d)", c->replica, rep(k));
+  L->rep_prev = k > 0 ? rep(k - 1) : 1;
+  L->rep_self = rep(k);
+  L->rep_next = k + 1 < N ? rep(k + 1) : 1;
+  const int64_t B = c->batch / L->rep_self;  // rows of this context (a replica: its slice)
   const int64_t T = c->seq_len;
   const int64_t R = B * T;
   L->T = (int)T;
@@ -353,6 +371,7 @@ st_status query_sizes(const st_config* c, st_sizes* out) {
 st_status ctx_wait(st_ctx* c);
 
 static void begin_session(st_ctx* c, int64_t M) {
+  p2p_begin_session(c);
   c->program = build_program(c->N, c->k, M);
   c->plan = build_comm_plan(c->N, c->k, M);
   c->pc = 0;
@@ -384,7 +403,13 @@ st_status ctx_init(const st_config* cfg, const st_buffers* bufs, void* stream, v
   std::unique_ptr<st_ctx> c(new st_ctx());
   c->N = cfg->num_stages;
   c->k = cfg->stage;
-  c->B = cfg->batch;
+  c->B = (int)(L.R / L.T);  // rows of this context: the global batch, or a replica's slice
+  c->B_global = cfg->batch;
+  c->rep_prev = L.rep_prev;
+  c->rep_self = L.rep_self;
+  c->rep_next = L.rep_next;
+  c->replica = cfg->replica;
+  for (int s2 = 0; s2 < c->N; ++s2) c->reps.push_back(cfg->replicas ? cfg->replicas[s2] : 1);
   c->T = L.T;
   c->R = L.R;
   c->embed_first = L.embed_first;
@@ -502,8 +527,14 @@ st_status ctx_init(const st_config* cfg, const st_buffers* bufs, void* stream, v
 
   if (c->transport_kind == ST_TRANSPORT_NCCL) {
     st_status e;
-    c->tp = make_nccl_transport(cfg->nccl_id, c->N, c->k, c->device, &e);
+    c->tp = make_nccl_transport(cfg->nccl_id, c->N, c->k, c->device, c->reps, c->replica, &e);
     if (e != ST_OK) return e;
+  } else if (c->transport_kind == ST_TRANSPORT_P2P && c->N > 1) {
+    const st_status e = p2p_alloc(c.get());
+    if (e != ST_OK) {
+      p2p_free(c.get());
+      return e;
+    }
   }
   ST_CUDA_TRY(cudaStreamCreateWithFlags(&c->side, cudaStreamNonBlocking));
   c->side_events.resize(c->layers.size() + 1);
@@ -533,25 +564,40 @@ st_status ctx_init(const st_config* cfg, const st_buffers* bufs, void* stream, v
 }
 
 st_status ctx_connect_local(st_ctx** ctxs, int n) {
-  if (!ctxs || n < 1) return set_error(ST_ERR_INPUT, "connect_local: need >= 1 context");
+  if (!ctxs || n < 1 || !ctxs[0]) return set_error(ST_ERR_INPUT, "connect_local: need >= 1 context");
   const int N = ctxs[0]->N;
-  if (n != N) return set_error(ST_ERR_INPUT, "connect_local: %d contexts for a %d-stage pipeline", n, N);
-  for (int k = 0; k < n; ++k) {
-    if (!ctxs[k] || ctxs[k]->k != k || ctxs[k]->N != N || ctxs[k]->transport_kind != ST_TRANSPORT_LOCAL)
-      return set_error(ST_ERR_INPUT, "connect_local: context %d is not stage %d of a LOCAL %d-stage pipeline", k, k,
-                       N);
-    if (ctxs[k]->B != ctxs[0]->B) return set_error(ST_ERR_SHAPE, "connect_local: batch mismatch");
-    if (k > 0 && ctxs[k - 1]->out_last != ctxs[k]->in_first)
-      return set_error(ST_ERR_SHAPE, "connect_local: cut width mismatch between stages %d and %d", k - 1, k);
-  }
-  auto link = make_local_link(N);
-  for (int k = 0; k < n; ++k) {
-    st_ctx* c = ctxs[k];
-    ST_CUDA_TRY(cudaSetDevice(c->device));
-    st_status e;
-    c->tp = make_local_transport(link, k, c->ring_fwd, c->ring_bwd, c->ring_fwd_elems, c->ring_bwd_elems, &e);
-    if (e != ST_OK) return e;
-    c->link = link;
+  const std::vector<int> reps = ctxs[0]->reps;
+  int total = 0;
+  for (int r : reps) total += r;
+  if (n != total)
+    return set_error(ST_ERR_INPUT, "connect_local: %d contexts for a %d-stage pipeline with %d stage contexts", n, N,
+                     total);
+  // stage-major, replica-minor order
+  int i = 0;
+  for (int k = 0; k < N; ++k)
+    for (int r = 0; r < reps[k]; ++r, ++i) {
+      st_ctx* c = ctxs[i];
+      if (!c || c->k != k || c->N != N || c->replica != r || c->transport_kind != ST_TRANSPORT_LOCAL || c->reps != reps)
+        return set_error(ST_ERR_INPUT, "connect_local: context %d is not stage %d replica %d of a LOCAL %d-stage "
+                         "pipeline (same replicas table)", i, k, r, N);
+      if (c->B_global != ctxs[0]->B_global) return set_error(ST_ERR_SHAPE, "connect_local: batch mismatch");
+      if (k > 0 && ctxs[i - 1 - r]->out_last != c->in_first)
+        return set_error(ST_ERR_SHAPE, "connect_local: cut width mismatch between stages %d and %d", k - 1, k);
+    }
+  auto link = make_local_link(N, reps);
+  i = 0;
+  for (int k = 0; k < N; ++k) {
+    std::shared_ptr<ReplicaGroup> group = reps[k] > 1 ? make_replica_group(reps[k], link) : nullptr;
+    for (int r = 0; r < reps[k]; ++r, ++i) {
+      st_ctx* c = ctxs[i];
+      ST_CUDA_TRY(cudaSetDevice(c->device));
+      st_status e;
+      c->tp = make_local_transport(link, k, c->ring_fwd, c->ring_bwd, c->ring_fwd_elems, c->ring_bwd_elems,
+                                   c->replica, c->rep_prev, c->rep_self, c->rep_next, &e);
+      if (e != ST_OK) return e;
+      c->link = link;
+      c->rgroup = group;
+    }
   }
   return ST_OK;
 }
@@ -573,6 +619,7 @@ void ctx_destroy(st_ctx* c) {
   if (c->comm_fwd) cudaStreamSynchronize(c->comm_fwd);
   if (c->comm_bwd) cudaStreamSynchronize(c->comm_bwd);
   c->tp.reset();  // communicators before the streams they used
+  p2p_free(c);
   for (int b = 0; b < 2; ++b)
     for (cudaEvent_t e : {c->ev_sent_fwd[b], c->ev_sent_bwd[b], c->ev_recv_bwd[b], c->ev_bwd_ring[b], c->ev_join[b]})
       if (e) cudaEventDestroy(e);
@@ -653,6 +700,30 @@ static CommOp comm_op(st_ctx* c, int kind, int64_t mb) {
   }
 }
 
+// one message to / from a neighbour — split into row slices, one per replica, when that
+// neighbour is a replicated stage (hybrid DP × PP); chan = the replica of the
+// replicated side of the channel
+static st_status move(st_ctx* c, const CommOp& o, cudaStream_t cs) {
+  const bool to_next = o.kind == CK_SEND_FWD || o.kind == CK_RECV_BWD;
+  const int nrep = to_next ? c->rep_next : c->rep_prev;
+  const bool send = o.kind == CK_SEND_FWD || o.kind == CK_SEND_BWD;
+  if (nrep <= 1) {
+    const int chan = c->rep_self > 1 ? c->replica : 0;
+    return send ? c->tp->send(o.kind, o.mb, o.buf, o.count, cs, chan) : c->tp->recv(o.kind, o.mb, o.buf, o.count, cs, chan);
+  }
+  const size_t part = o.count / (size_t)nrep;  // rows split evenly (B divisible by the replica count)
+  ST_TRY(c->tp->group_begin());
+  for (int r = 0; r < nrep; ++r) {
+    const st_status e = send ? c->tp->send(o.kind, o.mb, o.buf + r * part, part, cs, r)
+                             : c->tp->recv(o.kind, o.mb, o.buf + r * part, part, cs, r);
+    if (e != ST_OK) {
+      c->tp->group_end();
+      return e;
+    }
+  }
+  return c->tp->group_end();
+}
+
 static st_status issue_op(st_ctx* c, const CommGroup& g) {
   if (!c->tp) return set_error(ST_ERR_STATE, "stage %d: transport not connected", c->k);
   for (int i = 0; i < g.n_ops; ++i) {
@@ -675,10 +746,7 @@ static st_status issue_op(st_ctx* c, const CommGroup& g) {
       static const char* names[4] = {"stage %d send_fwd(%lld)", "stage %d recv_fwd(%lld)", "stage %d send_bwd(%lld)",
                                      "stage %d recv_bwd(%lld)"};
       NvtxRange range(names[o.kind & 3], c->k, (long long)o.mb);
-      if (o.kind == CK_SEND_FWD || o.kind == CK_SEND_BWD)
-        ST_TRY(c->tp->send(o.kind, o.mb, o.buf, o.count, cs));
-      else
-        ST_TRY(c->tp->recv(o.kind, o.mb, o.buf, o.count, cs));
+      ST_TRY(move(c, o, cs));
     }
     switch (o.kind) {
       case CK_SEND_FWD:
@@ -743,7 +811,7 @@ st_status ctx_wait(st_ctx* c) {
   int sleep_us = 2;
   for (;;) {
     const cudaError_t q = cudaStreamQuery(c->stream);
-    if (q == cudaSuccess) return ST_OK;
+    if (q == cudaSuccess) return c->p2p ? p2p_check(c) : ST_OK;
     if (q != cudaErrorNotReady) return set_error(ST_ERR_CUDA, "stage %d: %s", c->k, cudaGetErrorString(q));
     const st_status e = c->tp->poll();
     if (e != ST_OK) {
@@ -1209,7 +1277,12 @@ static st_status backward_compute(st_ctx* c, int64_t mb, bool fused = false) {
     }
     // the layer-0 dX is the message to stage k−1: its send may start now, overlapping
     // this layer's dW + update on the side stream
-    if (l == 0 && D && !c->first_stage) ST_CUDA_TRY(cudaEventRecord(c->ev_dx_ready, c->stream));
+    if (l == 0 && D && !c->first_stage) {
+      if (c->p2p)
+        ST_TRY(p2p_after_dx(c, mb));  // the gradient is in stage k−1's ring slot
+      else
+        ST_CUDA_TRY(cudaEventRecord(c->ev_dx_ready, c->stream));
+    }
     if (D) dZ = D;
     if (c->prof.layers) ST_TRY(join_side());  // per-layer profile: no cross-layer overlap
   }
@@ -1227,7 +1300,8 @@ static st_status run_task(st_ctx* c, const float* x_dev, const int32_t* y_dev, b
   // programmatic dependent launches for this task (the backward refines it per layer)
   c->pdl_now = c->pdl_dense;
   set_thread_pdl(c->pdl_now ? 1 : 0);
-  ST_TRY(comm_before_task(c, c->pc));
+  const bool p2p = c->p2p != nullptr;  // no comm plan: the GEMMs write the peer buffers
+  if (!p2p) ST_TRY(comm_before_task(c, c->pc));
   st_event e{};
   e.stage = c->k;
   e.op_idx = (int32_t)c->trace.size();
@@ -1244,23 +1318,47 @@ static st_status run_task(st_ctx* c, const float* x_dev, const int32_t* y_dev, b
   const int b = (int)(t.mb % 2);
   const size_t slot = (size_t)(t.mb % c->S);
   if (t.dir == ST_FWD) {
-    if (!c->first_stage) ST_CUDA_TRY(cudaStreamWaitEvent(c->stream, c->ev_recv_fwd[slot], 0));  // input arrived
-    if (!c->last_stage) {  // the output slot's previous send (mb − 2) has left
-      if (c->sent_fwd_pending[b]) ST_CUDA_TRY(cudaStreamWaitEvent(c->stream, c->ev_sent_fwd[b], 0));
-      c->send_fwd = c->send_fwd2[b];
+    if (p2p) {
+      ST_TRY(p2p_before_forward(c, t.mb));  // input landed; output = the peer's stash slot
+    } else {
+      if (!c->first_stage) ST_CUDA_TRY(cudaStreamWaitEvent(c->stream, c->ev_recv_fwd[slot], 0));  // input arrived
+      if (!c->last_stage) {  // the output slot's previous send (mb − 2) has left
+        if (c->sent_fwd_pending[b]) ST_CUDA_TRY(cudaStreamWaitEvent(c->stream, c->ev_sent_fwd[b], 0));
+        c->send_fwd = c->send_fwd2[b];
+      }
     }
     ST_TRY(forward_compute(c, t.mb, x_dev, y_dev, host_io, loss_host));
-    if (!c->last_stage) ST_CUDA_TRY(cudaEventRecord(c->ev_fwd_done, c->stream));
+    if (p2p)
+      ST_TRY(p2p_after_forward(c, t.mb));
+    else if (!c->last_stage)
+      ST_CUDA_TRY(cudaEventRecord(c->ev_fwd_done, c->stream));
   } else {
-    if (!c->last_stage) {  // the gradient from k+1 arrived
-      ST_CUDA_TRY(cudaStreamWaitEvent(c->stream, c->ev_recv_bwd[b], 0));
-      c->recv_bwd = c->recv_bwd2[b];
+    if (p2p) {
+      ST_TRY(p2p_before_backward(c, t.mb));  // gradient landed; layer-0 dX = the peer's ring slot
+    } else {
+      if (!c->last_stage) {  // the gradient from k+1 arrived
+        ST_CUDA_TRY(cudaStreamWaitEvent(c->stream, c->ev_recv_bwd[b], 0));
+        c->recv_bwd = c->recv_bwd2[b];
+      }
+      if (!c->first_stage) {
+        if (c->sent_bwd_pending[b]) ST_CUDA_TRY(cudaStreamWaitEvent(c->stream, c->ev_sent_bwd[b], 0));
+        c->send_bwd = c->send_bwd2[b];
+      }
     }
-    if (!c->first_stage) {
-      if (c->sent_bwd_pending[b]) ST_CUDA_TRY(cudaStreamWaitEvent(c->stream, c->ev_sent_bwd[b], 0));
-      c->send_bwd = c->send_bwd2[b];
+    // a replicated stage (hybrid DP × PP): G of this replica's rows, summed over the
+    // replicas, then the same K-B update on every replica
+    const bool replicated = c->rep_self > 1;
+    ST_TRY(backward_compute(c, t.mb, fused_update && !replicated));
+    if (replicated) {
+      Timed tc(c, KC_COMM);
+      if (c->rgroup)
+        ST_TRY(replica_reduce_local(c->rgroup.get(), c->replica, c->G, (size_t)c->P, c->stream));
+      else if (c->tp)
+        ST_TRY(c->tp->allreduce_sum(c->G, (size_t)c->P, c->stream));
+      else
+        return set_error(ST_ERR_STATE, "stage %d replica %d: transport not connected", c->k, c->replica);
     }
-    ST_TRY(backward_compute(c, t.mb, fused_update));
+    if (p2p) ST_TRY(p2p_after_backward(c, t.mb));
     // this backward's readers are done with its stash slot and its gradient slot
     ST_CUDA_TRY(cudaEventRecord(c->ev_bwd_slot[slot], c->stream));
     c->bwd_slot_done[slot] = 1;
@@ -1274,12 +1372,19 @@ static st_status run_task(st_ctx* c, const float* x_dev, const int32_t* y_dev, b
         ++i;
       }
     }
-    if (fused_update)
+    if (fused_update && replicated) {
+      const UpdateConsts kc = make_update_consts(c->lr, c->gamma, c->sF, c->sB, c->momentum);
+      Timed tu(c, KC_UPDATE);
+      ST_TRY(launch_update_predict(c->W, c->V, c->G, c->WF_out, c->WB_out, (size_t)c->P, kc, c->stream));
+      c->launches += 1;
+      c->version += 1;
+    } else if (fused_update) {
       c->version += 1;  // the update already ran inside the dW epilogues
-    else
+    } else {
       c->pending_update = true;
+    }
   }
-  ST_TRY(comm_after_task(c, c->pc));
+  if (!p2p) ST_TRY(comm_after_task(c, c->pc));
   c->pc++;
   return ST_OK;
 }
@@ -1333,7 +1438,9 @@ st_status ctx_predict_and_update(st_ctx* c) {
 }
 
 static const float* x_of(st_ctx* c, const float* xs, int64_t mb) {
-  return (c->first_stage && xs) ? xs + (size_t)mb * c->R * (c->embed_first ? 1 : c->in_first) : nullptr;
+  // a replica of a replicated first stage reads its row slice of each mini-batch
+  const size_t w = c->embed_first ? 1 : (size_t)c->in_first;
+  return (c->first_stage && xs) ? xs + ((size_t)mb * c->B_global * c->T + (size_t)c->replica * c->R) * w : nullptr;
 }
 static const int32_t* y_of(st_ctx* c, const int32_t* ys, int64_t mb) {
   return (c->last_stage && ys) ? ys + (size_t)mb * c->R : nullptr;

@@ -34,8 +34,18 @@ st_status partition_layers(const double* cost, int L, int N, int32_t* cuts, doub
 class Transport {
  public:
   virtual ~Transport() = default;
-  virtual st_status send(int kind, int64_t mb, const float* buf, size_t count, cudaStream_t s) = 0;
-  virtual st_status recv(int kind, int64_t mb, float* buf, size_t count, cudaStream_t s) = 0;
+  // chan: the replica index of the replicated side of this channel (hybrid DP × PP,
+  // NEXT-4; 0 when neither neighbour is replicated)
+  virtual st_status send(int kind, int64_t mb, const float* buf, size_t count, cudaStream_t s, int chan = 0) = 0;
+  virtual st_status recv(int kind, int64_t mb, float* buf, size_t count, cudaStream_t s, int chan = 0) = 0;
+  // the ops to / from several replicas of a neighbour form one group (NCCL: ncclGroupStart / End)
+  virtual st_status group_begin() { return ST_OK; }
+  virtual st_status group_end() { return ST_OK; }
+  // sum `buf` over the replicas of this stage (NCCL: ncclAllReduce on the replica communicator)
+  virtual st_status allreduce_sum(float* buf, size_t n, cudaStream_t s) {
+    (void)buf; (void)n; (void)s;
+    return set_error(ST_ERR_STATE, "transport: no replica all-reduce");
+  }
   // asynchronous failure of the transport (NCCL: ncclCommGetAsyncError on both
   // communicators); ST_OK while healthy
   virtual st_status poll() { return ST_OK; }
@@ -44,14 +54,26 @@ class Transport {
   virtual void abort() {}
 };
 
-std::unique_ptr<Transport> make_nccl_transport(const uint8_t id[128], int N, int k, int device, st_status* err);
+// reps: replicas per stage (NCCL ranks are stage-major: rank(s, r) = Σ_{j<s} reps[j] + r)
+std::unique_ptr<Transport> make_nccl_transport(const uint8_t id[128], int N, int k, int device,
+                                               const std::vector<int>& reps, int replica, st_status* err);
 
 struct LocalLink;  // shared channels of a LOCAL pipeline (transport.cpp)
 std::unique_ptr<Transport> make_local_transport(std::shared_ptr<LocalLink> link, int k, float* ring_fwd,
-                                                float* ring_bwd, size_t fwd_elems, size_t bwd_elems,
-                                                st_status* err);
-std::shared_ptr<LocalLink> make_local_link(int N);
+                                                float* ring_bwd, size_t fwd_elems, size_t bwd_elems, int replica,
+                                                int rep_prev, int rep_self, int rep_next, st_status* err);
+std::shared_ptr<LocalLink> make_local_link(int N, const std::vector<int>& reps);
 void abort_local_link(LocalLink* link);
+
+// co-located replicas of one stage (LOCAL transport): in-place sum of their gradient
+// arenas, each replica reducing one slice of every arena (transport.cpp)
+struct ReplicaGroup;
+std::shared_ptr<ReplicaGroup> make_replica_group(int R, std::shared_ptr<LocalLink> link);
+st_status replica_reduce_local(ReplicaGroup* g, int replica, float* G, size_t n, cudaStream_t s);
+
+// P2P transport (p2p.cu): the producing kernels write into the peer's buffers, flags
+// in the waiter's memory hand them over (NEXT-3)
+struct P2pState;
 
 struct LayerInfo {
   int n_in, n_out, act, bias, kind;
@@ -209,7 +231,28 @@ struct st_ctx {
   std::vector<st_event> trace;
   std::unique_ptr<st::Transport> tp;
   std::shared_ptr<st::LocalLink> link;
+  st::P2pState* p2p = nullptr;  // ST_TRANSPORT_P2P
+  // hybrid DP × PP (NEXT-4): replicas of stages k−1, k, k+1, this context's replica index
+  int rep_prev = 1, rep_self = 1, rep_next = 1, replica = 0;
+  int B_global = 1;
+  std::vector<int> reps;                         // replicas per stage (all N)
+  std::shared_ptr<st::ReplicaGroup> rgroup;      // LOCAL: the stage's co-located replicas
 
   st::Profiler prof;
   int64_t launches = 0;
 };
+
+namespace st {
+st_status p2p_alloc(st_ctx* c);
+void p2p_free(st_ctx* c);
+st_status p2p_export(st_ctx* c, st_p2p_desc* out);
+st_status p2p_connect(st_ctx* c, const st_p2p_desc* prev, const st_p2p_desc* next);
+void p2p_begin_session(st_ctx* c);
+st_status p2p_before_forward(st_ctx* c, int64_t mb);
+st_status p2p_after_forward(st_ctx* c, int64_t mb);
+st_status p2p_before_backward(st_ctx* c, int64_t mb);
+st_status p2p_after_dx(st_ctx* c, int64_t mb);
+st_status p2p_after_backward(st_ctx* c, int64_t mb);
+st_status p2p_check(st_ctx* c);
+st_status launch_replica_sum(float* const* Gs, int R, size_t begin, size_t end, cudaStream_t s);
+}  // namespace st

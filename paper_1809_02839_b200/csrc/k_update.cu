@@ -231,7 +231,37 @@ __global__ void pred_err_final_kernel(const double* __restrict__ part, int nb, d
   out[1] = q;
 }
 
+// Hybrid DP × PP (NEXT-4): in-place sum of the gradient arenas of a stage's R
+// co-located replicas over elements [begin, end): every arena receives Σ_j G_j, summed
+// in the fixed order j = 0..R−1 (all replicas end bit-identical). Each replica reduces
+// its own slice of the arenas, so the R launches touch disjoint memory.
+constexpr int kMaxReplicas = 16;
+struct GPtrs {
+  float* g[kMaxReplicas];
+};
+
+__global__ void replica_sum_kernel(GPtrs p, int R, size_t begin, size_t end) {
+  const size_t stride = (size_t)gridDim.x * blockDim.x;
+  for (size_t i = begin + (size_t)blockIdx.x * blockDim.x + threadIdx.x; i < end; i += stride) {
+    float acc = p.g[0][i];
+    for (int j = 1; j < R; ++j) acc = __fadd_rn(acc, p.g[j][i]);
+    for (int j = 0; j < R; ++j) p.g[j][i] = acc;
+  }
+}
+
 }  // namespace
+
+st_status launch_replica_sum(float* const* Gs, int R, size_t begin, size_t end, cudaStream_t s) {
+  if (R < 1 || R > kMaxReplicas) return set_error(ST_ERR_INPUT, "replica sum: %d replicas (max %d)", R, kMaxReplicas);
+  if (end <= begin) return ST_OK;
+  GPtrs p{};
+  for (int j = 0; j < R; ++j) p.g[j] = Gs[j];
+  const size_t n = end - begin;
+  const int grid = (int)std::min<size_t>((size_t)device_sm_count() * 8, (n + 255) / 256);
+  replica_sum_kernel<<<std::max(1, grid), 256, 0, s>>>(p, R, begin, end);
+  ST_CUDA_TRY(cudaGetLastError());
+  return ST_OK;
+}
 
 int64_t prediction_error_work_bytes() { return (int64_t)(2 * kErrBlocks + 2) * 8; }
 

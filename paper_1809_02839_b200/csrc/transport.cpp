@@ -42,28 +42,53 @@ namespace {
 // thread on one comm stream, in the same order on every rank (the comm plan).
 class NcclTransport final : public Transport {
  public:
-  NcclTransport(ncclComm_t f, ncclComm_t b, int N, int k) : fwd_(f), bwd_(b), N_(N), k_(k) {}
+  NcclTransport(ncclComm_t f, ncclComm_t b, ncclComm_t rep, int N, int k, std::vector<int> reps)
+      : fwd_(f), bwd_(b), rep_(rep), N_(N), k_(k), reps_(std::move(reps)) {
+    base_.assign(N_ + 1, 0);
+    for (int s = 0; s < N_; ++s) base_[s + 1] = base_[s] + reps_[s];
+  }
   ~NcclTransport() override {
     if (aborted_) return;
     if (fwd_) ncclCommDestroy(fwd_);
     if (bwd_) ncclCommDestroy(bwd_);
+    if (rep_) ncclCommDestroy(rep_);
   }
-  st_status send(int kind, int64_t mb, const float* buf, size_t count, cudaStream_t s) override {
+  // rank of the peer stage's context on this channel: its replica `chan` if it is the
+  // replicated side, else its only context
+  int rank_of(int stage, int chan) const { return base_[stage] + (reps_[stage] > 1 ? chan : 0); }
+  st_status group_begin() override {
+    ncclResult_t r = ncclGroupStart();
+    return r == ncclSuccess ? ST_OK : set_error(ST_ERR_NCCL, "ncclGroupStart: %s", ncclGetErrorString(r));
+  }
+  st_status group_end() override {
+    ncclResult_t r = ncclGroupEnd();
+    return r == ncclSuccess ? ST_OK : set_error(ST_ERR_NCCL, "ncclGroupEnd: %s", ncclGetErrorString(r));
+  }
+  st_status allreduce_sum(float* buf, size_t n, cudaStream_t s) override {
+    if (!rep_) return set_error(ST_ERR_STATE, "stage %d: not replicated", k_);
+    ncclResult_t r = ncclAllReduce(buf, buf, n, ncclFloat32, ncclSum, rep_, s);
+    if (r != ncclSuccess)
+      return set_error(ST_ERR_NCCL, "stage %d: ncclAllReduce (replica gradients): %s", k_, ncclGetErrorString(r));
+    return ST_OK;
+  }
+  st_status send(int kind, int64_t mb, const float* buf, size_t count, cudaStream_t s, int chan) override {
     const bool f = kind == CK_SEND_FWD;
     if (!f && kind != CK_SEND_BWD) return set_error(ST_ERR_INPUT, "nccl send: bad kind %d", kind);
-    const int peer = f ? k_ + 1 : k_ - 1;
-    if (peer < 0 || peer >= N_) return set_error(ST_ERR_STATE, "stage %d: no peer %d", k_, peer);
+    const int ps = f ? k_ + 1 : k_ - 1;
+    if (ps < 0 || ps >= N_) return set_error(ST_ERR_STATE, "stage %d: no peer %d", k_, ps);
+    const int peer = rank_of(ps, chan);
     ncclResult_t r = ncclSend(buf, count, ncclFloat32, peer, f ? fwd_ : bwd_, s);
     if (r != ncclSuccess)
       return set_error(ST_ERR_NCCL, "stage %d: ncclSend(mb %lld -> %d): %s", k_, (long long)mb, peer,
                        ncclGetErrorString(r));
     return ST_OK;
   }
-  st_status recv(int kind, int64_t mb, float* buf, size_t count, cudaStream_t s) override {
+  st_status recv(int kind, int64_t mb, float* buf, size_t count, cudaStream_t s, int chan) override {
     const bool f = kind == CK_RECV_FWD;
     if (!f && kind != CK_RECV_BWD) return set_error(ST_ERR_INPUT, "nccl recv: bad kind %d", kind);
-    const int peer = f ? k_ - 1 : k_ + 1;
-    if (peer < 0 || peer >= N_) return set_error(ST_ERR_STATE, "stage %d: no peer %d", k_, peer);
+    const int ps = f ? k_ - 1 : k_ + 1;
+    if (ps < 0 || ps >= N_) return set_error(ST_ERR_STATE, "stage %d: no peer %d", k_, ps);
+    const int peer = rank_of(ps, chan);
     ncclResult_t r = ncclRecv(buf, count, ncclFloat32, peer, f ? fwd_ : bwd_, s);
     if (r != ncclSuccess)
       return set_error(ST_ERR_NCCL, "stage %d: ncclRecv(mb %lld <- %d): %s", k_, (long long)mb, peer,
@@ -72,7 +97,8 @@ class NcclTransport final : public Transport {
   }
   st_status poll() override {
     if (aborted_) return set_error(ST_ERR_NCCL, "stage %d: communicators were aborted", k_);
-    for (ncclComm_t c : {fwd_, bwd_}) {
+    for (ncclComm_t c : {fwd_, bwd_, rep_}) {
+      if (!c) continue;
       ncclResult_t a = ncclSuccess;
       ncclResult_t r = ncclCommGetAsyncError(c, &a);
       if (r != ncclSuccess)
@@ -95,21 +121,33 @@ class NcclTransport final : public Transport {
       cudaSetDevice(dev);
       ncclCommAbort(bwd_);
     });
+    std::thread t2([this, dev] {
+      cudaSetDevice(dev);
+      if (rep_) ncclCommAbort(rep_);
+    });
     ncclCommAbort(fwd_);
     t.join();
+    t2.join();
   }
 
  private:
-  ncclComm_t fwd_, bwd_;
+  ncclComm_t fwd_, bwd_, rep_;
   int N_, k_;
+  std::vector<int> reps_, base_;
   bool aborted_ = false;
 };
 
 }  // namespace
 
-std::unique_ptr<Transport> make_nccl_transport(const uint8_t id[128], int N, int k, int device, st_status* err) {
+std::unique_ptr<Transport> make_nccl_transport(const uint8_t id[128], int N, int k, int device,
+                                               const std::vector<int>& reps, int replica, st_status* err) {
   *err = ST_OK;
-  if (N == 1) return nullptr;  // a 1-stage pipeline never communicates
+  int world = 0, rank = 0;
+  for (int s = 0; s < N; ++s) {
+    if (s == k) rank = world + replica;
+    world += reps[s];
+  }
+  if (world == 1) return nullptr;  // a 1-stage, unreplicated pipeline never communicates
   ncclUniqueId uid;
   static_assert(sizeof(uid.internal) == 128, "ncclUniqueId size");
   memcpy(uid.internal, id, 128);
@@ -117,20 +155,32 @@ std::unique_ptr<Transport> make_nccl_transport(const uint8_t id[128], int N, int
     *err = set_error(ST_ERR_CUDA, "cudaSetDevice(%d)", device);
     return nullptr;
   }
-  ncclComm_t f = nullptr, b = nullptr;
-  ncclResult_t r = ncclCommInitRank(&f, N, uid, k);
+  ncclComm_t f = nullptr, b = nullptr, rc = nullptr;
+  ncclResult_t r = ncclCommInitRank(&f, world, uid, rank);
   if (r != ncclSuccess) {
-    *err = set_error(ST_ERR_NCCL, "ncclCommInitRank(N=%d, rank=%d): %s", N, k, ncclGetErrorString(r));
+    *err = set_error(ST_ERR_NCCL, "ncclCommInitRank(world=%d, rank=%d): %s", world, rank, ncclGetErrorString(r));
     return nullptr;
   }
   // the gradient-direction communicator: same ranks, same order (collective over all stages)
-  r = ncclCommSplit(f, 0, k, &b, nullptr);
+  r = ncclCommSplit(f, 0, rank, &b, nullptr);
   if (r != ncclSuccess || !b) {
-    *err = set_error(ST_ERR_NCCL, "ncclCommSplit (gradient communicator, rank %d): %s", k, ncclGetErrorString(r));
+    *err = set_error(ST_ERR_NCCL, "ncclCommSplit (gradient communicator, rank %d): %s", rank, ncclGetErrorString(r));
     ncclCommDestroy(f);
     return nullptr;
   }
-  return std::unique_ptr<Transport>(new NcclTransport(f, b, N, k));
+  // the replicas of each replicated stage (collective over all ranks; others get none)
+  bool any_rep = false;
+  for (int s = 0; s < N; ++s) any_rep |= reps[s] > 1;
+  if (any_rep) {
+    r = ncclCommSplit(f, reps[k] > 1 ? k : NCCL_SPLIT_NOCOLOR, replica, &rc, nullptr);
+    if (r != ncclSuccess) {
+      *err = set_error(ST_ERR_NCCL, "ncclCommSplit (replica communicator, rank %d): %s", rank, ncclGetErrorString(r));
+      ncclCommDestroy(f);
+      ncclCommDestroy(b);
+      return nullptr;
+    }
+  }
+  return std::unique_ptr<Transport>(new NcclTransport(f, b, rc, N, k, reps));
 }
 
 // ------------------------------------------------------------------ LOCAL
@@ -154,15 +204,24 @@ struct Channel {
 struct LocalLink {
   int N = 0;
   std::atomic<bool> aborted{false};
-  std::vector<std::unique_ptr<Channel>> fwd, bwd;  // fwd[k]: k→k+1, bwd[k]: k+1→k
+  // fwd[k][c]: k→k+1, bwd[k][c]: k+1→k; c = replica of the replicated side of the
+  // boundary (one channel per replica; one channel when neither side is replicated)
+  std::vector<std::vector<std::unique_ptr<Channel>>> fwd, bwd;
+  std::vector<std::condition_variable*> extra_cvs;  // replica-group barriers woken by an abort
+  std::mutex extra_mu;
 };
 
-std::shared_ptr<LocalLink> make_local_link(int N) {
+std::shared_ptr<LocalLink> make_local_link(int N, const std::vector<int>& reps) {
   auto l = std::make_shared<LocalLink>();
   l->N = N;
   for (int k = 0; k + 1 < N; ++k) {
-    l->fwd.emplace_back(new Channel());
-    l->bwd.emplace_back(new Channel());
+    const int nc = std::max(reps[k], reps[k + 1]);
+    l->fwd.emplace_back();
+    l->bwd.emplace_back();
+    for (int c = 0; c < nc; ++c) {
+      l->fwd.back().emplace_back(new Channel());
+      l->bwd.back().emplace_back(new Channel());
+    }
   }
   return l;
 }
@@ -171,10 +230,13 @@ void abort_local_link(LocalLink* l) {
   if (!l) return;
   l->aborted = true;
   for (auto* v : {&l->fwd, &l->bwd})
-    for (auto& ch : *v) {
-      { std::lock_guard<std::mutex> g(ch->mu); }
-      ch->cv.notify_all();
-    }
+    for (auto& row : *v)
+      for (auto& ch : row) {
+        { std::lock_guard<std::mutex> g(ch->mu); }
+        ch->cv.notify_all();
+      }
+  std::lock_guard<std::mutex> g(l->extra_mu);
+  for (auto* cv : l->extra_cvs) cv->notify_all();
 }
 
 namespace {
@@ -189,29 +251,50 @@ class LocalTransport final : public Transport {
     for (auto& e : owned_) cudaEventDestroy(e);
   }
 
-  st_status setup(float* ring_fwd, float* ring_bwd, size_t fwd_elems, size_t bwd_elems) {
+  // replica: this context's index within its stage; rep_prev / rep_self / rep_next:
+  // replicas of stages k−1, k, k+1. A replicated context owns channel `replica` of its
+  // boundaries; an unreplicated one next to a replicated stage owns all of them. The
+  // ring of a sender with several outgoing channels is split between them.
+  st_status setup(float* ring_fwd, float* ring_bwd, size_t fwd_elems, size_t bwd_elems, int replica, int rep_prev,
+                  int rep_self, int rep_next) {
     const int N = link_->N;
     const int R = kRingSlots(N);
+    auto chans = [&](int rep_other) {
+      std::vector<int> v;
+      if (rep_self > 1) v.push_back(replica);
+      else for (int c = 0; c < rep_other; ++c) v.push_back(c);
+      return v;
+    };
     // As sender: own the ring + ready events of my outgoing channels.
-    if (k_ + 1 < N) ST_TRY(init_sender(*link_->fwd[k_], ring_fwd, fwd_elems, R));
-    if (k_ > 0) ST_TRY(init_sender(*link_->bwd[k_ - 1], ring_bwd, bwd_elems, R));
+    if (k_ + 1 < N) {
+      auto cs = chans(rep_next);
+      const size_t e = fwd_elems / cs.size();
+      for (size_t i = 0; i < cs.size(); ++i) ST_TRY(init_sender(*link_->fwd[k_][cs[i]], ring_fwd + i * e * R, e, R));
+    }
+    if (k_ > 0) {
+      auto cs = chans(rep_prev);
+      const size_t e = bwd_elems / cs.size();
+      for (size_t i = 0; i < cs.size(); ++i) ST_TRY(init_sender(*link_->bwd[k_ - 1][cs[i]], ring_bwd + i * e * R, e, R));
+    }
     // As receiver: consumed events of my incoming channels.
-    if (k_ > 0) ST_TRY(init_receiver(*link_->fwd[k_ - 1], R));
-    if (k_ + 1 < N) ST_TRY(init_receiver(*link_->bwd[k_], R));
+    if (k_ > 0)
+      for (int c : chans(rep_prev)) ST_TRY(init_receiver(*link_->fwd[k_ - 1][c], R));
+    if (k_ + 1 < N)
+      for (int c : chans(rep_next)) ST_TRY(init_receiver(*link_->bwd[k_][c], R));
     return ST_OK;
   }
 
-  st_status send(int kind, int64_t mb, const float* buf, size_t count, cudaStream_t s) override {
+  st_status send(int kind, int64_t mb, const float* buf, size_t count, cudaStream_t s, int chan) override {
     switch (kind) {
-      case CK_SEND_FWD: return do_send(*link_->fwd[k_], mb, buf, count, s);
-      case CK_SEND_BWD: return do_send(*link_->bwd[k_ - 1], mb, buf, count, s);
+      case CK_SEND_FWD: return do_send(*link_->fwd[k_][chan], mb, buf, count, s);
+      case CK_SEND_BWD: return do_send(*link_->bwd[k_ - 1][chan], mb, buf, count, s);
       default: return set_error(ST_ERR_INPUT, "local transport: bad send kind %d", kind);
     }
   }
-  st_status recv(int kind, int64_t mb, float* buf, size_t count, cudaStream_t s) override {
+  st_status recv(int kind, int64_t mb, float* buf, size_t count, cudaStream_t s, int chan) override {
     switch (kind) {
-      case CK_RECV_FWD: return do_recv(*link_->fwd[k_ - 1], mb, buf, count, s);
-      case CK_RECV_BWD: return do_recv(*link_->bwd[k_], mb, buf, count, s);
+      case CK_RECV_FWD: return do_recv(*link_->fwd[k_ - 1][chan], mb, buf, count, s);
+      case CK_RECV_BWD: return do_recv(*link_->bwd[k_][chan], mb, buf, count, s);
       default: return set_error(ST_ERR_INPUT, "local transport: bad recv kind %d", kind);
     }
   }
@@ -299,12 +382,80 @@ class LocalTransport final : public Transport {
 }  // namespace
 
 std::unique_ptr<Transport> make_local_transport(std::shared_ptr<LocalLink> link, int k, float* ring_fwd,
-                                                float* ring_bwd, size_t fwd_elems, size_t bwd_elems,
-                                                st_status* err) {
+                                                float* ring_bwd, size_t fwd_elems, size_t bwd_elems, int replica,
+                                                int rep_prev, int rep_self, int rep_next, st_status* err) {
   auto t = std::unique_ptr<LocalTransport>(new LocalTransport(std::move(link), k));
-  *err = t->setup(ring_fwd, ring_bwd, fwd_elems, bwd_elems);
+  *err = t->setup(ring_fwd, ring_bwd, fwd_elems, bwd_elems, replica, rep_prev, rep_self, rep_next);
   if (*err != ST_OK) return nullptr;
   return std::unique_ptr<Transport>(t.release());
+}
+
+// ------------------------------------------------------------------ LOCAL replica group
+// In-place all-reduce of the R co-located replicas' gradient arenas (hybrid DP × PP):
+// (1) every replica's backward finished (event + host barrier), (2) replica r sums
+// slice r of all R arenas into all of them (disjoint memory per launch, fixed order),
+// (3) every slice is summed (event + host barrier) before any replica's update reads
+// its arena. A replica's next backward, which overwrites its arena, follows its own
+// wait in (3), and the others' next reads of it follow the next (1).
+struct ReplicaGroup {
+  int R = 0;
+  std::shared_ptr<LocalLink> link;
+  std::mutex mu;
+  std::condition_variable cv;
+  int arrived = 0;
+  int64_t gen = 0;
+  std::vector<float*> G;
+  std::vector<cudaEvent_t> ev_bwd, ev_sum;
+  ~ReplicaGroup() {
+    for (auto e : ev_bwd) cudaEventDestroy(e);
+    for (auto e : ev_sum) cudaEventDestroy(e);
+  }
+  st_status barrier() {
+    std::unique_lock<std::mutex> lk(mu);
+    const int64_t my = gen;
+    if (++arrived == R) {
+      arrived = 0;
+      ++gen;
+      lk.unlock();
+      cv.notify_all();
+      return ST_OK;
+    }
+    if (!cv.wait_for(lk, std::chrono::duration<double>(kTimeoutS), [&] { return gen != my || link->aborted; }))
+      return set_error(ST_ERR_STATE, "replica group: barrier timeout");
+    if (gen == my) return set_error(ST_ERR_STATE, "local transport: a peer stage failed (replica barrier)");
+    return ST_OK;
+  }
+};
+
+std::shared_ptr<ReplicaGroup> make_replica_group(int R, std::shared_ptr<LocalLink> link) {
+  auto g = std::make_shared<ReplicaGroup>();
+  g->R = R;
+  g->link = link;
+  g->G.assign(R, nullptr);
+  g->ev_bwd.assign(R, nullptr);
+  g->ev_sum.assign(R, nullptr);
+  for (int r = 0; r < R; ++r) {
+    cudaEventCreateWithFlags(&g->ev_bwd[r], cudaEventDisableTiming);
+    cudaEventCreateWithFlags(&g->ev_sum[r], cudaEventDisableTiming);
+  }
+  std::lock_guard<std::mutex> lk(link->extra_mu);
+  link->extra_cvs.push_back(&g->cv);
+  return g;
+}
+
+st_status replica_reduce_local(ReplicaGroup* g, int replica, float* G, size_t n, cudaStream_t s) {
+  g->G[replica] = G;
+  ST_CUDA_TRY(cudaEventRecord(g->ev_bwd[replica], s));
+  ST_TRY(g->barrier());
+  for (int j = 0; j < g->R; ++j)
+    if (j != replica) ST_CUDA_TRY(cudaStreamWaitEvent(s, g->ev_bwd[j], 0));
+  const size_t b = n * (size_t)replica / g->R, e = n * (size_t)(replica + 1) / g->R;
+  ST_TRY(launch_replica_sum(g->G.data(), g->R, b, e, s));
+  ST_CUDA_TRY(cudaEventRecord(g->ev_sum[replica], s));
+  ST_TRY(g->barrier());
+  for (int j = 0; j < g->R; ++j)
+    if (j != replica) ST_CUDA_TRY(cudaStreamWaitEvent(s, g->ev_sum[j], 0));
+  return ST_OK;
 }
 
 }  // namespace st

@@ -33,8 +33,13 @@ class Stage:
                  pred: int = L.ST_PRED_SPECTRAIN, momentum: int = L.ST_MOMENTUM_EMA, gemm: int = L.ST_GEMM_FP32X3,
                  transport: int = L.ST_TRANSPORT_NCCL, device: int = 0, max_minibatches: int = 256,
                  nccl_id: Optional[bytes] = None, stream: Optional[torch.cuda.Stream] = None, seq_len: int = 1,
-                 comm_streams: Optional[Tuple[torch.cuda.Stream, torch.cuda.Stream]] = None):
+                 comm_streams: Optional[Tuple[torch.cuda.Stream, torch.cuda.Stream]] = None,
+                 replicas: Optional[Sequence[int]] = None, replica: int = 0):
+        """replicas / replica: hybrid data × pipeline parallelism (st_config.replicas; `batch`
+        stays the global mini-batch, a replica of a replicated stage computes its row slice)."""
         self.layers = [tuple(int(v) for v in l) for l in layers]
+        self.replicas = list(replicas) if replicas is not None else None
+        self.replica = replica
         self.cuts = list(cuts)
         self.k = stage
         self.N = len(cuts) + 1
@@ -42,7 +47,8 @@ class Stage:
         self.device = torch.device("cuda", device)
         self.seq_len = seq_len
         self.cfg, self._keep = L.make_config(self.layers, self.cuts, stage, batch, lr, gamma, pred, momentum, gemm,
-                                             transport, device, max_minibatches, nccl_id, seq_len)
+                                             transport, device, max_minibatches, nccl_id, seq_len, replicas,
+                                             replica)
         self.sizes = L.query_sizes(self.cfg)
         self.stream = stream if stream is not None else torch.cuda.Stream(device=self.device)
         # activation / gradient transfer streams (None: the library creates its own)
@@ -186,6 +192,42 @@ class Stage:
 
     def kernel_launches(self) -> int:
         return int(lib.st_kernel_launches(self.ctx))
+
+
+def p2p_export(stage: Stage) -> bytes:
+    """The stage's P2P descriptor (st_p2p_export): 1024 opaque bytes to hand to its
+    neighbours (same process, or another process through torch.distributed)."""
+    buf = ctypes.create_string_buffer(L.P2P_DESC_BYTES)
+    check(lib.st_p2p_export(stage.ctx, buf))
+    return buf.raw
+
+
+def p2p_connect(stage: Stage, prev: Optional[bytes], nxt: Optional[bytes]) -> None:
+    """Map the neighbours' buffers (st_p2p_connect): prev = stage k−1's descriptor
+    (None for stage 0), nxt = stage k+1's (None for the last stage)."""
+    def b(d):
+        return None if d is None else ctypes.create_string_buffer(bytes(d), L.P2P_DESC_BYTES)
+    check(lib.st_p2p_connect(stage.ctx, b(prev), b(nxt)))
+
+
+def connect_p2p_local(stages: Sequence[Stage]) -> None:
+    """P2P transport between the stage contexts of THIS process (run them with
+    run_group): the producing kernels write each other's buffers directly."""
+    descs = [p2p_export(s) for s in stages]
+    for k, s in enumerate(stages):
+        p2p_connect(s, descs[k - 1] if k > 0 else None, descs[k + 1] if k + 1 < len(stages) else None)
+
+
+def connect_p2p(stage: Stage, group=None) -> None:
+    """P2P transport across processes (one stage per rank, rank = stage index): the
+    descriptors are all-gathered over `group` (torch.distributed, any backend) and the
+    neighbours' buffers opened with CUDA IPC (NVLink / NVSwitch peer memory, or a GPU
+    shared by several processes)."""
+    import torch.distributed as dist
+    descs = [None] * dist.get_world_size(group)
+    dist.all_gather_object(descs, p2p_export(stage), group=group)
+    k, n = stage.k, len(descs)
+    p2p_connect(stage, descs[k - 1] if k > 0 else None, descs[k + 1] if k + 1 < n else None)
 
 
 def connect_local(stages: Sequence[Stage]) -> None:

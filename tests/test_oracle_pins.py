@@ -741,3 +741,37 @@ def test_data_parallel_equals_global_batch_sgd():
     ref = O.run(model, sd.widen(w0), X.astype(np.float64), Y, 0.05, 0.9)
     np.testing.assert_allclose(W, np.concatenate(ref.W), rtol=0, atol=1e-13)
     np.testing.assert_allclose(losses, ref.losses, rtol=1e-13)
+
+
+def test_hybrid_replica_rows_sum_to_the_stage_gradient():
+    """Reading D25 (hybrid DP × PP): a replicated stage k < N−1
+    splits each mini-batch by rows. Its upstream gradient already carries the 1/B of the
+    GLOBAL batch-mean loss (computed once, by the unreplicated last stage), so the
+    replicas' gradients must be SUMMED — unlike D23's data parallelism, where each shard
+    computes its own batch mean and the shards are averaged. With the oracle's building
+    blocks on a dense + conv stage: the row slices' outputs and input gradients
+    concatenate to the whole batch's, and their gradients sum to the whole batch's
+    gradient (so every other stage sees identical messages and the update is identical:
+    the hybrid pipeline computes the unreplicated one). Averaging is off by 1/R."""
+    rng = np.random.default_rng(31)
+    for model, width_in in ((sd.mlp([24, 16, 12, 5], cuts=[2]), 24),
+                            (sd.vgg(cfg=(4, "M"), fc=(6,), classes=3, hw=4, in_ch=2, cuts=[2]), 4 * 4 * 2)):
+        layers = model.stage_layers(0)
+        w = np.concatenate(sd.widen(sd.parity_inputs(model, 1, 8, seed=4)[0][:1]))
+        B, R = 8, 4
+        A = rng.standard_normal((B, width_in))
+        out, stash = O.stage_forward(layers, w, A)
+        dOut = rng.standard_normal(out.shape) / B  # the last stage's 1/B (global batch mean)
+        g, dA = O.stage_backward(layers, w, stash, dOut)
+        gs, outs, dAs = [], [], []
+        for r in range(R):
+            rows = slice(r * B // R, (r + 1) * B // R)
+            o_r, st_r = O.stage_forward(layers, w, A[rows])
+            g_r, dA_r = O.stage_backward(layers, w, st_r, dOut[rows])
+            gs.append(g_r)
+            outs.append(o_r)
+            dAs.append(dA_r)
+        np.testing.assert_allclose(np.concatenate(outs), out, rtol=1e-13, atol=1e-15)
+        np.testing.assert_allclose(np.concatenate(dAs), dA, rtol=1e-12, atol=1e-15)
+        np.testing.assert_allclose(np.sum(gs, axis=0), g, rtol=1e-12, atol=1e-15)
+        assert np.linalg.norm(np.mean(gs, axis=0) - g) > 0.5 * np.linalg.norm(g)  # averaging would be wrong
