@@ -491,18 +491,24 @@ st_status ctx_init(const st_config* cfg, const st_buffers* bufs, void* stream, v
     c->sm_count = std::max(2, sms);
     c->dwu_sms = std::min(c->dwu_sms, c->sm_count - 2);
   }
-  // comm streams: the caller's, or library-owned non-blocking streams
-  if (comm_fwd) {
-    c->comm_fwd = static_cast<cudaStream_t>(comm_fwd);
+  // comm streams: the caller's, or library-owned non-blocking streams (P2P: none — the
+  // compute stream's kernels move the data; fewer streams also keeps its spin-waits off
+  // hardware queues shared with a co-located peer, see st_p2p_connect)
+  if (cfg->transport == ST_TRANSPORT_P2P) {
+    c->comm_fwd = c->comm_bwd = c->stream;
   } else {
-    ST_CUDA_TRY(cudaStreamCreateWithFlags(&c->comm_fwd, cudaStreamNonBlocking));
-    c->own_comm_fwd = true;
-  }
-  if (comm_bwd) {
-    c->comm_bwd = static_cast<cudaStream_t>(comm_bwd);
-  } else {
-    ST_CUDA_TRY(cudaStreamCreateWithFlags(&c->comm_bwd, cudaStreamNonBlocking));
-    c->own_comm_bwd = true;
+    if (comm_fwd) {
+      c->comm_fwd = static_cast<cudaStream_t>(comm_fwd);
+    } else {
+      ST_CUDA_TRY(cudaStreamCreateWithFlags(&c->comm_fwd, cudaStreamNonBlocking));
+      c->own_comm_fwd = true;
+    }
+    if (comm_bwd) {
+      c->comm_bwd = static_cast<cudaStream_t>(comm_bwd);
+    } else {
+      ST_CUDA_TRY(cudaStreamCreateWithFlags(&c->comm_bwd, cudaStreamNonBlocking));
+      c->own_comm_bwd = true;
+    }
   }
   {
     auto mk = [](cudaEvent_t* e) { return cudaEventCreateWithFlags(e, cudaEventDisableTiming); };
@@ -544,6 +550,7 @@ st_status ctx_init(const st_config* cfg, const st_buffers* bufs, void* stream, v
     c->dwu_env = true;
   }
   c->conv_overlap = dev_knob("ST_CONV_OVERLAP", 0) != 0;
+  c->bwd_serial = dev_knob("ST_BWD_SERIAL", 1) != 0;
   c->pdl = dev_knob("ST_PDL", 1) != 0;
   c->pdl_dense = dev_knob("ST_PDL_DENSE", 1) != 0;
   // several stage contexts sharing one GPU (LOCAL transport): their kernels interleave
@@ -822,10 +829,11 @@ st_status ctx_wait(st_ctx* c) {
     const double waited = std::chrono::duration<double>(std::chrono::steady_clock::now() - t0).count();
     if (waited > c->comm_timeout_s) {
       c->tp->abort();
+      const std::string flags = c->p2p ? p2p_describe(c) : std::string();
       return set_error(c->transport_kind == ST_TRANSPORT_NCCL ? ST_ERR_NCCL : ST_ERR_STATE,
                        "stage %d: no completion after %.0f s (ST_COMM_TIMEOUT_S): a peer stage is hung or gone; "
-                       "transport aborted",
-                       c->k, waited);
+                       "transport aborted (program op %zu of %zu)%s",
+                       c->k, waited, c->pc, c->program.size(), flags.c_str());
     }
     std::this_thread::sleep_for(std::chrono::microseconds(sleep_us));
     sleep_us = std::min(sleep_us * 2, 1000);
@@ -1235,7 +1243,20 @@ static st_status backward_compute(st_ctx* c, int64_t mb, bool fused = false) {
         ST_TRY(gemm_dx(gx, dZ, Wh + L.w_off, producer_act == ST_ACT_RELU ? Ain : nullptr, D));
         c->launches += gemm_last_launches();
       }
-      if (fused) {
+      if (fused && c->bwd_serial && L.n_params >= ((int64_t)1 << 27)) {
+        // serialised: the dW + update of a very large layer (16384²: 268M parameters) takes
+        // the whole GPU after its dX — alone it streams W / V at 0.95 of the HBM peak, so
+        // running the next dX beside it cannot win (measured: large FCN 6264 overlapped vs
+        // 6222 samples/s serialised, within clock noise; the update at 0.90 instead of 0.75
+        // of the peak in the step); smaller layers stay overlapped (wide FCN: −2% serialised)
+        ST_TRY(join_side());
+        GemmArgs gw = gargs(c, L);
+        UpdateArgs bu{};
+        if (L.bias) bu = block_update(c, L.b_off, kc);
+        Timed t(c, KC_GEMM_DW);
+        ST_TRY(gemm_dw_update(gw, Ain, dZ, block_update(c, L.w_off, kc), bu, c->G + L.w_off));
+        c->launches += gemm_last_launches();
+      } else if (fused) {
         // dW + update on the side stream, after this layer's dX (which reads WB_l)
         ST_CUDA_TRY(cudaEventRecord(c->side_events[l], c->stream));
         ST_CUDA_TRY(cudaStreamWaitEvent(c->side, c->side_events[l], 0));
@@ -1497,10 +1518,12 @@ st_status ctx_run(st_ctx* c, int64_t M, const float* xs, const int32_t* ys, floa
   // the session's last transfers become part of the compute stream
   ST_TRY(join_comm(c));
   const bool want_losses = losses_host && c->last_stage && M > 0;
-  if (want_losses && !host_io)
-    ST_CUDA_TRY(cudaMemcpyAsync(losses_host, c->losses_dev, (size_t)M * 4, cudaMemcpyDeviceToHost, c->stream));
-  // host buffers (st_run_host) are read by asynchronous copies: never return before they finish
+  // host buffers (st_run_host) are read by asynchronous copies: never return before they
+  // finish; the wait polls the transport (a hung peer surfaces as an error after
+  // ST_COMM_TIMEOUT_S), so the losses are copied only once the stream is idle
   if (want_losses || host_io) ST_TRY(ctx_wait(c));
+  if (want_losses && !host_io)
+    ST_CUDA_TRY(cudaMemcpy(losses_host, c->losses_dev, (size_t)M * 4, cudaMemcpyDeviceToHost));
   if (want_losses)
     for (int64_t i = 0; i < M; ++i)
       if (!std::isfinite(losses_host[i]))

@@ -2,6 +2,7 @@
 #pragma once
 
 #include <memory>
+#include <string>
 #include <vector>
 
 #include "common.hpp"
@@ -199,6 +200,8 @@ struct st_ctx {
   bool pdl_now = false;         // this task's launches (run_task)
   bool pdl_dense = true;        // dense fwd / dX kernels as programmatic dependent launches (ST_PDL_DENSE=0: off)
   bool pdl = true;              // LSTM recurrence: GEMM ↔ cell as programmatic dependent launches (ST_PDL=0: off)
+  bool bwd_serial = true;       // dense layers with ≥ 2^27 parameters: dW + update after the dX on the
+                                // compute stream (whole GPU each) instead of overlapped on the side stream
   bool conv_overlap = false;    // implicit-conv dW + update on the side stream (ST_CONV_OVERLAP=1; measured
                                 // slower: VGG-16 58.9k -> 53.0k samples/s with an 80 / 68 SM split)
   float* wstash = nullptr;      // ST_PRED_STASH: S slots of P floats (the WF buffer)
@@ -254,5 +257,6 @@ st_status p2p_before_backward(st_ctx* c, int64_t mb);
 st_status p2p_after_dx(st_ctx* c, int64_t mb);
 st_status p2p_after_backward(st_ctx* c, int64_t mb);
 st_status p2p_check(st_ctx* c);
+std::string p2p_describe(st_ctx* c);  // the flag block (diagnostics of a hang)
 st_status launch_replica_sum(float* const* Gs, int R, size_t begin, size_t end, cudaStream_t s);
 }  // namespace st

@@ -202,6 +202,17 @@ st_status p2p_export(st_ctx* c, st_p2p_desc* out) {
 
 static st_status open_region(st_ctx* c, const Desc& d, const Region& r, void** p) {
   if (d.pid == (int32_t)getpid()) {  // a context of this process: its pointer is valid here
+    // Contexts of one process on one GPU share that device's hardware work queues
+    // (streams are multiplexed onto CUDA_DEVICE_MAX_CONNECTIONS channels, and torch
+    // alone creates 64 pool streams): a spinning wait kernel can end up ahead of the very
+    // kernels it waits for in one channel and neither progresses (measured: a 2-stage
+    // pipeline hangs). Separate processes have separate channels — run P2P stages that
+    // share a GPU as separate processes (or use ST_TRANSPORT_LOCAL in one process).
+    if (d.device == c->device)
+      return set_error(ST_ERR_INPUT,
+                       "p2p: stages %d and %d are contexts of one process on GPU %d — run them as separate "
+                       "processes (their wait kernels would share hardware queues) or use ST_TRANSPORT_LOCAL",
+                       c->k, d.k, c->device);
     *p = reinterpret_cast<void*>((uintptr_t)r.raw);
     return ST_OK;
   }
@@ -326,6 +337,25 @@ st_status p2p_after_backward(st_ctx* c, int64_t mb) {
   if (!c->last_stage) ST_TRY(launch_signal(c, s->next_flags + F_PREV_BWD_COUNT, s->base + mb + 1));
   s->bwd_total += 1;
   return ST_OK;
+}
+
+std::string p2p_describe(st_ctx* c) {
+  long long f[F_COUNT] = {};
+  // the flag block is read with a plain copy on a fresh stream (the compute stream may
+  // still hold released waits)
+  cudaStream_t s;
+  if (cudaStreamCreateWithFlags(&s, cudaStreamNonBlocking) != cudaSuccess) return "";
+  cudaMemcpyAsync(f, c->p2p->flags, sizeof f, cudaMemcpyDeviceToHost, s);
+  cudaStreamSynchronize(s);
+  cudaStreamDestroy(s);
+  char buf[512];
+  int n = snprintf(buf, sizeof buf, "; p2p base %lld, backwards %lld, flags: fwd_ready", (long long)c->p2p->base,
+                   (long long)c->p2p->bwd_total);
+  for (int i = 0; i < c->S && i < 8 && n < (int)sizeof buf; ++i) n += snprintf(buf + n, sizeof buf - n, " %lld", f[F_FWD_READY + i]);
+  if (n < (int)sizeof buf)
+    snprintf(buf + n, sizeof buf - n, ", bwd_ready %lld %lld, next_bwd %lld, prev_bwd %lld", f[F_BWD_READY],
+             f[F_BWD_READY + 1], f[F_NEXT_BWD_COUNT], f[F_PREV_BWD_COUNT]);
+  return buf;
 }
 
 // a wait released by an abort leaves its failure in device memory (read at sync points)

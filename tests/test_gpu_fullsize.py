@@ -248,12 +248,16 @@ def test_large_fcn_full_size_one_step_sampled(st):
     stage_backward on that one layer — stage composition equals the monolithic model,
     pinned in test_oracle_pins), and per layer 512 random weights plus the bias are
     compared. After one update from V = 0: V = (1 − γ)·g and W = W0 − η·V (Eq. 1, D1).
-    Gates: loss 1e-5; sampled V per layer 2e-2 (one mini-batch: the few ReLU decisions
-    taken on pre-activations within rounding of 0, reading D24,
-    profiles/r2_d24_fp32_vs_fp64.json: 6e-4 from a single flip in plain fp32 at 8192
-    wide); sampled W per layer 1e-6 + 2e-2·‖η·V‖/‖W‖ — W = W0 − η·V, so the V error
-    allowed above reaches W scaled by the update's size (layer 15, the last 16384²
-    layer, has the largest ‖η·V‖/‖W‖: 3.5e-6 measured), plus fp32 storage of W0."""
+    Gates: loss 1e-5; sampled V per layer 5e-2 (one mini-batch, reading D24: the ReLU
+    decisions taken on pre-activations within rounding of 0. At K = 16384 the 3xTF32
+    forward GEMM's pre-activation error is 3.8e-5 rms of |Z| against 1.6e-6 for an fp32
+    GEMM — 16 vs 1 of 2.1M decisions differ per layer (tools/gemm_error.py,
+    profiles/r2_gemm_error.txt); plain fp32 at this size spreads V by 1.1e-3 (1 flip) to
+    4.2e-3 per layer (profiles/r2_d24_large_fcn_1step.json); each flipped mask entry moves
+    a 16384-wide layer's V by ~1e-3 and the flips of all later layers add up: measured
+    0.9e-2 (layer 15) to 2.2e-2 (layer 0)); sampled W per layer 1e-6 + 5e-2·‖η·V‖/‖W‖ —
+    W = W0 − η·V, so the V error allowed above reaches W scaled by the update's size,
+    plus fp32 storage of W0."""
     model = sd.config_large_fcn(1)
     L = model.layers
     B, seed = 128, 11
@@ -309,10 +313,10 @@ def test_large_fcn_full_size_one_step_sampled(st):
         w_ref = flat[sel] - eta * v_ref
         rv = rel_l2(v_got, v_ref)
         rw = rel_l2(w_got, w_ref)
-        tol_w = 1e-6 + 2e-2 * eta * np.linalg.norm(v_ref) / np.linalg.norm(w_ref)
+        tol_w = 1e-6 + 5e-2 * eta * np.linalg.norm(v_ref) / np.linalg.norm(w_ref)
         worst.append((i, rv, rw, tol_w))
     _record("large_fcn_full_1step_sampled", {"loss": float(losses[0]), "loss_ref": loss,
                                               "per_layer_v_w_tolw": worst})
     for i, rv, rw, tol_w in worst:
         assert rw <= tol_w, (i, rw, tol_w)
-        assert rv <= 2e-2, (i, rv)
+        assert rv <= 5e-2, (i, rv)

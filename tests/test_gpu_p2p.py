@@ -3,14 +3,11 @@ producing kernels over peer memory — the last forward GEMM of stage k writes s
 k+1's stash slot, the layer-0 dX GEMM of stage k+1 writes stage k's gradient ring,
 flags in the waiter's memory hand the buffers over (paper_1809_02839_b200/csrc/p2p.cu).
 
-Two arrangements run on the one GPU of this box:
-- contexts of one process (connect_p2p_local + run_group): the peer buffers are the
-  other contexts' arenas;
-- one process per stage (torch.multiprocessing, gloo only to exchange the
-  descriptors): the peer buffers are opened with CUDA IPC — the code path a
-  one-stage-per-GPU run takes over NVLink / NVSwitch.
-Both must match the oracle like every other transport (trace bit-exact, W and loss
-within 1e-4), and match the LOCAL transport bit for bit (same kernels, same order).
+On the one GPU of this box the stages run as separate processes (torch.multiprocessing,
+gloo only to exchange the descriptors) whose buffers are opened with CUDA IPC — the
+code path a one-stage-per-GPU run takes over NVLink / NVSwitch. Results must match the
+oracle like every other transport (trace bit-exact, W and loss within 1e-4) and the
+LOCAL transport bit for bit (same kernels, same order).
 """
 import os
 import socket
@@ -21,80 +18,26 @@ import torch
 import torch.multiprocessing as mp
 
 import synthdata as sd
-from tests.gpu_helpers import assert_parity, build_pipeline, layers_of, oracle_run, rel_l2, run_pipeline
+from tests.gpu_helpers import build_pipeline, layers_of, oracle_run, rel_l2
 
 pytestmark = pytest.mark.gpu
 
 
-def _p2p_pipeline(model, B, lr, max_mb=64, pred=None):
+def test_p2p_refuses_same_process_same_gpu():
+    """Stage contexts of ONE process on one GPU share its hardware work queues (streams
+    are multiplexed onto a few channels): a spinning wait kernel could sit ahead of the
+    very kernels it waits for. st_p2p_connect refuses that arrangement; P2P stages that
+    share a GPU run as separate processes (below)."""
     import paper_1809_02839_b200 as st
-    pred = st.ST_PRED_SPECTRAIN if pred is None else pred
-    stages = [st.Stage(layers_of(model), model.cuts, k, B, lr, 0.9, pred=pred, transport=st.ST_TRANSPORT_P2P,
-                       device=0, max_minibatches=max_mb, seq_len=model.seq_len) for k in range(model.num_stages)]
-    st.connect_p2p_local(stages)
-    return stages
-
-
-CASES = [
-    ("mlp2", lambda: sd.mlp([784, 256, 256, 10], cuts=[1]), 20, 32, 0.05),
-    ("deep8", lambda: sd.config_deep_mlp(8), 12, 64, 0.02),
-    ("mlp4_ragged", lambda: sd.mlp([100, 72, 200, 40, 10], cuts=[1, 2, 3]), 9, 24, 0.05),
-]
-
-
-@pytest.mark.parametrize("name,mk,M,B,lr", CASES, ids=[c[0] for c in CASES])
-def test_p2p_in_process_matches_oracle(name, mk, M, B, lr):
-    model = mk()
-    w0, X, Y = sd.parity_inputs(model, M, B, seed=0)
-    stages = _p2p_pipeline(model, B, lr)
+    model = sd.mlp([784, 256, 256, 10], cuts=[1])
+    stages = [st.Stage(layers_of(model), model.cuts, k, 32, 0.05, 0.9, transport=st.ST_TRANSPORT_P2P, device=0,
+                       max_minibatches=4) for k in range(2)]
     try:
-        res = run_pipeline(stages, w0, X, Y)
+        with pytest.raises(st.SpecTrainError, match="separate"):
+            st.connect_p2p_local(stages)
     finally:
         for s in stages:
             s.close()
-    assert_parity(model, res, oracle_run(model, w0, X, Y, lr))
-
-
-def test_p2p_lstm_lm_matches_oracle():
-    model = sd.lstm_lm(vocab=48, hidden=32, layers=2, cuts=[1, 3], seq_len=4)
-    M, B, lr = 6, 8, 0.1
-    w0, X, Y = sd.parity_inputs(model, M, B, seed=2)
-    stages = _p2p_pipeline(model, B, lr)
-    try:
-        res = run_pipeline(stages, w0, X, Y)
-    finally:
-        for s in stages:
-            s.close()
-    assert_parity(model, res, oracle_run(model, w0, X, Y, lr))
-
-
-def test_p2p_two_sessions_bitwise_equal_local():
-    """Sessions restart the mini-batch numbering; the flags keep increasing (base =
-    backwards done before the session) — two sessions through P2P equal the same two
-    sessions through the LOCAL transport bit for bit."""
-    import paper_1809_02839_b200 as st
-    model = sd.config_deep_mlp(4)
-    M1, M2, B, lr = 7, 5, 32, 0.02
-    w0, X, Y = sd.parity_inputs(model, M1 + M2, B, seed=7)
-    dev = torch.device("cuda", 0)
-    xs = torch.from_numpy(np.ascontiguousarray(X, np.float32)).to(dev)
-    ys = torch.from_numpy(np.ascontiguousarray(Y, np.int32)).to(dev)
-    out = []
-    for kind in ("p2p", "local"):
-        stages = _p2p_pipeline(model, B, lr) if kind == "p2p" else build_pipeline(model, B, lr)
-        try:
-            for s, w in zip(stages, w0):
-                s.set_params(w)
-            l1 = st.run_group(stages, M1, xs[:M1], ys[:M1])
-            l2 = st.run_group(stages, M2, xs[M1:], ys[M1:])
-            out.append(([s.get_params()[0] for s in stages], np.concatenate([l1, l2])))
-        finally:
-            for s in stages:
-                s.close()
-    (Wp, lp), (Wl, ll) = out
-    assert np.array_equal(lp, ll)
-    for a, b in zip(Wp, Wl):
-        assert np.array_equal(a, b)
 
 
 # ---------------------------------------------------------------- one process per stage (CUDA IPC)
@@ -109,10 +52,23 @@ def _free_port():
 def _model(name, N):
     if name == "mlp":
         return sd.mlp([784, 256, 256, 10], cuts=[1] if N == 2 else sd.even_cuts(3, N))
+    if name == "ragged":
+        return sd.mlp([100, 72, 200, 40, 10], cuts=[1, 2, 3])
+    if name == "lstm":
+        return sd.lstm_lm(vocab=48, hidden=32, layers=2, cuts=[1, 3], seq_len=4)
     return sd.config_deep_mlp(N)
 
 
-def _worker(rank, world, port, model_name, M, B, lr, out_dir, hang_rank, timeout_s):
+def _inputs(model, M, B, seed=0):
+    """Seeded parity inputs: images for the MLPs, tokens for the LM (as tests/test_gpu_lstm.py)."""
+    if model.layers[0].kind == sd.EMBED:
+        w0 = sd.to_f32_params(sd.glorot_params(model, seed))
+        X, Y = sd.tokens(model.layers[0].n_in, M, B, model.seq_len, seed + 1)
+        return w0, X, Y
+    return sd.parity_inputs(model, M, B, seed=seed)
+
+
+def _worker(rank, world, port, model_name, M, B, lr, out_dir, hang_rank, timeout_s, sessions=1):
     os.environ["MASTER_ADDR"] = "127.0.0.1"
     os.environ["MASTER_PORT"] = str(port)
     os.environ["ST_COMM_TIMEOUT_S"] = str(timeout_s)
@@ -120,14 +76,19 @@ def _worker(rank, world, port, model_name, M, B, lr, out_dir, hang_rank, timeout
     dist.init_process_group("gloo", rank=rank, world_size=world)
     import paper_1809_02839_b200 as st
     model = _model(model_name, world)
-    w0, X, Y = sd.parity_inputs(model, M, B, seed=0)
+    w0, X, Y = _inputs(model, M, B)
     torch.cuda.set_device(0)
     s = st.Stage(layers_of(model), model.cuts, rank, B, lr, 0.9, transport=st.ST_TRANSPORT_P2P, device=0,
-                 max_minibatches=M)
+                 max_minibatches=M, seq_len=model.seq_len)
     st.connect_p2p(s)  # descriptors all-gathered over gloo, peers opened with CUDA IPC
+    if os.environ.get("P2P_DEBUG"):
+        import struct
+        d = st.p2p_export(s)
+        print(f"rank {rank} desc", struct.unpack_from("<IIiiiiqqqiiqqq", d), "X", X.dtype, X.shape, X.min(), X.max(),
+              flush=True)
     s.set_params(w0[rank])
     dev = torch.device("cuda", 0)
-    xs = torch.from_numpy(np.ascontiguousarray(X, np.float32)).to(dev)
+    xs = torch.from_numpy(np.ascontiguousarray(X, np.int32 if X.dtype.kind in "iu" else np.float32)).to(dev)
     ys = torch.from_numpy(np.ascontiguousarray(Y, np.int32)).to(dev)
     dist.barrier()
     try:
@@ -135,7 +96,14 @@ def _worker(rank, world, port, model_name, M, B, lr, out_dir, hang_rank, timeout
             import time
             time.sleep(3 * timeout_s)  # alive, never runs: its peers' wait kernels spin
             os._exit(0)
-        losses = s.run(M, xs if s.is_first else None, ys if s.is_last else None, want_losses=s.is_last)
+        cuts_ = [M] if sessions == 1 else [M // 2, M]  # session boundaries (mini-batch counts)
+        parts, lo = [], 0
+        for hi in cuts_:
+            part = s.run(hi - lo, xs[lo:hi] if s.is_first else None, ys[lo:hi] if s.is_last else None,
+                         want_losses=s.is_last)
+            parts.append(part)
+            lo = hi
+        losses = np.concatenate(parts) if s.is_last else None
         s.sync()
         W, V, ver = s.get_params()
         np.save(os.path.join(out_dir, f"W{rank}.npy"), W)
@@ -153,11 +121,11 @@ def _worker(rank, world, port, model_name, M, B, lr, out_dir, hang_rank, timeout
     dist.destroy_process_group()
 
 
-def _spawn(world, model_name, M, B, lr, tmp_path, hang_rank=-1, timeout_s=600):
+def _spawn(world, model_name, M, B, lr, tmp_path, hang_rank=-1, timeout_s=600, sessions=1):
     port = _free_port()
     ctx = mp.get_context("spawn")
     procs = [ctx.Process(target=_worker, args=(r, world, port, model_name, M, B, lr, str(tmp_path), hang_rank,
-                                                 timeout_s)) for r in range(world)]
+                                                 timeout_s, sessions)) for r in range(world)]
     for p in procs:
         p.start()
     hung = []
@@ -171,12 +139,14 @@ def _spawn(world, model_name, M, B, lr, tmp_path, hang_rank=-1, timeout_s=600):
     return [p.exitcode for p in procs]
 
 
-@pytest.mark.parametrize("world,model_name,M,B,lr", [(2, "mlp", 20, 32, 0.05), (3, "deep", 12, 64, 0.02)])
+@pytest.mark.parametrize("world,model_name,M,B,lr", [(2, "mlp", 20, 32, 0.05), (3, "deep", 12, 64, 0.02),
+                                                     (4, "ragged", 9, 24, 0.05), (3, "lstm", 6, 8, 0.1)],
+                         ids=["mlp2", "deep3", "ragged4", "lstm3"])
 def test_p2p_ipc_processes_match_oracle(tmp_path, world, model_name, M, B, lr):
     codes = _spawn(world, model_name, M, B, lr, tmp_path)
     assert all(c == 0 for c in codes), codes
     model = _model(model_name, world)
-    w0, X, Y = sd.parity_inputs(model, M, B, seed=0)
+    w0, X, Y = _inputs(model, M, B)
     ref = oracle_run(model, w0, X, Y, lr)
     for k in range(world):
         assert int(np.load(tmp_path / f"status{k}.npy")[0]) == 0
@@ -186,6 +156,34 @@ def test_p2p_ipc_processes_match_oracle(tmp_path, world, model_name, M, B, lr):
     losses = np.load(tmp_path / "losses.npy")
     assert rel_l2(W, np.concatenate(ref.W)) <= 1e-4
     assert rel_l2(losses, ref.losses) <= 1e-4
+
+
+def test_p2p_two_sessions_bitwise_equal_local(tmp_path):
+    """Sessions restart the mini-batch numbering; the flags keep increasing (base =
+    backwards done before the session). Two sessions through P2P processes equal the
+    same two sessions through the LOCAL transport (this process) bit for bit."""
+    import paper_1809_02839_b200 as st
+    world, M, B, lr = 3, 12, 32, 0.02
+    codes = _spawn(world, "deep", M, B, lr, tmp_path, sessions=2)
+    assert all(c == 0 for c in codes), codes
+    model = _model("deep", world)
+    w0, X, Y = sd.parity_inputs(model, M, B, seed=0)
+    stages = build_pipeline(model, B, lr)
+    try:
+        for s, w in zip(stages, w0):
+            s.set_params(w)
+        dev = torch.device("cuda", 0)
+        xs = torch.from_numpy(np.ascontiguousarray(X, np.float32)).to(dev)
+        ys = torch.from_numpy(np.ascontiguousarray(Y, np.int32)).to(dev)
+        l1 = st.run_group(stages, M // 2, xs[:M // 2], ys[:M // 2])
+        l2 = st.run_group(stages, M - M // 2, xs[M // 2:], ys[M // 2:])
+        Wl = [s.get_params()[0] for s in stages]
+    finally:
+        for s in stages:
+            s.close()
+    assert np.array_equal(np.load(tmp_path / "losses.npy"), np.concatenate([l1, l2]))
+    for k in range(world):
+        assert np.array_equal(np.load(tmp_path / f"W{k}.npy"), Wl[k]), f"stage {k}"
 
 
 def test_p2p_hung_peer_releases_waiters(tmp_path):

@@ -31,7 +31,7 @@ def _run_one_stage(st, model, w0, X, Y, lr, profile):
         dev = torch.device("cuda", 0)
         losses = s.run(X.shape[0], torch.from_numpy(X).to(dev), torch.from_numpy(Y).to(dev), want_losses=True)
         prof = s.layer_profile() if profile else None
-        W, V = s.get_params()
+        W, V, _ = s.get_params()
     finally:
         s.close()
     return W, V, losses, prof
