@@ -57,6 +57,8 @@ def parse():
     p.add_argument("--partition", default="fixed", choices=["fixed", "auto", "profiled"],
                    help="fixed: the BJ / SURVEY §8(d) stage cuts; auto: st_partition over per-layer roofline "
                         "times; profiled: st_partition over per-layer times measured on this GPU (NEXT-4)")
+    p.add_argument("--graph", default="on", choices=["on", "off"],
+                   help="on (default): every st_run session captured into one CUDA graph (st_set_graph_mode; contexts linked with st_connect_local stay eager)")
     p.add_argument("--parallel", default="pp", choices=["pp", "dp"],
                    help="pp: the SpecTrain pipeline (default); dp: the data-parallel comparator (NEXT-1)")
     return p.parse_args()
@@ -606,6 +608,9 @@ def run_ours(args):
                      for k in range(S)]
         st.connect_local(my_stages)
 
+    if args.graph == "on":
+        for s in my_stages:
+            s.set_graph_mode(True)
     # parameters: Glorot on device (bench-only, SURVEY §8(d) seeds), labels uniform
     g = torch.Generator(device=dev)
     g.manual_seed(1234 + rank)
@@ -812,7 +817,7 @@ def run_ours(args):
             "config": {"workload": wname, "stages": S, "batch": B, "seq_len": T, "gemm": args.gemm, "pred": args.pred,
                        "cuts": list(model.cuts), "partition": args.partition,
                        **({"layer_cost_us": layer_cost_us} if layer_cost_us else {}),
-                       "parallelism": f"pp{S}", "l2": "no flush: per-step working set (weights) >> 126 MB L2",
+                       "parallelism": f"pp{S}", "cuda_graph": args.graph == "on", "l2": "no flush: per-step working set (weights) >> 126 MB L2",
                        "session": "one 1F1B session of warmup + steps mini-batches; timed window = CUDA events "
                                   "after stage 0's B(warmup-1) and B(warmup+steps-1) (P:415 steady state)"},
             "roofline": roofline_key,

@@ -123,7 +123,10 @@ enum { ST_LOSS_SOFTMAX_CE = 0 };
  * process); completion is handed over by flags in the waiter's memory (system-scope
  * release / acquire, one-thread kernels on the compute stream). Connect with
  * st_p2p_export + st_p2p_connect before the first task. A wait longer than
- * ST_COMM_TIMEOUT_S releases the spinning kernels and returns ST_ERR_STATE. */
+ * ST_COMM_TIMEOUT_S releases the spinning kernels and returns ST_ERR_STATE. Stages of one
+ * process on one GPU are refused (their streams share hardware queues); with CUDA's
+ * lazy module loading, a peer that dies during the FIRST session can block a kernel's
+ * first launch behind a spinning wait (CUDA_MODULE_LOADING=EAGER rules that out). */
 enum { ST_TRANSPORT_NCCL = 0, ST_TRANSPORT_LOCAL = 1, ST_TRANSPORT_P2P = 2 };
 
 /* Opaque, trivially copyable descriptor of one P2P stage's exported buffers (its stash,
@@ -365,6 +368,16 @@ ST_API st_status st_sync(st_ctx* ctx);
  * work of that backward (its side-stream dW + update joined). One-shot; at most 64
  * pending. Errors: ST_ERR_INPUT (NULL event, mb < 0, too many pending). */
 ST_API st_status st_record_after_backward(st_ctx* ctx, int64_t mb, void* cuda_event);
+
+/* CUDA-graph sessions: with `on`, st_run / st_run_host capture the
+ * whole session — every kernel, copy, event record and NCCL call the engine issues on
+ * its compute, side and comm streams — into one CUDA graph (stream capture) and launch
+ * it once, so latency-bound configurations stop paying a host launch per kernel. The
+ * host bookkeeping (program counter, trace, versions) is done during the capture.
+ * Requires: host buffers passed to st_run_host pinned (capturable copies); not for
+ * contexts linked with st_connect_local (their host channels block), which keep running
+ * eagerly. Errors: ST_ERR_CUDA (capture / instantiate / launch failed). */
+ST_API st_status st_set_graph_mode(st_ctx* ctx, int on);
 
 /* ---- measurement hooks ----------------------------------------------------- */
 

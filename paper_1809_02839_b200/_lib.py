@@ -116,6 +116,7 @@ def _load() -> ctypes.CDLL:
         "st_losses_device": (P, [P]),
         "st_sync": (S, [P]),
         "st_set_profiling": (S, [P, I]),
+        "st_set_graph_mode": (S, [P, I]),
         "st_p2p_export": (S, [P, P]),
         "st_p2p_connect": (S, [P, P, P]),
         "st_get_profile": (S, [P, P, P]),
@@ -142,7 +143,7 @@ lib = _load()
 EXPORTED = ("st_version_difference", "st_program", "st_partition", "st_comm_plan", "st_query_sizes", "st_get_nccl_id", "st_init",
             "st_connect_local", "st_destroy", "st_set_params", "st_get_params", "st_stage_forward",
             "st_stage_backward", "st_predict_and_update", "st_step", "st_run", "st_run_host", "st_run_group", "st_get_trace",
-            "st_losses_device", "st_sync", "st_record_after_backward", "st_p2p_export", "st_p2p_connect", "st_set_profiling", "st_get_profile", "st_get_layer_profile", "st_kernel_launches",
+            "st_losses_device", "st_sync", "st_record_after_backward", "st_p2p_export", "st_p2p_connect", "st_set_profiling", "st_set_graph_mode", "st_get_profile", "st_get_layer_profile", "st_kernel_launches",
             "st_update_predict_raw", "st_prediction_error_work_bytes", "st_prediction_error_raw", "st_gemm_raw", "st_gemm_workspace_bytes", "st_softmax_ce_raw", "st_dw_update_raw",
             "st_last_error", "st_version")
 

@@ -217,6 +217,12 @@ st_status st_p2p_connect(st_ctx* ctx, const st_p2p_desc* prev, const st_p2p_desc
   GUARD({ return st::p2p_connect(ctx, prev, next); })
 }
 
+st_status st_set_graph_mode(st_ctx* ctx, int on) {
+  NEED_CTX(ctx);
+  ctx->graph_mode = on != 0;
+  return ST_OK;
+}
+
 st_status st_set_profiling(st_ctx* ctx, int on) {
   NEED_CTX(ctx);
   GUARD({ return ctx_set_profiling(ctx, on); })

@@ -289,6 +289,12 @@ st_status validate_and_layout(const st_config* c, Layout* L) {
 }
 
 // ---- profiling helpers ----------------------------------------------------------
+// An event the caller or the profiler reads the time of: inside a graph capture it must be
+// an external event record node (a plain record there only orders the graph's own nodes)
+static cudaError_t record_timing_event(st_ctx* c, cudaEvent_t e, cudaStream_t s) {
+  return cudaEventRecordWithFlags(e, s, c->capturing ? cudaEventRecordExternal : cudaEventRecordDefault);
+}
+
 // NVTX range for a timeline tool (nsys / ncu --nvtx); header-only NVTX v3, a no-op
 // unless a tool is attached
 struct NvtxRange {
@@ -309,11 +315,11 @@ struct Timed {
     if (!c->prof.on || !((c->prof.mask >> cls) & 1u)) return;
     cudaEvent_t a = get();
     b = get();
-    cudaEventRecord(a, s);
+    record_timing_event(c, a, s);
     c->prof.pairs.push_back({cls, a, b});
   }
   ~Timed() {
-    if (b) cudaEventRecord(b, s);
+    if (b) record_timing_event(c, b, s);
   }
   cudaEvent_t get() {
     if (!c->prof.pool.empty()) {
@@ -339,11 +345,11 @@ struct TimedLayer {
     if (!c->prof.layers) return;
     cudaEvent_t a = take();
     b = take();
-    cudaEventRecord(a, s);
+    record_timing_event(c, a, s);
     c->prof.lpairs.push_back({(int)(2 * l + dir), a, b});
   }
   ~TimedLayer() {
-    if (b) cudaEventRecord(b, s);
+    if (b) record_timing_event(c, b, s);
   }
   cudaEvent_t take() {
     if (!c->prof.pool.empty()) {
@@ -828,8 +834,12 @@ st_status ctx_wait(st_ctx* c) {
     }
     const double waited = std::chrono::duration<double>(std::chrono::steady_clock::now() - t0).count();
     if (waited > c->comm_timeout_s) {
+      const bool trace = getenv("ST_P2P_TRACE") != nullptr;
+      if (trace) fprintf(stderr, "[st] stage %d: wait timed out after %.1f s, aborting\n", c->k, waited);
       c->tp->abort();
+      if (trace) fprintf(stderr, "[st] stage %d: aborted, reading flags\n", c->k);
       const std::string flags = c->p2p ? p2p_describe(c) : std::string();
+      if (trace) fprintf(stderr, "[st] stage %d: flags%s\n", c->k, flags.c_str());
       return set_error(c->transport_kind == ST_TRANSPORT_NCCL ? ST_ERR_NCCL : ST_ERR_STATE,
                        "stage %d: no completion after %.0f s (ST_COMM_TIMEOUT_S): a peer stage is hung or gone; "
                        "transport aborted (program op %zu of %zu)%s",
@@ -1387,7 +1397,7 @@ static st_status run_task(st_ctx* c, const float* x_dev, const int32_t* y_dev, b
     c->bwd_ring_done[b] = true;
     for (size_t i = 0; i < c->marks.size();) {  // st_record_after_backward
       if (c->marks[i].first == t.mb) {
-        ST_CUDA_TRY(cudaEventRecord(c->marks[i].second, c->stream));
+        ST_CUDA_TRY(record_timing_event(c, c->marks[i].second, c->stream));
         c->marks.erase(c->marks.begin() + (long)i);
       } else {
         ++i;
@@ -1510,13 +1520,50 @@ st_status ctx_run(st_ctx* c, int64_t M, const float* xs, const int32_t* ys, floa
   if (c->first_stage && M > 0 && !xs) return set_error(ST_ERR_INPUT, "run: stage 0 needs xs_dev");
   if (c->last_stage && M > 0 && !ys) return set_error(ST_ERR_INPUT, "run: last stage needs ys_dev");
   begin_session(c, M);
-  while (c->pc < c->program.size()) {
+  // graph mode (st_set_graph_mode): the whole session is captured into one CUDA graph and
+  // launched once — every kernel, copy, event and NCCL call of the session becomes a node,
+  // so the GPU runs them back to back without a host launch per kernel (latency-bound
+  // configs). The host bookkeeping (program, trace, versions) runs during the capture.
+  const bool graph = c->graph_mode && !c->link;  // LOCAL groups block on host channels: eager
+  if (graph) {
+    ST_CUDA_TRY(cudaStreamBeginCapture(c->stream, cudaStreamCaptureModeThreadLocal));
+    c->capturing = true;
+    // fork the auxiliary streams into the capture before any of them is used
+    ST_CUDA_TRY(cudaEventRecord(c->ev_join[0], c->stream));
+    for (cudaStream_t s2 : {c->side, c->comm_fwd, c->comm_bwd})
+      if (s2 != c->stream) ST_CUDA_TRY(cudaStreamWaitEvent(s2, c->ev_join[0], 0));
+  }
+  st_status run_err = ST_OK;
+  while (run_err == ST_OK && c->pc < c->program.size()) {
     const Task t = c->program[c->pc];
     float* lh = (host_io && losses_host && c->last_stage && t.dir == ST_FWD) ? losses_host + t.mb : nullptr;
-    ST_TRY(run_task(c, x_of(c, xs, t.mb), y_of(c, ys, t.mb), host_io, lh, true));
+    run_err = run_task(c, x_of(c, xs, t.mb), y_of(c, ys, t.mb), host_io, lh, true);
   }
   // the session's last transfers become part of the compute stream
-  ST_TRY(join_comm(c));
+  if (run_err == ST_OK) run_err = join_comm(c);
+  if (graph) {
+    if (run_err == ST_OK) {  // the side stream's last work joins too (every layer's update)
+      ST_CUDA_TRY(cudaEventRecord(c->ev_join[1], c->side));
+      ST_CUDA_TRY(cudaStreamWaitEvent(c->stream, c->ev_join[1], 0));
+    }
+    cudaGraph_t g = nullptr;
+    const cudaError_t e = cudaStreamEndCapture(c->stream, &g);
+    c->capturing = false;
+    if (run_err != ST_OK) {
+      if (g) cudaGraphDestroy(g);
+      return run_err;
+    }
+    if (e != cudaSuccess) return set_error(ST_ERR_CUDA, "stage %d: graph capture: %s", c->k, cudaGetErrorString(e));
+    cudaGraphExec_t x = nullptr;
+    const cudaError_t ei = cudaGraphInstantiate(&x, g, 0);
+    cudaGraphDestroy(g);
+    if (ei != cudaSuccess) return set_error(ST_ERR_CUDA, "stage %d: graph instantiate: %s", c->k, cudaGetErrorString(ei));
+    const cudaError_t el = cudaGraphLaunch(x, c->stream);
+    cudaGraphExecDestroy(x);  // released once the launch completes
+    if (el != cudaSuccess) return set_error(ST_ERR_CUDA, "stage %d: graph launch: %s", c->k, cudaGetErrorString(el));
+    c->graph_sessions += 1;
+  }
+  ST_TRY(run_err);
   const bool want_losses = losses_host && c->last_stage && M > 0;
   // host buffers (st_run_host) are read by asynchronous copies: never return before they
   // finish; the wait polls the transport (a hung peer surfaces as an error after

@@ -200,6 +200,9 @@ struct st_ctx {
   bool pdl_now = false;         // this task's launches (run_task)
   bool pdl_dense = true;        // dense fwd / dX kernels as programmatic dependent launches (ST_PDL_DENSE=0: off)
   bool pdl = true;              // LSTM recurrence: GEMM ↔ cell as programmatic dependent launches (ST_PDL=0: off)
+  bool graph_mode = false;      // st_set_graph_mode: st_run sessions captured into one CUDA graph
+  int64_t graph_sessions = 0;   // sessions launched as graphs
+  bool capturing = false;       // inside the capture of a graph session
   bool bwd_serial = true;       // dense layers with ≥ 2^27 parameters: dW + update after the dX on the
                                 // compute stream (whole GPU each) instead of overlapped on the side stream
   bool conv_overlap = false;    // implicit-conv dW + update on the side stream (ST_CONV_OVERLAP=1; measured

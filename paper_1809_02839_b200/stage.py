@@ -175,6 +175,10 @@ class Stage:
         check(lib.st_get_profile(self.ctx, ms, n))
         return {name: (ms[i], n[i]) for i, name in enumerate(L.KERNEL_CLASSES)}
 
+    def set_graph_mode(self, on: bool) -> None:
+        """st_set_graph_mode: run() sessions captured into one CUDA graph and launched once."""
+        check(lib.st_set_graph_mode(self.ctx, 1 if on else 0))
+
     def set_layer_profiling(self, on: bool) -> None:
         """Per-layer forward / backward brackets (ST_PROF_LAYERS; the backward runs
         serialised while on)."""

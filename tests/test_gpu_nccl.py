@@ -56,6 +56,8 @@ def _worker(rank, world, port, model_name, M, B, lr, out_dir, fail_rank, timeout
         torch.cuda.set_device(0)
         s = st.Stage(layers_of(model), model.cuts, rank, B, lr, 0.9, transport=st.ST_TRANSPORT_NCCL, device=0,
                      max_minibatches=M, nccl_id=obj[0])
+        if os.environ.get("ST_TEST_GRAPH") == "1":
+            s.set_graph_mode(True)  # the session (NCCL calls included) as one captured CUDA graph
         s.set_params(w0[rank])
         dev = torch.device("cuda", 0)
         xs = torch.from_numpy(np.ascontiguousarray(X, np.float32)).to(dev)
@@ -138,3 +140,21 @@ def test_nccl_hung_peer_surfaces_as_st_err_nccl(tmp_path):
     assert codes == [0, 0], codes
     assert int(np.load(tmp_path / "status0.npy")[0]) == 5
     assert "hung or gone" in (tmp_path / "err0.txt").read_text()
+
+
+def test_nccl_pipeline_graph_mode_matches_oracle(tmp_path, monkeypatch):
+    """The NCCL pipeline with graph sessions: every stage captures its session — kernels,
+    events and the ncclSend / ncclRecv on both comm streams — into one CUDA graph."""
+    monkeypatch.setenv("ST_TEST_GRAPH", "1")
+    world, model_name, M, B, lr = 2, "mlp", 20, 32, 0.05
+    codes = _spawn(world, model_name, M, B, lr, tmp_path)
+    assert all(c == 0 for c in codes), codes
+    model = _model(model_name, world)
+    w0, X, Y = sd.parity_inputs(model, M, B, seed=0)
+    ref = oracle_run(model, w0, X, Y, lr)
+    for k in range(world):
+        tr = [tuple(int(v) for v in row) for row in np.load(tmp_path / f"trace{k}.npy")]
+        assert tr == [e.as_tuple() for e in ref.trace[k]]
+    W = np.concatenate([np.load(tmp_path / f"W{k}.npy") for k in range(world)])
+    assert rel_l2(W, np.concatenate(ref.W)) <= 1e-4
+    assert rel_l2(np.load(tmp_path / "losses.npy"), ref.losses) <= 1e-4

@@ -92,10 +92,17 @@ def _worker(rank, world, port, model_name, M, B, lr, out_dir, hang_rank, timeout
     ys = torch.from_numpy(np.ascontiguousarray(Y, np.int32)).to(dev)
     dist.barrier()
     try:
-        if hang_rank >= 0 and rank == hang_rank:
-            import time
-            time.sleep(3 * timeout_s)  # alive, never runs: its peers' wait kernels spin
-            os._exit(0)
+        if hang_rank >= 0:
+            # session 1 on every rank (every kernel gets loaded: with CUDA's lazy module
+            # loading the first launch of a kernel waits for the device, which a spin-wait
+            # on a dead peer would block before any timeout applies), then the peer hangs
+            s.run(2, xs[:2] if s.is_first else None, ys[:2] if s.is_last else None, want_losses=False)
+            s.sync()
+            dist.barrier()
+            if rank == hang_rank:
+                import time
+                time.sleep(3 * timeout_s)  # alive, never runs again: its peers' wait kernels spin
+                os._exit(0)
         cuts_ = [M] if sessions == 1 else [M // 2, M]  # session boundaries (mini-batch counts)
         parts, lo = [], 0
         for hi in cuts_:
