@@ -59,6 +59,9 @@ def parse():
                         "times; profiled: st_partition over per-layer times measured on this GPU (NEXT-4)")
     p.add_argument("--graph", default="on", choices=["on", "off"],
                    help="on (default): every st_run session captured into one CUDA graph (st_set_graph_mode; contexts linked with st_connect_local stay eager)")
+    p.add_argument("--replicas", default="",
+                   help="hybrid DP x PP (NEXT-4, P:380): comma list of replicas per stage, e.g. 2,1,1,1 — one "
+                        "context per replica (N > 1: WORLD_SIZE = their sum, one per GPU; N = 1: co-located)")
     p.add_argument("--parallel", default="pp", choices=["pp", "dp"],
                    help="pp: the SpecTrain pipeline (default); dp: the data-parallel comparator (NEXT-1)")
     return p.parse_args()
@@ -559,9 +562,17 @@ def run_ours(args):
     N = args.gpus
     if world != N:
         raise SystemExit(f"--gpus {N} but WORLD_SIZE={world}: launch N>1 with torchrun")
-    S = args.stages or N
-    if N > 1 and S != N:
-        raise SystemExit("--stages must equal --gpus when N > 1")
+    reps = [int(v) for v in args.replicas.split(",")] if args.replicas else None
+    if reps:
+        S = len(reps)
+        if args.stages and args.stages != S:
+            raise SystemExit("--stages must equal the number of --replicas entries")
+        if N > 1 and sum(reps) != N:
+            raise SystemExit(f"--replicas {args.replicas}: WORLD_SIZE must be {sum(reps)} (one context per GPU)")
+    else:
+        S = args.stages or N
+        if N > 1 and S != N:
+            raise SystemExit("--stages must equal --gpus when N > 1")
     torch.cuda.set_device(local)
     dev = torch.device("cuda", local)
     if N > 1:
@@ -593,7 +604,22 @@ def run_ours(args):
         raise SystemExit("--steps must be >= 1")
     M = W_ + K  # one session: W warm-up mini-batches, then the K timed ones
 
-    if N > 1:
+    if reps:
+        # stage-major contexts: context i = (stage k, replica r); NCCL rank i = i (one per GPU)
+        ctx_of = [(k, r) for k in range(S) for r in range(reps[k])]
+        if N > 1:
+            obj = [st.nccl_id() if rank == 0 else None]
+            dist.broadcast_object_list(obj, src=0)
+            k, r = ctx_of[rank]
+            my_stages = [st.Stage(layers, model.cuts, k, B, args.lr, 0.9, pred=pred, gemm=gemm,
+                                  transport=st.ST_TRANSPORT_NCCL, device=local, max_minibatches=M, nccl_id=obj[0],
+                                  seq_len=T, replicas=reps, replica=r)]
+        else:
+            my_stages = [st.Stage(layers, model.cuts, k, B, args.lr, 0.9, pred=pred, gemm=gemm,
+                                  transport=st.ST_TRANSPORT_LOCAL, device=local, max_minibatches=M, seq_len=T,
+                                  replicas=reps, replica=r) for k, r in ctx_of]
+            st.connect_local(my_stages)
+    elif N > 1:
         obj = [st.nccl_id() if rank == 0 else None]
         dist.broadcast_object_list(obj, src=0)
         my_stages = [st.Stage(layers, model.cuts, rank, B, args.lr, 0.9, pred=pred, gemm=gemm,
@@ -612,10 +638,12 @@ def run_ours(args):
         for s in my_stages:
             s.set_graph_mode(True)
     # parameters: Glorot on device (bench-only, SURVEY §8(d) seeds), labels uniform
+    for s in my_stages:  # seeded per stage: the replicas of a stage start identical
+        gk = torch.Generator(device=dev)
+        gk.manual_seed(1234 + s.k)
+        init_params(s, model.stage_layers(s.k), dev, gk)
     g = torch.Generator(device=dev)
-    g.manual_seed(1234 + rank)
-    for s in my_stages:
-        init_params(s, model.stage_layers(s.k), dev, g)
+    g.manual_seed(4321)
     n_in, n_cls = model.layers[0].width_in, model.layers[-1].n_out
     first = my_stages[0].is_first
     last = my_stages[-1].is_last
@@ -662,7 +690,7 @@ def run_ours(args):
         dist.all_reduce(t, op=dist.ReduceOp.MAX)
         return float(t.item())
 
-    nccl_parity = nccl_parity_leg(args, N, rank, local, dev) if N > 1 else None
+    nccl_parity = nccl_parity_leg(args, N, rank, local, dev) if (N > 1 and not reps) else None
 
     # the timed session: only the dominant kernel class is bracketed with CUDA events
     # (two event records per launch; events pre-created); the all-class breakdown comes
@@ -688,8 +716,8 @@ def run_ours(args):
     for s in my_stages:
         s.set_profiling(False)
     # per-stage busy time (compute classes, comm excluded) of the breakdown session
-    busy_local = [(s.k, sum(p[c][0] for c in ("update", "gemm_fwd", "gemm_dx", "gemm_dw", "loss")) / n_brk)
-                  for s, p in zip(my_stages, brk)]
+    busy_local = [((s.k, s.replica), sum(p[c][0] for c in ("update", "gemm_fwd", "gemm_dx", "gemm_dw", "loss"))
+                   / n_brk) for s, p in zip(my_stages, brk)]
     if N > 1:
         allb = [None] * N
         dist.all_gather_object(allb, busy_local)
@@ -817,7 +845,8 @@ def run_ours(args):
             "config": {"workload": wname, "stages": S, "batch": B, "seq_len": T, "gemm": args.gemm, "pred": args.pred,
                        "cuts": list(model.cuts), "partition": args.partition,
                        **({"layer_cost_us": layer_cost_us} if layer_cost_us else {}),
-                       "parallelism": f"pp{S}", "cuda_graph": args.graph == "on", "l2": "no flush: per-step working set (weights) >> 126 MB L2",
+                       "parallelism": (f"pp{S}" if not reps else f"pp{S}xdp" + "-".join(map(str, reps))),
+                       **({"replicas": reps} if reps else {}), "cuda_graph": args.graph == "on", "l2": "no flush: per-step working set (weights) >> 126 MB L2",
                        "session": "one 1F1B session of warmup + steps mini-batches; timed window = CUDA events "
                                   "after stage 0's B(warmup-1) and B(warmup+steps-1) (P:415 steady state)"},
             "roofline": roofline_key,
