@@ -57,8 +57,9 @@ def parse():
     p.add_argument("--partition", default="fixed", choices=["fixed", "auto", "profiled"],
                    help="fixed: the BJ / SURVEY §8(d) stage cuts; auto: st_partition over per-layer roofline "
                         "times; profiled: st_partition over per-layer times measured on this GPU (NEXT-4)")
-    p.add_argument("--graph", default="on", choices=["on", "off"],
-                   help="on (default): every st_run session captured into one CUDA graph (st_set_graph_mode; contexts linked with st_connect_local stay eager)")
+    p.add_argument("--graph", default="auto", choices=["auto", "on", "off"],
+                   help="on: every st_run session captured into one CUDA graph (st_set_graph_mode; contexts "
+                        "linked with st_connect_local stay eager); auto (default): on at N = 1, off under torchrun")
     p.add_argument("--replicas", default="",
                    help="hybrid DP x PP (NEXT-4, P:380): comma list of replicas per stage, e.g. 2,1,1,1 — one "
                         "context per replica (N > 1: WORLD_SIZE = their sum, one per GPU; N = 1: co-located)")
@@ -634,7 +635,8 @@ def run_ours(args):
                      for k in range(S)]
         st.connect_local(my_stages)
 
-    if args.graph == "on":
+    use_graph = args.graph == "on" or (args.graph == "auto" and N == 1)
+    if use_graph:
         for s in my_stages:
             s.set_graph_mode(True)
     # parameters: Glorot on device (bench-only, SURVEY §8(d) seeds), labels uniform
@@ -846,7 +848,7 @@ def run_ours(args):
                        "cuts": list(model.cuts), "partition": args.partition,
                        **({"layer_cost_us": layer_cost_us} if layer_cost_us else {}),
                        "parallelism": (f"pp{S}" if not reps else f"pp{S}xdp" + "-".join(map(str, reps))),
-                       **({"replicas": reps} if reps else {}), "cuda_graph": args.graph == "on", "l2": "no flush: per-step working set (weights) >> 126 MB L2",
+                       **({"replicas": reps} if reps else {}), "cuda_graph": use_graph, "l2": "no flush: per-step working set (weights) >> 126 MB L2",
                        "session": "one 1F1B session of warmup + steps mini-batches; timed window = CUDA events "
                                   "after stage 0's B(warmup-1) and B(warmup+steps-1) (P:415 steady state)"},
             "roofline": roofline_key,
