@@ -1,8 +1,8 @@
 """Small round-2 scenarios for compute-sanitizer (profiles/sanitizer/r2_*):
   hybrid  — co-located hybrid DP x PP (stage 0 replicated x2, LOCAL, in-place replica reduce)
   graph   — graph-captured sessions (MLP and an LSTM LM, two sessions each)
-  p2p     — a 2-stage P2P pipeline, one process per stage (CUDA IPC); run with
-            compute-sanitizer --target-processes all
+  p2p_rank <rank> <port> <dir> — one rank of a 2-stage P2P pipeline (CUDA IPC); run each
+            rank as its own process under compute-sanitizer
   layers  — per-layer profiling session"""
 import os, sys, tempfile
 sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
@@ -33,6 +33,11 @@ if __name__ == "__main__":
         d = Path(tempfile.mkdtemp())
         codes = T._spawn(2, "mlp", 4, 32, 0.05, d)
         assert all(c == 0 for c in codes), codes
+    elif what == "p2p_rank":  # one rank of a 2-stage P2P pipeline (run each under compute-sanitizer)
+        from tests import test_gpu_p2p as T
+        rank, port, out = int(sys.argv[2]), int(sys.argv[3]), sys.argv[4]
+        T._worker(rank, 2, port, "mlp", 4, 32, 0.05, out, -1, 120)
+        assert (Path(out) / f"status{rank}.npy").exists()
     elif what == "layers":
         from tests import test_gpu_partition as T
         import synthdata as sd
