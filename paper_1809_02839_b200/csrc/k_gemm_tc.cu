@@ -2590,6 +2590,7 @@ void plan_splits(TcParams& p, int M, int N, int K, int budget) {
   const int tiles = mt * nt;
   int splits = 1;
   if (tiles < budget) splits = std::min(budget / tiles, p.kb_total);
+  if (const int f = dev_knob("ST_FORCE_SPLITS", 0)) splits = std::min(f, p.kb_total);  // development: accuracy vs K
   if (splits < 1) splits = 1;
   const size_t part_bytes = (size_t)BNMAX * BM * 4;
   const size_t ws_cap = (size_t)2 * kWsSms * BNMAX * BM * 4;
