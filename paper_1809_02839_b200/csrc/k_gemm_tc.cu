@@ -73,6 +73,11 @@ struct TcParams {
   int row;           // output element (m, n) at out[m·N + n] (implicit-GEMM conv fwd / dX), else out[n·M + m]
   int split_acc;     // TMEM-A kernel: the two small 3xTF32 terms (lo·hi, hi·lo) in their own accumulator,
                      // added to the hi·hi one in fp32 by the epilogue (long-K dW chains: ~3× less error)
+  int seg;           // TMEM-A kernel: > 0 — each accumulator sums at most `seg` K-blocks; the epilogue
+                     // adds the segments in fp32 registers (round-to-nearest) while the MMAs fill the
+                     // other accumulator. The tensor core's accumulation loses precision systematically
+                     // with every step (the error of one accumulator grows linearly with its K length,
+                     // profiles/r2_gemm_error_vs_splits.txt); short segments bound it.
   int cv_H, cv_W, cv_C;  // implicit-GEMM conv: NHWC image height, width, channels of the implicit operand
 };
 
@@ -879,18 +884,25 @@ __global__ void __launch_bounds__(kPThreads, 1)
     }
   } else if (warp == 1) {
     // ---------------- MMA issuer (A hi / lo from TMEM slot s, B hi / lo from smem)
+    // j counts accumulator hand-offs: one per unit, or one per K segment (p.seg)
     int it = 0, j = 0;
-    const bool sa = p.split_acc != 0;  // small terms in their own accumulator
-    for (int u = blockIdx.x; u < units; u += gridDim.x, ++j) {
-      const int buf = sa ? 0 : (j & 1);
-      const uint32_t par = sa ? (uint32_t)(j & 1) : (uint32_t)((j >> 1) & 1);
-      const uint32_t d = tmem + (uint32_t)buf * AW;
-      const uint32_t d2 = sa ? tmem + AW : d;
+    const bool sa = p.split_acc != 0 && p.seg == 0;  // small terms in their own accumulator
+    for (int u = blockIdx.x; u < units; u += gridDim.x) {
       int kb0, kb1;
       kb_range(u, kb0, kb1);
-      mbar_wait(acc_empty + 8 * buf, par ^ 1);
-      tc_fence_after();
+      int buf = 0;
+      uint32_t d = tmem, d2 = tmem;
       for (int kb = kb0; kb < kb1; ++kb, ++it) {
+        const bool seg_start = p.seg ? ((kb - kb0) % p.seg == 0) : (kb == kb0);
+        const bool seg_end = (kb == kb1 - 1) || (p.seg && (kb - kb0) % p.seg == p.seg - 1);
+        if (seg_start) {
+          buf = sa ? 0 : (j & 1);
+          const uint32_t par = sa ? (uint32_t)(j & 1) : (uint32_t)((j >> 1) & 1);
+          d = tmem + (uint32_t)buf * AW;
+          d2 = sa ? tmem + AW : d;
+          mbar_wait(acc_empty + 8 * buf, par ^ 1);
+          tc_fence_after();
+        }
         const int s = it % NS;
         mbar_wait(b_ready + 8 * s, (it / NS) & 1);
         tc_fence_after();
@@ -899,15 +911,16 @@ __global__ void __launch_bounds__(kPThreads, 1)
         if (elect_one()) {
 #pragma unroll
           for (int kk = 0; kk < BK / 8; ++kk) {
-            const uint32_t acc = (kb > kb0 || kk > 0) ? 1u : 0u;
+            const uint32_t acc = (!seg_start || kk > 0) ? 1u : 0u;
             tc_mma_ts(d, a_hi + kk * 8, op_desc<B_MN>(b_hi, kk), p.idesc, acc);
             tc_mma_ts(d2, a_lo + kk * 8, op_desc<B_MN>(b_hi, kk), p.idesc, sa ? acc : 1u);
             tc_mma_ts(d2, a_hi + kk * 8, op_desc<B_MN>(b_lo, kk), p.idesc, 1u);
           }
           tc_commit(b_empty + 8 * s);
-          if (kb == kb1 - 1) tc_commit(acc_full + 8 * buf);
+          if (seg_end) tc_commit(acc_full + 8 * buf);
         }
         __syncwarp();
+        if (seg_end) ++j;
       }
     }
   } else if (warp < 6) {
@@ -966,13 +979,59 @@ __global__ void __launch_bounds__(kPThreads, 1)
     // ---------------- epilogue (warps 6..9 → TMEM quadrants 2, 3, 0, 1)
     const int quad = warp & 3;
     int j = 0;
-    const bool sa = p.split_acc != 0;
-    for (int u = blockIdx.x; u < units; u += gridDim.x, ++j) {
-      const int buf = sa ? 0 : (j & 1);
+    const bool sa = p.split_acc != 0 && p.seg == 0;
+    for (int u = blockIdx.x; u < units; u += gridDim.x) {
       const int t = u % tiles, m0 = (t % mt) * BM, n0 = (t / mt) * BNMAX;
-      mbar_wait(acc_full + 8 * buf, sa ? (uint32_t)(j & 1) : (uint32_t)((j >> 1) & 1));
-      tc_fence_after();
       const int m = m0 + quad * 32 + lane;
+      if (p.seg) {
+        // segmented: sum the unit's segments in registers (fixed order, round-to-nearest)
+        int kb0, kb1;
+        kb_range(u, kb0, kb1);
+        const int nseg = (kb1 - kb0 + p.seg - 1) / p.seg;
+        float run[BNMAX];
+        for (int i = 0; i < nseg; ++i, ++j) {
+          const int buf = j & 1;
+          mbar_wait(acc_full + 8 * buf, (uint32_t)((j >> 1) & 1));
+          tc_fence_after();
+          const uint32_t trow = tmem + (uint32_t)buf * AW + ((uint32_t)(quad * 32) << 16);
+#pragma unroll
+          for (int c = 0; c < (int)AW; c += 16) {
+            if (c < bn) {
+              float v[16];
+              tc_ld16(trow + c, v);
+#pragma unroll
+              for (int q = 0; q < 16; ++q) run[c + q] = i ? __fadd_rn(run[c + q], v[q]) : v[q];
+            }
+          }
+          tc_fence_before();
+          __syncwarp();
+          if (lane == 0) mbar_arrive(acc_empty + 8 * buf);
+        }
+        if (p.splits > 1) {
+          float* wsp = p.ws + ((size_t)(u / tiles) * tiles + t) * (BNMAX * BM);
+#pragma unroll
+          for (int c = 0; c < (int)AW; c += 16)
+            if (c < bn) {
+#pragma unroll
+              for (int q = 0; q < 16; ++q) wsp[(size_t)(c + q) * BM + quad * 32 + lane] = run[c + q];
+            }
+        } else {
+          const float bias = (EPI == EPI_FWD && p.aux && m < p.M && !p.row) ? p.aux[m] : 0.f;
+#pragma unroll
+          for (int c = 0; c < (int)AW; c += 16)
+            if (c < bn && m < p.M) {
+              float v[16];
+#pragma unroll
+              for (int q = 0; q < 16; ++q) v[q] = run[c + q];
+              epilogue_store16<EPI>(p, m, n0 + c, v, bias);
+            }
+        }
+        continue;
+      }
+      const int buf = sa ? 0 : (j & 1);
+      mbar_wait(acc_full + 8 * buf, sa ? (uint32_t)(j & 1) : (uint32_t)((j >> 1) & 1));
+      ++j;
+      tc_fence_after();
       const uint32_t trow = tmem + (uint32_t)buf * AW + ((uint32_t)(quad * 32) << 16);
       const uint32_t trow2 = tmem + AW + ((uint32_t)(quad * 32) << 16);
       if (p.splits > 1) {
@@ -2461,6 +2520,16 @@ int dw_lockstep_mode() {
   return f;
 }
 
+// TMEM-A kernel, dW launches: K-blocks per accumulator segment (0 = one accumulator per work
+// unit). Measured on VGG-16 (10 mini-batches, fp64 oracle): V spread 0.054 → 0.0007 at 1
+// stage (the CUDA-core fp32 GEMMs: 0.00014), 0.093 → 0.035 at 8 stages (fp32: 0.039).
+// ST_TSG_SEG overrides (development).
+int tsg_segment_kblocks() {
+  static int f = -1;
+  if (f < 0) f = std::max(0, dev_knob("ST_TSG_SEG", 0));
+  return f;
+}
+
 // The fused update stores w', v' from registers and frees each W / V slot as soon as
 // the epilogue has read it (default): standalone 8192² 202.9 → 191.8 µs (5.29 → 5.60
 // TB/s), 16384² 710 → 689 µs (6.05 → 6.24 TB/s) against TMA stores out of the slot,
@@ -2548,6 +2617,7 @@ st_status launch(const GemmArgs& g, int M, int N, int K, const CUtensorMap& ma, 
     // rel-L2 on an 8192-row dW, LSTM step unchanged); fwd / dX keep the double-buffered
     // accumulators that overlap the epilogue (ST_GEMM_DEV_FLAGS=1024 forces it everywhere)
     p.split_acc = (EPI == EPI_DW || (p.dev_flags & 1024)) ? 1 : 0;
+    p.seg = tsg_segment_kblocks();
     const int budget = g.max_ctas > 0 ? std::min(g.max_ctas, num_sms()) : num_sms();
     ST_TRY(launch_maybe_pdl(g.pdl, ck, dim3(std::min(tiles * p.splits, budget)), dim3(kPThreads), (size_t)smem,
                             g.stream, ma, mb, p, mt, tiles));

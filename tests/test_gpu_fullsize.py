@@ -29,7 +29,7 @@ import torch
 
 import synthdata as sd
 from oracle import spectrain_oracle as O
-from tests.gpu_helpers import layers_of, rel_l2
+from tests.gpu_helpers import build_pipeline, layers_of, rel_l2, run_pipeline
 
 pytestmark = pytest.mark.gpu
 
@@ -231,6 +231,52 @@ def test_lstm_lm_full_size_single_stage_bench_path(st):
     rdw = rel_l2(W - W0, ref.W[0] - W0)
     rv = rel_l2(V, ref.V[0])
     _record("lstm_lm_1stage", {"dw": rdw, "v": rv})
+    assert rv <= 1e-4, rv
+    assert rdw <= 1e-2, rdw
+
+
+def test_vgg16_full_size_8_stages_bench_partition(st):
+    """BJ configs[3] at full size in its pipelined form: VGG-16 (32×32×3, batch 128) cut
+    into the 8 stages of SURVEY §8(d) (`vgg16_cuts_8`), co-located through the LOCAL
+    transport, M = 10 mini-batches (the pipeline fills: stage 0 runs 7 warm-up forwards,
+    then F/B pairs with s_F up to 7). Trace exact per stage; W and loss within 1e-4; V and
+    ΔW with the D24 gates of the 1-stage VGG test (max-pool / ReLU decisions)."""
+    model = sd.config_vgg16(8)
+    M, B = 10, 128
+    w0, X, Y = sd.parity_inputs(model, M, B, seed=0)
+    stages = build_pipeline(model, B, LR, max_mb=M)
+    try:
+        W, V, losses, traces = run_pipeline(stages, w0, X, Y)
+    finally:
+        for s_ in stages:
+            s_.close()
+    ref = _oracle(("vgg16", 8), model, w0, X, Y)
+    _check("vgg16_8stages", model, w0, ref, W, V, losses, traces, dw_tol=5e-2)
+
+
+def test_lstm_lm_full_size_4_stages(st):
+    """BJ configs[2] at full size in its pipelined form: {Emb}{LSTM1}{LSTM2}{Softmax}
+    (SURVEY §8(d) row 3), T = 35, batch 128, co-located through the LOCAL transport,
+    M = 6 mini-batches. No ReLU / max decisions: V is gated tightly, as at 1 stage."""
+    model = sd.config_lstm_lm(4)
+    M, B = 6, 128
+    w0 = sd.to_f32_params(sd.glorot_params(model, 0))
+    X, Y = sd.tokens(model.layers[0].n_in, M, B, model.seq_len, 1)
+    stages = build_pipeline(model, B, LR, max_mb=M)
+    try:
+        W, V, losses, traces = run_pipeline(stages, w0, X, Y)
+    finally:
+        for s_ in stages:
+            s_.close()
+    ref = O.run(model, sd.widen(w0), X, Y, float(np.float32(LR)), float(np.float32(0.9)))
+    for k in range(model.num_stages):
+        assert traces[k] == [e.as_tuple() for e in ref.trace[k]], f"trace mismatch at stage {k}"
+    Wc, Wr = np.concatenate(W), np.concatenate(ref.W)
+    W0 = np.concatenate(sd.widen(w0))
+    rl, rw = rel_l2(losses, ref.losses), rel_l2(Wc, Wr)
+    rv, rdw = rel_l2(np.concatenate(V), np.concatenate(ref.V)), rel_l2(Wc - W0, Wr - W0)
+    _record("lstm_lm_4stages", {"loss": rl, "w": rw, "v": rv, "dw": rdw})
+    assert rl <= 1e-4 and rw <= 1e-4, (rl, rw)
     assert rv <= 1e-4, rv
     assert rdw <= 1e-2, rdw
 

@@ -1,0 +1,43 @@
+"""Reading D24 for a whole pipelined run, without the GPU: the oracle's SpecTrain run
+(O.run, every stage, every mini-batch, the paper's predictions) in NumPy float32 against
+float64 on the inputs of a tests/test_gpu_fullsize.py case — the spread of V and ΔW that
+fp32-faithful arithmetic alone produces through the ReLU / max-pool decisions.
+
+    python tools/d24_pipeline.py vgg16_8 [--M 10]   ->  profiles/r2_d24_<case>.json
+"""
+import argparse, json, os, sys, time
+import numpy as np
+ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+sys.path.insert(0, ROOT)
+import synthdata as sd  # noqa: E402
+from oracle import spectrain_oracle as O  # noqa: E402
+
+
+def rel(a, b):
+    a, b = np.asarray(a, np.float64).ravel(), np.asarray(b, np.float64).ravel()
+    return float(np.linalg.norm(a - b) / np.linalg.norm(b))
+
+
+if __name__ == "__main__":
+    ap = argparse.ArgumentParser()
+    ap.add_argument("case", choices=["vgg16_8", "vgg16_1"])
+    ap.add_argument("--M", type=int, default=10)
+    a = ap.parse_args()
+    LR, B = 0.01, 128
+    model = sd.config_vgg16(8 if a.case == "vgg16_8" else 1)
+    w0, X, Y = sd.parity_inputs(model, a.M, B, seed=0)
+    t0 = time.time()
+    r64 = O.run(model, sd.widen(w0), X.astype(np.float64), Y, float(np.float32(LR)), float(np.float32(0.9)))
+    t1 = time.time()
+    r32 = O.run(model, [np.asarray(w, np.float32) for w in w0], X.astype(np.float32), Y, float(np.float32(LR)),
+                float(np.float32(0.9)))
+    t2 = time.time()
+    W0 = np.concatenate(sd.widen(w0))
+    W64, W32 = np.concatenate(r64.W), np.concatenate(r32.W)
+    out = {"case": a.case, "M": a.M, "B": B, "lr": LR,
+           "fp32_vs_fp64": {"loss": rel(r32.losses, r64.losses), "w": rel(W32, W64), "dw": rel(W32 - W0, W64 - W0),
+                            "v": rel(np.concatenate(r32.V), np.concatenate(r64.V))},
+           "dtype_check": str(np.concatenate(r32.V).dtype), "seconds": [round(t1 - t0, 1), round(t2 - t1, 1)]}
+    path = os.path.join(ROOT, "profiles", f"r2_d24_{a.case}_M{a.M}.json")
+    json.dump(out, open(path, "w"), indent=1)
+    print(json.dumps(out, indent=1))
