@@ -199,6 +199,43 @@ def test_query_sizes_and_validation(st):
         assert (z.wb_bytes > 0) == (0 < sb != sf)
 
 
+def test_replica_config_sizes_and_validation(st):
+    """Hybrid DP × PP configs (st_config.replicas, NEXT-4): a replica's arenas hold its row
+    slice (stash B/R rows), its parameters are the whole stage's; the limits of the
+    header are enforced by st_query_sizes (no device work)."""
+    from paper_1809_02839_b200 import _lib as L
+    model = sd.mlp([784, 256, 192, 128, 10], cuts=[1, 3])
+    layers = [(l.n_in, l.n_out, L.ST_ACT_RELU if l.act == sd.RELU else L.ST_ACT_NONE, 1) for l in model.layers]
+    B = 32
+    full, k0 = L.make_config(layers, model.cuts, 0, B, 0.05, 0.9)
+    rep, k1 = L.make_config(layers, model.cuts, 0, B, 0.05, 0.9, replicas=[4, 1, 1], replica=3)
+    sf, sr = L.query_sizes(full), L.query_sizes(rep)
+    assert sr.params == sf.params and sr.w_bytes == sf.w_bytes
+    assert sr.stash_bytes * 4 == sf.stash_bytes  # 3 slots × (B/4) rows × 784
+    nxt, k2 = L.make_config(layers, model.cuts, 1, B, 0.05, 0.9, replicas=[4, 1, 1])
+    assert L.query_sizes(nxt).stash_bytes == L.query_sizes(L.make_config(layers, model.cuts, 1, B, 0.05, 0.9)[0]).stash_bytes
+    bad_cases = [
+        ([1, 1, 2], 0, "last stage"),          # the last stage owns the batch-mean loss
+        ([2, 2, 1], 0, "adjacent"),            # neighbouring replicated stages
+        ([3, 1, 1], 0, "divisible"),           # 32 rows over 3 replicas
+        ([2, 1, 1], 2, "replica"),             # replica index outside [0, 2)
+        ([0, 1, 1], 0, "must be >= 1"),
+    ]
+    for reps, r, msg in bad_cases:
+        c, kk = L.make_config(layers, model.cuts, 0, B, 0.05, 0.9, replicas=reps, replica=r)
+        with pytest.raises(L.SpecTrainError, match=msg):
+            L.query_sizes(c)
+    c, kk = L.make_config(layers, model.cuts, 0, B, 0.05, 0.9, transport=L.ST_TRANSPORT_P2P, replicas=[2, 1, 1])
+    with pytest.raises(L.SpecTrainError, match="NCCL or LOCAL"):
+        L.query_sizes(c)
+    lm = sd.lstm_lm(vocab=32, hidden=16, layers=2, cuts=[1, 3], seq_len=4)
+    ll = [(l.n_in, l.n_out, 0, 1 if l.bias else 0, {sd.EMBED: L.ST_LAYER_EMBED, sd.LSTM: L.ST_LAYER_LSTM,
+                                                  sd.DENSE: L.ST_LAYER_DENSE}[l.kind]) for l in lm.layers]
+    c, kk = L.make_config(ll, lm.cuts, 1, 8, 0.1, 0.9, seq_len=4, replicas=[1, 2, 1])
+    with pytest.raises(L.SpecTrainError, match="seq_len"):
+        L.query_sizes(c)
+
+
 # ---------------------------------------------------------------- st_partition (NEXT-4)
 
 def _brute_partition(cost, N):

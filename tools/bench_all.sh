@@ -12,3 +12,6 @@ timeout 600 python bench.py --workload large_fcn --no-cpu --steps 10 --warmup 3 
 for s in 2 4 8; do
   timeout 600 python bench.py --workload large_fcn --stages $s --no-cpu --steps 10 --warmup 3 > $OUT/large_fcn_s$s.json 2>&1
 done
+# NEXT-4 on VGG-16's imbalanced 8-stage pipeline (co-located): profiled cuts, a replicated conv front
+timeout 600 python bench.py --workload vgg16 --stages 8 --partition profiled --no-cpu > $OUT/vgg16_s8_profiled.json 2>&1
+timeout 600 python bench.py --workload vgg16 --replicas 2,1,1,1,1,1,1,1 --no-cpu > $OUT/vgg16_s8_rep2.json 2>&1
