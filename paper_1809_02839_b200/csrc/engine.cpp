@@ -251,8 +251,8 @@ st_status validate_and_layout(const st_config* c, Layout* L) {
     L->off_ldh = take(B * max_h);
     L->off_ldc = take(B * max_h);
     L->off_ldG = take(R * 4 * max_h);
-    L->off_lhlo = take(B * max_h);
-    L->off_ldglo = take(B * 4 * max_h);
+    L->off_lhlo = take(2 * B * max_h);       // two slots: the persistent recurrence reads h_{t−1}'s
+    L->off_ldglo = take(2 * B * 4 * max_h);  // lo while step t writes h_t's (dG likewise)
   }
   if (max_vocab > 0) L->off_escr = take(embed_grad_scratch_bytes((int)R, max_vocab) / 4 + 1);
   if (max_col > 0) {
@@ -562,6 +562,9 @@ st_status ctx_init(const st_config* cfg, const st_buffers* bufs, void* stream, v
   // several stage contexts sharing one GPU (LOCAL transport): their kernels interleave
   // across streams and waiting dependents would hold SMs the other stages need
   // (wide FCN at 2 co-located stages 45.8k → 41.8k samples/s with it)
+  int co_located = 0;
+  for (int r : c->reps) co_located += r;
+  c->shares_gpu = c->transport_kind == ST_TRANSPORT_LOCAL && co_located > 1;
   if (c->transport_kind == ST_TRANSPORT_LOCAL && c->N > 1) {
     c->pdl_dense = false;
     c->pdl = false;
@@ -899,6 +902,19 @@ static st_status lstm_forward(st_ctx* c, const LayerInfo& L, const float* Wh, co
     c->launches += gemm_last_launches();
   }
   ST_CUDA_TRY(cudaMemsetAsync(hbuf, 0, (size_t)B * H * 4, c->stream));          // h_{-1} = 0
+  if (!c->shares_gpu) {
+    // all T steps in one persistent launch (k_lstm_rec.cu); the per-step path below when the
+    // shapes do not allow it. Not with co-located contexts: two cooperative grids filling
+    // the GPU at once could each wait for SMs the other holds.
+    Timed tt(c, KC_GEMM_FWD);
+    const st_status r = lstm_rec_fwd(gargs_rows(c, B, H, 4 * H), B, H, T, Wh + L.whh_off, gates, hbuf, cbuf,
+                                     c->lstm_hlo);
+    if (r == ST_OK) {
+      c->launches += 1;
+      return ST_OK;
+    }
+    if (r != ST_ERR_UNSUPPORTED) return r;
+  }
   ST_CUDA_TRY(cudaMemsetAsync(c->lstm_hlo, 0, (size_t)B * H * 4, c->stream));  // its tf32 lo
   for (int t = 0; t < T; ++t) {
     float* h_prev = hbuf + (size_t)t * B * H;
@@ -1031,8 +1047,20 @@ static st_status lstm_backward(st_ctx* c, const LayerInfo& L, const float* Wh, c
   const float* gates = slot + L.gates_off;
   const float* cbuf = slot + L.c_off;
   const float* hbuf = slot + L.h_off;
+  bool rec_done = false;
+  if (!c->shares_gpu) {  // all T steps in one persistent launch (see lstm_forward)
+    Timed tt(c, KC_GEMM_DX);
+    const st_status r = lstm_rec_bwd(gargs_rows(c, B, H, 4 * H), B, H, T, Wh + L.whh_off, gates, cbuf, dOut,
+                                     c->lstm_dG, c->lstm_dglo, c->lstm_dc);
+    if (r == ST_OK) {
+      c->launches += 1;
+      rec_done = true;
+    } else if (r != ST_ERR_UNSUPPORTED) {
+      return r;
+    }
+  }
   SplitPlan plan;  // dh_next of the step after t (splits = 0: none at t = T−1)
-  for (int t = T - 1; t >= 0; --t) {
+  for (int t = rec_done ? -1 : T - 1; t >= 0; --t) {
     {
       Timed tt(c, KC_LOSS);
       ST_TRY(launch_lstm_cell_bwd(gates + (size_t)t * B * 4 * H, cbuf + (size_t)t * B * H,

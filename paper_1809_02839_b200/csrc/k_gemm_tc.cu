@@ -29,6 +29,7 @@
 
 #include "knobs.hpp"
 #include "kernels.hpp"
+#include "tc_ptx.cuh"
 
 namespace st {
 
@@ -81,158 +82,8 @@ struct TcParams {
   int cv_H, cv_W, cv_C;  // implicit-GEMM conv: NHWC image height, width, channels of the implicit operand
 };
 
-// ------------------------------------------------------------------ PTX helpers
-// 1024-B aligned base of the dynamic smem window. Pointer arithmetic on the __shared__
-// array itself (not a uintptr_t round trip) keeps the address space visible to the
-// compiler, so reads through it are LDS, not generic LD.
-__device__ __forceinline__ bool elect_one() {
-  uint32_t pred = 0;
-  asm volatile(
-      "{\n .reg .pred p;\n elect.sync _|p, 0xffffffff;\n selp.u32 %0, 1, 0, p;\n}" : "=r"(pred)::"memory");
-  return pred != 0;
-}
-__device__ __forceinline__ char* align_smem_1k(uint8_t* raw) {
-  const uint32_t a = (uint32_t)__cvta_generic_to_shared(raw);
-  return reinterpret_cast<char*>(raw) + ((1024u - (a & 1023u)) & 1023u);
-}
-__device__ __forceinline__ uint32_t smem_u32(const void* p) { return (uint32_t)__cvta_generic_to_shared(p); }
+using namespace ptx;
 
-__device__ __forceinline__ void mbar_init(uint32_t bar, uint32_t count) {
-  asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(bar), "r"(count) : "memory");
-}
-__device__ __forceinline__ void mbar_expect_tx(uint32_t bar, uint32_t bytes) {
-  asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(bar), "r"(bytes) : "memory");
-}
-__device__ __forceinline__ void mbar_arrive(uint32_t bar) {
-  asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(bar) : "memory");
-}
-__device__ __forceinline__ void mbar_wait(uint32_t bar, uint32_t parity) {
-  uint32_t ok = 0;
-  do {
-    asm volatile(
-        "{\n .reg .pred p;\n mbarrier.try_wait.parity.shared::cta.b64 p, [%1], %2;\n selp.u32 %0, 1, 0, p;\n}"
-        : "=r"(ok)
-        : "r"(bar), "r"(parity)
-        : "memory");
-  } while (!ok);
-}
-__device__ __forceinline__ void tma_load_2d(uint32_t dst, const CUtensorMap* map, int c0, int c1, uint32_t bar) {
-  asm volatile(
-      "cp.async.bulk.tensor.2d.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1, {%2, %3}], [%4];" ::"r"(
-          dst),
-      "l"(reinterpret_cast<uint64_t>(map)), "r"(c0), "r"(c1), "r"(bar)
-      : "memory");
-}
-__device__ __forceinline__ void tma_load_3d(uint32_t dst, const CUtensorMap* map, int c0, int c1, int c2,
-                                            uint32_t bar) {
-  asm volatile(
-      "cp.async.bulk.tensor.3d.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1, {%2, %3, %4}], [%5];" ::
-          "r"(dst),
-      "l"(reinterpret_cast<uint64_t>(map)), "r"(c0), "r"(c1), "r"(c2), "r"(bar)
-      : "memory");
-}
-// 4-D box of an NHWC activation tensor (dims C, W, H, B); coordinates may be negative or
-// past the edge: TMA zero-fills those elements, which is exactly the conv's zero padding.
-__device__ __forceinline__ void tma_load_4d(uint32_t dst, const CUtensorMap* map, int c0, int c1, int c2, int c3,
-                                            uint32_t bar) {
-  asm volatile(
-      "cp.async.bulk.tensor.4d.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1, {%2, %3, %4, %5}], "
-      "[%6];" ::"r"(dst),
-      "l"(reinterpret_cast<uint64_t>(map)), "r"(c0), "r"(c1), "r"(c2), "r"(c3), "r"(bar)
-      : "memory");
-}
-__device__ __forceinline__ void fence_proxy_async() { asm volatile("fence.proxy.async.shared::cta;" ::: "memory"); }
-// TMA store of a 2-D box from smem (bulk-group completion)
-__device__ __forceinline__ void tma_store_2d(const CUtensorMap* map, uint32_t src, int c0, int c1) {
-  asm volatile("cp.async.bulk.tensor.2d.global.shared::cta.bulk_group [%0, {%2, %3}], [%1];" ::"l"(
-                   reinterpret_cast<uint64_t>(map)),
-               "r"(src), "r"(c0), "r"(c1)
-               : "memory");
-}
-__device__ __forceinline__ void bulk_commit() { asm volatile("cp.async.bulk.commit_group;" ::: "memory"); }
-template <int N>
-__device__ __forceinline__ void bulk_wait_read() { asm volatile("cp.async.bulk.wait_group.read %0;" ::"n"(N) : "memory"); }
-__device__ __forceinline__ void tc_fence_before() { asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory"); }
-__device__ __forceinline__ void tc_fence_after() { asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory"); }
-
-__device__ __forceinline__ void tc_mma(uint32_t tmem_d, uint64_t adesc, uint64_t bdesc, uint32_t idesc,
-                                       uint32_t accum) {
-  asm volatile(
-      "{\n .reg .pred p;\n setp.ne.b32 p, %4, 0;\n tcgen05.mma.cta_group::1.kind::tf32 [%0], %1, %2, %3, p;\n}" ::"r"(
-          tmem_d),
-      "l"(adesc), "l"(bdesc), "r"(idesc), "r"(accum)
-      : "memory");
-}
-__device__ __forceinline__ void tc_commit(uint32_t bar) {
-  asm volatile("tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.b64 [%0];" ::"r"(bar) : "memory");
-}
-__device__ __forceinline__ void tc_ld16_nowait(uint32_t taddr, uint32_t* r) {
-  asm volatile(
-      "tcgen05.ld.sync.aligned.32x32b.x16.b32 {%0,%1,%2,%3,%4,%5,%6,%7,%8,%9,%10,%11,%12,%13,%14,%15}, [%16];"
-      : "=r"(r[0]), "=r"(r[1]), "=r"(r[2]), "=r"(r[3]), "=r"(r[4]), "=r"(r[5]), "=r"(r[6]), "=r"(r[7]), "=r"(r[8]),
-        "=r"(r[9]), "=r"(r[10]), "=r"(r[11]), "=r"(r[12]), "=r"(r[13]), "=r"(r[14]), "=r"(r[15])
-      : "r"(taddr));
-}
-__device__ __forceinline__ void tc_ld8_nowait(uint32_t taddr, uint32_t* r) {
-  asm volatile("tcgen05.ld.sync.aligned.32x32b.x8.b32 {%0,%1,%2,%3,%4,%5,%6,%7}, [%8];"
-               : "=r"(r[0]), "=r"(r[1]), "=r"(r[2]), "=r"(r[3]), "=r"(r[4]), "=r"(r[5]), "=r"(r[6]), "=r"(r[7])
-               : "r"(taddr));
-}
-__device__ __forceinline__ void tc_wait_ld() { asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory"); }
-__device__ __forceinline__ void tc_ld16(uint32_t taddr, float* v) {
-  uint32_t r[16];
-  asm volatile(
-      "tcgen05.ld.sync.aligned.32x32b.x16.b32 {%0,%1,%2,%3,%4,%5,%6,%7,%8,%9,%10,%11,%12,%13,%14,%15}, [%16];"
-      : "=r"(r[0]), "=r"(r[1]), "=r"(r[2]), "=r"(r[3]), "=r"(r[4]), "=r"(r[5]), "=r"(r[6]), "=r"(r[7]), "=r"(r[8]),
-        "=r"(r[9]), "=r"(r[10]), "=r"(r[11]), "=r"(r[12]), "=r"(r[13]), "=r"(r[14]), "=r"(r[15])
-      : "r"(taddr));
-  asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory");
-#pragma unroll
-  for (int i = 0; i < 16; ++i) v[i] = __uint_as_float(r[i]);
-}
-
-// UMMA shared-memory descriptors (sm_100 version 1).
-// K-major operand: rows of 128 B (32 fp32 along K), SWIZZLE_128B, 8-row atoms of
-// 1024 B (SBO); a K step of 8 tf32 advances the start address by 32 B.
-__device__ __forceinline__ uint64_t desc_kmajor(uint32_t saddr) {
-  return (uint64_t)((saddr >> 4) & 0x3FFF) | ((uint64_t)1 << 16) | ((uint64_t)(1024 >> 4) << 32) |
-         ((uint64_t)1 << 46) | ((uint64_t)2 << 61);
-}
-// MN-major operand (32-bit elements need SWIZZLE_128B_BASE32B): 32-element MN
-// chunks of 128 B per k row, 32 k rows per chunk (4 KB → LBO), 4-row k groups
-// of 512 B (SBO); a K step of 8 advances the start address by 1024 B.
-__device__ __forceinline__ uint64_t desc_mnmajor(uint32_t saddr) {
-  return (uint64_t)((saddr >> 4) & 0x3FFF) | ((uint64_t)(4096 >> 4) << 16) | ((uint64_t)(512 >> 4) << 32) |
-         ((uint64_t)1 << 46) | ((uint64_t)1 << 61);
-}
-template <bool MN>
-__device__ __forceinline__ uint64_t op_desc(uint32_t base, int kk) {
-  return MN ? desc_mnmajor(base + kk * 1024) : desc_kmajor(base + kk * 32);
-}
-
-// The tensor core truncates fp32 operands to tf32 (measured: tools/probe_tcgen05.cu),
-// so the raw tile IS the "hi" operand and lo = x − trunc_tf32(x) is exact in fp32.
-__device__ __forceinline__ float lo_part(float x) { return x - __uint_as_float(__float_as_uint(x) & 0xFFFFE000u); }
-
-// lo = x − hi over `chunks` 16-byte chunks: elementwise, so it is layout-agnostic
-// (raw and lo buffers share the same swizzled arrangement).
-__device__ __forceinline__ void make_lo(const char* raw, char* lo, int chunks, int tid) {
-  int c = tid;
-  for (; c + 3 * 128 < chunks; c += 4 * 128) {
-    float4 v[4];
-#pragma unroll
-    for (int u = 0; u < 4; ++u) v[u] = *reinterpret_cast<const float4*>(raw + (c + u * 128) * 16);
-#pragma unroll
-    for (int u = 0; u < 4; ++u) {
-      float4 l = make_float4(lo_part(v[u].x), lo_part(v[u].y), lo_part(v[u].z), lo_part(v[u].w));
-      *reinterpret_cast<float4*>(lo + (c + u * 128) * 16) = l;
-    }
-  }
-  for (; c < chunks; c += 128) {
-    const float4 v = *reinterpret_cast<const float4*>(raw + c * 16);
-    *reinterpret_cast<float4*>(lo + c * 16) = make_float4(lo_part(v.x), lo_part(v.y), lo_part(v.z), lo_part(v.w));
-  }
-}
 
 
 // Development timeline (ST_GEMM_DEV_FLAGS bit 7): %globaltimer at fixed points of each
@@ -774,9 +625,6 @@ __global__ void __launch_bounds__(kPThreads, 1)
   }
 }
 
-__device__ __forceinline__ void tc_mma_ts(uint32_t tmem_d, uint32_t tmem_a, uint64_t bdesc, uint32_t idesc,
-                                          uint32_t accum);
-__device__ __forceinline__ void tc_st32(uint32_t taddr, const uint32_t* v);
 
 // FP32X3 persistent GEMM with the A operand in TMEM (A-from-TMEM MMAs): the implicit-conv
 // fwd / dX / dW and the tall dense dW (LSTM / LM softmax: K = T·B rows).
@@ -1202,25 +1050,6 @@ constexpr int TS_THREADS = 224;          // 7 warps
 constexpr int TS_B_STAGE = 2 * BNMAX * BK * 4;
 constexpr int ts_smem_bytes() { return TS_RA * TILE_BYTES + TS_RB * TS_B_STAGE + 1024 + 512; }
 
-__device__ __forceinline__ void tc_mma_ts(uint32_t tmem_d, uint32_t tmem_a, uint64_t bdesc, uint32_t idesc,
-                                          uint32_t accum) {
-  asm volatile(
-      "{\n .reg .pred p;\n setp.ne.b32 p, %4, 0;\n tcgen05.mma.cta_group::1.kind::tf32 [%0], [%1], %2, %3, p;\n}" ::"r"(
-          tmem_d),
-      "r"(tmem_a), "l"(bdesc), "r"(idesc), "r"(accum)
-      : "memory");
-}
-
-__device__ __forceinline__ void tc_st32(uint32_t taddr, const uint32_t* v) {
-  asm volatile(
-      "tcgen05.st.sync.aligned.32x32b.x32.b32 [%0], {%1,%2,%3,%4,%5,%6,%7,%8,%9,%10,%11,%12,%13,%14,%15,%16,%17,%18,"
-      "%19,%20,%21,%22,%23,%24,%25,%26,%27,%28,%29,%30,%31,%32};" ::"r"(taddr),
-      "r"(v[0]), "r"(v[1]), "r"(v[2]), "r"(v[3]), "r"(v[4]), "r"(v[5]), "r"(v[6]), "r"(v[7]), "r"(v[8]), "r"(v[9]),
-      "r"(v[10]), "r"(v[11]), "r"(v[12]), "r"(v[13]), "r"(v[14]), "r"(v[15]), "r"(v[16]), "r"(v[17]), "r"(v[18]),
-      "r"(v[19]), "r"(v[20]), "r"(v[21]), "r"(v[22]), "r"(v[23]), "r"(v[24]), "r"(v[25]), "r"(v[26]), "r"(v[27]),
-      "r"(v[28]), "r"(v[29]), "r"(v[30]), "r"(v[31])
-      : "memory");
-}
 
 template <int EPI, bool A_MN>
 __global__ void __launch_bounds__(TS_THREADS, 1)
@@ -2795,6 +2624,13 @@ st_status launch_ts(const GemmArgs& g, int M, int N, int K, const CUtensorMap& m
 }  // namespace
 
 int device_sm_count() { return num_sms(); }
+
+// exported for the persistent LSTM recurrence (k_lstm_rec.cu)
+bool tc_make_map(CUtensorMap* m, const float* base, int inner, int outer, int pitch, int box_outer, bool mn_major) {
+  return make_map(m, base, inner, outer, pitch, box_outer, mn_major);
+}
+st_status tc_ensure_max_smem(const void* fn, int bytes) { return ensure_max_smem(fn, bytes); }
+uint32_t make_idesc_tf32(int bn, int mma_m) { return make_idesc(bn, false, false, mma_m); }
 
 int tc_last_launches() { return g_launches; }
 // counters (64 KB, zero-initialised by the owner, self-resetting) + split-K partials

@@ -100,6 +100,15 @@ struct GemmArgs {
 };
 int64_t gemm_workspace_bytes(int B, int max_in, int max_out);
 st_status gemm_fwd(const GemmArgs& g, const float* X, const float* W, const float* bias, float* Z, int relu);
+// Persistent LSTM recurrence (k_lstm_rec.cu): all T steps of one layer in one cooperative
+// launch (FP32X3, B ≤ 128, H % 4 == 0). Forward: gates [T][B][4H] holds Gx_t (+ bias) and
+// receives the activated gates, hbuf [(T+1)][B][H] (hbuf[0] = h_{−1}, not read), cbuf
+// [T][B][H], hlo2 [2][B][H] scratch. Backward: dOut [T][B][H] → dG [T][B][4H], dc [B][H]
+// scratch, dglo2 [2][B][4H] scratch. ST_ERR_UNSUPPORTED: shapes / device do not allow it.
+st_status lstm_rec_fwd(const GemmArgs& g, int B, int H, int T, const float* Whh, float* gates, float* hbuf,
+                       float* cbuf, float* hlo2);
+st_status lstm_rec_bwd(const GemmArgs& g, int B, int H, int T, const float* Whh, const float* gates,
+                       const float* cbuf, const float* dOut, float* dG, float* dglo2, float* dc);
 st_status gemm_dx(const GemmArgs& g, const float* dZ, const float* W, const float* mask, float* D);
 st_status gemm_dw(const GemmArgs& g, const float* X, const float* dZ, float* G, float* gb);
 // dW fused with the K-B update (NEXT-3): g = Xᵀ·dZ never reaches HBM;

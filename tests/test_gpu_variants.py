@@ -52,3 +52,17 @@ def test_conv_variants_pass_parity(env):
     r = subprocess.run([sys.executable, "-m", "pytest", "-q", "-x", "-m", "gpu", "-p", "no:cacheprovider",
                         *CONV_CASES], cwd=ROOT, env=e, capture_output=True, text=True, timeout=900)
     assert r.returncode == 0, r.stdout[-3000:] + r.stderr[-2000:]
+
+
+@pytest.mark.gpu
+def test_lstm_persistent_recurrence_variant():
+    """Development opt-in ST_LSTM_PERSIST=1: the LSTM recurrence as one persistent
+    cooperative launch per layer and direction (k_lstm_rec.cu) — the LSTM parity tests
+    (incl. the single-stage shapes and their launch-count invariant) and the full-size LM
+    at one stage against the same gates."""
+    e = _dev_env({"ST_LSTM_PERSIST": "1"})
+    r = subprocess.run([sys.executable, "-m", "pytest", "-q", "-x", "-m", "gpu", "-p", "no:cacheprovider",
+                        "tests/test_gpu_lstm.py",
+                        "tests/test_gpu_fullsize.py::test_lstm_lm_full_size_single_stage_bench_path"],
+                       cwd=ROOT, env=e, capture_output=True, text=True, timeout=900)
+    assert r.returncode == 0, r.stdout[-3000:] + r.stderr[-2000:]

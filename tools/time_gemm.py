@@ -41,8 +41,12 @@ def t_op(op, mode, B, n_in, n_out, reps=10):
 
 if __name__ == "__main__":
     shapes = [(128, 8192, 8192)] + ([(128, 784, 8192), (128, 8192, 10)] if "--all" in sys.argv else [])
+    modes = ((0, "fp32x3"), (1, "tf32"))
+    if "--shape" in sys.argv:  # --shape B,in,out: fp32x3 only
+        shapes = [tuple(int(v) for v in sys.argv[sys.argv.index("--shape") + 1].split(","))]
+        modes = ((0, "fp32x3"),)
     for (B, i, o) in shapes:
-        for mode, mname in ((0, "fp32x3"), (1, "tf32")):
+        for mode, mname in modes:
             for op, oname in ((0, "fwd"), (1, "dX"), (2, "dW"), (3, "dWU")):
                 us, tf, gbs = t_op(op, mode, B, i, o)
                 print(f"{oname:3s} {mname:6s} B={B} in={i} out={o}: {us:8.1f} us  {tf:7.1f} TFLOP/s  weight-bytes {gbs:7.1f} GB/s")
