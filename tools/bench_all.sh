@@ -15,3 +15,7 @@ done
 # NEXT-4 on VGG-16's imbalanced 8-stage pipeline (co-located): profiled cuts, a replicated conv front
 timeout 600 python bench.py --workload vgg16 --stages 8 --partition profiled --no-cpu > $OUT/vgg16_s8_profiled.json 2>&1
 timeout 600 python bench.py --workload vgg16 --replicas 2,1,1,1,1,1,1,1 --no-cpu > $OUT/vgg16_s8_rep2.json 2>&1
+# 1xTF32 "fast" mode of the tensor-bound workloads (parity is checked in 3xTF32 only)
+for w in vgg16 lstm_lm wide_fcn; do
+  timeout 300 python bench.py --workload $w --gemm tf32 --no-cpu > $OUT/${w}_tf32.json 2> $OUT/${w}_tf32.err
+done
