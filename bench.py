@@ -574,6 +574,13 @@ def run_ours(args):
         S = args.stages or N
         if N > 1 and S != N:
             raise SystemExit("--stages must equal --gpus when N > 1")
+    shared_gpu = N > 1 and os.environ.get("ST_BENCH_SHARED_GPU") == "1"
+    if shared_gpu:
+        # validation of the torchrun path on a one-GPU box (tools/gpu_torchrun.sh): every rank
+        # on cuda:0, each rank its own NCCL "host" so NCCL accepts two ranks on one device.
+        # The ranks time-slice the GPU: the numbers are not a scaling measurement.
+        os.environ["NCCL_HOSTID"] = f"st-bench-host-{rank}"
+        local = 0
     torch.cuda.set_device(local)
     dev = torch.device("cuda", local)
     if N > 1:
@@ -848,7 +855,9 @@ def run_ours(args):
                        "cuts": list(model.cuts), "partition": args.partition,
                        **({"layer_cost_us": layer_cost_us} if layer_cost_us else {}),
                        "parallelism": (f"pp{S}" if not reps else f"pp{S}xdp" + "-".join(map(str, reps))),
-                       **({"replicas": reps} if reps else {}), "cuda_graph": use_graph, "l2": "no flush: per-step working set (weights) >> 126 MB L2",
+                       **({"replicas": reps} if reps else {}),
+                       **({"shared_gpu_validation": "all ranks on one GPU: not a scaling number"} if shared_gpu else {}),
+                       "cuda_graph": use_graph, "l2": "no flush: per-step working set (weights) >> 126 MB L2",
                        "session": "one 1F1B session of warmup + steps mini-batches; timed window = CUDA events "
                                   "after stage 0's B(warmup-1) and B(warmup+steps-1) (P:415 steady state)"},
             "roofline": roofline_key,
