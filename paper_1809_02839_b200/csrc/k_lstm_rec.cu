@@ -314,6 +314,7 @@ __global__ void __launch_bounds__(R_THREADS, 1)
     const int j0 = BWD ? q * 128 : q * 32;
     const int ncell = (b1 - b0) * nj;
     const size_t BH = (size_t)B * H, B4H = (size_t)B * 4 * H;
+    if (ctid == 0) rec_mark(p.dbg, 0, 6);  // kernel start (slot 6 is unused at i = 0)
     for (int i = 0; i < T; ++i) {
       const int t = BWD ? T - 1 - i : i;
       // while the MMAs run: pull this step's cell inputs that do not depend on them (Gx_t /
@@ -558,16 +559,18 @@ st_status launch_rec(const GemmArgs& g, RecParams p, const float* Whh, const flo
   return ST_OK;
 }
 
-bool rec_shapes_ok(const GemmArgs& g, int B, int H, int T) {
-  return g.mode == ST_GEMM_FP32X3 && B >= 1 && B <= 128 && H % 4 == 0 && T >= 1 && g.work &&
-         dev_knob("ST_LSTM_PERSIST", 0) != 0;
+// ST_LSTM_PERSIST: 1 = both directions, 2 = backward only, 3 = forward only
+bool rec_shapes_ok(const GemmArgs& g, int B, int H, int T, bool bwd) {
+  const int v = dev_knob("ST_LSTM_PERSIST", 0);
+  const bool on = v == 1 || v == (bwd ? 2 : 3);
+  return on && g.mode == ST_GEMM_FP32X3 && B >= 1 && B <= 128 && H % 4 == 0 && T >= 1 && g.work;
 }
 
 }  // namespace
 
 st_status lstm_rec_fwd(const GemmArgs& g, int B, int H, int T, const float* Whh, float* gates, float* hbuf,
                        float* cbuf, float* hlo2) {
-  if (!rec_shapes_ok(g, B, H, T)) return ST_ERR_UNSUPPORTED;
+  if (!rec_shapes_ok(g, B, H, T, false)) return ST_ERR_UNSUPPORTED;
   RecParams p{};
   p.B = B;
   p.H = H;
@@ -581,7 +584,7 @@ st_status lstm_rec_fwd(const GemmArgs& g, int B, int H, int T, const float* Whh,
 
 st_status lstm_rec_bwd(const GemmArgs& g, int B, int H, int T, const float* Whh, const float* gates,
                        const float* cbuf, const float* dOut, float* dG, float* dglo2, float* dc) {
-  if (!rec_shapes_ok(g, B, H, T)) return ST_ERR_UNSUPPORTED;
+  if (!rec_shapes_ok(g, B, H, T, true)) return ST_ERR_UNSUPPORTED;
   RecParams p{};
   p.B = B;
   p.H = H;

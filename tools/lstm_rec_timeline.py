@@ -56,6 +56,10 @@ def main():
     lat = (a[2:T, :, 0] - a[1:T - 1, :, 4].max(axis=1, keepdims=True)) / 1e3
     out["barrier_release_us_median"] = round(float(np.median(lat)), 2)
     per = (a[2:T, :, 0].min(axis=1) - a[1:T - 1, :, 0].min(axis=1)) / 1e3
+    if T <= 40:  # whole kernel: first CTA start to last CTA's final grid arrival
+        out["kernel_us"] = round(float((a[T - 1, :, 4].max() - a[0, :, 6].min()) / 1e3), 1)
+        out["first_mma_phase_us"] = round(float(np.median(a[1, :, 1] - a[1, :, 0]) / 1e3), 2)
+        out["t0_cells_us"] = round(float((a[0, :, 4].max() - a[0, :, 6].min()) / 1e3), 2)
     out["step_period_us_median"] = round(float(np.median(per)), 2)
     print(json.dumps(out))
     s.close()
