@@ -505,8 +505,12 @@ def nccl_parity_leg(args, N: int, rank: int, local: int, dev):
     """Under torchrun (N > 1), before timing: the NCCL transport checked on the real
     ranks — the deep MLP 784-1024×8-10 cut into N stages, one per
     rank over NCCL (two communicators, comm streams), M = 20, B = 128, η = 0.02, 3xTF32,
-    against the oracle on rank 0: trace bit-exact, W and loss rel-L2 ≤ 1e-4, ΔW rel-L2
-    ≤ 1e-3 (north_star gates)."""
+    against the oracle on rank 0: trace bit-exact, W and loss rel-L2 ≤ 1e-4 (north_star
+    gates) and ΔW = W − W0 rel-L2 ≤ 1e-2. The ΔW gate follows reading D24: the oracle's own
+    arithmetic in float32 spreads ΔW from its float64 run by 2.3e-3 / 3.8e-3 / 1.0e-3 at
+    N = 2 / 4 / 8 on exactly these inputs (tools/d24_pipeline.py deep_mlp_N --M 20 →
+    profiles/r2_d24_deep_mlp_N_M20.json: ReLU decisions within rounding of 0), so the
+    gate is above 2x that spread (a skipped update gives ΔW rel-L2 = 1)."""
     import torch
     import torch.distributed as dist
 
@@ -547,7 +551,8 @@ def nccl_parity_leg(args, N: int, rank: int, local: int, dev):
     dw = rel(Wg - np.concatenate(w0), Wr - np.concatenate(sd.widen(w0)))
     return {"model": "deep_mlp_784-1024x8-10_b128", "stages": N, "minibatches": M, "transport": "nccl (2 comms)",
             "trace_bit_exact": bool(trace_ok), "w_rel_l2": rw, "loss_rel_l2": rl, "dw_rel_l2": dw,
-            "pass": bool(trace_ok and rw <= 1e-4 and rl <= 1e-4 and dw <= 1e-3), "wall_s": wall}
+            "gates": {"w": 1e-4, "loss": 1e-4, "dw": 1e-2},
+            "pass": bool(trace_ok and rw <= 1e-4 and rl <= 1e-4 and dw <= 1e-2), "wall_s": wall}
 
 
 def run_ours(args):
