@@ -37,7 +37,7 @@ def rel(a, b):
 
 if __name__ == "__main__":
     ap = argparse.ArgumentParser()
-    ap.add_argument("case", choices=["vgg16_8", "vgg16_1", "deep_mlp_2", "deep_mlp_4", "deep_mlp_8"])
+    ap.add_argument("case", choices=["deep_mlp_2", "deep_mlp_4", "deep_mlp_8", "vgg16_8", "vgg16_1"])
     ap.add_argument("--M", type=int, default=10)
     a = ap.parse_args()
     if a.case.startswith("deep_mlp"):  # bench.py's NCCL parity leg: 784-1024×8-10, B = 128, η = 0.02
@@ -53,6 +53,10 @@ if __name__ == "__main__":
     r32 = oracle_float32().run(model, [np.asarray(w, np.float32) for w in w0], X.astype(np.float32), Y, float(np.float32(LR)),
                 float(np.float32(0.9)))
     t2 = time.time()
+    # the float32 copy must really have run in float32 (the conv / pool paths of the oracle
+    # cast to float64 in places the module-level patch does not reach: refuse those cases)
+    if np.concatenate(r32.V).dtype != np.float32:
+        raise SystemExit(f"{a.case}: the float32 oracle copy did not stay in float32")
     W0 = np.concatenate(sd.widen(w0))
     W64, W32 = np.concatenate(r64.W), np.concatenate(r32.W)
     out = {"case": a.case, "M": a.M, "B": B, "lr": LR,
