@@ -2860,13 +2860,13 @@ bool tc_conv_ok(int mode, int H, int W, int Cin, int Cout) {
 // Conv forward on the CTA-pair TMEM-A kernel (tc_ts2_kernel<…, CONV>): weights on M
 // (Cout ≥ 256, so every pair tile is full), pixels on N — the pair's MMAs run at ~1.5× the
 // per-SM rate of the single-CTA N ≤ 128 ones (profiles/r1_probe_mma_rate_tf32.txt). The
-// activation lo is split once into the workspace tail. Opt-in (ST_CONV_PAIR=1): in the
-// serialised, cache-flushed ncu list its conv3–5 forwards are ~25% faster, but in the warm
-// step the forward class is unchanged (0.638 vs 0.644 ms; VGG-16 58.9k vs 59.0k samples/s).
+// activation lo is split once into the workspace tail. Default since round 2 (with PDL and
+// graph sessions in the step): VGG-16 62.3k → 63.4k samples/s (two runs each, one box);
+// round 1 had measured it neutral (58.9k vs 59.0k). ST_CONV_PAIR=0: single-CTA conv forward.
 bool conv_pair_on() {
   static int f = -1;
   if (f < 0) {
-    f = dev_knob("ST_CONV_PAIR", 0) == 1 ? 1 : 0;
+    f = dev_knob("ST_CONV_PAIR", 1) != 0 ? 1 : 0;
   }
   return f != 0;
 }

@@ -77,8 +77,8 @@ def test_vgg_implicit_batch1(st):
 
 
 def test_vgg_wide_conv_pair_kernel(st):
-    """Cout ≥ 256 (256 / 384 channels). With ST_CONV_PAIR=1 (tests/test_gpu_variants.py
-    runs this in a child process) the conv forward is the CTA-pair TMEM-A kernel (weights on M,
+    """Cout ≥ 256 (256 / 384 channels). By default (ST_CONV_PAIR=0 in the dev build, run by
+    tests/test_gpu_variants.py, selects the single-CTA kernel) the conv forward is the CTA-pair TMEM-A kernel (weights on M,
     64-pixel window boxes per CTA, activation lo split once); 384 output channels leave a
     padding CTA in the last pair; 8×8 and 4×4 images, ragged pixel tiles (batch 3)."""
     model = sd.vgg(cfg=(32, 384, "M", 256, "M"), fc=(16,), classes=10, hw=8, in_ch=32, cuts=[2])

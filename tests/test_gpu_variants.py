@@ -42,11 +42,11 @@ CONV_CASES = ["tests/test_gpu_conv.py"]
 
 
 @pytest.mark.gpu
-@pytest.mark.parametrize("env", [{"ST_CONV_PAIR": "1"}, {"ST_CONV_OVERLAP": "1"}, {"ST_TS_SPLIT_ACC": "0"},
+@pytest.mark.parametrize("env", [{"ST_CONV_PAIR": "0"}, {"ST_CONV_OVERLAP": "1"}, {"ST_TS_SPLIT_ACC": "0"},
                                  {"ST_TSG_NARROW": "0"}],
-                         ids=["conv_pair", "conv_overlap", "one_accumulator", "tsg_4_stages"])
+                         ids=["conv_single_cta", "conv_overlap", "one_accumulator", "tsg_4_stages"])
 def test_conv_variants_pass_parity(env):
-    """Opt-in conv paths: the CTA-pair conv forward, side-stream overlap of the conv dW +
+    """Non-default conv paths: the single-CTA conv forward, side-stream overlap of the conv dW +
     update, the single-accumulator pair kernel, the 4-stage TMEM-A ring for N ≤ 64."""
     e = _dev_env(env)
     r = subprocess.run([sys.executable, "-m", "pytest", "-q", "-x", "-m", "gpu", "-p", "no:cacheprovider",
