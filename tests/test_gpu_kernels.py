@@ -139,7 +139,7 @@ def test_stage_gemms_vs_fp64(st, mode, B, n_in, n_out):
     np.testing.assert_allclose(gb.cpu().numpy(), dZ64.sum(0), rtol=1e-5, atol=1e-5)
 
 
-@pytest.mark.parametrize("B,C", [(32, 10), (128, 10), (7, 1000), (64, 10000)])
+@pytest.mark.parametrize("B,C", [(32, 10), (128, 10), (7, 1000), (64, 10000), (3, 13), (5, 4096)])
 def test_softmax_ce_vs_oracle(st, B, C):
     rng = np.random.default_rng(C + B)
     Z = (3 * rng.standard_normal((B, C))).astype(np.float32)
