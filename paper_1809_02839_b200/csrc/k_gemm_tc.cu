@@ -2398,7 +2398,7 @@ bool conv_persistent_off() {
 
 template <int EPI, bool A_MN, bool B_MN, int CV = CV_NONE>
 st_status launch(const GemmArgs& g, int M, int N, int K, const CUtensorMap& ma, const CUtensorMap& mb, float* out,
-                 const float* aux, int relu, int cvH = 0, int cvW = 0, int cvC = 0) {
+                 const float* aux, int relu, int cvH = 0, int cvW = 0, int cvC = 0, bool tall_fwd = false) {
   TcParams p{};
   p.dev_flags = dev_flags();
   p.row = (CV == CV_FWD || CV == CV_DX || CV == CV_ROWS || CV == CV_DWT) ? 1 : 0;
@@ -2434,8 +2434,9 @@ st_status launch(const GemmArgs& g, int M, int N, int K, const CUtensorMap& ma, 
   (void)ai;
   ST_TRY(ensure_max_smem((const void*)kern, smem_bytes(S)));
   p.ext_reduce = p.splits >= ext_reduce_splits();
-  if (g.mode == ST_GEMM_FP32X3 && conv_ts_on() && (CV != CV_NONE || EPI == EPI_DW)) {
-    // persistent TMEM-A kernel: implicit conv (all passes) and the tall dense dW
+  if (g.mode == ST_GEMM_FP32X3 && conv_ts_on() && (CV != CV_NONE || EPI == EPI_DW || tall_fwd)) {
+    // persistent TMEM-A kernel: implicit conv (all passes), the tall dense dW and the tall
+    // dense forward (many row tiles: the epilogue of one tile overlaps the next one's MMAs)
     const bool narrow = p.bn <= 64 && tsg_narrow_on();
     auto ck = narrow ? tc_tsg_kernel<EPI, A_MN, B_MN, CV, true> : tc_tsg_kernel<EPI, A_MN, B_MN, CV, false>;
     const int smem = narrow ? tsg_smem_bytes<true>() : tsg_smem_bytes<false>();
@@ -2647,6 +2648,17 @@ st_status simt_dx(const GemmArgs& g, const float* dZ, const float* W, const floa
 st_status simt_dw(const GemmArgs& g, const float* X, const float* dZ, float* G, float* gb);
 int simt_last_launches();
 
+// Forward GEMMs with many row tiles (N = T·B ≥ 8 × 128: the LSTM input projections, the LM
+// softmax, explicit-im2col convs) on the persistent TMEM-A kernel instead of one CTA pair per
+// tile: a CTA's next tile fills one accumulator while the epilogue drains the other. LM
+// per-layer profile: softmax forward 653 → 610 µs, LSTM forward 1048 → 1000 µs
+// (gpurun_out/r2ft). ST_FWD_TSG=0 (development build): the CTA-pair kernel.
+bool tall_fwd_tsg() {
+  static int f = -1;
+  if (f < 0) f = dev_knob("ST_FWD_TSG", 1) != 0 ? 1 : 0;
+  return f != 0;
+}
+
 // fwd: M = out, N = B, K = in
 st_status tc_fwd(const GemmArgs& g, const float* X, const float* W, const float* bias, float* Z, int relu) {
   if (!tma_ok(W, g.n_out) || !tma_ok(X, g.n_in) || !get_encode()) {
@@ -2656,10 +2668,15 @@ st_status tc_fwd(const GemmArgs& g, const float* X, const float* W, const float*
     return s;
   }
   CUtensorMap ma, mb;
-  if (g.mode == ST_GEMM_FP32X3) {
+  if (g.mode == ST_GEMM_FP32X3 && !(tall_fwd_tsg() && g.B >= 8 * BNMAX && !g.defer)) {
     if (!make_map(&ma, W, g.n_out, g.n_in, g.n_out, 32, true))
       return set_error(ST_ERR_CUDA, "cuTensorMapEncodeTiled failed (fwd)");
     return launch_ts<EPI_FWD, true>(g, g.n_out, g.B, g.n_in, ma, X, Z, bias, relu);
+  }
+  if (g.mode == ST_GEMM_FP32X3) {  // tall forward (T·B rows: LSTM input projection, LM softmax)
+    if (!make_map(&ma, W, g.n_out, g.n_in, g.n_out, 32, true) || !make_map(&mb, X, g.n_in, g.B, g.n_in, BNMAX, false))
+      return set_error(ST_ERR_CUDA, "cuTensorMapEncodeTiled failed (fwd)");
+    return launch<EPI_FWD, true, false>(g, g.n_out, g.B, g.n_in, ma, mb, Z, bias, relu, 0, 0, 0, true);
   }
   if (!make_map(&ma, W, g.n_out, g.n_in, g.n_out, 32, true) || !make_map(&mb, X, g.n_in, g.B, g.n_in, bn_for(g.B), false))
     return set_error(ST_ERR_CUDA, "cuTensorMapEncodeTiled failed (fwd)");

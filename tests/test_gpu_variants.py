@@ -66,3 +66,14 @@ def test_lstm_persistent_recurrence_variant():
                         "tests/test_gpu_fullsize.py::test_lstm_lm_full_size_single_stage_bench_path"],
                        cwd=ROOT, env=e, capture_output=True, text=True, timeout=900)
     assert r.returncode == 0, r.stdout[-3000:] + r.stderr[-2000:]
+
+
+@pytest.mark.gpu
+def test_tall_forward_on_pair_kernel_variant():
+    """ST_FWD_TSG=0: the tall dense forward (T·B rows) back on the CTA-pair kernel — the
+    LSTM parity tests and the explicit-im2col conv cases against the same gates."""
+    e = _dev_env({"ST_FWD_TSG": "0"})
+    r = subprocess.run([sys.executable, "-m", "pytest", "-q", "-x", "-m", "gpu", "-p", "no:cacheprovider",
+                        "tests/test_gpu_lstm.py", "tests/test_gpu_conv.py"],
+                       cwd=ROOT, env=e, capture_output=True, text=True, timeout=900)
+    assert r.returncode == 0, r.stdout[-3000:] + r.stderr[-2000:]
