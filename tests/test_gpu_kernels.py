@@ -101,8 +101,10 @@ MODES = {"simt": 2, "fp32x3": 0, "tf32": 1}
 @pytest.mark.parametrize("mode", GEMM_MODES)
 @pytest.mark.parametrize("B,n_in,n_out", [(32, 784, 256), (128, 300, 70), (5, 33, 17), (128, 1024, 1024),
                                           (96, 160, 200), (128, 4096, 512), (7, 264, 136), (128, 784, 384),
-                                          (16, 128, 4096)])
+                                          (16, 128, 4096), (1100, 96, 200), (4480, 64, 136)])
 def test_stage_gemms_vs_fp64(st, mode, B, n_in, n_out):
+    """fwd (bias + ReLU), dX (ReLU mask), dW (+ bias grad) against fp64. B ≥ 1024 rows: the
+    forward runs on the persistent TMEM-A kernel (tall forward; ragged last row tile)."""
     rng = np.random.default_rng(B * 7 + n_in)
     dev = torch.device("cuda", 0)
     X = rng.standard_normal((B, n_in)).astype(np.float32)
