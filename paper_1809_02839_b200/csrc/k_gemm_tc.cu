@@ -1513,8 +1513,17 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(TS_THREADS, 1)
     const int quad = warp & 3;
     const int r = quad * 32 + lane;
     uint64_t w_a = 0, w_e = 0, w_s = 0;
+    // dX with a ReLU mask and no K split: the epilogue (these warps, after the last K-block)
+    // reads a 128 × bn mask tile written long ago (the stashed activation, in HBM); pull it
+    // into L2 ~16 K-blocks before the end, late enough that the weight stream does not evict it
+    const int pf_at = (EPI == EPI_DX && p.aux && p.splits == 1 && !p.row) ? max(0, nkb - 16) : -1;
     for (int i = 0; i < nkb; ++i) {
       const int s = i % TS_RA, ta = i % TA;
+      if (i == pf_at && m0 + r < p.M) {
+        const float* mrow = p.aux + m0 + r;
+        for (int n = n0; n < min(p.N, n0 + p.bn); ++n)
+          asm volatile("prefetch.global.L2 [%0];" ::"l"(mrow + (size_t)n * p.M));
+      }
       const uint64_t c0 = clock64();
       mbar_wait(a_full + 8 * s, (i / TS_RA) & 1);
       w_a += clock64() - c0;
