@@ -557,6 +557,7 @@ st_status ctx_init(const st_config* cfg, const st_buffers* bufs, void* stream, v
   }
   c->conv_overlap = dev_knob("ST_CONV_OVERLAP", 0) != 0;
   c->bwd_serial = dev_knob("ST_BWD_SERIAL", 1) != 0;
+  c->pdl_serial = dev_knob("ST_PDL_SERIAL", 1) != 0;
   c->pdl = dev_knob("ST_PDL", 1) != 0;
   c->pdl_dense = dev_knob("ST_PDL_DENSE", 1) != 0;
   // several stage contexts sharing one GPU (LOCAL transport): their kernels interleave
@@ -1135,7 +1136,11 @@ static st_status backward_compute(st_ctx* c, int64_t mb, bool fused = false) {
     // layer the main-stream dX overlaps the side-stream dW + update, and early-launched
     // CTAs waiting on their predecessor hold SMs the other stream needs (large FCN −5%),
     // so those layers launch normally
-    c->pdl_now = c->pdl_dense && !(fused && L.kind == ST_LAYER_DENSE && L.n_params >= ((int64_t)1 << 22));
+    // — unless the layer's dW + update is serialised after its dX (≥ 2^27 parameters): then
+    // one stream has the GPU again and the launches chain programmatically (ST_PDL_SERIAL)
+    const bool serial_layer = fused && c->bwd_serial && c->pdl_serial && L.n_params >= ((int64_t)1 << 27);
+    c->pdl_now = c->pdl_dense &&
+                 (serial_layer || !(fused && L.kind == ST_LAYER_DENSE && L.n_params >= ((int64_t)1 << 22)));
     set_thread_pdl(c->pdl_now ? 1 : 0);
     float* Ain = layer_in(c, slot, (size_t)l);
     const bool need_dx = !(c->first_stage && l == 0) && L.kind != ST_LAYER_EMBED;

@@ -242,7 +242,8 @@ struct st_ctx {
   int rep_prev = 1, rep_self = 1, rep_next = 1, replica = 0;
   int B_global = 1;
   std::vector<int> reps;                         // replicas per stage (all N)
-  bool shares_gpu = false;  // LOCAL transport with other stage / replica contexts in this process
+  bool shares_gpu = false;
+  bool pdl_serial = true;  // programmatic launches for the serialised backward of ≥ 2^27-parameter layers  // LOCAL transport with other stage / replica contexts in this process
   std::shared_ptr<st::ReplicaGroup> rgroup;      // LOCAL: the stage's co-located replicas
 
   st::Profiler prof;
