@@ -216,7 +216,9 @@ __global__ void __launch_bounds__(256) colsum4_partial_kernel(const float* __res
 int launch_bias_grad(const float* dZ, int rows, int n_out, float* gb, void* work, int64_t work_bytes,
                      cudaStream_t s) {
   const int cb = (n_out + 31) / 32;
-  int nb = rows > 1024 ? std::min(1024, std::max(1, (2 * device_sm_count()) / cb)) : 1;
+  // tall sums: enough row blocks for ~8 CTAs per SM (the LSTM / LM bias gradients: 6000 or
+  // 10 000 columns over T·B = 4480 rows were one pass of 188 / 313 CTAs, ~60 µs each)
+  int nb = rows > 1024 ? std::min(1024, std::max(2, (8 * device_sm_count() + cb - 1) / cb)) : 1;
   nb = std::min(nb, (rows + 255) / 256);
   if (nb > 1 && work && (int64_t)nb * n_out * 4 <= work_bytes - 64 * 1024) {
     const int rpb = (rows + nb - 1) / nb;
